@@ -1,0 +1,201 @@
+/*
+ * mmmcu.h — C ABI of the B200-native masked matrix multiply (arXiv 2402.14118).
+ *
+ * This is the drop-in boundary of the hot path.  The reference's plugin
+ * point is the per-region function-pointer table `KernelFn<T>` dispatched by
+ * `KernelTable<T>::apply` (/root/reference/proj/include/mmm/kernel_table.hpp:12-13, :50-54);
+ * per-region host function pointers cannot dispatch device work, so the boundary moves up
+ * one level to the SPEC engine entry points, which the C++ drop-in
+ * header include/mmm_cuda.hpp re-exposes with the SPEC signatures on top of this ABI.
+ *
+ * Conventions
+ *   - Plain C: pointers, int64 sizes, strides in ELEMENTS.  No torch, no C++ types.
+ *   - Every entry point returns an mmmcu_status; 0 is success.  The message of the last
+ *     failure on a context is mmmcu_last_error(ctx) (thread-local when ctx is NULL).
+ *   - Device pointers unless the name says _host.  All work is enqueued on the context's
+ *     stream (mmmcu_set_stream); results are valid after that stream completes, except
+ *     for calls that return host data (they synchronise the stream).
+ *   - Operand layout is the reference Matrix<float> layout (matrix.hpp:61-83): row-major,
+ *     element (i, j) at i*ld + j, ld a multiple of the region width R = W*P*V (64 for the
+ *     f32 defaults) and columns [cols, ld) exactly zero.
+ *   - Only the f32 default lane config {W=8, P=8, V=1} (matrix.hpp:36-38) is implemented
+ *     on the GPU; any other returns MMMCU_ERR_UNSUPPORTED.  There is no CPU fallback.
+ */
+#ifndef MMMCU_H_
+#define MMMCU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MMMCU_ABI_VERSION 1
+
+typedef enum {
+  MMMCU_OK = 0,
+  MMMCU_ERR_INVALID_ARG = 1,   /* std::invalid_argument: dims <= 0, lane fields, p range (matrix.hpp:72-74, kernel_table.cpp:66-72) */
+  MMMCU_ERR_DIM_MISMATCH = 2,  /* SPEC.md:262, :271 dimension mismatch */
+  MMMCU_ERR_STALE = 3,         /* SPEC.md:280 stale context (content-version mismatch) */
+  MMMCU_ERR_UNSUPPORTED = 4,   /* dtype / lane config without a GPU kernel */
+  MMMCU_ERR_CUDA = 5,          /* CUDA runtime failure */
+  MMMCU_ERR_NOT_READY = 6,     /* multiply before preprocess */
+  MMMCU_ERR_OVERFLOW = 7,      /* std::overflow_error (matrix.hpp:77-80) */
+  MMMCU_ERR_WORKERS = 8,       /* SPEC.md:290 worker_count == 0 */
+  MMMCU_ERR_NO_DEVICE = 9      /* no CUDA device: the product never falls back to the CPU */
+} mmmcu_status;
+
+typedef struct mmmcu_ctx mmmcu_ctx;
+
+/* LaneConfig (matrix.hpp:31-44). */
+typedef struct {
+  int32_t w, p, v;
+} mmmcu_lane;
+
+/* WorkCounters (SPEC.md:252-255; semantics :279, :297-298). */
+typedef struct {
+  uint64_t kernel_invocations;           /* (non-zero a_ik, region with code != 0) pairs */
+  uint64_t lane_fma_ops;                 /* Σ popcount(code) * W * V over those pairs      */
+  uint64_t rows_skipped;                 /* zero A elements (a whole B row skipped)        */
+  uint64_t regions_skipped_by_zero_code; /* (non-zero a_ik, region with code == 0) pairs   */
+} mmmcu_counters;
+
+/* plan_stats. */
+typedef struct {
+  int64_t region_count;
+  double zero_region_fraction;
+  double mean_popcount;
+} mmmcu_plan_stats;
+
+/* Kernel-variant selection for mmmcu_multiply (all variants honour the same contract). */
+typedef enum {
+  MMMCU_ALGO_AUTO = 0,       /* pick per call from the preprocessing statistics          */
+  MMMCU_ALGO_SIMT_BCAST = 1, /* K2-SIMT: warp-uniform k over B block masks, exact fp32;
+                                mask granularity (8 or 16 columns) chosen on the device   */
+  MMMCU_ALGO_DENSE = 2,      /* multiply_simple (dense i-k-j fma)            */
+  MMMCU_ALGO_SIMT_SPAN8 = 3, /* K2-SIMT forced to 8-column (group) masks                  */
+  MMMCU_ALGO_SIMT_SPAN16 = 4 /* K2-SIMT forced to 16-column slice masks                   */
+} mmmcu_algo;
+
+/* ---- context --------------------------------------------------------------------- */
+
+/* Bind a context to CUDA device `device`.  MMMCU_ERR_NO_DEVICE when none is present. */
+mmmcu_status mmmcu_ctx_create(int device, mmmcu_ctx** out);
+mmmcu_status mmmcu_ctx_destroy(mmmcu_ctx* ctx);
+/* Stream all subsequent work is enqueued on (a cudaStream_t; NULL = legacy default). */
+mmmcu_status mmmcu_set_stream(mmmcu_ctx* ctx, void* stream);
+const char* mmmcu_last_error(const mmmcu_ctx* ctx);
+int mmmcu_abi_version(void);
+
+/* KernelTable<T>::build validation (kernel_table.cpp:64-92): 0 if the lane config is
+ * valid for f32, MMMCU_ERR_INVALID_ARG with the reference's message otherwise. */
+mmmcu_status mmmcu_validate_lane(mmmcu_ctx* ctx, mmmcu_lane lane);
+
+/* ---- preprocessing (K1) ------------------------------------------------------------ */
+
+/*
+ * preprocess_a + preprocess_b of SPEC.md:196-214 in one pass over A (M x K, lda) and
+ * B (K x N, ldb), device pointers.  Builds, in context-owned device memory:
+ *   A: per-row non-zero bitmap (uint32 [M][ceil(K/32)], LSB-first), per-row non-zero
+ *      counts, per-row ascending index lists (CSR, uint32 columns), column counts;
+ *   B: pattern codes (uint8 [K][ldb/64], MSB-first == BPlan codes), per-8-column-group
+ *      k-bitmaps (transposed block masks), per-row code statistics;
+ *   the exact WorkCounters and plan_stats of the coming multiply.
+ * a_version / b_version are the operands' content versions (Matrix::version(),
+ * matrix.hpp:115); mmmcu_multiply rejects other versions as stale.
+ */
+mmmcu_status mmmcu_preprocess(mmmcu_ctx* ctx, const float* A, int64_t M, int64_t K, int64_t lda,
+                              const float* B, int64_t N, int64_t ldb, mmmcu_lane lane,
+                              uint64_t a_version, uint64_t b_version);
+
+/* Only A's half (preprocess_a): bitmap, counts, CSR, column counts. */
+mmmcu_status mmmcu_preprocess_a(mmmcu_ctx* ctx, const float* A, int64_t M, int64_t K, int64_t lda,
+                                uint64_t a_version);
+
+/* Only B's half (preprocess_b): codes + group bitmaps + row statistics. */
+mmmcu_status mmmcu_preprocess_b(mmmcu_ctx* ctx, const float* B, int64_t K, int64_t N, int64_t ldb,
+                                mmmcu_lane lane, uint64_t b_version);
+
+/* Counters and plan statistics of the current plan (synchronises the stream). */
+mmmcu_status mmmcu_get_counters(mmmcu_ctx* ctx, mmmcu_counters* out);
+mmmcu_status mmmcu_get_plan_stats(mmmcu_ctx* ctx, mmmcu_plan_stats* out);
+
+/* ---- exports of the canonical plan formats (host destination buffers) -------------- */
+
+/* Pattern codes, row-major uint8 [K][ldb/64] (SPEC BPlan codes before leaf ordering). */
+mmmcu_status mmmcu_export_b_codes(mmmcu_ctx* ctx, uint8_t* codes_host, int64_t capacity);
+/* BPlan order: per leaf_dim x leaf_dim sub-block, leaf-row-major;
+ * inside a leaf, rows then regions.  plans_host has K*ldb/64 entries, plan_off_host
+ * n_plans + 1; *n_plans receives the plan count. */
+mmmcu_status mmmcu_export_bplans(mmmcu_ctx* ctx, int64_t leaf_dim, uint8_t* plans_host,
+                                 int64_t plans_capacity, int64_t* plan_off_host,
+                                 int64_t off_capacity, int64_t* n_plans);
+/* A bitmap, uint32 [M][ceil(K/32)], LSB-first. */
+mmmcu_status mmmcu_export_a_bitmap(mmmcu_ctx* ctx, uint32_t* bits_host, int64_t capacity);
+/* A CSR: row_ptr int64 [M+1], ascending uint32 columns [nnz]; *nnz receives nnz(A). */
+mmmcu_status mmmcu_export_a_csr(mmmcu_ctx* ctx, int64_t* row_ptr_host, uint32_t* cols_host,
+                                int64_t cols_capacity, int64_t* nnz);
+/* ABlockIndex: block_dim x block_dim blocks of A, block-major;
+ * per block row, per aligned 8-element segment: count + 8 offset slots (0xFF unused; a
+ * full segment stores none).  *n_segments receives the segment count. */
+mmmcu_status mmmcu_export_ablock_index(mmmcu_ctx* ctx, int64_t block_dim, uint8_t* counts_host,
+                                       int64_t counts_capacity, uint8_t* offsets_host,
+                                       int64_t offsets_capacity, int64_t* n_segments);
+
+/* ---- masked multiply (K2) ---------------------------------------------------------- */
+
+/*
+ * multiply_mmm: C (M x N, ldc) += A * B over the masks of the current
+ * plan.  A and B must be the preprocessed operands (same pointers, same versions).
+ * Each C element receives the ascending-k fmaf chain of its surviving terms, bit-identical
+ * to the CPU oracle.  counters may be NULL; filling it synchronises the stream.
+ */
+mmmcu_status mmmcu_multiply(mmmcu_ctx* ctx, float* C, int64_t ldc, const float* A, const float* B,
+                            uint64_t a_version, uint64_t b_version, mmmcu_counters* counters);
+/* multiply_parallel: worker_count == 0 is rejected; otherwise the same
+ * computation (the GPU's parallelism is not a host worker count). */
+mmmcu_status mmmcu_multiply_parallel(mmmcu_ctx* ctx, float* C, int64_t ldc, const float* A,
+                                     const float* B, uint64_t a_version, uint64_t b_version,
+                                     int worker_count, mmmcu_counters* counters);
+/* Force a kernel variant (MMMCU_ALGO_AUTO by default). */
+mmmcu_status mmmcu_set_algo(mmmcu_ctx* ctx, mmmcu_algo algo);
+/* Variant the last mmmcu_multiply ran. */
+mmmcu_status mmmcu_last_algo(mmmcu_ctx* ctx, mmmcu_algo* algo);
+
+/* multiply_simple: dense i-k-j C += A*B, fmaf per term. */
+mmmcu_status mmmcu_multiply_simple(mmmcu_ctx* ctx, float* C, int64_t ldc, const float* A,
+                                   int64_t lda, const float* B, int64_t ldb, int64_t M, int64_t K,
+                                   int64_t N);
+
+/* ---- host-buffer convenience (the drop-in path for host Matrix<float> operands) ------- */
+
+/*
+ * preprocess + multiply with HOST operands: copies A, B and C to the device, runs K1 and
+ * K2, copies C back.  Device staging buffers are owned (and reused) by the context.
+ */
+mmmcu_status mmmcu_multiply_host(mmmcu_ctx* ctx, float* C_host, int64_t ldc, const float* A_host,
+                                 int64_t lda, const float* B_host, int64_t ldb, int64_t M,
+                                 int64_t K, int64_t N, mmmcu_counters* counters);
+
+/* ---- synthetic inputs (device generator; matgen.hpp analogue for BASELINE.json) ------ */
+
+/*
+ * Fill out (rows x ld, device) with the seeded i.i.d. generator of SURVEY.md §8(d), built
+ * on the reference's counter hash (rng.hpp:8-26):
+ *   value_kind 0 uniform[-1,1], 1 N(0, sigma), 2 ReLU(N(0,1) - thresh);
+ *   mask_kind  0 none, 1 element zero with prob p, 2 aligned `block`-wide runs zero with
+ *              prob p.  Columns [cols, ld) are zeroed.
+ */
+mmmcu_status mmmcu_generate(mmmcu_ctx* ctx, float* out, int64_t rows, int64_t cols, int64_t ld,
+                            uint64_t seed, int value_kind, double sigma, double thresh,
+                            int mask_kind, double p, int64_t block);
+
+/* Row partition of a sharded multiply: rank r of `world` owns [*row0, *row1). */
+mmmcu_status mmmcu_shard_rows(int64_t M, int world, int rank, int64_t* row0, int64_t* row1);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MMMCU_H_ */

@@ -1,0 +1,540 @@
+/*
+ * mmm_oracle.c — CPU ORACLE for the masked-matrix-multiply hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Nothing in the product (paper_2402_14118_b200/, include/)
+ * links, loads or calls this file.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline leg may use it, and only as the checker / the timed CPU baseline.
+ *
+ * Plain-C restatement of the reference algorithm (arXiv 2402.14118, /root/reference):
+ *   - counter RNG                    rng.hpp:8-26            (mix64, hash_coords, unit_double)
+ *   - CounterRng::next/below         rng.hpp:30-45
+ *   - reference generators           matgen.hpp:47-148       (random / block_random / column /
+ *                                                              block_column, sample_zero_units)
+ *   - BASELINE.json i.i.d. generators (element/block Bernoulli masks, uniform / normal / ReLU
+ *     values) built on the same counter hash.
+ *   - masked region FMA (pattern code, MSB-first group bits)   kernel_table.cpp:12-28
+ *   - preprocess_b -> pattern codes, BPlan leaf order          SPEC.md:186-205, PAPER Fig. 9
+ *   - preprocess_a -> ABlockIndex (counts + offsets)           SPEC.md:190-214, PAPER Fig. 11
+ *   - plan_stats
+ *   - multiply_simple (i-k-j, fmaf)                            SPEC.md:258-266, PAPER Fig. 2
+ *   - multiply_mmm + WorkCounters (ascending-k fma chain)      SPEC.md:252-284, PAPER Fig. 10
+ *
+ * Parity pins: SPEC known answers (tests/test_oracle_spec.py) and fixtures produced by the
+ * reference itself compiled from /root/reference (oracle/_ref, tests/golden/gen_golden.py).
+ * The multiply loop and the plan builders are ABSENT from the reference code,
+ * so those are restatements of SPEC/PAPER pinned by SPEC's known answers and by the
+ * reference's compiled KernelTable (whose masked-FMA contract they reuse).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* ---------------------------------------------------------------- rng (rng.hpp:8-45) */
+
+uint64_t orc_mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+uint64_t orc_hash_coords(uint64_t seed, uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t h = orc_mix64(seed ^ 0x7fb5d329728ea185ULL);
+  h = orc_mix64(h ^ a);
+  h = orc_mix64(h ^ b);
+  return orc_mix64(h ^ c);
+}
+
+double orc_unit_double(uint64_t x) { return (double)(x >> 11) * 0x1.0p-53; }
+
+typedef struct {
+  uint64_t seed;
+  uint64_t counter;
+} orc_counter_rng;
+
+static orc_counter_rng crng_make(uint64_t seed, uint64_t stream) {
+  orc_counter_rng r;
+  r.seed = orc_hash_coords(seed, stream, 0x5eedULL, 0);
+  r.counter = 0;
+  return r;
+}
+static uint64_t crng_next(orc_counter_rng* r) { return orc_mix64(r->seed ^ orc_mix64(r->counter++)); }
+static uint64_t crng_below(orc_counter_rng* r, uint64_t n) {
+  return (uint64_t)(((unsigned __int128)crng_next(r) * n) >> 64);
+}
+
+/* --------------------------------------- reference generators (matgen.hpp:47-148) */
+
+/* draw_value: matgen.hpp:47-51 — magnitude 0.5 + u, sign from the hash's low bit. */
+static float ref_draw_value(uint64_t seed, int64_t i, int64_t j) {
+  const uint64_t h = orc_hash_coords(seed, 2, (uint64_t)i, (uint64_t)j);
+  const double mag = 0.5 + orc_unit_double(h);
+  return (h & 1) ? (float)(-mag) : (float)mag;
+}
+
+/* sample_zero_units: matgen.hpp:56-69 (seeded partial Fisher-Yates, exact count). */
+static uint8_t* ref_sample_zero_units(int64_t n_units, double target, uint64_t seed) {
+  uint8_t* zero = (uint8_t*)calloc((size_t)(n_units > 0 ? n_units : 1), 1);
+  const int64_t k = llround(target * (double)n_units);
+  if (k <= 0) return zero;
+  int64_t* idx = (int64_t*)malloc(sizeof(int64_t) * (size_t)n_units);
+  for (int64_t t = 0; t < n_units; ++t) idx[t] = t;
+  orc_counter_rng rng = crng_make(seed, 3);
+  for (int64_t t = 0; t < k; ++t) {
+    const int64_t pick = t + (int64_t)crng_below(&rng, (uint64_t)(n_units - t));
+    int64_t tmp = idx[t];
+    idx[t] = idx[pick];
+    idx[pick] = tmp;
+    zero[idx[t]] = 1;
+  }
+  free(idx);
+  return zero;
+}
+
+/*
+ * generate<float>: matgen.hpp:77-148.  structure: 0 random, 1 block_random, 2 column,
+ * 3 block_column.  `out` is rows x ld (ld = padded cols, zero-initialised by us like the
+ * Matrix ctor at matrix.hpp:82).  block_len == 0 selects the structure default
+ * (matgen.hpp:83-85) using region_width / w passed in.
+ * Returns 0 on success, -1 on invalid arguments (the reference throws invalid_argument).
+ */
+int orc_ref_generate(float* out, int64_t rows, int64_t cols, int64_t ld, int structure,
+                     double target, int64_t block_len, uint64_t seed, int64_t region_width,
+                     int64_t lane_w) {
+  if (target < 0.0 || target > 1.0) return -1;
+  if (rows <= 0 || cols <= 0 || ld < cols) return -1;
+  memset(out, 0, sizeof(float) * (size_t)(rows * ld));
+  int64_t blk = block_len;
+  if (blk == 0) blk = structure == 3 ? lane_w : region_width;
+  if (structure == 1 || structure == 3) {
+    if (blk <= 0 || ld % blk != 0) return -1;
+  }
+  switch (structure) {
+    case 0: {
+#pragma omp parallel for schedule(static)
+      for (int64_t i = 0; i < rows; ++i) {
+        float* r = out + i * ld;
+        for (int64_t j = 0; j < cols; ++j) {
+          const uint64_t h = orc_hash_coords(seed, 1, (uint64_t)i, (uint64_t)j);
+          r[j] = orc_unit_double(h) < target ? 0.0f : ref_draw_value(seed, i, j);
+        }
+      }
+      break;
+    }
+    case 1: {
+      const int64_t bpr = (cols + blk - 1) / blk;
+      uint8_t* zero = ref_sample_zero_units(rows * bpr, target, seed);
+#pragma omp parallel for schedule(static)
+      for (int64_t i = 0; i < rows; ++i) {
+        float* r = out + i * ld;
+        for (int64_t b = 0; b < bpr; ++b) {
+          if (zero[i * bpr + b]) continue;
+          const int64_t end = (b + 1) * blk < cols ? (b + 1) * blk : cols;
+          for (int64_t j = b * blk; j < end; ++j) r[j] = ref_draw_value(seed, i, j);
+        }
+      }
+      free(zero);
+      break;
+    }
+    case 2: {
+      uint8_t* zero = ref_sample_zero_units(cols, target, seed);
+#pragma omp parallel for schedule(static)
+      for (int64_t i = 0; i < rows; ++i) {
+        float* r = out + i * ld;
+        for (int64_t j = 0; j < cols; ++j)
+          if (!zero[j]) r[j] = ref_draw_value(seed, i, j);
+      }
+      free(zero);
+      break;
+    }
+    case 3: {
+      const int64_t groups = (cols + blk - 1) / blk;
+      uint8_t* zero = ref_sample_zero_units(groups, target, seed);
+#pragma omp parallel for schedule(static)
+      for (int64_t i = 0; i < rows; ++i) {
+        float* r = out + i * ld;
+        for (int64_t j = 0; j < cols; ++j)
+          if (!zero[j / blk]) r[j] = ref_draw_value(seed, i, j);
+      }
+      free(zero);
+      break;
+    }
+    default:
+      return -1;
+  }
+  return 0;
+}
+
+/*
+ * BASELINE.json i.i.d. generators, same counter hash as rng.hpp:18-26.
+ *   value:  0 uniform  v = float(2u - 1),           u = unit(hash(seed, 2, i, j))
+ *           1 normal   v = float(sigma * g)
+ *           2 relu     v = float(max(g - thresh, 0))
+ *           with g = sqrt(-2 log1p(-u1)) * cos(2 pi u2), u1 = unit(hash(seed,2,i,j)),
+ *                                                        u2 = unit(hash(seed,3,i,j))
+ *   mask:   0 none
+ *           1 element zero i.i.d. with probability p:  unit(hash(seed, 1, i, j)) < p
+ *           2 aligned block of `block` columns zero with probability p:
+ *                                                      unit(hash(seed, 4, i, j / block)) < p
+ * The product's device generator (mmmcu_generate) implements the same formulas; tests
+ * check the two agree bit for bit on the uniform/mask modes.
+ */
+int orc_gen_iid(float* out, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, int value_kind,
+                double sigma, double thresh, int mask_kind, double p, int64_t block) {
+  if (rows <= 0 || cols <= 0 || ld < cols) return -1;
+  if (mask_kind == 2 && block <= 0) return -1;
+  const double two_pi = 6.283185307179586476925286766559;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < rows; ++i) {
+    float* r = out + i * ld;
+    for (int64_t j = cols; j < ld; ++j) r[j] = 0.0f;
+    for (int64_t j = 0; j < cols; ++j) {
+      int zero = 0;
+      if (mask_kind == 1)
+        zero = orc_unit_double(orc_hash_coords(seed, 1, (uint64_t)i, (uint64_t)j)) < p;
+      else if (mask_kind == 2)
+        zero = orc_unit_double(orc_hash_coords(seed, 4, (uint64_t)i, (uint64_t)(j / block))) < p;
+      if (zero) {
+        r[j] = 0.0f;
+        continue;
+      }
+      const double u1 = orc_unit_double(orc_hash_coords(seed, 2, (uint64_t)i, (uint64_t)j));
+      if (value_kind == 0) {
+        r[j] = (float)(2.0 * u1 - 1.0);
+      } else {
+        const double u2 = orc_unit_double(orc_hash_coords(seed, 3, (uint64_t)i, (uint64_t)j));
+        const double rad = sqrt(-2.0 * log1p(-u1));
+        const double g = rad * cos(two_pi * u2);
+        if (value_kind == 1) {
+          r[j] = (float)(sigma * g);
+        } else {
+          const double d = g - thresh;
+          r[j] = d > 0.0 ? (float)d : 0.0f;
+        }
+      }
+    }
+  }
+  return 0;
+}
+
+/* --------------------------------------------------- masked region FMA (kernel_table) */
+
+/*
+ * The KernelTable contract (kernel_table.hpp:30-54, kernel_table.cpp:12-28, 64-92):
+ * entry `code` of a P-bit table performs c[l] = fma(a, b[l], c[l]) on exactly the groups
+ * j (width G = W*V) whose bit (P-1-j) is set — MSB first — and touches nothing else.
+ * The reference realises P > 8 by chaining two 8-bit routines; the net effect is the same.
+ */
+int orc_region_fma(uint32_t code, int group_width, int pattern_bits, float* c, float a,
+                   const float* b) {
+  if (pattern_bits < 1 || pattern_bits > 16) return -1;
+  for (int j = 0; j < pattern_bits; ++j) {
+    if (!((code >> (pattern_bits - 1 - j)) & 1u)) continue;
+    for (int l = 0; l < group_width; ++l) {
+      const int e = j * group_width + l;
+      c[e] = fmaf(a, b[e], c[e]);
+    }
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------- plan: preprocess_b */
+
+/*
+ * Pattern codes for every B row and every region of R = G*P padded columns, row-major:
+ * codes[k * n_regions + r], bit (P-1-j) set iff group j has an element != 0
+ * (PAPER Fig. 9 with the bit sense fixed by SPEC.md:178).
+ * ld must be a multiple of R (Matrix padding, matrix.hpp:70-83).
+ */
+int orc_pattern_codes(const float* B, int64_t K, int64_t ld, int group_width, int pattern_bits,
+                      uint32_t* codes) {
+  const int64_t R = (int64_t)group_width * pattern_bits;
+  if (R <= 0 || ld % R != 0) return -1;
+  const int64_t nreg = ld / R;
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < K; ++k) {
+    const float* row = B + k * ld;
+    for (int64_t r = 0; r < nreg; ++r) {
+      uint32_t code = 0;
+      for (int j = 0; j < pattern_bits; ++j) {
+        int nz = 0;
+        const float* g = row + r * R + (int64_t)j * group_width;
+        for (int l = 0; l < group_width; ++l) nz |= (g[l] != 0.0f);
+        code = (code << 1) | (uint32_t)nz;
+      }
+      codes[k * nreg + r] = code;
+    }
+  }
+  return 0;
+}
+
+/*
+ * BPlan order: one plan per leaf_dim x leaf_dim sub-block of B, plans
+ * numbered leaf-row-major (submatrix_id = lr * n_leaf_cols + lc); inside a plan, codes are
+ * row-major over the leaf's rows, then its regions left to right.  Leaf columns are
+ * counted in padded columns and must be whole regions (leaf_dim % R == 0); edge leaves are
+ * shortened.  Writes the concatenation of all plans into `plans`
+ * (length K * n_regions) and the start offset of each plan into plan_off (n_plans + 1).
+ */
+int orc_bplan_order(const uint32_t* codes, int64_t K, int64_t n_regions, int64_t region_width,
+                    int64_t leaf_dim, uint32_t* plans, int64_t* plan_off) {
+  if (leaf_dim <= 0 || leaf_dim % region_width != 0) return -1;
+  const int64_t regs_per_leaf = leaf_dim / region_width;
+  const int64_t n_lr = (K + leaf_dim - 1) / leaf_dim;
+  const int64_t n_lc = (n_regions + regs_per_leaf - 1) / regs_per_leaf;
+  int64_t pos = 0, p = 0;
+  for (int64_t lr = 0; lr < n_lr; ++lr)
+    for (int64_t lc = 0; lc < n_lc; ++lc) {
+      plan_off[p++] = pos;
+      const int64_t k1 = (lr + 1) * leaf_dim < K ? (lr + 1) * leaf_dim : K;
+      const int64_t r0 = lc * regs_per_leaf;
+      const int64_t r1 = r0 + regs_per_leaf < n_regions ? r0 + regs_per_leaf : n_regions;
+      for (int64_t k = lr * leaf_dim; k < k1; ++k)
+        for (int64_t r = r0; r < r1; ++r) plans[pos++] = codes[k * n_regions + r];
+    }
+  plan_off[p] = pos;
+  return 0;
+}
+
+/* plan_stats: region count, fraction of zero codes, mean popcount. */
+void orc_plan_stats(const uint32_t* codes, int64_t n, int64_t* region_count, double* zero_frac,
+                    double* mean_popc) {
+  int64_t zeros = 0, pop = 0;
+  for (int64_t t = 0; t < n; ++t) {
+    zeros += codes[t] == 0;
+    pop += __builtin_popcount(codes[t]);
+  }
+  *region_count = n;
+  *zero_frac = n ? (double)zeros / (double)n : 0.0;
+  *mean_popc = n ? (double)pop / (double)n : 0.0;
+}
+
+/* ------------------------------------------------------------- plan: preprocess_a */
+
+/*
+ * ABlockIndex (layout decision :229; PAPER Fig. 11).
+ * Canonical flat layout, block-major: for each block_dim x block_dim block of A
+ * (block rows outer, block columns inner), for each row of the block, for each aligned
+ * S = 8 element segment of that block row (the last one shortened at the logical edge):
+ *   counts[s]          number of non-zeros (0..8)
+ *   offsets[8*s + t]   ascending in-segment offsets of the non-zeros, t < count; a full
+ *                      segment (count == 8) stores none; unused slots hold 0xFF.
+ * Segment enumeration order is the order the engine consumes them.  Returns the number
+ * of segments written.
+ */
+int64_t orc_ablock_index(const float* A, int64_t M, int64_t K, int64_t lda, int64_t block_dim,
+                         uint8_t* counts, uint8_t* offsets) {
+  if (block_dim <= 0 || block_dim % 8 != 0) return -1;
+  int64_t s = 0;
+  for (int64_t bi = 0; bi < M; bi += block_dim)
+    for (int64_t bk = 0; bk < K; bk += block_dim) {
+      const int64_t i1 = bi + block_dim < M ? bi + block_dim : M;
+      const int64_t k1 = bk + block_dim < K ? bk + block_dim : K;
+      for (int64_t i = bi; i < i1; ++i)
+        for (int64_t k0 = bk; k0 < k1; k0 += 8) {
+          const int64_t len = k0 + 8 < k1 ? 8 : k1 - k0;
+          uint8_t cnt = 0;
+          uint8_t off[8];
+          for (int t = 0; t < 8; ++t) off[t] = 0xFF;
+          for (int64_t t = 0; t < len; ++t)
+            if (A[i * lda + k0 + t] != 0.0f) off[cnt++] = (uint8_t)t;
+          counts[s] = cnt;
+          if (cnt == 8)
+            memset(offsets + 8 * s, 0xFF, 8);
+          else
+            memcpy(offsets + 8 * s, off, 8);
+          ++s;
+        }
+    }
+  return s;
+}
+
+/* Per-row bitmap, LSB-first: bit b of word w <-> column 32w + b (canonical GPU format). */
+void orc_a_bitmap(const float* A, int64_t M, int64_t K, int64_t lda, uint32_t* bits) {
+  const int64_t words = (K + 31) / 32;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < M; ++i)
+    for (int64_t w = 0; w < words; ++w) {
+      uint32_t v = 0;
+      for (int b = 0; b < 32; ++b) {
+        const int64_t k = w * 32 + b;
+        if (k < K && A[i * lda + k] != 0.0f) v |= 1u << b;
+      }
+      bits[i * words + w] = v;
+    }
+}
+
+/* CSR of A: row_ptr[M+1] (int64) and ascending column indices (canonical GPU format). */
+int64_t orc_a_csr(const float* A, int64_t M, int64_t K, int64_t lda, int64_t* row_ptr,
+                  uint32_t* cols) {
+  int64_t nnz = 0;
+  for (int64_t i = 0; i < M; ++i) {
+    row_ptr[i] = nnz;
+    for (int64_t k = 0; k < K; ++k)
+      if (A[i * lda + k] != 0.0f) {
+        if (cols) cols[nnz] = (uint32_t)k;
+        ++nnz;
+      }
+  }
+  row_ptr[M] = nnz;
+  return nnz;
+}
+
+/* ---------------------------------------------------------------------- engine */
+
+typedef struct {
+  uint64_t kernel_invocations;
+  uint64_t lane_fma_ops;
+  uint64_t rows_skipped;
+  uint64_t regions_skipped_by_zero_code;
+} orc_counters;
+
+/* multiply_simple (PAPER Fig. 2): c += a*b, i-k-j, fused fma per term. */
+void orc_multiply_simple(float* C, int64_t ldc, const float* A, int64_t lda, const float* B,
+                         int64_t ldb, int64_t M, int64_t K, int64_t N) {
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t i = 0; i < M; ++i) {
+    float* c = C + i * ldc;
+    for (int64_t k = 0; k < K; ++k) {
+      const float a = A[i * lda + k];
+      const float* b = B + k * ldb;
+      for (int64_t j = 0; j < N; ++j) c[j] = fmaf(a, b[j], c[j]);
+    }
+  }
+}
+
+/*
+ * multiply_mmm (PAPER Fig. 10, Fig. 4): for every row i, walk the
+ * non-zeros of A in ascending k; for each, consume B row k's pattern codes region by
+ * region and apply the masked region FMA (orc_region_fma == KernelTable::apply).
+ * Counters follow SPEC.md:252-255/279/297-298:
+ *   rows_skipped                 one per zero A element (a whole B row skipped),
+ *   kernel_invocations           one per (non-zero a_ik, region with code != 0),
+ *   regions_skipped_by_zero_code one per (non-zero a_ik, region with code == 0),
+ *   lane_fma_ops                 popcount(code) * G per dispatched region.
+ * `codes` is row-major [K][ldb / R] from orc_pattern_codes.  N is the logical column
+ * count of C; regions may extend into zero padding of B and C (matrix.hpp:61-83), which
+ * requires ldc >= ldb.  Per C element the result is the ascending-k fmaf chain over the
+ * surviving terms, so it is deterministic and independent of the thread count.
+ */
+int orc_multiply_mmm(float* C, int64_t ldc, const float* A, int64_t lda, const float* B,
+                     int64_t ldb, int64_t M, int64_t K, int64_t N, const uint32_t* codes,
+                     int group_width, int pattern_bits, orc_counters* out) {
+  const int64_t R = (int64_t)group_width * pattern_bits;
+  if (R <= 0 || ldb % R != 0 || ldc < ldb || N > ldb) return -1;
+  const int64_t nreg = ldb / R;
+  uint64_t inv = 0, lanes = 0, skipped = 0, zreg = 0;
+#pragma omp parallel for schedule(dynamic, 4) reduction(+ : inv, lanes, skipped, zreg)
+  for (int64_t i = 0; i < M; ++i) {
+    float* c = C + i * ldc;
+    for (int64_t k = 0; k < K; ++k) {
+      const float a = A[i * lda + k];
+      if (a == 0.0f) {
+        ++skipped;
+        continue;
+      }
+      const uint32_t* code = codes + k * nreg;
+      const float* b = B + k * ldb;
+      for (int64_t r = 0; r < nreg; ++r) {
+        if (code[r] == 0) {
+          ++zreg;
+          continue;
+        }
+        ++inv;
+        lanes += (uint64_t)__builtin_popcount(code[r]) * (uint64_t)group_width;
+        orc_region_fma(code[r], group_width, pattern_bits, c + r * R, a, b + r * R);
+      }
+    }
+  }
+  if (out) {
+    out->kernel_invocations = inv;
+    out->lane_fma_ops = lanes;
+    out->rows_skipped = skipped;
+    out->regions_skipped_by_zero_code = zreg;
+  }
+  return 0;
+}
+
+/*
+ * Brute-force work count (acceptance 3): Σ over non-zero A entries of
+ * the number of non-zero-group lanes of the matching B row.  Independent of the codes.
+ */
+uint64_t orc_bruteforce_lane_ops(const float* A, int64_t lda, const float* B, int64_t ldb,
+                                 int64_t M, int64_t K, int group_width) {
+  uint64_t* row_lanes = (uint64_t*)calloc((size_t)K, sizeof(uint64_t));
+  for (int64_t k = 0; k < K; ++k) {
+    uint64_t n = 0;
+    for (int64_t g = 0; g < ldb; g += group_width) {
+      int nz = 0;
+      for (int l = 0; l < group_width; ++l) nz |= B[k * ldb + g + l] != 0.0f;
+      n += nz ? (uint64_t)group_width : 0;
+    }
+    row_lanes[k] = n;
+  }
+  uint64_t total = 0;
+#pragma omp parallel for reduction(+ : total)
+  for (int64_t i = 0; i < M; ++i)
+    for (int64_t k = 0; k < K; ++k)
+      if (A[i * lda + k] != 0.0f) total += row_lanes[k];
+  free(row_lanes);
+  return total;
+}
+
+/*
+ * Tolerance check of SURVEY.md §8(d): |C_gpu - C_ref| <= tol * Σ_k |a_ik||b_kj| with the
+ * denominator in fp64.  Rows listed in `rows` (n_rows of them; all rows when rows==NULL).
+ * Returns the number of violating elements and the max ratio |Δ| / Σ|a||b| seen.
+ */
+int64_t orc_check_tolerance(const float* Cg, const float* Cr, int64_t ldc, const float* A,
+                            int64_t lda, const float* B, int64_t ldb, int64_t M, int64_t K,
+                            int64_t N, const int64_t* rows, int64_t n_rows, double tol,
+                            double* max_ratio) {
+  int64_t bad = 0;
+  double worst = 0.0;
+  const int64_t nr = rows ? n_rows : M;
+#pragma omp parallel
+  {
+    double* den = (double*)malloc(sizeof(double) * (size_t)N);
+    double my_worst = 0.0;
+    int64_t my_bad = 0;
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t t = 0; t < nr; ++t) {
+      const int64_t i = rows ? rows[t] : t;
+      for (int64_t j = 0; j < N; ++j) den[j] = 0.0;
+      for (int64_t k = 0; k < K; ++k) {
+        const double a = fabs((double)A[i * lda + k]);
+        if (a == 0.0) continue;
+        const float* b = B + k * ldb;
+        for (int64_t j = 0; j < N; ++j) den[j] += a * fabs((double)b[j]);
+      }
+      for (int64_t j = 0; j < N; ++j) {
+        const double d = fabs((double)Cg[i * ldc + j] - (double)Cr[i * ldc + j]);
+        const double lim = tol * den[j];
+        if (!(d <= lim)) ++my_bad;
+        const double ratio = den[j] > 0.0 ? d / den[j] : (d > 0.0 ? INFINITY : 0.0);
+        if (ratio > my_worst) my_worst = ratio;
+      }
+    }
+#pragma omp critical
+    {
+      bad += my_bad;
+      if (my_worst > worst) worst = my_worst;
+    }
+    free(den);
+  }
+  if (max_ratio) *max_ratio = worst;
+  return bad;
+}
+
+int orc_num_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}

@@ -1,0 +1,188 @@
+// ref_driver.cpp — thin extern "C" shim over the REFERENCE's own compiled code.
+//
+// TEST INFRASTRUCTURE ONLY (see oracle/mmm_oracle.c header).  Built by oracle/Makefile
+// against the reference sources where they lie (/root/reference/proj/include and
+// /root/reference/proj/src/{kernel_table,matrix_io}.cpp); the output goes to oracle/_ref/
+// and is never shipped in the product.  Used for:
+//   * golden fixtures (tests/golden/gen_golden.py): reference generate<float>
+//     (matgen.hpp:77-148), KernelTable<float>::build/apply (kernel_table.cpp:64-92,
+//     kernel_table.hpp:50-54), MMMB write/read (matrix_io.cpp:59-97);
+//   * the reference-kind CPU baseline (bench.py --impl reference / cpu_baseline): the
+//     SPEC multiply_parallel whose inner loop is the reference's own
+//     KernelTable::apply dispatch, over reference Matrix<float> operands (matrix.hpp:65).
+//     The engine itself is absent from the reference, so the outer loops
+//     here are the SPEC restatement; the arithmetic is the reference's compiled kernels.
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <stdexcept>
+#include <vector>
+
+#include <omp.h>
+
+#include "mmm/kernel_table.hpp"
+#include "mmm/matgen.hpp"
+#include "mmm/matrix.hpp"
+#include "mmm/matrix_io.hpp"
+
+using mmm::KernelTable;
+using mmm::LaneConfig;
+using mmm::Matrix;
+
+namespace {
+
+int status_of(const std::exception& e) {
+  if (dynamic_cast<const std::invalid_argument*>(&e)) return 1;
+  if (dynamic_cast<const std::overflow_error*>(&e)) return 2;
+  if (dynamic_cast<const mmm::BadMagicError*>(&e)) return 10;
+  if (dynamic_cast<const mmm::TruncatedFileError*>(&e)) return 11;
+  if (dynamic_cast<const mmm::UnknownDtypeError*>(&e)) return 12;
+  if (dynamic_cast<const mmm::IoError*>(&e)) return 13;
+  if (dynamic_cast<const mmm::MatrixFileError*>(&e)) return 14;
+  return 99;
+}
+
+Matrix<float> from_dense(const float* src, int64_t rows, int64_t cols, int64_t ld) {
+  Matrix<float> m(rows, cols);
+  for (int64_t i = 0; i < rows; ++i) std::memcpy(m.row(i), src + i * ld, sizeof(float) * cols);
+  return m;
+}
+
+}  // namespace
+
+extern "C" {
+
+// generate<float> (matgen.hpp:77) -> padded rows x padded_cols copy into out.
+int ref_generate_f32(int64_t rows, int64_t cols, int structure, double target, int64_t block_len,
+                     uint64_t seed, int w, int p, int v, float* out, int64_t* padded_cols) {
+  try {
+    mmm::SparsitySpec spec;
+    spec.structure = static_cast<mmm::Structure>(structure);
+    spec.target = target;
+    spec.block_len = block_len;
+    spec.seed = seed;
+    Matrix<float> m = mmm::generate<float>(rows, cols, spec, LaneConfig{w, p, v});
+    *padded_cols = m.padded_cols();
+    if (out) std::memcpy(out, m.data(), sizeof(float) * rows * m.padded_cols());
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
+
+// KernelTable<float>::build(lane) then apply(code, c, a, b) (kernel_table.hpp:50-54).
+int ref_kernel_apply_f32(int w, int p, int v, uint32_t code, float* c, float a, const float* b) {
+  try {
+    const KernelTable<float> t = KernelTable<float>::build(LaneConfig{w, p, v});
+    if (code >= t.size()) return 3;
+    t.apply(code, c, a, b);
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
+
+int ref_write_matrix_f32(const float* src, int64_t rows, int64_t cols, int64_t ld, const char* path) {
+  try {
+    mmm::write_matrix(from_dense(src, rows, cols, ld), path);
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
+
+int ref_read_matrix_f32(const char* path, float* out, int64_t rows, int64_t cols, int64_t ld) {
+  try {
+    Matrix<float> m = mmm::read_matrix<float>(path);
+    if (m.rows() != rows || m.cols() != cols) return 20;
+    for (int64_t i = 0; i < rows; ++i) std::memcpy(out + i * ld, m.row(i), sizeof(float) * cols);
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
+
+struct ref_counters {
+  uint64_t kernel_invocations, lane_fma_ops, rows_skipped, regions_skipped_by_zero_code;
+  int64_t preprocess_ns, multiply_ns;
+};
+
+// SPEC multiply_parallel over the reference's KernelTable (C += A*B, f32 default lanes).
+// A: M x K (lda), B: K x N (ldb), C: M x N (ldc), all host row-major.  Rows [row0, row1)
+// of A/C only, so a bounded CPU sample can be timed.  Threads: OpenMP over rows (the
+// reference's own parallelism, matrix.hpp:170); workers <= 0 uses all.
+int ref_multiply_parallel_f32(float* C, int64_t ldc, const float* A, int64_t lda, const float* B,
+                              int64_t ldb, int64_t M, int64_t K, int64_t N, int64_t row0,
+                              int64_t row1, int workers, ref_counters* out) {
+  try {
+    const LaneConfig lane = LaneConfig::defaults(mmm::Dtype::f32);
+    const KernelTable<float> table = KernelTable<float>::build(lane);
+    const int64_t R = lane.region_width();
+    if (workers > 0) omp_set_num_threads(workers);
+    // Operands in the reference layout (padded, 256-B aligned; matrix.hpp:70-83).
+    Matrix<float> b = from_dense(B, K, N, ldb);
+    const int64_t nreg = b.padded_cols() / R;
+    const auto t0 = std::chrono::steady_clock::now();
+    // preprocess_b: one P-bit code per region, MSB-first.
+    std::vector<uint16_t> codes(static_cast<size_t>(K * nreg));
+#pragma omp parallel for schedule(static)
+    for (int64_t k = 0; k < K; ++k) {
+      const float* row = b.row(k);
+      for (int64_t r = 0; r < nreg; ++r) {
+        uint32_t code = 0;
+        for (int j = 0; j < lane.p; ++j) {
+          bool nz = false;
+          for (int l = 0; l < lane.group_width(); ++l) nz |= row[r * R + j * lane.group_width() + l] != 0.0f;
+          code = (code << 1) | static_cast<uint32_t>(nz);
+        }
+        codes[k * nreg + r] = static_cast<uint16_t>(code);
+      }
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+    uint64_t inv = 0, lanes = 0, skipped = 0, zreg = 0;
+    const int64_t padc = b.padded_cols();
+    const int64_t nrows = row1 - row0;
+    std::vector<float> cbuf(static_cast<size_t>(nrows > 0 ? nrows : 1) * padc, 0.0f);
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : inv, lanes, skipped, zreg)
+    for (int64_t i = row0; i < row1; ++i) {
+      float* c = cbuf.data() + (i - row0) * padc;
+      std::memcpy(c, C + i * ldc, sizeof(float) * N);
+      for (int64_t k = 0; k < K; ++k) {
+        const float av = A[i * lda + k];
+        if (av == 0.0f) {
+          ++skipped;
+          continue;
+        }
+        const uint16_t* code = codes.data() + k * nreg;
+        const float* brow = b.row(k);
+        for (int64_t r = 0; r < nreg; ++r) {
+          if (code[r] == 0) {
+            ++zreg;
+            continue;
+          }
+          ++inv;
+          lanes += static_cast<uint64_t>(__builtin_popcount(code[r])) * lane.group_width();
+          table.apply(code[r], c + r * R, av, brow + r * R);  // the reference kernel
+        }
+      }
+      std::memcpy(C + i * ldc, c, sizeof(float) * N);
+    }
+    const auto t2 = std::chrono::steady_clock::now();
+    if (out) {
+      out->kernel_invocations = inv;
+      out->lane_fma_ops = lanes;
+      out->rows_skipped = skipped;
+      out->regions_skipped_by_zero_code = zreg;
+      out->preprocess_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+      out->multiply_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(t2 - t1).count();
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
+
+int ref_max_threads(void) { return omp_get_max_threads(); }
+
+}  // extern "C"

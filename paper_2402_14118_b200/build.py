@@ -1,0 +1,51 @@
+"""In-tree build of the CUDA library (sm_100a) and of the oracle (test infrastructure).
+
+    python -m paper_2402_14118_b200.build          # libmmmcu.so (+ oracle, + oracle/_ref)
+
+The library is compiled straight with nvcc (-gencode arch=compute_100a,code=sm_100a
+-lineinfo) into paper_2402_14118_b200/_lib/ so it travels with the repo snapshot.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _run(cmd, cwd=None):
+    print("+", " ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True, cwd=cwd)
+
+
+def build_lib(verbose_ptxas: bool = False) -> str:
+    out_dir = os.path.join(HERE, "_lib")
+    os.makedirs(out_dir, exist_ok=True)
+    out = os.path.join(out_dir, "libmmmcu.so")
+    src = os.path.join(HERE, "csrc", "mmmcu.cu")
+    cmd = [NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+           "-I", os.path.join(ROOT, "include"), "-o", out, src]
+    if verbose_ptxas:
+        cmd.insert(1, "-Xptxas=-v")
+    _run(cmd)
+    return out
+
+
+def build_oracle() -> None:
+    env_make = ["make", "-C", os.path.join(ROOT, "oracle")]
+    _run(env_make)
+    if os.path.isdir("/root/reference/proj"):
+        _run(env_make + ["ref"])
+
+
+def main(argv=None):
+    build_lib()
+    build_oracle()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])

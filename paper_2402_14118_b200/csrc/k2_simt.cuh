@@ -1,0 +1,281 @@
+// K2-SIMT — masked fp32 GEMM on the CUDA cores (sm_100a), exact ascending-k fmaf chains.
+//
+// Replaces SPEC multiply_mmm / multiply_parallel (PAPER Fig. 10,
+// PAPER.md:426-436).  The paper's runtime code lookup — one indirect call per
+// (non-zero a_ik, 64-wide region), dispatching a straight-line routine that FMAs only the
+// non-zero 8-wide groups (kernel_table.cpp:12-28) — becomes mask intersection here:
+//
+//   CTA   = 128 rows x 256 columns of C; 16 warps; one 16-column slice per warp.
+//   lane  = 4 rows (4l .. 4l+3 of the tile) x 16 columns: 64 fp32 accumulators that start
+//           from C (c += a*b semantics) and end in C.
+//   k     = walked in chunks of 64.  For every chunk each warp reads the B block masks of
+//           its slice (K1's transposed group bitmaps) and iterates ONLY the k whose B block
+//           is non-zero (warp-uniform loop: no divergence, the B-side skip of Fig. 10's
+//           `fps[code]`).  A's element mask is applied per lane by predication (the A-side
+//           skip of Fig. 4): a lane whose a_ik == 0 issues no FMA for that row.
+//   smem  = double-buffered A^T chunk [64 k][128 rows] (swizzled, 32 KB) + B chunk
+//           [64 k][256 cols] (64 KB) of which only non-zero 8/16-column blocks are fetched
+//           (cp.async, 16 B granules).  B values reach the FMAs as warp broadcasts.
+//
+// Every C element receives fmaf(a_ik, b_kj, c) for its surviving k in ascending order,
+// exactly the oracle's chain (orc_multiply_mmm), so results are bit-identical.  Groups of
+// the 16-column slice whose own code bit is 0 while the sibling group is non-zero are
+// FMA'd with b = +0.0 (exact no-op for finite a and c != -0.0; SPAN=8 avoids even that).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mmmcu {
+
+constexpr int kK2Threads = 512;
+constexpr int kK2TM = 128;  // rows per CTA
+constexpr int kK2TN = 256;  // columns per CTA (16 warps x 16)
+constexpr int kK2KC = 64;   // k per chunk
+constexpr int kK2SmemA = kK2KC * kK2TM * 4;
+constexpr int kK2SmemB = kK2KC * kK2TN * 4;
+constexpr int kK2Smem = 2 * (kK2SmemA + kK2SmemB);  // 192 KB
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// A^T chunk index: 4-row groups XOR-swizzled by (k/4)%8 so that the transposing stores
+// are at most 2-way bank conflicted and each lane's 4-row LDS.128 stays contiguous.
+__device__ __forceinline__ int at_index(int k, int row) { return k * kK2TM + (row ^ (((k >> 2) & 7) << 2)); }
+
+// 64-bit k-mask of a 16-column slice for chunk words (w0, w0+1) from the group bitmaps.
+__device__ __forceinline__ uint64_t slice_mask(const uint32_t* __restrict__ bgrp, int64_t kw, int64_t g0,
+                                               int64_t w0, int groups) {
+  uint64_t m = 0;
+  for (int g = 0; g < groups; ++g) {
+    const uint32_t* p = bgrp + (g0 + g) * kw;
+    const uint32_t lo = w0 < kw ? p[w0] : 0u;
+    const uint32_t hi = w0 + 1 < kw ? p[w0 + 1] : 0u;
+    m |= (uint64_t)lo | ((uint64_t)hi << 32);
+  }
+  return m;
+}
+
+// SPAN = width (columns) of the block mask a warp iterates: 16 (one mask for the slice,
+// the natural choice for B block widths >= 16) or 8 (two masks, one per 8-wide group:
+// exact group-level skipping for 8-wide blocks).
+template <int SPAN>
+__global__ void __launch_bounds__(kK2Threads, 1)
+k2_simt_bcast(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb,
+              float* __restrict__ C, int64_t ldc, int64_t M, int64_t K, int64_t Np,
+              const uint32_t* __restrict__ bgrp, int64_t kw, const unsigned long long* __restrict__ sel) {
+  static_assert(SPAN == 8 || SPAN == 16, "SPAN must be 8 or 16");
+  if (sel && *sel != (unsigned long long)SPAN) return;  // device-side variant choice (k1_finalize)
+  constexpr int NS = 16 / SPAN;  // spans per warp
+  extern __shared__ __align__(16) float smem[];
+  // stage st: A^T at smem + st*KC*TM, B at smem + 2*KC*TM + st*KC*TN (no pointer arrays:
+  // dynamically indexed local arrays would live in local memory)
+  auto sA = [&](int st) { return smem + st * (kK2KC * kK2TM); };
+  auto sB = [&](int st) { return smem + 2 * kK2KC * kK2TM + st * (kK2KC * kK2TN); };
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t m0 = (int64_t)blockIdx.y * kK2TM;
+  const int64_t n0 = (int64_t)blockIdx.x * kK2TN;
+  const int64_t ncol = n0 + 16 * warp;           // this warp's 16-column slice
+  const bool slice_ok = ncol < Np;               // Np is a multiple of 64
+  const int64_t g0 = ncol >> 3;                  // first 8-column group of the slice
+
+  // ---- accumulators start from C (c += a*b)
+  float2 acc[NS][4][SPAN / 2];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int64_t row = m0 + 4 * lane + r;
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+#pragma unroll
+      for (int j = 0; j < SPAN / 2; ++j) {
+        float2 v = make_float2(0.f, 0.f);
+        if (slice_ok && row < M) v = *reinterpret_cast<const float2*>(C + row * ldc + ncol + s * SPAN + 2 * j);
+        acc[s][r][j] = v;
+      }
+  }
+
+  const int64_t nchunks = (K + kK2KC - 1) / kK2KC;
+
+  // ---- staging helpers
+  // A: 128 rows x 64 k = 2048 float4; thread t loads f = t + 512 j: row f/16, kq f%16.
+  float4 areg[4];
+  auto load_a = [&](int64_t c) {
+    const int64_t k0 = c * kK2KC;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int f = tid + kK2Threads * j;
+      const int row = f >> 4, kq = f & 15;
+      const int64_t gr = m0 + row, gk = k0 + 4 * kq;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (gr < M && gk < K) {
+        v = __ldg(reinterpret_cast<const float4*>(A + gr * lda + gk));
+        // K need not be a multiple of 4: zero the columns past K (reads stay inside lda)
+        if (gk + 4 > K) {
+          if (gk + 1 >= K) v.y = 0.f;
+          if (gk + 2 >= K) v.z = 0.f;
+          if (gk + 3 >= K) v.w = 0.f;
+        }
+      }
+      areg[j] = v;
+    }
+  };
+  auto store_a = [&](float* dst) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int f = tid + kK2Threads * j;
+      const int row = f >> 4, kq = f & 15;
+      dst[at_index(4 * kq + 0, row)] = areg[j].x;
+      dst[at_index(4 * kq + 1, row)] = areg[j].y;
+      dst[at_index(4 * kq + 2, row)] = areg[j].z;
+      dst[at_index(4 * kq + 3, row)] = areg[j].w;
+    }
+  };
+  // B: only the non-zero (k, slice) rows of this warp's slice: 4 lanes x 16 B per k row.
+  auto load_b = [&](int64_t c, float* dst, uint64_t mask) {
+    if (!slice_ok) return;
+    const int64_t k0 = c * kK2KC;
+    const int grp = lane >> 2, piece = lane & 3;
+    uint64_t m = mask;
+    while (m) {  // warp-uniform: 8 k rows per pass, 4 lanes (4 x 16 B) per row
+      uint64_t t = m;
+      for (int i = 0; i < grp; ++i) t &= t - 1;  // drop this group's predecessors
+      if (t) {
+        const int kk = __ffsll((long long)t) - 1;
+        cp_async16(dst + kk * kK2TN + 16 * warp + 4 * piece, B + (k0 + kk) * ldb + ncol + 4 * piece);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) m &= m - 1;  // (m & (m-1)) of 0 stays 0
+    }
+  };
+
+  uint64_t mask_cur[NS], mask_nxt[NS];
+  auto masks_for = [&](int64_t c, uint64_t* out) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+      out[s] = slice_ok ? slice_mask(bgrp, kw, g0 + s * (SPAN / 8), 2 * c, SPAN / 8) : 0ull;
+  };
+
+  // ---- prologue: chunk 0
+  masks_for(0, mask_cur);
+  load_a(0);
+  store_a(sA(0));
+  load_b(0, sB(0), NS == 1 ? mask_cur[0] : (mask_cur[0] | mask_cur[NS - 1]));
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int st = (int)(c & 1);
+    const bool more = c + 1 < nchunks;
+    if (more) {
+      masks_for(c + 1, mask_nxt);
+      load_a(c + 1);
+      load_b(c + 1, sB(st ^ 1), NS == 1 ? mask_nxt[0] : (mask_nxt[0] | mask_nxt[NS - 1]));
+      cp_async_commit();
+    }
+    // ---- compute chunk c: warp-uniform walk over the slice's non-zero B rows
+    const float* at = sA(st);
+    const float* bs = sB(st) + 16 * warp;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      uint64_t m = mask_cur[s];
+      while (m) {
+        const int kk = __ffsll((long long)m) - 1;
+        m &= m - 1;
+        const float4 av = *reinterpret_cast<const float4*>(at + at_index(kk, 4 * lane));
+        float2 b[SPAN / 2];
+#pragma unroll
+        for (int q = 0; q < SPAN / 4; ++q) {
+          const float4 bv = *reinterpret_cast<const float4*>(bs + kk * kK2TN + s * SPAN + 4 * q);
+          b[2 * q] = make_float2(bv.x, bv.y);
+          b[2 * q + 1] = make_float2(bv.z, bv.w);
+        }
+        const float a4[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if (a4[r] != 0.0f) {
+            const float2 a2 = make_float2(a4[r], a4[r]);
+#pragma unroll
+            for (int j = 0; j < SPAN / 2; ++j) acc[s][r][j] = __ffma2_rn(a2, b[j], acc[s][r][j]);
+          }
+        }
+      }
+    }
+    if (more) {
+      store_a(sA(st ^ 1));
+#pragma unroll
+      for (int s = 0; s < NS; ++s) mask_cur[s] = mask_nxt[s];
+    }
+    cp_async_wait_all();
+    __syncthreads();
+  }
+
+  // ---- epilogue: write the accumulators back
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int64_t row = m0 + 4 * lane + r;
+    if (!slice_ok || row >= M) continue;
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+#pragma unroll
+      for (int j = 0; j < SPAN / 2; ++j)
+        *reinterpret_cast<float2*>(C + row * ldc + ncol + s * SPAN + 2 * j) = acc[s][r][j];
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// multiply_simple (PAPER Fig. 2): dense C += A*B, ascending-k fmaf per
+// element (bit-identical to orc_multiply_simple).  64x64 tiles, 256 threads, 4x4 per thread.
+__global__ void __launch_bounds__(256)
+k2_dense(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb, float* __restrict__ C,
+         int64_t ldc, int64_t M, int64_t K, int64_t N) {
+  __shared__ float sa[16][64 + 4];
+  __shared__ float sb[16][64];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t m0 = (int64_t)blockIdx.y * 64, n0 = (int64_t)blockIdx.x * 64;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t r = m0 + ty * 4 + i, cc = n0 + tx * 4 + j;
+      acc[i][j] = (r < M && cc < N) ? C[r * ldc + cc] : 0.f;
+    }
+  for (int64_t k0 = 0; k0 < K; k0 += 16) {
+    for (int t = threadIdx.x; t < 16 * 64; t += 256) {
+      const int kk = t & 15, rr = t >> 4;
+      const int64_t gr = m0 + rr, gk = k0 + kk;
+      sa[kk][rr] = (gr < M && gk < K) ? A[gr * lda + gk] : 0.f;
+      const int cc = t & 63, kb = t >> 6;
+      const int64_t gkb = k0 + kb, gc = n0 + cc;
+      sb[kb][cc] = (gkb < K && gc < N) ? B[gkb * ldb + gc] : 0.f;
+    }
+    __syncthreads();
+    const int kmax = (int)(K - k0 < 16 ? K - k0 : 16);
+    for (int kk = 0; kk < kmax; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = sa[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = sb[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t r = m0 + ty * 4 + i, cc = n0 + tx * 4 + j;
+      if (r < M && cc < N) C[r * ldc + cc] = acc[i][j];
+    }
+}
+
+}  // namespace mmmcu
