@@ -182,13 +182,14 @@ mmmcu_status mmmcu_multiply_host(mmmcu_ctx* ctx, float* C_host, int64_t ldc, con
 
 /*
  * Fill out (rows x ld, device) with the seeded i.i.d. generator of SURVEY.md §8(d), built
- * on the reference's counter hash (rng.hpp:8-26):
+ * on the reference's counter hash (rng.hpp:8-26).  Row r of `out` is global row row0 + r
+ * of the matrix the seed defines (so row shards generate their own slice):
  *   value_kind 0 uniform[-1,1], 1 N(0, sigma), 2 ReLU(N(0,1) - thresh);
  *   mask_kind  0 none, 1 element zero with prob p, 2 aligned `block`-wide runs zero with
  *              prob p.  Columns [cols, ld) are zeroed.
  */
 mmmcu_status mmmcu_generate(mmmcu_ctx* ctx, float* out, int64_t rows, int64_t cols, int64_t ld,
-                            uint64_t seed, int value_kind, double sigma, double thresh,
+                            int64_t row0, uint64_t seed, int value_kind, double sigma, double thresh,
                             int mask_kind, double p, int64_t block);
 
 /* Row partition of a sharded multiply: rank r of `world` owns [*row0, *row1). */

@@ -79,7 +79,8 @@ SIGNATURES = [
                                       c_int64, c_int64]),
     ("mmmcu_multiply_host", c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64,
                                     c_int64, c_int64, POINTER(Counters)]),
-    ("mmmcu_generate", c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_uint64, c_int, c_double, c_double,
+    ("mmmcu_generate", c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64, c_uint64, c_int, c_double,
+                               c_double,
                                c_int, c_double, c_int64]),
     ("mmmcu_shard_rows", c_int, [c_int64, c_int, c_int, POINTER(c_int64), POINTER(c_int64)]),
 ]

@@ -396,12 +396,12 @@ MASK_NONE, MASK_ELEMENT, MASK_BLOCK = 0, 1, 2
 
 def generate(out, seed: int, value_kind: int = VALUE_UNIFORM, sigma: float = 1.0, thresh: float = 0.0,
              mask_kind: int = MASK_NONE, p: float = 0.0, block: int = 1, cols: Optional[int] = None,
-             ctx: Optional[MmmContext] = None):
+             row0: int = 0, ctx: Optional[MmmContext] = None):
     """Fill a CUDA float32 tensor with the seeded i.i.d. generator (mmmcu_generate)."""
     po, ld = _check_tensor(out, "out")
     cx = _ctx_for(out, ctx, LaneConfig())
     cx._sync_stream()
-    cx._check(_lib().mmmcu_generate(cx._h, po, out.shape[0], out.shape[1] if cols is None else cols, ld,
+    cx._check(_lib().mmmcu_generate(cx._h, po, out.shape[0], out.shape[1] if cols is None else cols, ld, int(row0),
                                     ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), value_kind, sigma, thresh,
                                     mask_kind, p, block))
     return out

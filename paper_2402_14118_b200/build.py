@@ -35,6 +35,16 @@ def build_lib(verbose_ptxas: bool = False) -> str:
     return out
 
 
+def build_probe() -> str:
+    """FP32 peak probe used by bench.py for the SIMT roofline denominator (tools/, not product)."""
+    out_dir = os.path.join(ROOT, "tools", "_lib")
+    os.makedirs(out_dir, exist_ok=True)
+    out = os.path.join(out_dir, "libfp32probe.so")
+    _run([NVCC, *GENCODE, "-O3", "-Xcompiler", "-fPIC", "-shared", "-o", out,
+          os.path.join(ROOT, "tools", "probe", "fp32_probe.cu")])
+    return out
+
+
 def build_oracle() -> None:
     env_make = ["make", "-C", os.path.join(ROOT, "oracle")]
     _run(env_make)
@@ -44,6 +54,7 @@ def build_oracle() -> None:
 
 def main(argv=None):
     build_lib()
+    build_probe()
     build_oracle()
 
 

@@ -29,12 +29,12 @@ __device__ __forceinline__ double unit_double(uint64_t x) { return __dmul_rn(__u
 
 // value_kind 0 uniform[-1,1], 1 N(0, sigma), 2 ReLU(N(0,1) - thresh)
 // mask_kind  0 none, 1 element zero w.p. p (stream 1), 2 aligned block zero w.p. p (stream 4)
-__global__ void k_generate(float* __restrict__ out, int64_t rows, int64_t cols, int64_t ld, uint64_t seed,
+__global__ void k_generate(float* __restrict__ out, int64_t rows, int64_t cols, int64_t ld, int64_t row0, uint64_t seed,
                            int value_kind, double sigma, double thresh, int mask_kind, double p, int64_t block) {
   const int64_t total = rows * ld;
   const double two_pi = 6.283185307179586476925286766559;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t / ld, j = t % ld;
+    const int64_t i = row0 + t / ld, j = t % ld;
     float v = 0.0f;
     if (j < cols) {
       bool zero = false;

@@ -41,150 +41,226 @@ __device__ __forceinline__ uint32_t nz4(float4 v) {
          ((uint32_t)(v.w != 0.0f) << 3);
 }
 
-// --------------------------------------------------------------------------- A pass
-// grid (ceil(K/1024), ceil(M/32)); thread t owns columns c = 1024*bx + 4t .. +3 and walks
-// 32 rows.  lanes 8q..8q+7 of a warp hold the 32 columns of one bitmap word.
-__global__ void __launch_bounds__(kK1Threads)
-k1_a_pass(const float* __restrict__ A, int64_t M, int64_t K, int64_t lda, uint32_t* __restrict__ abits,
-          int64_t kw, uint32_t* __restrict__ arow, uint32_t* __restrict__ acol) {
+// Zero-initialised per-plan scratch (one cudaMemsetAsync per preprocess):
+//   za = arow[M] | acol[K] | tile_sum[M/32];  zb = slice_nz (u64) | bpop[K] | bnz[K]
+struct K1Scratch {
+  uint32_t* arow;
+  uint32_t* acol;
+  uint32_t* tile_sum;     // [ceil(M/32)] non-zeros per 32-row tile (zeroed)
+  int64_t* tile_prefix;   // [ceil(M/32) + 1] exclusive prefix of tile_sum (written by the last CTA)
+  uint32_t* bpop;
+  uint32_t* bnz;
+  unsigned long long* slice_nz;
+  unsigned int* done;
+};
+
+// --------------------------------------------------------------------------- A tile
+// Tile (tx, ty): columns 1024*tx + 4t .. +3 for thread t, rows 32*ty .. +31.  Lanes
+// 8q..8q+7 of a warp hold the 32 columns of one bitmap word.  Rows are processed 8 at a
+// time so eight 16-byte loads per thread are in flight before the first shuffle.
+__device__ __forceinline__ void k1_a_tile(const float* __restrict__ A, int64_t M, int64_t K, int64_t lda,
+                                          uint32_t* __restrict__ abits, int64_t kw, const K1Scratch& z, int64_t tx,
+                                          int64_t ty) {
   const int lane = threadIdx.x & 31;
-  const int64_t c = (int64_t)blockIdx.x * kK1Cols + 4 * threadIdx.x;
-  const int64_t r0 = (int64_t)blockIdx.y * kK1Rows;
+  const int64_t c = tx * kK1Cols + 4 * threadIdx.x;
+  const int64_t r0 = ty * kK1Rows;
   const bool col_ok = c < K;
-  // valid-column mask of this thread's 4 columns (K need not be a multiple of 4)
   const uint32_t vmask = col_ok ? (K - c >= 4 ? 0xFu : ((1u << (K - c)) - 1u)) : 0u;
   uint32_t ccount[4] = {0, 0, 0, 0};
+  uint32_t warp_total = 0;
   const int64_t rend = min(r0 + kK1Rows, M);
-#pragma unroll 4
-  for (int64_t i = r0; i < rend; ++i) {
-    uint32_t nib = 0;
-    if (col_ok) nib = nz4(ldg_stream(A + i * lda + c)) & vmask;
+  for (int64_t rb = r0; rb < rend; rb += 8) {
+    float4 v[8];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) ccount[q] += (nib >> q) & 1u;
-    uint32_t word = nib << (4 * (lane & 7));
-    word |= __shfl_xor_sync(0xffffffffu, word, 1);
-    word |= __shfl_xor_sync(0xffffffffu, word, 2);
-    word |= __shfl_xor_sync(0xffffffffu, word, 4);
-    uint32_t cnt = __popc(nib);
-    cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
-    cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
-    cnt += __shfl_xor_sync(0xffffffffu, cnt, 4);
-    cnt += __shfl_xor_sync(0xffffffffu, cnt, 8);
-    cnt += __shfl_xor_sync(0xffffffffu, cnt, 16);
-    if ((lane & 7) == 0 && col_ok) abits[i * kw + (c >> 5)] = word;
-    if (lane == 0 && cnt) atomicAdd(&arow[i], cnt);
+    for (int u = 0; u < 8; ++u)
+      v[u] = (col_ok && rb + u < rend) ? ldg_stream(A + (rb + u) * lda + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = rb + u;
+      const uint32_t nib = nz4(v[u]) & vmask;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ccount[q] += (nib >> q) & 1u;
+      uint32_t word = nib << (4 * (lane & 7));
+      word |= __shfl_xor_sync(0xffffffffu, word, 1);
+      word |= __shfl_xor_sync(0xffffffffu, word, 2);
+      word |= __shfl_xor_sync(0xffffffffu, word, 4);
+      uint32_t cnt = __popc(word);  // per 32-column word; lanes 8q hold distinct words
+      cnt = (lane & 7) == 0 ? cnt : 0u;
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, 8);
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, 16);
+      if (i < rend) {
+        if ((lane & 7) == 0 && col_ok) abits[i * kw + (c >> 5)] = word;
+        if (lane == 0 && cnt) atomicAdd(&z.arow[i], cnt);
+        warp_total += cnt;
+      }
+    }
   }
+  if (lane == 0 && warp_total) atomicAdd(&z.tile_sum[ty], warp_total);
   if (col_ok) {
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      if (ccount[q]) atomicAdd(&acol[c + q], ccount[q]);
+      if (ccount[q]) atomicAdd(&z.acol[c + q], ccount[q]);
   }
 }
 
-// --------------------------------------------------------------------------- B pass
-// grid (ceil(ldb/1024), ceil(K/32)); thread t owns columns c = 1024*bx + 4t .. +3 of the
-// padded row (ldb is a multiple of 64, padding is zero) and walks the 32 rows of one
-// k-word.  Lane pairs form 8-column groups; 16 lanes form one 64-column region (code).
-__global__ void __launch_bounds__(kK1Threads)
-k1_b_pass(const float* __restrict__ B, int64_t K, int64_t ldb, uint8_t* __restrict__ codes, int64_t nreg,
-          uint32_t* __restrict__ bgrp, int64_t kw, uint32_t* __restrict__ bpop, uint32_t* __restrict__ bnz,
-          unsigned long long* __restrict__ slice_nz) {
+// --------------------------------------------------------------------------- B tile
+// Tile (tx, kw_idx): columns 1024*tx + 4t .. +3 of the padded row (ldb is a multiple of
+// 64, padding is zero) over the 32 rows of one k-word.  Lane pairs form 8-column groups;
+// 16 lanes form one 64-column region (code).
+__device__ __forceinline__ void k1_b_tile(const float* __restrict__ B, int64_t K, int64_t ldb,
+                                          uint8_t* __restrict__ codes, int64_t nreg, uint32_t* __restrict__ bgrp,
+                                          int64_t kw, const K1Scratch& z, int64_t tx, int64_t kw_idx) {
   const int lane = threadIdx.x & 31;
-  const int64_t c = (int64_t)blockIdx.x * kK1Cols + 4 * threadIdx.x;
-  const int64_t kw_idx = blockIdx.y;
+  const int64_t c = tx * kK1Cols + 4 * threadIdx.x;
   const int64_t k0 = kw_idx * 32;
   const bool col_ok = c < ldb;
-  uint32_t gword = 0;  // group k-bitmap word over the 32 rows
+  uint32_t gword = 0;   // group k-bitmap word over the 32 rows
   uint32_t slices = 0;  // (k, 16-column slice) pairs with a non-zero, counted by lane%4==0
   const int64_t kend = min(k0 + 32, K);
-#pragma unroll 4
-  for (int64_t k = k0; k < kend; ++k) {
-    uint32_t any = 0;
-    if (col_ok) any = nz4(ldg_stream(B + k * ldb + c)) != 0u;
-    any |= __shfl_xor_sync(0xffffffffu, any, 1);  // 8-column group
-    gword |= any << (uint32_t)(k - k0);
-    const uint32_t sibling = __shfl_xor_sync(0xffffffffu, any, 2);  // other group of the slice
-    if ((lane & 3) == 0 && col_ok) slices += any | sibling;
-    // region code: group j = (lane & 15) >> 1 -> bit 7 - j (MSB first)
-    uint32_t code = any << (7 - ((lane & 15) >> 1));
-    code |= __shfl_xor_sync(0xffffffffu, code, 2);
-    code |= __shfl_xor_sync(0xffffffffu, code, 4);
-    code |= __shfl_xor_sync(0xffffffffu, code, 8);
-    uint32_t pop = ((lane & 15) == 0 && col_ok) ? __popc(code) : 0u;
-    uint32_t nzc = ((lane & 15) == 0 && col_ok) ? (uint32_t)(code != 0) : 0u;
-    pop += __shfl_xor_sync(0xffffffffu, pop, 16);
-    nzc += __shfl_xor_sync(0xffffffffu, nzc, 16);
-    if ((lane & 15) == 0 && col_ok) codes[k * nreg + (c >> 6)] = (uint8_t)code;
-    if (lane == 0) {
-      if (pop) atomicAdd(&bpop[k], pop);
-      if (nzc) atomicAdd(&bnz[k], nzc);
+  for (int64_t kb = k0; kb < kend; kb += 8) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      v[u] = (col_ok && kb + u < kend) ? ldg_stream(B + (kb + u) * ldb + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t k = kb + u;
+      uint32_t any = nz4(v[u]) != 0u;
+      any |= __shfl_xor_sync(0xffffffffu, any, 1);  // 8-column group
+      gword |= any << (uint32_t)(k - k0);
+      const uint32_t sibling = __shfl_xor_sync(0xffffffffu, any, 2);  // other group of the slice
+      if ((lane & 3) == 0 && col_ok && k < kend) slices += any | sibling;
+      // region code: group j = (lane & 15) >> 1 -> bit 7 - j (MSB first)
+      uint32_t code = any << (7 - ((lane & 15) >> 1));
+      code |= __shfl_xor_sync(0xffffffffu, code, 2);
+      code |= __shfl_xor_sync(0xffffffffu, code, 4);
+      code |= __shfl_xor_sync(0xffffffffu, code, 8);
+      uint32_t pop = ((lane & 15) == 0 && col_ok) ? __popc(code) : 0u;
+      uint32_t nzc = ((lane & 15) == 0 && col_ok) ? (uint32_t)(code != 0) : 0u;
+      pop += __shfl_xor_sync(0xffffffffu, pop, 16);
+      nzc += __shfl_xor_sync(0xffffffffu, nzc, 16);
+      if (k < kend) {
+        if ((lane & 15) == 0 && col_ok) codes[k * nreg + (c >> 6)] = (uint8_t)code;
+        if (lane == 0) {
+          if (pop) atomicAdd(&z.bpop[k], pop);
+          if (nzc) atomicAdd(&z.bnz[k], nzc);
+        }
+      }
     }
   }
   if ((lane & 1) == 0 && col_ok) bgrp[(c >> 3) * kw + kw_idx] = gword;
 #pragma unroll
   for (int o = 16; o; o >>= 1) slices += __shfl_xor_sync(0xffffffffu, slices, o);
-  if (lane == 0 && slices) atomicAdd(slice_nz, (unsigned long long)slices);
+  if (lane == 0 && slices) atomicAdd(z.slice_nz, (unsigned long long)slices);
 }
 
-// ------------------------------------------------------------------ row_ptr (scan)
-// Single CTA exclusive scan of arow -> row_ptr[0..M]; M up to a few million rows.
-__global__ void __launch_bounds__(1024) k1_scan_rows(const uint32_t* __restrict__ arow, int64_t M,
-                                                     int64_t* __restrict__ row_ptr) {
-  __shared__ int64_t warp_sums[32];
-  __shared__ int64_t carry;
-  if (threadIdx.x == 0) carry = 0;
+__device__ void k1_finalize_block(const uint32_t* __restrict__ acol, const uint32_t* __restrict__ bpop,
+                                  const uint32_t* __restrict__ bnz, int64_t K, int64_t M, int64_t nreg, int has_a,
+                                  int has_b, const unsigned long long* __restrict__ slice_nz,
+                                  unsigned long long* __restrict__ out);
+
+// ------------------------------------------------------------------ fused K1 pass
+// One launch: CTAs [0, nA) are A tiles, [nA, nA + nB) are B tiles; the last CTA to finish
+// (threadfence + done-counter) computes the exact counters and plan statistics.
+__global__ void __launch_bounds__(kK1Threads, 4)
+k1_pass(const float* __restrict__ A, int64_t M, int64_t K, int64_t lda, uint32_t* __restrict__ abits,
+        int64_t a_tiles_x, int64_t nA, const float* __restrict__ B, int64_t ldb, uint8_t* __restrict__ codes,
+        int64_t nreg, uint32_t* __restrict__ bgrp, int64_t b_tiles_x, int64_t nB, int64_t kw, K1Scratch z,
+        int has_a, int has_b, unsigned long long* __restrict__ stats) {
+  const int64_t bid = blockIdx.x;
+  if (bid < nA)
+    k1_a_tile(A, M, K, lda, abits, kw, z, bid % a_tiles_x, bid / a_tiles_x);
+  else
+    k1_b_tile(B, K, ldb, codes, nreg, bgrp, kw, z, (bid - nA) % b_tiles_x, (bid - nA) / b_tiles_x);
+  __shared__ unsigned int last;
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int64_t base = 0; base < M; base += 1024) {
-    const int64_t i = base + threadIdx.x;
-    int64_t v = i < M ? (int64_t)arow[i] : 0;
-    int64_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) warp_sums[warp] = x;
+  if (threadIdx.x == 0) {
+    __threadfence();  // cumulative over the CTA's writes ordered by the barrier above
+    last = atomicAdd(z.done, 1u) == (unsigned int)(nA + nB - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x == 0) *z.done = 0u;  // ready for the next launch (no other CTA is left)
+  k1_finalize_block(z.acol, z.bpop, z.bnz, K, M, nreg, has_a, has_b, z.slice_nz, stats);
+  if (nA > 0) {  // exclusive prefix of the 32-row tile sums for k1_csr's row_ptr
+    __shared__ int64_t carry;
+    __shared__ int64_t wsum[kK1Threads / 32];
+    if (threadIdx.x == 0) carry = 0;
     __syncthreads();
-    if (warp == 0) {
-      int64_t s = warp_sums[lane];
+    const int64_t ntile = (M + kK1Rows - 1) / kK1Rows;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t base = 0; base < ntile; base += kK1Threads) {
+      const int64_t t = base + threadIdx.x;
+      const int64_t v = t < ntile ? (int64_t)z.tile_sum[t] : 0;
+      int64_t x = v;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        int64_t y = __shfl_up_sync(0xffffffffu, s, o);
-        if (lane >= o) s += y;
+        const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
       }
-      warp_sums[lane] = s;  // inclusive over warps
+      if (lane == 31) wsum[warp] = x;
+      __syncthreads();
+      int64_t before = carry;
+      for (int w = 0; w < warp; ++w) before += wsum[w];
+      if (t < ntile) z.tile_prefix[t] = before + x - v;
+      __syncthreads();
+      if (threadIdx.x == kK1Threads - 1) carry = before + x;
+      __syncthreads();
     }
-    __syncthreads();
-    const int64_t before = carry + (warp ? warp_sums[warp - 1] : 0) + x - v;
-    if (i < M) row_ptr[i] = before;
-    __syncthreads();
-    if (threadIdx.x == 1023) carry = before + v;
-    __syncthreads();
+    if (threadIdx.x == 0) z.tile_prefix[ntile] = carry;
   }
-  if (threadIdx.x == 0) row_ptr[M] = carry;
 }
 
 // --------------------------------------------------------------- CSR index lists
-// One warp per row: popc of each bitmap word, warp prefix sum, then each lane expands its
-// word's set bits into ascending column indices.  Reads only the bitmap (no second pass
-// over A).  Index type: uint16 when K <= 65536, else uint32.
+// Per-row ascending index lists (CSR) from the bitmap, no second pass over A.  A CTA owns
+// 8 rows (one per warp).  row_ptr comes from the 32-row tile prefix the K1 pass's last CTA
+// scanned, plus at most 31 row counts: no separate scan launch.  Each warp then expands its
+// row: popc per bitmap word, warp prefix sum, each lane writes its word's set bits.  Index
+// type: uint16 when K <= 65536, else uint32.
+constexpr int kCsrRows = 8;
+
 template <typename Idx>
-__global__ void __launch_bounds__(256) k1_csr(const uint32_t* __restrict__ abits, int64_t M, int64_t kw,
-                                              const int64_t* __restrict__ row_ptr, Idx* __restrict__ cols) {
-  const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+__global__ void __launch_bounds__(256) k1_csr(const uint32_t* __restrict__ abits, const uint32_t* __restrict__ arow,
+                                              const int64_t* __restrict__ tile_prefix, int64_t M, int64_t kw,
+                                              int64_t* __restrict__ row_ptr, Idx* __restrict__ cols) {
+  __shared__ int64_t s_off[kCsrRows + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r0 = (int64_t)blockIdx.x * kCsrRows;
+  if (warp == 0) {
+    const int64_t t0 = (r0 / 32) * 32;  // first row of r0's 32-row tile
+    // counts of rows [t0, r0) (lanes 0..r0-t0-1) and of this CTA's rows (lanes 24..31 -> rows r0..r0+7)
+    const int64_t i_pre = t0 + lane;
+    uint32_t pre = (i_pre < r0) ? arow[i_pre] : 0u;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+    const int64_t i_own = r0 + (lane & 7);
+    const uint32_t own = (lane < 8 && i_own < M) ? arow[i_own] : 0u;
+    uint32_t x = own;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if ((lane & 7) >= o) x += y;
+    }
+    const int64_t base = tile_prefix[r0 / 32] + (int64_t)pre;
+    if (lane < 8) s_off[lane] = base + (int64_t)(x - own);
+    if (lane == 7) s_off[8] = base + (int64_t)x;
+  }
+  __syncthreads();
+  const int64_t row = r0 + warp;
+  if (threadIdx.x < kCsrRows && r0 + threadIdx.x < M) row_ptr[r0 + threadIdx.x] = s_off[threadIdx.x];
+  if (threadIdx.x == 0 && r0 + kCsrRows >= M) row_ptr[M] = s_off[M - r0];
   if (row >= M) return;
-  int64_t out = row_ptr[row];
+  int64_t out = s_off[warp];
   const uint32_t* bits = abits + row * kw;
   for (int64_t w0 = 0; w0 < kw; w0 += 32) {
     const int64_t w = w0 + lane;
     uint32_t word = w < kw ? bits[w] : 0u;
-    uint32_t n = __popc(word);
+    const uint32_t n = __popc(word);
     uint32_t x = n;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
       if (lane >= o) x += y;
     }
     int64_t pos = out + x - n;
@@ -208,11 +284,11 @@ __global__ void __launch_bounds__(256) k1_csr(const uint32_t* __restrict__ abits
 //   span: K2-SIMT mask granularity, from the cost model of DESIGN.md (K2 variants):
 //   16-column slices cost ~41 issue slots per non-zero (k, slice), 8-column groups ~23 per
 //   non-zero (k, group); pick the cheaper (slice_nz[0] = # non-zero (k, slice) pairs).
-__global__ void __launch_bounds__(1024) k1_finalize(const uint32_t* __restrict__ acol, const uint32_t* __restrict__ bpop,
+__device__ void k1_finalize_block(const uint32_t* __restrict__ acol, const uint32_t* __restrict__ bpop,
                                                     const uint32_t* __restrict__ bnz, int64_t K, int64_t M,
-                                                    int64_t nreg, int has_a, int has_b,
-                                                    const unsigned long long* __restrict__ slice_nz,
-                                                    unsigned long long* __restrict__ out) {
+                                  int64_t nreg, int has_a, int has_b,
+                                  const unsigned long long* __restrict__ slice_nz,
+                                  unsigned long long* __restrict__ out) {
   unsigned long long s[6] = {0, 0, 0, 0, 0, 0};
   for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
     const unsigned long long a = has_a ? acol[k] : 0ull;
@@ -252,6 +328,14 @@ __global__ void __launch_bounds__(1024) k1_finalize(const uint32_t* __restrict__
     out[6] = red[0][5];
     out[7] = (has_b && 41ull * slice_nz[0] > 23ull * red[0][4]) ? 8ull : 16ull;
   }
+}
+
+__global__ void __launch_bounds__(1024) k1_finalize(const uint32_t* __restrict__ acol, const uint32_t* __restrict__ bpop,
+                                                    const uint32_t* __restrict__ bnz, int64_t K, int64_t M,
+                                                    int64_t nreg, int has_a, int has_b,
+                                                    const unsigned long long* __restrict__ slice_nz,
+                                                    unsigned long long* __restrict__ out) {
+  k1_finalize_block(acol, bpop, bnz, K, M, nreg, has_a, has_b, slice_nz, out);
 }
 
 // ------------------------------------------------------------ ABlockIndex export

@@ -152,18 +152,22 @@ k2_simt_bcast(const float* __restrict__ A, int64_t lda, const float* __restrict_
     }
   };
 
-  uint64_t mask_cur[NS], mask_nxt[NS];
+  // Slice masks are loaded two chunks ahead (registers) so that the B fetch of chunk c+1,
+  // issued at the top of iteration c, never waits on a fresh global load.
+  uint64_t mask_cur[NS], mask_nxt[NS], mask_nn[NS];
   auto masks_for = [&](int64_t c, uint64_t* out) {
 #pragma unroll
     for (int s = 0; s < NS; ++s)
-      out[s] = slice_ok ? slice_mask(bgrp, kw, g0 + s * (SPAN / 8), 2 * c, SPAN / 8) : 0ull;
+      out[s] = (slice_ok && c < nchunks) ? slice_mask(bgrp, kw, g0 + s * (SPAN / 8), 2 * c, SPAN / 8) : 0ull;
   };
+  auto bmask = [&](const uint64_t* m) { return NS == 1 ? m[0] : (m[0] | m[NS - 1]); };
 
-  // ---- prologue: chunk 0
+  // ---- prologue: chunk 0 staged, chunk 1 masks in flight
   masks_for(0, mask_cur);
+  masks_for(1, mask_nxt);
   load_a(0);
   store_a(sA(0));
-  load_b(0, sB(0), NS == 1 ? mask_cur[0] : (mask_cur[0] | mask_cur[NS - 1]));
+  load_b(0, sB(0), bmask(mask_cur));
   cp_async_commit();
   cp_async_wait_all();
   __syncthreads();
@@ -172,11 +176,11 @@ k2_simt_bcast(const float* __restrict__ A, int64_t lda, const float* __restrict_
     const int st = (int)(c & 1);
     const bool more = c + 1 < nchunks;
     if (more) {
-      masks_for(c + 1, mask_nxt);
       load_a(c + 1);
-      load_b(c + 1, sB(st ^ 1), NS == 1 ? mask_nxt[0] : (mask_nxt[0] | mask_nxt[NS - 1]));
+      load_b(c + 1, sB(st ^ 1), bmask(mask_nxt));
       cp_async_commit();
     }
+    masks_for(c + 2, mask_nn);
     // ---- compute chunk c: warp-uniform walk over the slice's non-zero B rows
     const float* at = sA(st);
     const float* bs = sB(st) + 16 * warp;
@@ -205,10 +209,11 @@ k2_simt_bcast(const float* __restrict__ A, int64_t lda, const float* __restrict_
         }
       }
     }
-    if (more) {
-      store_a(sA(st ^ 1));
+    if (more) store_a(sA(st ^ 1));
 #pragma unroll
-      for (int s = 0; s < NS; ++s) mask_cur[s] = mask_nxt[s];
+    for (int s = 0; s < NS; ++s) {
+      mask_cur[s] = mask_nxt[s];
+      mask_nxt[s] = mask_nn[s];
     }
     cp_async_wait_all();
     __syncthreads();

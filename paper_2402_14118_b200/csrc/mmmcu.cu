@@ -62,14 +62,15 @@ struct mmmcu_ctx {
   int64_t M = 0, Ka = 0, lda = 0;
   uint64_t av = 0;
   int csr_idx_bytes = 4;
-  DevBuf abits, arow, acol, row_ptr, cols;
+  DevBuf abits, za, tile_prefix, row_ptr, cols;
 
   // ---- B plan (preprocess_b)
   bool has_b = false;
   const float* B = nullptr;
   int64_t Kb = 0, N = 0, ldb = 0;
   uint64_t bv = 0;
-  DevBuf codes, bgrp, bpop, bnz;
+  DevBuf codes, bgrp, zb;
+  DevBuf ctl;
 
   // ---- statistics: u64 [16] = {inv, lanes, skipped, zreg, nnzA, pop, zero_codes, span, slice_nz}
   DevBuf stats;
@@ -132,19 +133,17 @@ mmmcu_status check_lane(mmmcu_ctx* ctx, mmmcu_lane lane) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-mmmcu_status run_finalize(mmmcu_ctx* ctx) {
-  const int64_t K = ctx->has_a ? ctx->Ka : ctx->Kb;
-  if (ctx->has_a && ctx->has_b && ctx->Ka != ctx->Kb) return MMMCU_OK;  // mismatched: multiply rejects
-  const int64_t nreg = ctx->has_b ? ctx->ldb / 64 : 0;
-  mmmcu::k1_finalize<<<1, 1024, 0, ctx->stream>>>(
-      ctx->has_a ? ctx->acol.as<uint32_t>() : nullptr, ctx->has_b ? ctx->bpop.as<uint32_t>() : nullptr,
-      ctx->has_b ? ctx->bnz.as<uint32_t>() : nullptr, K, ctx->has_a ? ctx->M : 0, nreg, ctx->has_a ? 1 : 0,
-      ctx->has_b ? 1 : 0, ctx->stats.as<unsigned long long>() + 8, ctx->stats.as<unsigned long long>());
-  MMMCU_LAUNCHED();
-  return MMMCU_OK;
-}
+// Zeroed scratch of the fused K1 launch: za = [arow M | acol K], zb = [slice_nz u64 |
+// bpop K | bnz K]; ctl = the last-block counter, which the last block resets itself.
+uint32_t* za_arow(mmmcu_ctx* ctx) { return ctx->za.as<uint32_t>(); }
+uint32_t* za_acol(mmmcu_ctx* ctx) { return ctx->za.as<uint32_t>() + ctx->M; }
+uint32_t* za_tiles(mmmcu_ctx* ctx) { return ctx->za.as<uint32_t>() + ctx->M + ctx->Ka; }
+int64_t n_row_tiles(int64_t M) { return (M + mmmcu::kK1Rows - 1) / mmmcu::kK1Rows; }
+unsigned long long* zb_slice(mmmcu_ctx* ctx) { return ctx->zb.as<unsigned long long>(); }
+uint32_t* zb_bpop(mmmcu_ctx* ctx) { return reinterpret_cast<uint32_t*>(ctx->zb.as<unsigned long long>() + 1); }
+uint32_t* zb_bnz(mmmcu_ctx* ctx) { return zb_bpop(ctx) + ctx->Kb; }
 
-mmmcu_status do_preprocess_a(mmmcu_ctx* ctx, const float* A, int64_t M, int64_t K, int64_t lda, uint64_t av) {
+mmmcu_status stage_a(mmmcu_ctx* ctx, const float* A, int64_t M, int64_t K, int64_t lda, uint64_t av) {
   if (M <= 0 || K <= 0) return fail(ctx, MMMCU_ERR_INVALID_ARG, "matrix dimensions must be positive");
   if (!A) return fail(ctx, MMMCU_ERR_INVALID_ARG, "A is null");
   if (lda < K || lda % 4 != 0 || !aligned16(A))
@@ -153,34 +152,11 @@ mmmcu_status do_preprocess_a(mmmcu_ctx* ctx, const float* A, int64_t M, int64_t 
   ctx->has_a = false;
   ctx->csr_idx_bytes = K <= 65536 ? 2 : 4;
   MMMCU_CUDA(ctx->abits.ensure(sizeof(uint32_t) * M * kw));
-  MMMCU_CUDA(ctx->arow.ensure(sizeof(uint32_t) * M));
-  MMMCU_CUDA(ctx->acol.ensure(sizeof(uint32_t) * K));
+  MMMCU_CUDA(ctx->za.ensure(sizeof(uint32_t) * (M + K + n_row_tiles(M))));
+  MMMCU_CUDA(ctx->tile_prefix.ensure(sizeof(int64_t) * (n_row_tiles(M) + 1)));
   MMMCU_CUDA(ctx->row_ptr.ensure(sizeof(int64_t) * (M + 1)));
   MMMCU_CUDA(ctx->cols.ensure((size_t)ctx->csr_idx_bytes * M * K));
-  MMMCU_CUDA(ctx->stats.ensure(sizeof(unsigned long long) * 16));
-  MMMCU_CUDA(cudaMemsetAsync(ctx->arow.p, 0, sizeof(uint32_t) * M, ctx->stream));
-  MMMCU_CUDA(cudaMemsetAsync(ctx->acol.p, 0, sizeof(uint32_t) * K, ctx->stream));
-  // grid.y is limited to 65535 row tiles per launch: slice very tall operands
-  const int64_t rows_per_launch = (int64_t)65535 * mmmcu::kK1Rows;
-  for (int64_t r0 = 0; r0 < M; r0 += rows_per_launch) {
-    const int64_t mr = std::min(rows_per_launch, M - r0);
-    dim3 grid((unsigned)((K + mmmcu::kK1Cols - 1) / mmmcu::kK1Cols), (unsigned)((mr + mmmcu::kK1Rows - 1) / mmmcu::kK1Rows));
-    mmmcu::k1_a_pass<<<grid, mmmcu::kK1Threads, 0, ctx->stream>>>(A + r0 * lda, mr, K, lda,
-                                                                    ctx->abits.as<uint32_t>() + r0 * kw, kw,
-                                                                    ctx->arow.as<uint32_t>() + r0, ctx->acol.as<uint32_t>());
-    MMMCU_LAUNCHED();
-  }
-  mmmcu::k1_scan_rows<<<1, 1024, 0, ctx->stream>>>(ctx->arow.as<uint32_t>(), M, ctx->row_ptr.as<int64_t>());
-  MMMCU_LAUNCHED();
-  const unsigned csr_blocks = (unsigned)((M + 7) / 8);
-  if (ctx->csr_idx_bytes == 2)
-    mmmcu::k1_csr<uint16_t><<<csr_blocks, 256, 0, ctx->stream>>>(ctx->abits.as<uint32_t>(), M, kw,
-                                                                 ctx->row_ptr.as<int64_t>(), ctx->cols.as<uint16_t>());
-  else
-    mmmcu::k1_csr<uint32_t><<<csr_blocks, 256, 0, ctx->stream>>>(ctx->abits.as<uint32_t>(), M, kw,
-                                                                 ctx->row_ptr.as<int64_t>(), ctx->cols.as<uint32_t>());
-  MMMCU_LAUNCHED();
-  ctx->has_a = true;
+  MMMCU_CUDA(cudaMemsetAsync(ctx->za.p, 0, sizeof(uint32_t) * (M + K + n_row_tiles(M)), ctx->stream));
   ctx->A = A;
   ctx->M = M;
   ctx->Ka = K;
@@ -189,35 +165,74 @@ mmmcu_status do_preprocess_a(mmmcu_ctx* ctx, const float* A, int64_t M, int64_t 
   return MMMCU_OK;
 }
 
-mmmcu_status do_preprocess_b(mmmcu_ctx* ctx, const float* B, int64_t K, int64_t N, int64_t ldb, uint64_t bv) {
+mmmcu_status stage_b(mmmcu_ctx* ctx, const float* B, int64_t K, int64_t N, int64_t ldb, uint64_t bv) {
   if (K <= 0 || N <= 0) return fail(ctx, MMMCU_ERR_INVALID_ARG, "matrix dimensions must be positive");
   if (!B) return fail(ctx, MMMCU_ERR_INVALID_ARG, "B is null");
   if (ldb < N || ldb % 64 != 0 || !aligned16(B))
     return fail(ctx, MMMCU_ERR_INVALID_ARG,
                 "B must be 16-byte aligned with ldb >= N and ldb a multiple of the region width 64");
   const int64_t kw = (K + 31) / 32;
-  if (kw > 65535) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "K larger than 2097120 is not supported");
   const int64_t nreg = ldb / 64, ngrp = ldb / 8;
   ctx->has_b = false;
   MMMCU_CUDA(ctx->codes.ensure((size_t)K * nreg));
   MMMCU_CUDA(ctx->bgrp.ensure(sizeof(uint32_t) * ngrp * kw));
-  MMMCU_CUDA(ctx->bpop.ensure(sizeof(uint32_t) * K));
-  MMMCU_CUDA(ctx->bnz.ensure(sizeof(uint32_t) * K));
-  MMMCU_CUDA(ctx->stats.ensure(sizeof(unsigned long long) * 16));
-  MMMCU_CUDA(cudaMemsetAsync(ctx->bpop.p, 0, sizeof(uint32_t) * K, ctx->stream));
-  MMMCU_CUDA(cudaMemsetAsync(ctx->bnz.p, 0, sizeof(uint32_t) * K, ctx->stream));
-  MMMCU_CUDA(cudaMemsetAsync(ctx->stats.as<unsigned long long>() + 8, 0, sizeof(unsigned long long), ctx->stream));
-  dim3 grid((unsigned)((ldb + mmmcu::kK1Cols - 1) / mmmcu::kK1Cols), (unsigned)kw);
-  mmmcu::k1_b_pass<<<grid, mmmcu::kK1Threads, 0, ctx->stream>>>(
-      B, K, ldb, ctx->codes.as<uint8_t>(), nreg, ctx->bgrp.as<uint32_t>(), kw, ctx->bpop.as<uint32_t>(),
-      ctx->bnz.as<uint32_t>(), ctx->stats.as<unsigned long long>() + 8);
-  MMMCU_LAUNCHED();
-  ctx->has_b = true;
+  MMMCU_CUDA(ctx->zb.ensure(sizeof(unsigned long long) + sizeof(uint32_t) * 2 * K));
+  MMMCU_CUDA(cudaMemsetAsync(ctx->zb.p, 0, sizeof(unsigned long long) + sizeof(uint32_t) * 2 * K, ctx->stream));
   ctx->B = B;
   ctx->Kb = K;
   ctx->N = N;
   ctx->ldb = ldb;
   ctx->bv = bv;
+  return MMMCU_OK;
+}
+
+// One fused K1 launch over the staged operand(s), then (for A) the CSR index lists.
+mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
+  MMMCU_CUDA(ctx->stats.ensure(sizeof(unsigned long long) * 16));
+  if (ctx->ctl.cap == 0) {
+    MMMCU_CUDA(ctx->ctl.ensure(256));
+    MMMCU_CUDA(cudaMemsetAsync(ctx->ctl.p, 0, 256, ctx->stream));
+  }
+  const bool a_valid = do_a || ctx->has_a;
+  const bool b_valid = do_b || ctx->has_b;
+  const bool same_k = a_valid && b_valid && ctx->Ka == ctx->Kb;
+  const int64_t K = do_a ? ctx->Ka : ctx->Kb;
+  const int64_t kw = (K + 31) / 32;
+  const int64_t a_tx = (ctx->Ka + mmmcu::kK1Cols - 1) / mmmcu::kK1Cols;
+  const int64_t nA = do_a ? a_tx * ((ctx->M + mmmcu::kK1Rows - 1) / mmmcu::kK1Rows) : 0;
+  const int64_t b_tx = (ctx->ldb + mmmcu::kK1Cols - 1) / mmmcu::kK1Cols;
+  const int64_t nB = do_b ? b_tx * ((ctx->Kb + 31) / 32) : 0;
+  if (nA + nB > 0x7fffffff) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "operand too large for one K1 launch");
+  mmmcu::K1Scratch z;
+  z.arow = a_valid ? za_arow(ctx) : nullptr;
+  z.acol = a_valid ? za_acol(ctx) : nullptr;
+  z.tile_sum = do_a ? za_tiles(ctx) : nullptr;
+  z.tile_prefix = do_a ? ctx->tile_prefix.as<int64_t>() : nullptr;
+  z.bpop = b_valid ? zb_bpop(ctx) : nullptr;
+  z.bnz = b_valid ? zb_bnz(ctx) : nullptr;
+  z.slice_nz = b_valid ? zb_slice(ctx) : ctx->stats.as<unsigned long long>() + 15;
+  z.done = ctx->ctl.as<unsigned int>();
+  const int has_a = a_valid && (same_k || !b_valid) ? 1 : 0;
+  const int has_b = b_valid && (same_k || !a_valid) ? 1 : 0;
+  mmmcu::k1_pass<<<(unsigned)(nA + nB), mmmcu::kK1Threads, 0, ctx->stream>>>(
+      ctx->A, ctx->M, K, ctx->lda, ctx->abits.as<uint32_t>(), a_tx, nA, ctx->B, ctx->ldb, ctx->codes.as<uint8_t>(),
+      ctx->ldb / 64, ctx->bgrp.as<uint32_t>(), b_tx, nB, kw, z, has_a, has_b, ctx->stats.as<unsigned long long>());
+  MMMCU_LAUNCHED();
+  if (do_a) {
+    const unsigned blocks = (unsigned)((ctx->M + mmmcu::kCsrRows - 1) / mmmcu::kCsrRows);
+    const int64_t akw = (ctx->Ka + 31) / 32;
+    if (ctx->csr_idx_bytes == 2)
+      mmmcu::k1_csr<uint16_t><<<blocks, 256, 0, ctx->stream>>>(ctx->abits.as<uint32_t>(), za_arow(ctx),
+                                                               ctx->tile_prefix.as<int64_t>(), ctx->M, akw,
+                                                               ctx->row_ptr.as<int64_t>(), ctx->cols.as<uint16_t>());
+    else
+      mmmcu::k1_csr<uint32_t><<<blocks, 256, 0, ctx->stream>>>(ctx->abits.as<uint32_t>(), za_arow(ctx),
+                                                               ctx->tile_prefix.as<int64_t>(), ctx->M, akw,
+                                                               ctx->row_ptr.as<int64_t>(), ctx->cols.as<uint32_t>());
+    MMMCU_LAUNCHED();
+  }
+  if (do_a) ctx->has_a = true;
+  if (do_b) ctx->has_b = true;
   return MMMCU_OK;
 }
 
@@ -304,8 +319,8 @@ mmmcu_status mmmcu_ctx_destroy(mmmcu_ctx* ctx) {
   if (!ctx) return MMMCU_OK;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-  for (DevBuf* b : {&ctx->abits, &ctx->arow, &ctx->acol, &ctx->row_ptr, &ctx->cols, &ctx->codes, &ctx->bgrp,
-                    &ctx->bpop, &ctx->bnz, &ctx->stats, &ctx->hA, &ctx->hB, &ctx->hC, &ctx->scratch0, &ctx->scratch1})
+  for (DevBuf* b : {&ctx->abits, &ctx->za, &ctx->tile_prefix, &ctx->row_ptr, &ctx->cols, &ctx->codes, &ctx->bgrp, &ctx->zb,
+                    &ctx->ctl, &ctx->stats, &ctx->hA, &ctx->hB, &ctx->hC, &ctx->scratch0, &ctx->scratch1})
     b->release();
   delete ctx;
   return MMMCU_OK;
@@ -321,25 +336,25 @@ mmmcu_status mmmcu_validate_lane(mmmcu_ctx* ctx, mmmcu_lane lane) { return check
 
 mmmcu_status mmmcu_preprocess_a(mmmcu_ctx* ctx, const float* A, int64_t M, int64_t K, int64_t lda, uint64_t av) {
   MMMCU_TRY(bind(ctx));
-  MMMCU_TRY(do_preprocess_a(ctx, A, M, K, lda, av));
-  return run_finalize(ctx);
+  MMMCU_TRY(stage_a(ctx, A, M, K, lda, av));
+  return launch_k1(ctx, true, false);
 }
 
 mmmcu_status mmmcu_preprocess_b(mmmcu_ctx* ctx, const float* B, int64_t K, int64_t N, int64_t ldb, mmmcu_lane lane,
                                 uint64_t bv) {
   MMMCU_TRY(bind(ctx));
   MMMCU_TRY(check_lane(ctx, lane));
-  MMMCU_TRY(do_preprocess_b(ctx, B, K, N, ldb, bv));
-  return run_finalize(ctx);
+  MMMCU_TRY(stage_b(ctx, B, K, N, ldb, bv));
+  return launch_k1(ctx, false, true);
 }
 
 mmmcu_status mmmcu_preprocess(mmmcu_ctx* ctx, const float* A, int64_t M, int64_t K, int64_t lda, const float* B,
                               int64_t N, int64_t ldb, mmmcu_lane lane, uint64_t av, uint64_t bv) {
   MMMCU_TRY(bind(ctx));
   MMMCU_TRY(check_lane(ctx, lane));
-  MMMCU_TRY(do_preprocess_a(ctx, A, M, K, lda, av));
-  MMMCU_TRY(do_preprocess_b(ctx, B, K, N, ldb, bv));
-  return run_finalize(ctx);
+  MMMCU_TRY(stage_a(ctx, A, M, K, lda, av));
+  MMMCU_TRY(stage_b(ctx, B, K, N, ldb, bv));
+  return launch_k1(ctx, true, true);
 }
 
 mmmcu_status mmmcu_get_counters(mmmcu_ctx* ctx, mmmcu_counters* out) {
@@ -535,16 +550,16 @@ mmmcu_status mmmcu_multiply_host(mmmcu_ctx* ctx, float* C_host, int64_t ldc, con
   return fill_counters(ctx, counters);
 }
 
-mmmcu_status mmmcu_generate(mmmcu_ctx* ctx, float* out, int64_t rows, int64_t cols, int64_t ld, uint64_t seed,
+mmmcu_status mmmcu_generate(mmmcu_ctx* ctx, float* out, int64_t rows, int64_t cols, int64_t ld, int64_t row0, uint64_t seed,
                             int value_kind, double sigma, double thresh, int mask_kind, double p, int64_t block) {
   MMMCU_TRY(bind(ctx));
-  if (rows <= 0 || cols <= 0 || ld < cols || !out) return fail(ctx, MMMCU_ERR_INVALID_ARG, "bad generator shape");
+  if (rows <= 0 || cols <= 0 || ld < cols || row0 < 0 || !out) return fail(ctx, MMMCU_ERR_INVALID_ARG, "bad generator shape");
   if (value_kind < 0 || value_kind > 2 || mask_kind < 0 || mask_kind > 2 || (mask_kind == 2 && block <= 0) ||
       !(p >= 0.0 && p <= 1.0))
     return fail(ctx, MMMCU_ERR_INVALID_ARG, "bad generator spec");
   const int64_t total = rows * ld;
   const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 64);
-  mmmcu::k_generate<<<blocks, 256, 0, ctx->stream>>>(out, rows, cols, ld, seed, value_kind, sigma, thresh, mask_kind, p,
+  mmmcu::k_generate<<<blocks, 256, 0, ctx->stream>>>(out, rows, cols, ld, row0, seed, value_kind, sigma, thresh, mask_kind, p,
                                                      block);
   MMMCU_LAUNCHED();
   return MMMCU_OK;
