@@ -75,7 +75,9 @@ typedef enum {
                                 mask granularity (8 or 16 columns) chosen on the device   */
   MMMCU_ALGO_DENSE = 2,      /* multiply_simple (dense i-k-j fma)            */
   MMMCU_ALGO_SIMT_SPAN8 = 3, /* K2-SIMT forced to 8-column (group) masks                  */
-  MMMCU_ALGO_SIMT_SPAN16 = 4 /* K2-SIMT forced to 16-column slice masks                   */
+  MMMCU_ALGO_SIMT_SPAN16 = 4,/* K2-SIMT forced to 16-column slice masks                   */
+  MMMCU_ALGO_TC = 5          /* K2-TC: tcgen05 3xTF32 over k-compacted 16-column slices;
+                                tolerance-matched (|dC| <= 1e-5 * sum|a||b|), not bit-exact */
 } mmmcu_algo;
 
 /* ---- context --------------------------------------------------------------------- */

@@ -30,6 +30,7 @@ ALGO_SIMT_BCAST = 1
 ALGO_DENSE = 2
 ALGO_SIMT_SPAN8 = 3
 ALGO_SIMT_SPAN16 = 4
+ALGO_TC = 5
 
 
 class Lane(ctypes.Structure):

@@ -16,6 +16,7 @@
 #include "gen.cuh"
 #include "k1_preprocess.cuh"
 #include "k2_simt.cuh"
+#include "k2_tc.cuh"
 
 namespace {
 
@@ -474,7 +475,7 @@ mmmcu_status mmmcu_export_ablock_index(mmmcu_ctx* ctx, int64_t block_dim, uint8_
 
 mmmcu_status mmmcu_set_algo(mmmcu_ctx* ctx, mmmcu_algo algo) {
   MMMCU_TRY(bind(ctx));
-  if (algo < MMMCU_ALGO_AUTO || algo > MMMCU_ALGO_SIMT_SPAN16)
+  if (algo < MMMCU_ALGO_AUTO || algo > MMMCU_ALGO_TC)
     return fail(ctx, MMMCU_ERR_INVALID_ARG, "unknown algorithm");
   ctx->algo = algo;
   return MMMCU_OK;
@@ -494,7 +495,17 @@ mmmcu_status mmmcu_multiply(mmmcu_ctx* ctx, float* C, int64_t ldc, const float* 
   if (ldc < round_up(ctx->N, 64) || ldc % 4 != 0 || !aligned16(C))
     return fail(ctx, MMMCU_ERR_INVALID_ARG,
                 "C must be 16-byte aligned with ldc >= round_up(N, 64) (Matrix padding) and ldc % 4 == 0");
-  if (ctx->algo == MMMCU_ALGO_DENSE) {
+  if (ctx->algo == MMMCU_ALGO_TC) {
+    ctx->last_algo = MMMCU_ALGO_TC;
+    const int64_t Np = round_up(ctx->N, 64), kw = (ctx->Ka + 31) / 32;
+    const int64_t row_tiles = (ctx->M + mmmcu::kTcTM - 1) / mmmcu::kTcTM;
+    if (row_tiles > 65535) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "M too large for the TC grid");
+    MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, mmmcu::kTcSmem));
+    dim3 grid((unsigned)((Np + mmmcu::kTcTN - 1) / mmmcu::kTcTN), (unsigned)row_tiles);
+    mmmcu::k2_tc<<<grid, mmmcu::kTcThreads, mmmcu::kTcSmem, ctx->stream>>>(
+        ctx->A, ctx->lda, ctx->B, ctx->ldb, C, ldc, ctx->M, ctx->Ka, Np, ctx->bgrp.as<uint32_t>(), kw);
+    MMMCU_LAUNCHED();
+  } else if (ctx->algo == MMMCU_ALGO_DENSE) {
     ctx->last_algo = MMMCU_ALGO_DENSE;
     dim3 grid((unsigned)((ctx->N + 63) / 64), (unsigned)((ctx->M + 63) / 64));
     mmmcu::k2_dense<<<grid, 256, 0, ctx->stream>>>(ctx->A, ctx->lda, ctx->B, ctx->ldb, C, ldc, ctx->M, ctx->Ka, ctx->N);

@@ -296,3 +296,22 @@ def test_device_generator_matches_oracle(ctx):
     g = t.cpu().numpy()
     assert ((g == 0) == (host == 0)).mean() > 0.9999
     assert np.allclose(g, host, rtol=1e-6, atol=1e-7)
+
+
+# --------------------------------------------------------------- K2-TC (tcgen05 3xTF32)
+@pytest.mark.parametrize("M,K,N_,zA,zB,bw", [(1024, 1024, 1024, 0.8, 0.8, 16), (100, 77, 130, 0.6, 0.6, 8),
+                                            (257, 1000, 600, 0.0, 0.0, 16), (4096, 4096, 4096, 0.6, 0.6, 32),
+                                            (4096, 4096, 4096, 0.95, 0.95, 8), (129, 65, 257, 1.0, 0.5, 16)])
+def test_tc_tolerance(ctx, M, K, N_, zA, zB, bw):
+    # north_star: |C_gpu - C_ref| <= 1e-5 * Σ_k |a_ik||b_kj| (fp64 denominator); exact counters
+    A, B = gen_pair(21, M, K, N_, zA, zB, bw)
+    rng = np.random.default_rng(K)
+    C0 = np.zeros((M, B.shape[1]), np.float32)
+    C0[:, :N_] = rng.uniform(-1, 1, (M, N_)).astype(np.float32)
+    C, cnt = run_gpu(ctx, A, B, C0=C0, algo=N.ALGO_TC, N_=N_)
+    Cr, ocnt = run_oracle(A, B, C0=C0)
+    bad, worst = o.check_tolerance(C, Cr, np.ascontiguousarray(A[:, :K]), B, tol=TOL)
+    assert bad == 0, worst
+    assert worst < 0.5 * TOL  # margin: typical worst ~4e-6 at dA = dB = 0.4
+    assert (C[:, N_:] == 0).all()
+    assert_counters(cnt, ocnt)
