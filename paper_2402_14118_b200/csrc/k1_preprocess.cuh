@@ -52,6 +52,13 @@ struct K1Scratch {
   uint32_t* bnz;
   unsigned long long* slice_nz;
   unsigned int* done;
+  // K2-TC operands (nullptr when the TC path is not prepared)
+  float* at;              // A^T per 128-row tile: at[(rt * kpad + k) * 128 + (i % 128)], zero padded
+  int64_t kpad;           // K rounded up to 32
+  int64_t m_at;           // M rounded up to 128
+  uint32_t* item_cnt;     // [n_tb][kw] B items per (256-column tile, 32-k chunk) (zeroed)
+  int64_t* item_off;      // [n_tb * kw + 1] exclusive prefix of item_cnt (last CTA)
+  int64_t n_tb;           // 256-column tiles of B
 };
 
 // --------------------------------------------------------------------------- A tile
@@ -69,11 +76,30 @@ __device__ __forceinline__ void k1_a_tile(const float* __restrict__ A, int64_t M
   uint32_t ccount[4] = {0, 0, 0, 0};
   uint32_t warp_total = 0;
   const int64_t rend = min(r0 + kK1Rows, M);
-  for (int64_t rb = r0; rb < rend; rb += 8) {
+  // with the TC operand enabled, rows run to the 128-row tile boundary (zeros past M)
+  const int64_t rend_at = z.at ? min(r0 + kK1Rows, z.m_at) : rend;
+  const bool at_ok = z.at != nullptr && c < z.kpad;
+  for (int64_t rb = r0; rb < rend_at; rb += 8) {
     float4 v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u)
       v[u] = (col_ok && rb + u < rend) ? ldg_stream(A + (rb + u) * lda + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (at_ok) {
+      // A^T tile row k = c+q holds rows rb..rb+7 at offset rb % 128: two 16-byte stores
+      const int64_t rt = rb >> 7;
+      float* dst = z.at + (rt * z.kpad + c) * 128 + (rb & 127);
+      const float e[4][8] = {{v[0].x, v[1].x, v[2].x, v[3].x, v[4].x, v[5].x, v[6].x, v[7].x},
+                             {v[0].y, v[1].y, v[2].y, v[3].y, v[4].y, v[5].y, v[6].y, v[7].y},
+                             {v[0].z, v[1].z, v[2].z, v[3].z, v[4].z, v[5].z, v[6].z, v[7].z},
+                             {v[0].w, v[1].w, v[2].w, v[3].w, v[4].w, v[5].w, v[6].w, v[7].w}};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float4* d4 = reinterpret_cast<float4*>(dst + q * 128);
+        d4[0] = make_float4(e[q][0], e[q][1], e[q][2], e[q][3]);
+        d4[1] = make_float4(e[q][4], e[q][5], e[q][6], e[q][7]);
+      }
+    }
+    if (rb >= rend) continue;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int64_t i = rb + u;
@@ -152,6 +178,16 @@ __device__ __forceinline__ void k1_b_tile(const float* __restrict__ B, int64_t K
 #pragma unroll
   for (int o = 16; o; o >>= 1) slices += __shfl_xor_sync(0xffffffffu, slices, o);
   if (lane == 0 && slices) atomicAdd(z.slice_nz, (unsigned long long)slices);
+  if (z.item_cnt) {
+    // K2-TC items of this chunk: ceil(popc(slice mask) / 8) per 16-column slice; a warp's
+    // 128 columns lie inside one 256-column tile
+    const uint32_t smask = gword | __shfl_xor_sync(0xffffffffu, gword, 2);
+    uint32_t items = ((lane & 3) == 0 && col_ok) ? (__popc(smask) + 7u) >> 3 : 0u;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) items += __shfl_xor_sync(0xffffffffu, items, o);
+    const int64_t c_warp = tx * kK1Cols + 128 * (threadIdx.x >> 5);
+    if (lane == 0 && items && c_warp < ldb) atomicAdd(&z.item_cnt[(c_warp >> 8) * kw + kw_idx], items);
+  }
 }
 
 __device__ void k1_finalize_block(const uint32_t* __restrict__ acol, const uint32_t* __restrict__ bpop,
@@ -183,6 +219,34 @@ k1_pass(const float* __restrict__ A, int64_t M, int64_t K, int64_t lda, uint32_t
   __threadfence();
   if (threadIdx.x == 0) *z.done = 0u;  // ready for the next launch (no other CTA is left)
   k1_finalize_block(z.acol, z.bpop, z.bnz, K, M, nreg, has_a, has_b, z.slice_nz, stats);
+  if (z.item_cnt && nB > 0) {  // exclusive prefix of the K2-TC item counts (tb-major, chunk-minor)
+    __shared__ int64_t icarry;
+    __shared__ int64_t iwsum[kK1Threads / 32];
+    if (threadIdx.x == 0) icarry = 0;
+    __syncthreads();
+    const int64_t ncnt = z.n_tb * kw;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t base = 0; base < ncnt; base += kK1Threads) {
+      const int64_t t = base + threadIdx.x;
+      const int64_t v = t < ncnt ? (int64_t)z.item_cnt[t] : 0;
+      int64_t x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) iwsum[warp] = x;
+      __syncthreads();
+      int64_t before = icarry;
+      for (int w = 0; w < warp; ++w) before += iwsum[w];
+      if (t < ncnt) z.item_off[t] = before + x - v;
+      __syncthreads();
+      if (threadIdx.x == kK1Threads - 1) icarry = before + x;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) z.item_off[ncnt] = icarry;
+    __syncthreads();
+  }
   if (nA > 0) {  // exclusive prefix of the 32-row tile sums for k1_csr's row_ptr
     __shared__ int64_t carry;
     __shared__ int64_t wsum[kK1Threads / 32];
@@ -336,6 +400,97 @@ __global__ void __launch_bounds__(1024) k1_finalize(const uint32_t* __restrict__
                                                     const unsigned long long* __restrict__ slice_nz,
                                                     unsigned long long* __restrict__ out) {
   k1_finalize_block(acol, bpop, bnz, K, M, nreg, has_a, has_b, slice_nz, out);
+}
+
+// ------------------------------------------------------------ B items for K2-TC
+// Packs, once per plan, the B operand of every K2-TC item: for each 256-column tile tb and
+// 32-k chunk c, slice j (16 columns) contributes ceil(n_j / 8) items, n_j = # k in the
+// chunk with a non-zero B block in the slice.  An item is the 8 gathered B rows (zero rows
+// as padding) x 16 columns, split into tf32 hi / lo and laid out as the K-major
+// SWIZZLE_NONE core matrices the UMMA smem descriptor reads: element (n, r) at
+// (n%8)*16 + (n/8)*128 + (r/4)*256 + (r%4)*4 bytes, lo at +512.  Its 16-byte meta record
+// holds the 8 gathered k (32 = padding -> the zero row of K2's A^T stage) and the slice.
+// Items of one (tb, c) are contiguous at item_off[tb * kw + c], so K2 moves them with one
+// bulk copy per chunk — and all 128-row tiles reuse them (B is packed once, not per tile).
+constexpr int kPackThreads = 128;
+constexpr int kPackMaxItems = 64;
+
+__global__ void __launch_bounds__(kPackThreads)
+k1_pack_b(const float* __restrict__ B, int64_t K, int64_t ldb, const uint32_t* __restrict__ bgrp, int64_t kw,
+          const int64_t* __restrict__ item_off, uint8_t* __restrict__ items, uint4* __restrict__ meta) {
+  extern __shared__ __align__(16) uint8_t pk_smem[];  // [64][1024] staged items
+  __shared__ uint8_t s_k[kPackMaxItems][8];
+  __shared__ uint8_t s_slice[kPackMaxItems];
+  __shared__ int s_n;
+  const int64_t c = blockIdx.x, tb = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t n0 = tb * 256, k0 = c * 32;
+  if (tid < 32) {
+    uint32_t m = 0;
+    if (lane < 16 && n0 + 16 * lane < ldb) {
+      const int64_t g = (n0 >> 3) + 2 * lane;
+      m = bgrp[g * kw + c] | bgrp[(g + 1) * kw + c];
+    }
+    const int n = __popc(m);
+    const int mine = (n + 7) >> 3;
+    int base = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, base, o);
+      if (lane >= o) base += y;
+    }
+    if (lane == 31) s_n = base;
+    base -= mine;
+    for (int g = 0; g < mine; ++g) {
+      s_slice[base + g] = (uint8_t)lane;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int idx = 8 * g + r;
+        int kk = 32;  // padding -> zero row
+        if (idx < n) {
+          uint32_t mm = m;
+          for (int d = 0; d < idx; ++d) mm &= mm - 1;
+          kk = __ffs(mm) - 1;
+        }
+        s_k[base + g][r] = (uint8_t)kk;
+      }
+    }
+  }
+  __syncthreads();
+  const int nitems = s_n;
+  const int64_t off = item_off[tb * kw + c];
+  // items: piece p = (item t, row r, quad q) -> 4 floats of B, split, scattered into smem
+  for (int p = tid; p < nitems * 32; p += kPackThreads) {
+    const int t = p >> 5, r = (p >> 2) & 7, q = p & 3;
+    const int kk = s_k[t][r];
+    const int j = s_slice[t];
+    float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (kk < 32) bv = ldg_stream(B + (k0 + kk) * ldb + n0 + 16 * j + 4 * q);
+    const float e[4] = {bv.x, bv.y, bv.z, bv.w};
+    uint8_t* blk = pk_smem + t * 1024 + (r >> 2) * 256 + (r & 3) * 4;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int nn = 4 * q + i;
+      const int o2 = (nn & 7) * 16 + (nn >> 3) * 128;
+      const uint32_t bits = __float_as_uint(e[i]);
+      const uint32_t hi = bits & 0xFFFFE000u;
+      const uint32_t lo = __float_as_uint(e[i] - __uint_as_float(hi));
+      *reinterpret_cast<uint32_t*>(blk + o2) = hi;
+      *reinterpret_cast<uint32_t*>(blk + 512 + o2) = lo;
+    }
+  }
+  __syncthreads();
+  uint4* dst = reinterpret_cast<uint4*>(items + off * 1024);
+  const uint4* src = reinterpret_cast<const uint4*>(pk_smem);
+  for (int v = tid; v < nitems * 64; v += kPackThreads) dst[v] = src[v];
+  for (int t = tid; t < nitems; t += kPackThreads) {
+    uint4 mrec;
+    mrec.x = *reinterpret_cast<const uint32_t*>(&s_k[t][0]);
+    mrec.y = *reinterpret_cast<const uint32_t*>(&s_k[t][4]);
+    mrec.z = s_slice[t];
+    mrec.w = 0;
+    meta[off + t] = mrec;
+  }
 }
 
 // ------------------------------------------------------------ ABlockIndex export

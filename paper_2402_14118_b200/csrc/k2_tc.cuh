@@ -3,29 +3,31 @@
 // Same contract as K2-SIMT (SPEC multiply_mmm; PAPER Fig. 10): C += A*B over
 // the runtime masks.  The B-side skip of the paper (a zero 8-wide group costs nothing,
 // kernel_table.cpp:17-20) is realised as k-compaction per 16-column slice: for C tile rows
-// [m0, m0+128) and slice j only the k whose B block is non-zero (K1's transposed block
-// masks) enter the product, so every MMA is
+// [m0, m0+128) and slice j only the k whose B block is non-zero enter the product, so every
+// MMA is
 //     D_j[128 x 16] += A[128 x 8 gathered k] * B[8 gathered k x 16]      ("an item").
 // The A-side zeros stay inside the MMA (the tensor core has no per-element skip): the
 // waste is 1/dA, against 1/(dA*dB) for a dense GEMM.
 //
-// Warp roles (288 threads, one CTA per SM, tile = 128 rows x 256 columns = 16 slices):
-//   warps 0-3  GATHER: thread t of warp w owns row 32w+t = TMEM lane 32w+t.  For each item
-//              it reads the 8 gathered A columns of its row from the staged A^T chunk
-//              (conflict-free: a warp reads 32 consecutive rows of one k), splits them into
-//              tf32 hi/lo and writes them to a TMEM ring slot (tcgen05.st); at the end it
-//              runs the epilogue C += D (tcgen05.ld).
-//   warp 4     MMA: one thread issues 3 tcgen05.mma per item (hi*hi, hi*lo, lo*hi) into the
-//              slice's accumulator columns; tcgen05.commit frees ring slots / chunk stages.
-//   warps 5-8  STAGE: per 32-k chunk, the slice masks -> item list, the A^T chunk (LDG rows,
-//              transposed STS), and the B items (LDG of the non-zero B rows only, tf32
-//              split, K-major SWIZZLE_NONE core matrices for the UMMA descriptor).
-// Pipelines: 2 chunk stages (full/empty mbarriers), 16 TMEM item slots (full/empty).
+// Operands come MMA-ready from K1 (k1_preprocess.cuh): A^T per 128-row tile (so a 32-k
+// chunk of the tile is one contiguous 16 KB block) and the packed B items (tf32 hi/lo in
+// K-major core-matrix layout + 16-byte meta: gathered k, slice), contiguous per
+// (256-column tile, chunk).  K2 therefore moves its operands with bulk async copies only.
 //
-// TMEM (512 columns): D = 256 fp32 accumulator columns, ring = 16 items x (8 hi + 8 lo).
-// 3xTF32: x_hi = top 19 bits of x, x_lo = x - x_hi (exact) — ~2^-21 relative per product,
-// inside the north_star tolerance |dC| <= 1e-5 * Σ|a||b|;
-// results are tolerance-matched, not bit-identical (the SIMT variants are bit-exact).
+// Warp roles (192 threads, one CTA per SM, tile = 128 rows x 256 columns = 16 slices):
+//   warps 0-3  GATHER: thread t of warp w owns row 32w+t = TMEM lane 32w+t.  Per item it
+//              reads the 8 gathered A columns of its row from the A^T stage (a warp reads 32
+//              consecutive floats of one k: conflict-free; padding points at a zero row),
+//              splits them into tf32 hi/lo and writes them to a TMEM ring slot; finally the
+//              epilogue C += D (tcgen05.ld).
+//   warp 4     MMA: one thread issues 3 tcgen05.mma per item (hi*hi, hi*lo, lo*hi) into the
+//              slice's accumulator columns; tcgen05.commit frees ring slots and stages.
+//   warp 5     PRODUCER: one thread issues cp.async.bulk (TMA bulk) copies of each chunk's
+//              A^T block and B items into 4 smem stages / a 128-item ring (mbarrier tx).
+//
+// TMEM (512 columns): D = 256 fp32 accumulator columns + 16 item slots x (8 hi + 8 lo).
+// 3xTF32: x_hi = top 19 bits, x_lo = x - x_hi (exact): ~2^-21 relative per product, inside
+// the north_star tolerance |dC| <= 1e-5 * Σ|a||b|; results are tolerance-matched.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -36,70 +38,72 @@ namespace mmmcu {
 
 constexpr int kTcTM = 128;
 constexpr int kTcTN = 256;
-constexpr int kTcSlices = kTcTN / 16;
-constexpr int kTcKC = 32;                              // k per chunk (one 32-bit mask word)
-constexpr int kTcStages = 2;
-constexpr int kTcRing = 16;                            // TMEM A item slots
-constexpr int kTcMaxItems = kTcSlices * (kTcKC / 8);   // 64 items per chunk at most
-constexpr int kTcItemBytes = 1024;                     // B hi (512 B) + lo (512 B)
-constexpr int kTcThreads = 9 * 32;
-constexpr int kTcStageThreads = 128;
+constexpr int kTcKC = 32;             // k per chunk = one 32-bit mask word
+constexpr int kTcStages = 4;          // A^T stages
+constexpr int kTcBRing = 128;         // B items resident in smem
+constexpr int kTcTmemRing = 16;       // gathered-A item slots in TMEM
+constexpr int kTcMaxChunkItems = 64;  // 16 slices x 4 items
+constexpr int kTcThreads = 6 * 32;
+constexpr int kTcBatch = 4;           // items per gather batch (one tcgen05.wait::st)
 
-struct alignas(128) TcStage {
-  float at[kTcKC][kTcTM];                       // 16 KB  A^T chunk
-  uint8_t b[kTcMaxItems][kTcItemBytes];         // 64 KB  B items (hi | lo)
-  uint8_t item_k[kTcMaxItems][8];               // gathered k (within chunk) per item row, 0xFF = pad
-  uint8_t item_slice[kTcMaxItems];
-  uint32_t nitems;
-};
-
-struct TcShared {
-  TcStage st[kTcStages];
-  uint64_t chunk_full[kTcStages];
-  uint64_t chunk_empty[kTcStages];
-  uint64_t item_full[kTcRing];
-  uint64_t item_empty[kTcRing];
+struct alignas(1024) TcShared {
+  uint8_t bring[kTcBRing][1024];                 // 128 KB  B items (hi | lo)
+  float at[kTcStages][kTcKC + 1][kTcTM];         // 66 KB   A^T stages; row 32 = zeros (padding)
+  uint4 mring[kTcBRing];                         // 2 KB    item meta
+  uint64_t full[kTcStages];
+  uint64_t empty[kTcStages];
+  uint64_t item_full[kTcTmemRing];
+  uint64_t item_empty[kTcTmemRing];
   uint64_t done;
+  uint32_t st_start[kTcStages];                  // ring position of the stage's first item
+  uint32_t st_count[kTcStages];
   uint32_t tmem_base;
 };
 constexpr int kTcSmem = (int)sizeof(TcShared) + 1024;
 
-__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   tc::smem_u32(smem_dst)),
+               "l"(gsrc), "r"(bytes), "r"(tc::smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(bar)), "r"(bytes)
+               : "memory");
 }
 
 __global__ void __launch_bounds__(kTcThreads, 1)
-k2_tc(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb, float* __restrict__ C,
-      int64_t ldc, int64_t M, int64_t K, int64_t Np, const uint32_t* __restrict__ bgrp, int64_t kw) {
+k2_tc(const float* __restrict__ AT, int64_t kpad, const uint8_t* __restrict__ items, const uint4* __restrict__ meta,
+      const int64_t* __restrict__ item_off, int64_t kw, float* __restrict__ C, int64_t ldc, int64_t M, int64_t Np) {
   extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
   TcShared& sh = *reinterpret_cast<TcShared*>(tc_smem_raw + ((1024 - (tc::smem_u32(tc_smem_raw) & 1023)) & 1023));
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t m0 = (int64_t)blockIdx.y * kTcTM;
-  const int64_t n0 = (int64_t)blockIdx.x * kTcTN;
-  const int64_t nchunks = (K + kTcKC - 1) / kTcKC;
+  const int64_t rt = blockIdx.y, tb = blockIdx.x;
+  const int64_t m0 = rt * kTcTM, n0 = tb * kTcTN;
+  const int64_t nchunks = kw;
+  const int64_t* offs = item_off + tb * kw;
 
-  // ---- setup: TMEM (warp 4 owns alloc/dealloc), barriers, zeroed accumulators
+  // ---- setup
   if (warp == 4) tc::tmem_alloc(&sh.tmem_base, 512);
   if (tid == 0) {
     for (int s = 0; s < kTcStages; ++s) {
-      tc::mbar_init(&sh.chunk_full[s], 4);   // 4 stage warps
-      tc::mbar_init(&sh.chunk_empty[s], 5);  // 4 gather warps + 1 MMA commit
+      tc::mbar_init(&sh.full[s], 1);   // producer arrive + tx bytes
+      tc::mbar_init(&sh.empty[s], 5);  // 4 gather warps + 1 MMA commit
     }
-    for (int i = 0; i < kTcRing; ++i) {
-      tc::mbar_init(&sh.item_full[i], 4);    // 4 gather warps
-      tc::mbar_init(&sh.item_empty[i], 1);   // MMA commit
+    for (int i = 0; i < kTcTmemRing; ++i) {
+      tc::mbar_init(&sh.item_full[i], 4);
+      tc::mbar_init(&sh.item_empty[i], 1);
     }
     tc::mbar_init(&sh.done, 1);
     tc::fence_mbar_init();
   }
+  for (int e = tid; e < kTcStages * kTcTM; e += kTcThreads) sh.at[e / kTcTM][kTcKC][e % kTcTM] = 0.f;
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = sh.tmem_base;
-  const uint32_t tD = tbase;             // accumulators, columns [0, 256)
-  const uint32_t tRing = tbase + kTcTN;  // A items, columns [256, 512)
-
+  const uint32_t tD = tbase, tRing = tbase + kTcTN;
   if (warp < 4) {
     uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const uint32_t lane_base = (uint32_t)(32 * warp) << 16;
@@ -110,111 +114,57 @@ k2_tc(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int
   __syncthreads();
   tc::fence_after_sync();
 
-  if (warp >= 5) {
-    // =========================================================== STAGE warps
-    const int st = tid - 5 * 32;  // 0..127
-    const int64_t arow = m0 + st;
-    for (int64_t c = 0; c < nchunks; ++c) {
-      const int s = (int)(c & 1);
-      TcStage& S = sh.st[s];
-      if (c >= kTcStages) tc::mbar_wait(&sh.chunk_empty[s], (uint32_t)(((c >> 1) - 1) & 1));
-      const int64_t k0 = c * kTcKC;
-      // A^T: thread = row, 8 x 16-byte loads in flight, transposed conflict-free stores
-      float4 v[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int64_t gk = k0 + 4 * q;
-        v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (arow < M && gk < K) {
-          v[q] = __ldg(reinterpret_cast<const float4*>(A + arow * lda + gk));
-          if (gk + 4 > K) {
-            if (gk + 1 >= K) v[q].y = 0.f;
-            if (gk + 2 >= K) v[q].z = 0.f;
-            if (gk + 3 >= K) v[q].w = 0.f;
-          }
+  if (warp == 5) {
+    // ============================================================= PRODUCER
+    if (lane == 0) {
+      uint32_t head = 0;   // ring position (monotonic) of the next item
+      uint32_t tail = 0;   // first ring position still in use
+      int64_t oldest = 0;  // oldest chunk not yet known to be released
+      for (int64_t c = 0; c < nchunks; ++c) {
+        const int s = (int)(c % kTcStages);
+        const int64_t off = offs[c];
+        const uint32_t n = (uint32_t)(offs[c + 1] - off);
+        // stage reuse and ring space: release chunks oldest-first
+        while (oldest < c && (c - oldest >= kTcStages || head + n - tail > (uint32_t)kTcBRing)) {
+          const int so = (int)(oldest % kTcStages);
+          tc::mbar_wait(&sh.empty[so], (uint32_t)((oldest / kTcStages) & 1));
+          tail = sh.st_start[so] + sh.st_count[so];
+          ++oldest;
         }
+        sh.st_start[s] = head;
+        sh.st_count[s] = n;
+        mbar_arrive_expect_tx(&sh.full[s], 16384u + n * (1024u + 16u));
+        bulk_g2s(&sh.at[s][0][0], AT + (rt * kpad + c * kTcKC) * kTcTM, 16384u, &sh.full[s]);
+        const uint32_t pos = head % kTcBRing;
+        const uint32_t first = min(n, (uint32_t)kTcBRing - pos);
+        if (first) {
+          bulk_g2s(&sh.bring[pos][0], items + off * 1024, first * 1024u, &sh.full[s]);
+          bulk_g2s(&sh.mring[pos], meta + off, first * 16u, &sh.full[s]);
+        }
+        if (n > first) {
+          bulk_g2s(&sh.bring[0][0], items + (off + first) * 1024, (n - first) * 1024u, &sh.full[s]);
+          bulk_g2s(&sh.mring[0], meta + off + first, (n - first) * 16u, &sh.full[s]);
+        }
+        head += n;
       }
-      // item list (first stage warp): lane j < 16 owns slice j
-      if (st < 32) {
-        uint32_t m = 0;
-        if (lane < kTcSlices && n0 + 16 * lane < Np) {
-          const int64_t g = (n0 >> 3) + 2 * lane;
-          m = bgrp[g * kw + c] | bgrp[(g + 1) * kw + c];
-        }
-        const int n = __popc(m);
-        const int my_items = (n + 7) >> 3;
-        int base = my_items;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, base, o);
-          if (lane >= o) base += y;
-        }
-        const int total = __shfl_sync(0xffffffffu, base, 31);
-        base -= my_items;
-        for (int g = 0; g < my_items; ++g) {
-          S.item_slice[base + g] = (uint8_t)lane;
-          uint32_t lo = 0, hi = 0;
-#pragma unroll
-          for (int r = 0; r < 8; ++r) {
-            const int idx = 8 * g + r;
-            const uint32_t kk = idx < n ? (uint32_t)tc::nth_set_bit(m, idx) : 0xFFu;
-            if (r < 4) lo |= kk << (8 * r);
-            else hi |= kk << (8 * (r - 4));
-          }
-          *reinterpret_cast<uint2*>(S.item_k[base + g]) = make_uint2(lo, hi);
-        }
-        if (lane == 0) S.nitems = (uint32_t)total;
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        S.at[4 * q + 0][st] = v[q].x;
-        S.at[4 * q + 1][st] = v[q].y;
-        S.at[4 * q + 2][st] = v[q].z;
-        S.at[4 * q + 3][st] = v[q].w;
-      }
-      named_bar_sync(1, kTcStageThreads);  // item list visible to all stage threads
-      const int nitems = (int)S.nitems;
-      // B items: piece p = (item t, row r, 4-column quad q); K-major core matrices:
-      // element (n, r) at (n%8)*16 + (n/8)*128 + (r/4)*256 + (r%4)*4 bytes (hi), +512 (lo)
-      for (int p = st; p < nitems * 32; p += kTcStageThreads) {
-        const int t = p >> 5, r = (p >> 2) & 7, q = p & 3;
-        const int j = S.item_slice[t];
-        const uint32_t kk = S.item_k[t][r];
-        float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (kk != 0xFFu) bv = __ldg(reinterpret_cast<const float4*>(B + (k0 + kk) * ldb + n0 + 16 * j + 4 * q));
-        const float e[4] = {bv.x, bv.y, bv.z, bv.w};
-        uint8_t* blk = S.b[t] + (r >> 2) * 256 + (r & 3) * 4;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int nn = 4 * q + i;
-          const int off = (nn & 7) * 16 + (nn >> 3) * 128;
-          uint32_t h, l;
-          tc::split_tf32(e[i], h, l);
-          *reinterpret_cast<uint32_t*>(blk + off) = h;
-          *reinterpret_cast<uint32_t*>(blk + 512 + off) = l;
-        }
-      }
-      tc::fence_async_smem();  // generic-proxy writes -> visible to the tensor core
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&sh.chunk_full[s]);
     }
   } else if (warp == 4) {
-    // =========================================================== MMA warp
+    // ============================================================= MMA
     if (lane == 0) {
       const uint32_t idesc = tc::idesc_tf32_m128(16);
-      uint32_t n = 0;
+      uint32_t ni = 0;
       for (int64_t c = 0; c < nchunks; ++c) {
-        const int s = (int)(c & 1);
-        TcStage& S = sh.st[s];
-        tc::mbar_wait(&sh.chunk_full[s], (uint32_t)((c >> 1) & 1));
-        const int nitems = (int)S.nitems;
-        for (int t = 0; t < nitems; ++t, ++n) {
-          const uint32_t slot = n % kTcRing;
-          tc::mbar_wait(&sh.item_full[slot], (n / kTcRing) & 1);
+        const int s = (int)(c % kTcStages);
+        tc::mbar_wait(&sh.full[s], (uint32_t)((c / kTcStages) & 1));
+        const uint32_t start = sh.st_start[s], cnt = sh.st_count[s];
+        for (uint32_t t = 0; t < cnt; ++t, ++ni) {
+          const uint32_t slot = ni % kTcTmemRing;
+          tc::mbar_wait(&sh.item_full[slot], (ni / kTcTmemRing) & 1);
           tc::fence_after_sync();
-          const uint32_t dcol = tD + 16 * S.item_slice[t];
+          const uint32_t bpos = (start + t) % kTcBRing;
+          const uint32_t dcol = tD + 16 * sh.mring[bpos].z;
           const uint32_t a_hi = tRing + slot * 16, a_lo = a_hi + 8;
-          const uint32_t bh = tc::smem_u32(S.b[t]);
+          const uint32_t bh = tc::smem_u32(&sh.bring[bpos][0]);
           const uint64_t dh = tc::smem_desc(bh, 256, 128);
           const uint64_t dl = tc::smem_desc(bh + 512, 256, 128);
           tc::mma_tf32_ts(dcol, a_hi, dh, idesc, 1);
@@ -222,41 +172,48 @@ k2_tc(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int
           tc::mma_tf32_ts(dcol, a_lo, dh, idesc, 1);
           tc::mma_commit(&sh.item_empty[slot]);
         }
-        tc::mma_commit(&sh.chunk_empty[s]);
+        tc::mma_commit(&sh.empty[s]);
       }
       tc::mma_commit(&sh.done);
     }
     __syncwarp();
   } else {
-    // =========================================================== GATHER warps
+    // ============================================================= GATHER (warps 0-3)
     const uint32_t lane_base = (uint32_t)(32 * warp) << 16;
-    uint32_t n = 0;
+    uint32_t ni = 0;
     for (int64_t c = 0; c < nchunks; ++c) {
-      const int s = (int)(c & 1);
-      TcStage& S = sh.st[s];
-      tc::mbar_wait(&sh.chunk_full[s], (uint32_t)((c >> 1) & 1));
-      const int nitems = (int)S.nitems;
-      const float* at = &S.at[0][tid];
-      for (int t = 0; t < nitems; ++t, ++n) {
-        const uint32_t slot = n % kTcRing;
-        if (n >= kTcRing) tc::mbar_wait(&sh.item_empty[slot], ((n / kTcRing) - 1) & 1);
-        const uint2 kq = *reinterpret_cast<const uint2*>(S.item_k[t]);
-        uint32_t h[8], l[8];
+      const int s = (int)(c % kTcStages);
+      tc::mbar_wait(&sh.full[s], (uint32_t)((c / kTcStages) & 1));
+      const uint32_t start = sh.st_start[s], cnt = sh.st_count[s];
+      const float* at = &sh.at[s][0][tid];
+      for (uint32_t t0 = 0; t0 < cnt; t0 += kTcBatch) {
+        const uint32_t b = min((uint32_t)kTcBatch, cnt - t0);
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          const uint32_t kk = ((r < 4 ? kq.x : kq.y) >> (8 * (r & 3))) & 0xFFu;
-          const float a = kk != 0xFFu ? at[kk * kTcTM] : 0.f;
-          tc::split_tf32(a, h[r], l[r]);
+        for (int i = 0; i < kTcBatch; ++i) {
+          if ((uint32_t)i < b) {
+            const uint32_t n_i = ni + i;
+            const uint32_t slot = n_i % kTcTmemRing;
+            if (n_i >= kTcTmemRing) tc::mbar_wait(&sh.item_empty[slot], ((n_i / kTcTmemRing) - 1) & 1);
+            const uint4 m = sh.mring[(start + t0 + i) % kTcBRing];
+            uint32_t h[8], l[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+              const uint32_t kk = ((r < 4 ? m.x : m.y) >> (8 * (r & 3))) & 0xFFu;
+              tc::split_tf32(at[kk * kTcTM], h[r], l[r]);
+            }
+            tc::tmem_st8(tRing + lane_base + slot * 16, h);
+            tc::tmem_st8(tRing + lane_base + slot * 16 + 8, l);
+          }
         }
-        tc::tmem_st8(tRing + lane_base + slot * 16, h);
-        tc::tmem_st8(tRing + lane_base + slot * 16 + 8, l);
         tc::tmem_st_wait();
         tc::fence_before_sync();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&sh.item_full[slot]);
+        if (lane == 0)
+          for (uint32_t i = 0; i < b; ++i) tc::mbar_arrive(&sh.item_full[(ni + i) % kTcTmemRing]);
+        ni += b;
       }
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&sh.chunk_empty[s]);
+      if (lane == 0) tc::mbar_arrive(&sh.empty[s]);
     }
     // ---- epilogue: C += D (thread = row)
     tc::mbar_wait(&sh.done, 0);

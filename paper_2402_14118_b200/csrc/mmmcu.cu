@@ -73,6 +73,11 @@ struct mmmcu_ctx {
   DevBuf codes, bgrp, zb;
   DevBuf ctl;
 
+  // ---- K2-TC operands (built by K1 when the TC path may run: algo AUTO or TC)
+  bool tc_a = false, tc_b = false;
+  int64_t kpad = 0, m_at = 0, n_tb = 0;
+  DevBuf at, items, meta, item_off;
+
   // ---- statistics: u64 [16] = {inv, lanes, skipped, zreg, nnzA, pop, zero_codes, span, slice_nz}
   DevBuf stats;
 
@@ -143,6 +148,8 @@ int64_t n_row_tiles(int64_t M) { return (M + mmmcu::kK1Rows - 1) / mmmcu::kK1Row
 unsigned long long* zb_slice(mmmcu_ctx* ctx) { return ctx->zb.as<unsigned long long>(); }
 uint32_t* zb_bpop(mmmcu_ctx* ctx) { return reinterpret_cast<uint32_t*>(ctx->zb.as<unsigned long long>() + 1); }
 uint32_t* zb_bnz(mmmcu_ctx* ctx) { return zb_bpop(ctx) + ctx->Kb; }
+uint32_t* zb_item_cnt(mmmcu_ctx* ctx) { return zb_bnz(ctx) + ctx->Kb; }
+bool want_tc(const mmmcu_ctx* ctx) { return ctx->algo == MMMCU_ALGO_AUTO || ctx->algo == MMMCU_ALGO_TC; }
 
 mmmcu_status stage_a(mmmcu_ctx* ctx, const float* A, int64_t M, int64_t K, int64_t lda, uint64_t av) {
   if (M <= 0 || K <= 0) return fail(ctx, MMMCU_ERR_INVALID_ARG, "matrix dimensions must be positive");
@@ -158,6 +165,12 @@ mmmcu_status stage_a(mmmcu_ctx* ctx, const float* A, int64_t M, int64_t K, int64
   MMMCU_CUDA(ctx->row_ptr.ensure(sizeof(int64_t) * (M + 1)));
   MMMCU_CUDA(ctx->cols.ensure((size_t)ctx->csr_idx_bytes * M * K));
   MMMCU_CUDA(cudaMemsetAsync(ctx->za.p, 0, sizeof(uint32_t) * (M + K + n_row_tiles(M)), ctx->stream));
+  ctx->tc_a = false;
+  if (want_tc(ctx)) {
+    ctx->kpad = round_up(K, 32);
+    ctx->m_at = round_up(M, 128);
+    MMMCU_CUDA(ctx->at.ensure(sizeof(float) * ctx->m_at * ctx->kpad));
+  }
   ctx->A = A;
   ctx->M = M;
   ctx->Ka = K;
@@ -177,8 +190,19 @@ mmmcu_status stage_b(mmmcu_ctx* ctx, const float* B, int64_t K, int64_t N, int64
   ctx->has_b = false;
   MMMCU_CUDA(ctx->codes.ensure((size_t)K * nreg));
   MMMCU_CUDA(ctx->bgrp.ensure(sizeof(uint32_t) * ngrp * kw));
-  MMMCU_CUDA(ctx->zb.ensure(sizeof(unsigned long long) + sizeof(uint32_t) * 2 * K));
-  MMMCU_CUDA(cudaMemsetAsync(ctx->zb.p, 0, sizeof(unsigned long long) + sizeof(uint32_t) * 2 * K, ctx->stream));
+  ctx->tc_b = false;
+  const int64_t n_tb = (ldb + 255) / 256;
+  const int64_t n_cnt = want_tc(ctx) ? n_tb * kw : 0;
+  const size_t zb_bytes = sizeof(unsigned long long) + sizeof(uint32_t) * (2 * K + n_cnt);
+  MMMCU_CUDA(ctx->zb.ensure(zb_bytes));
+  MMMCU_CUDA(cudaMemsetAsync(ctx->zb.p, 0, zb_bytes, ctx->stream));
+  if (want_tc(ctx)) {
+    // worst case 64 items (16 slices x 4) per (256-column tile, 32-k chunk): 2x B's bytes
+    ctx->n_tb = n_tb;
+    MMMCU_CUDA(ctx->item_off.ensure(sizeof(int64_t) * (n_cnt + 1)));
+    MMMCU_CUDA(ctx->items.ensure((size_t)n_cnt * 64 * 1024));
+    MMMCU_CUDA(ctx->meta.ensure((size_t)n_cnt * 64 * 16));
+  }
   ctx->B = B;
   ctx->Kb = K;
   ctx->N = N;
@@ -199,8 +223,10 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   const bool same_k = a_valid && b_valid && ctx->Ka == ctx->Kb;
   const int64_t K = do_a ? ctx->Ka : ctx->Kb;
   const int64_t kw = (K + 31) / 32;
+  const bool tc_a = do_a && want_tc(ctx), tc_b = do_b && want_tc(ctx);
   const int64_t a_tx = (ctx->Ka + mmmcu::kK1Cols - 1) / mmmcu::kK1Cols;
-  const int64_t nA = do_a ? a_tx * ((ctx->M + mmmcu::kK1Rows - 1) / mmmcu::kK1Rows) : 0;
+  const int64_t a_rows = tc_a ? ctx->m_at : ctx->M;  // A^T tiles are written to the 128-row boundary
+  const int64_t nA = do_a ? a_tx * ((a_rows + mmmcu::kK1Rows - 1) / mmmcu::kK1Rows) : 0;
   const int64_t b_tx = (ctx->ldb + mmmcu::kK1Cols - 1) / mmmcu::kK1Cols;
   const int64_t nB = do_b ? b_tx * ((ctx->Kb + 31) / 32) : 0;
   if (nA + nB > 0x7fffffff) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "operand too large for one K1 launch");
@@ -213,6 +239,12 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   z.bnz = b_valid ? zb_bnz(ctx) : nullptr;
   z.slice_nz = b_valid ? zb_slice(ctx) : ctx->stats.as<unsigned long long>() + 15;
   z.done = ctx->ctl.as<unsigned int>();
+  z.at = tc_a ? ctx->at.as<float>() : nullptr;
+  z.kpad = ctx->kpad;
+  z.m_at = ctx->m_at;
+  z.item_cnt = tc_b ? zb_item_cnt(ctx) : nullptr;
+  z.item_off = tc_b ? ctx->item_off.as<int64_t>() : nullptr;
+  z.n_tb = ctx->n_tb;
   const int has_a = a_valid && (same_k || !b_valid) ? 1 : 0;
   const int has_b = b_valid && (same_k || !a_valid) ? 1 : 0;
   mmmcu::k1_pass<<<(unsigned)(nA + nB), mmmcu::kK1Threads, 0, ctx->stream>>>(
@@ -232,8 +264,22 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
                                                                ctx->row_ptr.as<int64_t>(), ctx->cols.as<uint32_t>());
     MMMCU_LAUNCHED();
   }
-  if (do_a) ctx->has_a = true;
-  if (do_b) ctx->has_b = true;
+  if (tc_b) {
+    MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k1_pack_b, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    dim3 grid((unsigned)((ctx->Kb + 31) / 32), (unsigned)ctx->n_tb);
+    mmmcu::k1_pack_b<<<grid, mmmcu::kPackThreads, 64 * 1024, ctx->stream>>>(
+        ctx->B, ctx->Kb, ctx->ldb, ctx->bgrp.as<uint32_t>(), (ctx->Kb + 31) / 32, ctx->item_off.as<int64_t>(),
+        ctx->items.as<uint8_t>(), ctx->meta.as<uint4>());
+    MMMCU_LAUNCHED();
+  }
+  if (do_a) {
+    ctx->has_a = true;
+    ctx->tc_a = tc_a;
+  }
+  if (do_b) {
+    ctx->has_b = true;
+    ctx->tc_b = tc_b;
+  }
   return MMMCU_OK;
 }
 
@@ -321,7 +367,7 @@ mmmcu_status mmmcu_ctx_destroy(mmmcu_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : {&ctx->abits, &ctx->za, &ctx->tile_prefix, &ctx->row_ptr, &ctx->cols, &ctx->codes, &ctx->bgrp, &ctx->zb,
-                    &ctx->ctl, &ctx->stats, &ctx->hA, &ctx->hB, &ctx->hC, &ctx->scratch0, &ctx->scratch1})
+                    &ctx->ctl, &ctx->at, &ctx->items, &ctx->meta, &ctx->item_off, &ctx->stats, &ctx->hA, &ctx->hB, &ctx->hC, &ctx->scratch0, &ctx->scratch1})
     b->release();
   delete ctx;
   return MMMCU_OK;
@@ -496,14 +542,17 @@ mmmcu_status mmmcu_multiply(mmmcu_ctx* ctx, float* C, int64_t ldc, const float* 
     return fail(ctx, MMMCU_ERR_INVALID_ARG,
                 "C must be 16-byte aligned with ldc >= round_up(N, 64) (Matrix padding) and ldc % 4 == 0");
   if (ctx->algo == MMMCU_ALGO_TC) {
+    if (!ctx->tc_a || !ctx->tc_b)
+      return fail(ctx, MMMCU_ERR_NOT_READY, "the TC operands were not built: preprocess with algo AUTO or TC");
     ctx->last_algo = MMMCU_ALGO_TC;
     const int64_t Np = round_up(ctx->N, 64), kw = (ctx->Ka + 31) / 32;
-    const int64_t row_tiles = (ctx->M + mmmcu::kTcTM - 1) / mmmcu::kTcTM;
+    const int64_t row_tiles = ctx->m_at / mmmcu::kTcTM;
     if (row_tiles > 65535) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "M too large for the TC grid");
     MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, mmmcu::kTcSmem));
     dim3 grid((unsigned)((Np + mmmcu::kTcTN - 1) / mmmcu::kTcTN), (unsigned)row_tiles);
     mmmcu::k2_tc<<<grid, mmmcu::kTcThreads, mmmcu::kTcSmem, ctx->stream>>>(
-        ctx->A, ctx->lda, ctx->B, ctx->ldb, C, ldc, ctx->M, ctx->Ka, Np, ctx->bgrp.as<uint32_t>(), kw);
+        ctx->at.as<float>(), ctx->kpad, ctx->items.as<uint8_t>(), ctx->meta.as<uint4>(), ctx->item_off.as<int64_t>(),
+        kw, C, ldc, ctx->M, Np);
     MMMCU_LAUNCHED();
   } else if (ctx->algo == MMMCU_ALGO_DENSE) {
     ctx->last_algo = MMMCU_ALGO_DENSE;
