@@ -59,6 +59,9 @@ struct K1Scratch {
   uint32_t* item_cnt;     // [n_tb][kw] B items per (256-column tile, 32-k chunk) (zeroed)
   int64_t* item_off;      // [n_tb * kw + 1] exclusive prefix of item_cnt (last CTA)
   int64_t n_tb;           // 256-column tiles of B
+  // K2-SIMT operand: raw non-zero B block rows per (256-column tile, chunk)
+  uint32_t* row_cnt;      // [n_tb][kw] non-zero (k, 16-column slice) rows (zeroed)
+  int64_t* row_off;       // [n_tb * kw + 1] exclusive prefix of (row_cnt + 2 header rows), 64-byte units
 };
 
 // --------------------------------------------------------------------------- A tile
@@ -178,6 +181,15 @@ __device__ __forceinline__ void k1_b_tile(const float* __restrict__ B, int64_t K
 #pragma unroll
   for (int o = 16; o; o >>= 1) slices += __shfl_xor_sync(0xffffffffu, slices, o);
   if (lane == 0 && slices) atomicAdd(z.slice_nz, (unsigned long long)slices);
+  if (z.row_cnt) {
+    // K2-SIMT rows of this chunk: one 64-byte row per non-zero (k, 16-column slice)
+    const uint32_t smask = gword | __shfl_xor_sync(0xffffffffu, gword, 2);
+    uint32_t rows = ((lane & 3) == 0 && col_ok) ? (uint32_t)__popc(smask) : 0u;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) rows += __shfl_xor_sync(0xffffffffu, rows, o);
+    const int64_t c_warp = tx * kK1Cols + 128 * (threadIdx.x >> 5);
+    if (lane == 0 && rows && c_warp < ldb) atomicAdd(&z.row_cnt[(c_warp >> 8) * kw + kw_idx], rows);
+  }
   if (z.item_cnt) {
     // K2-TC items of this chunk: ceil(popc(slice mask) / 8) per 16-column slice; a warp's
     // 128 columns lie inside one 256-column tile
@@ -194,6 +206,36 @@ __device__ void k1_finalize_block(const uint32_t* __restrict__ acol, const uint3
                                   const uint32_t* __restrict__ bnz, int64_t K, int64_t M, int64_t nreg, int has_a,
                                   int has_b, const unsigned long long* __restrict__ slice_nz,
                                   unsigned long long* __restrict__ out);
+
+// Block-wide exclusive scan of (cnt[t] + add) -> out[0..n] (out[n] = total); one CTA.
+__device__ void k1_block_exclusive_scan(const uint32_t* __restrict__ cnt, int64_t n, uint32_t add,
+                                        int64_t* __restrict__ out) {
+  __shared__ int64_t carry;
+  __shared__ int64_t wsum[kK1Threads / 32];
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t base = 0; base < n; base += kK1Threads) {
+    const int64_t t = base + threadIdx.x;
+    const int64_t v = t < n ? (int64_t)cnt[t] + add : 0;
+    int64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    int64_t before = carry;
+    for (int w = 0; w < warp; ++w) before += wsum[w];
+    if (t < n) out[t] = before + x - v;
+    __syncthreads();
+    if (threadIdx.x == kK1Threads - 1) carry = before + x;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[n] = carry;
+  __syncthreads();
+}
 
 // ------------------------------------------------------------------ fused K1 pass
 // One launch: CTAs [0, nA) are A tiles, [nA, nA + nB) are B tiles; the last CTA to finish
@@ -219,34 +261,8 @@ k1_pass(const float* __restrict__ A, int64_t M, int64_t K, int64_t lda, uint32_t
   __threadfence();
   if (threadIdx.x == 0) *z.done = 0u;  // ready for the next launch (no other CTA is left)
   k1_finalize_block(z.acol, z.bpop, z.bnz, K, M, nreg, has_a, has_b, z.slice_nz, stats);
-  if (z.item_cnt && nB > 0) {  // exclusive prefix of the K2-TC item counts (tb-major, chunk-minor)
-    __shared__ int64_t icarry;
-    __shared__ int64_t iwsum[kK1Threads / 32];
-    if (threadIdx.x == 0) icarry = 0;
-    __syncthreads();
-    const int64_t ncnt = z.n_tb * kw;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int64_t base = 0; base < ncnt; base += kK1Threads) {
-      const int64_t t = base + threadIdx.x;
-      const int64_t v = t < ncnt ? (int64_t)z.item_cnt[t] : 0;
-      int64_t x = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      if (lane == 31) iwsum[warp] = x;
-      __syncthreads();
-      int64_t before = icarry;
-      for (int w = 0; w < warp; ++w) before += iwsum[w];
-      if (t < ncnt) z.item_off[t] = before + x - v;
-      __syncthreads();
-      if (threadIdx.x == kK1Threads - 1) icarry = before + x;
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) z.item_off[ncnt] = icarry;
-    __syncthreads();
-  }
+  if (z.item_cnt && nB > 0) k1_block_exclusive_scan(z.item_cnt, z.n_tb * kw, 0, z.item_off);
+  if (z.row_cnt && nB > 0) k1_block_exclusive_scan(z.row_cnt, z.n_tb * kw, 2, z.row_off);
   if (nA > 0) {  // exclusive prefix of the 32-row tile sums for k1_csr's row_ptr
     __shared__ int64_t carry;
     __shared__ int64_t wsum[kK1Threads / 32];
@@ -490,6 +506,51 @@ k1_pack_b(const float* __restrict__ B, int64_t K, int64_t ldb, const uint32_t* _
     mrec.z = s_slice[t];
     mrec.w = 0;
     meta[off + t] = mrec;
+  }
+}
+
+// ----------------------------------------------------------- B rows for K2-SIMT
+// For each 256-column tile tb and 32-k chunk c, a contiguous record at row_off[tb*kw + c]
+// (64-byte units): 2 header rows = the 32 group k-masks of the tile's 8-column groups
+// (uint32 each, bit kk <-> k = 32c + kk), then for slice j = 0..15 (16 columns = groups
+// 2j, 2j+1) and every k of the chunk with a non-zero block in the slice, ascending, the
+// raw 16 floats B[k][16j .. 16j+15].  K2-SIMT moves each record with one bulk copy.
+__global__ void __launch_bounds__(kPackThreads)
+k1_pack_rows(const float* __restrict__ B, int64_t K, int64_t ldb, const uint32_t* __restrict__ bgrp, int64_t kw,
+             const int64_t* __restrict__ row_off, uint4* __restrict__ rows) {
+  __shared__ uint32_t s_g[32];
+  __shared__ uint32_t s_base[17];
+  const int64_t c = blockIdx.x, tb = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t n0 = tb * 256, k0 = c * 32;
+  if (tid < 32) {
+    const int64_t g = (n0 >> 3) + lane;
+    const uint32_t m = (n0 + 8 * lane < ldb) ? bgrp[g * kw + c] : 0u;
+    s_g[lane] = m;
+    const uint32_t um = m | __shfl_xor_sync(0xffffffffu, m, 1);  // slice union (even lanes)
+    uint32_t n = (lane & 1) == 0 ? (uint32_t)__popc(um) : 0u;
+    uint32_t x = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if ((lane & 1) == 0) s_base[lane >> 1] = x - n;
+    if (lane == 31) s_base[16] = x;
+  }
+  __syncthreads();
+  uint4* out = rows + row_off[tb * kw + c] * 4;
+  if (tid < 8) out[tid] = make_uint4(s_g[4 * tid], s_g[4 * tid + 1], s_g[4 * tid + 2], s_g[4 * tid + 3]);
+  const uint32_t total = s_base[16];
+  for (uint32_t p = tid; p < total * 4; p += kPackThreads) {
+    const uint32_t t = p >> 2, q = p & 3;
+    int j = 0;
+    while (j < 15 && s_base[j + 1] <= t) ++j;
+    uint32_t m = s_g[2 * j] | s_g[2 * j + 1];
+    for (uint32_t d = t - s_base[j]; d; --d) m &= m - 1;
+    const int kk = __ffs(m) - 1;
+    const float4 v = ldg_stream(B + (k0 + kk) * ldb + n0 + 16 * j + 4 * q);
+    out[8 + p] = make_uint4(__float_as_uint(v.x), __float_as_uint(v.y), __float_as_uint(v.z), __float_as_uint(v.w));
   }
 }
 

@@ -283,4 +283,174 @@ k2_dense(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, 
     }
 }
 
+
+// ====================================================================================
+// K2-SIMT v2 — the same exact computation, fed by bulk async copies of K1's MMA-ready
+// operands (A^T per 128-row tile, raw non-zero B block rows per (256-column tile, chunk)).
+//
+//   CTA   = 128 rows x 256 columns of C, 16 compute warps (one 16-column slice each) +
+//           1 producer warp; 4 smem stages of {A^T chunk [32 k][128 rows] (16 KB),
+//           B record: 2 header rows (32 group k-masks) + the chunk's non-zero slice rows}.
+//   lane  = rows 4l .. 4l+3 of the tile x the warp's 16 columns (64 fp32 accumulators,
+//           initialised from C).  Per non-zero B row k of its slice the warp issues one
+//           conflict-free LDS.128 of the 4 A values, 4 broadcast LDS.128 of B[k][slice] and
+//           32 FFMA2 predicated on a != 0 — the ascending-k fmaf chain of the oracle.
+//   SPAN  = 16: one walk per slice over the union mask (zero groups add exact +0.0 terms);
+//           8: one walk per 8-column group over its own mask (exact group skipping).
+// ====================================================================================
+constexpr int kS2Warps = 16;
+constexpr int kS2Threads = (kS2Warps + 1) * 32;
+constexpr int kS2Stages = 4;
+constexpr int kS2KC = 32;
+constexpr int kS2MaxRows = 2 + 16 * kS2KC;  // header + every (k, slice) of a chunk
+
+struct alignas(128) S2Stage {
+  float at[kS2KC][128];          // 16 KB
+  float4 rows[kS2MaxRows][4];    // 32.8 KB: header (2 rows) + B block rows
+};
+struct S2Shared {
+  S2Stage st[kS2Stages];
+  uint64_t full[kS2Stages];
+  uint64_t empty[kS2Stages];
+  // followed by the tile's chunk offsets (int64, kw + 1), dynamic
+};
+constexpr int kS2SmemBase = (int)sizeof(S2Shared) + 128;
+
+__device__ __forceinline__ void s2_bulk(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(smem_dst)),
+               "l"(gsrc), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+__device__ __forceinline__ void s2_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void s2_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void s2_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
+}
+__device__ __forceinline__ void s2_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "S2W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra S2W_%=;\n\t}" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+template <int SPAN>
+__global__ void __launch_bounds__(kS2Threads, 1)
+k2_simt2(const float* __restrict__ AT, int64_t kpad, const float4* __restrict__ brows, const int64_t* __restrict__ row_off,
+         int64_t kw, float* __restrict__ C, int64_t ldc, int64_t M, int64_t Np, const unsigned long long* __restrict__ sel) {
+  static_assert(SPAN == 8 || SPAN == 16, "SPAN must be 8 or 16");
+  if (sel && *sel != (unsigned long long)SPAN) return;  // device-side variant choice (k1_finalize)
+  extern __shared__ __align__(128) uint8_t s2_raw[];
+  S2Shared& sh = *reinterpret_cast<S2Shared*>(s2_raw + ((128 - ((uint32_t)__cvta_generic_to_shared(s2_raw) & 127)) & 127));
+  int64_t* offs = reinterpret_cast<int64_t*>(&sh + 1);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t rt = blockIdx.y, tb = blockIdx.x;
+  const int64_t m0 = rt * 128, n0 = tb * 256;
+
+  for (int64_t c = tid; c <= kw; c += kS2Threads) offs[c] = row_off[tb * kw + c];
+  if (tid == 0) {
+    for (int s = 0; s < kS2Stages; ++s) {
+      s2_init(&sh.full[s], 1);
+      s2_init(&sh.empty[s], kS2Warps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kS2Warps) {
+    // ------------------------------------------------------------------ producer
+    if (lane == 0) {
+      for (int64_t c = 0; c < kw; ++c) {
+        const int s = (int)(c % kS2Stages);
+        if (c >= kS2Stages) s2_wait(&sh.empty[s], (uint32_t)(((c / kS2Stages) - 1) & 1));
+        const uint32_t nrows = (uint32_t)(offs[c + 1] - offs[c]);
+        s2_expect_tx(&sh.full[s], 16384u + nrows * 64u);
+        s2_bulk(&sh.st[s].at[0][0], AT + (rt * kpad + c * kS2KC) * 128, 16384u, &sh.full[s]);
+        s2_bulk(&sh.st[s].rows[0][0], brows + offs[c] * 4, nrows * 64u, &sh.full[s]);
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------------- compute
+  const int j = warp;                       // slice
+  const int64_t ncol = n0 + 16 * j;
+  const bool slice_ok = ncol < Np;
+  constexpr int NS = 16 / SPAN;
+  float2 acc[NS][4][SPAN / 2];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int64_t row = m0 + 4 * lane + r;
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+#pragma unroll
+      for (int q = 0; q < SPAN / 2; ++q)
+        acc[s][r][q] = (slice_ok && row < M) ? *reinterpret_cast<const float2*>(C + row * ldc + ncol + s * SPAN + 2 * q)
+                                             : make_float2(0.f, 0.f);
+  }
+
+  for (int64_t c = 0; c < kw; ++c) {
+    const int st = (int)(c % kS2Stages);
+    s2_wait(&sh.full[st], (uint32_t)((c / kS2Stages) & 1));
+    const S2Stage& S = sh.st[st];
+    const uint32_t* hdr = reinterpret_cast<const uint32_t*>(&S.rows[0][0]);
+    const uint32_t g0 = hdr[2 * j], g1 = hdr[2 * j + 1];
+    const uint32_t um = g0 | g1;
+    // first data row of this slice: 2 header rows + the rows of slices 0 .. j-1
+    uint32_t base = 2;
+    for (int jj = 0; jj < j; ++jj) base += __popc(hdr[2 * jj] | hdr[2 * jj + 1]);
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      uint32_t m = NS == 1 ? um : (s == 0 ? g0 : g1);
+      while (m) {
+        const int kk = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t row = base + (NS == 1 ? 0u : (uint32_t)__popc(um & ((1u << kk) - 1u)));
+        const float4 av = *reinterpret_cast<const float4*>(&S.at[kk][4 * lane]);
+        float2 b[SPAN / 2];
+#pragma unroll
+        for (int q = 0; q < SPAN / 4; ++q) {
+          const float4 bv = S.rows[row][s * (SPAN / 4) + q];
+          b[2 * q] = make_float2(bv.x, bv.y);
+          b[2 * q + 1] = make_float2(bv.z, bv.w);
+        }
+        if (NS == 1) ++base;
+        const float a4[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if (a4[r] != 0.0f) {
+            const float2 a2 = make_float2(a4[r], a4[r]);
+#pragma unroll
+            for (int q = 0; q < SPAN / 2; ++q) acc[s][r][q] = __ffma2_rn(a2, b[q], acc[s][r][q]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) s2_arrive(&sh.empty[st]);
+  }
+
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int64_t row = m0 + 4 * lane + r;
+    if (!slice_ok || row >= M) continue;
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+#pragma unroll
+      for (int q = 0; q < SPAN / 2; ++q)
+        *reinterpret_cast<float2*>(C + row * ldc + ncol + s * SPAN + 2 * q) = acc[s][r][q];
+  }
+}
+
 }  // namespace mmmcu

@@ -73,10 +73,10 @@ struct mmmcu_ctx {
   DevBuf codes, bgrp, zb;
   DevBuf ctl;
 
-  // ---- K2-TC operands (built by K1 when the TC path may run: algo AUTO or TC)
-  bool tc_a = false, tc_b = false;
+  // ---- K2 operands emitted by K1 (which ones depends on the algorithm, see ops_for)
+  bool op_at = false, op_rows = false, op_items = false;
   int64_t kpad = 0, m_at = 0, n_tb = 0;
-  DevBuf at, items, meta, item_off;
+  DevBuf at, items, meta, item_off, brows, row_off;
 
   // ---- statistics: u64 [16] = {inv, lanes, skipped, zreg, nnzA, pop, zero_codes, span, slice_nz}
   DevBuf stats;
@@ -148,8 +148,18 @@ int64_t n_row_tiles(int64_t M) { return (M + mmmcu::kK1Rows - 1) / mmmcu::kK1Row
 unsigned long long* zb_slice(mmmcu_ctx* ctx) { return ctx->zb.as<unsigned long long>(); }
 uint32_t* zb_bpop(mmmcu_ctx* ctx) { return reinterpret_cast<uint32_t*>(ctx->zb.as<unsigned long long>() + 1); }
 uint32_t* zb_bnz(mmmcu_ctx* ctx) { return zb_bpop(ctx) + ctx->Kb; }
+// Operand sets K1 emits for K2: A^T tiles (SIMT v2, TC), raw B rows (SIMT v2), tf32 B items (TC).
+enum { OP_AT = 1, OP_ROWS = 2, OP_ITEMS = 4 };
+int ops_for(const mmmcu_ctx* ctx) {
+  switch (ctx->algo) {
+    case MMMCU_ALGO_TC: return OP_AT | OP_ITEMS;
+    case MMMCU_ALGO_DENSE: return 0;
+    default: return OP_AT | OP_ROWS;
+  }
+}
+int64_t n_cnt_b(const mmmcu_ctx* ctx) { return ctx->n_tb * ((ctx->Kb + 31) / 32); }
 uint32_t* zb_item_cnt(mmmcu_ctx* ctx) { return zb_bnz(ctx) + ctx->Kb; }
-bool want_tc(const mmmcu_ctx* ctx) { return ctx->algo == MMMCU_ALGO_AUTO || ctx->algo == MMMCU_ALGO_TC; }
+uint32_t* zb_row_cnt(mmmcu_ctx* ctx) { return zb_item_cnt(ctx) + ((ops_for(ctx) & OP_ITEMS) ? n_cnt_b(ctx) : 0); }
 
 mmmcu_status stage_a(mmmcu_ctx* ctx, const float* A, int64_t M, int64_t K, int64_t lda, uint64_t av) {
   if (M <= 0 || K <= 0) return fail(ctx, MMMCU_ERR_INVALID_ARG, "matrix dimensions must be positive");
@@ -165,8 +175,8 @@ mmmcu_status stage_a(mmmcu_ctx* ctx, const float* A, int64_t M, int64_t K, int64
   MMMCU_CUDA(ctx->row_ptr.ensure(sizeof(int64_t) * (M + 1)));
   MMMCU_CUDA(ctx->cols.ensure((size_t)ctx->csr_idx_bytes * M * K));
   MMMCU_CUDA(cudaMemsetAsync(ctx->za.p, 0, sizeof(uint32_t) * (M + K + n_row_tiles(M)), ctx->stream));
-  ctx->tc_a = false;
-  if (want_tc(ctx)) {
+  ctx->op_at = false;
+  if (ops_for(ctx) & OP_AT) {
     ctx->kpad = round_up(K, 32);
     ctx->m_at = round_up(M, 128);
     MMMCU_CUDA(ctx->at.ensure(sizeof(float) * ctx->m_at * ctx->kpad));
@@ -190,18 +200,25 @@ mmmcu_status stage_b(mmmcu_ctx* ctx, const float* B, int64_t K, int64_t N, int64
   ctx->has_b = false;
   MMMCU_CUDA(ctx->codes.ensure((size_t)K * nreg));
   MMMCU_CUDA(ctx->bgrp.ensure(sizeof(uint32_t) * ngrp * kw));
-  ctx->tc_b = false;
+  ctx->op_rows = ctx->op_items = false;
+  const int ops = ops_for(ctx);
   const int64_t n_tb = (ldb + 255) / 256;
-  const int64_t n_cnt = want_tc(ctx) ? n_tb * kw : 0;
-  const size_t zb_bytes = sizeof(unsigned long long) + sizeof(uint32_t) * (2 * K + n_cnt);
+  const int64_t n_cnt = n_tb * kw;
+  const int64_t n_extra = ((ops & OP_ITEMS) ? n_cnt : 0) + ((ops & OP_ROWS) ? n_cnt : 0);
+  const size_t zb_bytes = sizeof(unsigned long long) + sizeof(uint32_t) * (2 * K + n_extra);
   MMMCU_CUDA(ctx->zb.ensure(zb_bytes));
   MMMCU_CUDA(cudaMemsetAsync(ctx->zb.p, 0, zb_bytes, ctx->stream));
-  if (want_tc(ctx)) {
+  ctx->n_tb = n_tb;
+  if (ops & OP_ITEMS) {
     // worst case 64 items (16 slices x 4) per (256-column tile, 32-k chunk): 2x B's bytes
-    ctx->n_tb = n_tb;
     MMMCU_CUDA(ctx->item_off.ensure(sizeof(int64_t) * (n_cnt + 1)));
     MMMCU_CUDA(ctx->items.ensure((size_t)n_cnt * 64 * 1024));
     MMMCU_CUDA(ctx->meta.ensure((size_t)n_cnt * 64 * 16));
+  }
+  if (ops & OP_ROWS) {
+    // worst case 2 header + 16 x 32 rows of 64 B per (tile, chunk): ~B's bytes
+    MMMCU_CUDA(ctx->row_off.ensure(sizeof(int64_t) * (n_cnt + 1)));
+    MMMCU_CUDA(ctx->brows.ensure((size_t)n_cnt * (2 + 16 * 32) * 64));
   }
   ctx->B = B;
   ctx->Kb = K;
@@ -223,7 +240,8 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   const bool same_k = a_valid && b_valid && ctx->Ka == ctx->Kb;
   const int64_t K = do_a ? ctx->Ka : ctx->Kb;
   const int64_t kw = (K + 31) / 32;
-  const bool tc_a = do_a && want_tc(ctx), tc_b = do_b && want_tc(ctx);
+  const int ops = ops_for(ctx);
+  const bool tc_a = do_a && (ops & OP_AT), items_b = do_b && (ops & OP_ITEMS), rows_b = do_b && (ops & OP_ROWS);
   const int64_t a_tx = (ctx->Ka + mmmcu::kK1Cols - 1) / mmmcu::kK1Cols;
   const int64_t a_rows = tc_a ? ctx->m_at : ctx->M;  // A^T tiles are written to the 128-row boundary
   const int64_t nA = do_a ? a_tx * ((a_rows + mmmcu::kK1Rows - 1) / mmmcu::kK1Rows) : 0;
@@ -242,8 +260,10 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   z.at = tc_a ? ctx->at.as<float>() : nullptr;
   z.kpad = ctx->kpad;
   z.m_at = ctx->m_at;
-  z.item_cnt = tc_b ? zb_item_cnt(ctx) : nullptr;
-  z.item_off = tc_b ? ctx->item_off.as<int64_t>() : nullptr;
+  z.item_cnt = items_b ? zb_item_cnt(ctx) : nullptr;
+  z.item_off = items_b ? ctx->item_off.as<int64_t>() : nullptr;
+  z.row_cnt = rows_b ? zb_row_cnt(ctx) : nullptr;
+  z.row_off = rows_b ? ctx->row_off.as<int64_t>() : nullptr;
   z.n_tb = ctx->n_tb;
   const int has_a = a_valid && (same_k || !b_valid) ? 1 : 0;
   const int has_b = b_valid && (same_k || !a_valid) ? 1 : 0;
@@ -264,7 +284,14 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
                                                                ctx->row_ptr.as<int64_t>(), ctx->cols.as<uint32_t>());
     MMMCU_LAUNCHED();
   }
-  if (tc_b) {
+  if (rows_b) {
+    dim3 grid((unsigned)((ctx->Kb + 31) / 32), (unsigned)ctx->n_tb);
+    mmmcu::k1_pack_rows<<<grid, mmmcu::kPackThreads, 0, ctx->stream>>>(
+        ctx->B, ctx->Kb, ctx->ldb, ctx->bgrp.as<uint32_t>(), (ctx->Kb + 31) / 32, ctx->row_off.as<int64_t>(),
+        ctx->brows.as<uint4>());
+    MMMCU_LAUNCHED();
+  }
+  if (items_b) {
     MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k1_pack_b, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     dim3 grid((unsigned)((ctx->Kb + 31) / 32), (unsigned)ctx->n_tb);
     mmmcu::k1_pack_b<<<grid, mmmcu::kPackThreads, 64 * 1024, ctx->stream>>>(
@@ -274,11 +301,12 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   }
   if (do_a) {
     ctx->has_a = true;
-    ctx->tc_a = tc_a;
+    ctx->op_at = tc_a;
   }
   if (do_b) {
     ctx->has_b = true;
-    ctx->tc_b = tc_b;
+    ctx->op_items = items_b;
+    ctx->op_rows = rows_b;
   }
   return MMMCU_OK;
 }
@@ -299,6 +327,27 @@ mmmcu_status check_plan(mmmcu_ctx* ctx, const float* A, const float* B, uint64_t
 mmmcu_status launch_simt(mmmcu_ctx* ctx, float* C, int64_t ldc, int span_hint) {
   const int64_t M = ctx->M, K = ctx->Ka, Np = round_up(ctx->N, 64);
   const int64_t kw = (K + 31) / 32;
+  const unsigned long long* sel2 = span_hint == 0 ? ctx->stats.as<unsigned long long>() + 7 : nullptr;
+  if (ctx->op_at && ctx->op_rows) {
+    const int smem = mmmcu::kS2SmemBase + (int)(sizeof(int64_t) * (kw + 1));
+    if (smem > 232448) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "K too large for the SIMT v2 kernel");
+    const int64_t row_tiles = ctx->m_at / 128;
+    if (row_tiles > 65535) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "M larger than 8388480 rows");
+    dim3 grid((unsigned)((Np + 255) / 256), (unsigned)row_tiles);
+    if (span_hint == 0 || span_hint == 8) {
+      MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k2_simt2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      mmmcu::k2_simt2<8><<<grid, mmmcu::kS2Threads, smem, ctx->stream>>>(
+          ctx->at.as<float>(), ctx->kpad, ctx->brows.as<float4>(), ctx->row_off.as<int64_t>(), kw, C, ldc, M, Np, sel2);
+      MMMCU_LAUNCHED();
+    }
+    if (span_hint == 0 || span_hint == 16) {
+      MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k2_simt2<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      mmmcu::k2_simt2<16><<<grid, mmmcu::kS2Threads, smem, ctx->stream>>>(
+          ctx->at.as<float>(), ctx->kpad, ctx->brows.as<float4>(), ctx->row_off.as<int64_t>(), kw, C, ldc, M, Np, sel2);
+      MMMCU_LAUNCHED();
+    }
+    return MMMCU_OK;
+  }
   const int64_t row_tiles = (M + mmmcu::kK2TM - 1) / mmmcu::kK2TM;
   if (row_tiles > 65535) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "M larger than 8388480 rows");
   dim3 grid((unsigned)((Np + mmmcu::kK2TN - 1) / mmmcu::kK2TN), (unsigned)row_tiles);
@@ -367,7 +416,8 @@ mmmcu_status mmmcu_ctx_destroy(mmmcu_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : {&ctx->abits, &ctx->za, &ctx->tile_prefix, &ctx->row_ptr, &ctx->cols, &ctx->codes, &ctx->bgrp, &ctx->zb,
-                    &ctx->ctl, &ctx->at, &ctx->items, &ctx->meta, &ctx->item_off, &ctx->stats, &ctx->hA, &ctx->hB, &ctx->hC, &ctx->scratch0, &ctx->scratch1})
+                    &ctx->ctl, &ctx->at, &ctx->items, &ctx->meta, &ctx->item_off, &ctx->brows, &ctx->row_off,
+                    &ctx->stats, &ctx->hA, &ctx->hB, &ctx->hC, &ctx->scratch0, &ctx->scratch1})
     b->release();
   delete ctx;
   return MMMCU_OK;
@@ -542,7 +592,7 @@ mmmcu_status mmmcu_multiply(mmmcu_ctx* ctx, float* C, int64_t ldc, const float* 
     return fail(ctx, MMMCU_ERR_INVALID_ARG,
                 "C must be 16-byte aligned with ldc >= round_up(N, 64) (Matrix padding) and ldc % 4 == 0");
   if (ctx->algo == MMMCU_ALGO_TC) {
-    if (!ctx->tc_a || !ctx->tc_b)
+    if (!ctx->op_at || !ctx->op_items)
       return fail(ctx, MMMCU_ERR_NOT_READY, "the TC operands were not built: preprocess with algo AUTO or TC");
     ctx->last_algo = MMMCU_ALGO_TC;
     const int64_t Np = round_up(ctx->N, 64), kw = (ctx->Ka + 31) / 32;

