@@ -180,6 +180,18 @@ mmmcu_status mmmcu_multiply_host(mmmcu_ctx* ctx, float* C_host, int64_t ldc, con
                                  int64_t lda, const float* B_host, int64_t ldb, int64_t M,
                                  int64_t K, int64_t N, mmmcu_counters* counters);
 
+/*
+ * Plan-owning host path used by the C++ drop-in (include/mmm_cuda.hpp): copy host A and B
+ * (reference Matrix<float> layout) into context-owned device buffers and preprocess them;
+ * later multiplies of that plan check the operands' content versions and
+ * move only C.
+ */
+mmmcu_status mmmcu_preprocess_host(mmmcu_ctx* ctx, const float* A_host, int64_t M, int64_t K, int64_t lda,
+                                   const float* B_host, int64_t N, int64_t ldb, mmmcu_lane lane,
+                                   uint64_t a_version, uint64_t b_version);
+mmmcu_status mmmcu_multiply_planned_host(mmmcu_ctx* ctx, float* C_host, int64_t ldc, uint64_t a_version,
+                                         uint64_t b_version, int worker_count, mmmcu_counters* counters);
+
 /* ---- synthetic inputs (device generator; matgen.hpp analogue for BASELINE.json) ------ */
 
 /*

@@ -184,14 +184,24 @@ int orc_ref_generate(float* out, int64_t rows, int64_t cols, int64_t ld, int str
  * The product's device generator (mmmcu_generate) implements the same formulas; tests
  * check the two agree bit for bit on the uniform/mask modes.
  */
+int orc_gen_iid_rows(float* out, int64_t rows, int64_t cols, int64_t ld, int64_t row0, uint64_t seed,
+                     int value_kind, double sigma, double thresh, int mask_kind, double p, int64_t block);
+
 int orc_gen_iid(float* out, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, int value_kind,
                 double sigma, double thresh, int mask_kind, double p, int64_t block) {
+  return orc_gen_iid_rows(out, rows, cols, ld, 0, seed, value_kind, sigma, thresh, mask_kind, p, block);
+}
+
+/* Same, for global rows [row0, row0 + rows) of the matrix the seed defines (row shards). */
+int orc_gen_iid_rows(float* out, int64_t rows, int64_t cols, int64_t ld, int64_t row0, uint64_t seed,
+                     int value_kind, double sigma, double thresh, int mask_kind, double p, int64_t block) {
   if (rows <= 0 || cols <= 0 || ld < cols) return -1;
   if (mask_kind == 2 && block <= 0) return -1;
   const double two_pi = 6.283185307179586476925286766559;
 #pragma omp parallel for schedule(static)
-  for (int64_t i = 0; i < rows; ++i) {
-    float* r = out + i * ld;
+  for (int64_t li = 0; li < rows; ++li) {
+    float* r = out + li * ld;
+    const int64_t i = row0 + li;
     for (int64_t j = cols; j < ld; ++j) r[j] = 0.0f;
     for (int64_t j = 0; j < cols; ++j) {
       int zero = 0;

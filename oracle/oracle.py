@@ -59,6 +59,9 @@ def lib():
         L.orc_gen_iid.restype = c_int
         L.orc_gen_iid.argtypes = [c_void_p, c_int64, c_int64, c_int64, c_uint64, c_int, c_double, c_double, c_int,
                                   c_double, c_int64]
+        L.orc_gen_iid_rows.restype = c_int
+        L.orc_gen_iid_rows.argtypes = [c_void_p, c_int64, c_int64, c_int64, c_int64, c_uint64, c_int, c_double,
+                                       c_double, c_int, c_double, c_int64]
         L.orc_region_fma.restype = c_int
         L.orc_region_fma.argtypes = [c_uint32, c_int, c_int, c_void_p, ctypes.c_float, c_void_p]
         L.orc_pattern_codes.restype = c_int
@@ -137,10 +140,11 @@ def ref_generate(rows, cols, structure="random", target=0.0, block_len=0, seed=0
     return out
 
 
-def gen_iid(rows, cols, seed, value_kind=0, sigma=1.0, thresh=0.0, mask_kind=0, p=0.0, block=1, ld=None):
+def gen_iid(rows, cols, seed, value_kind=0, sigma=1.0, thresh=0.0, mask_kind=0, p=0.0, block=1, ld=None, row0=0):
     ld = cols if ld is None else ld
     out = np.zeros((rows, ld), dtype=np.float32)
-    if lib().orc_gen_iid(_p(out), rows, cols, ld, seed, value_kind, sigma, thresh, mask_kind, p, block) != 0:
+    if lib().orc_gen_iid_rows(_p(out), rows, cols, ld, row0, seed, value_kind, sigma, thresh, mask_kind, p,
+                              block) != 0:
         raise ValueError("invalid generator arguments")
     return out
 

@@ -84,6 +84,10 @@ SIGNATURES = [
                                c_double,
                                c_int, c_double, c_int64]),
     ("mmmcu_shard_rows", c_int, [c_int64, c_int, c_int, POINTER(c_int64), POINTER(c_int64)]),
+    ("mmmcu_preprocess_host", c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int64, Lane,
+                                      c_uint64, c_uint64]),
+    ("mmmcu_multiply_planned_host", c_int, [c_void_p, c_void_p, c_int64, c_uint64, c_uint64, c_int,
+                                            POINTER(Counters)]),
 ]
 
 _lib = None

@@ -45,6 +45,19 @@ def build_probe() -> str:
     return out
 
 
+def build_dropin_test() -> str:
+    """C++ drop-in check (tests/cpp/dropin_test.cpp) against the reference's own headers; only
+    where /root/reference exists (the binary then travels with the repo snapshot)."""
+    ref_inc = "/root/reference/proj/include"
+    out = os.path.join(HERE, "_lib", "dropin_test")
+    if not os.path.isdir(ref_inc):
+        return ""
+    _run(["g++", "-std=c++20", "-O2", "-I", ref_inc, "-I", os.path.join(ROOT, "include"),
+          os.path.join(ROOT, "tests", "cpp", "dropin_test.cpp"), "-L", os.path.join(HERE, "_lib"), "-lmmmcu",
+          "-Wl,-rpath,$ORIGIN", "-o", out])
+    return out
+
+
 def build_oracle() -> None:
     env_make = ["make", "-C", os.path.join(ROOT, "oracle")]
     _run(env_make)
@@ -55,6 +68,7 @@ def build_oracle() -> None:
 def main(argv=None):
     build_lib()
     build_probe()
+    build_dropin_test()
     build_oracle()
 
 

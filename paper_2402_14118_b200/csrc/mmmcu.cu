@@ -660,6 +660,41 @@ mmmcu_status mmmcu_multiply_host(mmmcu_ctx* ctx, float* C_host, int64_t ldc, con
   return fill_counters(ctx, counters);
 }
 
+mmmcu_status mmmcu_preprocess_host(mmmcu_ctx* ctx, const float* A_host, int64_t M, int64_t K, int64_t lda,
+                                   const float* B_host, int64_t N, int64_t ldb, mmmcu_lane lane, uint64_t av,
+                                   uint64_t bv) {
+  MMMCU_TRY(bind(ctx));
+  MMMCU_TRY(check_lane(ctx, lane));
+  if (M <= 0 || K <= 0 || N <= 0) return fail(ctx, MMMCU_ERR_INVALID_ARG, "matrix dimensions must be positive");
+  if (!A_host || !B_host) return fail(ctx, MMMCU_ERR_INVALID_ARG, "null operand");
+  if (lda < K || ldb < N) return fail(ctx, MMMCU_ERR_DIM_MISMATCH, "leading dimension smaller than the row");
+  MMMCU_CUDA(ctx->hA.ensure(sizeof(float) * M * lda));
+  MMMCU_CUDA(ctx->hB.ensure(sizeof(float) * K * ldb));
+  MMMCU_CUDA(cudaMemcpyAsync(ctx->hA.p, A_host, sizeof(float) * M * lda, cudaMemcpyHostToDevice, ctx->stream));
+  MMMCU_CUDA(cudaMemcpyAsync(ctx->hB.p, B_host, sizeof(float) * K * ldb, cudaMemcpyHostToDevice, ctx->stream));
+  MMMCU_TRY(mmmcu_preprocess(ctx, ctx->hA.as<float>(), M, K, lda, ctx->hB.as<float>(), N, ldb, lane, av, bv));
+  MMMCU_CUDA(cudaStreamSynchronize(ctx->stream));  // the host buffers may change after return
+  return MMMCU_OK;
+}
+
+mmmcu_status mmmcu_multiply_planned_host(mmmcu_ctx* ctx, float* C_host, int64_t ldc, uint64_t av, uint64_t bv,
+                                         int worker_count, mmmcu_counters* counters) {
+  MMMCU_TRY(bind(ctx));
+  if (worker_count <= 0) return fail(ctx, MMMCU_ERR_WORKERS, "worker_count must be positive");
+  if (!C_host) return fail(ctx, MMMCU_ERR_INVALID_ARG, "C is null");
+  if (!ctx->has_a || !ctx->has_b || ctx->A != ctx->hA.as<float>() || ctx->B != ctx->hB.as<float>())
+    return fail(ctx, MMMCU_ERR_NOT_READY, "no host-operand plan: call mmmcu_preprocess_host first");
+  if (av != ctx->av || bv != ctx->bv)
+    return fail(ctx, MMMCU_ERR_STALE, "stale context: operands changed since preprocessing (Matrix::version)");
+  const int64_t M = ctx->M;
+  MMMCU_CUDA(ctx->hC.ensure(sizeof(float) * M * ldc));
+  MMMCU_CUDA(cudaMemcpyAsync(ctx->hC.p, C_host, sizeof(float) * M * ldc, cudaMemcpyHostToDevice, ctx->stream));
+  MMMCU_TRY(mmmcu_multiply(ctx, ctx->hC.as<float>(), ldc, ctx->A, ctx->B, av, bv, nullptr));
+  MMMCU_CUDA(cudaMemcpyAsync(C_host, ctx->hC.p, sizeof(float) * M * ldc, cudaMemcpyDeviceToHost, ctx->stream));
+  MMMCU_CUDA(cudaStreamSynchronize(ctx->stream));
+  return fill_counters(ctx, counters);
+}
+
 mmmcu_status mmmcu_generate(mmmcu_ctx* ctx, float* out, int64_t rows, int64_t cols, int64_t ld, int64_t row0, uint64_t seed,
                             int value_kind, double sigma, double thresh, int mask_kind, double p, int64_t block) {
   MMMCU_TRY(bind(ctx));

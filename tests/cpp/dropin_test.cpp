@@ -1,0 +1,107 @@
+// Drop-in check: a reference-style caller (SPEC engine API over the reference's own
+// Matrix<float> / generate<float>, /root/reference/proj/include) switched to
+// include/mmm_cuda.hpp.  Built by paper_2402_14118_b200/build.py when the reference headers
+// are present; run on the GPU by tests/test_gpu_parity.py::test_cpp_dropin.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
+#include "mmm/matgen.hpp"
+#include "mmm_cuda.hpp"
+
+using namespace mmm;
+
+#define CHECK(cond)                                                          \
+  do {                                                                       \
+    if (!(cond)) {                                                           \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);            \
+      std::exit(1);                                                          \
+    }                                                                        \
+  } while (0)
+
+int main() {
+  const int64_t M = 300, K = 520, N = 320;
+  SparsitySpec sa{Structure::random, 0.8, 0, 11};
+  SparsitySpec sb{Structure::block_random, 0.8, 16, 12};
+  Matrix<float> a = generate<float>(M, K, sa);
+  Matrix<float> b = generate<float>(K, N, sb);
+
+  // oracle: ascending-k fmaf chain over the non-zero A entries and non-zero 8-wide B groups
+  Matrix<float> ref(M, N);
+  uint64_t lanes = 0;
+  for (int64_t i = 0; i < M; ++i)
+    for (int64_t k = 0; k < K; ++k) {
+      const float av = a.at(i, k);
+      if (av == 0.0f) continue;
+      for (int64_t g = 0; g < b.padded_cols(); g += 8) {
+        bool nz = false;
+        for (int l = 0; l < 8; ++l) nz |= b.row(k)[g + l] != 0.0f;
+        if (!nz) continue;
+        lanes += 8;
+        for (int l = 0; l < 8 && g + l < N; ++l) ref.row(i)[g + l] = std::fma(av, b.row(k)[g + l], ref.row(i)[g + l]);
+      }
+    }
+
+  MmmContext<float> ctx(a, b);
+  Matrix<float> c(M, N);
+  WorkCounters w = multiply_mmm(ctx, c, a, b);
+  CHECK(w.lane_fma_ops == lanes);
+  CHECK(w.rows_skipped + (uint64_t)((1.0 - elementwise_sparsity(a)) * M * K + 0.5) == (uint64_t)(M * K));
+  for (int64_t i = 0; i < M; ++i)
+    for (int64_t j = 0; j < N; ++j) CHECK(c.at(i, j) == ref.at(i, j));  // bit-exact (K2-SIMT)
+  CHECK(c.padding_is_zero());
+
+  // multiply_parallel: same bits, worker_count 0 rejected
+  Matrix<float> c2(M, N);
+  WorkCounters w2 = multiply_parallel(ctx, c2, a, b, 8);
+  CHECK(w2.lane_fma_ops == w.lane_fma_ops);
+  bool threw = false;
+  try {
+    multiply_parallel(ctx, c2, a, b, 0);
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  CHECK(threw);
+
+  // stale context: any mutable access bumps Matrix::version
+  a.at(0, 0) = 1.0f;
+  threw = false;
+  try {
+    multiply_mmm(ctx, c, a, b);
+  } catch (const StaleContextError&) {
+    threw = true;
+  }
+  CHECK(threw);
+
+  // bad lane config: the reference's KernelTable::build message (kernel_table.cpp:66-67)
+  threw = false;
+  try {
+    MmmContext<float> bad(a, b, LaneConfig{8, 17, 1});
+  } catch (const std::invalid_argument& e) {
+    threw = std::string(e.what()).find("pattern size must lie in [1, 16]") != std::string::npos;
+  }
+  CHECK(threw);
+
+  // preprocess_b / plan_stats / preprocess_a
+  std::vector<BPlan> plans = preprocess_b(b, LaneConfig::defaults(Dtype::f32), 256);
+  CHECK(plans.size() == 6);  // ceil(520/256) = 3 leaf rows x ceil(5 regions / 4) = 2 leaf cols
+  PlanStats st = plan_stats(plans);
+  CHECK(st.region_count == K * (b.padded_cols() / 64));
+  ABlockIndex idx = preprocess_a(a, 256);
+  int64_t nnz = 0;
+  for (uint8_t cnt : idx.counts) nnz += cnt;
+  int64_t direct = 0;
+  for (int64_t i = 0; i < M; ++i)
+    for (int64_t k = 0; k < K; ++k) direct += a.at(i, k) != 0.0f;
+  CHECK(nnz == direct);
+
+  // multiply_simple: dense fmaf chain == masked chain on finite data
+  Matrix<float> c3(M, N);
+  Matrix<float> a2 = generate<float>(M, K, sa);
+  multiply_simple(c3, a2, b);
+  for (int64_t i = 0; i < M; ++i)
+    for (int64_t j = 0; j < N; ++j) CHECK(c3.at(i, j) == ref.at(i, j));
+
+  std::printf("DROPIN OK lane_fma_ops=%llu\n", (unsigned long long)w.lane_fma_ops);
+  return 0;
+}

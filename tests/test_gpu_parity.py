@@ -325,3 +325,17 @@ def test_tc_accumulate(ctx):
     Cr, _ = run_oracle(A, B, C0=C0)
     den = np.abs(A[:, :K]).astype(np.float64) @ np.abs(B).astype(np.float64) + np.abs(C0).astype(np.float64)
     assert (np.abs(C.astype(np.float64) - Cr) <= TOL * den).all()
+
+
+def test_cpp_dropin(ctx):
+    # the reference-side C++ caller (SPEC engine API on the reference's Matrix<float>) linked
+    # against libmmmcu.so through include/mmm_cuda.hpp
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(N.LIB_PATH), "dropin_test")
+    if not os.path.exists(exe):
+        pytest.skip("dropin_test not built (needs the reference headers at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "DROPIN OK" in out.stdout
