@@ -61,7 +61,7 @@ struct K1Scratch {
   int64_t n_tb;           // 256-column tiles of B
   // K2-SIMT operand: raw non-zero B block rows per (256-column tile, chunk)
   uint32_t* row_cnt;      // [n_tb][kw] non-zero (k, 16-column slice) rows (zeroed)
-  int64_t* row_off;       // [n_tb * kw + 1] exclusive prefix of (row_cnt + 2 header rows), 64-byte units
+  int64_t* row_off;       // [n_tb * kw + 1] exclusive prefix of (row_cnt + 3 header rows), 64-byte units
 };
 
 // --------------------------------------------------------------------------- A tile
@@ -262,7 +262,7 @@ k1_pass(const float* __restrict__ A, int64_t M, int64_t K, int64_t lda, uint32_t
   if (threadIdx.x == 0) *z.done = 0u;  // ready for the next launch (no other CTA is left)
   k1_finalize_block(z.acol, z.bpop, z.bnz, K, M, nreg, has_a, has_b, z.slice_nz, stats);
   if (z.item_cnt && nB > 0) k1_block_exclusive_scan(z.item_cnt, z.n_tb * kw, 0, z.item_off);
-  if (z.row_cnt && nB > 0) k1_block_exclusive_scan(z.row_cnt, z.n_tb * kw, 2, z.row_off);
+  if (z.row_cnt && nB > 0) k1_block_exclusive_scan(z.row_cnt, z.n_tb * kw, 3, z.row_off);
   if (nA > 0) {  // exclusive prefix of the 32-row tile sums for k1_csr's row_ptr
     __shared__ int64_t carry;
     __shared__ int64_t wsum[kK1Threads / 32];
@@ -511,8 +511,9 @@ k1_pack_b(const float* __restrict__ B, int64_t K, int64_t ldb, const uint32_t* _
 
 // ----------------------------------------------------------- B rows for K2-SIMT
 // For each 256-column tile tb and 32-k chunk c, a contiguous record at row_off[tb*kw + c]
-// (64-byte units): 2 header rows = the 32 group k-masks of the tile's 8-column groups
-// (uint32 each, bit kk <-> k = 32c + kk), then for slice j = 0..15 (16 columns = groups
+// (64-byte units): 3 header rows = the 32 group k-masks of the tile's 8-column groups
+// (uint32 each, bit kk <-> k = 32c + kk) and the 16 slices' first record rows, then for
+// slice j = 0..15 (16 columns = groups
 // 2j, 2j+1) and every k of the chunk with a non-zero block in the slice, ascending, the
 // raw 16 floats B[k][16j .. 16j+15].  K2-SIMT moves each record with one bulk copy.
 __global__ void __launch_bounds__(kPackThreads)
@@ -541,6 +542,10 @@ k1_pack_rows(const float* __restrict__ B, int64_t K, int64_t ldb, const uint32_t
   __syncthreads();
   uint4* out = rows + row_off[tb * kw + c] * 4;
   if (tid < 8) out[tid] = make_uint4(s_g[4 * tid], s_g[4 * tid + 1], s_g[4 * tid + 2], s_g[4 * tid + 3]);
+  if (tid >= 8 && tid < 12) {  // header row 2: first record row of each slice
+    const int q = 4 * (tid - 8);
+    out[tid] = make_uint4(3 + s_base[q], 3 + s_base[q + 1], 3 + s_base[q + 2], 3 + s_base[q + 3]);
+  }
   const uint32_t total = s_base[16];
   for (uint32_t p = tid; p < total * 4; p += kPackThreads) {
     const uint32_t t = p >> 2, q = p & 3;
@@ -550,7 +555,7 @@ k1_pack_rows(const float* __restrict__ B, int64_t K, int64_t ldb, const uint32_t
     for (uint32_t d = t - s_base[j]; d; --d) m &= m - 1;
     const int kk = __ffs(m) - 1;
     const float4 v = ldg_stream(B + (k0 + kk) * ldb + n0 + 16 * j + 4 * q);
-    out[8 + p] = make_uint4(__float_as_uint(v.x), __float_as_uint(v.y), __float_as_uint(v.z), __float_as_uint(v.w));
+    out[12 + p] = make_uint4(__float_as_uint(v.x), __float_as_uint(v.y), __float_as_uint(v.z), __float_as_uint(v.w));
   }
 }
 

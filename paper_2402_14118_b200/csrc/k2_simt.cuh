@@ -288,9 +288,12 @@ k2_dense(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, 
 // K2-SIMT v2 — the same exact computation, fed by bulk async copies of K1's MMA-ready
 // operands (A^T per 128-row tile, raw non-zero B block rows per (256-column tile, chunk)).
 //
-//   CTA   = 128 rows x 256 columns of C, 16 compute warps (one 16-column slice each) +
-//           1 producer warp; 4 smem stages of {A^T chunk [32 k][128 rows] (16 KB),
-//           B record: 2 header rows (32 group k-masks) + the chunk's non-zero slice rows}.
+//   CTA   = 128 rows x 256 columns of C, 16 compute warps (one 16-column slice each).  A 17th
+//           producer warp would put 5 warps on one SMSP and cap registers at 96, which
+//           serialises the B loads; instead the LAST warp to finish a chunk refills its
+//           stage (shared counter, acq_rel).  4 smem stages of {A^T chunk [32 k][128 rows],
+//           B record: 3 header rows (32 group k-masks, 16 slice offsets) + the chunk's
+//           non-zero slice rows}.
 //   lane  = rows 4l .. 4l+3 of the tile x the warp's 16 columns (64 fp32 accumulators,
 //           initialised from C).  Per non-zero B row k of its slice the warp issues one
 //           conflict-free LDS.128 of the 4 A values, 4 broadcast LDS.128 of B[k][slice] and
@@ -299,19 +302,19 @@ k2_dense(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, 
 //           8: one walk per 8-column group over its own mask (exact group skipping).
 // ====================================================================================
 constexpr int kS2Warps = 16;
-constexpr int kS2Threads = (kS2Warps + 1) * 32;
+constexpr int kS2Threads = kS2Warps * 32;  // no producer warp: 4 warps/SMSP keep 128 registers
 constexpr int kS2Stages = 4;
 constexpr int kS2KC = 32;
-constexpr int kS2MaxRows = 2 + 16 * kS2KC;  // header + every (k, slice) of a chunk
+constexpr int kS2MaxRows = 3 + 16 * kS2KC;  // header + every (k, slice) of a chunk
 
 struct alignas(128) S2Stage {
   float at[kS2KC][128];          // 16 KB
-  float4 rows[kS2MaxRows][4];    // 32.8 KB: header (2 rows) + B block rows
+  float4 rows[kS2MaxRows][4];    // 33 KB: header (3 rows) + B block rows
 };
 struct S2Shared {
   S2Stage st[kS2Stages];
   uint64_t full[kS2Stages];
-  uint64_t empty[kS2Stages];
+  uint32_t pend[kS2Stages];  // warps done with the stage's current chunk
   // followed by the tile's chunk offsets (int64, kw + 1), dynamic
 };
 constexpr int kS2SmemBase = (int)sizeof(S2Shared) + 128;
@@ -362,26 +365,22 @@ k2_simt2(const float* __restrict__ AT, int64_t kpad, const float4* __restrict__ 
   if (tid == 0) {
     for (int s = 0; s < kS2Stages; ++s) {
       s2_init(&sh.full[s], 1);
-      s2_init(&sh.empty[s], kS2Warps);
+      sh.pend[s] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  if (warp == kS2Warps) {
-    // ------------------------------------------------------------------ producer
-    if (lane == 0) {
-      for (int64_t c = 0; c < kw; ++c) {
-        const int s = (int)(c % kS2Stages);
-        if (c >= kS2Stages) s2_wait(&sh.empty[s], (uint32_t)(((c / kS2Stages) - 1) & 1));
-        const uint32_t nrows = (uint32_t)(offs[c + 1] - offs[c]);
-        s2_expect_tx(&sh.full[s], 16384u + nrows * 64u);
-        s2_bulk(&sh.st[s].at[0][0], AT + (rt * kpad + c * kS2KC) * 128, 16384u, &sh.full[s]);
-        s2_bulk(&sh.st[s].rows[0][0], brows + offs[c] * 4, nrows * 64u, &sh.full[s]);
-      }
-    }
-    return;
-  }
+  // chunk x lives in stage x % S: chunks 0..S-1 now, chunk x + S by the last warp done with x
+  auto issue = [&](int64_t x) {
+    const int s = (int)(x % kS2Stages);
+    const uint32_t nrows = (uint32_t)(offs[x + 1] - offs[x]);
+    s2_expect_tx(&sh.full[s], 16384u + nrows * 64u);
+    s2_bulk(&sh.st[s].at[0][0], AT + (rt * kpad + x * kS2KC) * 128, 16384u, &sh.full[s]);
+    s2_bulk(&sh.st[s].rows[0][0], brows + offs[x] * 4, nrows * 64u, &sh.full[s]);
+  };
+  if (tid == 0)
+    for (int64_t x = 0; x < kw && x < kS2Stages; ++x) issue(x);
 
   // -------------------------------------------------------------------- compute
   const int j = warp;                       // slice
@@ -407,25 +406,19 @@ k2_simt2(const float* __restrict__ AT, int64_t kpad, const float4* __restrict__ 
     const uint32_t* hdr = reinterpret_cast<const uint32_t*>(&S.rows[0][0]);
     const uint32_t g0 = hdr[2 * j], g1 = hdr[2 * j + 1];
     const uint32_t um = g0 | g1;
-    // first data row of this slice: 2 header rows + the rows of slices 0 .. j-1
-    uint32_t base = 2;
-    for (int jj = 0; jj < j; ++jj) base += __popc(hdr[2 * jj] | hdr[2 * jj + 1]);
+    uint32_t base = hdr[32 + j];  // first record row of this slice (header row 2)
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       uint32_t m = NS == 1 ? um : (s == 0 ? g0 : g1);
-      while (m) {
-        const int kk = __ffs(m) - 1;
-        m &= m - 1;
-        const uint32_t row = base + (NS == 1 ? 0u : (uint32_t)__popc(um & ((1u << kk) - 1u)));
-        const float4 av = *reinterpret_cast<const float4*>(&S.at[kk][4 * lane]);
+      // two non-zero B rows per iteration: both rows' loads are issued before the FMAs
+      // (ILP across k); FMAs stay in ascending k, so the per-element fmaf chain is unchanged
+      auto fma_row = [&](const float4& av, const float4 (&bq)[SPAN / 4]) {
         float2 b[SPAN / 2];
 #pragma unroll
         for (int q = 0; q < SPAN / 4; ++q) {
-          const float4 bv = S.rows[row][s * (SPAN / 4) + q];
-          b[2 * q] = make_float2(bv.x, bv.y);
-          b[2 * q + 1] = make_float2(bv.z, bv.w);
+          b[2 * q] = make_float2(bq[q].x, bq[q].y);
+          b[2 * q + 1] = make_float2(bq[q].z, bq[q].w);
         }
-        if (NS == 1) ++base;
         const float a4[4] = {av.x, av.y, av.z, av.w};
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
@@ -435,10 +428,41 @@ k2_simt2(const float* __restrict__ AT, int64_t kpad, const float4* __restrict__ 
             for (int q = 0; q < SPAN / 2; ++q) acc[s][r][q] = __ffma2_rn(a2, b[q], acc[s][r][q]);
           }
         }
+      };
+      while (m) {
+        const int k1 = __ffs(m) - 1;
+        m &= m - 1;
+        const bool two = m != 0;
+        const int k2 = two ? __ffs(m) - 1 : k1;
+        if (two) m &= m - 1;
+        const uint32_t r1 = base + (NS == 1 ? 0u : (uint32_t)__popc(um & ((1u << k1) - 1u)));
+        const uint32_t r2 = NS == 1 ? r1 + (two ? 1u : 0u) : base + (uint32_t)__popc(um & ((1u << k2) - 1u));
+        if (NS == 1) base += two ? 2u : 1u;
+        const float4 av1 = *reinterpret_cast<const float4*>(&S.at[k1][4 * lane]);
+        const float4 av2 = *reinterpret_cast<const float4*>(&S.at[k2][4 * lane]);
+        float4 b1[SPAN / 4], b2[SPAN / 4];
+#pragma unroll
+        for (int q = 0; q < SPAN / 4; ++q) {
+          b1[q] = S.rows[r1][s * (SPAN / 4) + q];
+          b2[q] = S.rows[r2][s * (SPAN / 4) + q];
+        }
+        fma_row(av1, b1);
+        if (two) fma_row(av2, b2);
       }
     }
     __syncwarp();
-    if (lane == 0) s2_arrive(&sh.empty[st]);
+    if (lane == 0) {
+      uint32_t old;
+      asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                   : "=r"(old)
+                   : "r"((uint32_t)__cvta_generic_to_shared(&sh.pend[st]))
+                   : "memory");
+      if (old == kS2Warps - 1) {  // every warp is done with stage st: refill it
+        sh.pend[st] = 0;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (c + kS2Stages < kw) issue(c + kS2Stages);
+      }
+    }
   }
 
 #pragma unroll

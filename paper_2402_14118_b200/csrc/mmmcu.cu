@@ -216,9 +216,9 @@ mmmcu_status stage_b(mmmcu_ctx* ctx, const float* B, int64_t K, int64_t N, int64
     MMMCU_CUDA(ctx->meta.ensure((size_t)n_cnt * 64 * 16));
   }
   if (ops & OP_ROWS) {
-    // worst case 2 header + 16 x 32 rows of 64 B per (tile, chunk): ~B's bytes
+    // worst case 3 header + 16 x 32 rows of 64 B per (tile, chunk): ~B's bytes
     MMMCU_CUDA(ctx->row_off.ensure(sizeof(int64_t) * (n_cnt + 1)));
-    MMMCU_CUDA(ctx->brows.ensure((size_t)n_cnt * (2 + 16 * 32) * 64));
+    MMMCU_CUDA(ctx->brows.ensure((size_t)n_cnt * (3 + 16 * 32) * 64));
   }
   ctx->B = B;
   ctx->Kb = K;
