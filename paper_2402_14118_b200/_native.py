@@ -10,7 +10,7 @@ import os
 from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_uint8, c_uint32, c_uint64, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libmmmcu.so")
+LIB_PATH = os.environ.get("MMMCU_LIB") or os.path.join(_HERE, "_lib", "libmmmcu.so")
 
 # mmmcu_status
 OK = 0

@@ -26,6 +26,7 @@ namespace mmmcu {
 constexpr int kK1Threads = 256;  // 8 warps; each thread owns 4 consecutive columns
 constexpr int kK1Cols = 4 * kK1Threads;  // 1024 columns per CTA tile
 constexpr int kK1Rows = 32;              // rows per CTA tile (one 32-bit k-word for B)
+constexpr int kTcTileN = 192;            // K2-TC C tile width (columns)
 
 __device__ __forceinline__ float4 ldg_stream(const float* p) {
   float4 v;
@@ -56,9 +57,9 @@ struct K1Scratch {
   float* at;              // A^T per 128-row tile: at[(rt * kpad + k) * 128 + (i % 128)], zero padded
   int64_t kpad;           // K rounded up to 32
   int64_t m_at;           // M rounded up to 128
-  uint32_t* item_cnt;     // [n_tb][kw] B items per (256-column tile, 32-k chunk) (zeroed)
-  int64_t* item_off;      // [n_tb * kw + 1] exclusive prefix of item_cnt (last CTA)
-  int64_t n_tb;           // 256-column tiles of B
+  uint32_t* tlive;        // [n_tc][kw] live-k mask per kTcTileN-column TC tile: bit kk of word c
+                          // set iff B[32c + kk, tile columns] has a non-zero (zeroed, atomicOr)
+  int64_t n_tb;           // 256-column tiles of B (K2-SIMT records)
   // K2-SIMT operand: raw non-zero B block rows per (256-column tile, chunk)
   uint32_t* row_cnt;      // [n_tb][kw] non-zero (k, 16-column slice) rows (zeroed)
   int64_t* row_off;       // [n_tb * kw + 1] exclusive prefix of (row_cnt + 3 header rows), 64-byte units
@@ -190,15 +191,20 @@ __device__ __forceinline__ void k1_b_tile(const float* __restrict__ B, int64_t K
     const int64_t c_warp = tx * kK1Cols + 128 * (threadIdx.x >> 5);
     if (lane == 0 && rows && c_warp < ldb) atomicAdd(&z.row_cnt[(c_warp >> 8) * kw + kw_idx], rows);
   }
-  if (z.item_cnt) {
-    // K2-TC items of this chunk: ceil(popc(slice mask) / 8) per 16-column slice; a warp's
-    // 128 columns lie inside one 256-column tile
-    const uint32_t smask = gword | __shfl_xor_sync(0xffffffffu, gword, 2);
-    uint32_t items = ((lane & 3) == 0 && col_ok) ? (__popc(smask) + 7u) >> 3 : 0u;
+  if (z.tlive) {
+    // K2-TC live k of this chunk: OR of the group k-masks per TC tile; a warp's 128
+    // columns touch at most two 192-column tiles (a lane's 4 columns lie in one)
+    const int64_t t_lane = c / kTcTileN;
+    const int64_t t0 = __shfl_sync(0xffffffffu, t_lane, 0);
+    uint32_t w0 = (col_ok && t_lane == t0) ? gword : 0u;
+    uint32_t w1 = (col_ok && t_lane != t0) ? gword : 0u;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) items += __shfl_xor_sync(0xffffffffu, items, o);
-    const int64_t c_warp = tx * kK1Cols + 128 * (threadIdx.x >> 5);
-    if (lane == 0 && items && c_warp < ldb) atomicAdd(&z.item_cnt[(c_warp >> 8) * kw + kw_idx], items);
+    for (int o = 16; o; o >>= 1) {
+      w0 |= __shfl_xor_sync(0xffffffffu, w0, o);
+      w1 |= __shfl_xor_sync(0xffffffffu, w1, o);
+    }
+    if (lane == 0 && w0) atomicOr(&z.tlive[t0 * kw + kw_idx], w0);
+    if (lane == 0 && w1) atomicOr(&z.tlive[(t0 + 1) * kw + kw_idx], w1);
   }
 }
 
@@ -261,7 +267,6 @@ k1_pass(const float* __restrict__ A, int64_t M, int64_t K, int64_t lda, uint32_t
   __threadfence();
   if (threadIdx.x == 0) *z.done = 0u;  // ready for the next launch (no other CTA is left)
   k1_finalize_block(z.acol, z.bpop, z.bnz, K, M, nreg, has_a, has_b, z.slice_nz, stats);
-  if (z.item_cnt && nB > 0) k1_block_exclusive_scan(z.item_cnt, z.n_tb * kw, 0, z.item_off);
   if (z.row_cnt && nB > 0) k1_block_exclusive_scan(z.row_cnt, z.n_tb * kw, 3, z.row_off);
   if (nA > 0) {  // exclusive prefix of the 32-row tile sums for k1_csr's row_ptr
     __shared__ int64_t carry;
@@ -418,95 +423,103 @@ __global__ void __launch_bounds__(1024) k1_finalize(const uint32_t* __restrict__
   k1_finalize_block(acol, bpop, bnz, K, M, nreg, has_a, has_b, slice_nz, out);
 }
 
-// ------------------------------------------------------------ B items for K2-TC
-// Packs, once per plan, the B operand of every K2-TC item: for each 256-column tile tb and
-// 32-k chunk c, slice j (16 columns) contributes ceil(n_j / 8) items, n_j = # k in the
-// chunk with a non-zero B block in the slice.  An item is the 8 gathered B rows (zero rows
-// as padding) x 16 columns, split into tf32 hi / lo and laid out as the K-major
-// SWIZZLE_NONE core matrices the UMMA smem descriptor reads: element (n, r) at
-// (n%8)*16 + (n/8)*128 + (r/4)*256 + (r%4)*4 bytes, lo at +512.  Its 16-byte meta record
-// holds the 8 gathered k (32 = padding -> the zero row of K2's A^T stage) and the slice.
-// Items of one (tb, c) are contiguous at item_off[tb * kw + c], so K2 moves them with one
-// bulk copy per chunk — and all 128-row tiles reuse them (B is packed once, not per tile).
-constexpr int kPackThreads = 128;
-constexpr int kPackMaxItems = 64;
+// ------------------------------------------------------ B steps for K2-TC (dense tiles)
+// For each 192-column TC tile tb, the live k (B[k, tile] has a non-zero; tlive) are
+// numbered in ascending order, positions p = 0 .. nlive-1, and grouped 8 per MMA step.  Step
+// s of tile tb is a 12 KB image at tcb + (tb * maxsteps + s) * 3072 floats: B[k_p][n] for
+// its 8 positions split into tf32 hi (first 6 KB) and lo = v - hi (second 6 KB), each in the
+// K-major SWIZZLE_NONE core-matrix layout the UMMA descriptor reads with LBO = 128 B and
+// SBO = 256 B: element (n, j) at (n % 8) * 16 + (n / 8) * 256 + (j / 4) * 128 + (j % 4) * 4.
+// tck[tb][p] = k_p (-1 past nlive, whose B entries are zero); tcn[tb] = nlive.  Every CTA
+// of a tile re-derives the tile's chunk prefix from the kw mask words (no scan launch) and
+// packs kPtSteps steps; steps straddle chunk boundaries freely (positions, not chunks,
+// define a step), so padding is at most 7 k per tile.
+constexpr int kPackThreads = 128;  // k1_pack_rows
+constexpr int kPtSteps = 4;
+constexpr int kPtThreads = 256;
 
-__global__ void __launch_bounds__(kPackThreads)
-k1_pack_b(const float* __restrict__ B, int64_t K, int64_t ldb, const uint32_t* __restrict__ bgrp, int64_t kw,
-          const int64_t* __restrict__ item_off, uint8_t* __restrict__ items, uint4* __restrict__ meta) {
-  extern __shared__ __align__(16) uint8_t pk_smem[];  // [64][1024] staged items
-  __shared__ uint8_t s_k[kPackMaxItems][8];
-  __shared__ uint8_t s_slice[kPackMaxItems];
-  __shared__ int s_n;
-  const int64_t c = blockIdx.x, tb = blockIdx.y;
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int64_t n0 = tb * 256, k0 = c * 32;
-  if (tid < 32) {
-    uint32_t m = 0;
-    if (lane < 16 && n0 + 16 * lane < ldb) {
-      const int64_t g = (n0 >> 3) + 2 * lane;
-      m = bgrp[g * kw + c] | bgrp[(g + 1) * kw + c];
-    }
-    const int n = __popc(m);
-    const int mine = (n + 7) >> 3;
-    int base = mine;
+__global__ void __launch_bounds__(kPtThreads)
+k1_pack_tc(const float* __restrict__ B, int64_t K, int64_t ldb, const uint32_t* __restrict__ tlive, int64_t kw,
+           int64_t maxsteps, float* __restrict__ tcb, int32_t* __restrict__ tck, int32_t* __restrict__ tcn) {
+  extern __shared__ __align__(16) uint32_t pt_smem[];  // masks [kw] | prefix [kw + 1]
+  __shared__ int32_t s_k[kPtSteps * 8];
+  __shared__ int32_t wsum[kPtThreads / 32];
+  uint32_t* s_m = pt_smem;
+  int32_t* s_pre = reinterpret_cast<int32_t*>(pt_smem + kw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t tb = blockIdx.y, n0 = tb * kTcTileN;
+  // chunk masks and their exclusive popcount prefix (block scan, carried over kw / 256 rounds)
+  int32_t carry = 0;
+  for (int64_t base = 0; base < kw; base += kPtThreads) {
+    const int64_t c = base + tid;
+    const uint32_t m = c < kw ? tlive[tb * kw + c] : 0u;
+    if (c < kw) s_m[c] = m;
+    const int32_t v = __popc(m);
+    int32_t x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, base, o);
-      if (lane >= o) base += y;
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
-    if (lane == 31) s_n = base;
-    base -= mine;
-    for (int g = 0; g < mine; ++g) {
-      s_slice[base + g] = (uint8_t)lane;
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        const int idx = 8 * g + r;
-        int kk = 32;  // padding -> zero row
-        if (idx < n) {
-          uint32_t mm = m;
-          for (int d = 0; d < idx; ++d) mm &= mm - 1;
-          kk = __ffs(mm) - 1;
-        }
-        s_k[base + g][r] = (uint8_t)kk;
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    int32_t before = carry;
+    for (int w = 0; w < warp; ++w) before += wsum[w];
+    if (c < kw) s_pre[c] = before + x - v;
+    int32_t total_round = 0;
+    for (int w = 0; w < kPtThreads / 32; ++w) total_round += wsum[w];
+    carry += total_round;
+    __syncthreads();
+  }
+  if (tid == 0) s_pre[kw] = carry;
+  __syncthreads();
+  const int32_t total = carry;
+  const int64_t nsteps = (total + 7) / 8;
+  if (blockIdx.x == 0 && tid == 0) tcn[tb] = total;
+  const int64_t s0 = (int64_t)blockIdx.x * kPtSteps;
+  if (s0 >= nsteps) return;
+  if (tid < kPtSteps * 8) {
+    const int64_t p = s0 * 8 + tid;
+    int32_t k = -1;
+    if (p < total) {
+      int64_t lo = 0, hi = kw - 1;  // last chunk c with s_pre[c] <= p
+      while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (s_pre[mid] <= p) lo = mid;
+        else hi = mid - 1;
       }
+      uint32_t m = s_m[lo];
+      for (int64_t d = p - s_pre[lo]; d; --d) m &= m - 1;
+      k = (int32_t)(lo * 32 + __ffs(m) - 1);
     }
+    s_k[tid] = k;
+    if (p < maxsteps * 8) tck[tb * maxsteps * 8 + p] = k;
   }
   __syncthreads();
-  const int nitems = s_n;
-  const int64_t off = item_off[tb * kw + c];
-  // items: piece p = (item t, row r, quad q) -> 4 floats of B, split, scattered into smem
-  for (int p = tid; p < nitems * 32; p += kPackThreads) {
-    const int t = p >> 5, r = (p >> 2) & 7, q = p & 3;
-    const int kk = s_k[t][r];
-    const int j = s_slice[t];
-    float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (kk < 32) bv = ldg_stream(B + (k0 + kk) * ldb + n0 + 16 * j + 4 * q);
-    const float e[4] = {bv.x, bv.y, bv.z, bv.w};
-    uint8_t* blk = pk_smem + t * 1024 + (r >> 2) * 256 + (r & 3) * 4;
+  // job = (step, k-quad q, column n): 4 B values -> one float4 hi + one float4 lo
+  for (int j = tid; j < kPtSteps * 2 * kTcTileN; j += kPtThreads) {
+    const int sl = j / (2 * kTcTileN), q = (j / kTcTileN) & 1, n = j % kTcTileN;
+    const int64_t s = s0 + sl;
+    if (s >= nsteps) break;
+    const bool col_ok = n0 + n < ldb;
+    float v[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const int nn = 4 * q + i;
-      const int o2 = (nn & 7) * 16 + (nn >> 3) * 128;
-      const uint32_t bits = __float_as_uint(e[i]);
-      const uint32_t hi = bits & 0xFFFFE000u;
-      const uint32_t lo = __float_as_uint(e[i] - __uint_as_float(hi));
-      *reinterpret_cast<uint32_t*>(blk + o2) = hi;
-      *reinterpret_cast<uint32_t*>(blk + 512 + o2) = lo;
+      const int32_t k = s_k[sl * 8 + 4 * q + i];
+      v[i] = (k >= 0 && col_ok) ? __ldg(B + (int64_t)k * ldb + n0 + n) : 0.0f;
     }
+    uint32_t h[4], l[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      h[i] = __float_as_uint(v[i]) & 0xFFFFE000u;
+      l[i] = __float_as_uint(v[i] - __uint_as_float(h[i]));
+    }
+    float* img = tcb + (tb * maxsteps + s) * (kTcTileN * 16);
+    const int off = (n & 7) * 4 + (n >> 3) * 64 + q * 32;  // in floats
+    *reinterpret_cast<uint4*>(img + off) = make_uint4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<uint4*>(img + kTcTileN * 8 + off) = make_uint4(l[0], l[1], l[2], l[3]);
   }
-  __syncthreads();
-  uint4* dst = reinterpret_cast<uint4*>(items + off * 1024);
-  const uint4* src = reinterpret_cast<const uint4*>(pk_smem);
-  for (int v = tid; v < nitems * 64; v += kPackThreads) dst[v] = src[v];
-  for (int t = tid; t < nitems; t += kPackThreads) {
-    uint4 mrec;
-    mrec.x = *reinterpret_cast<const uint32_t*>(&s_k[t][0]);
-    mrec.y = *reinterpret_cast<const uint32_t*>(&s_k[t][4]);
-    mrec.z = s_slice[t];
-    mrec.w = 0;
-    meta[off + t] = mrec;
-  }
+  (void)K;
 }
 
 // ----------------------------------------------------------- B rows for K2-SIMT

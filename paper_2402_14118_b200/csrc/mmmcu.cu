@@ -74,9 +74,9 @@ struct mmmcu_ctx {
   DevBuf ctl;
 
   // ---- K2 operands emitted by K1 (which ones depends on the algorithm, see ops_for)
-  bool op_at = false, op_rows = false, op_items = false;
-  int64_t kpad = 0, m_at = 0, n_tb = 0;
-  DevBuf at, items, meta, item_off, brows, row_off;
+  bool op_at = false, op_rows = false, op_tcb = false;
+  int64_t kpad = 0, m_at = 0, n_tb = 0, n_tc = 0, tc_steps = 0;
+  DevBuf at, tcb, tck, tcn, brows, row_off;
 
   // ---- statistics: u64 [16] = {inv, lanes, skipped, zreg, nnzA, pop, zero_codes, span, slice_nz}
   DevBuf stats;
@@ -148,18 +148,19 @@ int64_t n_row_tiles(int64_t M) { return (M + mmmcu::kK1Rows - 1) / mmmcu::kK1Row
 unsigned long long* zb_slice(mmmcu_ctx* ctx) { return ctx->zb.as<unsigned long long>(); }
 uint32_t* zb_bpop(mmmcu_ctx* ctx) { return reinterpret_cast<uint32_t*>(ctx->zb.as<unsigned long long>() + 1); }
 uint32_t* zb_bnz(mmmcu_ctx* ctx) { return zb_bpop(ctx) + ctx->Kb; }
-// Operand sets K1 emits for K2: A^T tiles (SIMT v2, TC), raw B rows (SIMT v2), tf32 B items (TC).
-enum { OP_AT = 1, OP_ROWS = 2, OP_ITEMS = 4 };
+// Operand sets K1 emits for K2: A^T tiles (SIMT v2, TC), raw B rows (SIMT v2), tf32 B step
+// images + live-k lists (TC).
+enum { OP_AT = 1, OP_ROWS = 2, OP_TCB = 4 };
 int ops_for(const mmmcu_ctx* ctx) {
   switch (ctx->algo) {
-    case MMMCU_ALGO_TC: return OP_AT | OP_ITEMS;
+    case MMMCU_ALGO_TC: return OP_AT | OP_TCB;
     case MMMCU_ALGO_DENSE: return 0;
     default: return OP_AT | OP_ROWS;
   }
 }
-int64_t n_cnt_b(const mmmcu_ctx* ctx) { return ctx->n_tb * ((ctx->Kb + 31) / 32); }
-uint32_t* zb_item_cnt(mmmcu_ctx* ctx) { return zb_bnz(ctx) + ctx->Kb; }
-uint32_t* zb_row_cnt(mmmcu_ctx* ctx) { return zb_item_cnt(ctx) + ((ops_for(ctx) & OP_ITEMS) ? n_cnt_b(ctx) : 0); }
+uint32_t* zb_tlive(mmmcu_ctx* ctx) { return zb_bnz(ctx) + ctx->Kb; }
+int64_t n_cnt_tc(const mmmcu_ctx* ctx) { return ctx->n_tc * ((ctx->Kb + 31) / 32); }
+uint32_t* zb_row_cnt(mmmcu_ctx* ctx) { return zb_tlive(ctx) + ((ops_for(ctx) & OP_TCB) ? n_cnt_tc(ctx) : 0); }
 
 mmmcu_status stage_a(mmmcu_ctx* ctx, const float* A, int64_t M, int64_t K, int64_t lda, uint64_t av) {
   if (M <= 0 || K <= 0) return fail(ctx, MMMCU_ERR_INVALID_ARG, "matrix dimensions must be positive");
@@ -200,20 +201,23 @@ mmmcu_status stage_b(mmmcu_ctx* ctx, const float* B, int64_t K, int64_t N, int64
   ctx->has_b = false;
   MMMCU_CUDA(ctx->codes.ensure((size_t)K * nreg));
   MMMCU_CUDA(ctx->bgrp.ensure(sizeof(uint32_t) * ngrp * kw));
-  ctx->op_rows = ctx->op_items = false;
+  ctx->op_rows = ctx->op_tcb = false;
   const int ops = ops_for(ctx);
   const int64_t n_tb = (ldb + 255) / 256;
   const int64_t n_cnt = n_tb * kw;
-  const int64_t n_extra = ((ops & OP_ITEMS) ? n_cnt : 0) + ((ops & OP_ROWS) ? n_cnt : 0);
+  const int64_t n_tc = (ldb + mmmcu::kTcTileN - 1) / mmmcu::kTcTileN;
+  const int64_t n_extra = ((ops & OP_TCB) ? n_tc * kw : 0) + ((ops & OP_ROWS) ? n_cnt : 0);
   const size_t zb_bytes = sizeof(unsigned long long) + sizeof(uint32_t) * (2 * K + n_extra);
   MMMCU_CUDA(ctx->zb.ensure(zb_bytes));
   MMMCU_CUDA(cudaMemsetAsync(ctx->zb.p, 0, zb_bytes, ctx->stream));
   ctx->n_tb = n_tb;
-  if (ops & OP_ITEMS) {
-    // worst case 64 items (16 slices x 4) per (256-column tile, 32-k chunk): 2x B's bytes
-    MMMCU_CUDA(ctx->item_off.ensure(sizeof(int64_t) * (n_cnt + 1)));
-    MMMCU_CUDA(ctx->items.ensure((size_t)n_cnt * 64 * 1024));
-    MMMCU_CUDA(ctx->meta.ensure((size_t)n_cnt * 64 * 16));
+  ctx->n_tc = n_tc;
+  if (ops & OP_TCB) {
+    // worst case every k live in every tile: kw*4 steps of 12 KB per tile = 2x B's bytes
+    ctx->tc_steps = kw * 4;
+    MMMCU_CUDA(ctx->tcb.ensure((size_t)n_tc * ctx->tc_steps * mmmcu::kTdStepFloats * 4));
+    MMMCU_CUDA(ctx->tck.ensure(sizeof(int32_t) * n_tc * ctx->tc_steps * 8));
+    MMMCU_CUDA(ctx->tcn.ensure(sizeof(int32_t) * n_tc));
   }
   if (ops & OP_ROWS) {
     // worst case 3 header + 16 x 32 rows of 64 B per (tile, chunk): ~B's bytes
@@ -241,7 +245,7 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   const int64_t K = do_a ? ctx->Ka : ctx->Kb;
   const int64_t kw = (K + 31) / 32;
   const int ops = ops_for(ctx);
-  const bool tc_a = do_a && (ops & OP_AT), items_b = do_b && (ops & OP_ITEMS), rows_b = do_b && (ops & OP_ROWS);
+  const bool tc_a = do_a && (ops & OP_AT), tcb_b = do_b && (ops & OP_TCB), rows_b = do_b && (ops & OP_ROWS);
   const int64_t a_tx = (ctx->Ka + mmmcu::kK1Cols - 1) / mmmcu::kK1Cols;
   const int64_t a_rows = tc_a ? ctx->m_at : ctx->M;  // A^T tiles are written to the 128-row boundary
   const int64_t nA = do_a ? a_tx * ((a_rows + mmmcu::kK1Rows - 1) / mmmcu::kK1Rows) : 0;
@@ -260,8 +264,7 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   z.at = tc_a ? ctx->at.as<float>() : nullptr;
   z.kpad = ctx->kpad;
   z.m_at = ctx->m_at;
-  z.item_cnt = items_b ? zb_item_cnt(ctx) : nullptr;
-  z.item_off = items_b ? ctx->item_off.as<int64_t>() : nullptr;
+  z.tlive = tcb_b ? zb_tlive(ctx) : nullptr;
   z.row_cnt = rows_b ? zb_row_cnt(ctx) : nullptr;
   z.row_off = rows_b ? ctx->row_off.as<int64_t>() : nullptr;
   z.n_tb = ctx->n_tb;
@@ -291,12 +294,15 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
         ctx->brows.as<uint4>());
     MMMCU_LAUNCHED();
   }
-  if (items_b) {
-    MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k1_pack_b, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    dim3 grid((unsigned)((ctx->Kb + 31) / 32), (unsigned)ctx->n_tb);
-    mmmcu::k1_pack_b<<<grid, mmmcu::kPackThreads, 64 * 1024, ctx->stream>>>(
-        ctx->B, ctx->Kb, ctx->ldb, ctx->bgrp.as<uint32_t>(), (ctx->Kb + 31) / 32, ctx->item_off.as<int64_t>(),
-        ctx->items.as<uint8_t>(), ctx->meta.as<uint4>());
+  if (tcb_b) {
+    const int64_t bkw = (ctx->Kb + 31) / 32;
+    const int smem = (int)(sizeof(uint32_t) * (2 * bkw + 1));
+    if (smem > 200 * 1024) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "K too large for the TC packer");
+    MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k1_pack_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    dim3 grid((unsigned)((ctx->tc_steps + mmmcu::kPtSteps - 1) / mmmcu::kPtSteps), (unsigned)ctx->n_tc);
+    mmmcu::k1_pack_tc<<<grid, mmmcu::kPtThreads, smem, ctx->stream>>>(
+        ctx->B, ctx->Kb, ctx->ldb, zb_tlive(ctx), bkw, ctx->tc_steps, ctx->tcb.as<float>(), ctx->tck.as<int32_t>(),
+        ctx->tcn.as<int32_t>());
     MMMCU_LAUNCHED();
   }
   if (do_a) {
@@ -305,7 +311,7 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   }
   if (do_b) {
     ctx->has_b = true;
-    ctx->op_items = items_b;
+    ctx->op_tcb = tcb_b;
     ctx->op_rows = rows_b;
   }
   return MMMCU_OK;
@@ -367,6 +373,20 @@ mmmcu_status launch_simt(mmmcu_ctx* ctx, float* C, int64_t ldc, int span_hint) {
   return MMMCU_OK;
 }
 
+// K2-TC over the dense-tile operands (sel: device-side path choice, nullptr = forced).
+mmmcu_status launch_tc(mmmcu_ctx* ctx, float* C, int64_t ldc, const unsigned long long* sel) {
+  const int64_t row_tiles = ctx->m_at / mmmcu::kTdTM;
+  if (ctx->n_tc > 65535) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "N too large for the TC grid");
+  MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, mmmcu::kTdSmem));
+  dim3 grid((unsigned)row_tiles, (unsigned)ctx->n_tc);
+  mmmcu::k2_tc<<<grid, mmmcu::kTdThreads, mmmcu::kTdSmem, ctx->stream>>>(
+      ctx->at.as<float>(), ctx->kpad, ctx->tcb.as<float>(), ctx->tck.as<int32_t>(), ctx->tcn.as<int32_t>(),
+      ctx->tc_steps, C, ldc, ctx->M, ctx->N, sel);
+  MMMCU_LAUNCHED();
+
+  return MMMCU_OK;
+}
+
 mmmcu_status read_stats(mmmcu_ctx* ctx, unsigned long long* host16) {
   MMMCU_CUDA(cudaMemcpyAsync(host16, ctx->stats.p, sizeof(unsigned long long) * 16, cudaMemcpyDeviceToHost, ctx->stream));
   MMMCU_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -416,7 +436,7 @@ mmmcu_status mmmcu_ctx_destroy(mmmcu_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : {&ctx->abits, &ctx->za, &ctx->tile_prefix, &ctx->row_ptr, &ctx->cols, &ctx->codes, &ctx->bgrp, &ctx->zb,
-                    &ctx->ctl, &ctx->at, &ctx->items, &ctx->meta, &ctx->item_off, &ctx->brows, &ctx->row_off,
+                    &ctx->ctl, &ctx->at, &ctx->tcb, &ctx->tck, &ctx->tcn, &ctx->brows, &ctx->row_off,
                     &ctx->stats, &ctx->hA, &ctx->hB, &ctx->hC, &ctx->scratch0, &ctx->scratch1})
     b->release();
   delete ctx;
@@ -592,18 +612,10 @@ mmmcu_status mmmcu_multiply(mmmcu_ctx* ctx, float* C, int64_t ldc, const float* 
     return fail(ctx, MMMCU_ERR_INVALID_ARG,
                 "C must be 16-byte aligned with ldc >= round_up(N, 64) (Matrix padding) and ldc % 4 == 0");
   if (ctx->algo == MMMCU_ALGO_TC) {
-    if (!ctx->op_at || !ctx->op_items)
-      return fail(ctx, MMMCU_ERR_NOT_READY, "the TC operands were not built: preprocess with algo AUTO or TC");
+    if (!ctx->op_at || !ctx->op_tcb)
+      return fail(ctx, MMMCU_ERR_NOT_READY, "the TC operands were not built: preprocess with algo TC");
     ctx->last_algo = MMMCU_ALGO_TC;
-    const int64_t Np = round_up(ctx->N, 64), kw = (ctx->Ka + 31) / 32;
-    const int64_t row_tiles = ctx->m_at / mmmcu::kTcTM;
-    if (row_tiles > 65535) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "M too large for the TC grid");
-    MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, mmmcu::kTcSmem));
-    dim3 grid((unsigned)((Np + mmmcu::kTcTN - 1) / mmmcu::kTcTN), (unsigned)row_tiles);
-    mmmcu::k2_tc<<<grid, mmmcu::kTcThreads, mmmcu::kTcSmem, ctx->stream>>>(
-        ctx->at.as<float>(), ctx->kpad, ctx->items.as<uint8_t>(), ctx->meta.as<uint4>(), ctx->item_off.as<int64_t>(),
-        kw, C, ldc, ctx->M, Np);
-    MMMCU_LAUNCHED();
+    MMMCU_TRY(launch_tc(ctx, C, ldc, nullptr));
   } else if (ctx->algo == MMMCU_ALGO_DENSE) {
     ctx->last_algo = MMMCU_ALGO_DENSE;
     dim3 grid((unsigned)((ctx->N + 63) / 64), (unsigned)((ctx->M + 63) / 64));

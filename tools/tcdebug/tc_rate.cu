@@ -163,7 +163,7 @@ __global__ void k_st_rate(int n, long long* cycles) {
 
 int main() {
   long long* d; cudaMalloc(&d, 64); long long h[8];
-  for (int N : {16, 32, 64, 128, 256}) for (int same : {4, 2, 3}) {
+  for (int N : {16, 32, 64, 128, 192, 256}) for (int same : {4, 2, 3}) {
     k_mma_rate<<<1, 128>>>(4096, N, d, same);
     cudaError_t e = cudaDeviceSynchronize();
     cudaMemcpy(h, d, 8, cudaMemcpyDeviceToHost);
