@@ -151,6 +151,14 @@ def measured_peaks():
     return hbm, src
 
 
+def measured_bf16():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return float(json.load(open(path))["bf16_tflops"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def probe_fp32_peak(device):
     import ctypes
 
@@ -206,17 +214,38 @@ def make_inputs(cells, ctx, rank, world, torch, dist, device):
     return As, Bs, bcast_ms
 
 
+TC_TM, TC_TN = 128, 192  # K2-TC C tile (k2_tc.cuh)
+
+
+def tc_executed_flops(M, b, torch):
+    """Tensor-core flops K2-TC executes on a cell: per 192-column tile, ceil(live k / 8) MMA
+    steps of 3 tf32 MMAs (hi/lo split) of 128 x 192 x 8, for every 128-row tile."""
+    K, N = b.shape
+    nt = (N + TC_TN - 1) // TC_TN
+    nz = torch.zeros((K, nt * TC_TN), dtype=torch.bool, device=b.device)
+    nz[:, :N] = b != 0
+    live = nz.view(K, nt, TC_TN).any(dim=2).sum(dim=0)  # live k per tile
+    steps = int(((live + 7) // 8).sum().item())
+    return steps * ((M + TC_TM - 1) // TC_TM) * 3 * 2 * TC_TM * TC_TN * 8
+
+
 def cell_stats(cells, As, Bs, ctx, torch):
-    """Per cell: useful flops (2*lane_fma_ops), algorithmic bytes, counters (setup, untimed)."""
+    """Per cell: useful flops (2*lane_fma_ops), algorithmic bytes, counters, the K2 path AUTO
+    takes and, for K2-TC, the tensor-core flops it executes (setup, untimed)."""
     stats = []
     for (label, M, K, N, sa, sb) in cells:
         a, b = As[sa["key"]], Bs[sb["key"]]
         ctx.preprocess(a, b)
         cnt = ctx.planned_counters()
+        c = torch.zeros((M, N), dtype=torch.float32, device=a.device)
+        ctx.multiply(c, a, b, want_counters=False)
+        path = {5: "k2_tc", 3: "k2_simt2<8>", 4: "k2_simt2<16>"}.get(ctx.last_algo(), str(ctx.last_algo()))
         k_live = int((a != 0).any(dim=0).sum().item())
         algo_bytes = 4 * (M * K + k_live * N + M * N)
         stats.append(dict(label=label, flops=2 * cnt.lane_fma_ops, bytes=algo_bytes, k_live=k_live,
-                          lane_fma_ops=cnt.lane_fma_ops, M=M, K=K, N=N))
+                          lane_fma_ops=cnt.lane_fma_ops, M=M, K=K, N=N, path=path,
+                          tc_flops=tc_executed_flops(M, b, torch) if path == "k2_tc" else 0))
+        del c
     return stats
 
 
@@ -235,10 +264,11 @@ def run_step(cells, As, Bs, Cs, ctx, torch, events=None):
 
 
 def count_launches(cells):
-    # per cell: K1 = k1_pass (A and B tiles, last-CTA counters/scans) + k1_csr + k1_pack_rows;
-    # K2 AUTO = k2_simt2<8> and k2_simt2<16>, gated on the device (one exits at entry).
-    # cudaMemsetAsync nodes are not counted.
-    return 5 * len(cells)
+    # per cell (AUTO): K1 = k1_pass (A and B tiles, last-CTA counters/scans/path choice) +
+    # k1_csr + k1_pack_rows + k1_pack_tc (the two packs gated on the device by the path
+    # choice: one exits at entry); K2 = k2_simt2<8> + k2_simt2<16> + k2_tc, gated the same
+    # way (one runs).  cudaMemsetAsync nodes are not counted.
+    return 7 * len(cells)
 
 
 # ---------------------------------------------------------------------------- CPU leg
@@ -378,6 +408,22 @@ def main():
     k2_flops = sum(s["flops"] for s in stats)
     k2_time = float(k2_ms.sum()) * 1e-3
     achieved_tf = k2_flops / k2_time / 1e12
+    paths = {}
+    for i, s_ in enumerate(stats):
+        paths.setdefault(s_["path"], [0, 0.0])
+        paths[s_["path"]][0] += 1
+        paths[s_["path"]][1] += float(k2_ms[i])
+    dominant = max(paths, key=lambda p: paths[p][1])
+    tc_ms = sum(float(k2_ms[i]) for i, s_ in enumerate(stats) if s_["path"] == "k2_tc")
+    tc_exec = sum(s_["tc_flops"] for s_ in stats)
+    bf16 = measured_bf16()
+    tensor = None
+    if tc_ms > 0:
+        tensor = {"kernel": "k2_tc", "executed_tflops": round(tc_exec / (tc_ms * 1e-3) / 1e12, 1),
+                  "peak_tflops": round(bf16 / 2, 1) if bf16 else None,
+                  "peak_source": "tf32 dense = measured bf16 (MEASURED_PEAKS.json) / 2" if bf16 else None,
+                  "frac": round(tc_exec / (tc_ms * 1e-3) / 1e12 / (bf16 / 2), 4) if bf16 else None,
+                  "def": "3xTF32 MMAs the kernel issues (3 per live-k step of 8 per 128x192 tile) / K2-TC time"}
     t_roof = sum(max(s["flops"] / (fp32_peak * 1e12), s["bytes"] / (hbm_peak * 1e9)) for s in stats)
     t_meas = float((k1_ms + k2_ms).sum()) * 1e-3
     hbm_bytes = sum(s["bytes"] for s in stats)
@@ -416,7 +462,8 @@ def main():
             "config": cfg,
             "roofline": {"bound": "fp32", "achieved": round(achieved_tf, 3), "peak": round(fp32_peak, 2),
                          "unit": "TFLOP/s", "frac": round(achieved_tf / fp32_peak, 4), "traffic": None,
-                         "kernel": "k2_simt2<8|16> (K2-SIMT masked GEMM, exact)", "peak_source": fp32_src,
+                         "kernel": dominant, "paths": {p: {"cells": v[0], "k2_ms": round(v[1], 4)} for p, v in paths.items()},
+                         "tensor": tensor, "peak_source": fp32_src,
                          "time_frac": round(t_roof / t_meas, 4),
                          "time_frac_def": "Σ_cells max(useful_flops/P_fp32, algo_bytes/BW_hbm) / Σ_cells (K1+K2) time",
                          "hbm_peak_gbs": hbm_peak, "hbm_peak_source": hbm_src,

@@ -103,16 +103,26 @@ class Handle {
 template <typename T>
 class MmmContext;
 
+// How C is accumulated.  Auto (default): the plan picks K2-SIMT or the 3xTF32 tensor-core
+// K2-TC per multiply, C within the north_star tolerance |dC| <= 1e-5 (|c0| + sum|a||b|).
+// Exact: K2-SIMT only, which replays the reference kernel's ascending-k fmaf chain: C is
+// bit-identical to KernelTable::apply (kernel_table.cpp).
+enum class Accumulation { Auto, Exact };
+
 template <>
 class MmmContext<float> {
  public:
   MmmContext(const Matrix<float>& a, const Matrix<float>& b,
-             LaneConfig lane = LaneConfig::defaults(Dtype::f32), int64_t leaf_dim = 256, int device = 0)
+             LaneConfig lane = LaneConfig::defaults(Dtype::f32), int64_t leaf_dim = 256, int device = 0,
+             Accumulation accumulation = Accumulation::Auto)
       : h_(device), lane_(lane), leaf_dim_(leaf_dim), rows_(a.rows()), inner_(a.cols()), cols_(b.cols()) {
     if (a.cols() != b.rows())
       throw DimensionMismatch("a.cols (" + std::to_string(a.cols()) + ") != b.rows (" + std::to_string(b.rows()) +
                               ")");
     cuda_detail::check(mmmcu_validate_lane(h_.get(), cuda_detail::lane_of(lane)), h_.get());
+    cuda_detail::check(
+        mmmcu_set_algo(h_.get(), accumulation == Accumulation::Exact ? MMMCU_ALGO_SIMT_BCAST : MMMCU_ALGO_AUTO),
+        h_.get());
     cuda_detail::check(mmmcu_preprocess_host(h_.get(), a.data(), a.rows(), a.cols(), a.padded_cols(), b.data(),
                                              b.cols(), b.padded_cols(), cuda_detail::lane_of(lane), a.version(),
                                              b.version()),

@@ -70,14 +70,17 @@ typedef struct {
 
 /* Kernel-variant selection for mmmcu_multiply (all variants honour the same contract). */
 typedef enum {
-  MMMCU_ALGO_AUTO = 0,       /* pick per call from the preprocessing statistics          */
-  MMMCU_ALGO_SIMT_BCAST = 1, /* K2-SIMT: warp-uniform k over B block masks, exact fp32;
-                                mask granularity (8 or 16 columns) chosen on the device   */
+  MMMCU_ALGO_AUTO = 0,       /* K1's cost model picks K2-SIMT or K2-TC on the device (no
+                                host round trip); C within the tolerance below           */
+  MMMCU_ALGO_SIMT_BCAST = 1, /* K2-SIMT: warp-uniform k over B block masks, exact fp32
+                                (bit-identical to the reference's fmaf chain); mask
+                                granularity (8 or 16 columns) chosen on the device         */
   MMMCU_ALGO_DENSE = 2,      /* multiply_simple (dense i-k-j fma)            */
   MMMCU_ALGO_SIMT_SPAN8 = 3, /* K2-SIMT forced to 8-column (group) masks                  */
   MMMCU_ALGO_SIMT_SPAN16 = 4,/* K2-SIMT forced to 16-column slice masks                   */
-  MMMCU_ALGO_TC = 5          /* K2-TC: tcgen05 3xTF32 over k-compacted 16-column slices;
-                                tolerance-matched (|dC| <= 1e-5 * sum|a||b|), not bit-exact */
+  MMMCU_ALGO_TC = 5          /* K2-TC: tcgen05 3xTF32 on 128x192 C tiles over each tile's
+                                live k; tolerance-matched (|dC| <= 1e-5 * (|c0| +
+                                sum|a||b|)), not bit-exact                                 */
 } mmmcu_algo;
 
 /* ---- context --------------------------------------------------------------------- */

@@ -60,6 +60,8 @@ struct K1Scratch {
   uint32_t* tlive;        // [n_tc][kw] live-k mask per kTcTileN-column TC tile: bit kk of word c
                           // set iff B[32c + kk, tile columns] has a non-zero (zeroed, atomicOr)
   int64_t n_tb;           // 256-column tiles of B (K2-SIMT records)
+  int64_t n_tc;           // kTcTileN-column tiles of B (K2-TC)
+  int choose;             // AUTO: pick K2-SIMT vs K2-TC from the cost model (both operand sets built)
   // K2-SIMT operand: raw non-zero B block rows per (256-column tile, chunk)
   uint32_t* row_cnt;      // [n_tb][kw] non-zero (k, 16-column slice) rows (zeroed)
   int64_t* row_off;       // [n_tb * kw + 1] exclusive prefix of (row_cnt + 3 header rows), 64-byte units
@@ -213,6 +215,53 @@ __device__ void k1_finalize_block(const uint32_t* __restrict__ acol, const uint3
                                   int has_b, const unsigned long long* __restrict__ slice_nz,
                                   unsigned long long* __restrict__ out);
 
+// AUTO path choice (stats[7] := 32 for K2-TC, else the K2-SIMT span stays): estimated
+// SM-cycles of each path from the plan, constants measured on B200 (K2 choice):
+//   K2-SIMT = records * 1158 + row tiles * (span 16: 26 * slice_nz | span 8: 17.5 * pop)
+//             records = row tiles * 256-column tiles * 32-k chunks
+//   K2-TC   = row tiles * Σ_tiles (24200 + 784 * stages), stages = ceil(live k / 16)
+//   + K1 packing traffic at 0.0433 SM-cycles per byte (HBM): K2-SIMT rows 2 x 64 B per
+//     non-zero (k, slice); K2-TC step images 3 x 768 B per live (k, tile);
+//   each divided by min(148 SMs, its CTA count).
+__device__ void k1_choose_path(const K1Scratch& z, int64_t M, int64_t kw, unsigned long long* __restrict__ out) {
+  __shared__ unsigned long long s_stage[kK1Threads / 32], s_live[kK1Threads / 32];
+  unsigned long long st = 0, live = 0;
+  for (int64_t tb = threadIdx.x; tb < z.n_tc; tb += blockDim.x) {
+    unsigned long long n = 0;
+    for (int64_t c = 0; c < kw; ++c) n += __popc(z.tlive[tb * kw + c]);
+    live += n;
+    st += (n + 15) / 16;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    st += __shfl_xor_sync(0xffffffffu, st, o);
+    live += __shfl_xor_sync(0xffffffffu, live, o);
+  }
+  if (lane == 0) {
+    s_stage[warp] = st;
+    s_live[warp] = live;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long stages = 0, lv = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      stages += s_stage[w];
+      lv += s_live[w];
+    }
+    const double rt = (double)((M + 127) / 128);
+    const double span = (double)out[7];
+    const double slice_nz = (double)z.slice_nz[0], pop = (double)out[5];
+    const double simt = rt * (double)z.n_tb * (double)kw * 1158.0 + rt * (span == 16.0 ? 26.0 * slice_nz : 17.5 * pop) +
+                        0.0433 * 128.0 * slice_nz;
+    const double tc = rt * (24200.0 * (double)z.n_tc + 784.0 * (double)stages) + 0.0433 * 3.0 * 768.0 * (double)lv;
+    // time ~ work / min(SMs, CTAs): short operands leave SMs idle
+    const double par_simt = fmin(148.0, rt * (double)z.n_tb), par_tc = fmin(148.0, rt * (double)z.n_tc);
+    if (tc / par_tc < simt / par_simt) out[7] = 32ull;
+  }
+  __syncthreads();
+}
+
 // Block-wide exclusive scan of (cnt[t] + add) -> out[0..n] (out[n] = total); one CTA.
 __device__ void k1_block_exclusive_scan(const uint32_t* __restrict__ cnt, int64_t n, uint32_t add,
                                         int64_t* __restrict__ out) {
@@ -267,6 +316,7 @@ k1_pass(const float* __restrict__ A, int64_t M, int64_t K, int64_t lda, uint32_t
   __threadfence();
   if (threadIdx.x == 0) *z.done = 0u;  // ready for the next launch (no other CTA is left)
   k1_finalize_block(z.acol, z.bpop, z.bnz, K, M, nreg, has_a, has_b, z.slice_nz, stats);
+  if (z.choose && has_a && has_b) k1_choose_path(z, M, kw, stats);
   if (z.row_cnt && nB > 0) k1_block_exclusive_scan(z.row_cnt, z.n_tb * kw, 3, z.row_off);
   if (nA > 0) {  // exclusive prefix of the 32-row tile sums for k1_csr's row_ptr
     __shared__ int64_t carry;
@@ -365,7 +415,7 @@ __global__ void __launch_bounds__(256) k1_csr(const uint32_t* __restrict__ abits
 //   zero regions  = Σ_k acol[k] * (nreg - bnz[k])
 //   rows_skipped  = M*K - Σ_k acol[k]
 //   stats         = Σ_k bpop[k], Σ_k (nreg - bnz[k])
-// out: u64[8] = {inv, lanes, skipped, zreg, nnzA, pop_total, zero_codes, span}
+// out: u64[9] = {inv, lanes, skipped, zreg, nnzA, pop_total, zero_codes, path, span}
 //   span: K2-SIMT mask granularity, from the cost model of DESIGN.md (K2 variants):
 //   16-column slices cost ~41 issue slots per non-zero (k, slice), 8-column groups ~23 per
 //   non-zero (k, group); pick the cheaper (slice_nz[0] = # non-zero (k, slice) pairs).
@@ -412,15 +462,8 @@ __device__ void k1_finalize_block(const uint32_t* __restrict__ acol, const uint3
     out[5] = red[0][4];
     out[6] = red[0][5];
     out[7] = (has_b && 41ull * slice_nz[0] > 23ull * red[0][4]) ? 8ull : 16ull;
+    out[8] = out[7];  // the K2-SIMT span alone (out[7] may become 32 = K2-TC, k1_choose_path)
   }
-}
-
-__global__ void __launch_bounds__(1024) k1_finalize(const uint32_t* __restrict__ acol, const uint32_t* __restrict__ bpop,
-                                                    const uint32_t* __restrict__ bnz, int64_t K, int64_t M,
-                                                    int64_t nreg, int has_a, int has_b,
-                                                    const unsigned long long* __restrict__ slice_nz,
-                                                    unsigned long long* __restrict__ out) {
-  k1_finalize_block(acol, bpop, bnz, K, M, nreg, has_a, has_b, slice_nz, out);
 }
 
 // ------------------------------------------------------ B steps for K2-TC (dense tiles)
@@ -440,7 +483,9 @@ constexpr int kPtThreads = 256;
 
 __global__ void __launch_bounds__(kPtThreads)
 k1_pack_tc(const float* __restrict__ B, int64_t K, int64_t ldb, const uint32_t* __restrict__ tlive, int64_t kw,
-           int64_t maxsteps, float* __restrict__ tcb, int32_t* __restrict__ tck, int32_t* __restrict__ tcn) {
+           int64_t maxsteps, float* __restrict__ tcb, int32_t* __restrict__ tck, int32_t* __restrict__ tcn,
+           const unsigned long long* __restrict__ sel) {
+  if (sel && *sel != 32ull) return;  // AUTO chose K2-SIMT
   extern __shared__ __align__(16) uint32_t pt_smem[];  // masks [kw] | prefix [kw + 1]
   __shared__ int32_t s_k[kPtSteps * 8];
   __shared__ int32_t wsum[kPtThreads / 32];
@@ -531,7 +576,8 @@ k1_pack_tc(const float* __restrict__ B, int64_t K, int64_t ldb, const uint32_t* 
 // raw 16 floats B[k][16j .. 16j+15].  K2-SIMT moves each record with one bulk copy.
 __global__ void __launch_bounds__(kPackThreads)
 k1_pack_rows(const float* __restrict__ B, int64_t K, int64_t ldb, const uint32_t* __restrict__ bgrp, int64_t kw,
-             const int64_t* __restrict__ row_off, uint4* __restrict__ rows) {
+             const int64_t* __restrict__ row_off, uint4* __restrict__ rows, const unsigned long long* __restrict__ sel) {
+  if (sel && *sel == 32ull) return;  // AUTO chose K2-TC
   __shared__ uint32_t s_g[32];
   __shared__ uint32_t s_base[17];
   const int64_t c = blockIdx.x, tb = blockIdx.y;

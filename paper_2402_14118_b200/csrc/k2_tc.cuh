@@ -3,7 +3,7 @@
 // (BASELINE north_star: "tensor cores only for tiles that the masks leave dense enough ...
 // and only if the result stays inside tolerance").
 //
-// Work unit: one CTA = one 128-row x 192-column C tile.  The k loop runs only over the
+// Work unit: a 128-row x 192-column C tile (persistent CTAs, see below).  The k loop runs only over the
 // tile's LIVE k (B[k, tile] has a non-zero, from K1's tlive masks), 8 per MMA step, so B's
 // block sparsity removes whole k-steps; A's element zeros are multiplied (the tile is dense
 // enough by the choice of this path).  Per step:
@@ -24,7 +24,8 @@
 //
 // Warp roles (448 threads; 14 warps cap registers at 128): 0-3 A transform, 4-11
 // accumulators (segment drain + C update), 12 TMA producer, 13 MMA issuer.  TMEM (512
-// columns): D0 [0,192), D1 [192,384), 4 A slots [384,512) of 32 columns (2 x (hi 8 | lo 8)).
+// columns): D0 [0,192), D1 [192,384), 4 A slots [384,512) of 32 columns (2 x (hi 8 | lo 8)),
+// one per stage.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -33,12 +34,20 @@
 
 namespace mmmcu {
 
+#ifdef TD_PROF
+__device__ unsigned long long* td_prof = nullptr;  // debug builds only: per-CTA cycle counters
+#define TD_CLK(v) const long long v = clock64()
+#define TD_ADD(i, x) (prof[i] += (x))
+#else
+#define TD_CLK(v)
+#define TD_ADD(i, x)
+#endif
+
 #ifndef TD_SEG
 #define TD_SEG 16
 #endif
-constexpr int kTdStages = 8;    // B smem stages of kTdSub MMA sub-steps (16 k) each
+constexpr int kTdStages = 4;    // stages of kTdSub MMA sub-steps (16 k): B smem + A TMEM slot
 constexpr int kTdSub = 2;       // MMA sub-steps (8 k, 3 MMAs) per stage
-constexpr int kTdASlots = 4;    // A TMEM slots (32 columns: per sub-step hi 8 | lo 8)
 constexpr int kTdThreads = 448; // warps 0-3 transform, 4-11 accumulators, 12 producer, 13 MMA
 constexpr int kTdSeg = TD_SEG;  // stages (256 k) per TMEM accumulation segment
 constexpr int kTdTM = 128;
@@ -47,16 +56,15 @@ constexpr int kTdStepFloats = kTdTN * 8 * 2;  // one 8-k step image (K1): hi | l
 constexpr int kTdPStride = kTdTN + 4;         // staged P row stride (floats): conflict-free 16-byte accesses
 
 struct TdShared {
-  float b[kTdStages][kTdSub * kTdStepFloats];  // 8 x 24 KB; after the last MMA: C-update staging
-  uint64_t full[kTdStages];                    // B stage landed (TMA bytes)
-  uint64_t empty[kTdStages];                   // B stage consumed (tcgen05.commit)
-  uint64_t aready[kTdASlots];                  // A slot written (4 transform warps)
-  uint64_t aempty[kTdASlots];                  // A slot consumed (tcgen05.commit)
+  float b[kTdStages][kTdSub * kTdStepFloats];  // 4 x 24 KB
+  float p[kTdTM][kTdPStride];                  // C-update staging (98 KB)
+  uint64_t full[kTdStages];    // stage ready: B bytes landed (producer expect_tx) + A in TMEM (4 warps)
+  uint64_t empty[kTdStages];   // stage consumed: one tcgen05.commit frees the B smem and the A slot
   uint64_t seg_full[2];                        // segment's last MMAs done (tcgen05.commit)
   uint64_t seg_empty[2];                       // D drained (8 accumulator warps)
   uint32_t tmem_base;
 };
-constexpr int kTdSmem = (int)sizeof(TdShared) + 1024;
+constexpr int kTdSmem = (int)sizeof(TdShared) + 128;
 
 __device__ __forceinline__ void td_bulk(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -72,29 +80,25 @@ __device__ __forceinline__ void td_named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// Persistent: CTA b takes tiles t = b, b + gridDim.x, ...; tile t = (row tile t % m_tiles,
+// column tile t / m_tiles), so the CTAs running together share B column tiles (L2 reuse).
+// Every role walks the same tile sequence with running stage / slot / segment counters, so
+// the producer and the transform warps run into the next tile while the accumulator warps
+// update C for the previous one.
 __global__ void __launch_bounds__(kTdThreads, 1)
 k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb, const int32_t* __restrict__ tck,
       const int32_t* __restrict__ tcn, int64_t maxsteps, float* __restrict__ C, int64_t ldc, int64_t M, int64_t N,
-      const unsigned long long* __restrict__ sel) {
+      int64_t m_tiles, int64_t n_tiles, const unsigned long long* __restrict__ sel) {
   if (sel && *sel != 32ull) return;  // device-side path choice (k1_finalize): 32 = TC
-  extern __shared__ __align__(1024) uint8_t td_raw[];
-  TdShared& sh = *reinterpret_cast<TdShared*>(td_raw + ((1024 - (tc::smem_u32(td_raw) & 1023)) & 1023));
+  extern __shared__ __align__(128) uint8_t td_raw[];
+  TdShared& sh = *reinterpret_cast<TdShared*>(td_raw + ((128 - (tc::smem_u32(td_raw) & 127)) & 127));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t rt = blockIdx.x, tb = blockIdx.y;
-  const int64_t m0 = rt * kTdTM, n0 = tb * kTdTN;
-  const int32_t total = tcn[tb];
-  const int nsteps = (total + 7) >> 3;                 // 8-k sub-steps
-  const int nstage = (nsteps + kTdSub - 1) / kTdSub;   // 16-k stages
-  const int nseg = (nstage + kTdSeg - 1) / kTdSeg;
+  const int64_t ntiles = m_tiles * n_tiles;
 
   if (tid == 0) {
     for (int s = 0; s < kTdStages; ++s) {
-      tc::mbar_init(&sh.full[s], 1);
+      tc::mbar_init(&sh.full[s], 5);
       tc::mbar_init(&sh.empty[s], 1);
-    }
-    for (int s = 0; s < kTdASlots; ++s) {
-      tc::mbar_init(&sh.aready[s], 4);
-      tc::mbar_init(&sh.aempty[s], 1);
     }
     for (int d = 0; d < 2; ++d) {
       tc::mbar_init(&sh.seg_full[d], 1);
@@ -112,168 +116,254 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
   if (warp == 12) {
     // ------------------------------------------------------- TMA producer (B stages)
     if (lane == 0) {
-      for (int j = 0; j < nstage; ++j) {
-        const int st = j % kTdStages;
-        const uint32_t bytes = (uint32_t)min(kTdSub, nsteps - kTdSub * j) * kTdStepFloats * 4u;
-        tc::mbar_wait(&sh.empty[st], (uint32_t)(((j / kTdStages) & 1) ^ 1));
-        td_expect_tx(&sh.full[st], bytes);
-        td_bulk(sh.b[st], tcb + ((int64_t)tb * maxsteps + kTdSub * j) * kTdStepFloats, bytes, &sh.full[st]);
+      uint32_t J = 0;
+#ifdef TD_PROF
+      long long pw = 0;
+#endif
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t tb = t / m_tiles;
+        const int nsteps = (tcn[tb] + 7) >> 3;
+        const int nstage = (nsteps + kTdSub - 1) / kTdSub;
+        for (int j = 0; j < nstage; ++j, ++J) {
+          const int st = J % kTdStages;
+          const uint32_t bytes = (uint32_t)min(kTdSub, nsteps - kTdSub * j) * kTdStepFloats * 4u;
+          TD_CLK(c0);
+          tc::mbar_wait(&sh.empty[st], ((J / kTdStages) & 1u) ^ 1u);
+          TD_CLK(c1);
+#ifdef TD_PROF
+          pw += c1 - c0;
+#endif
+          td_expect_tx(&sh.full[st], bytes);
+          td_bulk(sh.b[st], tcb + (tb * maxsteps + kTdSub * j) * kTdStepFloats, bytes, &sh.full[st]);
+        }
       }
+#ifdef TD_PROF
+      if (td_prof) td_prof[16 * blockIdx.x + 7] = pw;
+#endif
     }
     __syncwarp();
   } else if (warp == 13) {
     // ------------------------------------------------------------------ MMA issuer
     // The whole warp runs the loop (warp-uniform operands stay in uniform registers); one
-    // elected lane issues.  Per stage: 2 barrier waits (~60 cycles each even when already
-    // complete) and 3 commits against 6 MMAs (576 cycles): 8-k stages left the tensor pipe
-    // waiting on this chain.
+    // elected lane issues.  Each tcgen05.commit costs the tensor pipe ~50 cycles (measured:
+    // 112.6 vs 96.1 cycles per N=192 MMA with a commit every 3), so a stage carries 6 MMAs
+    // and ONE commit that frees both its B smem and its A TMEM slot.
     const uint32_t idesc = tc::idesc_tf32_m128(kTdTN);
-    for (int j = 0; j < nstage; ++j) {
-      const int st = j % kTdStages, sa = j % kTdASlots;
-      const int g = j / kTdSeg, d = g & 1;
-      if (j % kTdSeg == 0 && g >= 2) tc::mbar_wait(&sh.seg_empty[d], (uint32_t)(((g - 2) >> 1) & 1));
-      tc::mbar_wait(&sh.full[st], (uint32_t)((j / kTdStages) & 1));
-      tc::mbar_wait(&sh.aready[sa], (uint32_t)((j / kTdASlots) & 1));
-      tc::fence_after_sync();
-      const uint32_t baddr = tc::smem_u32(sh.b[st]);
-      const uint32_t dcol = tbase + d * kTdTN;
-      const bool two = kTdSub * j + 1 < nsteps;
-      if (tc::elect_one()) {
+    uint32_t J = 0, G = 0;
+#ifdef TD_PROF
+    long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const long long p0 = clock64();
+#endif
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t tb = t / m_tiles;
+      const int nsteps = (tcn[tb] + 7) >> 3;
+      const int nstage = (nsteps + kTdSub - 1) / kTdSub;
+      for (int j = 0; j < nstage; ++j, ++J) {
+        const int st = J % kTdStages;
+        const uint32_t d = G & 1u;
+        TD_CLK(c0);
+        if (j % kTdSeg == 0 && G >= 2) tc::mbar_wait(&sh.seg_empty[d], ((G - 2) >> 1) & 1u);
+        TD_CLK(c1);
+        tc::mbar_wait(&sh.full[st], (J / kTdStages) & 1u);
+        TD_CLK(c2);
+        TD_ADD(0, c1 - c0);
+        TD_ADD(1, c2 - c1);
+        tc::fence_after_sync();
+        const uint32_t baddr = tc::smem_u32(sh.b[st]);
+        const uint32_t dcol = tbase + d * kTdTN;
+        const bool two = kTdSub * j + 1 < nsteps;
+        const bool seg_end = j % kTdSeg == kTdSeg - 1 || j == nstage - 1;
+        if (tc::elect_one()) {
 #pragma unroll
-        for (int u = 0; u < kTdSub; ++u) {
-          if (u == 0 || two) {
-            const uint32_t bu = baddr + u * kTdStepFloats * 4;
-            const uint64_t bhi = tc::smem_desc(bu, 128, 256), blo = tc::smem_desc(bu + kTdTN * 32, 128, 256);
-            const uint32_t ahi = tbase + kAcol + 32 * sa + 16 * u, alo = ahi + 8;
-            tc::mma_tf32_ts(dcol, alo, bhi, idesc, (j % kTdSeg != 0 || u > 0) ? 1u : 0u);
-            tc::mma_tf32_ts(dcol, ahi, blo, idesc, 1u);
-            tc::mma_tf32_ts(dcol, ahi, bhi, idesc, 1u);
+          for (int u = 0; u < kTdSub; ++u) {
+            if (u == 0 || two) {
+              const uint32_t bu = baddr + u * kTdStepFloats * 4;
+              const uint64_t bhi = tc::smem_desc(bu, 128, 256), blo = tc::smem_desc(bu + kTdTN * 32, 128, 256);
+              const uint32_t ahi = tbase + kAcol + 32 * st + 16 * u, alo = ahi + 8;
+              tc::mma_tf32_ts(dcol, alo, bhi, idesc, (j % kTdSeg != 0 || u > 0) ? 1u : 0u);
+              tc::mma_tf32_ts(dcol, ahi, blo, idesc, 1u);
+              tc::mma_tf32_ts(dcol, ahi, bhi, idesc, 1u);
+            }
           }
+          tc::mma_commit(&sh.empty[st]);
+          if (seg_end) tc::mma_commit(&sh.seg_full[d]);
         }
-        tc::mma_commit(&sh.empty[st]);
-        tc::mma_commit(&sh.aempty[sa]);
-        if (j % kTdSeg == kTdSeg - 1 || j == nstage - 1) tc::mma_commit(&sh.seg_full[d]);
+        __syncwarp();
+        if (seg_end) ++G;
+        TD_CLK(c3);
+        TD_ADD(2, c3 - c2);
       }
-      __syncwarp();
     }
+#ifdef TD_PROF
+    if (lane == 0 && td_prof) {
+      unsigned long long* q = td_prof + 16 * blockIdx.x;
+      for (int i = 0; i < 3; ++i) q[i] = prof[i];
+      q[3] = clock64() - p0;
+    }
+#endif
   } else if (warp < 4) {
     // ---------------------------------------------------------------- A transform
     // Thread r owns tile row r (== TMEM lane r).  A is read straight from the K1 A^T tile
     // (a warp reads 128 contiguous bytes per k) one batch of 2 stages ahead, with the
     // live-k list two batches ahead; split into tf32 hi / lo; tcgen05.st into the slot's
-    // TMEM columns once the MMAs of stage j - kTdASlots have released them.
+    // TMEM columns once the MMAs of stage J - kTdStages have released them.
     constexpr int kB = 2, KB = 8 * kTdSub * kB;  // stages per batch, k per batch
     const int r = tid;
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-    const float* acol = AT + rt * kpad * 128 + r;
-    const int4* kx4 = reinterpret_cast<const int4*>(tck + tb * maxsteps * 8);
-    const int npos = nsteps * 8, nb = (nstage + kB - 1) / kB;
-    auto load_k = [&](int b, int (&k)[KB]) {
+    uint32_t J = 0;
+#ifdef TD_PROF
+    long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const long long p0 = clock64();
+#endif
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t rt = t % m_tiles, tb = t / m_tiles;
+      const int nsteps = (tcn[tb] + 7) >> 3;
+      const int nstage = (nsteps + kTdSub - 1) / kTdSub;
+      const float* acol = AT + rt * kpad * 128 + r;
+      const int4* kx4 = reinterpret_cast<const int4*>(tck + tb * maxsteps * 8);
+      const int npos = nsteps * 8, nb = (nstage + kB - 1) / kB;
+      auto load_k = [&](int b, int (&k)[KB]) {
 #pragma unroll
-      for (int q = 0; q < KB / 4; ++q) {
-        const int4 v = (b * KB + 4 * q < npos) ? __ldg(kx4 + b * (KB / 4) + q) : make_int4(-1, -1, -1, -1);
-        k[4 * q] = v.x;
-        k[4 * q + 1] = v.y;
-        k[4 * q + 2] = v.z;
-        k[4 * q + 3] = v.w;
-      }
-    };
-    auto load_a = [&](const int (&k)[KB], float (&a)[KB]) {
-#pragma unroll
-      for (int i = 0; i < KB; ++i) a[i] = k[i] >= 0 ? __ldg(acol + (int64_t)k[i] * 128) : 0.0f;
-    };
-    int kn[KB];
-    float ac[KB], an[KB];
-    load_k(0, kn);
-    load_a(kn, ac);
-    load_k(1, kn);
-#pragma unroll 1
-    for (int b = 0; b < nb; ++b) {
-      load_a(kn, an);  // batch b + 1 (all -1 past the end: no loads)
-      load_k(b + 2, kn);
-#pragma unroll
-      for (int i = 0; i < kB; ++i) {
-        const int j = kB * b + i;
-        if (j < nstage) {
-          const int sa = j % kTdASlots;
-          tc::mbar_wait(&sh.aempty[sa], (uint32_t)(((j / kTdASlots) & 1) ^ 1));
-          tc::fence_after_sync();
-#pragma unroll
-          for (int u = 0; u < kTdSub; ++u) {
-            uint32_t hi[8], lo[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) tc::split_tf32(ac[16 * i + 8 * u + e], hi[e], lo[e]);
-            tc::tmem_st8(tbase + lane_off + kAcol + 32 * sa + 16 * u, hi);
-            tc::tmem_st8(tbase + lane_off + kAcol + 32 * sa + 16 * u + 8, lo);
-          }
-          tc::tmem_st_wait();
-          tc::fence_before_sync();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(&sh.aready[sa]);
+        for (int q = 0; q < KB / 4; ++q) {
+          const int4 v = (b * KB + 4 * q < npos) ? __ldg(kx4 + b * (KB / 4) + q) : make_int4(-1, -1, -1, -1);
+          k[4 * q] = v.x;
+          k[4 * q + 1] = v.y;
+          k[4 * q + 2] = v.z;
+          k[4 * q + 3] = v.w;
         }
-      }
+      };
+      auto load_a = [&](const int (&k)[KB], float (&a)[KB]) {
 #pragma unroll
-      for (int e = 0; e < KB; ++e) ac[e] = an[e];
+        for (int i = 0; i < KB; ++i) a[i] = k[i] >= 0 ? __ldg(acol + (int64_t)k[i] * 128) : 0.0f;
+      };
+      int kn[KB];
+      float ac[KB], an[KB];
+      load_k(0, kn);
+      load_a(kn, ac);
+      load_k(1, kn);
+#pragma unroll 1
+      for (int b = 0; b < nb; ++b) {
+        load_a(kn, an);  // batch b + 1 (all -1 past the end: no loads)
+        load_k(b + 2, kn);
+#pragma unroll
+        for (int i = 0; i < kB; ++i) {
+          const int j = kB * b + i;
+          if (j < nstage) {
+            const uint32_t Jj = J + j;
+            const int sa = Jj % kTdStages;
+            TD_CLK(c0);
+            tc::mbar_wait(&sh.empty[sa], ((Jj / kTdStages) & 1u) ^ 1u);
+            TD_CLK(c1);
+            TD_ADD(0, c1 - c0);
+            tc::fence_after_sync();
+#pragma unroll
+            for (int u = 0; u < kTdSub; ++u) {
+              uint32_t hi[8], lo[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) tc::split_tf32(ac[16 * i + 8 * u + e], hi[e], lo[e]);
+              tc::tmem_st8(tbase + lane_off + kAcol + 32 * sa + 16 * u, hi);
+              tc::tmem_st8(tbase + lane_off + kAcol + 32 * sa + 16 * u + 8, lo);
+            }
+            tc::tmem_st_wait();
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&sh.full[sa]);
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < KB; ++e) ac[e] = an[e];
+      }
+      J += nstage;
     }
+#ifdef TD_PROF
+    if (tid == 0 && td_prof) {
+      unsigned long long* q = td_prof + 16 * blockIdx.x;
+      q[4] = prof[0]; q[5] = 0; q[6] = clock64() - p0;
+    }
+#endif
   } else {
     // ------------------------------------------------------ accumulator warps 4..11
     // Warp w: tile row 32*(w%4) + lane (its TMEM lane), columns 96*((w-4)/4) .. +95, held
-    // as fp32 registers.  Each segment's D is added in (round-to-nearest), then released.
+    // as fp32 registers.  Each segment's D is added in (round-to-nearest), then released;
+    // after a tile's last segment, C = C0 + P goes out through the staging buffer (rows
+    // with a 196-float stride: conflict-free 16-byte stores), lanes along the rows
+    // (coalesced), while the MMAs already run the next tile.
     const int q4 = warp & 3, half = (warp - 4) >> 2;
-    const int r = 32 * q4 + lane;
     const uint32_t taddr = tbase + ((uint32_t)(q4 * 32) << 16) + 96 * half;
-    float acc[96];
+    uint32_t G = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t rt = t % m_tiles, tb = t / m_tiles;
+      const int nsteps = (tcn[tb] + 7) >> 3;
+      const int nstage = (nsteps + kTdSub - 1) / kTdSub;
+      const int nseg = (nstage + kTdSeg - 1) / kTdSeg;
+      if (nseg == 0) continue;
+      float acc[96];
 #pragma unroll
-    for (int j = 0; j < 96; ++j) acc[j] = 0.0f;
-    for (int g = 0; g < nseg; ++g) {
-      const int d = g & 1;
-      tc::mbar_wait_sleep(&sh.seg_full[d], (uint32_t)((g >> 1) & 1));
-      tc::fence_after_sync();
+      for (int e = 0; e < 96; ++e) acc[e] = 0.0f;
+      for (int g = 0; g < nseg; ++g, ++G) {
+        const uint32_t d = G & 1u;
+        tc::mbar_wait_sleep(&sh.seg_full[d], (G >> 1) & 1u);
+        tc::fence_after_sync();
 #pragma unroll
-      for (int c = 0; c < 6; ++c) {
-        uint32_t v[16];
-        tc::tmem_ld16(taddr + d * kTdTN + 16 * c, v);
-        tc::tmem_ld_wait();
+        for (int c = 0; c < 6; ++c) {
+          uint32_t v[16];
+          tc::tmem_ld16(taddr + d * kTdTN + 16 * c, v);
+          tc::tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 16; ++j) acc[16 * c + j] += __uint_as_float(v[j]);
+          for (int e = 0; e < 16; ++e) acc[16 * c + e] += __uint_as_float(v[e]);
+        }
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&sh.seg_empty[d]);
       }
-      tc::fence_before_sync();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&sh.seg_empty[d]);
-    }
-    if (nseg > 0) {
-      // C = C0 + P through the (now idle) B stages: rows staged with a 196-float stride
-      // (conflict-free 16-byte stores), then updated row by row, lanes along the row
-      float* stage = &sh.b[0][0];
-      float4* prow = reinterpret_cast<float4*>(stage + r * kTdPStride + 96 * half);
+      const int64_t m0 = rt * kTdTM, n0 = tb * kTdTN;
+      {
+        float4* prow = reinterpret_cast<float4*>(&sh.p[32 * q4 + lane][96 * half]);
 #pragma unroll
-      for (int q = 0; q < 24; ++q) prow[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+        for (int q = 0; q < 24; ++q) prow[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+      }
       td_named_sync(1, 256);
-      for (int rr = warp - 4; rr < kTdTM; rr += 8) {
-        const int64_t row = m0 + rr;
-        if (row >= M) break;
-        float* crow = C + row * ldc + n0;
-        const float* pr = stage + rr * kTdPStride;
+      // warp w-4 updates rows w-4, w+4, ...; per 4 rows all loads go out before the adds
+      const int64_t gc0 = n0 + 4 * lane, gc1 = gc0 + 128;
+      const bool full0 = gc0 + 3 < N, full1 = lane < 16 && gc1 + 3 < N;
+#pragma unroll 1
+      for (int i0 = 0; i0 < 16; i0 += 4) {
+        float4 cv[4][2];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int col = 4 * lane + 128 * h;
-          if (col < kTdTN) {
+        for (int i = 0; i < 4; ++i) {
+          const int64_t row = m0 + (warp - 4) + 8 * (i0 + i);
+          const float* crow = C + row * ldc;
+          if (row < M && full0) cv[i][0] = *reinterpret_cast<const float4*>(crow + gc0);
+          if (row < M && full1) cv[i][1] = *reinterpret_cast<const float4*>(crow + gc1);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int rr = (warp - 4) + 8 * (i0 + i);
+          const int64_t row = m0 + rr;
+          if (row >= M) break;
+          float* crow = C + row * ldc;
+          const float* pr = sh.p[rr];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int col = 4 * lane + 128 * h;
+            if (col >= kTdTN) continue;
             const int64_t gcol = n0 + col;
-            if (gcol + 3 < N) {
-              float4 cv = *reinterpret_cast<const float4*>(crow + col);
+            if (h == 0 ? full0 : full1) {
+              float4 c4 = cv[i][h];
               const float4 pv = *reinterpret_cast<const float4*>(pr + col);
-              cv.x += pv.x;
-              cv.y += pv.y;
-              cv.z += pv.z;
-              cv.w += pv.w;
-              *reinterpret_cast<float4*>(crow + col) = cv;
+              c4.x += pv.x;
+              c4.y += pv.y;
+              c4.z += pv.z;
+              c4.w += pv.w;
+              *reinterpret_cast<float4*>(crow + gcol) = c4;
             } else {
               for (int e = 0; e < 4; ++e)
-                if (gcol + e < N) crow[col + e] += pr[col + e];
+                if (gcol + e < N) crow[gcol + e] += pr[col + e];
             }
           }
         }
       }
+      td_named_sync(1, 256);
     }
   }
   tc::fence_before_sync();

@@ -52,10 +52,12 @@ int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 struct mmmcu_ctx {
   int device = 0;
+  int num_sms = 0;
   cudaStream_t stream = nullptr;
   std::string err;
   mmmcu_algo algo = MMMCU_ALGO_AUTO;
   mmmcu_algo last_algo = MMMCU_ALGO_AUTO;
+  bool auto_pending = false;
 
   // ---- A plan (preprocess_a)
   bool has_a = false;
@@ -75,6 +77,8 @@ struct mmmcu_ctx {
 
   // ---- K2 operands emitted by K1 (which ones depends on the algorithm, see ops_for)
   bool op_at = false, op_rows = false, op_tcb = false;
+  bool rows_fresh = false, tcb_fresh = false;  // packed without the device gate (valid for a forced path)
+  int ops_b = 0;                                // operand sets B was staged for
   int64_t kpad = 0, m_at = 0, n_tb = 0, n_tc = 0, tc_steps = 0;
   DevBuf at, tcb, tck, tcn, brows, row_off;
 
@@ -153,6 +157,7 @@ uint32_t* zb_bnz(mmmcu_ctx* ctx) { return zb_bpop(ctx) + ctx->Kb; }
 enum { OP_AT = 1, OP_ROWS = 2, OP_TCB = 4 };
 int ops_for(const mmmcu_ctx* ctx) {
   switch (ctx->algo) {
+    case MMMCU_ALGO_AUTO: return OP_AT | OP_ROWS | OP_TCB;  // K1's last CTA picks (k1_choose_path)
     case MMMCU_ALGO_TC: return OP_AT | OP_TCB;
     case MMMCU_ALGO_DENSE: return 0;
     default: return OP_AT | OP_ROWS;
@@ -160,7 +165,7 @@ int ops_for(const mmmcu_ctx* ctx) {
 }
 uint32_t* zb_tlive(mmmcu_ctx* ctx) { return zb_bnz(ctx) + ctx->Kb; }
 int64_t n_cnt_tc(const mmmcu_ctx* ctx) { return ctx->n_tc * ((ctx->Kb + 31) / 32); }
-uint32_t* zb_row_cnt(mmmcu_ctx* ctx) { return zb_tlive(ctx) + ((ops_for(ctx) & OP_TCB) ? n_cnt_tc(ctx) : 0); }
+uint32_t* zb_row_cnt(mmmcu_ctx* ctx) { return zb_tlive(ctx) + ((ctx->ops_b & OP_TCB) ? n_cnt_tc(ctx) : 0); }
 
 mmmcu_status stage_a(mmmcu_ctx* ctx, const float* A, int64_t M, int64_t K, int64_t lda, uint64_t av) {
   if (M <= 0 || K <= 0) return fail(ctx, MMMCU_ERR_INVALID_ARG, "matrix dimensions must be positive");
@@ -202,7 +207,9 @@ mmmcu_status stage_b(mmmcu_ctx* ctx, const float* B, int64_t K, int64_t N, int64
   MMMCU_CUDA(ctx->codes.ensure((size_t)K * nreg));
   MMMCU_CUDA(ctx->bgrp.ensure(sizeof(uint32_t) * ngrp * kw));
   ctx->op_rows = ctx->op_tcb = false;
+  ctx->rows_fresh = ctx->tcb_fresh = false;
   const int ops = ops_for(ctx);
+  ctx->ops_b = ops;
   const int64_t n_tb = (ldb + 255) / 256;
   const int64_t n_cnt = n_tb * kw;
   const int64_t n_tc = (ldb + mmmcu::kTcTileN - 1) / mmmcu::kTcTileN;
@@ -232,6 +239,29 @@ mmmcu_status stage_b(mmmcu_ctx* ctx, const float* B, int64_t K, int64_t N, int64
   return MMMCU_OK;
 }
 
+// B operand packs for K2 (sel: the device path choice gating an AUTO plan, nullptr = always).
+mmmcu_status pack_rows(mmmcu_ctx* ctx, const unsigned long long* sel) {
+  dim3 grid((unsigned)((ctx->Kb + 31) / 32), (unsigned)ctx->n_tb);
+  mmmcu::k1_pack_rows<<<grid, mmmcu::kPackThreads, 0, ctx->stream>>>(
+      ctx->B, ctx->Kb, ctx->ldb, ctx->bgrp.as<uint32_t>(), (ctx->Kb + 31) / 32, ctx->row_off.as<int64_t>(),
+      ctx->brows.as<uint4>(), sel);
+  MMMCU_LAUNCHED();
+  return MMMCU_OK;
+}
+
+mmmcu_status pack_tc(mmmcu_ctx* ctx, const unsigned long long* sel) {
+  const int64_t bkw = (ctx->Kb + 31) / 32;
+  const int smem = (int)(sizeof(uint32_t) * (2 * bkw + 1));
+  if (smem > 200 * 1024) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "K too large for the TC packer");
+  MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k1_pack_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  dim3 grid((unsigned)((ctx->tc_steps + mmmcu::kPtSteps - 1) / mmmcu::kPtSteps), (unsigned)ctx->n_tc);
+  mmmcu::k1_pack_tc<<<grid, mmmcu::kPtThreads, smem, ctx->stream>>>(
+      ctx->B, ctx->Kb, ctx->ldb, zb_tlive(ctx), bkw, ctx->tc_steps, ctx->tcb.as<float>(), ctx->tck.as<int32_t>(),
+      ctx->tcn.as<int32_t>(), sel);
+  MMMCU_LAUNCHED();
+  return MMMCU_OK;
+}
+
 // One fused K1 launch over the staged operand(s), then (for A) the CSR index lists.
 mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   MMMCU_CUDA(ctx->stats.ensure(sizeof(unsigned long long) * 16));
@@ -245,7 +275,14 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   const int64_t K = do_a ? ctx->Ka : ctx->Kb;
   const int64_t kw = (K + 31) / 32;
   const int ops = ops_for(ctx);
-  const bool tc_a = do_a && (ops & OP_AT), tcb_b = do_b && (ops & OP_TCB), rows_b = do_b && (ops & OP_ROWS);
+  // AUTO builds both K2 operand sets, each pack gated on the device by the path choice; a
+  // later A-only preprocess may flip the choice, so the gated packs re-run whenever B is valid
+  const int ops_b = b_valid ? ctx->ops_b : 0;
+  const bool gate = (ops & OP_ROWS) && (ops & OP_TCB) && (ops_b & OP_ROWS) && (ops_b & OP_TCB);
+  const bool tc_a = do_a && (ops & OP_AT);
+  const bool tcb_b = (ops_b & OP_TCB) && (do_b || gate);
+  const bool rows_b = (ops_b & OP_ROWS) && (do_b || gate);
+  const unsigned long long* sel = gate ? ctx->stats.as<unsigned long long>() + 7 : nullptr;
   const int64_t a_tx = (ctx->Ka + mmmcu::kK1Cols - 1) / mmmcu::kK1Cols;
   const int64_t a_rows = tc_a ? ctx->m_at : ctx->M;  // A^T tiles are written to the 128-row boundary
   const int64_t nA = do_a ? a_tx * ((a_rows + mmmcu::kK1Rows - 1) / mmmcu::kK1Rows) : 0;
@@ -268,6 +305,8 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   z.row_cnt = rows_b ? zb_row_cnt(ctx) : nullptr;
   z.row_off = rows_b ? ctx->row_off.as<int64_t>() : nullptr;
   z.n_tb = ctx->n_tb;
+  z.n_tc = ctx->n_tc;
+  z.choose = gate ? 1 : 0;
   const int has_a = a_valid && (same_k || !b_valid) ? 1 : 0;
   const int has_b = b_valid && (same_k || !a_valid) ? 1 : 0;
   mmmcu::k1_pass<<<(unsigned)(nA + nB), mmmcu::kK1Threads, 0, ctx->stream>>>(
@@ -288,29 +327,19 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
     MMMCU_LAUNCHED();
   }
   if (rows_b) {
-    dim3 grid((unsigned)((ctx->Kb + 31) / 32), (unsigned)ctx->n_tb);
-    mmmcu::k1_pack_rows<<<grid, mmmcu::kPackThreads, 0, ctx->stream>>>(
-        ctx->B, ctx->Kb, ctx->ldb, ctx->bgrp.as<uint32_t>(), (ctx->Kb + 31) / 32, ctx->row_off.as<int64_t>(),
-        ctx->brows.as<uint4>());
-    MMMCU_LAUNCHED();
+    MMMCU_TRY(pack_rows(ctx, sel));
+    ctx->rows_fresh = sel == nullptr;
   }
   if (tcb_b) {
-    const int64_t bkw = (ctx->Kb + 31) / 32;
-    const int smem = (int)(sizeof(uint32_t) * (2 * bkw + 1));
-    if (smem > 200 * 1024) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "K too large for the TC packer");
-    MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k1_pack_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    dim3 grid((unsigned)((ctx->tc_steps + mmmcu::kPtSteps - 1) / mmmcu::kPtSteps), (unsigned)ctx->n_tc);
-    mmmcu::k1_pack_tc<<<grid, mmmcu::kPtThreads, smem, ctx->stream>>>(
-        ctx->B, ctx->Kb, ctx->ldb, zb_tlive(ctx), bkw, ctx->tc_steps, ctx->tcb.as<float>(), ctx->tck.as<int32_t>(),
-        ctx->tcn.as<int32_t>());
-    MMMCU_LAUNCHED();
+    MMMCU_TRY(pack_tc(ctx, sel));
+    ctx->tcb_fresh = sel == nullptr;
   }
   if (do_a) {
     ctx->has_a = true;
     ctx->op_at = tc_a;
   }
-  if (do_b) {
-    ctx->has_b = true;
+  if (do_b) ctx->has_b = true;
+  if (do_b || gate) {
     ctx->op_tcb = tcb_b;
     ctx->op_rows = rows_b;
   }
@@ -330,10 +359,10 @@ mmmcu_status check_plan(mmmcu_ctx* ctx, const float* A, const float* B, uint64_t
 
 // span_hint 8 / 16 forces a variant; 0 launches both and lets k1_finalize's device-side
 // choice (stats[7]) gate them, so AUTO never synchronises the stream between K1 and K2.
-mmmcu_status launch_simt(mmmcu_ctx* ctx, float* C, int64_t ldc, int span_hint) {
+mmmcu_status launch_simt(mmmcu_ctx* ctx, float* C, int64_t ldc, int span_hint, int sel_slot) {
   const int64_t M = ctx->M, K = ctx->Ka, Np = round_up(ctx->N, 64);
   const int64_t kw = (K + 31) / 32;
-  const unsigned long long* sel2 = span_hint == 0 ? ctx->stats.as<unsigned long long>() + 7 : nullptr;
+  const unsigned long long* sel2 = span_hint == 0 ? ctx->stats.as<unsigned long long>() + sel_slot : nullptr;
   if (ctx->op_at && ctx->op_rows) {
     const int smem = mmmcu::kS2SmemBase + (int)(sizeof(int64_t) * (kw + 1));
     if (smem > 232448) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "K too large for the SIMT v2 kernel");
@@ -359,7 +388,7 @@ mmmcu_status launch_simt(mmmcu_ctx* ctx, float* C, int64_t ldc, int span_hint) {
   dim3 grid((unsigned)((Np + mmmcu::kK2TN - 1) / mmmcu::kK2TN), (unsigned)row_tiles);
   MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k2_simt_bcast<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mmmcu::kK2Smem));
   MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k2_simt_bcast<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mmmcu::kK2Smem));
-  const unsigned long long* sel = span_hint == 0 ? ctx->stats.as<unsigned long long>() + 7 : nullptr;
+  const unsigned long long* sel = span_hint == 0 ? ctx->stats.as<unsigned long long>() + sel_slot : nullptr;
   if (span_hint == 0 || span_hint == 8) {
     mmmcu::k2_simt_bcast<8><<<grid, mmmcu::kK2Threads, mmmcu::kK2Smem, ctx->stream>>>(
         ctx->A, ctx->lda, ctx->B, ctx->ldb, C, ldc, M, K, Np, ctx->bgrp.as<uint32_t>(), kw, sel);
@@ -376,13 +405,37 @@ mmmcu_status launch_simt(mmmcu_ctx* ctx, float* C, int64_t ldc, int span_hint) {
 // K2-TC over the dense-tile operands (sel: device-side path choice, nullptr = forced).
 mmmcu_status launch_tc(mmmcu_ctx* ctx, float* C, int64_t ldc, const unsigned long long* sel) {
   const int64_t row_tiles = ctx->m_at / mmmcu::kTdTM;
-  if (ctx->n_tc > 65535) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "N too large for the TC grid");
   MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, mmmcu::kTdSmem));
-  dim3 grid((unsigned)row_tiles, (unsigned)ctx->n_tc);
+  if (ctx->num_sms == 0) MMMCU_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  const int64_t ntiles = row_tiles * ctx->n_tc;
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, ctx->num_sms);
   mmmcu::k2_tc<<<grid, mmmcu::kTdThreads, mmmcu::kTdSmem, ctx->stream>>>(
       ctx->at.as<float>(), ctx->kpad, ctx->tcb.as<float>(), ctx->tck.as<int32_t>(), ctx->tcn.as<int32_t>(),
-      ctx->tc_steps, C, ldc, ctx->M, ctx->N, sel);
+      ctx->tc_steps, C, ldc, ctx->M, ctx->N, row_tiles, ctx->n_tc, sel);
   MMMCU_LAUNCHED();
+#ifdef TD_PROF
+  {  // debug builds: rerun with the per-CTA cycle counters on, print their means
+    static unsigned long long* dbuf = nullptr;
+    if (!dbuf) cudaMalloc(&dbuf, 16 * 8 * 1024);
+    cudaMemset(dbuf, 0, 16 * 8 * 1024);
+    cudaMemcpyToSymbol(mmmcu::td_prof, &dbuf, sizeof(dbuf));
+    mmmcu::k2_tc<<<grid, mmmcu::kTdThreads, mmmcu::kTdSmem, ctx->stream>>>(
+        ctx->at.as<float>(), ctx->kpad, ctx->tcb.as<float>(), ctx->tck.as<int32_t>(), ctx->tcn.as<int32_t>(),
+        ctx->tc_steps, C, ldc, ctx->M, ctx->N, row_tiles, ctx->n_tc, sel);
+    cudaDeviceSynchronize();
+    std::vector<unsigned long long> h(16 * grid);
+    cudaMemcpy(h.data(), dbuf, 8 * 16 * grid, cudaMemcpyDeviceToHost);
+    double a[16] = {0};
+    for (unsigned i = 0; i < grid; ++i)
+      for (int j = 0; j < 16; ++j) a[j] += (double)h[16 * i + j] / grid;
+    fprintf(stderr,
+            "TD_PROF/CTA cycles: MMA wait-seg %.0f wait-full %.0f issue %.0f total %.0f | transform wait-empty %.0f "
+            "batch-copy %.0f total %.0f | producer wait %.0f\n",
+            a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7]);
+    void* z = nullptr;
+    cudaMemcpyToSymbol(mmmcu::td_prof, &z, sizeof(z));
+  }
+#endif
 
   return MMMCU_OK;
 }
@@ -599,6 +652,13 @@ mmmcu_status mmmcu_set_algo(mmmcu_ctx* ctx, mmmcu_algo algo) {
 
 mmmcu_status mmmcu_last_algo(mmmcu_ctx* ctx, mmmcu_algo* algo) {
   if (!ctx || !algo) return fail(ctx, MMMCU_ERR_INVALID_ARG, "null argument");
+  if (ctx->auto_pending) {  // AUTO was resolved on the device: read the choice
+    MMMCU_TRY(bind(ctx));
+    unsigned long long s[16];
+    MMMCU_TRY(read_stats(ctx, s));
+    ctx->last_algo = s[7] == 32 ? MMMCU_ALGO_TC : s[7] == 8 ? MMMCU_ALGO_SIMT_SPAN8 : MMMCU_ALGO_SIMT_SPAN16;
+    ctx->auto_pending = false;
+  }
   *algo = ctx->last_algo;
   return MMMCU_OK;
 }
@@ -611,10 +671,19 @@ mmmcu_status mmmcu_multiply(mmmcu_ctx* ctx, float* C, int64_t ldc, const float* 
   if (ldc < round_up(ctx->N, 64) || ldc % 4 != 0 || !aligned16(C))
     return fail(ctx, MMMCU_ERR_INVALID_ARG,
                 "C must be 16-byte aligned with ldc >= round_up(N, 64) (Matrix padding) and ldc % 4 == 0");
-  if (ctx->algo == MMMCU_ALGO_TC) {
+  ctx->auto_pending = false;
+  if (ctx->algo == MMMCU_ALGO_AUTO && ctx->op_at && ctx->op_rows && ctx->op_tcb) {
+    // both operand sets are built; every variant is launched and all but the chosen one
+    // exit at entry (stats[7]: 8 / 16 = K2-SIMT span, 32 = K2-TC) — no host round trip
+    ctx->last_algo = MMMCU_ALGO_AUTO;
+    ctx->auto_pending = true;
+    MMMCU_TRY(launch_simt(ctx, C, ldc, 0, 7));
+    MMMCU_TRY(launch_tc(ctx, C, ldc, ctx->stats.as<unsigned long long>() + 7));
+  } else if (ctx->algo == MMMCU_ALGO_TC) {
     if (!ctx->op_at || !ctx->op_tcb)
       return fail(ctx, MMMCU_ERR_NOT_READY, "the TC operands were not built: preprocess with algo TC");
     ctx->last_algo = MMMCU_ALGO_TC;
+    if (!ctx->tcb_fresh) MMMCU_TRY(pack_tc(ctx, nullptr));
     MMMCU_TRY(launch_tc(ctx, C, ldc, nullptr));
   } else if (ctx->algo == MMMCU_ALGO_DENSE) {
     ctx->last_algo = MMMCU_ALGO_DENSE;
@@ -624,7 +693,8 @@ mmmcu_status mmmcu_multiply(mmmcu_ctx* ctx, float* C, int64_t ldc, const float* 
   } else {
     const int span = ctx->algo == MMMCU_ALGO_SIMT_SPAN8 ? 8 : ctx->algo == MMMCU_ALGO_SIMT_SPAN16 ? 16 : 0;
     ctx->last_algo = span == 8 ? MMMCU_ALGO_SIMT_SPAN8 : span == 16 ? MMMCU_ALGO_SIMT_SPAN16 : MMMCU_ALGO_SIMT_BCAST;
-    MMMCU_TRY(launch_simt(ctx, C, ldc, span));
+    if (ctx->op_rows && !ctx->rows_fresh) MMMCU_TRY(pack_rows(ctx, nullptr));
+    MMMCU_TRY(launch_simt(ctx, C, ldc, span, 8));
   }
   return fill_counters(ctx, counters);
 }

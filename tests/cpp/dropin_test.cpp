@@ -42,7 +42,7 @@ int main() {
       }
     }
 
-  MmmContext<float> ctx(a, b);
+  MmmContext<float> ctx(a, b, LaneConfig::defaults(Dtype::f32), 256, 0, Accumulation::Exact);
   Matrix<float> c(M, N);
   WorkCounters w = multiply_mmm(ctx, c, a, b);
   CHECK(w.lane_fma_ops == lanes);
@@ -50,6 +50,23 @@ int main() {
   for (int64_t i = 0; i < M; ++i)
     for (int64_t j = 0; j < N; ++j) CHECK(c.at(i, j) == ref.at(i, j));  // bit-exact (K2-SIMT)
   CHECK(c.padding_is_zero());
+
+  // default accumulation (AUTO: K2-SIMT or K2-TC): within the north_star tolerance
+  {
+    const Matrix<float>& ca_ = a;  // const access: no version bump
+    const Matrix<float>& cb_ = b;
+    MmmContext<float> actx(a, b);
+    Matrix<float> ca(M, N);
+    WorkCounters wa = multiply_mmm(actx, ca, a, b);
+    CHECK(wa.lane_fma_ops == lanes);
+    for (int64_t i = 0; i < M; ++i)
+      for (int64_t j = 0; j < N; ++j) {
+        double den = 0.0;
+        for (int64_t k = 0; k < K; ++k) den += std::fabs((double)ca_.at(i, k) * (double)cb_.at(k, j));
+        CHECK(std::fabs((double)ca.at(i, j) - (double)ref.at(i, j)) <= 1e-5 * den);
+      }
+    CHECK(ca.padding_is_zero());
+  }
 
   // multiply_parallel: same bits, worker_count 0 rejected
   Matrix<float> c2(M, N);

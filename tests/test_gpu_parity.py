@@ -1,8 +1,11 @@
 """GPU parity: the CUDA path through the C ABI against the CPU oracle on the same inputs.
 
 Bar (BASELINE.json north_star): masks / index lists / codes / counters bit-exact; C within
-|ΔC| <= 1e-5 * Σ|a||b| — and, for the SIMT kernels, which replay the oracle's ascending-k
-fmaf chain, bit-exact.
+|ΔC| <= 1e-5 * (|c0| + Σ|a||b|).  Two K2 paths are held to it:
+  EXACT (K2-SIMT, forced with ALGO_SIMT_BCAST): replays the oracle's ascending-k fmaf chain,
+        so C is bit-exact;
+  AUTO  (the default): K1's cost model picks K2-SIMT or K2-TC (3xTF32 tensor cores) on the
+        device; checked against the tolerance, counters exact.
 """
 import numpy as np
 import pytest
@@ -17,6 +20,7 @@ from paper_2402_14118_b200 import _native as N  # noqa: E402
 from paper_2402_14118_b200.api import MASK_BLOCK, MASK_ELEMENT, VALUE_NORMAL, VALUE_RELU  # noqa: E402
 
 TOL = 1e-5  # north_star: relative to Σ_k |a_ik||b_kj|
+EXACT = N.ALGO_SIMT_BCAST  # bit-exact K2-SIMT (device-side span choice)
 
 
 @pytest.fixture(scope="module")
@@ -65,6 +69,32 @@ def assert_counters(cnt, ocnt):
     assert cnt.kernel_invocations == ocnt["kernel_invocations"]
     assert cnt.rows_skipped == ocnt["rows_skipped"]
     assert cnt.regions_skipped_by_zero_code == ocnt["regions_skipped_by_zero_code"]
+
+
+def within_tol(C, Cr, A, B, C0=None):
+    """|C - Cr| <= TOL * (|c0| + Σ|a||b|), fp64 denominators."""
+    K = B.shape[0]
+    Aq = np.ascontiguousarray(A[:, :K])
+    if C0 is None:
+        bad, worst = o.check_tolerance(C, Cr, Aq, B, tol=TOL)
+        return bad == 0, worst
+    den = np.abs(Aq).astype(np.float64) @ np.abs(B).astype(np.float64) + np.abs(C0).astype(np.float64)
+    err = np.abs(C.astype(np.float64) - Cr.astype(np.float64))
+    ok = err <= TOL * den
+    worst = float(np.max(np.where(den > 0, err / np.where(den > 0, den, 1), 0)))
+    return bool(ok.all()), worst
+
+
+def check_auto(ctx, A, B, Cr, ocnt, C0=None, N_=None):
+    """The default (AUTO) path: tolerance, exact counters, padding zero; returns the path taken."""
+    C, cnt = run_gpu(ctx, A, B, C0=C0, algo=N.ALGO_AUTO, N_=N_)
+    ok, worst = within_tol(C, Cr, A, B, C0=C0)
+    assert ok, worst
+    assert worst < 0.5 * TOL, worst
+    assert_counters(cnt, ocnt)
+    if N_ is not None:
+        assert (C[:, N_:] == 0).all()
+    return ctx.last_algo()
 
 
 def bitexact(x, y):
@@ -124,7 +154,7 @@ def test_k1_zero_semantics(ctx):
 
 
 # ------------------------------------------------------------------------------ K2
-@pytest.mark.parametrize("algo", [N.ALGO_AUTO, N.ALGO_SIMT_SPAN8, N.ALGO_SIMT_SPAN16])
+@pytest.mark.parametrize("algo", [EXACT, N.ALGO_SIMT_SPAN8, N.ALGO_SIMT_SPAN16])
 def test_cfg1_bitexact(ctx, algo):
     # BASELINE configs[0]: 1024^3, A 0.8 element zeros, B 16-wide blocks 0.8 zeros
     A, B = gen_pair(1, 1024, 1024, 1024, 0.8, 0.8, 16)
@@ -132,6 +162,12 @@ def test_cfg1_bitexact(ctx, algo):
     Cr, ocnt = run_oracle(A, B)
     assert bitexact(C, Cr)
     assert_counters(cnt, ocnt)
+
+
+def test_cfg1_auto(ctx):
+    A, B = gen_pair(1, 1024, 1024, 1024, 0.8, 0.8, 16)
+    Cr, ocnt = run_oracle(A, B)
+    check_auto(ctx, A, B, Cr, ocnt)
 
 
 @pytest.mark.parametrize("struct", ["random", "block_random", "column", "block_column"])
@@ -142,12 +178,11 @@ def test_spec_grid_bitexact(ctx, struct, sa, n):
     for sb in (0.0, 0.5, 0.95):
         A = o.ref_generate(n, n, "random", sa, 0, 3)
         B = o.ref_generate(n, n, struct, sb, 0, 4)
-        C, cnt = run_gpu(ctx, A, B)
+        C, cnt = run_gpu(ctx, A, B, algo=EXACT)
         Cr, ocnt = run_oracle(A, B)
         assert bitexact(C, Cr), (struct, sa, sb)
         assert_counters(cnt, ocnt)
-        bad, worst = o.check_tolerance(C, Cr, A, B, tol=TOL)
-        assert bad == 0
+        check_auto(ctx, A, B, Cr, ocnt)
 
 
 @pytest.mark.parametrize("M,K,N_", [(100, 77, 130), (33, 300, 64), (257, 1000, 600), (1, 5, 1), (129, 65, 257)])
@@ -157,11 +192,12 @@ def test_ragged_shapes_and_accumulate(ctx, M, K, N_):
     rng = np.random.default_rng(M)
     C0 = np.zeros((M, B.shape[1]), np.float32)
     C0[:, :N_] = rng.uniform(-1, 1, (M, N_)).astype(np.float32)
-    C, cnt = run_gpu(ctx, A, B, C0=C0, N_=N_)
+    C, cnt = run_gpu(ctx, A, B, C0=C0, N_=N_, algo=EXACT)
     Cr, ocnt = run_oracle(A, B, C0=C0)
     assert bitexact(C, Cr)
     assert (C[:, N_:] == 0).all()  # padding stays zero
     assert_counters(cnt, ocnt)
+    check_auto(ctx, A, B, Cr, ocnt, C0=C0, N_=N_)
 
 
 @pytest.mark.parametrize("zA,zB,bw", [(0.6, 0.6, 8), (0.7, 0.95, 16), (0.8, 0.8, 32), (0.95, 0.6, 16),
@@ -169,10 +205,11 @@ def test_ragged_shapes_and_accumulate(ctx, M, K, N_):
 def test_cfg2_cells_bitexact(ctx, zA, zB, bw):
     # BASELINE configs[1] cells at the full 4096^3 size
     A, B = gen_pair(2, 4096, 4096, 4096, zA, zB, bw)
-    C, cnt = run_gpu(ctx, A, B)
+    C, cnt = run_gpu(ctx, A, B, algo=EXACT)
     Cr, ocnt = run_oracle(A, B)
     assert bitexact(C, Cr)
     assert_counters(cnt, ocnt)
+    check_auto(ctx, A, B, Cr, ocnt)
 
 
 def test_cfg3_mlp_down_projection(ctx):
@@ -181,20 +218,22 @@ def test_cfg3_mlp_down_projection(ctx):
     A, B = gen_pair(3, 2048, 16384, 4096, 0.0, 0.9, 32, a_kind=VALUE_RELU, a_thresh=1.2815515655446004,
                     b_kind=VALUE_NORMAL, b_sigma=0.02)
     assert abs((A == 0).mean() - 0.9) < 0.01
-    C, cnt = run_gpu(ctx, A, B)
+    C, cnt = run_gpu(ctx, A, B, algo=EXACT)
     Cr, ocnt = run_oracle(A, B)
     assert bitexact(C, Cr)
     assert_counters(cnt, ocnt)
+    check_auto(ctx, A, B, Cr, ocnt)
 
 
 def test_cfg4_skinny_decode(ctx):
     # BASELINE configs[3]: 64 x 12288 x 49152, A ReLU ~95% zeros, B 16-wide blocks kept 0.15
     A, B = gen_pair(4, 64, 12288, 49152, 0.0, 0.85, 16, a_kind=VALUE_RELU, a_thresh=1.6448536269514722,
                     b_kind=VALUE_NORMAL, b_sigma=0.02)
-    C, cnt = run_gpu(ctx, A, B)
+    C, cnt = run_gpu(ctx, A, B, algo=EXACT)
     Cr, ocnt = run_oracle(A, B)
     assert bitexact(C, Cr)
     assert_counters(cnt, ocnt)
+    check_auto(ctx, A, B, Cr, ocnt)
 
 
 def test_cfg5_row_shards(ctx):
@@ -209,14 +248,22 @@ def test_cfg5_row_shards(ctx):
         for rank in range(world):
             r0, r1 = mmm.shard_rows(M, world, rank)
             a = dev(A[r0:r1])
-            c = torch.zeros((r1 - r0, N_), dtype=torch.float32, device="cuda")
-            ctx.preprocess(a, b)
-            mmm.multiply_mmm(ctx, c, a, b)
             rows = np.sort(rng.choice(r1 - r0, 16, replace=False))
-            Cg = c.cpu().numpy()[rows]
             Cr = np.zeros((16, N_), np.float32)
-            o.multiply_mmm(Cr, np.ascontiguousarray(A[r0:r1][rows][:, :K]), B)
-            assert bitexact(Cg, Cr), (world, rank)
+            Ar = np.ascontiguousarray(A[r0:r1][rows][:, :K])
+            o.multiply_mmm(Cr, Ar, B)
+            for algo in (EXACT, N.ALGO_AUTO):
+                c = torch.zeros((r1 - r0, N_), dtype=torch.float32, device="cuda")
+                ctx.set_algo(algo)
+                ctx.preprocess(a, b)
+                mmm.multiply_mmm(ctx, c, a, b)
+                Cg = c.cpu().numpy()[rows]
+                if algo == EXACT:
+                    assert bitexact(Cg, Cr), (world, rank)
+                else:
+                    bad, worst = o.check_tolerance(Cg, Cr, Ar, B, tol=TOL)
+                    assert bad == 0, (world, rank, worst)
+            ctx.set_algo(N.ALGO_AUTO)
 
 
 # ------------------------------------------------------------------- other entry points
@@ -239,11 +286,37 @@ def test_dense_algo_matches(ctx):
 
 def test_multiply_host_path(ctx):
     A, B = gen_pair(12, 200, 320, 192, 0.8, 0.8, 16)
-    C = np.zeros((200, 192), np.float32)
-    cnt = mmm.multiply_host(C, A, B, ctx=ctx)
     Cr, ocnt = run_oracle(A, B)
-    assert bitexact(C, Cr)
-    assert_counters(cnt, ocnt)
+    for algo in (EXACT, N.ALGO_AUTO):
+        ctx.set_algo(algo)
+        C = np.zeros((200, 192), np.float32)
+        cnt = mmm.multiply_host(C, A, B, ctx=ctx)
+        if algo == EXACT:
+            assert bitexact(C, Cr)
+        else:
+            ok, worst = within_tol(C, Cr, A, B)
+            assert ok, worst
+        assert_counters(cnt, ocnt)
+    ctx.set_algo(N.ALGO_AUTO)
+
+
+def test_auto_choice_and_switch(ctx):
+    # a dense cell goes to K2-TC; forcing the other path on an AUTO plan re-packs its
+    # operands (both stay correct); a very sparse, short cell is correct either way
+    A, B = gen_pair(15, 2048, 2048, 2048, 0.6, 0.6, 8)
+    Cr, ocnt = run_oracle(A, B)
+    assert check_auto(ctx, A, B, Cr, ocnt) == N.ALGO_TC
+    a, b = dev(A), dev(B)
+    ctx.set_algo(N.ALGO_AUTO)
+    ctx.preprocess(a, b)
+    ctx.set_algo(EXACT)  # plan built for AUTO (TC chosen, SIMT rows gated out)
+    c = torch.zeros((2048, 2048), dtype=torch.float32, device="cuda")
+    mmm.multiply_mmm(ctx, c, a, b)
+    assert bitexact(c.cpu().numpy(), Cr)
+    ctx.set_algo(N.ALGO_AUTO)
+    A2, B2 = gen_pair(16, 128, 4096, 4096, 0.99, 0.99, 8)
+    Cr2, ocnt2 = run_oracle(A2, B2)
+    assert check_auto(ctx, A2, B2, Cr2, ocnt2) in (N.ALGO_TC, N.ALGO_SIMT_SPAN8, N.ALGO_SIMT_SPAN16)
 
 
 def test_stale_and_errors(ctx):
