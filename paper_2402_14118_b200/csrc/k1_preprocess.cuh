@@ -386,6 +386,11 @@ __global__ void __launch_bounds__(256) k1_csr(const uint32_t* __restrict__ abits
   if (threadIdx.x < kCsrRows && r0 + threadIdx.x < M) row_ptr[r0 + threadIdx.x] = s_off[threadIdx.x];
   if (threadIdx.x == 0 && r0 + kCsrRows >= M) row_ptr[M] = s_off[M - r0];
   if (row >= M) return;
+  // per 1024-column chunk: lanes expand their words' set bits into the warp's smem buffer
+  // at their prefix offsets, then the warp streams the chunk's list out contiguously
+  // (coalesced stores instead of 32 scattered 2-byte streams)
+  __shared__ Idx s_buf[kCsrRows][1024];
+  Idx* buf = s_buf[warp];
   int64_t out = s_off[warp];
   const uint32_t* bits = abits + row * kw;
   for (int64_t w0 = 0; w0 < kw; w0 += 32) {
@@ -398,13 +403,17 @@ __global__ void __launch_bounds__(256) k1_csr(const uint32_t* __restrict__ abits
       const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
       if (lane >= o) x += y;
     }
-    int64_t pos = out + x - n;
+    uint32_t pos = x - n;
     while (word) {
       const int b = __ffs(word) - 1;
       word &= word - 1;
-      cols[pos++] = (Idx)(w * 32 + b);
+      buf[pos++] = (Idx)(w * 32 + b);
     }
-    out += __shfl_sync(0xffffffffu, x, 31);
+    const uint32_t total = __shfl_sync(0xffffffffu, x, 31);
+    __syncwarp();
+    for (uint32_t i = lane; i < total; i += 32) cols[out + i] = buf[i];
+    __syncwarp();
+    out += total;
   }
 }
 
@@ -477,22 +486,35 @@ __device__ void k1_finalize_block(const uint32_t* __restrict__ acol, const uint3
 // of a tile re-derives the tile's chunk prefix from the kw mask words (no scan launch) and
 // packs kPtSteps steps; steps straddle chunk boundaries freely (positions, not chunks,
 // define a step), so padding is at most 7 k per tile.
-constexpr int kPackThreads = 128;  // k1_pack_rows
+constexpr int kPackThreads = 256;  // k1_pack_rows
 constexpr int kPtSteps = 4;
 constexpr int kPtThreads = 256;
 
-__global__ void __launch_bounds__(kPtThreads)
-k1_pack_tc(const float* __restrict__ B, int64_t K, int64_t ldb, const uint32_t* __restrict__ tlive, int64_t kw,
-           int64_t maxsteps, float* __restrict__ tcb, int32_t* __restrict__ tck, int32_t* __restrict__ tcn,
-           const unsigned long long* __restrict__ sel) {
-  if (sel && *sel != 32ull) return;  // AUTO chose K2-SIMT
+struct PackTcArgs {
+  const float* B;
+  int64_t ldb;
+  const uint32_t* tlive;
+  int64_t kw, maxsteps;
+  float* tcb;
+  int32_t* tck;
+  int32_t* tcn;
+};
+
+// CTA (bx = step block, tb = tile) of the K2-TC pack; dynamic smem (2 kw + 1) words.
+__device__ __forceinline__ void k1_pack_tc_cta(const PackTcArgs& g, int64_t bx, int64_t tb) {
+  const float* __restrict__ B = g.B;
+  const int64_t ldb = g.ldb, kw = g.kw, maxsteps = g.maxsteps;
+  const uint32_t* __restrict__ tlive = g.tlive;
+  float* __restrict__ tcb = g.tcb;
+  int32_t* __restrict__ tck = g.tck;
+  int32_t* __restrict__ tcn = g.tcn;
   extern __shared__ __align__(16) uint32_t pt_smem[];  // masks [kw] | prefix [kw + 1]
   __shared__ int32_t s_k[kPtSteps * 8];
   __shared__ int32_t wsum[kPtThreads / 32];
   uint32_t* s_m = pt_smem;
   int32_t* s_pre = reinterpret_cast<int32_t*>(pt_smem + kw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t tb = blockIdx.y, n0 = tb * kTcTileN;
+  const int64_t n0 = tb * kTcTileN;
   // chunk masks and their exclusive popcount prefix (block scan, carried over kw / 256 rounds)
   int32_t carry = 0;
   for (int64_t base = 0; base < kw; base += kPtThreads) {
@@ -520,8 +542,8 @@ k1_pack_tc(const float* __restrict__ B, int64_t K, int64_t ldb, const uint32_t* 
   __syncthreads();
   const int32_t total = carry;
   const int64_t nsteps = (total + 7) / 8;
-  if (blockIdx.x == 0 && tid == 0) tcn[tb] = total;
-  const int64_t s0 = (int64_t)blockIdx.x * kPtSteps;
+  if (bx == 0 && tid == 0) tcn[tb] = total;
+  const int64_t s0 = bx * kPtSteps;
   if (s0 >= nsteps) return;
   if (tid < kPtSteps * 8) {
     const int64_t p = s0 * 8 + tid;
@@ -564,8 +586,9 @@ k1_pack_tc(const float* __restrict__ B, int64_t K, int64_t ldb, const uint32_t* 
     *reinterpret_cast<uint4*>(img + off) = make_uint4(h[0], h[1], h[2], h[3]);
     *reinterpret_cast<uint4*>(img + kTcTileN * 8 + off) = make_uint4(l[0], l[1], l[2], l[3]);
   }
-  (void)K;
 }
+
+__global__ void __launch_bounds__(kPtThreads) k1_pack_tc(PackTcArgs g) { k1_pack_tc_cta(g, blockIdx.x, blockIdx.y); }
 
 // ----------------------------------------------------------- B rows for K2-SIMT
 // For each 256-column tile tb and 32-k chunk c, a contiguous record at row_off[tb*kw + c]
@@ -574,13 +597,24 @@ k1_pack_tc(const float* __restrict__ B, int64_t K, int64_t ldb, const uint32_t* 
 // slice j = 0..15 (16 columns = groups
 // 2j, 2j+1) and every k of the chunk with a non-zero block in the slice, ascending, the
 // raw 16 floats B[k][16j .. 16j+15].  K2-SIMT moves each record with one bulk copy.
-__global__ void __launch_bounds__(kPackThreads)
-k1_pack_rows(const float* __restrict__ B, int64_t K, int64_t ldb, const uint32_t* __restrict__ bgrp, int64_t kw,
-             const int64_t* __restrict__ row_off, uint4* __restrict__ rows, const unsigned long long* __restrict__ sel) {
-  if (sel && *sel == 32ull) return;  // AUTO chose K2-TC
+struct PackRowsArgs {
+  const float* B;
+  int64_t ldb;
+  const uint32_t* bgrp;
+  int64_t kw;
+  const int64_t* row_off;
+  uint4* rows;
+};
+
+// CTA (c = 32-k chunk, tb = 256-column tile) of the K2-SIMT pack.
+__device__ __forceinline__ void k1_pack_rows_cta(const PackRowsArgs& g, int64_t c, int64_t tb) {
+  const float* __restrict__ B = g.B;
+  const int64_t ldb = g.ldb, kw = g.kw;
+  const uint32_t* __restrict__ bgrp = g.bgrp;
+  const int64_t* __restrict__ row_off = g.row_off;
+  uint4* __restrict__ rows = g.rows;
   __shared__ uint32_t s_g[32];
   __shared__ uint32_t s_base[17];
-  const int64_t c = blockIdx.x, tb = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t n0 = tb * 256, k0 = c * 32;
   if (tid < 32) {
@@ -615,6 +649,25 @@ k1_pack_rows(const float* __restrict__ B, int64_t K, int64_t ldb, const uint32_t
     const int kk = __ffs(m) - 1;
     const float4 v = ldg_stream(B + (k0 + kk) * ldb + n0 + 16 * j + 4 * q);
     out[12 + p] = make_uint4(__float_as_uint(v.x), __float_as_uint(v.y), __float_as_uint(v.z), __float_as_uint(v.w));
+  }
+}
+
+__global__ void __launch_bounds__(kPackThreads) k1_pack_rows(PackRowsArgs g) {
+  k1_pack_rows_cta(g, blockIdx.x, blockIdx.y);
+}
+
+// AUTO: both packs in one launch (CTAs [0, n_rows) = K2-SIMT rows, the rest = K2-TC steps),
+// each CTA gated by the path K1's last CTA chose — one launch instead of two, and the
+// gated-out half exits at entry.
+__global__ void __launch_bounds__(kPtThreads)
+k1_pack_auto(PackRowsArgs gr, int64_t rows_x, int64_t n_rows, PackTcArgs gt, int64_t tc_x,
+             const unsigned long long* __restrict__ sel) {
+  const int64_t bid = blockIdx.x;
+  const bool tc = *sel == 32ull;
+  if (bid < n_rows) {
+    if (!tc) k1_pack_rows_cta(gr, bid % rows_x, bid / rows_x);
+  } else if (tc) {
+    k1_pack_tc_cta(gt, (bid - n_rows) % tc_x, (bid - n_rows) / tc_x);
   }
 }
 

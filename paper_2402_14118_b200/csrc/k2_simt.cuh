@@ -348,11 +348,10 @@ __device__ __forceinline__ void s2_wait(uint64_t* bar, uint32_t parity) {
 }
 
 template <int SPAN>
-__global__ void __launch_bounds__(kS2Threads, 1)
-k2_simt2(const float* __restrict__ AT, int64_t kpad, const float4* __restrict__ brows, const int64_t* __restrict__ row_off,
-         int64_t kw, float* __restrict__ C, int64_t ldc, int64_t M, int64_t Np, const unsigned long long* __restrict__ sel) {
+__device__ __forceinline__ void k2_simt2_body(const float* __restrict__ AT, int64_t kpad,
+                                              const float4* __restrict__ brows, const int64_t* __restrict__ row_off,
+                                              int64_t kw, float* __restrict__ C, int64_t ldc, int64_t M, int64_t Np) {
   static_assert(SPAN == 8 || SPAN == 16, "SPAN must be 8 or 16");
-  if (sel && *sel != (unsigned long long)SPAN) return;  // device-side variant choice (k1_finalize)
   extern __shared__ __align__(128) uint8_t s2_raw[];
   S2Shared& sh = *reinterpret_cast<S2Shared*>(s2_raw + ((128 - ((uint32_t)__cvta_generic_to_shared(s2_raw) & 127)) & 127));
   int64_t* offs = reinterpret_cast<int64_t*>(&sh + 1);
@@ -475,6 +474,27 @@ k2_simt2(const float* __restrict__ AT, int64_t kpad, const float4* __restrict__ 
       for (int q = 0; q < SPAN / 2; ++q)
         *reinterpret_cast<float2*>(C + row * ldc + ncol + s * SPAN + 2 * q) = acc[s][r][q];
   }
+}
+
+template <int SPAN>
+__global__ void __launch_bounds__(kS2Threads, 1)
+k2_simt2(const float* __restrict__ AT, int64_t kpad, const float4* __restrict__ brows, const int64_t* __restrict__ row_off,
+         int64_t kw, float* __restrict__ C, int64_t ldc, int64_t M, int64_t Np, const unsigned long long* __restrict__ sel) {
+  if (sel && *sel != (unsigned long long)SPAN) return;  // device-side span choice (k1_finalize_block)
+  k2_simt2_body<SPAN>(AT, kpad, brows, row_off, kw, C, ldc, M, Np);
+}
+
+// One launch for both spans (and AUTO): *sel = 8 / 16 runs that span, anything else (32 =
+// K2-TC chosen) exits at entry.
+__global__ void __launch_bounds__(kS2Threads, 1)
+k2_simt2_any(const float* __restrict__ AT, int64_t kpad, const float4* __restrict__ brows,
+             const int64_t* __restrict__ row_off, int64_t kw, float* __restrict__ C, int64_t ldc, int64_t M, int64_t Np,
+             const unsigned long long* __restrict__ sel) {
+  const unsigned long long v = *sel;
+  if (v == 8ull)
+    k2_simt2_body<8>(AT, kpad, brows, row_off, kw, C, ldc, M, Np);
+  else if (v == 16ull)
+    k2_simt2_body<16>(AT, kpad, brows, row_off, kw, C, ldc, M, Np);
 }
 
 }  // namespace mmmcu

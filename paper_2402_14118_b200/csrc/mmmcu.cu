@@ -239,25 +239,44 @@ mmmcu_status stage_b(mmmcu_ctx* ctx, const float* B, int64_t K, int64_t N, int64
   return MMMCU_OK;
 }
 
-// B operand packs for K2 (sel: the device path choice gating an AUTO plan, nullptr = always).
-mmmcu_status pack_rows(mmmcu_ctx* ctx, const unsigned long long* sel) {
+// B operand packs for K2: K2-SIMT rows, K2-TC step images, or (AUTO) both in one launch
+// gated on the device by the path choice.
+mmmcu::PackRowsArgs rows_args(mmmcu_ctx* ctx) {
+  return mmmcu::PackRowsArgs{ctx->B, ctx->ldb, ctx->bgrp.as<uint32_t>(), (ctx->Kb + 31) / 32,
+                             ctx->row_off.as<int64_t>(), ctx->brows.as<uint4>()};
+}
+mmmcu::PackTcArgs tc_args(mmmcu_ctx* ctx) {
+  return mmmcu::PackTcArgs{ctx->B, ctx->ldb, zb_tlive(ctx), (ctx->Kb + 31) / 32, ctx->tc_steps,
+                           ctx->tcb.as<float>(), ctx->tck.as<int32_t>(), ctx->tcn.as<int32_t>()};
+}
+int pack_tc_smem(mmmcu_ctx* ctx) { return (int)(sizeof(uint32_t) * (2 * ((ctx->Kb + 31) / 32) + 1)); }
+
+mmmcu_status pack_rows(mmmcu_ctx* ctx) {
   dim3 grid((unsigned)((ctx->Kb + 31) / 32), (unsigned)ctx->n_tb);
-  mmmcu::k1_pack_rows<<<grid, mmmcu::kPackThreads, 0, ctx->stream>>>(
-      ctx->B, ctx->Kb, ctx->ldb, ctx->bgrp.as<uint32_t>(), (ctx->Kb + 31) / 32, ctx->row_off.as<int64_t>(),
-      ctx->brows.as<uint4>(), sel);
+  mmmcu::k1_pack_rows<<<grid, mmmcu::kPackThreads, 0, ctx->stream>>>(rows_args(ctx));
   MMMCU_LAUNCHED();
   return MMMCU_OK;
 }
 
-mmmcu_status pack_tc(mmmcu_ctx* ctx, const unsigned long long* sel) {
-  const int64_t bkw = (ctx->Kb + 31) / 32;
-  const int smem = (int)(sizeof(uint32_t) * (2 * bkw + 1));
+mmmcu_status pack_tc(mmmcu_ctx* ctx) {
+  const int smem = pack_tc_smem(ctx);
   if (smem > 200 * 1024) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "K too large for the TC packer");
   MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k1_pack_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   dim3 grid((unsigned)((ctx->tc_steps + mmmcu::kPtSteps - 1) / mmmcu::kPtSteps), (unsigned)ctx->n_tc);
-  mmmcu::k1_pack_tc<<<grid, mmmcu::kPtThreads, smem, ctx->stream>>>(
-      ctx->B, ctx->Kb, ctx->ldb, zb_tlive(ctx), bkw, ctx->tc_steps, ctx->tcb.as<float>(), ctx->tck.as<int32_t>(),
-      ctx->tcn.as<int32_t>(), sel);
+  mmmcu::k1_pack_tc<<<grid, mmmcu::kPtThreads, smem, ctx->stream>>>(tc_args(ctx));
+  MMMCU_LAUNCHED();
+  return MMMCU_OK;
+}
+
+mmmcu_status pack_auto(mmmcu_ctx* ctx, const unsigned long long* sel) {
+  const int smem = pack_tc_smem(ctx);
+  if (smem > 200 * 1024) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "K too large for the TC packer");
+  const int64_t rows_x = (ctx->Kb + 31) / 32, n_rows = rows_x * ctx->n_tb;
+  const int64_t tc_x = (ctx->tc_steps + mmmcu::kPtSteps - 1) / mmmcu::kPtSteps, n_tc = tc_x * ctx->n_tc;
+  if (n_rows + n_tc > 0x7fffffff) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "B too large for one pack launch");
+  MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k1_pack_auto, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  mmmcu::k1_pack_auto<<<(unsigned)(n_rows + n_tc), mmmcu::kPtThreads, smem, ctx->stream>>>(
+      rows_args(ctx), rows_x, n_rows, tc_args(ctx), tc_x, sel);
   MMMCU_LAUNCHED();
   return MMMCU_OK;
 }
@@ -326,13 +345,18 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
                                                                ctx->row_ptr.as<int64_t>(), ctx->cols.as<uint32_t>());
     MMMCU_LAUNCHED();
   }
-  if (rows_b) {
-    MMMCU_TRY(pack_rows(ctx, sel));
-    ctx->rows_fresh = sel == nullptr;
-  }
-  if (tcb_b) {
-    MMMCU_TRY(pack_tc(ctx, sel));
-    ctx->tcb_fresh = sel == nullptr;
+  if (gate) {
+    MMMCU_TRY(pack_auto(ctx, sel));
+    ctx->rows_fresh = ctx->tcb_fresh = false;
+  } else {
+    if (rows_b) {
+      MMMCU_TRY(pack_rows(ctx));
+      ctx->rows_fresh = true;
+    }
+    if (tcb_b) {
+      MMMCU_TRY(pack_tc(ctx));
+      ctx->tcb_fresh = true;
+    }
   }
   if (do_a) {
     ctx->has_a = true;
@@ -369,13 +393,19 @@ mmmcu_status launch_simt(mmmcu_ctx* ctx, float* C, int64_t ldc, int span_hint, i
     const int64_t row_tiles = ctx->m_at / 128;
     if (row_tiles > 65535) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "M larger than 8388480 rows");
     dim3 grid((unsigned)((Np + 255) / 256), (unsigned)row_tiles);
-    if (span_hint == 0 || span_hint == 8) {
+    if (span_hint == 0) {  // one launch, span (or exit) chosen on the device
+      MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k2_simt2_any, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      mmmcu::k2_simt2_any<<<grid, mmmcu::kS2Threads, smem, ctx->stream>>>(
+          ctx->at.as<float>(), ctx->kpad, ctx->brows.as<float4>(), ctx->row_off.as<int64_t>(), kw, C, ldc, M, Np, sel2);
+      MMMCU_LAUNCHED();
+    }
+    if (span_hint == 8) {
       MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k2_simt2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       mmmcu::k2_simt2<8><<<grid, mmmcu::kS2Threads, smem, ctx->stream>>>(
           ctx->at.as<float>(), ctx->kpad, ctx->brows.as<float4>(), ctx->row_off.as<int64_t>(), kw, C, ldc, M, Np, sel2);
       MMMCU_LAUNCHED();
     }
-    if (span_hint == 0 || span_hint == 16) {
+    if (span_hint == 16) {
       MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k2_simt2<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       mmmcu::k2_simt2<16><<<grid, mmmcu::kS2Threads, smem, ctx->stream>>>(
           ctx->at.as<float>(), ctx->kpad, ctx->brows.as<float4>(), ctx->row_off.as<int64_t>(), kw, C, ldc, M, Np, sel2);
@@ -683,7 +713,10 @@ mmmcu_status mmmcu_multiply(mmmcu_ctx* ctx, float* C, int64_t ldc, const float* 
     if (!ctx->op_at || !ctx->op_tcb)
       return fail(ctx, MMMCU_ERR_NOT_READY, "the TC operands were not built: preprocess with algo TC");
     ctx->last_algo = MMMCU_ALGO_TC;
-    if (!ctx->tcb_fresh) MMMCU_TRY(pack_tc(ctx, nullptr));
+    if (!ctx->tcb_fresh) {
+      MMMCU_TRY(pack_tc(ctx));
+      ctx->tcb_fresh = true;
+    }
     MMMCU_TRY(launch_tc(ctx, C, ldc, nullptr));
   } else if (ctx->algo == MMMCU_ALGO_DENSE) {
     ctx->last_algo = MMMCU_ALGO_DENSE;
@@ -693,7 +726,10 @@ mmmcu_status mmmcu_multiply(mmmcu_ctx* ctx, float* C, int64_t ldc, const float* 
   } else {
     const int span = ctx->algo == MMMCU_ALGO_SIMT_SPAN8 ? 8 : ctx->algo == MMMCU_ALGO_SIMT_SPAN16 ? 16 : 0;
     ctx->last_algo = span == 8 ? MMMCU_ALGO_SIMT_SPAN8 : span == 16 ? MMMCU_ALGO_SIMT_SPAN16 : MMMCU_ALGO_SIMT_BCAST;
-    if (ctx->op_rows && !ctx->rows_fresh) MMMCU_TRY(pack_rows(ctx, nullptr));
+    if (ctx->op_rows && !ctx->rows_fresh) {
+      MMMCU_TRY(pack_rows(ctx));
+      ctx->rows_fresh = true;
+    }
     MMMCU_TRY(launch_simt(ctx, C, ldc, span, 8));
   }
   return fill_counters(ctx, counters);
