@@ -12,7 +12,8 @@
 //   acol    uint32 [K]              non-zeros per A column (for the exact WorkCounters)
 //   row_ptr int64  [M+1], cols      per-row ascending index lists (CSR), ballot/popc + scan
 //   codes   uint8  [K][nreg]        B pattern codes, bit 7-j <-> 8-column group j (MSB first,
-//                                   kernel_table.cpp:19) == the BPlan codes
+//                                   kernel_table.cpp:19) == the BPlan codes; rebuilt from bgrp
+//                                   by k1_codes_export on request (not on the hot path)
 //   bgrp    uint32 [ngrp][kw]       B group k-bitmaps: bit (k%32) of word k/32 of group g set
 //                                   iff B[k, 8g:8g+8] has a non-zero (transposed block masks)
 //   bpop    uint32 [K]              Σ popcount(codes[k][:])   (lane ops per A non-zero / 8)
@@ -23,7 +24,8 @@
 
 namespace mmmcu {
 
-constexpr int kK1Threads = 256;  // 8 warps; each thread owns 4 consecutive columns
+constexpr int kK1Threads = 256;  // 8 compute warps; each lane owns 4 columns of a 1024-column tile
+constexpr int kK1Block = kK1Threads + 32;  // + the TMA producer warp (k1_pass)
 constexpr int kK1Cols = 4 * kK1Threads;  // 1024 columns per CTA tile
 constexpr int kK1Rows = 32;              // rows per CTA tile (one 32-bit k-word for B)
 constexpr int kTcTileN = 192;            // K2-TC C tile width (columns)
@@ -43,7 +45,7 @@ __device__ __forceinline__ uint32_t nz4(float4 v) {
 }
 
 // Zero-initialised per-plan scratch (one cudaMemsetAsync per preprocess):
-//   za = arow[M] | acol[K] | tile_sum[M/32];  zb = slice_nz (u64) | bpop[K] | bnz[K]
+//   za = arow[M] | acol[K] | tile_sum[M/32];  zb = btot (3 x u64) | bpop[K] | bnz[K] | ...
 struct K1Scratch {
   uint32_t* arow;
   uint32_t* acol;
@@ -51,7 +53,7 @@ struct K1Scratch {
   int64_t* tile_prefix;   // [ceil(M/32) + 1] exclusive prefix of tile_sum (written by the last CTA)
   uint32_t* bpop;
   uint32_t* bnz;
-  unsigned long long* slice_nz;
+  unsigned long long* btot;  // B totals: {Σ non-zero (k, slice), Σ bpop, Σ bnz} (zeroed)
   unsigned int* done;
   // K2-TC operands (nullptr when the TC path is not prepared)
   float* at;              // A^T per 128-row tile: at[(rt * kpad + k) * 128 + (i % 128)], zero padded
@@ -67,153 +69,8 @@ struct K1Scratch {
   int64_t* row_off;       // [n_tb * kw + 1] exclusive prefix of (row_cnt + 3 header rows), 64-byte units
 };
 
-// --------------------------------------------------------------------------- A tile
-// Tile (tx, ty): columns 1024*tx + 4t .. +3 for thread t, rows 32*ty .. +31.  Lanes
-// 8q..8q+7 of a warp hold the 32 columns of one bitmap word.  Rows are processed 8 at a
-// time so eight 16-byte loads per thread are in flight before the first shuffle.
-__device__ __forceinline__ void k1_a_tile(const float* __restrict__ A, int64_t M, int64_t K, int64_t lda,
-                                          uint32_t* __restrict__ abits, int64_t kw, const K1Scratch& z, int64_t tx,
-                                          int64_t ty) {
-  const int lane = threadIdx.x & 31;
-  const int64_t c = tx * kK1Cols + 4 * threadIdx.x;
-  const int64_t r0 = ty * kK1Rows;
-  const bool col_ok = c < K;
-  const uint32_t vmask = col_ok ? (K - c >= 4 ? 0xFu : ((1u << (K - c)) - 1u)) : 0u;
-  uint32_t ccount[4] = {0, 0, 0, 0};
-  uint32_t warp_total = 0;
-  const int64_t rend = min(r0 + kK1Rows, M);
-  // with the TC operand enabled, rows run to the 128-row tile boundary (zeros past M)
-  const int64_t rend_at = z.at ? min(r0 + kK1Rows, z.m_at) : rend;
-  const bool at_ok = z.at != nullptr && c < z.kpad;
-  for (int64_t rb = r0; rb < rend_at; rb += 8) {
-    float4 v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      v[u] = (col_ok && rb + u < rend) ? ldg_stream(A + (rb + u) * lda + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-    if (at_ok) {
-      // A^T tile row k = c+q holds rows rb..rb+7 at offset rb % 128: two 16-byte stores
-      const int64_t rt = rb >> 7;
-      float* dst = z.at + (rt * z.kpad + c) * 128 + (rb & 127);
-      const float e[4][8] = {{v[0].x, v[1].x, v[2].x, v[3].x, v[4].x, v[5].x, v[6].x, v[7].x},
-                             {v[0].y, v[1].y, v[2].y, v[3].y, v[4].y, v[5].y, v[6].y, v[7].y},
-                             {v[0].z, v[1].z, v[2].z, v[3].z, v[4].z, v[5].z, v[6].z, v[7].z},
-                             {v[0].w, v[1].w, v[2].w, v[3].w, v[4].w, v[5].w, v[6].w, v[7].w}};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float4* d4 = reinterpret_cast<float4*>(dst + q * 128);
-        d4[0] = make_float4(e[q][0], e[q][1], e[q][2], e[q][3]);
-        d4[1] = make_float4(e[q][4], e[q][5], e[q][6], e[q][7]);
-      }
-    }
-    if (rb >= rend) continue;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int64_t i = rb + u;
-      const uint32_t nib = nz4(v[u]) & vmask;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) ccount[q] += (nib >> q) & 1u;
-      uint32_t word = nib << (4 * (lane & 7));
-      word |= __shfl_xor_sync(0xffffffffu, word, 1);
-      word |= __shfl_xor_sync(0xffffffffu, word, 2);
-      word |= __shfl_xor_sync(0xffffffffu, word, 4);
-      uint32_t cnt = __popc(word);  // per 32-column word; lanes 8q hold distinct words
-      cnt = (lane & 7) == 0 ? cnt : 0u;
-      cnt += __shfl_xor_sync(0xffffffffu, cnt, 8);
-      cnt += __shfl_xor_sync(0xffffffffu, cnt, 16);
-      if (i < rend) {
-        if ((lane & 7) == 0 && col_ok) abits[i * kw + (c >> 5)] = word;
-        if (lane == 0 && cnt) atomicAdd(&z.arow[i], cnt);
-        warp_total += cnt;
-      }
-    }
-  }
-  if (lane == 0 && warp_total) atomicAdd(&z.tile_sum[ty], warp_total);
-  if (col_ok) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (ccount[q]) atomicAdd(&z.acol[c + q], ccount[q]);
-  }
-}
-
-// --------------------------------------------------------------------------- B tile
-// Tile (tx, kw_idx): columns 1024*tx + 4t .. +3 of the padded row (ldb is a multiple of
-// 64, padding is zero) over the 32 rows of one k-word.  Lane pairs form 8-column groups;
-// 16 lanes form one 64-column region (code).
-__device__ __forceinline__ void k1_b_tile(const float* __restrict__ B, int64_t K, int64_t ldb,
-                                          uint8_t* __restrict__ codes, int64_t nreg, uint32_t* __restrict__ bgrp,
-                                          int64_t kw, const K1Scratch& z, int64_t tx, int64_t kw_idx) {
-  const int lane = threadIdx.x & 31;
-  const int64_t c = tx * kK1Cols + 4 * threadIdx.x;
-  const int64_t k0 = kw_idx * 32;
-  const bool col_ok = c < ldb;
-  uint32_t gword = 0;   // group k-bitmap word over the 32 rows
-  uint32_t slices = 0;  // (k, 16-column slice) pairs with a non-zero, counted by lane%4==0
-  const int64_t kend = min(k0 + 32, K);
-  for (int64_t kb = k0; kb < kend; kb += 8) {
-    float4 v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      v[u] = (col_ok && kb + u < kend) ? ldg_stream(B + (kb + u) * ldb + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int64_t k = kb + u;
-      uint32_t any = nz4(v[u]) != 0u;
-      any |= __shfl_xor_sync(0xffffffffu, any, 1);  // 8-column group
-      gword |= any << (uint32_t)(k - k0);
-      const uint32_t sibling = __shfl_xor_sync(0xffffffffu, any, 2);  // other group of the slice
-      if ((lane & 3) == 0 && col_ok && k < kend) slices += any | sibling;
-      // region code: group j = (lane & 15) >> 1 -> bit 7 - j (MSB first)
-      uint32_t code = any << (7 - ((lane & 15) >> 1));
-      code |= __shfl_xor_sync(0xffffffffu, code, 2);
-      code |= __shfl_xor_sync(0xffffffffu, code, 4);
-      code |= __shfl_xor_sync(0xffffffffu, code, 8);
-      uint32_t pop = ((lane & 15) == 0 && col_ok) ? __popc(code) : 0u;
-      uint32_t nzc = ((lane & 15) == 0 && col_ok) ? (uint32_t)(code != 0) : 0u;
-      pop += __shfl_xor_sync(0xffffffffu, pop, 16);
-      nzc += __shfl_xor_sync(0xffffffffu, nzc, 16);
-      if (k < kend) {
-        if ((lane & 15) == 0 && col_ok) codes[k * nreg + (c >> 6)] = (uint8_t)code;
-        if (lane == 0) {
-          if (pop) atomicAdd(&z.bpop[k], pop);
-          if (nzc) atomicAdd(&z.bnz[k], nzc);
-        }
-      }
-    }
-  }
-  if ((lane & 1) == 0 && col_ok) bgrp[(c >> 3) * kw + kw_idx] = gword;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) slices += __shfl_xor_sync(0xffffffffu, slices, o);
-  if (lane == 0 && slices) atomicAdd(z.slice_nz, (unsigned long long)slices);
-  if (z.row_cnt) {
-    // K2-SIMT rows of this chunk: one 64-byte row per non-zero (k, 16-column slice)
-    const uint32_t smask = gword | __shfl_xor_sync(0xffffffffu, gword, 2);
-    uint32_t rows = ((lane & 3) == 0 && col_ok) ? (uint32_t)__popc(smask) : 0u;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) rows += __shfl_xor_sync(0xffffffffu, rows, o);
-    const int64_t c_warp = tx * kK1Cols + 128 * (threadIdx.x >> 5);
-    if (lane == 0 && rows && c_warp < ldb) atomicAdd(&z.row_cnt[(c_warp >> 8) * kw + kw_idx], rows);
-  }
-  if (z.tlive) {
-    // K2-TC live k of this chunk: OR of the group k-masks per TC tile; a warp's 128
-    // columns touch at most two 192-column tiles (a lane's 4 columns lie in one)
-    const int64_t t_lane = c / kTcTileN;
-    const int64_t t0 = __shfl_sync(0xffffffffu, t_lane, 0);
-    uint32_t w0 = (col_ok && t_lane == t0) ? gword : 0u;
-    uint32_t w1 = (col_ok && t_lane != t0) ? gword : 0u;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      w0 |= __shfl_xor_sync(0xffffffffu, w0, o);
-      w1 |= __shfl_xor_sync(0xffffffffu, w1, o);
-    }
-    if (lane == 0 && w0) atomicOr(&z.tlive[t0 * kw + kw_idx], w0);
-    if (lane == 0 && w1) atomicOr(&z.tlive[(t0 + 1) * kw + kw_idx], w1);
-  }
-}
-
-__device__ void k1_finalize_block(const uint32_t* __restrict__ acol, const uint32_t* __restrict__ bpop,
-                                  const uint32_t* __restrict__ bnz, int64_t K, int64_t M, int64_t nreg, int has_a,
-                                  int has_b, const unsigned long long* __restrict__ slice_nz,
-                                  unsigned long long* __restrict__ out);
+__device__ void k1_plan_totals(const unsigned long long* __restrict__ btot, int64_t K, int64_t nreg, int has_b,
+                               unsigned long long* __restrict__ out);
 
 // AUTO path choice (stats[7] := 32 for K2-TC, else the K2-SIMT span stays): estimated
 // SM-cycles of each path from the plan, constants measured on B200 (K2 choice):
@@ -224,13 +81,22 @@ __device__ void k1_finalize_block(const uint32_t* __restrict__ acol, const uint3
 //     non-zero (k, slice); K2-TC step images 3 x 768 B per live (k, tile);
 //   each divided by min(148 SMs, its CTA count).
 __device__ void k1_choose_path(const K1Scratch& z, int64_t M, int64_t kw, unsigned long long* __restrict__ out) {
-  __shared__ unsigned long long s_stage[kK1Threads / 32], s_live[kK1Threads / 32];
+  __shared__ unsigned long long s_stage[32], s_live[32];
   unsigned long long st = 0, live = 0;
-  for (int64_t tb = threadIdx.x; tb < z.n_tc; tb += blockDim.x) {
-    unsigned long long n = 0;
-    for (int64_t c = 0; c < kw; ++c) n += __popc(z.tlive[tb * kw + c]);
-    live += n;
-    st += (n + 15) / 16;
+  {
+    // warp per tile: lanes stream the tile's kw mask words (coalesced), warp popc sum
+    const int lane0 = threadIdx.x & 31, nw = (int)(blockDim.x >> 5);
+    for (int64_t tb = threadIdx.x >> 5; tb < z.n_tc; tb += nw) {
+      uint32_t n = 0;
+#pragma unroll 4
+      for (int64_t c = lane0; c < kw; c += 32) n += __popc(z.tlive[tb * kw + c]);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+      if (lane0 == 0) {
+        live += n;
+        st += (n + 15) / 16;
+      }
+    }
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -251,7 +117,7 @@ __device__ void k1_choose_path(const K1Scratch& z, int64_t M, int64_t kw, unsign
     }
     const double rt = (double)((M + 127) / 128);
     const double span = (double)out[7];
-    const double slice_nz = (double)z.slice_nz[0], pop = (double)out[5];
+    const double slice_nz = (double)z.btot[0], pop = (double)out[5];
     const double simt = rt * (double)z.n_tb * (double)kw * 1158.0 + rt * (span == 16.0 ? 26.0 * slice_nz : 17.5 * pop) +
                         0.0433 * 128.0 * slice_nz;
     const double tc = rt * (24200.0 * (double)z.n_tc + 784.0 * (double)stages) + 0.0433 * 3.0 * 768.0 * (double)lv;
@@ -263,88 +129,420 @@ __device__ void k1_choose_path(const K1Scratch& z, int64_t M, int64_t kw, unsign
 }
 
 // Block-wide exclusive scan of (cnt[t] + add) -> out[0..n] (out[n] = total); one CTA.
-__device__ void k1_block_exclusive_scan(const uint32_t* __restrict__ cnt, int64_t n, uint32_t add,
-                                        int64_t* __restrict__ out) {
-  __shared__ int64_t carry;
-  __shared__ int64_t wsum[kK1Threads / 32];
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
+// Each thread owns a contiguous segment and loads it with independent loads (one memory
+// latency for the whole scan, not one per 256 elements), then one block scan of the sums.
+template <typename T, typename F>
+__device__ void k1_block_scan_fn(int64_t n, F load, int64_t* __restrict__ out) {
+  __shared__ int64_t wsum[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int64_t base = 0; base < n; base += kK1Threads) {
-    const int64_t t = base + threadIdx.x;
-    const int64_t v = t < n ? (int64_t)cnt[t] + add : 0;
-    int64_t x = v;
+  const int64_t seg = (n + blockDim.x - 1) / blockDim.x;
+  const int64_t b0 = threadIdx.x * seg, b1 = min(b0 + seg, n);
+  int64_t local = 0;
+  for (int64_t i = b0; i < b1; ++i) local += (int64_t)load(i);
+  int64_t x = local;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) wsum[warp] = x;
-    __syncthreads();
-    int64_t before = carry;
-    for (int w = 0; w < warp; ++w) before += wsum[w];
-    if (t < n) out[t] = before + x - v;
-    __syncthreads();
-    if (threadIdx.x == kK1Threads - 1) carry = before + x;
-    __syncthreads();
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
   }
-  if (threadIdx.x == 0) out[n] = carry;
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  int64_t before = 0;
+  for (int w2 = 0; w2 < warp; ++w2) before += wsum[w2];
+  int64_t run = before + x - local;
+  for (int64_t i = b0; i < b1; ++i) {
+    out[i] = run;
+    run += (int64_t)load(i);
+  }
+  if (threadIdx.x == blockDim.x - 1) out[n] = run;
   __syncthreads();
 }
 
+__device__ void k1_block_exclusive_scan(const uint32_t* __restrict__ cnt, int64_t n, uint32_t add,
+                                        int64_t* __restrict__ out) {
+  k1_block_scan_fn<uint32_t>(n, [&](int64_t i) { return (int64_t)cnt[i] + add; }, out);
+}
+
+// The K2-SIMT record offsets on their own (a forced K2-SIMT multiply on an AUTO plan whose
+// last CTA chose K2-TC and skipped them).
+__global__ void __launch_bounds__(kK1Threads) k1_row_off(const uint32_t* __restrict__ cnt, int64_t n,
+                                                         int64_t* __restrict__ out) {
+  k1_block_exclusive_scan(cnt, n, 3, out);
+}
+
 // ------------------------------------------------------------------ fused K1 pass
-// One launch: CTAs [0, nA) are A tiles, [nA, nA + nB) are B tiles; the last CTA to finish
-// (threadfence + done-counter) computes the exact counters and plan statistics.
-__global__ void __launch_bounds__(kK1Threads, 4)
-k1_pass(const float* __restrict__ A, int64_t M, int64_t K, int64_t lda, uint32_t* __restrict__ abits,
-        int64_t a_tiles_x, int64_t nA, const float* __restrict__ B, int64_t ldb, uint8_t* __restrict__ codes,
-        int64_t nreg, uint32_t* __restrict__ bgrp, int64_t b_tiles_x, int64_t nB, int64_t kw, K1Scratch z,
-        int has_a, int has_b, unsigned long long* __restrict__ stats) {
-  const int64_t bid = blockIdx.x;
-  if (bid < nA)
-    k1_a_tile(A, M, K, lda, abits, kw, z, bid % a_tiles_x, bid / a_tiles_x);
-  else
-    k1_b_tile(B, K, ldb, codes, nreg, bgrp, kw, z, (bid - nA) % b_tiles_x, (bid - nA) / b_tiles_x);
+// One persistent launch (2 CTAs per SM): tiles [0, nA) are A tiles, [nA, nA + nB) B tiles,
+// CTA b takes tiles b, b + gridDim.x, ...  Rows reach the SM by TMA bulk copies (one per
+// row segment of <= 4 KB) into a ring of kK1Stages 8-row stages, so HBM sees the copies of
+// the next stages while the warps run the mask / shuffle / A^T work of the current one:
+// thread 0 refills a stage as soon as the 8 warps have read it into registers.  The last
+// CTA to finish (threadfence + done-counter) computes the exact counters, plan statistics
+// and the AUTO path choice.
+constexpr int kK1Stages = 2;
+#ifdef K1_PROF
+__device__ unsigned long long* k1_prof = nullptr;  // debug builds: per-CTA globaltimer stamps
+__device__ __forceinline__ unsigned long long k1_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
+struct K1Ring {
+  float4 buf[kK1Stages][8][kK1Threads];  // 8 rows x 1024 columns per stage (32 KB)
+  uint64_t full[kK1Stages];
+  uint64_t empty[kK1Stages];
+};
+
+__device__ __forceinline__ void k1_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+__device__ __forceinline__ void k1_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "K1W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra K1W_%=;\n\t}" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+struct K1Args {
+  const float* A;
+  int64_t M, K, lda;
+  uint32_t* abits;
+  int64_t a_tx, nA;
+  const float* B;
+  int64_t ldb;
+  int64_t nreg;
+  uint32_t* bgrp;
+  int64_t b_tx, nB, kw;
+};
+
+// Row groups in consumption order: the tiles of this CTA, each tile's 8-row groups.
+struct K1Cursor {
+  const K1Args* g;
+  const K1Scratch* z;
+  int64_t t, rb, rend, c0;  // current tile, its next group's first row, row end, first column
+  const float* base;
+  int64_t ld, cols;         // row stride, readable columns of the operand
+  __device__ void tile_setup() {
+    const K1Args& a = *g;
+    while (t < a.nA + a.nB) {
+      if (t < a.nA) {
+        const int64_t tx = t % a.a_tx, ty = t / a.a_tx;
+        rb = ty * kK1Rows;
+        const int64_t rows_end = z->at ? z->m_at : a.M;  // A^T tiles run to the 128-row boundary
+        rend = min(rb + kK1Rows, rows_end);
+        c0 = tx * kK1Cols;
+        base = a.A;
+        ld = a.lda;
+        cols = (a.K + 3) & ~int64_t(3);
+        // copies stop at row M (rows past it are zeros, not read)
+        if (rb < rend) return;
+      } else {
+        const int64_t tt = t - a.nA, tx = tt % a.b_tx, kwi = tt / a.b_tx;
+        rb = kwi * 32;
+        rend = min(rb + 32, a.K);
+        c0 = tx * kK1Cols;
+        base = a.B;
+        ld = a.ldb;
+        cols = a.ldb;
+        if (rb < rend) return;
+      }
+      t += gridDim.x;
+    }
+  }
+  __device__ bool done() const { return t >= g->nA + g->nB; }
+  // issue this group's row copies into stage slot s, then advance
+  __device__ void issue(K1Ring& r, int s) {
+    const K1Args& a = *g;
+    const int64_t lim = t < a.nA ? a.M : rend;  // A rows past M are zeros: not read
+    const int64_t rows_valid = lim - rb >= 8 ? 8 : (lim - rb > 0 ? lim - rb : 0);
+    const uint32_t bytes = (uint32_t)((cols - c0 >= kK1Cols ? kK1Cols : cols - c0) * 4);
+    mbar_expect(&r.full[s], (uint32_t)rows_valid * bytes);
+    for (int u = 0; u < rows_valid; ++u) k1_bulk(&r.buf[s][u][0], base + (rb + u) * ld + c0, bytes, &r.full[s]);
+    rb += 8;
+    if (rb >= rend) {
+      t += gridDim.x;
+      tile_setup();
+    }
+  }
+  __device__ static void mbar_expect(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(bar)),
+                 "r"(bytes)
+                 : "memory");
+  }
+};
+
+// Loader for the tile functions: the next 8-row group from the ring (thread 0 also refills).
+struct K1RingLoader {
+  K1Ring& r;
+  K1Cursor& cur;
+  uint32_t J;  // groups consumed
+  __device__ void rows8(float4 (&v)[8], const float*, int64_t, bool col_ok, int nvalid) {
+    const int s = J % kK1Stages;
+    k1_wait(&r.full[s], (J / kK1Stages) & 1u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      v[u] = (col_ok && u < nvalid) ? r.buf[s][u][threadIdx.x] : make_float4(0.f, 0.f, 0.f, 0.f);
+    // the TMA refill of this slot (async proxy) must not overtake these generic-proxy reads
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                                                  (uint32_t)__cvta_generic_to_shared(&r.empty[s]))
+                                              : "memory");
+    if (threadIdx.x == 0 && !cur.done()) {  // refill this slot with group J + kK1Stages
+      k1_wait(&r.empty[s], (J / kK1Stages) & 1u);
+      cur.issue(r, s);
+    }
+    ++J;
+  }
+  // x[u][j] = row u, column colofs[j] of the next 8-row group (0 for !ok[j] or u >= nvalid)
+  __device__ void rows(float (&x)[8][4], const int (&colofs)[4], const bool (&ok)[4], int nvalid) {
+    const int s = J % kK1Stages;
+    k1_wait(&r.full[s], (J / kK1Stages) & 1u);
+    const float* st = reinterpret_cast<const float*>(&r.buf[s][0][0]);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) x[u][j] = (ok[j] && u < nvalid) ? st[u * kK1Cols + colofs[j]] : 0.0f;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                                                  (uint32_t)__cvta_generic_to_shared(&r.empty[s]))
+                                              : "memory");
+    ++J;
+  }
+};
+
+// Ballot formulation over the smem ring (k1_pass): warp w owns the 32-column chunks
+// {2w, 2w+1, 2w+16, 2w+17} of the 1024-column tile (a 64-column region is one warp's chunk
+// pair) and lane l column l of each chunk, so one __ballot_sync per (row, chunk) IS the
+// 32-bit mask word: bitmap words, region codes, group / slice masks and popcounts all come
+// from warp-uniform ballots instead of per-lane shuffle chains.
+__device__ __forceinline__ int k1_chunk(int w, int j) { return 2 * w + (j & 1) + 16 * (j >> 1); }
+
+template <typename Loader>
+__device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, uint32_t* __restrict__ abits, int64_t kw,
+                                            const K1Scratch& z, int64_t tx, int64_t ty) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c0 = tx * kK1Cols, r0 = ty * kK1Rows;
+  int colofs[4];
+  bool ok[4];
+  int64_t col[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    colofs[j] = 32 * k1_chunk(w, j) + lane;
+    col[j] = c0 + colofs[j];
+    ok[j] = col[j] < K;
+  }
+  uint32_t ccount[4] = {0, 0, 0, 0};
+  uint32_t warp_total = 0;
+  const int64_t rend = min(r0 + kK1Rows, M);
+  const int64_t rend_at = z.at ? min(r0 + kK1Rows, z.m_at) : rend;
+  for (int64_t rb = r0; rb < rend_at; rb += 8) {
+    float x[8][4];
+    ld.rows(x, colofs, ok, rend - rb >= 8 ? 8 : (rend - rb > 0 ? (int)(rend - rb) : 0));
+#ifdef K1_NOCOMP_A
+    continue;
+#endif
+#ifndef K1_NOAT
+    if (z.at) {
+#else
+    if (false) {
+#endif
+      // A^T tile row k = col holds rows rb..rb+7 at offset rb % 128: two 16-byte stores
+      const int64_t rt = rb >> 7;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (col[j] < z.kpad) {
+          float4* d4 = reinterpret_cast<float4*>(z.at + (rt * z.kpad + col[j]) * 128 + (rb & 127));
+          d4[0] = make_float4(x[0][j], x[1][j], x[2][j], x[3][j]);
+          d4[1] = make_float4(x[4][j], x[5][j], x[6][j], x[7][j]);
+        }
+    }
+    if (rb >= rend) continue;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = rb + u;
+      if (i >= rend) break;
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const bool nz = x[u][j] != 0.0f;
+        const uint32_t m = __ballot_sync(0xffffffffu, nz);
+        ccount[j] += nz ? 1u : 0u;
+        cnt += __popc(m);
+        const int64_t wd = (c0 >> 5) + k1_chunk(w, j);
+        if (lane == j && wd < kw) abits[i * kw + wd] = m;
+      }
+      if (lane == 0 && cnt) atomicAdd(&z.arow[i], cnt);
+      warp_total += cnt;
+    }
+  }
+  if (lane == 0 && warp_total) atomicAdd(&z.tile_sum[ty], warp_total);
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (ok[j] && ccount[j]) atomicAdd(&z.acol[col[j]], ccount[j]);
+}
+
+// B tile: per row only the 8-column group bits enter the group k-masks (gword; the lane
+// owning group g keeps it).  Everything else per row — region codes, Σ popcount(code) and
+// # non-zero codes (the WorkCounters factors), (k, slice) counts — follows from the 32 k-bit
+// masks at the end of the tile: row k's groups are the set bits k of the warp's 16 masks
+// (one ballot per k), a region's code is 8 of them.  The codes themselves are not stored:
+// k1_codes_export rebuilds them from bgrp when a caller asks (export path).
+template <typename Loader>
+__device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, int64_t nreg,
+                                            uint32_t* __restrict__ bgrp, int64_t kw, const K1Scratch& z, int64_t tx,
+                                            int64_t kwi) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c0 = tx * kK1Cols, k0 = kwi * 32;
+  int colofs[4];
+  bool ok[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    colofs[j] = 32 * k1_chunk(w, j) + lane;
+    ok[j] = c0 + colofs[j] < ldb;
+  }
+  // lane g < 16 owns 8-column group g of the warp: chunk g >> 2, sub-group g & 3; lanes
+  // 0..7 are region (chunks 0, 1), lanes 8..15 region (chunks 2, 3)
+  const int gj = (lane >> 2) & 3, gs = lane & 3;
+  const int64_t gcol = c0 + 32 * k1_chunk(w, gj) + 8 * gs;
+  const bool gown = lane < 16 && gcol < ldb;
+  uint32_t gword = 0;
+  const int64_t kend = min(k0 + 32, K);
+  for (int64_t kb = k0; kb < kend; kb += 8) {
+    float x[8][4];
+    ld.rows(x, colofs, ok, kend - kb >= 8 ? 8 : (int)(kend - kb));
+#ifdef K1_NOCOMP_B
+    continue;
+#endif
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      uint32_t m[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) m[j] = __ballot_sync(0xffffffffu, x[u][j] != 0.0f);
+      const uint32_t mg = gj == 0 ? m[0] : gj == 1 ? m[1] : gj == 2 ? m[2] : m[3];
+      gword |= (uint32_t)(((mg >> (8 * gs)) & 0xFFu) != 0) << (uint32_t)(kb - k0 + u);
+    }
+  }
+  if (!gown) gword = 0;
+  if (gown) bgrp[(gcol >> 3) * kw + kwi] = gword;
+  // per k: # non-zero groups (-> bpop) and # non-zero regions (-> bnz) of the warp
+  uint32_t pop_w = 0, nz_w = 0;
+  for (int kk = 0; kk < kend - k0; ++kk) {
+    const uint32_t b = __ballot_sync(0xffffffffu, (gword >> kk) & 1u);
+    const uint32_t pop = __popc(b), nzc = (uint32_t)((b & 0xFFu) != 0) + (uint32_t)((b & 0xFF00u) != 0);
+    pop_w += pop;
+    nz_w += nzc;
+    if (lane == 0 && b) {
+      atomicAdd(&z.bpop[k0 + kk], pop);
+      atomicAdd(&z.bnz[k0 + kk], nzc);
+    }
+  }
+  if (lane == 0 && pop_w) atomicAdd(&z.btot[1], (unsigned long long)pop_w);
+  if (lane == 0 && nz_w) atomicAdd(&z.btot[2], (unsigned long long)nz_w);
+  // (k, 16-column slice) pairs with a non-zero: even group lanes own slice (2s, 2s+1)
+  const uint32_t sib = __shfl_down_sync(0xffffffffu, gword, 1);
+  uint32_t srows = (gown && (lane & 1) == 0) ? (uint32_t)__popc(gword | sib) : 0u;
+  if (z.row_cnt && srows) atomicAdd(&z.row_cnt[(gcol >> 8) * kw + kwi], srows);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) srows += __shfl_xor_sync(0xffffffffu, srows, o);
+  if (lane == 0 && srows) atomicAdd(&z.btot[0], (unsigned long long)srows);
+  if (z.tlive && gword) atomicOr(&z.tlive[(gcol / kTcTileN) * kw + kwi], gword);
+}
+
+// Region codes (kernel_table.cpp:19: bit 7-j <-> 8-column group j, MSB first) from the group
+// k-masks — export path (BPlan codes), one thread per (k, region).
+__global__ void k1_codes_export(const uint32_t* __restrict__ bgrp, int64_t K, int64_t nreg, int64_t kw,
+                                uint8_t* __restrict__ codes) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= K * nreg) return;
+  const int64_t k = t / nreg, r = t % nreg;
+  uint32_t code = 0;
+#pragma unroll
+  for (int g = 0; g < 8; ++g) code |= ((bgrp[(8 * r + g) * kw + (k >> 5)] >> (k & 31)) & 1u) << (7 - g);
+  codes[t] = (uint8_t)code;
+}
+
+__global__ void __launch_bounds__(kK1Block, 3)
+k1_pass(K1Args g, K1Scratch z, int has_a, int has_b, unsigned long long* __restrict__ stats) {
+#ifdef K1_PROF
+  const unsigned long long t_start = k1_now();
+#endif
+  extern __shared__ __align__(128) uint8_t k1_raw[];
+  K1Ring& r = *reinterpret_cast<K1Ring*>(k1_raw + ((128 - ((uint32_t)__cvta_generic_to_shared(k1_raw) & 127)) & 127));
+  const int64_t M = g.M, K = g.K, nA = g.nA, nB = g.nB, kw = g.kw, nreg = g.nreg;
+  K1Cursor cur{&g, &z, (int64_t)blockIdx.x, 0, 0, 0, nullptr, 0, 0};
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kK1Stages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(&r.full[s])),
+                   "r"(1u)
+                   : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(&r.empty[s])),
+                   "r"((uint32_t)(kK1Threads / 32))
+                   : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x >= kK1Threads) {
+    // TMA producer warp: refill a stage as soon as the 8 compute warps have read it
+    if (threadIdx.x == kK1Threads) {
+      cur.tile_setup();
+      for (uint32_t J = 0; !cur.done(); ++J) {
+        const int s = J % kK1Stages;
+        k1_wait(&r.empty[s], ((J / kK1Stages) & 1u) ^ 1u);
+        cur.issue(r, s);
+      }
+    }
+  } else {
+    K1RingLoader ld{r, cur, 0u};
+    for (int64_t t = blockIdx.x; t < nA + nB; t += gridDim.x) {
+      if (t < nA)
+        k1_a_tile_b(ld, M, K, g.abits, kw, z, t % g.a_tx, t / g.a_tx);
+      else
+        k1_b_tile_b(ld, K, g.ldb, nreg, g.bgrp, kw, z, (t - nA) % g.b_tx, (t - nA) / g.b_tx);
+    }
+  }
   __shared__ unsigned int last;
   __syncthreads();
+#ifdef K1_PROF
+  if (threadIdx.x == 0 && k1_prof) {
+    k1_prof[4 * blockIdx.x] = t_start;
+    k1_prof[4 * blockIdx.x + 1] = k1_now();
+  }
+#endif
   if (threadIdx.x == 0) {
     __threadfence();  // cumulative over the CTA's writes ordered by the barrier above
-    last = atomicAdd(z.done, 1u) == (unsigned int)(nA + nB - 1);
+    last = atomicAdd(z.done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
   if (!last) return;
   __threadfence();
   if (threadIdx.x == 0) *z.done = 0u;  // ready for the next launch (no other CTA is left)
-  k1_finalize_block(z.acol, z.bpop, z.bnz, K, M, nreg, has_a, has_b, z.slice_nz, stats);
+  k1_plan_totals(z.btot, K, nreg, has_b, stats);
   if (z.choose && has_a && has_b) k1_choose_path(z, M, kw, stats);
-  if (z.row_cnt && nB > 0) k1_block_exclusive_scan(z.row_cnt, z.n_tb * kw, 3, z.row_off);
+  // the K2-SIMT record offsets only when K2-SIMT can run (its pack is gated out otherwise)
+  if (z.row_cnt && nB > 0 && !(z.choose && stats[7] == 32ull))
+    k1_block_exclusive_scan(z.row_cnt, z.n_tb * kw, 3, z.row_off);
   if (nA > 0) {  // exclusive prefix of the 32-row tile sums for k1_csr's row_ptr
-    __shared__ int64_t carry;
-    __shared__ int64_t wsum[kK1Threads / 32];
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
     const int64_t ntile = (M + kK1Rows - 1) / kK1Rows;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int64_t base = 0; base < ntile; base += kK1Threads) {
-      const int64_t t = base + threadIdx.x;
-      const int64_t v = t < ntile ? (int64_t)z.tile_sum[t] : 0;
-      int64_t x = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      if (lane == 31) wsum[warp] = x;
-      __syncthreads();
-      int64_t before = carry;
-      for (int w = 0; w < warp; ++w) before += wsum[w];
-      if (t < ntile) z.tile_prefix[t] = before + x - v;
-      __syncthreads();
-      if (threadIdx.x == kK1Threads - 1) carry = before + x;
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) z.tile_prefix[ntile] = carry;
+    const uint32_t* ts = z.tile_sum;
+    k1_block_scan_fn<uint32_t>(ntile, [&](int64_t i) { return (int64_t)ts[i]; }, z.tile_prefix);
   }
+#ifdef K1_PROF
+  if (threadIdx.x == 0 && k1_prof) {
+    k1_prof[4 * blockIdx.x + 2] = k1_now();
+    k1_prof[4 * blockIdx.x + 3] = 1;
+  }
+#endif
 }
 
 // --------------------------------------------------------------- CSR index lists
@@ -418,61 +616,67 @@ __global__ void __launch_bounds__(256) k1_csr(const uint32_t* __restrict__ abits
 }
 
 // ---------------------------------------------------------------- counters + stats
-// Exact WorkCounters of the coming multiply and plan_stats:
+// Exact WorkCounters of the coming multiply:
 //   lane_fma_ops  = Σ_k acol[k] * 8 * bpop[k]
 //   invocations   = Σ_k acol[k] * bnz[k]
 //   zero regions  = Σ_k acol[k] * (nreg - bnz[k])
 //   rows_skipped  = M*K - Σ_k acol[k]
-//   stats         = Σ_k bpop[k], Σ_k (nreg - bnz[k])
-// out: u64[9] = {inv, lanes, skipped, zreg, nnzA, pop_total, zero_codes, path, span}
-//   span: K2-SIMT mask granularity, from the cost model of DESIGN.md (K2 variants):
-//   16-column slices cost ~41 issue slots per non-zero (k, slice), 8-column groups ~23 per
-//   non-zero (k, group); pick the cheaper (slice_nz[0] = # non-zero (k, slice) pairs).
-__device__ void k1_finalize_block(const uint32_t* __restrict__ acol, const uint32_t* __restrict__ bpop,
-                                                    const uint32_t* __restrict__ bnz, int64_t K, int64_t M,
-                                  int64_t nreg, int has_a, int has_b,
-                                  const unsigned long long* __restrict__ slice_nz,
-                                  unsigned long long* __restrict__ out) {
-  unsigned long long s[6] = {0, 0, 0, 0, 0, 0};
+// out[0..4] = {inv, lanes, skipped, zreg, nnzA}.  Only a caller that asks for the counters
+// pays for this pass (mmmcu_get_counters / multiply with counters): it is not needed to
+// multiply.  The plan totals out[5] = Σ bpop (pop_total), out[6] = Σ (nreg - bnz)
+// (zero codes) and the path choice out[7] / span out[8] come from K1's last CTA
+// (k1_plan_totals) out of per-warp atomics of the B tiles.
+__global__ void __launch_bounds__(1024) k1_counters(const uint32_t* __restrict__ acol, const uint32_t* __restrict__ bpop,
+                                                    const uint32_t* __restrict__ bnz, int64_t K, int64_t M, int64_t nreg,
+                                                    int has_a, int has_b, unsigned long long* __restrict__ out) {
+  unsigned long long s[4] = {0, 0, 0, 0};
+#pragma unroll 4
   for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
     const unsigned long long a = has_a ? acol[k] : 0ull;
     const unsigned long long p = has_b ? bpop[k] : 0ull;
-    const unsigned long long z = has_b ? (unsigned long long)(nreg - (int64_t)bnz[k]) : 0ull;
     const unsigned long long n = has_b ? bnz[k] : 0ull;
+    const unsigned long long z = has_b ? (unsigned long long)nreg - n : 0ull;
     s[0] += a * n;
     s[1] += a * 8ull * p;
     s[2] += a * z;
     s[3] += a;
-    s[4] += p;
-    s[5] += z;
   }
-  __shared__ unsigned long long red[32][6];
+  __shared__ unsigned long long red[32][4];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int q = 0; q < 6; ++q) {
+  for (int q = 0; q < 4; ++q) {
     unsigned long long v = s[q];
 #pragma unroll
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if (lane == 0) red[warp][q] = v;
   }
   __syncthreads();
-  if (threadIdx.x < 6) {
-    unsigned long long v = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[w][threadIdx.x];
-    red[0][threadIdx.x] = v;
-  }
-  __syncthreads();
   if (threadIdx.x == 0) {
-    out[0] = red[0][0];
-    out[1] = red[0][1];
-    out[2] = (unsigned long long)(M * K) - red[0][3];
-    out[3] = red[0][2];
-    out[4] = red[0][3];
-    out[5] = red[0][4];
-    out[6] = red[0][5];
-    out[7] = (has_b && 41ull * slice_nz[0] > 23ull * red[0][4]) ? 8ull : 16ull;
+    unsigned long long v[4] = {0, 0, 0, 0};
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+      for (int q = 0; q < 4; ++q) v[q] += red[w][q];
+    out[0] = v[0];
+    out[1] = v[1];
+    out[2] = (unsigned long long)(M * K) - v[3];
+    out[3] = v[2];
+    out[4] = v[3];
+  }
+}
+
+// Plan totals (K1's last CTA): pop_total, zero codes and the K2-SIMT span from the B tiles'
+// totals btot = {Σ non-zero (k, slice), Σ bpop, Σ bnz}.
+//   span: 16-column slices cost ~41 issue slots per non-zero (k, slice), 8-column groups ~23
+//   per non-zero (k, group); pick the cheaper.
+__device__ void k1_plan_totals(const unsigned long long* __restrict__ btot, int64_t K, int64_t nreg, int has_b,
+                               unsigned long long* __restrict__ out) {
+  if (threadIdx.x == 0) {
+    const unsigned long long pop = has_b ? btot[1] : 0ull, bnz = has_b ? btot[2] : 0ull;
+    out[5] = pop;
+    out[6] = has_b ? (unsigned long long)(K * nreg) - bnz : 0ull;
+    out[7] = (has_b && 41ull * btot[0] > 23ull * pop) ? 8ull : 16ull;
     out[8] = out[7];  // the K2-SIMT span alone (out[7] may become 32 = K2-TC, k1_choose_path)
   }
+  __syncthreads();
 }
 
 // ------------------------------------------------------ B steps for K2-TC (dense tiles)

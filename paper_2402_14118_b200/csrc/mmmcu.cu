@@ -150,7 +150,7 @@ uint32_t* za_acol(mmmcu_ctx* ctx) { return ctx->za.as<uint32_t>() + ctx->M; }
 uint32_t* za_tiles(mmmcu_ctx* ctx) { return ctx->za.as<uint32_t>() + ctx->M + ctx->Ka; }
 int64_t n_row_tiles(int64_t M) { return (M + mmmcu::kK1Rows - 1) / mmmcu::kK1Rows; }
 unsigned long long* zb_slice(mmmcu_ctx* ctx) { return ctx->zb.as<unsigned long long>(); }
-uint32_t* zb_bpop(mmmcu_ctx* ctx) { return reinterpret_cast<uint32_t*>(ctx->zb.as<unsigned long long>() + 1); }
+uint32_t* zb_bpop(mmmcu_ctx* ctx) { return reinterpret_cast<uint32_t*>(ctx->zb.as<unsigned long long>() + 3); }
 uint32_t* zb_bnz(mmmcu_ctx* ctx) { return zb_bpop(ctx) + ctx->Kb; }
 // Operand sets K1 emits for K2: A^T tiles (SIMT v2, TC), raw B rows (SIMT v2), tf32 B step
 // images + live-k lists (TC).
@@ -214,7 +214,7 @@ mmmcu_status stage_b(mmmcu_ctx* ctx, const float* B, int64_t K, int64_t N, int64
   const int64_t n_cnt = n_tb * kw;
   const int64_t n_tc = (ldb + mmmcu::kTcTileN - 1) / mmmcu::kTcTileN;
   const int64_t n_extra = ((ops & OP_TCB) ? n_tc * kw : 0) + ((ops & OP_ROWS) ? n_cnt : 0);
-  const size_t zb_bytes = sizeof(unsigned long long) + sizeof(uint32_t) * (2 * K + n_extra);
+  const size_t zb_bytes = 3 * sizeof(unsigned long long) + sizeof(uint32_t) * (2 * K + n_extra);
   MMMCU_CUDA(ctx->zb.ensure(zb_bytes));
   MMMCU_CUDA(cudaMemsetAsync(ctx->zb.p, 0, zb_bytes, ctx->stream));
   ctx->n_tb = n_tb;
@@ -315,7 +315,7 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   z.tile_prefix = do_a ? ctx->tile_prefix.as<int64_t>() : nullptr;
   z.bpop = b_valid ? zb_bpop(ctx) : nullptr;
   z.bnz = b_valid ? zb_bnz(ctx) : nullptr;
-  z.slice_nz = b_valid ? zb_slice(ctx) : ctx->stats.as<unsigned long long>() + 15;
+  z.btot = b_valid ? zb_slice(ctx) : ctx->stats.as<unsigned long long>() + 12;
   z.done = ctx->ctl.as<unsigned int>();
   z.at = tc_a ? ctx->at.as<float>() : nullptr;
   z.kpad = ctx->kpad;
@@ -328,10 +328,44 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   z.choose = gate ? 1 : 0;
   const int has_a = a_valid && (same_k || !b_valid) ? 1 : 0;
   const int has_b = b_valid && (same_k || !a_valid) ? 1 : 0;
-  mmmcu::k1_pass<<<(unsigned)(nA + nB), mmmcu::kK1Threads, 0, ctx->stream>>>(
-      ctx->A, ctx->M, K, ctx->lda, ctx->abits.as<uint32_t>(), a_tx, nA, ctx->B, ctx->ldb, ctx->codes.as<uint8_t>(),
-      ctx->ldb / 64, ctx->bgrp.as<uint32_t>(), b_tx, nB, kw, z, has_a, has_b, ctx->stats.as<unsigned long long>());
+  if (ctx->num_sms == 0) MMMCU_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  const mmmcu::K1Args g{ctx->A, ctx->M, K, ctx->lda, ctx->abits.as<uint32_t>(), a_tx, nA,
+                        ctx->B, ctx->ldb, ctx->ldb / 64, ctx->bgrp.as<uint32_t>(), b_tx, nB, kw};
+  const int k1_smem = (int)sizeof(mmmcu::K1Ring) + 128;
+  MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k1_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, k1_smem));
+  const unsigned k1_grid = (unsigned)std::min<int64_t>(nA + nB, 3 * (int64_t)ctx->num_sms);
+  mmmcu::k1_pass<<<k1_grid, mmmcu::kK1Block, k1_smem, ctx->stream>>>(g, z, has_a, has_b,
+                                                                       ctx->stats.as<unsigned long long>());
   MMMCU_LAUNCHED();
+#ifdef K1_PROF
+  {
+    static unsigned long long* dbuf = nullptr;
+    if (!dbuf) cudaMalloc(&dbuf, 8 * 4 * 4096);
+    cudaDeviceSynchronize();
+    cudaMemset(dbuf, 0, 8 * 4 * 4096);
+    cudaMemcpyToSymbol(mmmcu::k1_prof, &dbuf, sizeof(dbuf));
+    // rerun (idempotent outputs; counters are re-zeroed by the caller's memsets only once, so
+    // use the stamps, not the counters)
+    mmmcu::k1_pass<<<k1_grid, mmmcu::kK1Block, k1_smem, ctx->stream>>>(g, z, has_a, has_b,
+                                                                         ctx->stats.as<unsigned long long>());
+    cudaDeviceSynchronize();
+    std::vector<unsigned long long> h(4 * k1_grid);
+    cudaMemcpy(h.data(), dbuf, 8 * 4 * k1_grid, cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ull, t1 = 0, tmax_start = 0, fin = 0, fin_start = 0;
+    double dsum = 0;
+    for (unsigned i = 0; i < k1_grid; ++i) {
+      t0 = std::min(t0, h[4 * i]);
+      tmax_start = std::max(tmax_start, h[4 * i]);
+      t1 = std::max(t1, h[4 * i + 1]);
+      dsum += (double)(h[4 * i + 1] - h[4 * i]);
+      if (h[4 * i + 3]) { fin = h[4 * i + 2]; fin_start = h[4 * i + 1]; }
+    }
+    fprintf(stderr, "K1_PROF: grid %u, CTA start spread %.1f us, tiles done by %.1f us (mean CTA %.1f us), finalize %.1f us, total %.1f us\n",
+            k1_grid, (tmax_start - t0) / 1e3, (t1 - t0) / 1e3, dsum / k1_grid / 1e3, (fin - fin_start) / 1e3, (fin - t0) / 1e3);
+    void* zp = nullptr;
+    cudaMemcpyToSymbol(mmmcu::k1_prof, &zp, sizeof(zp));
+  }
+#endif
   if (do_a) {
     const unsigned blocks = (unsigned)((ctx->M + mmmcu::kCsrRows - 1) / mmmcu::kCsrRows);
     const int64_t akw = (ctx->Ka + 31) / 32;
@@ -478,6 +512,15 @@ mmmcu_status read_stats(mmmcu_ctx* ctx, unsigned long long* host16) {
 
 mmmcu_status fill_counters(mmmcu_ctx* ctx, mmmcu_counters* out) {
   if (!out) return MMMCU_OK;
+  // the A-dependent sums are computed on request only (k1_counters)
+  const bool a_ok = ctx->has_a, b_ok = ctx->has_b;
+  const bool same_k = a_ok && b_ok && ctx->Ka == ctx->Kb;
+  const int64_t K = b_ok ? ctx->Kb : ctx->Ka;
+  mmmcu::k1_counters<<<1, 1024, 0, ctx->stream>>>(a_ok ? za_acol(ctx) : nullptr, b_ok ? zb_bpop(ctx) : nullptr,
+                                                  b_ok ? zb_bnz(ctx) : nullptr, K, ctx->M, ctx->ldb / 64,
+                                                  (a_ok && (same_k || !b_ok)) ? 1 : 0, (b_ok && (same_k || !a_ok)) ? 1 : 0,
+                                                  ctx->stats.as<unsigned long long>());
+  MMMCU_LAUNCHED();
   unsigned long long s[16];
   MMMCU_TRY(read_stats(ctx, s));
   out->kernel_invocations = s[0];
@@ -577,11 +620,21 @@ mmmcu_status mmmcu_get_plan_stats(mmmcu_ctx* ctx, mmmcu_plan_stats* out) {
   return MMMCU_OK;
 }
 
+// The region codes are not materialised by K1's hot pass; rebuild them from the group masks.
+mmmcu_status build_codes(mmmcu_ctx* ctx) {
+  const int64_t n = ctx->Kb * (ctx->ldb / 64);
+  mmmcu::k1_codes_export<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(
+      ctx->bgrp.as<uint32_t>(), ctx->Kb, ctx->ldb / 64, (ctx->Kb + 31) / 32, ctx->codes.as<uint8_t>());
+  MMMCU_LAUNCHED();
+  return MMMCU_OK;
+}
+
 mmmcu_status mmmcu_export_b_codes(mmmcu_ctx* ctx, uint8_t* codes_host, int64_t capacity) {
   MMMCU_TRY(bind(ctx));
   if (!ctx->has_b) return fail(ctx, MMMCU_ERR_NOT_READY, "no B plan");
   const int64_t n = ctx->Kb * (ctx->ldb / 64);
   if (!codes_host || capacity < n) return fail(ctx, MMMCU_ERR_INVALID_ARG, "codes buffer too small");
+  MMMCU_TRY(build_codes(ctx));
   MMMCU_CUDA(cudaMemcpyAsync(codes_host, ctx->codes.p, (size_t)n, cudaMemcpyDeviceToHost, ctx->stream));
   MMMCU_CUDA(cudaStreamSynchronize(ctx->stream));
   return MMMCU_OK;
@@ -599,6 +652,7 @@ mmmcu_status mmmcu_export_bplans(mmmcu_ctx* ctx, int64_t leaf_dim, uint8_t* plan
   if (!plans_host || plans_capacity < K * nreg || !plan_off_host || off_capacity < n_lr * n_lc + 1)
     return fail(ctx, MMMCU_ERR_INVALID_ARG, "plan buffers too small");
   std::vector<uint8_t> codes((size_t)(K * nreg));
+  MMMCU_TRY(build_codes(ctx));
   MMMCU_CUDA(cudaMemcpyAsync(codes.data(), ctx->codes.p, codes.size(), cudaMemcpyDeviceToHost, ctx->stream));
   MMMCU_CUDA(cudaStreamSynchronize(ctx->stream));
   int64_t pos = 0, p = 0;
@@ -727,6 +781,9 @@ mmmcu_status mmmcu_multiply(mmmcu_ctx* ctx, float* C, int64_t ldc, const float* 
     const int span = ctx->algo == MMMCU_ALGO_SIMT_SPAN8 ? 8 : ctx->algo == MMMCU_ALGO_SIMT_SPAN16 ? 16 : 0;
     ctx->last_algo = span == 8 ? MMMCU_ALGO_SIMT_SPAN8 : span == 16 ? MMMCU_ALGO_SIMT_SPAN16 : MMMCU_ALGO_SIMT_BCAST;
     if (ctx->op_rows && !ctx->rows_fresh) {
+      mmmcu::k1_row_off<<<1, mmmcu::kK1Threads, 0, ctx->stream>>>(zb_row_cnt(ctx), ctx->n_tb * ((ctx->Kb + 31) / 32),
+                                                                   ctx->row_off.as<int64_t>());
+      MMMCU_LAUNCHED();
       MMMCU_TRY(pack_rows(ctx));
       ctx->rows_fresh = true;
     }
