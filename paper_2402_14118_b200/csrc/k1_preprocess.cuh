@@ -311,7 +311,9 @@ struct K1RingLoader {
     for (int u = 0; u < 8; ++u)
 #pragma unroll
       for (int j = 0; j < 4; ++j) x[u][j] = (ok[j] && u < nvalid) ? st[u * kK1Cols + colofs[j]] : 0.0f;
+#ifndef K1_NOFENCE
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
     __syncwarp();
     if ((threadIdx.x & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
                                                   (uint32_t)__cvta_generic_to_shared(&r.empty[s]))
@@ -343,6 +345,7 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
   }
   uint32_t ccount[4] = {0, 0, 0, 0};
   uint32_t warp_total = 0;
+  __shared__ uint32_t s_ab[kK1Rows][32];  // the tile's bitmap words (row, chunk)
   const int64_t rend = min(r0 + kK1Rows, M);
   const int64_t rend_at = z.at ? min(r0 + kK1Rows, z.m_at) : rend;
   for (int64_t rb = r0; rb < rend_at; rb += 8) {
@@ -378,10 +381,11 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
         const uint32_t m = __ballot_sync(0xffffffffu, nz);
         ccount[j] += nz ? 1u : 0u;
         cnt += __popc(m);
-        const int64_t wd = (c0 >> 5) + k1_chunk(w, j);
-        if (lane == j && wd < kw) abits[i * kw + wd] = m;
+        if (lane == j) s_ab[i - r0][k1_chunk(w, j)] = m;  // staged: written row-contiguous below
       }
+#ifndef K1_NOATOM
       if (lane == 0 && cnt) atomicAdd(&z.arow[i], cnt);
+#endif
       warp_total += cnt;
     }
   }
@@ -389,6 +393,12 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
 #pragma unroll
   for (int j = 0; j < 4; ++j)
     if (ok[j] && ccount[j]) atomicAdd(&z.acol[col[j]], ccount[j]);
+  // the tile's bitmap words, row by row (32 words = 128 contiguous bytes per row)
+  asm volatile("bar.sync 2, %0;" ::"r"(kK1Threads) : "memory");
+  const int64_t wd = (c0 >> 5) + lane;
+  for (int rr = w; rr < kK1Rows; rr += kK1Threads / 32)
+    if (r0 + rr < rend && wd < kw) abits[(r0 + rr) * kw + wd] = s_ab[rr][lane];
+  asm volatile("bar.sync 2, %0;" ::"r"(kK1Threads) : "memory");
 }
 
 // B tile: per row only the 8-column group bits enter the group k-masks (gword; the lane
@@ -434,17 +444,19 @@ __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, 
   }
   if (!gown) gword = 0;
   if (gown) bgrp[(gcol >> 3) * kw + kwi] = gword;
-  // per k: # non-zero groups (-> bpop) and # non-zero regions (-> bnz) of the warp
-  uint32_t pop_w = 0, nz_w = 0;
-  for (int kk = 0; kk < kend - k0; ++kk) {
-    const uint32_t b = __ballot_sync(0xffffffffu, (gword >> kk) & 1u);
-    const uint32_t pop = __popc(b), nzc = (uint32_t)((b & 0xFFu) != 0) + (uint32_t)((b & 0xFF00u) != 0);
-    pop_w += pop;
-    nz_w += nzc;
-    if (lane == 0 && b) {
-      atomicAdd(&z.bpop[k0 + kk], pop);
-      atomicAdd(&z.bnz[k0 + kk], nzc);
-    }
+  // plan totals of the warp: Σ_k # non-zero groups = Σ_g popc(gword_g); Σ_k # non-zero
+  // regions = popc of each region's OR-ed masks (lanes 0-7 / 8-15).  The per-k factors
+  // (bpop, bnz) are derived from bgrp only when counters are requested (k1_counters).
+  uint32_t pop_w = __popc(gword);
+  uint32_t ror = gword;
+  ror |= __shfl_xor_sync(0xffffffffu, ror, 1);
+  ror |= __shfl_xor_sync(0xffffffffu, ror, 2);
+  ror |= __shfl_xor_sync(0xffffffffu, ror, 4);
+  uint32_t nz_w = (lane == 0 || lane == 8) ? (uint32_t)__popc(ror) : 0u;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    pop_w += __shfl_xor_sync(0xffffffffu, pop_w, o);
+    nz_w += __shfl_xor_sync(0xffffffffu, nz_w, o);
   }
   if (lane == 0 && pop_w) atomicAdd(&z.btot[1], (unsigned long long)pop_w);
   if (lane == 0 && nz_w) atomicAdd(&z.btot[2], (unsigned long long)nz_w);
@@ -626,6 +638,29 @@ __global__ void __launch_bounds__(256) k1_csr(const uint32_t* __restrict__ abits
 // multiply.  The plan totals out[5] = Σ bpop (pop_total), out[6] = Σ (nreg - bnz)
 // (zero codes) and the path choice out[7] / span out[8] come from K1's last CTA
 // (k1_plan_totals) out of per-warp atomics of the B tiles.
+// bpop[k] (# non-zero 8-column groups of row k) and bnz[k] (# non-zero 64-column regions)
+// from the group k-masks: thread per k walks the ld/8 groups.
+__global__ void k1_bcounts(const uint32_t* __restrict__ bgrp, int64_t K, int64_t nreg, int64_t kw,
+                           uint32_t* __restrict__ bpop, uint32_t* __restrict__ bnz) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const int64_t w = k >> 5;
+  const uint32_t bit = 1u << (k & 31);
+  uint32_t pop = 0, nz = 0;
+  for (int64_t r = 0; r < nreg; ++r) {
+    uint32_t any = 0;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      const uint32_t b = (bgrp[(8 * r + g) * kw + w] & bit) ? 1u : 0u;
+      pop += b;
+      any |= b;
+    }
+    nz += any;
+  }
+  bpop[k] = pop;
+  bnz[k] = nz;
+}
+
 __global__ void __launch_bounds__(1024) k1_counters(const uint32_t* __restrict__ acol, const uint32_t* __restrict__ bpop,
                                                     const uint32_t* __restrict__ bnz, int64_t K, int64_t M, int64_t nreg,
                                                     int has_a, int has_b, unsigned long long* __restrict__ out) {

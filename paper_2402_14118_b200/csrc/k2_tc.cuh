@@ -57,9 +57,11 @@ constexpr int kTdPStride = kTdTN + 4;         // staged P row stride (floats): c
 
 struct TdShared {
   float b[kTdStages][kTdSub * kTdStepFloats];  // 4 x 24 KB
+  float a[kTdStages][8 * kTdSub][kTdTM];       // the stage's live A^T rows (4 x 8 KB)
   float p[kTdTM][kTdPStride];                  // C-update staging (98 KB)
-  uint64_t full[kTdStages];    // stage ready: B bytes landed (producer expect_tx) + A in TMEM (4 warps)
-  uint64_t empty[kTdStages];   // stage consumed: one tcgen05.commit frees the B smem and the A slot
+  uint64_t tma[kTdStages];     // the stage's B image and A rows landed (TMA bytes)
+  uint64_t full[kTdStages];    // stage ready: A split into its TMEM slot (4 transform warps)
+  uint64_t empty[kTdStages];   // stage consumed: one tcgen05.commit frees B / A smem and the A slot
   uint64_t seg_full[2];                        // segment's last MMAs done (tcgen05.commit)
   uint64_t seg_empty[2];                       // D drained (8 accumulator warps)
   uint32_t tmem_base;
@@ -76,6 +78,11 @@ __device__ __forceinline__ void td_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+// A tile whose B columns leave >= 3/4 of k live gets its A rows by TMA (runs of consecutive
+// live k: ~1 copy per stage); sparser tiles would need up to 16 copies of 512 B per stage,
+// more TMA time than the MMAs leave, so their A rows come through the transform warps' loads.
+__device__ __forceinline__ bool td_dense(int32_t live, int64_t kpad) { return 4 * (int64_t)live >= 3 * kpad; }
+
 __device__ __forceinline__ void td_named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -97,7 +104,8 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
 
   if (tid == 0) {
     for (int s = 0; s < kTdStages; ++s) {
-      tc::mbar_init(&sh.full[s], 5);
+      tc::mbar_init(&sh.tma[s], 1);
+      tc::mbar_init(&sh.full[s], 4);
       tc::mbar_init(&sh.empty[s], 1);
     }
     for (int d = 0; d < 2; ++d) {
@@ -114,34 +122,51 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
   constexpr uint32_t kAcol = 2 * kTdTN;  // TMEM columns of the A slots
 
   if (warp == 12) {
-    // ------------------------------------------------------- TMA producer (B stages)
-    if (lane == 0) {
-      uint32_t J = 0;
-#ifdef TD_PROF
-      long long pw = 0;
-#endif
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int64_t tb = t / m_tiles;
-        const int nsteps = (tcn[tb] + 7) >> 3;
-        const int nstage = (nsteps + kTdSub - 1) / kTdSub;
-        for (int j = 0; j < nstage; ++j, ++J) {
-          const int st = J % kTdStages;
-          const uint32_t bytes = (uint32_t)min(kTdSub, nsteps - kTdSub * j) * kTdStepFloats * 4u;
-          TD_CLK(c0);
-          tc::mbar_wait(&sh.empty[st], ((J / kTdStages) & 1u) ^ 1u);
-          TD_CLK(c1);
-#ifdef TD_PROF
-          pw += c1 - c0;
-#endif
-          td_expect_tx(&sh.full[st], bytes);
-          td_bulk(sh.b[st], tcb + (tb * maxsteps + kTdSub * j) * kTdStepFloats, bytes, &sh.full[st]);
+    // ---------------------------------------------------- TMA producer (B and A per stage)
+    // Per stage: one bulk copy of the two B step images, and the stage's 16 live A^T rows
+    // of the tile — one bulk copy per run of consecutive live k (a dense tile: 1 copy of
+    // 8 KB).  Lane e < 16 holds live k number e of the stage (prefetched a stage ahead).
+    uint32_t J = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t rt = t % m_tiles, tb = t / m_tiles;
+      const int32_t total = tcn[tb];
+      const int nsteps = (total + 7) >> 3;
+      const int nstage = (nsteps + kTdSub - 1) / kTdSub;
+      const bool a_tma = td_dense(total, kpad);  // else the transform warps load A (LDG)
+      const int32_t* kx = tck + tb * maxsteps * 8;
+      const float* atile = AT + rt * kpad * 128;
+      const int npos = nsteps * 8;
+      // lane l holds live k number 32p + l for the stage pair p (prefetched a pair ahead:
+      // the tck latency stays off the per-stage issue path)
+      int kpair = lane < npos ? __ldg(kx + lane) : -1;
+      int knext = 0;
+      for (int j = 0; j < nstage; ++j, ++J) {
+        const int st = J % kTdStages;
+        if ((j & 1) == 0) {
+          const int pn = (j + 2) * 16 + lane;
+          knext = pn < npos ? __ldg(kx + pn) : -1;
         }
+        int kcur = __shfl_sync(0xffffffffu, kpair, 16 * (j & 1) + (lane & 15));
+        if (lane >= 16) kcur = -1;
+        const int prev = __shfl_up_sync(0xffffffffu, kcur, 1);
+        const bool valid = a_tma && lane < 16 && kcur >= 0;
+        const bool cont = valid && lane > 0 && prev + 1 == kcur;
+        const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+        const uint32_t cmask = __ballot_sync(0xffffffffu, cont);
+        const uint32_t bytes = (uint32_t)min(kTdSub, nsteps - kTdSub * j) * kTdStepFloats * 4u;
+        if (lane == 0) {
+          tc::mbar_wait(&sh.empty[st], ((J / kTdStages) & 1u) ^ 1u);
+          td_expect_tx(&sh.tma[st], bytes + 512u * (uint32_t)__popc(vmask));
+          td_bulk(sh.b[st], tcb + (tb * maxsteps + kTdSub * j) * kTdStepFloats, bytes, &sh.tma[st]);
+        }
+        __syncwarp();
+        if (valid && !cont) {  // run start: rows kcur .. kcur + len - 1 -> slots lane .. lane + len - 1
+          const uint32_t len = (uint32_t)__ffs(~(cmask >> (lane + 1)));
+          td_bulk(sh.a[st][lane], atile + (int64_t)kcur * 128, 512u * len, &sh.tma[st]);
+        }
+        if (j & 1) kpair = knext;
       }
-#ifdef TD_PROF
-      if (td_prof) td_prof[16 * blockIdx.x + 7] = pw;
-#endif
     }
-    __syncwarp();
   } else if (warp == 13) {
     // ------------------------------------------------------------------ MMA issuer
     // The whole warp runs the loop (warp-uniform operands stay in uniform registers); one
@@ -164,6 +189,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
         TD_CLK(c0);
         if (j % kTdSeg == 0 && G >= 2) tc::mbar_wait(&sh.seg_empty[d], ((G - 2) >> 1) & 1u);
         TD_CLK(c1);
+        tc::mbar_wait(&sh.tma[st], (J / kTdStages) & 1u);
         tc::mbar_wait(&sh.full[st], (J / kTdStages) & 1u);
         TD_CLK(c2);
         TD_ADD(0, c1 - c0);
@@ -203,84 +229,90 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
 #endif
   } else if (warp < 4) {
     // ---------------------------------------------------------------- A transform
-    // Thread r owns tile row r (== TMEM lane r).  A is read straight from the K1 A^T tile
-    // (a warp reads 128 contiguous bytes per k) one batch of 2 stages ahead, with the
-    // live-k list two batches ahead; split into tf32 hi / lo; tcgen05.st into the slot's
-    // TMEM columns once the MMAs of stage J - kTdStages have released them.
-    constexpr int kB = 2, KB = 8 * kTdSub * kB;  // stages per batch, k per batch
+    // Thread r owns tile row r (== TMEM lane r).  Per stage it splits the stage's 16 live A
+    // values of its row into tf32 hi / lo and stores them with one tcgen05.st of 32 columns
+    // into the stage's TMEM slot, then arrives on full.  The values come from smem (dense
+    // tiles: the producer's TMA runs, `tma` barrier) or from the K1 A^T tile directly
+    // (sparse tiles: coalesced loads one batch of 2 stages ahead, live-k list two batches
+    // ahead, after the slot's previous MMAs released it: `empty` barrier).
     const int r = tid;
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
     uint32_t J = 0;
-#ifdef TD_PROF
-    long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const long long p0 = clock64();
-#endif
+    auto store_slot = [&](int st, const float (&vals)[8 * kTdSub]) {
+      uint32_t v[32];  // slot columns: per sub-step u, hi at 16u .. 16u+7, lo at 16u+8 ..
+#pragma unroll
+      for (int u = 0; u < kTdSub; ++u)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) tc::split_tf32(vals[8 * u + e], v[16 * u + e], v[16 * u + 8 + e]);
+      tc::fence_after_sync();
+      tc::tmem_st32(tbase + lane_off + kAcol + 32 * st, v);
+      tc::tmem_st_wait();
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&sh.full[st]);
+    };
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int64_t rt = t % m_tiles, tb = t / m_tiles;
-      const int nsteps = (tcn[tb] + 7) >> 3;
+      const int32_t total = tcn[tb];
+      const int nsteps = (total + 7) >> 3;
       const int nstage = (nsteps + kTdSub - 1) / kTdSub;
-      const float* acol = AT + rt * kpad * 128 + r;
-      const int4* kx4 = reinterpret_cast<const int4*>(tck + tb * maxsteps * 8);
-      const int npos = nsteps * 8, nb = (nstage + kB - 1) / kB;
-      auto load_k = [&](int b, int (&k)[KB]) {
+      if (td_dense(total, kpad)) {
+        for (int j = 0; j < nstage; ++j, ++J) {
+          const int st = J % kTdStages;
+          const int nvalid = min(8 * kTdSub, total - 8 * kTdSub * j);
+          tc::mbar_wait(&sh.tma[st], (J / kTdStages) & 1u);  // implies the slot's MMAs are done
+          float vals[8 * kTdSub];
 #pragma unroll
-        for (int q = 0; q < KB / 4; ++q) {
-          const int4 v = (b * KB + 4 * q < npos) ? __ldg(kx4 + b * (KB / 4) + q) : make_int4(-1, -1, -1, -1);
-          k[4 * q] = v.x;
-          k[4 * q + 1] = v.y;
-          k[4 * q + 2] = v.z;
-          k[4 * q + 3] = v.w;
+          for (int q = 0; q < 8 * kTdSub; ++q) vals[q] = q < nvalid ? sh.a[st][q][r] : 0.0f;
+          store_slot(st, vals);
         }
-      };
-      auto load_a = [&](const int (&k)[KB], float (&a)[KB]) {
+      } else {
+        constexpr int kB = 2, KB = 8 * kTdSub * kB;  // stages per batch, k per batch
+        const float* acol = AT + rt * kpad * 128 + r;
+        const int4* kx4 = reinterpret_cast<const int4*>(tck + tb * maxsteps * 8);
+        const int npos = nsteps * 8, nb = (nstage + kB - 1) / kB;
+        auto load_k = [&](int b, int (&k)[KB]) {
 #pragma unroll
-        for (int i = 0; i < KB; ++i) a[i] = k[i] >= 0 ? __ldg(acol + (int64_t)k[i] * 128) : 0.0f;
-      };
-      int kn[KB];
-      float ac[KB], an[KB];
-      load_k(0, kn);
-      load_a(kn, ac);
-      load_k(1, kn);
-#pragma unroll 1
-      for (int b = 0; b < nb; ++b) {
-        load_a(kn, an);  // batch b + 1 (all -1 past the end: no loads)
-        load_k(b + 2, kn);
-#pragma unroll
-        for (int i = 0; i < kB; ++i) {
-          const int j = kB * b + i;
-          if (j < nstage) {
-            const uint32_t Jj = J + j;
-            const int sa = Jj % kTdStages;
-            TD_CLK(c0);
-            tc::mbar_wait(&sh.empty[sa], ((Jj / kTdStages) & 1u) ^ 1u);
-            TD_CLK(c1);
-            TD_ADD(0, c1 - c0);
-            tc::fence_after_sync();
-#pragma unroll
-            for (int u = 0; u < kTdSub; ++u) {
-              uint32_t hi[8], lo[8];
-#pragma unroll
-              for (int e = 0; e < 8; ++e) tc::split_tf32(ac[16 * i + 8 * u + e], hi[e], lo[e]);
-              tc::tmem_st8(tbase + lane_off + kAcol + 32 * sa + 16 * u, hi);
-              tc::tmem_st8(tbase + lane_off + kAcol + 32 * sa + 16 * u + 8, lo);
-            }
-            tc::tmem_st_wait();
-            tc::fence_before_sync();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&sh.full[sa]);
+          for (int q = 0; q < KB / 4; ++q) {
+            const int4 v = (b * KB + 4 * q < npos) ? __ldg(kx4 + b * (KB / 4) + q) : make_int4(-1, -1, -1, -1);
+            k[4 * q] = v.x;
+            k[4 * q + 1] = v.y;
+            k[4 * q + 2] = v.z;
+            k[4 * q + 3] = v.w;
           }
-        }
+        };
+        auto load_a = [&](const int (&k)[KB], float (&a)[KB]) {
 #pragma unroll
-        for (int e = 0; e < KB; ++e) ac[e] = an[e];
+          for (int i = 0; i < KB; ++i) a[i] = k[i] >= 0 ? __ldg(acol + (int64_t)k[i] * 128) : 0.0f;
+        };
+        int kn[KB];
+        float ac[KB], an[KB];
+        load_k(0, kn);
+        load_a(kn, ac);
+        load_k(1, kn);
+#pragma unroll 1
+        for (int b = 0; b < nb; ++b) {
+          load_a(kn, an);  // batch b + 1 (all -1 past the end: no loads)
+          load_k(b + 2, kn);
+#pragma unroll
+          for (int i = 0; i < kB; ++i) {
+            const int j = kB * b + i;
+            if (j < nstage) {
+              const uint32_t Jj = J + j;
+              const int st = Jj % kTdStages;
+              tc::mbar_wait(&sh.empty[st], ((Jj / kTdStages) & 1u) ^ 1u);
+              float vals[8 * kTdSub];
+#pragma unroll
+              for (int q = 0; q < 8 * kTdSub; ++q) vals[q] = ac[8 * kTdSub * i + q];
+              store_slot(st, vals);
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < KB; ++e) ac[e] = an[e];
+        }
+        J += nstage;
       }
-      J += nstage;
     }
-#ifdef TD_PROF
-    if (tid == 0 && td_prof) {
-      unsigned long long* q = td_prof + 16 * blockIdx.x;
-      q[4] = prof[0]; q[5] = 0; q[6] = clock64() - p0;
-    }
-#endif
   } else {
     // ------------------------------------------------------ accumulator warps 4..11
     // Warp w: tile row 32*(w%4) + lane (its TMEM lane), columns 96*((w-4)/4) .. +95, held

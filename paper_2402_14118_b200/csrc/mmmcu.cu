@@ -516,6 +516,11 @@ mmmcu_status fill_counters(mmmcu_ctx* ctx, mmmcu_counters* out) {
   const bool a_ok = ctx->has_a, b_ok = ctx->has_b;
   const bool same_k = a_ok && b_ok && ctx->Ka == ctx->Kb;
   const int64_t K = b_ok ? ctx->Kb : ctx->Ka;
+  if (b_ok) {
+    mmmcu::k1_bcounts<<<(unsigned)((ctx->Kb + 255) / 256), 256, 0, ctx->stream>>>(
+        ctx->bgrp.as<uint32_t>(), ctx->Kb, ctx->ldb / 64, (ctx->Kb + 31) / 32, zb_bpop(ctx), zb_bnz(ctx));
+    MMMCU_LAUNCHED();
+  }
   mmmcu::k1_counters<<<1, 1024, 0, ctx->stream>>>(a_ok ? za_acol(ctx) : nullptr, b_ok ? zb_bpop(ctx) : nullptr,
                                                   b_ok ? zb_bnz(ctx) : nullptr, K, ctx->M, ctx->ldb / 64,
                                                   (a_ok && (same_k || !b_ok)) ? 1 : 0, (b_ok && (same_k || !a_ok)) ? 1 : 0,
