@@ -17,7 +17,7 @@
 // Accuracy: the tensor core's fp32 accumulation truncates at every MMA, an error that grows
 // with the number of MMAs into one accumulator (measured worst 6.7e-6 * Σ|a||b| with 512
 // steps into one D at 4096^3, against the 1e-5 tolerance; 0.9e-6 with 64-step segments,
-// 0.7e-6 with 32).  So the k loop is cut into 256-k segments accumulated in two
+// 0.7e-6 with 32).  So the k loop is cut into 512-k segments accumulated in two
 // alternating TMEM accumulators D0 / D1: while the MMAs fill one, the 8 accumulator warps
 // add the other into fp32 registers (round-to-nearest adds), so the tensor pipe never waits
 // for a drain.  At the end C = C0 + P, staged through shared memory and coalesced.
@@ -44,12 +44,12 @@ __device__ unsigned long long* td_prof = nullptr;  // debug builds only: per-CTA
 #endif
 
 #ifndef TD_SEG
-#define TD_SEG 16
+#define TD_SEG 32
 #endif
 constexpr int kTdStages = 4;    // stages of kTdSub MMA sub-steps (16 k): B smem + A TMEM slot
 constexpr int kTdSub = 2;       // MMA sub-steps (8 k, 3 MMAs) per stage
 constexpr int kTdThreads = 448; // warps 0-3 transform, 4-11 accumulators, 12 producer, 13 MMA
-constexpr int kTdSeg = TD_SEG;  // stages (256 k) per TMEM accumulation segment
+constexpr int kTdSeg = TD_SEG;  // stages (512 k) per TMEM accumulation segment (worst 1.0e-6)
 constexpr int kTdTM = 128;
 constexpr int kTdTN = 192;
 constexpr int kTdStepFloats = kTdTN * 8 * 2;  // one 8-k step image (K1): hi | lo, 12 KB
