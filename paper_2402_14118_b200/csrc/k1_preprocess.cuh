@@ -50,10 +50,11 @@ struct K1Scratch {
   uint32_t* arow;
   uint32_t* acol;
   uint32_t* tile_sum;     // [ceil(M/32)] non-zeros per 32-row tile (zeroed)
+  uint32_t* nonfinite_a;  // set iff A holds an Inf / NaN (zeroed): AUTO then keeps K2-SIMT
   int64_t* tile_prefix;   // [ceil(M/32) + 1] exclusive prefix of tile_sum (written by the last CTA)
   uint32_t* bpop;
   uint32_t* bnz;
-  unsigned long long* btot;  // B totals: {Σ non-zero (k, slice), Σ bpop, Σ bnz} (zeroed)
+  unsigned long long* btot;  // B totals: {Σ non-zero (k, slice), Σ bpop, Σ bnz, Inf/NaN seen} (zeroed)
   unsigned int* done;
   // K2-TC operands (nullptr when the TC path is not prepared)
   float* at;              // A^T per 128-row tile: at[(rt * kpad + k) * 128 + (i % 128)], zero padded
@@ -123,7 +124,10 @@ __device__ void k1_choose_path(const K1Scratch& z, int64_t M, int64_t kw, unsign
     const double tc = rt * (24200.0 * (double)z.n_tc + 784.0 * (double)stages) + 0.0433 * 3.0 * 768.0 * (double)lv;
     // time ~ work / min(SMs, CTAs): short operands leave SMs idle
     const double par_simt = fmin(148.0, rt * (double)z.n_tb), par_tc = fmin(148.0, rt * (double)z.n_tc);
-    if (tc / par_tc < simt / par_simt) out[7] = 32ull;
+    // K2-TC multiplies A's zeros and splits values into hi / lo: an Inf or NaN operand
+    // would turn 0 * Inf terms the reference never forms into NaN — keep the exact path
+    const bool nonfinite = *z.nonfinite_a != 0u || z.btot[3] != 0ull;
+    if (!nonfinite && tc / par_tc < simt / par_simt) out[7] = 32ull;
   }
   __syncthreads();
 }
@@ -345,6 +349,7 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
   }
   uint32_t ccount[4] = {0, 0, 0, 0};
   uint32_t warp_total = 0;
+  bool nonfin = false;
   __shared__ uint32_t s_ab[kK1Rows][32];  // the tile's bitmap words (row, chunk)
   const int64_t rend = min(r0 + kK1Rows, M);
   const int64_t rend_at = z.at ? min(r0 + kK1Rows, z.m_at) : rend;
@@ -365,8 +370,16 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
       for (int j = 0; j < 4; ++j)
         if (col[j] < z.kpad) {
           float4* d4 = reinterpret_cast<float4*>(z.at + (rt * z.kpad + col[j]) * 128 + (rb & 127));
+#ifdef K1_STCS
+          __stcs(d4, make_float4(x[0][j], x[1][j], x[2][j], x[3][j]));
+          __stcs(d4 + 1, make_float4(x[4][j], x[5][j], x[6][j], x[7][j]));
+#elif defined(K1_STWT)
+          __stwt(d4, make_float4(x[0][j], x[1][j], x[2][j], x[3][j]));
+          __stwt(d4 + 1, make_float4(x[4][j], x[5][j], x[6][j], x[7][j]));
+#else
           d4[0] = make_float4(x[0][j], x[1][j], x[2][j], x[3][j]);
           d4[1] = make_float4(x[4][j], x[5][j], x[6][j], x[7][j]);
+#endif
         }
     }
     if (rb >= rend) continue;
@@ -378,6 +391,7 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const bool nz = x[u][j] != 0.0f;
+        nonfin |= !isfinite(x[u][j]);
         const uint32_t m = __ballot_sync(0xffffffffu, nz);
         ccount[j] += nz ? 1u : 0u;
         cnt += __popc(m);
@@ -390,6 +404,7 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
     }
   }
   if (lane == 0 && warp_total) atomicAdd(&z.tile_sum[ty], warp_total);
+  if (__any_sync(0xffffffffu, nonfin) && lane == 0) atomicOr(z.nonfinite_a, 1u);
 #pragma unroll
   for (int j = 0; j < 4; ++j)
     if (ok[j] && ccount[j]) atomicAdd(&z.acol[col[j]], ccount[j]);
@@ -426,6 +441,7 @@ __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, 
   const int64_t gcol = c0 + 32 * k1_chunk(w, gj) + 8 * gs;
   const bool gown = lane < 16 && gcol < ldb;
   uint32_t gword = 0;
+  bool nonfin = false;
   const int64_t kend = min(k0 + 32, K);
   for (int64_t kb = k0; kb < kend; kb += 8) {
     float x[8][4];
@@ -437,7 +453,10 @@ __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, 
     for (int u = 0; u < 8; ++u) {
       uint32_t m[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) m[j] = __ballot_sync(0xffffffffu, x[u][j] != 0.0f);
+      for (int j = 0; j < 4; ++j) {
+        m[j] = __ballot_sync(0xffffffffu, x[u][j] != 0.0f);
+        nonfin |= !isfinite(x[u][j]);
+      }
       const uint32_t mg = gj == 0 ? m[0] : gj == 1 ? m[1] : gj == 2 ? m[2] : m[3];
       gword |= (uint32_t)(((mg >> (8 * gs)) & 0xFFu) != 0) << (uint32_t)(kb - k0 + u);
     }
@@ -458,6 +477,7 @@ __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, 
     pop_w += __shfl_xor_sync(0xffffffffu, pop_w, o);
     nz_w += __shfl_xor_sync(0xffffffffu, nz_w, o);
   }
+  if (__any_sync(0xffffffffu, nonfin) && lane == 0) atomicOr(&z.btot[3], 1ull);
   if (lane == 0 && pop_w) atomicAdd(&z.btot[1], (unsigned long long)pop_w);
   if (lane == 0 && nz_w) atomicAdd(&z.btot[2], (unsigned long long)nz_w);
   // (k, 16-column slice) pairs with a non-zero: even group lanes own slice (2s, 2s+1)
@@ -816,9 +836,12 @@ __device__ __forceinline__ void k1_pack_tc_cta(const PackTcArgs& g, int64_t bx, 
     }
     uint32_t h[4], l[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      h[i] = __float_as_uint(v[i]) & 0xFFFFE000u;
-      l[i] = __float_as_uint(v[i] - __uint_as_float(h[i]));
+    for (int i = 0; i < 4; ++i) {  // tc::split_tf32 semantics (Inf / NaN: hi = v, lo = 0)
+      const uint32_t b = __float_as_uint(v[i]);
+      const bool special = (b & 0x7F800000u) == 0x7F800000u;
+      const bool nan = special && (b & 0x007FFFFFu) != 0u;
+      h[i] = nan ? 0x7FC00000u : special ? b : (b & 0xFFFFE000u);
+      l[i] = special ? 0u : __float_as_uint(v[i] - __uint_as_float(h[i]));
     }
     float* img = tcb + (tb * maxsteps + s) * (kTcTileN * 16);
     const int off = (n & 7) * 4 + (n >> 3) * 64 + q * 32;  // in floats

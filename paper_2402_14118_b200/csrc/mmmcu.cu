@@ -150,7 +150,9 @@ uint32_t* za_acol(mmmcu_ctx* ctx) { return ctx->za.as<uint32_t>() + ctx->M; }
 uint32_t* za_tiles(mmmcu_ctx* ctx) { return ctx->za.as<uint32_t>() + ctx->M + ctx->Ka; }
 int64_t n_row_tiles(int64_t M) { return (M + mmmcu::kK1Rows - 1) / mmmcu::kK1Rows; }
 unsigned long long* zb_slice(mmmcu_ctx* ctx) { return ctx->zb.as<unsigned long long>(); }
-uint32_t* zb_bpop(mmmcu_ctx* ctx) { return reinterpret_cast<uint32_t*>(ctx->zb.as<unsigned long long>() + 3); }
+uint32_t* zb_bpop(mmmcu_ctx* ctx) { return reinterpret_cast<uint32_t*>(ctx->zb.as<unsigned long long>() + 4); }
+// one word after the A scratch: set iff A holds an Inf / NaN (zeroed with za)
+uint32_t* za_nonfinite(mmmcu_ctx* ctx) { return za_tiles(ctx) + n_row_tiles(ctx->M); }
 uint32_t* zb_bnz(mmmcu_ctx* ctx) { return zb_bpop(ctx) + ctx->Kb; }
 // Operand sets K1 emits for K2: A^T tiles (SIMT v2, TC), raw B rows (SIMT v2), tf32 B step
 // images + live-k lists (TC).
@@ -176,11 +178,11 @@ mmmcu_status stage_a(mmmcu_ctx* ctx, const float* A, int64_t M, int64_t K, int64
   ctx->has_a = false;
   ctx->csr_idx_bytes = K <= 65536 ? 2 : 4;
   MMMCU_CUDA(ctx->abits.ensure(sizeof(uint32_t) * M * kw));
-  MMMCU_CUDA(ctx->za.ensure(sizeof(uint32_t) * (M + K + n_row_tiles(M))));
+  MMMCU_CUDA(ctx->za.ensure(sizeof(uint32_t) * (M + K + n_row_tiles(M) + 1)));
   MMMCU_CUDA(ctx->tile_prefix.ensure(sizeof(int64_t) * (n_row_tiles(M) + 1)));
   MMMCU_CUDA(ctx->row_ptr.ensure(sizeof(int64_t) * (M + 1)));
   MMMCU_CUDA(ctx->cols.ensure((size_t)ctx->csr_idx_bytes * M * K));
-  MMMCU_CUDA(cudaMemsetAsync(ctx->za.p, 0, sizeof(uint32_t) * (M + K + n_row_tiles(M)), ctx->stream));
+  MMMCU_CUDA(cudaMemsetAsync(ctx->za.p, 0, sizeof(uint32_t) * (M + K + n_row_tiles(M) + 1), ctx->stream));
   ctx->op_at = false;
   if (ops_for(ctx) & OP_AT) {
     ctx->kpad = round_up(K, 32);
@@ -214,7 +216,7 @@ mmmcu_status stage_b(mmmcu_ctx* ctx, const float* B, int64_t K, int64_t N, int64
   const int64_t n_cnt = n_tb * kw;
   const int64_t n_tc = (ldb + mmmcu::kTcTileN - 1) / mmmcu::kTcTileN;
   const int64_t n_extra = ((ops & OP_TCB) ? n_tc * kw : 0) + ((ops & OP_ROWS) ? n_cnt : 0);
-  const size_t zb_bytes = 3 * sizeof(unsigned long long) + sizeof(uint32_t) * (2 * K + n_extra);
+  const size_t zb_bytes = 4 * sizeof(unsigned long long) + sizeof(uint32_t) * (2 * K + n_extra);
   MMMCU_CUDA(ctx->zb.ensure(zb_bytes));
   MMMCU_CUDA(cudaMemsetAsync(ctx->zb.p, 0, zb_bytes, ctx->stream));
   ctx->n_tb = n_tb;
@@ -312,6 +314,7 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   z.arow = a_valid ? za_arow(ctx) : nullptr;
   z.acol = a_valid ? za_acol(ctx) : nullptr;
   z.tile_sum = do_a ? za_tiles(ctx) : nullptr;
+  z.nonfinite_a = a_valid ? za_nonfinite(ctx) : nullptr;
   z.tile_prefix = do_a ? ctx->tile_prefix.as<int64_t>() : nullptr;
   z.bpop = b_valid ? zb_bpop(ctx) : nullptr;
   z.bnz = b_valid ? zb_bnz(ctx) : nullptr;

@@ -412,3 +412,22 @@ def test_cpp_dropin(ctx):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "DROPIN OK" in out.stdout
+
+
+def test_nonfinite_operands_stay_exact(ctx):
+    # Inf / NaN are non-zero (matrix.hpp:152/174) and propagate through the reference's fmaf
+    # chain; K2-TC would form 0 * Inf terms the reference never forms, so K1 flags
+    # non-finite operands and AUTO keeps the exact K2-SIMT path
+    A, B = gen_pair(17, 512, 512, 512, 0.6, 0.6, 8)
+    A[3, 5] = np.inf
+    A[10, 20] = -np.inf
+    B[7, 9] = np.nan
+    B[30, 100] = np.inf
+    Cr, ocnt = run_oracle(A, B)
+    C, cnt = run_gpu(ctx, A, B, algo=N.ALGO_AUTO)
+    assert ctx.last_algo() in (N.ALGO_SIMT_SPAN8, N.ALGO_SIMT_SPAN16)
+    assert (np.isnan(C) == np.isnan(Cr)).all()
+    fin = ~np.isnan(Cr)
+    assert bitexact(C[fin], Cr[fin])
+    assert np.isinf(Cr).any() and np.isnan(Cr).any()
+    assert_counters(cnt, ocnt)
