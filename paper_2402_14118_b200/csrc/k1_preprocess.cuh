@@ -50,11 +50,11 @@ struct K1Scratch {
   uint32_t* arow;
   uint32_t* acol;
   uint32_t* tile_sum;     // [ceil(M/32)] non-zeros per 32-row tile (zeroed)
-  uint32_t* nonfinite_a;  // set iff A holds an Inf / NaN (zeroed): AUTO then keeps K2-SIMT
+  uint32_t* nonfinite_a;  // set iff A holds an Inf / NaN / subnormal (zeroed): AUTO keeps K2-SIMT
   int64_t* tile_prefix;   // [ceil(M/32) + 1] exclusive prefix of tile_sum (written by the last CTA)
   uint32_t* bpop;
   uint32_t* bnz;
-  unsigned long long* btot;  // B totals: {Σ non-zero (k, slice), Σ bpop, Σ bnz, Inf/NaN seen} (zeroed)
+  unsigned long long* btot;  // B totals: {Σ non-zero (k, slice), Σ bpop, Σ bnz, Inf/NaN/subnormal seen} (zeroed)
   unsigned int* done;
   // K2-TC operands (nullptr when the TC path is not prepared)
   float* at;              // A^T per 128-row tile: at[(rt * kpad + k) * 128 + (i % 128)], zero padded
@@ -124,8 +124,9 @@ __device__ void k1_choose_path(const K1Scratch& z, int64_t M, int64_t kw, unsign
     const double tc = rt * (24200.0 * (double)z.n_tc + 784.0 * (double)stages) + 0.0433 * 3.0 * 768.0 * (double)lv;
     // time ~ work / min(SMs, CTAs): short operands leave SMs idle
     const double par_simt = fmin(148.0, rt * (double)z.n_tb), par_tc = fmin(148.0, rt * (double)z.n_tc);
-    // K2-TC multiplies A's zeros and splits values into hi / lo: an Inf or NaN operand
-    // would turn 0 * Inf terms the reference never forms into NaN — keep the exact path
+    // K2-TC multiplies A's zeros and reads tf32: an Inf / NaN operand would turn 0 * Inf
+    // terms the reference never forms into NaN, subnormals would be flushed — keep the
+    // exact path
     const bool nonfinite = *z.nonfinite_a != 0u || z.btot[3] != 0ull;
     if (!nonfinite && tc / par_tc < simt / par_simt) out[7] = 32ull;
   }
@@ -333,6 +334,13 @@ struct K1RingLoader {
 // from warp-uniform ballots instead of per-lane shuffle chains.
 __device__ __forceinline__ int k1_chunk(int w, int j) { return 2 * w + (j & 1) + 16 * (j >> 1); }
 
+// Values K2-TC cannot reproduce within the tolerance: Inf / NaN (0 * Inf terms) and
+// subnormals (tf32 operands are flushed).  K1 flags them and AUTO keeps K2-SIMT.
+__device__ __forceinline__ bool k1_tc_unsafe(float v) {
+  const uint32_t e = __float_as_uint(v) & 0x7F800000u;
+  return e == 0x7F800000u || (e == 0u && (__float_as_uint(v) & 0x007FFFFFu) != 0u);
+}
+
 template <typename Loader>
 __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, uint32_t* __restrict__ abits, int64_t kw,
                                             const K1Scratch& z, int64_t tx, int64_t ty) {
@@ -391,7 +399,7 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const bool nz = x[u][j] != 0.0f;
-        nonfin |= !isfinite(x[u][j]);
+        nonfin |= k1_tc_unsafe(x[u][j]);
         const uint32_t m = __ballot_sync(0xffffffffu, nz);
         ccount[j] += nz ? 1u : 0u;
         cnt += __popc(m);
@@ -455,7 +463,7 @@ __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, 
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         m[j] = __ballot_sync(0xffffffffu, x[u][j] != 0.0f);
-        nonfin |= !isfinite(x[u][j]);
+        nonfin |= k1_tc_unsafe(x[u][j]);
       }
       const uint32_t mg = gj == 0 ? m[0] : gj == 1 ? m[1] : gj == 2 ? m[2] : m[3];
       gword |= (uint32_t)(((mg >> (8 * gs)) & 0xFFu) != 0) << (uint32_t)(kb - k0 + u);

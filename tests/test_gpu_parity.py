@@ -431,3 +431,15 @@ def test_nonfinite_operands_stay_exact(ctx):
     assert bitexact(C[fin], Cr[fin])
     assert np.isinf(Cr).any() and np.isnan(Cr).any()
     assert_counters(cnt, ocnt)
+
+
+def test_subnormal_operands_stay_exact(ctx):
+    # subnormals are non-zero (matrix.hpp:174); tf32 tensor-core operands would flush them,
+    # so AUTO keeps K2-SIMT (bit-exact) when K1 sees one
+    A, B = gen_pair(18, 256, 256, 256, 0.6, 0.6, 8)
+    A[:, 7] = np.float32(1e-40)  # a whole column of subnormals
+    Cr, ocnt = run_oracle(A, B)
+    C, cnt = run_gpu(ctx, A, B, algo=N.ALGO_AUTO)
+    assert ctx.last_algo() in (N.ALGO_SIMT_SPAN8, N.ALGO_SIMT_SPAN16)
+    assert bitexact(C, Cr)
+    assert_counters(cnt, ocnt)
