@@ -56,6 +56,7 @@ struct K1Scratch {
   uint32_t* bnz;
   unsigned long long* btot;  // B totals: {Σ non-zero (k, slice), Σ bpop, Σ bnz, Inf/NaN/subnormal seen} (zeroed)
   unsigned int* done;
+  unsigned int* next_tile;  // K1 tile counter (dynamic scheduling; reset by the last CTA)
   // K2-TC operands (nullptr when the TC path is not prepared)
   float* at;              // A^T per 128-row tile: at[(rt * kpad + k) * 128 + (i % 128)], zero padded
   int64_t kpad;           // K rounded up to 32
@@ -183,7 +184,14 @@ __global__ void __launch_bounds__(kK1Threads) k1_row_off(const uint32_t* __restr
 // thread 0 refills a stage as soon as the 8 warps have read it into registers.  The last
 // CTA to finish (threadfence + done-counter) computes the exact counters, plan statistics
 // and the AUTO path choice.
-constexpr int kK1Stages = 2;
+#ifndef K1_STAGES
+#define K1_STAGES 2
+#endif
+#ifndef K1_CTAS
+#define K1_CTAS 3
+#endif
+constexpr int kK1Stages = K1_STAGES;
+constexpr int kK1CtasPerSm = K1_CTAS;
 #ifdef K1_PROF
 __device__ unsigned long long* k1_prof = nullptr;  // debug builds: per-CTA globaltimer stamps
 __device__ __forceinline__ unsigned long long k1_now() {
@@ -197,6 +205,7 @@ struct K1Ring {
   float4 buf[kK1Stages][8][kK1Threads];  // 8 rows x 1024 columns per stage (32 KB)
   uint64_t full[kK1Stages];
   uint64_t empty[kK1Stages];
+  int64_t tile[kK1Stages];               // the tile this stage's group belongs to (-1: no more)
 };
 
 __device__ __forceinline__ void k1_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -228,12 +237,29 @@ struct K1Args {
 };
 
 // Row groups in consumption order: the tiles of this CTA, each tile's 8-row groups.
+// Tiles are handed out dynamically (atomic counter): the producer takes the next tile when
+// it starts issuing its groups and tags every stage with the tile, so the compute warps
+// follow the same sequence; a CTA that runs fast takes more tiles (no static tail).
 struct K1Cursor {
   const K1Args* g;
   const K1Scratch* z;
   int64_t t, rb, rend, c0;  // current tile, its next group's first row, row end, first column
   const float* base;
   int64_t ld, cols;         // row stride, readable columns of the operand
+  int64_t n_static = 0;     // this CTA's statically assigned tiles taken so far
+  // ~7/8 of the tiles are dealt statically (CTA b: b, b + grid, ...), the rest handed out
+  // through an atomic counter to whichever CTA is free first: balance without a
+  // contended counter on every tile
+  __device__ int64_t grab() {
+    const int64_t total = g->nA + g->nB;
+    const int64_t per = (total * 7 / 8) / gridDim.x;  // static tiles per CTA
+    if (n_static < per) return blockIdx.x + (n_static++) * (int64_t)gridDim.x;
+    return per * (int64_t)gridDim.x + (int64_t)atomicAdd(z->next_tile, 1u);
+  }
+  __device__ void next_tile() {
+    t = grab();
+    tile_setup();
+  }
   __device__ void tile_setup() {
     const K1Args& a = *g;
     while (t < a.nA + a.nB) {
@@ -258,7 +284,7 @@ struct K1Cursor {
         cols = a.ldb;
         if (rb < rend) return;
       }
-      t += gridDim.x;
+      t = grab();
     }
   }
   __device__ bool done() const { return t >= g->nA + g->nB; }
@@ -268,13 +294,16 @@ struct K1Cursor {
     const int64_t lim = t < a.nA ? a.M : rend;  // A rows past M are zeros: not read
     const int64_t rows_valid = lim - rb >= 8 ? 8 : (lim - rb > 0 ? lim - rb : 0);
     const uint32_t bytes = (uint32_t)((cols - c0 >= kK1Cols ? kK1Cols : cols - c0) * 4);
+    r.tile[s] = t;
     mbar_expect(&r.full[s], (uint32_t)rows_valid * bytes);
     for (int u = 0; u < rows_valid; ++u) k1_bulk(&r.buf[s][u][0], base + (rb + u) * ld + c0, bytes, &r.full[s]);
     rb += 8;
-    if (rb >= rend) {
-      t += gridDim.x;
-      tile_setup();
-    }
+    if (rb >= rend) next_tile();
+  }
+  // no more tiles: one stage tagged -1 tells the compute warps to stop
+  __device__ void finish(K1Ring& r, int s) {
+    r.tile[s] = -1;
+    mbar_expect(&r.full[s], 0u);
   }
   __device__ static void mbar_expect(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
@@ -289,6 +318,12 @@ struct K1RingLoader {
   K1Ring& r;
   K1Cursor& cur;
   uint32_t J;  // groups consumed
+  // the tile of the next group (-1: done); waits for the stage to land
+  __device__ int64_t peek() {
+    const int s = J % kK1Stages;
+    k1_wait(&r.full[s], (J / kK1Stages) & 1u);
+    return r.tile[s];
+  }
   __device__ void rows8(float4 (&v)[8], const float*, int64_t, bool col_ok, int nvalid) {
     const int s = J % kK1Stages;
     k1_wait(&r.full[s], (J / kK1Stages) & 1u);
@@ -337,8 +372,8 @@ __device__ __forceinline__ int k1_chunk(int w, int j) { return 2 * w + (j & 1) +
 // Values K2-TC cannot reproduce within the tolerance: Inf / NaN (0 * Inf terms) and
 // subnormals (tf32 operands are flushed).  K1 flags them and AUTO keeps K2-SIMT.
 __device__ __forceinline__ bool k1_tc_unsafe(float v) {
-  const uint32_t e = __float_as_uint(v) & 0x7F800000u;
-  return e == 0x7F800000u || (e == 0u && (__float_as_uint(v) & 0x007FFFFFu) != 0u);
+  const uint32_t a = __float_as_uint(v) & 0x7FFFFFFFu;  // |v|: subnormal in [1, 0x7FFFFF], Inf/NaN >= 0x7F800000
+  return (a - 1u < 0x007FFFFFu) | (a >= 0x7F800000u);   // branch-free (bitwise |)
 }
 
 template <typename Loader>
@@ -448,6 +483,10 @@ __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, 
   const int gj = (lane >> 2) & 3, gs = lane & 3;
   const int64_t gcol = c0 + 32 * k1_chunk(w, gj) + 8 * gs;
   const bool gown = lane < 16 && gcol < ldb;
+  uint32_t sel[4];  // lane's chunk as an all-ones mask (uniform chunk masks, per-lane selection)
+#pragma unroll
+  for (int j = 0; j < 4; ++j) sel[j] = gj == j ? 0xFFFFFFFFu : 0u;
+  const uint32_t gmask = 0xFFu << (8 * gs);
   uint32_t gword = 0;
   bool nonfin = false;
   const int64_t kend = min(k0 + 32, K);
@@ -465,8 +504,8 @@ __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, 
         m[j] = __ballot_sync(0xffffffffu, x[u][j] != 0.0f);
         nonfin |= k1_tc_unsafe(x[u][j]);
       }
-      const uint32_t mg = gj == 0 ? m[0] : gj == 1 ? m[1] : gj == 2 ? m[2] : m[3];
-      gword |= (uint32_t)(((mg >> (8 * gs)) & 0xFFu) != 0) << (uint32_t)(kb - k0 + u);
+      const uint32_t mg = (m[0] & sel[0]) | (m[1] & sel[1]) | (m[2] & sel[2]) | (m[3] & sel[3]);  // branch-free
+      gword |= (uint32_t)((mg & gmask) != 0) << (uint32_t)(kb - k0 + u);
     }
   }
   if (!gown) gword = 0;
@@ -511,7 +550,7 @@ __global__ void k1_codes_export(const uint32_t* __restrict__ bgrp, int64_t K, in
   codes[t] = (uint8_t)code;
 }
 
-__global__ void __launch_bounds__(kK1Block, 3)
+__global__ void __launch_bounds__(kK1Block, kK1CtasPerSm)
 k1_pass(K1Args g, K1Scratch z, int has_a, int has_b, unsigned long long* __restrict__ stats) {
 #ifdef K1_PROF
   const unsigned long long t_start = k1_now();
@@ -535,16 +574,22 @@ k1_pass(K1Args g, K1Scratch z, int has_a, int has_b, unsigned long long* __restr
   if (threadIdx.x >= kK1Threads) {
     // TMA producer warp: refill a stage as soon as the 8 compute warps have read it
     if (threadIdx.x == kK1Threads) {
-      cur.tile_setup();
-      for (uint32_t J = 0; !cur.done(); ++J) {
+      cur.next_tile();
+      uint32_t J = 0;
+      for (; !cur.done(); ++J) {
         const int s = J % kK1Stages;
         k1_wait(&r.empty[s], ((J / kK1Stages) & 1u) ^ 1u);
         cur.issue(r, s);
       }
+      const int s = J % kK1Stages;
+      k1_wait(&r.empty[s], ((J / kK1Stages) & 1u) ^ 1u);
+      cur.finish(r, s);
     }
   } else {
     K1RingLoader ld{r, cur, 0u};
-    for (int64_t t = blockIdx.x; t < nA + nB; t += gridDim.x) {
+    for (;;) {
+      const int64_t t = ld.peek();
+      if (t < 0) break;
       if (t < nA)
         k1_a_tile_b(ld, M, K, g.abits, kw, z, t % g.a_tx, t / g.a_tx);
       else
@@ -566,7 +611,10 @@ k1_pass(K1Args g, K1Scratch z, int has_a, int has_b, unsigned long long* __restr
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (threadIdx.x == 0) *z.done = 0u;  // ready for the next launch (no other CTA is left)
+  if (threadIdx.x == 0) {  // ready for the next launch (no other CTA is left)
+    *z.done = 0u;
+    *z.next_tile = 0u;
+  }
   k1_plan_totals(z.btot, K, nreg, has_b, stats);
   if (z.choose && has_a && has_b) k1_choose_path(z, M, kw, stats);
   // the K2-SIMT record offsets only when K2-SIMT can run (its pack is gated out otherwise)
@@ -844,12 +892,9 @@ __device__ __forceinline__ void k1_pack_tc_cta(const PackTcArgs& g, int64_t bx, 
     }
     uint32_t h[4], l[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {  // tc::split_tf32 semantics (Inf / NaN: hi = v, lo = 0)
-      const uint32_t b = __float_as_uint(v[i]);
-      const bool special = (b & 0x7F800000u) == 0x7F800000u;
-      const bool nan = special && (b & 0x007FFFFFu) != 0u;
-      h[i] = nan ? 0x7FC00000u : special ? b : (b & 0xFFFFE000u);
-      l[i] = special ? 0u : __float_as_uint(v[i] - __uint_as_float(h[i]));
+    for (int i = 0; i < 4; ++i) {  // tc::split_tf32
+      h[i] = __float_as_uint(v[i]) & 0xFFFFE000u;
+      l[i] = __float_as_uint(v[i] - __uint_as_float(h[i]));
     }
     float* img = tcb + (tb * maxsteps + s) * (kTcTileN * 16);
     const int off = (n & 7) * 4 + (n >> 3) * 64 + q * 32;  // in floats

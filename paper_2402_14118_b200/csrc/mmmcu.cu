@@ -320,6 +320,7 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   z.bnz = b_valid ? zb_bnz(ctx) : nullptr;
   z.btot = b_valid ? zb_slice(ctx) : ctx->stats.as<unsigned long long>() + 12;
   z.done = ctx->ctl.as<unsigned int>();
+  z.next_tile = ctx->ctl.as<unsigned int>() + 1;
   z.at = tc_a ? ctx->at.as<float>() : nullptr;
   z.kpad = ctx->kpad;
   z.m_at = ctx->m_at;
@@ -336,10 +337,23 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
                         ctx->B, ctx->ldb, ctx->ldb / 64, ctx->bgrp.as<uint32_t>(), b_tx, nB, kw};
   const int k1_smem = (int)sizeof(mmmcu::K1Ring) + 128;
   MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k1_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, k1_smem));
-  const unsigned k1_grid = (unsigned)std::min<int64_t>(nA + nB, 3 * (int64_t)ctx->num_sms);
+  const unsigned k1_grid = (unsigned)std::min<int64_t>(nA + nB, mmmcu::kK1CtasPerSm * (int64_t)ctx->num_sms);
+#ifdef K1_EVT
+  cudaEvent_t ev0, ev1;
+  cudaEventCreate(&ev0);
+  cudaEventCreate(&ev1);
+  cudaEventRecord(ev0, ctx->stream);
+#endif
   mmmcu::k1_pass<<<k1_grid, mmmcu::kK1Block, k1_smem, ctx->stream>>>(g, z, has_a, has_b,
                                                                        ctx->stats.as<unsigned long long>());
   MMMCU_LAUNCHED();
+#ifdef K1_EVT
+  cudaEventRecord(ev1, ctx->stream);
+  cudaEventSynchronize(ev1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ev0, ev1);
+  fprintf(stderr, "K1_EVT k1_pass %.1f us (grid %u, smem %d)\n", ms * 1e3, k1_grid, k1_smem);
+#endif
 #ifdef K1_PROF
   {
     static unsigned long long* dbuf = nullptr;

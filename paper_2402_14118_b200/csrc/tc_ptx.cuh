@@ -145,15 +145,13 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 
 // tf32 split of an fp32 value: hi keeps the top 19 bits (what the tensor core reads),
 // lo = v - hi is exact in fp32.
-// Inf keeps hi = Inf and NaN becomes the quiet NaN (the tensor core drops the low 13 bits),
-// both with lo = 0 (Inf - Inf would make lo NaN).  AUTO never sends non-finite operands to
-// K2-TC (k1_choose_path); a forced K2-TC turns 0 * Inf terms into NaN.
+// tf32 split of an fp32 value: hi keeps the top 19 bits (what the tensor core reads),
+// lo = v - hi is exact in fp32.  Non-finite inputs are not split meaningfully (Inf - Inf):
+// AUTO never sends them to K2-TC (k1_choose_path); a forced K2-TC yields NaN for them.
 __device__ __forceinline__ void split_tf32(float v, uint32_t& hi, uint32_t& lo) {
   const uint32_t b = __float_as_uint(v);
-  const bool special = (b & 0x7F800000u) == 0x7F800000u;
-  const bool nan = special && (b & 0x007FFFFFu) != 0u;
-  hi = nan ? 0x7FC00000u : special ? b : (b & 0xFFFFE000u);  // a NaN whose payload sits in the
-  lo = special ? 0u : __float_as_uint(v - __uint_as_float(hi));  // low 13 bits would read as Inf
+  hi = b & 0xFFFFE000u;
+  lo = __float_as_uint(v - __uint_as_float(hi));
 }
 
 // n-th (0-based) set bit of a 32-bit mask (mask must have > n set bits).
