@@ -18,12 +18,12 @@
 // with the number of MMAs into one accumulator (measured worst 6.7e-6 * Σ|a||b| with 512
 // steps into one D at 4096^3, against the 1e-5 tolerance; 0.9e-6 with 64-step segments,
 // 0.7e-6 with 32).  So the k loop is cut into 512-k segments accumulated in two
-// alternating TMEM accumulators D0 / D1: while the MMAs fill one, the 8 accumulator warps
-// add the other into fp32 registers (round-to-nearest adds), so the tensor pipe never waits
-// for a drain.  At the end C = C0 + P, staged through shared memory and coalesced.
+// alternating TMEM accumulators D0 / D1: while the MMAs fill one, the 4 accumulator warps
+// add the other into the tile's fp32 partial P in shared memory (round-to-nearest adds),
+// so the tensor pipe never waits for a drain.  At the end C = C0 + P, coalesced.
 //
-// Warp roles (448 threads; 14 warps cap registers at 128): 0-3 A transform, 4-11
-// accumulators (segment drain + C update), 12 TMA producer, 13 MMA issuer.  TMEM (512
+// Warp roles (320 threads): 0-3 A transform, 4-7 accumulators (segment drain + C update),
+// 8 TMA producer, 9 MMA issuer.  TMEM (512
 // columns): D0 [0,192), D1 [192,384), 4 A slots [384,512) of 32 columns (2 x (hi 8 | lo 8)),
 // one per stage.
 #pragma once
@@ -48,7 +48,7 @@ __device__ unsigned long long* td_prof = nullptr;  // debug builds only: per-CTA
 #endif
 constexpr int kTdStages = 4;    // stages of kTdSub MMA sub-steps (16 k): B smem + A TMEM slot
 constexpr int kTdSub = 2;       // MMA sub-steps (8 k, 3 MMAs) per stage
-constexpr int kTdThreads = 448; // warps 0-3 transform, 4-11 accumulators, 12 producer, 13 MMA
+constexpr int kTdThreads = 320; // warps 0-3 transform, 4-7 accumulators, 8 producer, 9 MMA
 constexpr int kTdSeg = TD_SEG;  // stages (512 k) per TMEM accumulation segment (worst 1.0e-6)
 constexpr int kTdTM = 128;
 constexpr int kTdTN = 192;
@@ -58,12 +58,12 @@ constexpr int kTdPStride = kTdTN + 4;         // staged P row stride (floats): c
 struct TdShared {
   float b[kTdStages][kTdSub * kTdStepFloats];  // 4 x 24 KB
   float a[kTdStages][8 * kTdSub][kTdTM];       // the stage's live A^T rows (4 x 8 KB)
-  float p[kTdTM][kTdPStride];                  // C-update staging (98 KB)
+  float p[kTdTM][kTdPStride];                  // the tile's fp32 partial P (98 KB)
   uint64_t tma[kTdStages];     // the stage's B image and A rows landed (TMA bytes)
   uint64_t full[kTdStages];    // stage ready: A split into its TMEM slot (4 transform warps)
   uint64_t empty[kTdStages];   // stage consumed: one tcgen05.commit frees B / A smem and the A slot
   uint64_t seg_full[2];                        // segment's last MMAs done (tcgen05.commit)
-  uint64_t seg_empty[2];                       // D drained (8 accumulator warps)
+  uint64_t seg_empty[2];                       // D drained (4 accumulator warps)
   uint32_t tmem_base;
 };
 constexpr int kTdSmem = (int)sizeof(TdShared) + 128;
@@ -110,7 +110,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
     }
     for (int d = 0; d < 2; ++d) {
       tc::mbar_init(&sh.seg_full[d], 1);
-      tc::mbar_init(&sh.seg_empty[d], 8);
+      tc::mbar_init(&sh.seg_empty[d], 4);
     }
     tc::fence_mbar_init();
   }
@@ -121,7 +121,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
   const uint32_t tbase = sh.tmem_base;
   constexpr uint32_t kAcol = 2 * kTdTN;  // TMEM columns of the A slots
 
-  if (warp == 12) {
+  if (warp == 8) {
     // ---------------------------------------------------- TMA producer (B and A per stage)
     // Per stage: one bulk copy of the two B step images, and the stage's 16 live A^T rows
     // of the tile — one bulk copy per run of consecutive live k (a dense tile: 1 copy of
@@ -167,7 +167,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
         if (j & 1) kpair = knext;
       }
     }
-  } else if (warp == 13) {
+  } else if (warp == 9) {
     // ------------------------------------------------------------------ MMA issuer
     // The whole warp runs the loop (warp-uniform operands stay in uniform registers); one
     // elected lane issues.  Each tcgen05.commit costs the tensor pipe ~50 cycles (measured:
@@ -314,14 +314,18 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       }
     }
   } else {
-    // ------------------------------------------------------ accumulator warps 4..11
-    // Warp w: tile row 32*(w%4) + lane (its TMEM lane), columns 96*((w-4)/4) .. +95, held
-    // as fp32 registers.  Each segment's D is added in (round-to-nearest), then released;
-    // after a tile's last segment, C = C0 + P goes out through the staging buffer (rows
-    // with a 196-float stride: conflict-free 16-byte stores), lanes along the rows
-    // (coalesced), while the MMAs already run the next tile.
-    const int q4 = warp & 3, half = (warp - 4) >> 2;
-    const uint32_t taddr = tbase + ((uint32_t)(q4 * 32) << 16) + 96 * half;
+    // ------------------------------------------------------- accumulator warps 4..7
+    // Thread = tile row r = 32*(w%4) + lane (its TMEM lane).  The tile's fp32 partial P lives
+    // in shared memory (row stride 196 floats: conflict-free 16-byte accesses): each
+    // segment's D is added into the row (round-to-nearest; P = D for the first segment),
+    // 16 columns per tcgen05.ld, then D is released.  After the tile's last segment,
+    // C = C0 + P goes out with lanes along the rows (coalesced), while the MMAs already run
+    // the next tile.  Keeping P out of registers leaves the transform warps the register
+    // file (a spilling transform ran sparse tiles 2x slower).
+    const int q4 = warp & 3;
+    const int r = 32 * q4 + lane;
+    const uint32_t taddr = tbase + ((uint32_t)(q4 * 32) << 16);
+    float4* prow = reinterpret_cast<float4*>(&sh.p[r][0]);
     uint32_t G = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int64_t rt = t % m_tiles, tb = t / m_tiles;
@@ -329,48 +333,51 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       const int nstage = (nsteps + kTdSub - 1) / kTdSub;
       const int nseg = (nstage + kTdSeg - 1) / kTdSeg;
       if (nseg == 0) continue;
-      float acc[96];
-#pragma unroll
-      for (int e = 0; e < 96; ++e) acc[e] = 0.0f;
       for (int g = 0; g < nseg; ++g, ++G) {
         const uint32_t d = G & 1u;
         tc::mbar_wait_sleep(&sh.seg_full[d], (G >> 1) & 1u);
         tc::fence_after_sync();
-#pragma unroll
-        for (int c = 0; c < 6; ++c) {
+#pragma unroll 1
+        for (int c = 0; c < kTdTN / 16; ++c) {
           uint32_t v[16];
           tc::tmem_ld16(taddr + d * kTdTN + 16 * c, v);
           tc::tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 16; ++e) acc[16 * c + e] += __uint_as_float(v[e]);
+          for (int q = 0; q < 4; ++q) {
+            float4 x = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                   __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+            if (g > 0) {
+              const float4 y = prow[4 * c + q];
+              x.x = y.x + x.x;
+              x.y = y.y + x.y;
+              x.z = y.z + x.z;
+              x.w = y.w + x.w;
+            }
+            prow[4 * c + q] = x;
+          }
         }
         tc::fence_before_sync();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&sh.seg_empty[d]);
       }
       const int64_t m0 = rt * kTdTM, n0 = tb * kTdTN;
-      {
-        float4* prow = reinterpret_cast<float4*>(&sh.p[32 * q4 + lane][96 * half]);
-#pragma unroll
-        for (int q = 0; q < 24; ++q) prow[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
-      }
-      td_named_sync(1, 256);
-      // warp w-4 updates rows w-4, w+4, ...; per 4 rows all loads go out before the adds
+      td_named_sync(1, 128);  // every row of P is final
+      // warp q4 updates rows q4, q4+4, ...; per 8 rows all loads go out before the adds
       const int64_t gc0 = n0 + 4 * lane, gc1 = gc0 + 128;
       const bool full0 = gc0 + 3 < N, full1 = lane < 16 && gc1 + 3 < N;
 #pragma unroll 1
-      for (int i0 = 0; i0 < 16; i0 += 4) {
-        float4 cv[4][2];
+      for (int i0 = 0; i0 < 32; i0 += 8) {
+        float4 cv[8][2];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int64_t row = m0 + (warp - 4) + 8 * (i0 + i);
+        for (int i = 0; i < 8; ++i) {
+          const int64_t row = m0 + q4 + 4 * (i0 + i);
           const float* crow = C + row * ldc;
           if (row < M && full0) cv[i][0] = *reinterpret_cast<const float4*>(crow + gc0);
           if (row < M && full1) cv[i][1] = *reinterpret_cast<const float4*>(crow + gc1);
         }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int rr = (warp - 4) + 8 * (i0 + i);
+        for (int i = 0; i < 8; ++i) {
+          const int rr = q4 + 4 * (i0 + i);
           const int64_t row = m0 + rr;
           if (row >= M) break;
           float* crow = C + row * ldc;
@@ -389,13 +396,14 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
               c4.w += pv.w;
               *reinterpret_cast<float4*>(crow + gcol) = c4;
             } else {
+#pragma unroll
               for (int e = 0; e < 4; ++e)
                 if (gcol + e < N) crow[gcol + e] += pr[col + e];
             }
           }
         }
       }
-      td_named_sync(1, 256);
+      td_named_sync(1, 128);  // P may be overwritten by the next tile's first drain
     }
   }
   tc::fence_before_sync();
