@@ -28,7 +28,10 @@ constexpr int kK1Threads = 256;  // 8 compute warps; each lane owns 4 columns of
 constexpr int kK1Block = kK1Threads + 32;  // + the TMA producer warp (k1_pass)
 constexpr int kK1Cols = 4 * kK1Threads;  // 1024 columns per CTA tile
 constexpr int kK1Rows = 32;              // rows per CTA tile (one 32-bit k-word for B)
-constexpr int kTcTileN = 192;            // K2-TC C tile width (columns)
+#ifndef TD_TN
+#define TD_TN 192
+#endif
+constexpr int kTcTileN = TD_TN;          // K2-TC C tile width (columns)
 
 __device__ __forceinline__ float4 ldg_stream(const float* p) {
   float4 v;

@@ -43,21 +43,30 @@ __device__ unsigned long long* td_prof = nullptr;  // debug builds only: per-CTA
 #define TD_ADD(i, x)
 #endif
 
+#ifndef TD_KB
+#define TD_KB 2
+#endif
 #ifndef TD_SEG
 #define TD_SEG 32
 #endif
-constexpr int kTdStages = 4;    // stages of kTdSub MMA sub-steps (16 k): B smem + A TMEM slot
+#ifndef TD_STAGES
+#define TD_STAGES 4
+#endif
+constexpr int kTdStages = TD_STAGES;  // stages of kTdSub MMA sub-steps (16 k): B smem + A TMEM slot
 constexpr int kTdSub = 2;       // MMA sub-steps (8 k, 3 MMAs) per stage
 constexpr int kTdThreads = 320; // warps 0-3 transform, 4-7 accumulators, 8 producer, 9 MMA
 constexpr int kTdSeg = TD_SEG;  // stages (512 k) per TMEM accumulation segment (worst 1.0e-6)
 constexpr int kTdTM = 128;
-constexpr int kTdTN = 192;
+#ifndef TD_TN
+#define TD_TN 192
+#endif
+constexpr int kTdTN = TD_TN;
 constexpr int kTdStepFloats = kTdTN * 8 * 2;  // one 8-k step image (K1): hi | lo, 12 KB
 constexpr int kTdPStride = kTdTN + 4;         // staged P row stride (floats): conflict-free 16-byte accesses
 
 struct TdShared {
-  float b[kTdStages][kTdSub * kTdStepFloats];  // 4 x 24 KB
-  float a[kTdStages][8 * kTdSub][kTdTM];       // the stage's live A^T rows (4 x 8 KB)
+  float b[kTdStages][kTdSub * kTdStepFloats];  // B step images
+  float a[kTdStages][8 * kTdSub][kTdTM];       // the stage's live A^T rows (8 KB each)
   float p[kTdTM][kTdPStride];                  // the tile's fp32 partial P (98 KB)
   uint64_t tma[kTdStages];     // the stage's B image and A rows landed (TMA bytes)
   uint64_t full[kTdStages];    // stage ready: A split into its TMEM slot (4 transform warps)
@@ -267,7 +276,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
           store_slot(st, vals);
         }
       } else {
-        constexpr int kB = 2, KB = 8 * kTdSub * kB;  // stages per batch, k per batch
+        constexpr int kB = TD_KB, KB = 8 * kTdSub * kB;  // stages per batch, k per batch
         const float* acol = AT + rt * kpad * 128 + r;
         const int4* kx4 = reinterpret_cast<const int4*>(tck + tb * maxsteps * 8);
         const int npos = nsteps * 8, nb = (nstage + kB - 1) / kB;
