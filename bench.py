@@ -218,15 +218,16 @@ TC_TM, TC_TN = 128, 192  # K2-TC C tile (k2_tc.cuh)
 
 
 def tc_executed_flops(M, b, torch):
-    """Tensor-core flops K2-TC executes on a cell: per 192-column tile, ceil(live k / 8) MMA
-    steps of 3 tf32 MMAs (hi/lo split) of 128 x 192 x 8, for every 128-row tile."""
+    """Tensor-core flops K2-TC executes on a cell (fp16 split, AUTO's TC path): per 192-column
+    tile, ceil(live k / 16) MMA steps of 3 fp16 MMAs (hi/lo split) of 128 x 192 x 16, for every
+    128-row tile."""
     K, N = b.shape
     nt = (N + TC_TN - 1) // TC_TN
     nz = torch.zeros((K, nt * TC_TN), dtype=torch.bool, device=b.device)
     nz[:, :N] = b != 0
     live = nz.view(K, nt, TC_TN).any(dim=2).sum(dim=0)  # live k per tile
-    steps = int(((live + 7) // 8).sum().item())
-    return steps * ((M + TC_TM - 1) // TC_TM) * 3 * 2 * TC_TM * TC_TN * 8
+    steps = int(((live + 15) // 16).sum().item())
+    return steps * ((M + TC_TM - 1) // TC_TM) * 3 * 2 * TC_TM * TC_TN * 16
 
 
 def cell_stats(cells, As, Bs, ctx, torch):
@@ -420,10 +421,10 @@ def main():
     tensor = None
     if tc_ms > 0:
         tensor = {"kernel": "k2_tc", "executed_tflops": round(tc_exec / (tc_ms * 1e-3) / 1e12, 1),
-                  "peak_tflops": round(bf16 / 2, 1) if bf16 else None,
-                  "peak_source": "tf32 dense = measured bf16 (MEASURED_PEAKS.json) / 2" if bf16 else None,
-                  "frac": round(tc_exec / (tc_ms * 1e-3) / 1e12 / (bf16 / 2), 4) if bf16 else None,
-                  "def": "3xTF32 MMAs the kernel issues (3 per live-k step of 8 per 128x192 tile) / K2-TC time"}
+                  "peak_tflops": round(bf16, 1) if bf16 else None,
+                  "peak_source": "fp16 dense = measured bf16 (MEASURED_PEAKS.json, same kind::f16 rate)" if bf16 else None,
+                  "frac": round(tc_exec / (tc_ms * 1e-3) / 1e12 / bf16, 4) if bf16 else None,
+                  "def": "fp16-split MMAs the kernel issues (3 per live-k step of 16 per 128x192 tile) / K2-TC time"}
     t_roof = sum(max(s["flops"] / (fp32_peak * 1e12), s["bytes"] / (hbm_peak * 1e9)) for s in stats)
     t_meas = float((k1_ms + k2_ms).sum()) * 1e-3
     hbm_bytes = sum(s["bytes"] for s in stats)

@@ -103,7 +103,7 @@ class Handle {
 template <typename T>
 class MmmContext;
 
-// How C is accumulated.  Auto (default): the plan picks K2-SIMT or the 3xTF32 tensor-core
+// How C is accumulated.  Auto (default): the plan picks K2-SIMT or the fp16-split tensor-core
 // K2-TC per multiply, C within the north_star tolerance |dC| <= 1e-5 (|c0| + sum|a||b|).
 // Exact: K2-SIMT only, which replays the reference kernel's ascending-k fmaf chain: C is
 // bit-identical to KernelTable::apply (kernel_table.cpp).

@@ -78,9 +78,12 @@ typedef enum {
   MMMCU_ALGO_DENSE = 2,      /* multiply_simple (dense i-k-j fma)            */
   MMMCU_ALGO_SIMT_SPAN8 = 3, /* K2-SIMT forced to 8-column (group) masks                  */
   MMMCU_ALGO_SIMT_SPAN16 = 4,/* K2-SIMT forced to 16-column slice masks                   */
-  MMMCU_ALGO_TC = 5          /* K2-TC: tcgen05 3xTF32 on 128x192 C tiles over each tile's
-                                live k; tolerance-matched (|dC| <= 1e-5 * (|c0| +
+  MMMCU_ALGO_TC = 5,         /* K2-TC: tcgen05 3-term fp16 split (kind::f16, operands
+                                scaled by powers of two) on 128x192 C tiles over each
+                                tile's live k; tolerance-matched (|dC| <= 1e-5 * (|c0| +
                                 sum|a||b|)), not bit-exact                                 */
+  MMMCU_ALGO_TC32 = 6        /* K2-TC with the 3xTF32 split (kind::tf32): same tiles and
+                                tolerance, half the k per MMA; no operand scaling          */
 } mmmcu_algo;
 
 /* ---- context --------------------------------------------------------------------- */

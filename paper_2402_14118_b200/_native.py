@@ -31,6 +31,7 @@ ALGO_DENSE = 2
 ALGO_SIMT_SPAN8 = 3
 ALGO_SIMT_SPAN16 = 4
 ALGO_TC = 5
+ALGO_TC32 = 6
 
 
 class Lane(ctypes.Structure):

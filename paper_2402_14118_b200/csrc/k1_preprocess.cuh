@@ -22,6 +22,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "tc_ptx.cuh"
+
 namespace mmmcu {
 
 constexpr int kK1Threads = 256;  // 8 compute warps; each lane owns 4 columns of a 1024-column tile
@@ -54,16 +56,18 @@ struct K1Scratch {
   uint32_t* acol;
   uint32_t* tile_sum;     // [ceil(M/32)] non-zeros per 32-row tile (zeroed)
   uint32_t* nonfinite_a;  // set iff A holds an Inf / NaN / subnormal (zeroed): AUTO keeps K2-SIMT
+  uint32_t* amax;         // bits of max|A| (zeroed, atomicMax): K2-TC's fp16 operand scale
   int64_t* tile_prefix;   // [ceil(M/32) + 1] exclusive prefix of tile_sum (written by the last CTA)
   uint32_t* bpop;
   uint32_t* bnz;
-  unsigned long long* btot;  // B totals: {Σ non-zero (k, slice), Σ bpop, Σ bnz, Inf/NaN/subnormal seen} (zeroed)
+  unsigned long long* btot;  // B totals: {Σ non-zero (k, slice), Σ bpop, Σ bnz, Inf/NaN/subnormal seen,
+                             //            bits of max|B|} (zeroed)
   unsigned int* done;
   unsigned int* next_tile;  // K1 tile counter (dynamic scheduling; reset by the last CTA)
   // K2-TC operands (nullptr when the TC path is not prepared)
   float* at;              // A^T per 128-row tile: at[(rt * kpad + k) * 128 + (i % 128)], zero padded
   int64_t kpad;           // K rounded up to 32
-  int64_t m_at;           // M rounded up to 128
+  int64_t m_at;           // M rounded up to 256 (K2-TC pair tiles)
   uint32_t* tlive;        // [n_tc][kw] live-k mask per kTcTileN-column TC tile: bit kk of word c
                           // set iff B[32c + kk, tile columns] has a non-zero (zeroed, atomicOr)
   int64_t n_tb;           // 256-column tiles of B (K2-SIMT records)
@@ -81,7 +85,8 @@ __device__ void k1_plan_totals(const unsigned long long* __restrict__ btot, int6
 // SM-cycles of each path from the plan, constants measured on B200 (K2 choice):
 //   K2-SIMT = records * 1158 + row tiles * (span 16: 26 * slice_nz | span 8: 17.5 * pop)
 //             records = row tiles * 256-column tiles * 32-k chunks
-//   K2-TC   = row tiles * Σ_tiles (24200 + 784 * stages), stages = ceil(live k / 16)
+//   K2-TC   = row tiles * Σ_tiles (24200 + 784 * stages), stages = ceil(live k / 32) (fp16
+//             split: 6 MMAs of 16 k per stage)
 //   + K1 packing traffic at 0.0433 SM-cycles per byte (HBM): K2-SIMT rows 2 x 64 B per
 //     non-zero (k, slice); K2-TC step images 3 x 768 B per live (k, tile);
 //   each divided by min(148 SMs, its CTA count).
@@ -99,7 +104,7 @@ __device__ void k1_choose_path(const K1Scratch& z, int64_t M, int64_t kw, unsign
       for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
       if (lane0 == 0) {
         live += n;
-        st += (n + 15) / 16;
+        st += (n + 31) / 32;  // fp16-split stages of 32 live k
       }
     }
   }
@@ -132,7 +137,13 @@ __device__ void k1_choose_path(const K1Scratch& z, int64_t M, int64_t kw, unsign
     // terms the reference never forms into NaN, subnormals would be flushed — keep the
     // exact path
     const bool nonfinite = *z.nonfinite_a != 0u || z.btot[3] != 0ull;
-    if (!nonfinite && tc / par_tc < simt / par_simt) out[7] = 32ull;
+    // fp16 split: operand scales within [-100, 100] (max|x| within 2^-86 .. 2^114)
+    auto range_ok = [](uint32_t m) {
+      const int e = (int)(m >> 23) - 127;
+      return m == 0u || (e >= -86 && e <= 114);
+    };
+    const bool ranged = range_ok(*z.amax) && range_ok((uint32_t)z.btot[4]);
+    if (!nonfinite && ranged && tc / par_tc < simt / par_simt) out[7] = 32ull;
   }
   __syncthreads();
 }
@@ -396,6 +407,7 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
   uint32_t ccount[4] = {0, 0, 0, 0};
   uint32_t warp_total = 0;
   bool nonfin = false;
+  float vmax = 0.0f;  // max |x| over the lane's elements (fp16 operand scale)
   __shared__ uint32_t s_ab[kK1Rows][32];  // the tile's bitmap words (row, chunk)
   const int64_t rend = min(r0 + kK1Rows, M);
   const int64_t rend_at = z.at ? min(r0 + kK1Rows, z.m_at) : rend;
@@ -438,6 +450,7 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
       for (int j = 0; j < 4; ++j) {
         const bool nz = x[u][j] != 0.0f;
         nonfin |= k1_tc_unsafe(x[u][j]);
+        vmax = fmaxf(vmax, fabsf(x[u][j]));
         const uint32_t m = __ballot_sync(0xffffffffu, nz);
         ccount[j] += nz ? 1u : 0u;
         cnt += __popc(m);
@@ -451,6 +464,10 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
   }
   if (lane == 0 && warp_total) atomicAdd(&z.tile_sum[ty], warp_total);
   if (__any_sync(0xffffffffu, nonfin) && lane == 0) atomicOr(z.nonfinite_a, 1u);
+  {
+    const uint32_t mb = __reduce_max_sync(0xffffffffu, __float_as_uint(vmax));
+    if (lane == 0 && mb && z.amax) atomicMax(z.amax, mb);
+  }
 #pragma unroll
   for (int j = 0; j < 4; ++j)
     if (ok[j] && ccount[j]) atomicAdd(&z.acol[col[j]], ccount[j]);
@@ -492,6 +509,7 @@ __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, 
   const uint32_t gmask = 0xFFu << (8 * gs);
   uint32_t gword = 0;
   bool nonfin = false;
+  float vmax = 0.0f;
   const int64_t kend = min(k0 + 32, K);
   for (int64_t kb = k0; kb < kend; kb += 8) {
     float x[8][4];
@@ -506,6 +524,7 @@ __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, 
       for (int j = 0; j < 4; ++j) {
         m[j] = __ballot_sync(0xffffffffu, x[u][j] != 0.0f);
         nonfin |= k1_tc_unsafe(x[u][j]);
+        vmax = fmaxf(vmax, fabsf(x[u][j]));
       }
       const uint32_t mg = (m[0] & sel[0]) | (m[1] & sel[1]) | (m[2] & sel[2]) | (m[3] & sel[3]);  // branch-free
       gword |= (uint32_t)((mg & gmask) != 0) << (uint32_t)(kb - k0 + u);
@@ -528,6 +547,10 @@ __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, 
     nz_w += __shfl_xor_sync(0xffffffffu, nz_w, o);
   }
   if (__any_sync(0xffffffffu, nonfin) && lane == 0) atomicOr(&z.btot[3], 1ull);
+  {
+    const uint32_t mb = __reduce_max_sync(0xffffffffu, __float_as_uint(vmax));
+    if (lane == 0 && mb) atomicMax(&z.btot[4], (unsigned long long)mb);
+  }
   if (lane == 0 && pop_w) atomicAdd(&z.btot[1], (unsigned long long)pop_w);
   if (lane == 0 && nz_w) atomicAdd(&z.btot[2], (unsigned long long)nz_w);
   // (k, 16-column slice) pairs with a non-zero: even group lanes own slice (2s, 2s+1)
@@ -682,9 +705,11 @@ __global__ void __launch_bounds__(256) k1_csr(const uint32_t* __restrict__ abits
   Idx* buf = s_buf[warp];
   int64_t out = s_off[warp];
   const uint32_t* bits = abits + row * kw;
+  uint32_t next = lane < kw ? bits[lane] : 0u;  // the next chunk's word is loaded a chunk ahead
   for (int64_t w0 = 0; w0 < kw; w0 += 32) {
     const int64_t w = w0 + lane;
-    uint32_t word = w < kw ? bits[w] : 0u;
+    uint32_t word = next;
+    next = w + 32 < kw ? bits[w + 32] : 0u;
     const uint32_t n = __popc(word);
     uint32_t x = n;
 #pragma unroll
@@ -816,6 +841,8 @@ struct PackTcArgs {
   float* tcb;
   int32_t* tck;
   int32_t* tcn;
+  int f16;                            // fp16 split: 16 live k per step, B scaled by 2^sB
+  const unsigned long long* bmax;     // bits of max|B| (K1 pass), fp16 only
 };
 
 // CTA (bx = step block, tb = tile) of the K2-TC pack; dynamic smem (2 kw + 1) words.
@@ -827,7 +854,7 @@ __device__ __forceinline__ void k1_pack_tc_cta(const PackTcArgs& g, int64_t bx, 
   int32_t* __restrict__ tck = g.tck;
   int32_t* __restrict__ tcn = g.tcn;
   extern __shared__ __align__(16) uint32_t pt_smem[];  // masks [kw] | prefix [kw + 1]
-  __shared__ int32_t s_k[kPtSteps * 8];
+  __shared__ int32_t s_k[kPtSteps * 16];
   __shared__ int32_t wsum[kPtThreads / 32];
   uint32_t* s_m = pt_smem;
   int32_t* s_pre = reinterpret_cast<int32_t*>(pt_smem + kw);
@@ -859,12 +886,13 @@ __device__ __forceinline__ void k1_pack_tc_cta(const PackTcArgs& g, int64_t bx, 
   if (tid == 0) s_pre[kw] = carry;
   __syncthreads();
   const int32_t total = carry;
-  const int64_t nsteps = (total + 7) / 8;
+  const int SK = g.f16 ? 16 : 8;  // live k per step
+  const int64_t nsteps = (total + SK - 1) / SK;
   if (bx == 0 && tid == 0) tcn[tb] = total;
   const int64_t s0 = bx * kPtSteps;
   if (s0 >= nsteps) return;
-  if (tid < kPtSteps * 8) {
-    const int64_t p = s0 * 8 + tid;
+  if (tid < kPtSteps * SK) {
+    const int64_t p = s0 * SK + tid;
     int32_t k = -1;
     if (p < total) {
       int64_t lo = 0, hi = kw - 1;  // last chunk c with s_pre[c] <= p
@@ -881,6 +909,36 @@ __device__ __forceinline__ void k1_pack_tc_cta(const PackTcArgs& g, int64_t bx, 
     if (p < maxsteps * 8) tck[tb * maxsteps * 8 + p] = k;
   }
   __syncthreads();
+  if (g.f16) {
+    // job = (step, k-octet q, column n): 8 B values (scaled by 2^sB) -> 8 fp16 hi + 8 fp16
+    // lo, one 16-byte store each.  K2-TC runs fp16 tiles on CTA pairs, each CTA holding one
+    // column half h (96 columns) of B: a tile's images are stored per half, [h][step], a
+    // half step = hi image (3 KB) | lo image (3 KB), element (c, j) of column c = n - 96h at
+    // byte (c % 8) * 16 + (c / 8) * 256 + (j / 8) * 128 + (j % 8) * 2 of its image
+    const float sb = tc::exp2_int(tc::f16_scale_exp((uint32_t)*g.bmax));
+    for (int j = tid; j < kPtSteps * 2 * kTcTileN; j += kPtThreads) {
+      const int sl = j / (2 * kTcTileN), q = (j / kTcTileN) & 1, n = j % kTcTileN;
+      const int64_t s = s0 + sl;
+      if (s >= nsteps) break;
+      const bool col_ok = n0 + n < ldb;
+      float v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int32_t k = s_k[sl * 16 + 8 * q + i];
+        v[i] = (k >= 0 && col_ok) ? __ldg(B + (int64_t)k * ldb + n0 + n) * sb : 0.0f;
+      }
+      uint32_t h[4], l[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) tc::split_f16x2(v[2 * i], v[2 * i + 1], h[i], l[i]);
+      constexpr int kHalf = kTcTileN / 2;
+      const int hf = n / kHalf, c = n % kHalf;
+      float* img = tcb + ((tb * 2 + hf) * maxsteps + s) * (kHalf * 16);
+      const int off = (c & 7) * 4 + (c >> 3) * 64 + q * 32;  // in floats
+      *reinterpret_cast<uint4*>(img + off) = make_uint4(h[0], h[1], h[2], h[3]);
+      *reinterpret_cast<uint4*>(img + kHalf * 8 + off) = make_uint4(l[0], l[1], l[2], l[3]);
+    }
+    return;
+  }
   // job = (step, k-quad q, column n): 4 B values -> one float4 hi + one float4 lo
   for (int j = tid; j < kPtSteps * 2 * kTcTileN; j += kPtThreads) {
     const int sl = j / (2 * kTcTileN), q = (j / kTcTileN) & 1, n = j % kTcTileN;

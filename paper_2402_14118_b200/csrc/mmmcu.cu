@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -78,8 +79,10 @@ struct mmmcu_ctx {
   // ---- K2 operands emitted by K1 (which ones depends on the algorithm, see ops_for)
   bool op_at = false, op_rows = false, op_tcb = false;
   bool rows_fresh = false, tcb_fresh = false;  // packed without the device gate (valid for a forced path)
+  bool tcb_f16 = true;                          // format of the packed K2-TC step images (fp16 / tf32 split)
   int ops_b = 0;                                // operand sets B was staged for
   int64_t kpad = 0, m_at = 0, n_tb = 0, n_tc = 0, tc_steps = 0;
+  int tc_pairs = 0;  // co-resident K2-TC CTA pairs (cudaOccupancyMaxActiveClusters), 0 = not queried
   DevBuf at, tcb, tck, tcn, brows, row_off;
 
   // ---- statistics: u64 [16] = {inv, lanes, skipped, zreg, nnzA, pop, zero_codes, span, slice_nz}
@@ -150,9 +153,15 @@ uint32_t* za_acol(mmmcu_ctx* ctx) { return ctx->za.as<uint32_t>() + ctx->M; }
 uint32_t* za_tiles(mmmcu_ctx* ctx) { return ctx->za.as<uint32_t>() + ctx->M + ctx->Ka; }
 int64_t n_row_tiles(int64_t M) { return (M + mmmcu::kK1Rows - 1) / mmmcu::kK1Rows; }
 unsigned long long* zb_slice(mmmcu_ctx* ctx) { return ctx->zb.as<unsigned long long>(); }
-uint32_t* zb_bpop(mmmcu_ctx* ctx) { return reinterpret_cast<uint32_t*>(ctx->zb.as<unsigned long long>() + 4); }
+uint32_t* zb_bpop(mmmcu_ctx* ctx) {
+  return reinterpret_cast<uint32_t*>(ctx->zb.as<unsigned long long>() + 6);  // after kZbHead
+}
 // one word after the A scratch: set iff A holds an Inf / NaN (zeroed with za)
 uint32_t* za_nonfinite(mmmcu_ctx* ctx) { return za_tiles(ctx) + n_row_tiles(ctx->M); }
+// and one more: bits of max|A| (K2-TC's fp16 scale)
+uint32_t* za_amax(mmmcu_ctx* ctx) { return za_nonfinite(ctx) + 1; }
+// zb starts with 6 u64 B totals (k1_preprocess.cuh K1Scratch::btot; [4] = bits of max|B|)
+constexpr int kZbHead = 6;
 uint32_t* zb_bnz(mmmcu_ctx* ctx) { return zb_bpop(ctx) + ctx->Kb; }
 // Operand sets K1 emits for K2: A^T tiles (SIMT v2, TC), raw B rows (SIMT v2), tf32 B step
 // images + live-k lists (TC).
@@ -160,7 +169,8 @@ enum { OP_AT = 1, OP_ROWS = 2, OP_TCB = 4 };
 int ops_for(const mmmcu_ctx* ctx) {
   switch (ctx->algo) {
     case MMMCU_ALGO_AUTO: return OP_AT | OP_ROWS | OP_TCB;  // K1's last CTA picks (k1_choose_path)
-    case MMMCU_ALGO_TC: return OP_AT | OP_TCB;
+    case MMMCU_ALGO_TC:
+    case MMMCU_ALGO_TC32: return OP_AT | OP_TCB;
     case MMMCU_ALGO_DENSE: return 0;
     default: return OP_AT | OP_ROWS;
   }
@@ -178,15 +188,15 @@ mmmcu_status stage_a(mmmcu_ctx* ctx, const float* A, int64_t M, int64_t K, int64
   ctx->has_a = false;
   ctx->csr_idx_bytes = K <= 65536 ? 2 : 4;
   MMMCU_CUDA(ctx->abits.ensure(sizeof(uint32_t) * M * kw));
-  MMMCU_CUDA(ctx->za.ensure(sizeof(uint32_t) * (M + K + n_row_tiles(M) + 1)));
+  MMMCU_CUDA(ctx->za.ensure(sizeof(uint32_t) * (M + K + n_row_tiles(M) + 2)));
   MMMCU_CUDA(ctx->tile_prefix.ensure(sizeof(int64_t) * (n_row_tiles(M) + 1)));
   MMMCU_CUDA(ctx->row_ptr.ensure(sizeof(int64_t) * (M + 1)));
   MMMCU_CUDA(ctx->cols.ensure((size_t)ctx->csr_idx_bytes * M * K));
-  MMMCU_CUDA(cudaMemsetAsync(ctx->za.p, 0, sizeof(uint32_t) * (M + K + n_row_tiles(M) + 1), ctx->stream));
+  MMMCU_CUDA(cudaMemsetAsync(ctx->za.p, 0, sizeof(uint32_t) * (M + K + n_row_tiles(M) + 2), ctx->stream));
   ctx->op_at = false;
   if (ops_for(ctx) & OP_AT) {
     ctx->kpad = round_up(K, 32);
-    ctx->m_at = round_up(M, 128);
+    ctx->m_at = round_up(M, 256);  // K2-TC pairs take row tiles two at a time
     MMMCU_CUDA(ctx->at.ensure(sizeof(float) * ctx->m_at * ctx->kpad));
   }
   ctx->A = A;
@@ -216,7 +226,7 @@ mmmcu_status stage_b(mmmcu_ctx* ctx, const float* B, int64_t K, int64_t N, int64
   const int64_t n_cnt = n_tb * kw;
   const int64_t n_tc = (ldb + mmmcu::kTcTileN - 1) / mmmcu::kTcTileN;
   const int64_t n_extra = ((ops & OP_TCB) ? n_tc * kw : 0) + ((ops & OP_ROWS) ? n_cnt : 0);
-  const size_t zb_bytes = 4 * sizeof(unsigned long long) + sizeof(uint32_t) * (2 * K + n_extra);
+  const size_t zb_bytes = kZbHead * sizeof(unsigned long long) + sizeof(uint32_t) * (2 * K + n_extra);
   MMMCU_CUDA(ctx->zb.ensure(zb_bytes));
   MMMCU_CUDA(cudaMemsetAsync(ctx->zb.p, 0, zb_bytes, ctx->stream));
   ctx->n_tb = n_tb;
@@ -247,10 +257,15 @@ mmmcu::PackRowsArgs rows_args(mmmcu_ctx* ctx) {
   return mmmcu::PackRowsArgs{ctx->B, ctx->ldb, ctx->bgrp.as<uint32_t>(), (ctx->Kb + 31) / 32,
                              ctx->row_off.as<int64_t>(), ctx->brows.as<uint4>()};
 }
-mmmcu::PackTcArgs tc_args(mmmcu_ctx* ctx) {
+mmmcu::PackTcArgs tc_args(mmmcu_ctx* ctx, bool f16) {
   return mmmcu::PackTcArgs{ctx->B, ctx->ldb, zb_tlive(ctx), (ctx->Kb + 31) / 32, ctx->tc_steps,
-                           ctx->tcb.as<float>(), ctx->tck.as<int32_t>(), ctx->tcn.as<int32_t>()};
+                           ctx->tcb.as<float>(), ctx->tck.as<int32_t>(), ctx->tcn.as<int32_t>(), f16 ? 1 : 0,
+                           zb_slice(ctx) + 4};
 }
+// AUTO and MMMCU_ALGO_TC use the fp16 split, MMMCU_ALGO_TC32 the tf32 split
+bool tc_f16(const mmmcu_ctx* ctx) { return ctx->algo != MMMCU_ALGO_TC32; }
+// most step images a tile can need: every k live, 16 (fp16) or 8 (tf32) per step
+int64_t pack_steps(const mmmcu_ctx* ctx, bool f16) { return f16 ? (ctx->tc_steps + 1) / 2 : ctx->tc_steps; }
 int pack_tc_smem(mmmcu_ctx* ctx) { return (int)(sizeof(uint32_t) * (2 * ((ctx->Kb + 31) / 32) + 1)); }
 
 mmmcu_status pack_rows(mmmcu_ctx* ctx) {
@@ -261,12 +276,14 @@ mmmcu_status pack_rows(mmmcu_ctx* ctx) {
 }
 
 mmmcu_status pack_tc(mmmcu_ctx* ctx) {
+  const bool f16 = tc_f16(ctx);
   const int smem = pack_tc_smem(ctx);
   if (smem > 200 * 1024) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "K too large for the TC packer");
   MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k1_pack_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  dim3 grid((unsigned)((ctx->tc_steps + mmmcu::kPtSteps - 1) / mmmcu::kPtSteps), (unsigned)ctx->n_tc);
-  mmmcu::k1_pack_tc<<<grid, mmmcu::kPtThreads, smem, ctx->stream>>>(tc_args(ctx));
+  dim3 grid((unsigned)((pack_steps(ctx, f16) + mmmcu::kPtSteps - 1) / mmmcu::kPtSteps), (unsigned)ctx->n_tc);
+  mmmcu::k1_pack_tc<<<grid, mmmcu::kPtThreads, smem, ctx->stream>>>(tc_args(ctx, f16));
   MMMCU_LAUNCHED();
+  ctx->tcb_f16 = f16;
   return MMMCU_OK;
 }
 
@@ -274,18 +291,19 @@ mmmcu_status pack_auto(mmmcu_ctx* ctx, const unsigned long long* sel) {
   const int smem = pack_tc_smem(ctx);
   if (smem > 200 * 1024) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "K too large for the TC packer");
   const int64_t rows_x = (ctx->Kb + 31) / 32, n_rows = rows_x * ctx->n_tb;
-  const int64_t tc_x = (ctx->tc_steps + mmmcu::kPtSteps - 1) / mmmcu::kPtSteps, n_tc = tc_x * ctx->n_tc;
+  const int64_t tc_x = (pack_steps(ctx, true) + mmmcu::kPtSteps - 1) / mmmcu::kPtSteps, n_tc = tc_x * ctx->n_tc;
   if (n_rows + n_tc > 0x7fffffff) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "B too large for one pack launch");
   MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k1_pack_auto, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   mmmcu::k1_pack_auto<<<(unsigned)(n_rows + n_tc), mmmcu::kPtThreads, smem, ctx->stream>>>(
-      rows_args(ctx), rows_x, n_rows, tc_args(ctx), tc_x, sel);
+      rows_args(ctx), rows_x, n_rows, tc_args(ctx, true), tc_x, sel);
   MMMCU_LAUNCHED();
+  ctx->tcb_f16 = true;
   return MMMCU_OK;
 }
 
 // One fused K1 launch over the staged operand(s), then (for A) the CSR index lists.
 mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
-  MMMCU_CUDA(ctx->stats.ensure(sizeof(unsigned long long) * 16));
+  MMMCU_CUDA(ctx->stats.ensure(sizeof(unsigned long long) * 24));
   if (ctx->ctl.cap == 0) {
     MMMCU_CUDA(ctx->ctl.ensure(256));
     MMMCU_CUDA(cudaMemsetAsync(ctx->ctl.p, 0, 256, ctx->stream));
@@ -305,7 +323,7 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   const bool rows_b = (ops_b & OP_ROWS) && (do_b || gate);
   const unsigned long long* sel = gate ? ctx->stats.as<unsigned long long>() + 7 : nullptr;
   const int64_t a_tx = (ctx->Ka + mmmcu::kK1Cols - 1) / mmmcu::kK1Cols;
-  const int64_t a_rows = tc_a ? ctx->m_at : ctx->M;  // A^T tiles are written to the 128-row boundary
+  const int64_t a_rows = tc_a ? ctx->m_at : ctx->M;  // A^T tiles are written to the 256-row boundary
   const int64_t nA = do_a ? a_tx * ((a_rows + mmmcu::kK1Rows - 1) / mmmcu::kK1Rows) : 0;
   const int64_t b_tx = (ctx->ldb + mmmcu::kK1Cols - 1) / mmmcu::kK1Cols;
   const int64_t nB = do_b ? b_tx * ((ctx->Kb + 31) / 32) : 0;
@@ -318,7 +336,8 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   z.tile_prefix = do_a ? ctx->tile_prefix.as<int64_t>() : nullptr;
   z.bpop = b_valid ? zb_bpop(ctx) : nullptr;
   z.bnz = b_valid ? zb_bnz(ctx) : nullptr;
-  z.btot = b_valid ? zb_slice(ctx) : ctx->stats.as<unsigned long long>() + 12;
+  z.btot = b_valid ? zb_slice(ctx) : ctx->stats.as<unsigned long long>() + 16;
+  z.amax = a_valid ? za_amax(ctx) : nullptr;
   z.done = ctx->ctl.as<unsigned int>();
   z.next_tile = ctx->ctl.as<unsigned int>() + 1;
   z.at = tc_a ? ctx->at.as<float>() : nullptr;
@@ -484,15 +503,48 @@ mmmcu_status launch_simt(mmmcu_ctx* ctx, float* C, int64_t ldc, int span_hint, i
 }
 
 // K2-TC over the dense-tile operands (sel: device-side path choice, nullptr = forced).
-mmmcu_status launch_tc(mmmcu_ctx* ctx, float* C, int64_t ldc, const unsigned long long* sel) {
+template <bool F16>
+mmmcu_status launch_tc_t(mmmcu_ctx* ctx, float* C, int64_t ldc, const unsigned long long* sel) {
   const int64_t row_tiles = ctx->m_at / mmmcu::kTdTM;
-  MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, mmmcu::kTdSmem));
+  constexpr int smem = mmmcu::td_smem<F16>();
+  MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k2_tc<F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   if (ctx->num_sms == 0) MMMCU_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
   const int64_t ntiles = row_tiles * ctx->n_tc;
   const unsigned grid = (unsigned)std::min<int64_t>(ntiles, ctx->num_sms);
-  mmmcu::k2_tc<<<grid, mmmcu::kTdThreads, mmmcu::kTdSmem, ctx->stream>>>(
+  if (F16) {  // CTA pairs: clusters of 2, one pair per two SMs, a pair tile = 256 rows
+    const int64_t units = ((row_tiles + 1) / 2) * ctx->n_tc;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2u);
+    cfg.blockDim = dim3(mmmcu::kTdThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    // persistent: exactly as many pairs as can be co-resident (not every SM can pair up with
+    // a TPC neighbour: a second wave of pairs would double the kernel time)
+    if (ctx->tc_pairs == 0) {
+      cfg.gridDim = dim3(2u * (unsigned)(ctx->num_sms / 2));
+      int nc = 0;
+      MMMCU_CUDA(cudaOccupancyMaxActiveClusters(&nc, mmmcu::k2_tc<F16>, &cfg));
+      ctx->tc_pairs = nc > 0 ? nc : 1;
+      if (getenv("MMMCU_VERBOSE")) fprintf(stderr, "mmmcu: K2-TC co-resident pairs %d (SMs %d)\n", nc, ctx->num_sms);
+    }
+    cfg.gridDim = dim3(2u * (unsigned)std::min<int64_t>(units, ctx->tc_pairs));
+    MMMCU_CUDA(cudaLaunchKernelEx(&cfg, mmmcu::k2_tc<F16>, (const float*)ctx->at.as<float>(), ctx->kpad,
+                                  (const float*)ctx->tcb.as<float>(), (const int32_t*)ctx->tck.as<int32_t>(),
+                                  (const int32_t*)ctx->tcn.as<int32_t>(), (int64_t)ctx->tc_steps, C, ldc, ctx->M,
+                                  ctx->N, row_tiles, ctx->n_tc, sel, (const uint32_t*)za_amax(ctx),
+                                  (const unsigned long long*)(zb_slice(ctx) + 4)));
+    return MMMCU_OK;
+  }
+  mmmcu::k2_tc<F16><<<grid, mmmcu::kTdThreads, smem, ctx->stream>>>(
       ctx->at.as<float>(), ctx->kpad, ctx->tcb.as<float>(), ctx->tck.as<int32_t>(), ctx->tcn.as<int32_t>(),
-      ctx->tc_steps, C, ldc, ctx->M, ctx->N, row_tiles, ctx->n_tc, sel);
+      ctx->tc_steps, C, ldc, ctx->M, ctx->N, row_tiles, ctx->n_tc, sel, za_amax(ctx), zb_slice(ctx) + 4);
   MMMCU_LAUNCHED();
 #ifdef TD_PROF
   {  // debug builds: rerun with the per-CTA cycle counters on, print their means
@@ -500,9 +552,9 @@ mmmcu_status launch_tc(mmmcu_ctx* ctx, float* C, int64_t ldc, const unsigned lon
     if (!dbuf) cudaMalloc(&dbuf, 16 * 8 * 1024);
     cudaMemset(dbuf, 0, 16 * 8 * 1024);
     cudaMemcpyToSymbol(mmmcu::td_prof, &dbuf, sizeof(dbuf));
-    mmmcu::k2_tc<<<grid, mmmcu::kTdThreads, mmmcu::kTdSmem, ctx->stream>>>(
+    mmmcu::k2_tc<F16><<<grid, mmmcu::kTdThreads, smem, ctx->stream>>>(
         ctx->at.as<float>(), ctx->kpad, ctx->tcb.as<float>(), ctx->tck.as<int32_t>(), ctx->tcn.as<int32_t>(),
-        ctx->tc_steps, C, ldc, ctx->M, ctx->N, row_tiles, ctx->n_tc, sel);
+        ctx->tc_steps, C, ldc, ctx->M, ctx->N, row_tiles, ctx->n_tc, sel, za_amax(ctx), zb_slice(ctx) + 4);
     cudaDeviceSynchronize();
     std::vector<unsigned long long> h(16 * grid);
     cudaMemcpy(h.data(), dbuf, 8 * 16 * grid, cudaMemcpyDeviceToHost);
@@ -519,6 +571,9 @@ mmmcu_status launch_tc(mmmcu_ctx* ctx, float* C, int64_t ldc, const unsigned lon
 #endif
 
   return MMMCU_OK;
+}
+mmmcu_status launch_tc(mmmcu_ctx* ctx, float* C, int64_t ldc, const unsigned long long* sel) {
+  return tc_f16(ctx) ? launch_tc_t<true>(ctx, C, ldc, sel) : launch_tc_t<false>(ctx, C, ldc, sel);
 }
 
 mmmcu_status read_stats(mmmcu_ctx* ctx, unsigned long long* host16) {
@@ -750,7 +805,7 @@ mmmcu_status mmmcu_export_ablock_index(mmmcu_ctx* ctx, int64_t block_dim, uint8_
 
 mmmcu_status mmmcu_set_algo(mmmcu_ctx* ctx, mmmcu_algo algo) {
   MMMCU_TRY(bind(ctx));
-  if (algo < MMMCU_ALGO_AUTO || algo > MMMCU_ALGO_TC)
+  if (algo < MMMCU_ALGO_AUTO || algo > MMMCU_ALGO_TC32)
     return fail(ctx, MMMCU_ERR_INVALID_ARG, "unknown algorithm");
   ctx->algo = algo;
   return MMMCU_OK;
@@ -785,11 +840,11 @@ mmmcu_status mmmcu_multiply(mmmcu_ctx* ctx, float* C, int64_t ldc, const float* 
     ctx->auto_pending = true;
     MMMCU_TRY(launch_simt(ctx, C, ldc, 0, 7));
     MMMCU_TRY(launch_tc(ctx, C, ldc, ctx->stats.as<unsigned long long>() + 7));
-  } else if (ctx->algo == MMMCU_ALGO_TC) {
+  } else if (ctx->algo == MMMCU_ALGO_TC || ctx->algo == MMMCU_ALGO_TC32) {
     if (!ctx->op_at || !ctx->op_tcb)
       return fail(ctx, MMMCU_ERR_NOT_READY, "the TC operands were not built: preprocess with algo TC");
-    ctx->last_algo = MMMCU_ALGO_TC;
-    if (!ctx->tcb_fresh) {
+    ctx->last_algo = ctx->algo;
+    if (!ctx->tcb_fresh || ctx->tcb_f16 != tc_f16(ctx)) {
       MMMCU_TRY(pack_tc(ctx));
       ctx->tcb_fresh = true;
     }

@@ -3,6 +3,7 @@
 // the CUTLASS cute/arch/mma_sm100_desc.hpp definitions vendored in this image).
 #pragma once
 #include <cstdint>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 namespace mmmcu {
@@ -152,6 +153,95 @@ __device__ __forceinline__ void split_tf32(float v, uint32_t& hi, uint32_t& lo) 
   const uint32_t b = __float_as_uint(v);
   hi = b & 0xFFFFE000u;
   lo = __float_as_uint(v - __uint_as_float(hi));
+}
+
+// ------------------------------------------------------- CTA pairs (cta_group::2)
+// A cluster of 2 CTAs on one TPC: the leader (rank 0) issues M=256 MMAs whose A rows and D
+// accumulators are split 128 / 128 between the two CTAs' TMEM and whose B columns are split
+// N/2 / N/2 between their shared memories.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Arrive on the mbarrier at the same smem offset in CTA `rank` (default .release.cta
+// semantics, as CUTLASS's ClusterBarrier: a .cluster-scope release compiles to
+// MEMBAR.ALL.GPU and its acquire to CCTL.IVALL, measured 1.7x slower per stage; what the
+// MMA reads — TMEM and async-proxy smem — is ordered by the tcgen05 fences and the
+// barrier's own completion, not by generic-proxy memory ordering).
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(r) : "memory");
+}
+__device__ __forceinline__ void tmem_alloc2(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "r"(ncols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_dealloc2(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
+}
+__device__ __forceinline__ void mma_f16_ts_pair(uint32_t d_taddr, uint32_t a_taddr, uint64_t b_desc, uint32_t idesc,
+                                                uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_taddr),
+      "r"(a_taddr), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Arrive on the mbarrier at this smem offset in both CTAs of the pair once the MMAs issued so
+// far complete.
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+// ---------------------------------------------------------------- fp16 split (kind::f16)
+// Instruction descriptor, kind::f16: D f32, A / B f16 (format 0), both K-major, M = 128.
+__host__ __device__ constexpr uint32_t idesc_f16_m128(uint32_t n) {
+  return (1u << 4) | (0u << 7) | (0u << 10) | ((n >> 3) << 17) | ((128u >> 4) << 24);
+}
+// M = 256 (cta_group::2: 128 rows per CTA of the pair)
+__host__ __device__ constexpr uint32_t idesc_f16_m256(uint32_t n) {
+  return (1u << 4) | (0u << 7) | (0u << 10) | ((n >> 3) << 17) | ((256u >> 4) << 24);
+}
+__device__ __forceinline__ void mma_f16_ts(uint32_t d_taddr, uint32_t a_taddr, uint64_t b_desc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_taddr),
+      "r"(a_taddr), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Power-of-two operand scale of the fp16 split: max|x| * 2^s lands in [2^14, 2^15), so the
+// hi parts use fp16's whole range and the lo parts (|lo| <= 2^-11 |hi|) stay normal for all
+// values within 2^17 of the maximum; s is clamped to [-100, 100] (AUTO keeps operands whose
+// maximum lies outside that range off the fp16 path).  maxbits = bits of max|x| (0: 2^0).
+__host__ __device__ inline int f16_scale_exp(uint32_t maxbits) {
+  if (maxbits == 0u) return 0;
+  int s = 14 - ((int)(maxbits >> 23) - 127);
+  return s < -100 ? -100 : (s > 100 ? 100 : s);
+}
+__device__ __forceinline__ float exp2_int(int s) { return __uint_as_float((uint32_t)(127 + s) << 23); }
+// fp16 split of two fp32 values (already scaled): hi = fp16(x), lo = fp16(x - hi) (x - hi is
+// exact in fp32), packed k-pairs as the UMMA operands read them (even k in the low half).
+__device__ __forceinline__ void split_f16x2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  uint32_t h;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(x1), "f"(x0));
+  const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&h));
+  uint32_t l;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(x1 - hf.y), "f"(x0 - hf.x));
+  hi = h;
+  lo = l;
 }
 
 // n-th (0-based) set bit of a 32-bit mask (mask must have > n set bits).

@@ -375,15 +375,45 @@ def test_device_generator_matches_oracle(ctx):
 @pytest.mark.parametrize("M,K,N_,zA,zB,bw", [(1024, 1024, 1024, 0.8, 0.8, 16), (100, 77, 130, 0.6, 0.6, 8),
                                             (257, 1000, 600, 0.0, 0.0, 16), (4096, 4096, 4096, 0.6, 0.6, 32),
                                             (4096, 4096, 4096, 0.95, 0.95, 8), (129, 65, 257, 1.0, 0.5, 16)])
-def test_tc_tolerance(ctx, M, K, N_, zA, zB, bw):
+@pytest.mark.parametrize("algo", [N.ALGO_TC, N.ALGO_TC32])
+def test_tc_tolerance(ctx, M, K, N_, zA, zB, bw, algo):
     # north_star: |C_gpu - C_ref| <= 1e-5 * Σ_k |a_ik||b_kj| (fp64 denominator); exact counters
+    # (ALGO_TC: fp16 split with power-of-two operand scales; ALGO_TC32: 3xTF32)
     A, B = gen_pair(21, M, K, N_, zA, zB, bw)
-    C, cnt = run_gpu(ctx, A, B, algo=N.ALGO_TC, N_=N_)
+    C, cnt = run_gpu(ctx, A, B, algo=algo, N_=N_)
     Cr, ocnt = run_oracle(A, B)
     bad, worst = o.check_tolerance(C, Cr, np.ascontiguousarray(A[:, :K]), B, tol=TOL)
     assert bad == 0, worst
     assert worst < 0.5 * TOL  # margin: typical worst ~4e-6 at dA = dB = 0.4
     assert (C[:, N_:] == 0).all()
+    assert_counters(cnt, ocnt)
+
+
+@pytest.mark.parametrize("sa,sb", [(1e6, 1e-8), (3e-20, 2e15), (65504.0, 65504.0), (1.0, 0.02)])
+def test_tc_f16_scaled_operands(ctx, sa, sb):
+    # the fp16 split scales each operand by a power of two (max|x| -> [2^14, 2^15)): operands
+    # far outside fp16's range stay within the tolerance
+    M, K, N_ = 384, 1024, 384
+    A, B = gen_pair(23, M, K, N_, 0.6, 0.7, 16)
+    A = (A * np.float32(sa)).astype(np.float32)
+    B = (B * np.float32(sb)).astype(np.float32)
+    C, cnt = run_gpu(ctx, A, B, algo=N.ALGO_TC, N_=N_)
+    Cr, ocnt = run_oracle(A, B)
+    bad, worst = o.check_tolerance(C, Cr, np.ascontiguousarray(A[:, :K]), B, tol=TOL)
+    assert bad == 0, worst
+    assert worst < 0.5 * TOL, worst
+    assert_counters(cnt, ocnt)
+
+
+def test_auto_range_guard(ctx):
+    # an operand maximum outside the fp16 split's scale range (max exponent > 114) keeps AUTO on the
+    # exact K2-SIMT path
+    A, B = gen_pair(24, 512, 512, 512, 0.6, 0.6, 16)
+    A = (A * np.float32(2.0 ** 116)).astype(np.float32)  # max|A| in [2^115, 2^116)
+    Cr, ocnt = run_oracle(A, B)
+    C, cnt = run_gpu(ctx, A, B, algo=N.ALGO_AUTO)
+    assert ctx.last_algo() in (N.ALGO_SIMT_SPAN8, N.ALGO_SIMT_SPAN16)
+    assert bitexact(C, Cr)
     assert_counters(cnt, ocnt)
 
 
