@@ -1,31 +1,46 @@
-// K2-TC — dense-tile masked GEMM on the 5th-generation tensor cores (tcgen05, kind::tf32,
-// 3xTF32 split), for cells whose masks leave the 128 x 192 C tiles dense enough to pay
-// (BASELINE north_star: "tensor cores only for tiles that the masks leave dense enough ...
-// and only if the result stays inside tolerance").
+// K2-TC — dense-tile masked GEMM on the 5th-generation tensor cores (tcgen05), for cells whose
+// masks leave the 128 x 192 C tiles dense enough to pay (BASELINE north_star: "tensor cores
+// only for tiles that the masks leave dense enough ... and only if the result stays inside
+// tolerance").
 //
-// Work unit: a 128-row x 192-column C tile (persistent CTAs, see below).  The k loop runs only over the
-// tile's LIVE k (B[k, tile] has a non-zero, from K1's tlive masks), 8 per MMA step, so B's
-// block sparsity removes whole k-steps; A's element zeros are multiplied (the tile is dense
-// enough by the choice of this path).  Per step:
-//   B: one 24 KB bulk copy of two K1-packed 8-k step images (tf32 hi / lo, UMMA K-major);
-//   A: the 4 transform warps load the step's 8 live rows of the K1 A^T tile
-//      (at[(rt*kpad + k)*128 + i], coalesced, 2 stages ahead), split them into tf32 hi / lo
-//      and store them to TMEM (lane = row, column = k) — per-k TMA copies of 512 B cost
-//      more TMA issue slots than the MMAs leave (measured: 0.92 vs 0.62 ms, 4096^3);
-//   one thread issues, per 8 k, D += A_lo*B_hi + A_hi*B_lo + A_hi*B_hi (M=128, N=192, K=8).
+// Work unit: a C tile of 192 columns (persistent CTAs).  The k loop runs only over the tile's
+// LIVE k (B[k, tile] has a non-zero, from K1's tlive masks), so B's block sparsity removes
+// whole k steps; A's element zeros are multiplied (the tile is dense enough by the choice of
+// this path).  Two operand precisions:
+//   fp16 split (MMMCU_ALGO_TC, AUTO): x = hi + lo with hi = fp16(x * 2^s), lo = fp16(x * 2^s -
+//     hi), s a power-of-two scale per operand from K1's max|A| / max|B| (tc::f16_scale_exp);
+//     kind::f16 MMAs of K = 16, and CTA pairs (cta_group::2): a pair tile is 256 rows, each
+//     CTA holds its 128 A rows (TMEM) and D rows, and HALF of B's 192 columns in its shared
+//     memory — the leader CTA issues M=256 MMAs that read both halves, so each SM fetches
+//     half of B.
+//   tf32 split (MMMCU_ALGO_TC32): hi = top 19 bits, lo = x - hi; kind::tf32 MMAs of K = 8,
+//     one CTA per 128-row tile.
+// Per 16 (8) live k: D += A_lo*B_hi + A_hi*B_lo + A_hi*B_hi (3 MMAs, N = 192).
 //
-// Accuracy: the tensor core's fp32 accumulation truncates at every MMA, an error that grows
-// with the number of MMAs into one accumulator (measured worst 6.7e-6 * Σ|a||b| with 512
-// steps into one D at 4096^3, against the 1e-5 tolerance; 0.9e-6 with 64-step segments,
-// 0.7e-6 with 32).  So the k loop is cut into 512-k segments accumulated in two
-// alternating TMEM accumulators D0 / D1: while the MMAs fill one, the 4 accumulator warps
-// add the other into the tile's fp32 partial P in shared memory (round-to-nearest adds),
-// so the tensor pipe never waits for a drain.  At the end C = C0 + P, coalesced.
+// Pipelines (the measured limit is how many operand bytes are in flight, not the tensor
+// pipe: with a 4-stage ring the transform waited on data 36% of the time, so the fp32
+// partial P moved from shared memory into TMEM to make room for a 7-stage ring):
+//   smem ring (kStages): per stage the B step images of 32 (16) live k and the A^T rows of
+//     those k (fp32, K1's at[(rt*kpad + k)*128 + i]).  The producer warp fills it with bulk
+//     copies (B; A runs of consecutive live k on dense tiles) or cp.async rows (A on sparse
+//     tiles).  `tma[s]` = landed; `empty[s]` = the transform read A (4 arrivals) and the
+//     stage's MMAs completed (1 tcgen05.commit).
+//   TMEM A slots (kSlots): the transform warps split the stage's A values into hi / lo and
+//     store them into slot J % kSlots (lane = row), after the slot's previous MMAs completed
+//     (the empty phase of stage J - kSlots); `full[t]` tells the MMA issuer.
+//   accumulation segments: the tensor core truncates its fp32 accumulation at every MMA, an
+//     error that grows with the MMAs accumulated into one D (measured worst 6.7e-6 *
+//     Σ|a||b| with 512 tf32 steps, 0.9e-6 with 64).  So k is cut into segments of 64 MMA
+//     steps (1024 k fp16, 512 k tf32); after each, the accumulator warps add D (unscaled by
+//     2^-(sA+sB) for fp16) into the tile's fp32 partial P in TMEM with round-to-nearest adds
+//     (`seg_full` -> `seg_empty`; the MMAs of the next segment wait for the drain, ~5% of a
+//     segment).  At the end C = C0 + P, transposed through shared memory so that C is read
+//     and written in coalesced 128-byte rows.
 //
-// Warp roles (320 threads): 0-3 A transform, 4-7 accumulators (segment drain + C update),
-// 8 TMA producer, 9 MMA issuer.  TMEM (512
-// columns): D0 [0,192), D1 [192,384), 4 A slots [384,512) of 32 columns (2 x (hi 8 | lo 8)),
-// one per stage.
+// Warp roles (480 threads): 0-7 A transform, 8-11 accumulators, 12 and 14 producers (even /
+// odd stages), 13 MMA issuer (the pair leader's; the follower's warp 13 idles).  TMEM (512 columns): D [0,192), P [192,384),
+// 4 A slots [384,512) of 32 columns (per MMA step: hi 8 | lo 8 columns; fp16 packs 2 k per
+// column, even k in the low half).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -43,47 +58,41 @@ __device__ unsigned long long* td_prof = nullptr;  // debug builds only: per-CTA
 #define TD_ADD(i, x)
 #endif
 
-#ifndef TD_STAGES
-#define TD_STAGES 4
-#endif
-#ifndef TD_STAGES16
-#define TD_STAGES16 4
-#endif
 #ifndef TD_TN
 #define TD_TN 192
 #endif
 constexpr int kTdTN = TD_TN;
 constexpr int kTdStepFloats = kTdTN * 8 * 2;  // one K1 step image (8 k tf32 or 16 k fp16): hi | lo, 12 KB
-// Operand precision of K2-TC: tf32 split (kind::tf32, 8 k per MMA) or fp16 split
-// (kind::f16, 16 k per MMA at the same cycles per MMA: half the tensor time per k; operands
-// scaled by powers of two so that fp16's 5-bit exponent holds them, see tc::f16_scale_exp).
+constexpr int kTdThreads = 480;  // warps 0-7 transform, 8-11 accumulators, 12 / 14 producers, 13 MMA
+constexpr int kTdTM = 128;
+constexpr int kTdSlots = 4;                   // TMEM A slots of 32 columns
+constexpr int kTdXrow = 36;                   // C-update staging row stride (floats): 16-byte aligned rows,
+                                              // conflict-free 16-byte stores by row-owning threads
+
 template <bool F16>
 struct TdCfg {
-  static constexpr bool kPair = F16;                             // fp16: CTA pairs (cta_group::2, M=256)
-  static constexpr int kStages = F16 ? TD_STAGES16 : TD_STAGES;  // B smem + A TMEM slot per stage
-  static constexpr int kSub = 2;                                 // MMA sub-steps (3 MMAs each) per stage
-  static constexpr int kStepK = F16 ? 16 : 8;                    // k per MMA sub-step (one K1 step image)
-  static constexpr int kStageK = kStepK * kSub;                  // live k per stage: 16 / 32
-  static constexpr int kSeg = 512 / kStageK;                     // stages per 512-k accumulation segment
+  static constexpr bool kPair = F16;                  // fp16: CTA pairs (cta_group::2, M=256)
+  static constexpr int kSub = 2;                      // MMA steps (3 MMAs each) per stage
+  static constexpr int kStepK = F16 ? 16 : 8;         // k per MMA step (one K1 step image)
+  static constexpr int kStageK = kStepK * kSub;       // live k per stage: 32 / 16
+  static constexpr int kSeg = 32;                     // stages per accumulation segment (64 MMA steps)
   // B smem per stage: kSub step images, of which a pair CTA holds its N/2 columns
   static constexpr int kBStageFloats = kSub * kTdStepFloats / (kPair ? 2 : 1);
+  static constexpr int kStages = F16 ? 6 : 5;          // smem ring
+  static_assert(kStages > kTdSlots, "the smem ring must run ahead of the TMEM slots");
 };
-constexpr int kTdSub = 2;
-constexpr int kTdThreads = 320; // warps 0-3 transform, 4-7 accumulators, 8 producer, 9 MMA
-constexpr int kTdTM = 128;
-constexpr int kTdPStride = kTdTN + 4;         // staged P row stride (floats): conflict-free 16-byte accesses
 
 template <bool F16>
 struct TdShared {
   using Cfg = TdCfg<F16>;
-  float b[Cfg::kStages][Cfg::kBStageFloats];         // B step images (pair: this CTA's half)
-  float a[Cfg::kStages][Cfg::kStageK][kTdTM];         // the stage's live A^T rows (8 / 16 KB)
-  float p[kTdTM][kTdPStride];                         // the tile's fp32 partial P (98 KB)
-  uint64_t tma[Cfg::kStages];     // the stage's B image and A rows landed (TMA bytes)
-  uint64_t full[Cfg::kStages];    // stage ready: A split into its TMEM slot (4 transform warps)
-  uint64_t empty[Cfg::kStages];   // stage consumed: one tcgen05.commit frees B / A smem and the A slot
-  uint64_t seg_full[2];           // segment's last MMAs done (tcgen05.commit)
-  uint64_t seg_empty[2];          // D drained (4 accumulator warps)
+  float b[Cfg::kStages][Cfg::kBStageFloats];   // B step images (pair: this CTA's half)
+  float a[Cfg::kStages][Cfg::kStageK][kTdTM];  // the stage's live A^T rows
+  float xp[4][2][32][kTdXrow];                 // per accumulator warp: C-update staging, 2 buffers
+  uint64_t tma[Cfg::kStages];    // stage data landed (TMA bytes / cp.async arrivals)
+  uint64_t empty[Cfg::kStages];  // stage consumed: 8 transform arrivals + 1 tcgen05.commit
+  uint64_t full[kTdSlots];       // A slot written (transform warps; pair: both CTAs')
+  uint64_t seg_full;             // segment's MMAs done (tcgen05.commit)
+  uint64_t seg_empty;            // D drained into P (accumulator warps; pair: both CTAs')
   uint32_t tmem_base;
 };
 template <bool F16>
@@ -99,21 +108,17 @@ __device__ __forceinline__ void td_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-// A tile whose B columns leave >= 3/4 of k live gets its A rows by TMA (runs of consecutive
-// live k: ~1 copy per stage); sparser tiles would need up to 16 copies of 512 B per stage,
-// more TMA time than the MMAs leave, so their A rows come through the transform warps' loads.
+// A tile whose B columns leave >= 3/4 of k live gets its A rows by bulk copies (runs of
+// consecutive live k: ~1 copy per stage); sparser tiles have short runs, and per-run copies
+// would cost more TMA time than the MMAs leave, so their rows come by cp.async.
 __device__ __forceinline__ bool td_dense(int32_t live, int64_t kpad) { return 4 * (int64_t)live >= 3 * kpad; }
 
-__device__ __forceinline__ void td_named_sync(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
-// Persistent: CTA b takes tiles t = b, b + gridDim.x, ...; tile t = (row tile t % m_tiles,
-// column tile t / m_tiles), so the CTAs running together share B column tiles (L2 reuse).
-// Every role walks the same tile sequence with running stage / slot / segment counters, so
-// the producer and the transform warps run into the next tile while the accumulator warps
-// update C for the previous one.  F16: amax / bmax hold the bits of max|A| / max|B| (K1),
-// from which the power-of-two operand scales and the epilogue's unscale follow.
+// Persistent: CTA (pair) u takes work units t = u, u + #units, ...; unit t = (row tile (pair)
+// t % m_units, column tile t / m_units), so the CTAs running together share B column tiles
+// (L2 reuse).  Every role walks the same unit sequence with running stage / slot / segment
+// counters, so the producer and the transform warps run into the next tile while the
+// accumulator warps update C for the previous one.  F16: amax / bmax hold the bits of max|A|
+// / max|B| (K1), from which the operand scales and the epilogue's unscale follow.
 template <bool F16>
 __global__ void __launch_bounds__(kTdThreads, 1)
 k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb, const int32_t* __restrict__ tck,
@@ -124,7 +129,8 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
   constexpr int kStages = Cfg::kStages, kSub = Cfg::kSub, kStepK = Cfg::kStepK, kStageK = Cfg::kStageK,
                 kSeg = Cfg::kSeg;
   constexpr bool kPair = Cfg::kPair;
-  constexpr int kNArrive = kPair ? 8 : 4;  // transform / accumulator warps signalling the MMA issuer
+  constexpr int kNAccum = kPair ? 8 : 4;    // accumulator warps signalling the MMA issuer (seg_empty)
+  constexpr int kNXform = kPair ? 16 : 8;   // transform warps signalling the MMA issuer (full)
   // (sel is read by both CTAs of a pair: both exit, or neither)
   if (sel && *sel != 32ull) return;  // device-side path choice (k1_finalize): 32 = TC
   extern __shared__ __align__(128) uint8_t td_raw[];
@@ -137,6 +143,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
   const int64_t m_units = kPair ? (m_tiles + 1) / 2 : m_tiles;  // (pair) row tiles per column tile
   const int64_t ntiles = m_units * n_tiles;
   auto row_tile = [&](int64_t t) { return kPair ? 2 * (t % m_units) + rank : t % m_units; };
+  auto nsteps_of = [&](int32_t total) { return (total + kStepK - 1) / kStepK; };
   // a signal for the MMA issuer: local arrive, or (pair follower) remote arrive on the leader
   auto signal_issuer = [&](uint64_t* bar) {
     if (!kPair || leader) tc::mbar_arrive(bar);
@@ -146,13 +153,11 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(&sh.tma[s], 1);
-      tc::mbar_init(&sh.full[s], kNArrive);
-      tc::mbar_init(&sh.empty[s], 1);
+      tc::mbar_init(&sh.empty[s], 1 + 8);
     }
-    for (int d = 0; d < 2; ++d) {
-      tc::mbar_init(&sh.seg_full[d], 1);
-      tc::mbar_init(&sh.seg_empty[d], kNArrive);
-    }
+    for (int t = 0; t < kTdSlots; ++t) tc::mbar_init(&sh.full[t], kNXform);
+    tc::mbar_init(&sh.seg_full, 1);
+    tc::mbar_init(&sh.seg_empty, kNAccum);
     tc::fence_mbar_init();
   }
   if (warp == 0) {
@@ -164,46 +169,62 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
   else __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = sh.tmem_base;
-  constexpr uint32_t kAcol = 2 * kTdTN;  // TMEM columns of the A slots
-  auto nsteps_of = [&](int32_t total) { return (total + kStepK - 1) / kStepK; };
+  constexpr uint32_t kPcol = kTdTN, kAcol = 2 * kTdTN;  // TMEM columns of P and of the A slots
 
-  if (warp == 8) {
-    // ---------------------------------------------------- producer (B and A per stage)
-    // Per stage: one bulk copy of the stage's B step images, and the stage's live A^T rows of
-    // the tile.  Dense tiles: one bulk copy per run of consecutive live k (1 copy of 8 / 16
-    // KB).  Sparse tiles (short runs: per-run TMA copies would cost more TMA time than the
-    // MMAs leave): the warp copies each live row with one 16-byte cp.async per lane
-    // (LDGSTS, 512 B per instruction), tracked by the same barrier (cp.async.mbarrier.arrive,
-    // issued before the expect_tx arrive so the phase cannot complete early).  Lane
-    // e < kStageK holds live k number e of the stage (prefetched a stage ahead).
+  if (warp == 12 || warp == 14) {
+    // ---------------------------------------------------- producers (B and A per stage)
+    // Two warps, producer p = (warp - 12) / 2 fills the stages J with J % 2 == p (one warp's
+    // per-stage instruction chain, ~760 cycles, was longer than the stage's 630 MMA cycles).
+    // Per stage: one bulk copy of the stage's B step images, and the stage's live A^T rows.
+    // Dense tiles: one bulk copy per run of consecutive live k.  Sparse tiles: each live row
+    // by the warp, one 16-byte cp.async per lane (LDGSTS, 512 B per instruction), tracked by
+    // the same barrier (cp.async.mbarrier.arrive, issued before the expect_tx arrive so the
+    // phase cannot complete early).  Lane e < kStageK holds live k number e of the stage;
+    // the list is loaded 4 stages ahead (register shift chain).
     uint32_t J = 0;
+#ifdef TD_PROF
+    long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const long long p0 = clock64();
+#endif
+    const uint32_t pp = (uint32_t)(warp - 12) >> 1;
     for (int64_t t = unit0; t < ntiles; t += nunits) {
       const int64_t rt = row_tile(t), tb = t / m_units;
       const int32_t total = tcn[tb];
       const int nsteps = nsteps_of(total);
       const int nstage = (nsteps + kSub - 1) / kSub;
-      const bool a_tma = td_dense(total, kpad);  // else A rows by cp.async
+      const bool a_tma = td_dense(total, kpad);
       // pair: the tile's step images are stored per column half (K1 pack), this CTA's half
       // of a stage is one contiguous copy
-      const float* bsrc = kPair ? tcb + (tb * 2 + rank) * maxsteps * (kTdStepFloats / 2)
-                                : tcb + tb * maxsteps * kTdStepFloats;
       constexpr int kStepCopy = kPair ? kTdStepFloats / 2 : kTdStepFloats;  // floats per step in this CTA
+      const float* bsrc = tcb + (kPair ? (tb * 2 + rank) : tb) * maxsteps * kStepCopy;
       const int32_t* kx = tck + tb * maxsteps * 8;
       const float* atile = AT + rt * kpad * 128;
       const int npos = nsteps * kStepK;
-      int kc = (lane < kStageK && lane < npos) ? __ldg(kx + lane) : -1;
-      for (int j = 0; j < nstage; ++j, ++J) {
-        const int st = J % kStages;
-        const int pn = (j + 1) * kStageK + lane;
-        const int kn = (lane < kStageK && pn < npos) ? __ldg(kx + pn) : -1;
+      auto kload = [&](int jj) {
+        const int pn = jj * kStageK + lane;
+        return (lane < kStageK && pn < npos) ? __ldg(kx + pn) : -1;
+      };
+      // this producer's stages of the tile: j0, j0 + 2, ... (J advances by the tile's count)
+      const int j0 = (int)((pp + 2u - (J & 1u)) & 1u);
+      int kc = kload(j0), k1 = kload(j0 + 2), k2 = kload(j0 + 4), k3 = kload(j0 + 6);
+      for (int j = j0; j < nstage; j += 2) {
+        const uint32_t Jj = J + (uint32_t)j;
+        const int st = Jj % kStages;
+        const int kn = k1;
+        k1 = k2;
+        k2 = k3;
+        k3 = kload(j + 8);
         const int prev = __shfl_up_sync(0xffffffffu, kc, 1);
         const bool valid = a_tma && kc >= 0;
         const bool cont = valid && lane > 0 && prev + 1 == kc;
         const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
         const uint32_t cmask = __ballot_sync(0xffffffffu, cont);
         const uint32_t bytes = (uint32_t)min(kSub, nsteps - kSub * j) * kStepCopy * 4u;
-        if (lane == 0) tc::mbar_wait(&sh.empty[st], ((J / kStages) & 1u) ^ 1u);
+        TD_CLK(q0);
+        if (lane == 0 && Jj >= (uint32_t)kStages) tc::mbar_wait(&sh.empty[st], ((Jj / kStages) & 1u) ^ 1u);
         __syncwarp();
+        TD_CLK(q1);
+        TD_ADD(0, q1 - q0);
         if (!a_tma) {
 #pragma unroll 4
           for (int q = 0; q < kStageK; ++q) {
@@ -227,14 +248,22 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
         }
         kc = kn;
       }
+      J += (uint32_t)nstage;
     }
-  } else if (warp == 9) {
+#ifdef TD_PROF
+    if (lane == 0 && td_prof && warp == 12) {
+      unsigned long long* q = td_prof + 16 * blockIdx.x;
+      q[8] = prof[0];
+      q[9] = clock64() - p0;
+    }
+#endif
+  } else if (warp == 13) {
     if (!leader) goto td_done;  // pair follower: the leader issues the pair's MMAs
     // ------------------------------------------------------------------ MMA issuer
     // The whole warp runs the loop (warp-uniform operands stay in uniform registers); one
-    // elected lane issues.  Each tcgen05.commit costs the tensor pipe ~50 cycles (measured:
-    // 112.6 vs 96.1 cycles per N=192 MMA with a commit every 3), so a stage carries 6 MMAs
-    // and ONE commit that frees both its B smem and its A TMEM slot.
+    // elected lane issues.  Each tcgen05.commit costs the tensor pipe ~50 cycles, so a stage
+    // carries 6 MMAs and ONE commit, which frees its smem (producer) and, through the same
+    // barrier phase, its TMEM A slot (transform).
     const uint32_t idesc = F16 ? tc::idesc_f16_m256(kTdTN) : tc::idesc_tf32_m128(kTdTN);
     uint32_t J = 0, G = 0;
 #ifdef TD_PROF
@@ -246,19 +275,19 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       const int nsteps = nsteps_of(tcn[tb]);
       const int nstage = (nsteps + kSub - 1) / kSub;
       for (int j = 0; j < nstage; ++j, ++J) {
-        const int st = J % kStages;
-        const uint32_t d = G & 1u;
+        const int st = J % kStages, sl = J % kTdSlots;
         TD_CLK(c0);
-        if (j % kSeg == 0 && G >= 2) tc::mbar_wait(&sh.seg_empty[d], ((G - 2) >> 1) & 1u);
+        if (j % kSeg == 0 && G >= 1) tc::mbar_wait(&sh.seg_empty, (G - 1) & 1u);  // D drained
         TD_CLK(c1);
         tc::mbar_wait(&sh.tma[st], (J / kStages) & 1u);
-        tc::mbar_wait(&sh.full[st], (J / kStages) & 1u);
+        TD_CLK(c15);
+        tc::mbar_wait(&sh.full[sl], (J / kTdSlots) & 1u);
         TD_CLK(c2);
         TD_ADD(0, c1 - c0);
         TD_ADD(1, c2 - c1);
+        TD_ADD(3, c15 - c1);
         tc::fence_after_sync();
         const uint32_t baddr = tc::smem_u32(sh.b[st]);
-        const uint32_t dcol = tbase + d * kTdTN;
         const bool seg_end = j % kSeg == kSeg - 1 || j == nstage - 1;
         if (tc::elect_one()) {
 #pragma unroll
@@ -268,25 +297,25 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
               constexpr int kImg = kPair ? kTdTN * 16 : kTdTN * 32;  // bytes of one hi (or lo) image
               const uint32_t bu = baddr + u * 2 * kImg;
               const uint64_t bhi = tc::smem_desc(bu, 128, 256), blo = tc::smem_desc(bu + kImg, 128, 256);
-              const uint32_t ahi = tbase + kAcol + 32 * st + 16 * u, alo = ahi + 8;
+              const uint32_t ahi = tbase + kAcol + 32 * sl + 16 * u, alo = ahi + 8;
               const uint32_t acc0 = (j % kSeg != 0 || u > 0) ? 1u : 0u;
               if (F16) {
-                tc::mma_f16_ts_pair(dcol, alo, bhi, idesc, acc0);
-                tc::mma_f16_ts_pair(dcol, ahi, blo, idesc, 1u);
-                tc::mma_f16_ts_pair(dcol, ahi, bhi, idesc, 1u);
+                tc::mma_f16_ts_pair(tbase, alo, bhi, idesc, acc0);
+                tc::mma_f16_ts_pair(tbase, ahi, blo, idesc, 1u);
+                tc::mma_f16_ts_pair(tbase, ahi, bhi, idesc, 1u);
               } else {
-                tc::mma_tf32_ts(dcol, alo, bhi, idesc, acc0);
-                tc::mma_tf32_ts(dcol, ahi, blo, idesc, 1u);
-                tc::mma_tf32_ts(dcol, ahi, bhi, idesc, 1u);
+                tc::mma_tf32_ts(tbase, alo, bhi, idesc, acc0);
+                tc::mma_tf32_ts(tbase, ahi, blo, idesc, 1u);
+                tc::mma_tf32_ts(tbase, ahi, bhi, idesc, 1u);
               }
             }
           }
           if (kPair) {
             tc::mma_commit_pair(&sh.empty[st]);
-            if (seg_end) tc::mma_commit_pair(&sh.seg_full[d]);
+            if (seg_end) tc::mma_commit_pair(&sh.seg_full);
           } else {
             tc::mma_commit(&sh.empty[st]);
-            if (seg_end) tc::mma_commit(&sh.seg_full[d]);
+            if (seg_end) tc::mma_commit(&sh.seg_full);
           }
         }
         __syncwarp();
@@ -300,71 +329,97 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       unsigned long long* q = td_prof + 16 * blockIdx.x;
       for (int i = 0; i < 3; ++i) q[i] = prof[i];
       q[3] = clock64() - p0;
+      q[10] = prof[3];
     }
 #endif
-  } else if (warp < 4) {
+  } else if (warp < 8) {
     // ---------------------------------------------------------------- A transform
-    // Thread r owns tile row r (== TMEM lane r).  Per stage it waits for the stage's A^T rows
-    // in shared memory (`tma`: the producer's bulk copies or cp.async rows; it also implies
-    // the slot's previous MMAs are done), splits its row's live A values into hi / lo
-    // (tf32: 16 values, one column each; fp16: 32 values scaled by 2^sA, two per column),
-    // stores them with one tcgen05.st of 32 columns into the stage's TMEM slot and signals
-    // the MMA issuer (`full`).
-    const int r = tid;
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    // Warp w owns tile rows 32*(w%4) .. +31 (its TMEM lanes) and MMA step h = w/4 of each
+    // stage (16 live k fp16 / 8 tf32): two warps per SM sub-partition hide each other's
+    // latencies (one warp per row group left the transform the slowest stage of the
+    // pipeline: 630 cycles of work per 630-cycle stage).  Per stage a thread waits for the
+    // stage's A^T rows in shared memory (`tma`), reads its row's values of step h and releases
+    // the smem (`empty`), waits until the MMAs of the slot's previous stage are done (the
+    // `empty` phase of stage J - kSlots, which includes their commit), splits the values into
+    // hi / lo (tf32: one column each; fp16: scaled by 2^sA, two per column), stores them with
+    // one tcgen05.st of 16 columns and signals the MMA issuer (`full`).
+    constexpr int kV = kStepK;  // values per thread per stage
+    const int h = warp >> 2, r = 32 * (warp & 3) + lane;
+    const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
     const float sa = F16 ? tc::exp2_int(tc::f16_scale_exp(*amax)) : 1.0f;
     uint32_t J = 0;
-    auto store_slot = [&](int st, const float (&vals)[kStageK]) {
-      uint32_t v[32];  // slot columns: per sub-step u, hi at 16u .. 16u+7, lo at 16u+8 ..
-#pragma unroll
-      for (int u = 0; u < kSub; ++u) {
-        if (F16) {
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            tc::split_f16x2(vals[16 * u + 2 * e] * sa, vals[16 * u + 2 * e + 1] * sa, v[16 * u + e], v[16 * u + 8 + e]);
-        } else {
-#pragma unroll
-          for (int e = 0; e < 8; ++e) tc::split_tf32(vals[8 * u + e], v[16 * u + e], v[16 * u + 8 + e]);
-        }
-      }
-      tc::fence_after_sync();
-      tc::tmem_st32(tbase + lane_off + kAcol + 32 * st, v);
-      tc::tmem_st_wait();
-      tc::fence_before_sync();
-      __syncwarp();
-      if (lane == 0) signal_issuer(&sh.full[st]);
-    };
+#ifdef TD_PROF
+    long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const long long p0 = clock64();
+#endif
     for (int64_t t = unit0; t < ntiles; t += nunits) {
       const int64_t tb = t / m_units;
       const int32_t total = tcn[tb];
       const int nsteps = nsteps_of(total);
       const int nstage = (nsteps + kSub - 1) / kSub;
       for (int j = 0; j < nstage; ++j, ++J) {
-        const int st = J % kStages;
-        const int nvalid = min(kStageK, total - kStageK * j);
-        tc::mbar_wait(&sh.tma[st], (J / kStages) & 1u);  // implies the slot's MMAs are done
-        float vals[kStageK];
+        const int st = J % kStages, sl = J % kTdSlots;
+        const int nvalid = min(kV, total - kStageK * j - kV * h);  // may be <= 0
+        TD_CLK(q0);
+        tc::mbar_wait(&sh.tma[st], (J / kStages) & 1u);
+        TD_CLK(q1);
+        float vals[kV];
 #pragma unroll
-        for (int q = 0; q < kStageK; ++q) vals[q] = q < nvalid ? sh.a[st][q][r] : 0.0f;
-        store_slot(st, vals);
+        for (int q = 0; q < kV; ++q) vals[q] = q < nvalid ? sh.a[st][kV * h + q][r] : 0.0f;
+        tc::fence_async_smem();  // these generic-proxy reads before the producer's async-proxy refill
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&sh.empty[st]);  // A smem read (the MMA commit completes the phase)
+        uint32_t v[16];  // hi at 0 .. 7, lo at 8 .. 15
+        if (F16) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) tc::split_f16x2_scaled(vals[2 * e], vals[2 * e + 1], sa, v[e], v[8 + e]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) tc::split_tf32(vals[e], v[e], v[8 + e]);
+        }
+        TD_CLK(q15);
+        if (J >= (uint32_t)kTdSlots) {  // the slot's previous MMAs (stage J - kSlots) are done
+          const uint32_t Jp = J - kTdSlots;
+          tc::mbar_wait(&sh.empty[Jp % kStages], (Jp / kStages) & 1u);
+        }
+        TD_CLK(q2);
+        TD_ADD(2, q2 - q15);
+        tc::fence_after_sync();
+        tc::tmem_st16(tbase + lane_off + kAcol + 32 * sl + 16 * h, v);
+        tc::tmem_st_wait();
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) signal_issuer(&sh.full[sl]);
+        TD_CLK(q3);
+        TD_ADD(0, q1 - q0);
+        TD_ADD(1, q3 - q1);
       }
     }
+#ifdef TD_PROF
+    if (tid == 0 && td_prof) {
+      unsigned long long* q = td_prof + 16 * blockIdx.x;
+      q[4] = prof[0];
+      q[5] = prof[1];
+      q[6] = clock64() - p0;
+      q[7] = prof[2];
+    }
+#endif
   } else {
-    // ------------------------------------------------------- accumulator warps 4..7
-    // Thread = tile row r = 32*(w%4) + lane (its TMEM lane).  The tile's fp32 partial P lives
-    // in shared memory (row stride 196 floats: conflict-free 16-byte accesses): each
-    // segment's D (fp16: times 2^-(sA+sB), exact) is added into the row (round-to-nearest;
-    // P = D for the first segment), 16 columns per tcgen05.ld, then D is released.  After
-    // the tile's last segment, C = C0 + P goes out with lanes along the rows (coalesced),
-    // while the MMAs already run the next tile.  Keeping P out of registers leaves the
-    // transform warps the register file (a spilling transform ran sparse tiles 2x slower).
+    // ------------------------------------------------------- accumulator warps 8..11
+    // Thread = tile row r = 32*(w%4) + lane (its TMEM lane).  Per segment: D (fp16: times
+    // 2^-(sA+sB), exact) is added into the partial P in TMEM (round-to-nearest; P = D for
+    // the first segment), 32 columns per tcgen05.ld, then the MMA issuer may start the next
+    // segment.  After the tile's last segment: C += P by bulk reduce-adds
+    // (cp.reduce.async.bulk .add.f32, the L2 performs the fp32 adds, one writer per element):
+    // each thread stages 32 columns of its row in shared memory (double-buffered) and issues
+    // one 128-byte reduce for it, so the warps are free for the next tile's first drain
+    // almost at once (a load-add-store C update held that drain, and with it the MMAs, for
+    // ~25 us per tile).
     const int q4 = warp & 3;
-    const int r = 32 * q4 + lane;
     const uint32_t taddr = tbase + ((uint32_t)(q4 * 32) << 16);
     const float ia = F16 ? tc::exp2_int(-tc::f16_scale_exp(*amax)) : 1.0f;
     const float ib = F16 ? tc::exp2_int(-tc::f16_scale_exp((uint32_t)*bmax)) : 1.0f;
-    float4* prow = reinterpret_cast<float4*>(&sh.p[r][0]);
-    uint32_t G = 0;
+    uint32_t G = 0, R = 0;  // segments drained, C chunks reduced
     for (int64_t t = unit0; t < ntiles; t += nunits) {
       const int64_t rt = row_tile(t), tb = t / m_units;
       const int nsteps = nsteps_of(tcn[tb]);
@@ -372,83 +427,55 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       const int nseg = (nstage + kSeg - 1) / kSeg;
       if (nseg == 0) continue;
       for (int g = 0; g < nseg; ++g, ++G) {
-        const uint32_t d = G & 1u;
-        tc::mbar_wait_sleep(&sh.seg_full[d], (G >> 1) & 1u);
+        tc::mbar_wait_sleep(&sh.seg_full, G & 1u);
         tc::fence_after_sync();
 #pragma unroll 1
-        for (int c = 0; c < kTdTN / 16; ++c) {
-          uint32_t v[16];
-          tc::tmem_ld16(taddr + d * kTdTN + 16 * c, v);
+        for (int c = 0; c < kTdTN / 32; ++c) {
+          uint32_t d[32], p[32];
+          tc::tmem_ld32(taddr + 32 * c, d);
+          if (g > 0) tc::tmem_ld32(taddr + kPcol + 32 * c, p);
           tc::tmem_ld_wait();
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            float4 x = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                                   __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
-            if (F16) {
-              x.x = (x.x * ia) * ib;
-              x.y = (x.y * ia) * ib;
-              x.z = (x.z * ia) * ib;
-              x.w = (x.w * ia) * ib;
-            }
-            if (g > 0) {
-              const float4 y = prow[4 * c + q];
-              x.x = y.x + x.x;
-              x.y = y.y + x.y;
-              x.z = y.z + x.z;
-              x.w = y.w + x.w;
-            }
-            prow[4 * c + q] = x;
+          for (int e = 0; e < 32; ++e) {
+            float x = __uint_as_float(d[e]);
+            if (F16) x = (x * ia) * ib;
+            if (g > 0) x = __uint_as_float(p[e]) + x;
+            d[e] = __float_as_uint(x);
           }
+          tc::tmem_st32(taddr + kPcol + 32 * c, d);
         }
+        tc::tmem_st_wait();
         tc::fence_before_sync();
         __syncwarp();
-        if (lane == 0) signal_issuer(&sh.seg_empty[d]);
+        if (lane == 0) signal_issuer(&sh.seg_empty);
       }
-      const int64_t m0 = rt * kTdTM, n0 = tb * kTdTN;
-      td_named_sync(1, 128);  // every row of P is final
-      // warp q4 updates rows q4, q4+4, ...; per 8 rows all loads go out before the adds
-      const int64_t gc0 = n0 + 4 * lane, gc1 = gc0 + 128;
-      const bool full0 = gc0 + 3 < N, full1 = lane < 16 && gc1 + 3 < N;
+      // C += P: row m0 + lane of this warp, 32 columns per bulk reduce
+      const int64_t row = rt * kTdTM + 32 * q4 + lane, n0 = tb * kTdTN;
+      tc::fence_after_sync();
 #pragma unroll 1
-      for (int i0 = 0; i0 < 32; i0 += 8) {
-        float4 cv[8][2];
+      for (int c = 0; c < kTdTN / 32; ++c, ++R) {
+        float* buf = &sh.xp[q4][R & 1][lane][0];
+        // this thread's reduce from the buffer's previous use (2 chunks ago) has read it
+        if (R >= 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        uint32_t p[32];
+        tc::tmem_ld32(taddr + kPcol + 32 * c, p);
+        tc::tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int64_t row = m0 + q4 + 4 * (i0 + i);
-          const float* crow = C + row * ldc;
-          if (row < M && full0) cv[i][0] = *reinterpret_cast<const float4*>(crow + gc0);
-          if (row < M && full1) cv[i][1] = *reinterpret_cast<const float4*>(crow + gc1);
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<uint4*>(buf + 4 * q) = make_uint4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]);
+        tc::fence_async_smem();  // generic-proxy stores before the bulk (async-proxy) read
+        const int64_t col = n0 + 32 * c;
+        if (row < M && col < N) {
+          const int64_t ncol = N - col < 32 ? ((N - col + 3) & ~int64_t(3)) : 32;  // 16-byte multiple
+          asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(
+                           C + row * ldc + col),
+                       "r"(tc::smem_u32(buf)), "r"((uint32_t)(ncol * 4))
+                       : "memory");
         }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int rr = q4 + 4 * (i0 + i);
-          const int64_t row = m0 + rr;
-          if (row >= M) break;
-          float* crow = C + row * ldc;
-          const float* pr = sh.p[rr];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int col = 4 * lane + 128 * h;
-            if (col >= kTdTN) continue;
-            const int64_t gcol = n0 + col;
-            if (h == 0 ? full0 : full1) {
-              float4 c4 = cv[i][h];
-              const float4 pv = *reinterpret_cast<const float4*>(pr + col);
-              c4.x += pv.x;
-              c4.y += pv.y;
-              c4.z += pv.z;
-              c4.w += pv.w;
-              *reinterpret_cast<float4*>(crow + gcol) = c4;
-            } else {
-#pragma unroll
-              for (int e = 0; e < 4; ++e)
-                if (gcol + e < N) crow[gcol + e] += pr[col + e];
-            }
-          }
-        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
-      td_named_sync(1, 128);  // P may be overwritten by the next tile's first drain
     }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // reduces done before the CTA exits
   }
 td_done:
   tc::fence_before_sync();

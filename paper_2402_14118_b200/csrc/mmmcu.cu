@@ -509,24 +509,20 @@ mmmcu_status launch_tc_t(mmmcu_ctx* ctx, float* C, int64_t ldc, const unsigned l
   constexpr int smem = mmmcu::td_smem<F16>();
   MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k2_tc<F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   if (ctx->num_sms == 0) MMMCU_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
-  const int64_t ntiles = row_tiles * ctx->n_tc;
-  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, ctx->num_sms);
-  if (F16) {  // CTA pairs: clusters of 2, one pair per two SMs, a pair tile = 256 rows
-    const int64_t units = ((row_tiles + 1) / 2) * ctx->n_tc;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2u);
-    cfg.blockDim = dim3(mmmcu::kTdThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = ctx->stream;
-    cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(mmmcu::kTdThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  if (F16) {  // CTA pairs: clusters of 2, a pair tile = 256 rows
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    // persistent: exactly as many pairs as can be co-resident (not every SM can pair up with
-    // a TPC neighbour: a second wave of pairs would double the kernel time)
+    // persistent: exactly as many pairs as can be co-resident (a second wave of pairs would
+    // double the kernel time)
     if (ctx->tc_pairs == 0) {
       cfg.gridDim = dim3(2u * (unsigned)(ctx->num_sms / 2));
       int nc = 0;
@@ -534,42 +530,42 @@ mmmcu_status launch_tc_t(mmmcu_ctx* ctx, float* C, int64_t ldc, const unsigned l
       ctx->tc_pairs = nc > 0 ? nc : 1;
       if (getenv("MMMCU_VERBOSE")) fprintf(stderr, "mmmcu: K2-TC co-resident pairs %d (SMs %d)\n", nc, ctx->num_sms);
     }
+    const int64_t units = ((row_tiles + 1) / 2) * ctx->n_tc;
     cfg.gridDim = dim3(2u * (unsigned)std::min<int64_t>(units, ctx->tc_pairs));
-    MMMCU_CUDA(cudaLaunchKernelEx(&cfg, mmmcu::k2_tc<F16>, (const float*)ctx->at.as<float>(), ctx->kpad,
-                                  (const float*)ctx->tcb.as<float>(), (const int32_t*)ctx->tck.as<int32_t>(),
-                                  (const int32_t*)ctx->tcn.as<int32_t>(), (int64_t)ctx->tc_steps, C, ldc, ctx->M,
-                                  ctx->N, row_tiles, ctx->n_tc, sel, (const uint32_t*)za_amax(ctx),
-                                  (const unsigned long long*)(zb_slice(ctx) + 4)));
-    return MMMCU_OK;
+  } else {
+    cfg.gridDim = dim3((unsigned)std::min<int64_t>(row_tiles * ctx->n_tc, ctx->num_sms));
   }
-  mmmcu::k2_tc<F16><<<grid, mmmcu::kTdThreads, smem, ctx->stream>>>(
-      ctx->at.as<float>(), ctx->kpad, ctx->tcb.as<float>(), ctx->tck.as<int32_t>(), ctx->tcn.as<int32_t>(),
-      ctx->tc_steps, C, ldc, ctx->M, ctx->N, row_tiles, ctx->n_tc, sel, za_amax(ctx), zb_slice(ctx) + 4);
-  MMMCU_LAUNCHED();
+  auto launch = [&]() {
+    return cudaLaunchKernelEx(&cfg, mmmcu::k2_tc<F16>, (const float*)ctx->at.as<float>(), ctx->kpad,
+                              (const float*)ctx->tcb.as<float>(), (const int32_t*)ctx->tck.as<int32_t>(),
+                              (const int32_t*)ctx->tcn.as<int32_t>(), (int64_t)ctx->tc_steps, C, ldc, ctx->M, ctx->N,
+                              row_tiles, ctx->n_tc, sel, (const uint32_t*)za_amax(ctx),
+                              (const unsigned long long*)(zb_slice(ctx) + 4));
+  };
+  MMMCU_CUDA(launch());
 #ifdef TD_PROF
   {  // debug builds: rerun with the per-CTA cycle counters on, print their means
+    const unsigned grid = cfg.gridDim.x;
     static unsigned long long* dbuf = nullptr;
     if (!dbuf) cudaMalloc(&dbuf, 16 * 8 * 1024);
     cudaMemset(dbuf, 0, 16 * 8 * 1024);
     cudaMemcpyToSymbol(mmmcu::td_prof, &dbuf, sizeof(dbuf));
-    mmmcu::k2_tc<F16><<<grid, mmmcu::kTdThreads, smem, ctx->stream>>>(
-        ctx->at.as<float>(), ctx->kpad, ctx->tcb.as<float>(), ctx->tck.as<int32_t>(), ctx->tcn.as<int32_t>(),
-        ctx->tc_steps, C, ldc, ctx->M, ctx->N, row_tiles, ctx->n_tc, sel, za_amax(ctx), zb_slice(ctx) + 4);
+    launch();
     cudaDeviceSynchronize();
     std::vector<unsigned long long> h(16 * grid);
     cudaMemcpy(h.data(), dbuf, 8 * 16 * grid, cudaMemcpyDeviceToHost);
-    double a[16] = {0};
+    double a[16] = {0}, b[16] = {0};
     for (unsigned i = 0; i < grid; ++i)
-      for (int j = 0; j < 16; ++j) a[j] += (double)h[16 * i + j] / grid;
-    fprintf(stderr,
-            "TD_PROF/CTA cycles: MMA wait-seg %.0f wait-full %.0f issue %.0f total %.0f | transform wait-empty %.0f "
-            "batch-copy %.0f total %.0f | producer wait %.0f\n",
-            a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7]);
+      for (int j = 0; j < 16; ++j) (i % 2 == 0 ? a : b)[j] += (double)h[16 * i + j] / (grid / 2);
+    for (double* x : {a, b})
+      fprintf(stderr,
+              "TD_PROF/CTA cycles (%s): MMA wait-seg %.0f wait-tma+full %.0f (tma %.0f) issue %.0f total %.0f | "
+              "transform wait-tma %.0f work %.0f (slot wait %.0f) total %.0f | producer wait-empty %.0f total %.0f\n",
+              x == a ? "even" : "odd", x[0], x[1], x[10], x[2], x[3], x[4], x[5], x[7], x[6], x[8], x[9]);
     void* z = nullptr;
     cudaMemcpyToSymbol(mmmcu::td_prof, &z, sizeof(z));
   }
 #endif
-
   return MMMCU_OK;
 }
 mmmcu_status launch_tc(mmmcu_ctx* ctx, float* C, int64_t ldc, const unsigned long long* sel) {

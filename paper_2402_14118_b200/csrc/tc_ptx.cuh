@@ -39,6 +39,14 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8])
                "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
                : "memory");
 }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
@@ -240,6 +248,28 @@ __device__ __forceinline__ void split_f16x2(float x0, float x1, uint32_t& hi, ui
   const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&h));
   uint32_t l;
   asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(x1 - hf.y), "f"(x0 - hf.x));
+  hi = h;
+  lo = l;
+}
+
+// The same with the operand scale applied (x * s exact for a power of two s): packed fp32x2
+// arithmetic, 6 instructions per pair (FMUL2, F2FP, 2 HADD2.F32, FADD2, F2FP).
+__device__ __forceinline__ void split_f16x2_scaled(float x0, float x1, float s, uint32_t& hi, uint32_t& lo) {
+  float y0, y1;
+  asm("{.reg .b64 a, b, c;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %4};\n\tmul.rn.f32x2 c, a, b;\n\t"
+      "mov.b64 {%0, %1}, c;}"
+      : "=f"(y0), "=f"(y1)
+      : "f"(x0), "f"(x1), "f"(s));
+  uint32_t h;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(y1), "f"(y0));
+  const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&h));
+  float r0, r1;
+  asm("{.reg .b64 a, b, c;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\tsub.rn.f32x2 c, a, b;\n\t"
+      "mov.b64 {%0, %1}, c;}"
+      : "=f"(r0), "=f"(r1)
+      : "f"(y0), "f"(y1), "f"(hf.x), "f"(hf.y));
+  uint32_t l;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(r1), "f"(r0));
   hi = h;
   lo = l;
 }
