@@ -21,7 +21,7 @@
 // pipe: with a 4-stage ring the transform waited on data 36% of the time, so the fp32
 // partial P moved from shared memory into TMEM to make room for a 7-stage ring):
 //   smem ring (kStages): per stage the B step images of 32 (16) live k and the A^T rows of
-//     those k (fp32, K1's at[(rt*kpad + k)*128 + i]).  The producer warp fills it with bulk
+//     those k (fp32, K1's at[(rt*kpad + k)*128 + i]).  Two producer warps fill it with bulk
 //     copies (B; A runs of consecutive live k on dense tiles) or cp.async rows (A on sparse
 //     tiles).  `tma[s]` = landed; `empty[s]` = the transform read A (4 arrivals) and the
 //     stage's MMAs completed (1 tcgen05.commit).
@@ -65,7 +65,12 @@ constexpr int kTdTN = TD_TN;
 constexpr int kTdStepFloats = kTdTN * 8 * 2;  // one K1 step image (8 k tf32 or 16 k fp16): hi | lo, 12 KB
 constexpr int kTdThreads = 480;  // warps 0-7 transform, 8-11 accumulators, 12 / 14 producers, 13 MMA
 constexpr int kTdTM = 128;
-constexpr int kTdSlots = 4;                   // TMEM A slots of 32 columns
+#ifndef TD_SLOTS32
+#define TD_SLOTS32 2
+#endif
+#ifndef TD_STAGES32
+#define TD_STAGES32 4
+#endif
 constexpr int kTdXrow = 36;                   // C-update staging row stride (floats): 16-byte aligned rows,
                                               // conflict-free 16-byte stores by row-owning threads
 
@@ -78,8 +83,15 @@ struct TdCfg {
   static constexpr int kSeg = 32;                     // stages per accumulation segment (64 MMA steps)
   // B smem per stage: kSub step images, of which a pair CTA holds its N/2 columns
   static constexpr int kBStageFloats = kSub * kTdStepFloats / (kPair ? 2 : 1);
-  static constexpr int kStages = F16 ? 6 : 5;          // smem ring
-  static_assert(kStages > kTdSlots, "the smem ring must run ahead of the TMEM slots");
+  static constexpr int kStages = F16 ? 6 : TD_STAGES32;  // smem ring
+  static constexpr int kSlots = F16 ? 4 : TD_SLOTS32;    // TMEM A slots of 32 columns
+  static_assert(kStages > kSlots, "the smem ring must run ahead of the TMEM slots");
+  // Two producers and two transform groups take alternate stages, and a waiter only ever
+  // observed the phases of ITS OWN earlier stages: a parity wait on the phase of stage J is
+  // sound only if the phase of stage J - kStages (smem ring) / J - kSlots - kStages (slot
+  // reuse) already completed, which the same-parity waiter guarantees iff both are even (odd
+  // counts gave false-positive waits: corrupted A slots with 4 / 5, a hang with 2 / 3).
+  static_assert(kStages % 2 == 0 && kSlots % 2 == 0, "alternating roles need even ring sizes");
 };
 
 template <bool F16>
@@ -89,8 +101,8 @@ struct TdShared {
   float a[Cfg::kStages][Cfg::kStageK][kTdTM];  // the stage's live A^T rows
   float xp[4][2][32][kTdXrow];                 // per accumulator warp: C-update staging, 2 buffers
   uint64_t tma[Cfg::kStages];    // stage data landed (TMA bytes / cp.async arrivals)
-  uint64_t empty[Cfg::kStages];  // stage consumed: 8 transform arrivals + 1 tcgen05.commit
-  uint64_t full[kTdSlots];       // A slot written (transform warps; pair: both CTAs')
+  uint64_t empty[Cfg::kStages];  // stage consumed: 4 transform arrivals (one group) + 1 tcgen05.commit
+  uint64_t full[Cfg::kSlots];       // A slot written (transform warps; pair: both CTAs')
   uint64_t seg_full;             // segment's MMAs done (tcgen05.commit)
   uint64_t seg_empty;            // D drained into P (accumulator warps; pair: both CTAs')
   uint32_t tmem_base;
@@ -127,10 +139,10 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       const uint32_t* __restrict__ amax, const unsigned long long* __restrict__ bmax) {
   using Cfg = TdCfg<F16>;
   constexpr int kStages = Cfg::kStages, kSub = Cfg::kSub, kStepK = Cfg::kStepK, kStageK = Cfg::kStageK,
-                kSeg = Cfg::kSeg;
+                kSeg = Cfg::kSeg, kTdSlots = Cfg::kSlots;
   constexpr bool kPair = Cfg::kPair;
   constexpr int kNAccum = kPair ? 8 : 4;    // accumulator warps signalling the MMA issuer (seg_empty)
-  constexpr int kNXform = kPair ? 16 : 8;   // transform warps signalling the MMA issuer (full)
+  constexpr int kNXform = kPair ? 8 : 4;    // transform warps signalling the MMA issuer (full): one group
   // (sel is read by both CTAs of a pair: both exit, or neither)
   if (sel && *sel != 32ull) return;  // device-side path choice (k1_finalize): 32 = TC
   extern __shared__ __align__(128) uint8_t td_raw[];
@@ -153,7 +165,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(&sh.tma[s], 1);
-      tc::mbar_init(&sh.empty[s], 1 + 8);
+      tc::mbar_init(&sh.empty[s], 1 + 4);
     }
     for (int t = 0; t < kTdSlots; ++t) tc::mbar_init(&sh.full[t], kNXform);
     tc::mbar_init(&sh.seg_full, 1);
@@ -334,17 +346,16 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
 #endif
   } else if (warp < 8) {
     // ---------------------------------------------------------------- A transform
-    // Warp w owns tile rows 32*(w%4) .. +31 (its TMEM lanes) and MMA step h = w/4 of each
-    // stage (16 live k fp16 / 8 tf32): two warps per SM sub-partition hide each other's
-    // latencies (one warp per row group left the transform the slowest stage of the
-    // pipeline: 630 cycles of work per 630-cycle stage).  Per stage a thread waits for the
-    // stage's A^T rows in shared memory (`tma`), reads its row's values of step h and releases
-    // the smem (`empty`), waits until the MMAs of the slot's previous stage are done (the
-    // `empty` phase of stage J - kSlots, which includes their commit), splits the values into
-    // hi / lo (tf32: one column each; fp16: scaled by 2^sA, two per column), stores them with
-    // one tcgen05.st of 16 columns and signals the MMA issuer (`full`).
-    constexpr int kV = kStepK;  // values per thread per stage
-    const int h = warp >> 2, r = 32 * (warp & 3) + lane;
+    // Two groups of 4 warps; group g = w/4 transforms the stages J with J % 2 == g, warp w
+    // owning tile rows 32*(w%4) .. +31 (its TMEM lanes), so two stages' chains of barrier
+    // waits, loads and TMEM stores overlap (one stage at a time left the transform the
+    // slowest stage of the pipeline).  Per stage a thread waits for the stage's A^T rows in
+    // shared memory (`tma`), reads its row's values and releases the smem (`empty`), splits
+    // them into hi / lo (tf32: one column each; fp16: scaled by 2^sA, two per column), waits
+    // until the MMAs of the slot's previous stage are done (the `empty` phase of stage
+    // J - kSlots, which includes their commit), stores them with one tcgen05.st of 32
+    // columns and signals the MMA issuer (`full`).
+    const int grp = warp >> 2, r = 32 * (warp & 3) + lane;
     const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
     const float sa = F16 ? tc::exp2_int(tc::f16_scale_exp(*amax)) : 1.0f;
     uint32_t J = 0;
@@ -357,35 +368,42 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       const int32_t total = tcn[tb];
       const int nsteps = nsteps_of(total);
       const int nstage = (nsteps + kSub - 1) / kSub;
-      for (int j = 0; j < nstage; ++j, ++J) {
-        const int st = J % kStages, sl = J % kTdSlots;
-        const int nvalid = min(kV, total - kStageK * j - kV * h);  // may be <= 0
+      const int j0 = (int)(((uint32_t)grp + 2u - (J & 1u)) & 1u);
+      for (int j = j0; j < nstage; j += 2) {
+        const uint32_t Jj = J + (uint32_t)j;
+        const int st = Jj % kStages, sl = Jj % kTdSlots;
+        const int nvalid = min(kStageK, total - kStageK * j);
         TD_CLK(q0);
-        tc::mbar_wait(&sh.tma[st], (J / kStages) & 1u);
+        tc::mbar_wait(&sh.tma[st], (Jj / kStages) & 1u);
         TD_CLK(q1);
-        float vals[kV];
+        float vals[kStageK];
 #pragma unroll
-        for (int q = 0; q < kV; ++q) vals[q] = q < nvalid ? sh.a[st][kV * h + q][r] : 0.0f;
+        for (int q = 0; q < kStageK; ++q) vals[q] = q < nvalid ? sh.a[st][q][r] : 0.0f;
         tc::fence_async_smem();  // these generic-proxy reads before the producer's async-proxy refill
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&sh.empty[st]);  // A smem read (the MMA commit completes the phase)
-        uint32_t v[16];  // hi at 0 .. 7, lo at 8 .. 15
-        if (F16) {
+        uint32_t v[32];  // per step u: hi at 16u .. 16u+7, lo at 16u+8 ..
 #pragma unroll
-          for (int e = 0; e < 8; ++e) tc::split_f16x2_scaled(vals[2 * e], vals[2 * e + 1], sa, v[e], v[8 + e]);
-        } else {
+        for (int u = 0; u < kSub; ++u) {
+          if (F16) {
 #pragma unroll
-          for (int e = 0; e < 8; ++e) tc::split_tf32(vals[e], v[e], v[8 + e]);
+            for (int e = 0; e < 8; ++e)
+              tc::split_f16x2_scaled(vals[16 * u + 2 * e], vals[16 * u + 2 * e + 1], sa, v[16 * u + e],
+                                     v[16 * u + 8 + e]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) tc::split_tf32(vals[8 * u + e], v[16 * u + e], v[16 * u + 8 + e]);
+          }
         }
         TD_CLK(q15);
-        if (J >= (uint32_t)kTdSlots) {  // the slot's previous MMAs (stage J - kSlots) are done
-          const uint32_t Jp = J - kTdSlots;
+        if (Jj >= (uint32_t)kTdSlots) {  // the slot's previous MMAs (stage Jj - kSlots) are done
+          const uint32_t Jp = Jj - kTdSlots;
           tc::mbar_wait(&sh.empty[Jp % kStages], (Jp / kStages) & 1u);
         }
         TD_CLK(q2);
         TD_ADD(2, q2 - q15);
         tc::fence_after_sync();
-        tc::tmem_st16(tbase + lane_off + kAcol + 32 * sl + 16 * h, v);
+        tc::tmem_st32(tbase + lane_off + kAcol + 32 * sl, v);
         tc::tmem_st_wait();
         tc::fence_before_sync();
         __syncwarp();
@@ -394,6 +412,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
         TD_ADD(0, q1 - q0);
         TD_ADD(1, q3 - q1);
       }
+      J += (uint32_t)nstage;
     }
 #ifdef TD_PROF
     if (tid == 0 && td_prof) {
