@@ -13,7 +13,9 @@ def main(path, last=None):
             hdr = r
             continue
         if hdr and len(r) == len(hdr):
-            data.append(dict(zip(hdr, r)))
+            d = dict(zip(hdr, r))
+            if d.get("Metric Name", "gpu__time_duration.sum") == "gpu__time_duration.sum":
+                data.append(d)
     if last:
         data = data[-int(last):]
     scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
