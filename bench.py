@@ -85,7 +85,7 @@ def seed_of(key, base=20240220):
 
 # ---------------------------------------------------------------------------- helpers
 class ClockSampler:
-    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock and clock-event-reason sampling DURING the timed region (B200_PROFILING.md clocks line)."""
 
     REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
                0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
@@ -95,8 +95,36 @@ class ClockSampler:
         self.device = device
         self.proc = None
         self.lines = []
+        self.nvml = None
 
     def start(self):
+        # NVML in a thread (5 ms period; the timed region of a sweep step is ~0.2 s, too short
+        # for nvidia-smi's start-up); nvidia-smi -lms as the fallback
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.nvml = (pynvml, h)
+            self.samples, self.run = [], True
+
+            def loop():
+                while self.run:
+                    try:
+                        self.samples.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                                             pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
+                    except Exception:  # noqa: BLE001
+                        pass
+                    time.sleep(0.005)
+
+            self.t = threading.Thread(target=loop, daemon=True)
+            self.t.start()
+            while not self.samples:  # sampling is live before the timed region starts
+                time.sleep(0.001)
+            self.samples.clear()
+            return
+        except Exception:  # noqa: BLE001
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
@@ -112,6 +140,19 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def stop(self):
+        if self.nvml is not None:
+            self.run = False
+            self.t.join(timeout=1)
+            pynvml, h = self.nvml
+            try:
+                mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            except Exception:  # noqa: BLE001
+                mx = None
+            sm = [float(c) for c, _ in self.samples]
+            reasons = {name for _, bits in self.samples for bit, name in self.REASONS.items()
+                       if bits & bit and name != "gpu_idle"}
+            return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                    "samples": len(sm), "source": "nvml"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
         time.sleep(0.06)

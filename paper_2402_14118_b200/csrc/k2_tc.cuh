@@ -17,14 +17,14 @@
 //     one CTA per 128-row tile.
 // Per 16 (8) live k: D += A_lo*B_hi + A_hi*B_lo + A_hi*B_hi (3 MMAs, N = 192).
 //
-// Pipelines (the measured limit is how many operand bytes are in flight, not the tensor
-// pipe: with a 4-stage ring the transform waited on data 36% of the time, so the fp32
-// partial P moved from shared memory into TMEM to make room for a 7-stage ring):
+// Pipelines (measured per-role cycle counts, TD_PROF builds, decided each of these: one
+// producer warp's per-stage instruction chain and one transform warp per row group were each
+// slower than a stage's MMAs; P in shared memory left room for only 4 stages):
 //   smem ring (kStages): per stage the B step images of 32 (16) live k and the A^T rows of
-//     those k (fp32, K1's at[(rt*kpad + k)*128 + i]).  Two producer warps fill it with bulk
-//     copies (B; A runs of consecutive live k on dense tiles) or cp.async rows (A on sparse
-//     tiles).  `tma[s]` = landed; `empty[s]` = the transform read A (4 arrivals) and the
-//     stage's MMAs completed (1 tcgen05.commit).
+//     those k (fp32, K1's at[(rt*kpad + k)*128 + i]).  Two producer warps (alternate
+//     stages) fill it with bulk copies (B; A runs of consecutive live k).  `tma[s]` =
+//     landed; `empty[s]` = the transform read A (4 arrivals) and the stage's MMAs completed
+//     (1 tcgen05.commit).
 //   TMEM A slots (kSlots): the transform warps split the stage's A values into hi / lo and
 //     store them into slot J % kSlots (lane = row), after the slot's previous MMAs completed
 //     (the empty phase of stage J - kSlots); `full[t]` tells the MMA issuer.
@@ -124,9 +124,7 @@ __device__ __forceinline__ void td_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-// A tile whose B columns leave >= 3/4 of k live gets its A rows by bulk copies (runs of
-// consecutive live k: ~1 copy per stage); sparser tiles have short runs, and per-run copies
-// would cost more TMA time than the MMAs leave, so their rows come by cp.async.
+// A tile is "mostly live" when >= 3/4 of its k are live (scheduling groups, below).
 __device__ __forceinline__ bool td_dense(int32_t live, int64_t kpad) { return 4 * (int64_t)live >= 3 * kpad; }
 
 // Persistent: CTA (pair) u takes work units t = u, u + #units, ...; unit t = (row tile (pair)
@@ -205,12 +203,11 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
     // ---------------------------------------------------- producers (B and A per stage)
     // Two warps, producer p = (warp - 12) / 2 fills the stages J with J % 2 == p (one warp's
     // per-stage instruction chain, ~760 cycles, was longer than the stage's 630 MMA cycles).
-    // Per stage: one bulk copy of the stage's B step images, and the stage's live A^T rows.
-    // Dense tiles: one bulk copy per run of consecutive live k.  Sparse tiles: each live row
-    // by the warp, one 16-byte cp.async per lane (LDGSTS, 512 B per instruction), tracked by
-    // the same barrier (cp.async.mbarrier.arrive, issued before the expect_tx arrive so the
-    // phase cannot complete early).  Lane e < kStageK holds live k number e of the stage;
-    // the list is loaded 4 stages ahead (register shift chain).
+    // Per stage: one bulk copy of the stage's B step images, and the stage's live A^T rows,
+    // one bulk copy per run of consecutive live k (with two producers this beats per-row
+    // cp.async on sparse tiles too: 0.25 vs 0.56 ms at zB = 0.8, bw = 32).  Lane
+    // e < kStageK holds live k number e of the stage; the list is loaded 4 stages ahead
+    // (register shift chain).
     uint32_t J = 0;
 #ifdef TD_PROF
     long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -224,7 +221,6 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       const int32_t total = tcn[tb];
       const int nsteps = nsteps_of(total);
       const int nstage = (nsteps + kSub - 1) / kSub;
-      const bool a_tma = td_dense(total, kpad);
       // pair: the tile's step images are stored per column half (K1 pack), this CTA's half
       // of a stage is one contiguous copy
       constexpr int kStepCopy = kPair ? kTdStepFloats / 2 : kTdStepFloats;  // floats per step in this CTA
@@ -247,7 +243,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
         k2 = k3;
         k3 = kload(j + 8);
         const int prev = __shfl_up_sync(0xffffffffu, kc, 1);
-        const bool valid = a_tma && kc >= 0;
+        const bool valid = kc >= 0;
         const bool cont = valid && lane > 0 && prev + 1 == kc;
         const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
         const uint32_t cmask = __ballot_sync(0xffffffffu, cont);
@@ -257,18 +253,6 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
         __syncwarp();
         TD_CLK(q1);
         TD_ADD(0, q1 - q0);
-        if (!a_tma) {
-#pragma unroll 4
-          for (int q = 0; q < kStageK; ++q) {
-            const int kq = __shfl_sync(0xffffffffu, kc, q);
-            if (kq >= 0)
-              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tc::smem_u32(&sh.a[st][q][4 * lane])),
-                           "l"(atile + (int64_t)kq * 128 + 4 * lane)
-                           : "memory");
-          }
-          asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&sh.tma[st])) : "memory");
-          __syncwarp();
-        }
         if (lane == 0) {
           td_expect_tx(&sh.tma[st], bytes + 512u * (uint32_t)__popc(vmask));
           td_bulk(sh.b[st], bsrc + (int64_t)kSub * j * kStepCopy, bytes, &sh.tma[st]);
