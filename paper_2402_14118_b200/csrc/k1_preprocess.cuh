@@ -85,10 +85,11 @@ __device__ void k1_plan_totals(const unsigned long long* __restrict__ btot, int6
 // SM-cycles of each path from the plan, constants measured on B200 (K2 choice):
 //   K2-SIMT = records * 1158 + row tiles * (span 16: 26 * slice_nz | span 8: 17.5 * pop)
 //             records = row tiles * 256-column tiles * 32-k chunks
-//   K2-TC   = row tiles * Σ_tiles (24200 + 784 * stages), stages = ceil(live k / 32) (fp16
-//             split: 6 MMAs of 16 k per stage)
+//   K2-TC   = row tiles * Σ_tiles (24200 + 940 * stages), stages = ceil(live k / 32) (fp16
+//             split on CTA pairs: 6 MMAs of 16 k per stage; 940 SM-cycles per 128-row stage
+//             measured on the dense 4096^3 cells)
 //   + K1 packing traffic at 0.0433 SM-cycles per byte (HBM): K2-SIMT rows 2 x 64 B per
-//     non-zero (k, slice); K2-TC step images 3 x 768 B per live (k, tile);
+//     non-zero (k, slice); K2-TC step images 2 x 768 B per live (k, tile) (fp16 hi | lo);
 //   each divided by min(148 SMs, its CTA count).
 __device__ void k1_choose_path(const K1Scratch& z, int64_t M, int64_t kw, unsigned long long* __restrict__ out) {
   __shared__ unsigned long long s_stage[32], s_live[32];
@@ -130,7 +131,7 @@ __device__ void k1_choose_path(const K1Scratch& z, int64_t M, int64_t kw, unsign
     const double slice_nz = (double)z.btot[0], pop = (double)out[5];
     const double simt = rt * (double)z.n_tb * (double)kw * 1158.0 + rt * (span == 16.0 ? 26.0 * slice_nz : 17.5 * pop) +
                         0.0433 * 128.0 * slice_nz;
-    const double tc = rt * (24200.0 * (double)z.n_tc + 784.0 * (double)stages) + 0.0433 * 3.0 * 768.0 * (double)lv;
+    const double tc = rt * (24200.0 * (double)z.n_tc + 940.0 * (double)stages) + 0.0433 * 2.0 * 768.0 * (double)lv;
     // time ~ work / min(SMs, CTAs): short operands leave SMs idle
     const double par_simt = fmin(148.0, rt * (double)z.n_tb), par_tc = fmin(148.0, rt * (double)z.n_tc);
     // K2-TC multiplies A's zeros and reads tf32: an Inf / NaN operand would turn 0 * Inf
@@ -384,11 +385,8 @@ struct K1RingLoader {
 __device__ __forceinline__ int k1_chunk(int w, int j) { return 2 * w + (j & 1) + 16 * (j >> 1); }
 
 // Values K2-TC cannot reproduce within the tolerance: Inf / NaN (0 * Inf terms) and
-// subnormals (tf32 operands are flushed).  K1 flags them and AUTO keeps K2-SIMT.
-__device__ __forceinline__ bool k1_tc_unsafe(float v) {
-  const uint32_t a = __float_as_uint(v) & 0x7FFFFFFFu;  // |v|: subnormal in [1, 0x7FFFFF], Inf/NaN >= 0x7F800000
-  return (a - 1u < 0x007FFFFFu) | (a >= 0x7F800000u);   // branch-free (bitwise |)
-}
+// subnormals (tf32 operands are flushed).  The tile loops track max / min of the |x| bit
+// patterns; K1 flags them and AUTO keeps K2-SIMT.
 
 template <typename Loader>
 __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, uint32_t* __restrict__ abits, int64_t kw,
@@ -404,10 +402,10 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
     col[j] = c0 + colofs[j];
     ok[j] = col[j] < K;
   }
-  uint32_t ccount[4] = {0, 0, 0, 0};
   uint32_t warp_total = 0;
-  bool nonfin = false;
-  float vmax = 0.0f;  // max |x| over the lane's elements (fp16 operand scale)
+  // |x| bit patterns: max (fp16 operand scale; >= 0x7F800000 = Inf / NaN) and min of
+  // |x| - 1 (unsigned: zeros wrap to 0xFFFFFFFF; < 0x7FFFFF = a subnormal)
+  uint32_t amax_b = 0u, amin_b = 0xFFFFFFFFu;
   __shared__ uint32_t s_ab[kK1Rows][32];  // the tile's bitmap words (row, chunk)
   const int64_t rend = min(r0 + kK1Rows, M);
   const int64_t rend_at = z.at ? min(r0 + kK1Rows, z.m_at) : rend;
@@ -449,10 +447,10 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const bool nz = x[u][j] != 0.0f;
-        nonfin |= k1_tc_unsafe(x[u][j]);
-        vmax = fmaxf(vmax, fabsf(x[u][j]));
+        const uint32_t ab = __float_as_uint(x[u][j]) & 0x7FFFFFFFu;
+        amax_b = max(amax_b, ab);
+        amin_b = min(amin_b, ab - 1u);
         const uint32_t m = __ballot_sync(0xffffffffu, nz);
-        ccount[j] += nz ? 1u : 0u;
         cnt += __popc(m);
         if (lane == j) s_ab[i - r0][k1_chunk(w, j)] = m;  // staged: written row-contiguous below
       }
@@ -463,14 +461,13 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
     }
   }
   if (lane == 0 && warp_total) atomicAdd(&z.tile_sum[ty], warp_total);
-  if (__any_sync(0xffffffffu, nonfin) && lane == 0) atomicOr(z.nonfinite_a, 1u);
   {
-    const uint32_t mb = __reduce_max_sync(0xffffffffu, __float_as_uint(vmax));
+    const uint32_t mb = __reduce_max_sync(0xffffffffu, amax_b), mn = __reduce_min_sync(0xffffffffu, amin_b);
+    if (lane == 0 && (mb >= 0x7F800000u || mn < 0x007FFFFFu)) atomicOr(z.nonfinite_a, 1u);
     if (lane == 0 && mb && z.amax) atomicMax(z.amax, mb);
   }
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
-    if (ok[j] && ccount[j]) atomicAdd(&z.acol[col[j]], ccount[j]);
+  // (per-column non-zero counts, for the WorkCounters only, come from the bitmap on request:
+  // k1_acol)
   // the tile's bitmap words, row by row (32 words = 128 contiguous bytes per row)
   asm volatile("bar.sync 2, %0;" ::"r"(kK1Threads) : "memory");
   const int64_t wd = (c0 >> 5) + lane;
@@ -508,8 +505,7 @@ __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, 
   for (int j = 0; j < 4; ++j) sel[j] = gj == j ? 0xFFFFFFFFu : 0u;
   const uint32_t gmask = 0xFFu << (8 * gs);
   uint32_t gword = 0;
-  bool nonfin = false;
-  float vmax = 0.0f;
+  uint32_t amax_b = 0u, amin_b = 0xFFFFFFFFu;  // as in k1_a_tile_b
   const int64_t kend = min(k0 + 32, K);
   for (int64_t kb = k0; kb < kend; kb += 8) {
     float x[8][4];
@@ -523,8 +519,9 @@ __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, 
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         m[j] = __ballot_sync(0xffffffffu, x[u][j] != 0.0f);
-        nonfin |= k1_tc_unsafe(x[u][j]);
-        vmax = fmaxf(vmax, fabsf(x[u][j]));
+        const uint32_t ab = __float_as_uint(x[u][j]) & 0x7FFFFFFFu;
+        amax_b = max(amax_b, ab);
+        amin_b = min(amin_b, ab - 1u);
       }
       const uint32_t mg = (m[0] & sel[0]) | (m[1] & sel[1]) | (m[2] & sel[2]) | (m[3] & sel[3]);  // branch-free
       gword |= (uint32_t)((mg & gmask) != 0) << (uint32_t)(kb - k0 + u);
@@ -546,9 +543,9 @@ __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, 
     pop_w += __shfl_xor_sync(0xffffffffu, pop_w, o);
     nz_w += __shfl_xor_sync(0xffffffffu, nz_w, o);
   }
-  if (__any_sync(0xffffffffu, nonfin) && lane == 0) atomicOr(&z.btot[3], 1ull);
   {
-    const uint32_t mb = __reduce_max_sync(0xffffffffu, __float_as_uint(vmax));
+    const uint32_t mb = __reduce_max_sync(0xffffffffu, amax_b), mn = __reduce_min_sync(0xffffffffu, amin_b);
+    if (lane == 0 && (mb >= 0x7F800000u || mn < 0x007FFFFFu)) atomicOr(&z.btot[3], 1ull);
     if (lane == 0 && mb) atomicMax(&z.btot[4], (unsigned long long)mb);
   }
   if (lane == 0 && pop_w) atomicAdd(&z.btot[1], (unsigned long long)pop_w);
@@ -744,6 +741,19 @@ __global__ void __launch_bounds__(256) k1_csr(const uint32_t* __restrict__ abits
 // (k1_plan_totals) out of per-warp atomics of the B tiles.
 // bpop[k] (# non-zero 8-column groups of row k) and bnz[k] (# non-zero 64-column regions)
 // from the group k-masks: thread per k walks the ld/8 groups.
+// Per-column non-zero counts of A from the bitmap (WorkCounters on request; the K1 pass no
+// longer accumulates them): thread = column k, its warp reads each row's word once.
+__global__ void k1_acol(const uint32_t* __restrict__ abits, int64_t M, int64_t K, int64_t kw,
+                        uint32_t* __restrict__ acol) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const int64_t w = k >> 5;
+  const uint32_t bit = k & 31;
+  uint32_t n = 0;
+  for (int64_t i = 0; i < M; ++i) n += (__ldg(abits + i * kw + w) >> bit) & 1u;
+  acol[k] = n;
+}
+
 __global__ void k1_bcounts(const uint32_t* __restrict__ bgrp, int64_t K, int64_t nreg, int64_t kw,
                            uint32_t* __restrict__ bpop, uint32_t* __restrict__ bnz) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

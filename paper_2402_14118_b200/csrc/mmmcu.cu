@@ -589,6 +589,11 @@ mmmcu_status fill_counters(mmmcu_ctx* ctx, mmmcu_counters* out) {
         ctx->bgrp.as<uint32_t>(), ctx->Kb, ctx->ldb / 64, (ctx->Kb + 31) / 32, zb_bpop(ctx), zb_bnz(ctx));
     MMMCU_LAUNCHED();
   }
+  if (a_ok) {
+    mmmcu::k1_acol<<<(unsigned)((ctx->Ka + 255) / 256), 256, 0, ctx->stream>>>(
+        ctx->abits.as<uint32_t>(), ctx->M, ctx->Ka, (ctx->Ka + 31) / 32, za_acol(ctx));
+    MMMCU_LAUNCHED();
+  }
   mmmcu::k1_counters<<<1, 1024, 0, ctx->stream>>>(a_ok ? za_acol(ctx) : nullptr, b_ok ? zb_bpop(ctx) : nullptr,
                                                   b_ok ? zb_bnz(ctx) : nullptr, K, ctx->M, ctx->ldb / 64,
                                                   (a_ok && (same_k || !b_ok)) ? 1 : 0, (b_ok && (same_k || !a_ok)) ? 1 : 0,
