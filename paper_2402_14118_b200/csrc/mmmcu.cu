@@ -121,9 +121,36 @@ mmmcu_status fail(mmmcu_ctx* ctx, mmmcu_status st, const std::string& msg) {
     if (s_ != MMMCU_OK) return s_;    \
   } while (0)
 
+// Every kernel of the per-call chain asks for the maximum shared-memory carveout, so that
+// consecutive kernels (K1 pass: 3 x 66 KB per SM, K2-TC: 210 KB, packs / CSR: small) never
+// make the SMs drain and reconfigure L1 / shared memory between launches.
+template <typename F>
+void max_carveout(F* f) {
+  cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+}
+void set_carveouts(int device) {
+  static bool done[64] = {false};
+  if (device < 0 || device >= 64 || done[device]) return;
+  done[device] = true;
+  max_carveout(mmmcu::k1_pass);
+  max_carveout(mmmcu::k1_csr<uint16_t>);
+  max_carveout(mmmcu::k1_csr<uint32_t>);
+  max_carveout(mmmcu::k1_pack_auto);
+  max_carveout(mmmcu::k1_pack_tc);
+  max_carveout(mmmcu::k1_pack_rows);
+  max_carveout(mmmcu::k1_row_off);
+  max_carveout(mmmcu::k2_simt2_any);
+  max_carveout(mmmcu::k2_simt2<8>);
+  max_carveout(mmmcu::k2_simt2<16>);
+  max_carveout(mmmcu::k2_tc<true>);
+  max_carveout(mmmcu::k2_tc<false>);
+  cudaGetLastError();  // attribute hints only
+}
+
 mmmcu_status bind(mmmcu_ctx* ctx) {
   if (!ctx) return fail(nullptr, MMMCU_ERR_INVALID_ARG, "null context");
   MMMCU_CUDA(cudaSetDevice(ctx->device));
+  set_carveouts(ctx->device);
   return MMMCU_OK;
 }
 
