@@ -14,7 +14,7 @@ hdr = rows[0]
 ix = {h: i for i, h in enumerate(hdr)}
 want = sys.argv[2] if len(sys.argv) > 2 else rows[1][0]
 seen = set()
-print(rows[1][ix["Kernel Name"]][:60])
+print(next(r for r in rows[1:] if r[0] == want)[ix["Kernel Name"]][:60])
 for r in rows[1:]:
     if r[0] != want:
         continue
