@@ -658,55 +658,57 @@ k1_pass(K1Args g, K1Scratch z, int has_a, int has_b, unsigned long long* __restr
 
 // --------------------------------------------------------------- CSR index lists
 // Per-row ascending index lists (CSR) from the bitmap, no second pass over A.  A CTA owns
-// 8 rows (one per warp).  row_ptr comes from the 32-row tile prefix the K1 pass's last CTA
-// scanned, plus at most 31 row counts: no separate scan launch.  Each warp then expands its
-// row: popc per bitmap word, warp prefix sum, each lane writes its word's set bits.  Index
-// type: uint16 when K <= 65536, else uint32.
-constexpr int kCsrRows = 8;
+// kCsrRows rows; its 8 warps take the (row, 1024-column chunk) pairs, so a row's chunks are
+// expanded in parallel (one warp walking a row's chunks in turn left the kernel latency-
+// bound: 11 us for a 4096^2 cell).  row_ptr comes from the 32-row tile prefix the K1 pass's
+// last CTA scanned, plus at most 31 row counts: no separate scan launch.  A warp's chunk
+// offset within its row is the popcount of the row's earlier words; it expands its chunk's
+// set bits through a per-warp smem buffer so the index stores are coalesced.  Index type:
+// uint16 when K <= 65536, else uint32.
+constexpr int kCsrRows = 2;
 
 template <typename Idx>
 __global__ void __launch_bounds__(256) k1_csr(const uint32_t* __restrict__ abits, const uint32_t* __restrict__ arow,
                                               const int64_t* __restrict__ tile_prefix, int64_t M, int64_t kw,
                                               int64_t* __restrict__ row_ptr, Idx* __restrict__ cols) {
   __shared__ int64_t s_off[kCsrRows + 1];
+  __shared__ Idx s_buf[8][1024];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t r0 = (int64_t)blockIdx.x * kCsrRows;
   if (warp == 0) {
     const int64_t t0 = (r0 / 32) * 32;  // first row of r0's 32-row tile
-    // counts of rows [t0, r0) (lanes 0..r0-t0-1) and of this CTA's rows (lanes 24..31 -> rows r0..r0+7)
+    // counts of rows [t0, r0) (lanes 0..r0-t0-1) and of this CTA's rows (lanes 0..kCsrRows-1)
     const int64_t i_pre = t0 + lane;
     uint32_t pre = (i_pre < r0) ? arow[i_pre] : 0u;
 #pragma unroll
     for (int o = 16; o; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
-    const int64_t i_own = r0 + (lane & 7);
-    const uint32_t own = (lane < 8 && i_own < M) ? arow[i_own] : 0u;
+    const int64_t i_own = r0 + lane;
+    const uint32_t own = (lane < kCsrRows && i_own < M) ? arow[i_own] : 0u;
     uint32_t x = own;
 #pragma unroll
-    for (int o = 1; o < 8; o <<= 1) {
+    for (int o = 1; o < kCsrRows; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if ((lane & 7) >= o) x += y;
+      if (lane >= o) x += y;
     }
     const int64_t base = tile_prefix[r0 / 32] + (int64_t)pre;
-    if (lane < 8) s_off[lane] = base + (int64_t)(x - own);
-    if (lane == 7) s_off[8] = base + (int64_t)x;
+    if (lane < kCsrRows) s_off[lane] = base + (int64_t)(x - own);
+    if (lane == kCsrRows - 1) s_off[kCsrRows] = base + (int64_t)x;
   }
   __syncthreads();
-  const int64_t row = r0 + warp;
   if (threadIdx.x < kCsrRows && r0 + threadIdx.x < M) row_ptr[r0 + threadIdx.x] = s_off[threadIdx.x];
   if (threadIdx.x == 0 && r0 + kCsrRows >= M) row_ptr[M] = s_off[M - r0];
-  if (row >= M) return;
-  // per 1024-column chunk: lanes expand their words' set bits into the warp's smem buffer
-  // at their prefix offsets, then the warp streams the chunk's list out contiguously
-  // (coalesced stores instead of 32 scattered 2-byte streams)
-  __shared__ Idx s_buf[kCsrRows][1024];
+  const int64_t nch = (kw + 31) / 32;
   Idx* buf = s_buf[warp];
-  int64_t out = s_off[warp];
-  const uint32_t* bits = abits + row * kw;
-  uint32_t next = lane < kw ? bits[lane] : 0u;  // the next chunk's word is loaded a chunk ahead
-  for (int64_t w0 = 0; w0 < kw; w0 += 32) {
-    const int64_t w = w0 + lane;
-    uint32_t word = next;
-    next = w + 32 < kw ? bits[w + 32] : 0u;
+  for (int64_t pr = warp; pr < kCsrRows * nch; pr += 8) {
+    const int64_t rr = pr / nch, ch = pr % nch, row = r0 + rr;
+    if (row >= M) break;
+    const uint32_t* bits = abits + row * kw;
+    const int64_t w = ch * 32 + lane;
+    uint32_t word = w < kw ? bits[w] : 0u;
+    uint32_t before = 0;  // set bits of the row's earlier chunks
+    for (int64_t e = lane; e < ch * 32; e += 32) before += __popc(bits[e]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
     const uint32_t n = __popc(word);
     uint32_t x = n;
 #pragma unroll
@@ -722,9 +724,9 @@ __global__ void __launch_bounds__(256) k1_csr(const uint32_t* __restrict__ abits
     }
     const uint32_t total = __shfl_sync(0xffffffffu, x, 31);
     __syncwarp();
+    const int64_t out = s_off[rr] + before;
     for (uint32_t i = lane; i < total; i += 32) cols[out + i] = buf[i];
     __syncwarp();
-    out += total;
   }
 }
 
@@ -1042,18 +1044,20 @@ __global__ void __launch_bounds__(kPackThreads) k1_pack_rows(PackRowsArgs g) {
   k1_pack_rows_cta(g, blockIdx.x, blockIdx.y);
 }
 
-// AUTO: both packs in one launch (CTAs [0, n_rows) = K2-SIMT rows, the rest = K2-TC steps),
+// AUTO: both packs in one launch (CTAs [0, n_tc) = K2-TC steps, the rest = K2-SIMT rows),
 // each CTA gated by the path K1's last CTA chose — one launch instead of two, and the
 // gated-out half exits at entry.
 __global__ void __launch_bounds__(kPtThreads)
 k1_pack_auto(PackRowsArgs gr, int64_t rows_x, int64_t n_rows, PackTcArgs gt, int64_t tc_x,
              const unsigned long long* __restrict__ sel) {
-  const int64_t bid = blockIdx.x;
+  // the K2-TC CTAs first: the gated-out K2-SIMT CTAs (the larger part of the grid) exit
+  // behind the work instead of in front of it when TC is chosen
+  const int64_t bid = blockIdx.x, n_tcb = (int64_t)gridDim.x - n_rows;
   const bool tc = *sel == 32ull;
-  if (bid < n_rows) {
-    if (!tc) k1_pack_rows_cta(gr, bid % rows_x, bid / rows_x);
-  } else if (tc) {
-    k1_pack_tc_cta(gt, (bid - n_rows) % tc_x, (bid - n_rows) / tc_x);
+  if (bid < n_tcb) {
+    if (tc) k1_pack_tc_cta(gt, bid % tc_x, bid / tc_x);
+  } else if (!tc) {
+    k1_pack_rows_cta(gr, (bid - n_tcb) % rows_x, (bid - n_tcb) / rows_x);
   }
 }
 

@@ -77,6 +77,9 @@ constexpr int kTdTM = 128;
 #ifndef TD_SEGS
 #define TD_SEGS 32
 #endif
+#ifndef TD_ACC_SLEEP
+#define TD_ACC_SLEEP 256  // ns between the accumulator warps' seg_full polls
+#endif
 #ifndef TD_HINT
 #define TD_HINT 1  // L2 evict_last on the A^T / B-image bulk copies (dense cell 0.31 -> 0.29 ms)
 #endif
@@ -480,7 +483,8 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       const int nseg = (nstage + kSeg - 1) / kSeg;
       if (nseg == 0) continue;
       for (int g = 0; g < nseg; ++g, ++G) {
-        tc::mbar_wait_sleep(&sh.seg_full, G & 1u);
+        if (TD_ACC_SLEEP > 0) tc::mbar_wait_sleep_ns(&sh.seg_full, G & 1u, TD_ACC_SLEEP);
+        else tc::mbar_wait(&sh.seg_full, G & 1u);
         tc::fence_after_sync();
 #pragma unroll 1
         for (int c = 0; c < kTdTN / 32; ++c) {
@@ -491,8 +495,9 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
             float x = __uint_as_float(d[e]);
-            if (F16) x = (x * ia) * ib;
-            if (g > 0) x = __uint_as_float(p[e]) + x;
+            if (F16) x *= ia;  // exact (power of two)
+            // p + x*ib in one rounding (x*ib exact): the same value as the add of the product
+            x = g > 0 ? fmaf(x, ib, __uint_as_float(p[e])) : x * ib;
             d[e] = __float_as_uint(x);
           }
           tc::tmem_st32(taddr + kPcol + 32 * c, d);
