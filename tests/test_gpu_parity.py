@@ -234,6 +234,13 @@ def test_cfg4_skinny_decode(ctx):
     assert bitexact(C, Cr)
     assert_counters(cnt, ocnt)
     check_auto(ctx, A, B, Cr, ocnt)
+    # forced K2-TC on the skinny shape: one 128-row tile, so the CTA pair's second row tile
+    # is all padding; fp16 scales from ReLU / N(0, 0.02) operands
+    for algo in (N.ALGO_TC, N.ALGO_TC32):
+        C, cnt = run_gpu(ctx, A, B, algo=algo)
+        ok, worst = within_tol(C, Cr, A, B)
+        assert ok and worst < 0.5 * TOL, (algo, worst)
+        assert_counters(cnt, ocnt)
 
 
 def test_cfg5_row_shards(ctx):
