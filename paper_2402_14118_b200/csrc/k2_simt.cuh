@@ -350,14 +350,14 @@ __device__ __forceinline__ void s2_wait(uint64_t* bar, uint32_t parity) {
 template <int SPAN>
 __device__ __forceinline__ void k2_simt2_body(const float* __restrict__ AT, int64_t kpad,
                                               const float4* __restrict__ brows, const int64_t* __restrict__ row_off,
-                                              int64_t kw, float* __restrict__ C, int64_t ldc, int64_t M, int64_t Np) {
+                                              int64_t kw, float* __restrict__ C, int64_t ldc, int64_t M, int64_t Np,
+                                              int64_t rt, int64_t tb) {
   static_assert(SPAN == 8 || SPAN == 16, "SPAN must be 8 or 16");
   extern __shared__ __align__(128) uint8_t s2_raw[];
   S2Shared& sh = *reinterpret_cast<S2Shared*>(s2_raw + ((128 - ((uint32_t)__cvta_generic_to_shared(s2_raw) & 127)) & 127));
   int64_t* offs = reinterpret_cast<int64_t*>(&sh + 1);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t rt = blockIdx.y, tb = blockIdx.x;
   const int64_t m0 = rt * 128, n0 = tb * 256;
 
   for (int64_t c = tid; c <= kw; c += kS2Threads) offs[c] = row_off[tb * kw + c];
@@ -481,20 +481,26 @@ __global__ void __launch_bounds__(kS2Threads, 1)
 k2_simt2(const float* __restrict__ AT, int64_t kpad, const float4* __restrict__ brows, const int64_t* __restrict__ row_off,
          int64_t kw, float* __restrict__ C, int64_t ldc, int64_t M, int64_t Np, const unsigned long long* __restrict__ sel) {
   if (sel && *sel != (unsigned long long)SPAN) return;  // device-side span choice (k1_finalize_block)
-  k2_simt2_body<SPAN>(AT, kpad, brows, row_off, kw, C, ldc, M, Np);
+  k2_simt2_body<SPAN>(AT, kpad, brows, row_off, kw, C, ldc, M, Np, blockIdx.y, blockIdx.x);
 }
 
 // One launch for both spans (and AUTO): *sel = 8 / 16 runs that span, anything else (32 =
-// K2-TC chosen) exits at entry.
+// K2-TC chosen) exits at entry.  Persistent (grid <= one CTA per SM, tiles t = blockIdx.x,
+// + gridDim.x, ...): when K2-TC was chosen the gated-out launch costs one wave of exiting
+// CTAs instead of four (5 us per call with a tile-per-CTA grid).
 __global__ void __launch_bounds__(kS2Threads, 1)
 k2_simt2_any(const float* __restrict__ AT, int64_t kpad, const float4* __restrict__ brows,
              const int64_t* __restrict__ row_off, int64_t kw, float* __restrict__ C, int64_t ldc, int64_t M, int64_t Np,
-             const unsigned long long* __restrict__ sel) {
+             const unsigned long long* __restrict__ sel, int64_t n_tb, int64_t n_rt) {
   const unsigned long long v = *sel;
-  if (v == 8ull)
-    k2_simt2_body<8>(AT, kpad, brows, row_off, kw, C, ldc, M, Np);
-  else if (v == 16ull)
-    k2_simt2_body<16>(AT, kpad, brows, row_off, kw, C, ldc, M, Np);
+  if (v != 8ull && v != 16ull) return;
+  for (int64_t t = blockIdx.x; t < n_tb * n_rt; t += gridDim.x) {
+    if (v == 8ull)
+      k2_simt2_body<8>(AT, kpad, brows, row_off, kw, C, ldc, M, Np, t / n_tb, t % n_tb);
+    else
+      k2_simt2_body<16>(AT, kpad, brows, row_off, kw, C, ldc, M, Np, t / n_tb, t % n_tb);
+    __syncthreads();  // the next tile re-initialises the stage barriers and offsets
+  }
 }
 
 }  // namespace mmmcu

@@ -492,8 +492,12 @@ mmmcu_status launch_simt(mmmcu_ctx* ctx, float* C, int64_t ldc, int span_hint, i
     dim3 grid((unsigned)((Np + 255) / 256), (unsigned)row_tiles);
     if (span_hint == 0) {  // one launch, span (or exit) chosen on the device
       MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k2_simt2_any, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      mmmcu::k2_simt2_any<<<grid, mmmcu::kS2Threads, smem, ctx->stream>>>(
-          ctx->at.as<float>(), ctx->kpad, ctx->brows.as<float4>(), ctx->row_off.as<int64_t>(), kw, C, ldc, M, Np, sel2);
+      if (ctx->num_sms == 0)
+        MMMCU_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
+      const int64_t ntl = (int64_t)grid.x * grid.y;
+      mmmcu::k2_simt2_any<<<(unsigned)std::min<int64_t>(ntl, ctx->num_sms), mmmcu::kS2Threads, smem, ctx->stream>>>(
+          ctx->at.as<float>(), ctx->kpad, ctx->brows.as<float4>(), ctx->row_off.as<int64_t>(), kw, C, ldc, M, Np, sel2,
+          (int64_t)grid.x, (int64_t)grid.y);
       MMMCU_LAUNCHED();
     }
     if (span_hint == 8) {
