@@ -621,6 +621,9 @@ k1_pass(K1Args g, K1Scratch z, int has_a, int has_b, unsigned long long* __restr
   }
   __shared__ unsigned int last;
   __syncthreads();
+  // every CTA's tiles are done: the CSR / pack CTAs may be scheduled while the last CTA
+  // finalises (they wait in griddepcontrol.wait for this grid to complete)
+  tc::pdl_trigger();
 #ifdef K1_PROF
   if (threadIdx.x == 0 && k1_prof) {
     k1_prof[4 * blockIdx.x] = t_start;
@@ -673,6 +676,7 @@ __global__ void __launch_bounds__(256) k1_csr(const uint32_t* __restrict__ abits
                                               int64_t* __restrict__ row_ptr, Idx* __restrict__ cols) {
   __shared__ int64_t s_off[kCsrRows + 1];
   __shared__ Idx s_buf[8][1024];
+  tc::pdl_wait();  // launched with programmatic serialization after k1_pass
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t r0 = (int64_t)blockIdx.x * kCsrRows;
   if (warp == 0) {
@@ -1052,6 +1056,7 @@ k1_pack_auto(PackRowsArgs gr, int64_t rows_x, int64_t n_rows, PackTcArgs gt, int
              const unsigned long long* __restrict__ sel) {
   // the K2-TC CTAs first: the gated-out K2-SIMT CTAs (the larger part of the grid) exit
   // behind the work instead of in front of it when TC is chosen
+  tc::pdl_wait();  // launched with programmatic serialization after k1_csr / k1_pass
   const int64_t bid = blockIdx.x, n_tcb = (int64_t)gridDim.x - n_rows;
   const bool tc = *sel == 32ull;
   if (bid < n_tcb) {

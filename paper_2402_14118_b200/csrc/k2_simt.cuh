@@ -337,6 +337,7 @@ __device__ __forceinline__ void s2_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void s2_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
 }
+__device__ __forceinline__ void pdl_wait_simt() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void s2_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -492,6 +493,7 @@ __global__ void __launch_bounds__(kS2Threads, 1)
 k2_simt2_any(const float* __restrict__ AT, int64_t kpad, const float4* __restrict__ brows,
              const int64_t* __restrict__ row_off, int64_t kw, float* __restrict__ C, int64_t ldc, int64_t M, int64_t Np,
              const unsigned long long* __restrict__ sel, int64_t n_tb, int64_t n_rt) {
+  pdl_wait_simt();  // launched with programmatic serialization after the K1 pack
   const unsigned long long v = *sel;
   if (v != 8ull && v != 16ull) return;
   for (int64_t t = blockIdx.x; t < n_tb * n_rt; t += gridDim.x) {

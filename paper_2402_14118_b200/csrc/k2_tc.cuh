@@ -171,6 +171,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
   constexpr bool kPair = Cfg::kPair;
   constexpr int kNAccum = kPair ? 8 : 4;    // accumulator warps signalling the MMA issuer (seg_empty)
   constexpr int kNXform = kPair ? 8 : 4;    // transform warps signalling the MMA issuer (full): one group
+  tc::pdl_wait();  // launched with programmatic serialization after the K1 kernels / gated K2-SIMT
   // (sel is read by both CTAs of a pair: both exit, or neither)
   if (sel && *sel != 32ull) return;  // device-side path choice (k1_finalize): 32 = TC
   extern __shared__ __align__(128) uint8_t td_raw[];

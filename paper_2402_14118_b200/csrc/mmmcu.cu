@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "gen.cuh"
@@ -120,6 +121,25 @@ mmmcu_status fail(mmmcu_ctx* ctx, mmmcu_status st, const std::string& msg) {
     mmmcu_status s_ = (expr);         \
     if (s_ != MMMCU_OK) return s_;    \
   } while (0)
+
+// Launch with programmatic stream serialization (PDL): the kernel's CTAs may be scheduled
+// before the previous kernel in the stream completes; the kernel waits for it in
+// griddepcontrol.wait (tc::pdl_wait) before reading its outputs.  Used for the kernels that
+// follow another kernel of the call chain (CSR, packs, K2).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 // Every kernel of the per-call chain asks for the maximum shared-memory carveout, so that
 // consecutive kernels (K1 pass: 3 x 66 KB per SM, K2-TC: 210 KB, packs / CSR: small) never
@@ -321,8 +341,8 @@ mmmcu_status pack_auto(mmmcu_ctx* ctx, const unsigned long long* sel) {
   const int64_t tc_x = (pack_steps(ctx, true) + mmmcu::kPtSteps - 1) / mmmcu::kPtSteps, n_tc = tc_x * ctx->n_tc;
   if (n_rows + n_tc > 0x7fffffff) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "B too large for one pack launch");
   MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k1_pack_auto, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  mmmcu::k1_pack_auto<<<(unsigned)(n_rows + n_tc), mmmcu::kPtThreads, smem, ctx->stream>>>(
-      rows_args(ctx), rows_x, n_rows, tc_args(ctx, true), tc_x, sel);
+  MMMCU_CUDA(launch_pdl(mmmcu::k1_pack_auto, dim3((unsigned)(n_rows + n_tc)), dim3(mmmcu::kPtThreads), smem,
+                        ctx->stream, rows_args(ctx), rows_x, n_rows, tc_args(ctx, true), tc_x, sel));
   MMMCU_LAUNCHED();
   ctx->tcb_f16 = true;
   return MMMCU_OK;
@@ -433,13 +453,15 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
     const unsigned blocks = (unsigned)((ctx->M + mmmcu::kCsrRows - 1) / mmmcu::kCsrRows);
     const int64_t akw = (ctx->Ka + 31) / 32;
     if (ctx->csr_idx_bytes == 2)
-      mmmcu::k1_csr<uint16_t><<<blocks, 256, 0, ctx->stream>>>(ctx->abits.as<uint32_t>(), za_arow(ctx),
-                                                               ctx->tile_prefix.as<int64_t>(), ctx->M, akw,
-                                                               ctx->row_ptr.as<int64_t>(), ctx->cols.as<uint16_t>());
+      MMMCU_CUDA(launch_pdl(mmmcu::k1_csr<uint16_t>, dim3(blocks), dim3(256), 0, ctx->stream,
+                            (const uint32_t*)ctx->abits.as<uint32_t>(), (const uint32_t*)za_arow(ctx),
+                            (const int64_t*)ctx->tile_prefix.as<int64_t>(), ctx->M, akw, ctx->row_ptr.as<int64_t>(),
+                            ctx->cols.as<uint16_t>()));
     else
-      mmmcu::k1_csr<uint32_t><<<blocks, 256, 0, ctx->stream>>>(ctx->abits.as<uint32_t>(), za_arow(ctx),
-                                                               ctx->tile_prefix.as<int64_t>(), ctx->M, akw,
-                                                               ctx->row_ptr.as<int64_t>(), ctx->cols.as<uint32_t>());
+      MMMCU_CUDA(launch_pdl(mmmcu::k1_csr<uint32_t>, dim3(blocks), dim3(256), 0, ctx->stream,
+                            (const uint32_t*)ctx->abits.as<uint32_t>(), (const uint32_t*)za_arow(ctx),
+                            (const int64_t*)ctx->tile_prefix.as<int64_t>(), ctx->M, akw, ctx->row_ptr.as<int64_t>(),
+                            ctx->cols.as<uint32_t>()));
     MMMCU_LAUNCHED();
   }
   if (gate) {
@@ -495,9 +517,10 @@ mmmcu_status launch_simt(mmmcu_ctx* ctx, float* C, int64_t ldc, int span_hint, i
       if (ctx->num_sms == 0)
         MMMCU_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
       const int64_t ntl = (int64_t)grid.x * grid.y;
-      mmmcu::k2_simt2_any<<<(unsigned)std::min<int64_t>(ntl, ctx->num_sms), mmmcu::kS2Threads, smem, ctx->stream>>>(
-          ctx->at.as<float>(), ctx->kpad, ctx->brows.as<float4>(), ctx->row_off.as<int64_t>(), kw, C, ldc, M, Np, sel2,
-          (int64_t)grid.x, (int64_t)grid.y);
+      MMMCU_CUDA(launch_pdl(mmmcu::k2_simt2_any, dim3((unsigned)std::min<int64_t>(ntl, ctx->num_sms)),
+                            dim3(mmmcu::kS2Threads), smem, ctx->stream, (const float*)ctx->at.as<float>(), ctx->kpad,
+                            (const float4*)ctx->brows.as<float4>(), (const int64_t*)ctx->row_off.as<int64_t>(), kw, C,
+                            ldc, M, Np, sel2, (int64_t)grid.x, (int64_t)grid.y));
       MMMCU_LAUNCHED();
     }
     if (span_hint == 8) {
@@ -544,14 +567,17 @@ mmmcu_status launch_tc_t(mmmcu_ctx* ctx, float* C, int64_t ldc, const unsigned l
   cfg.blockDim = dim3(mmmcu::kTdThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = ctx->stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL: k2_tc starts with pdl_wait
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   if (F16) {  // CTA pairs: clusters of 2, a pair tile = 256 rows
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 2;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.numAttrs = 2;
     // persistent: exactly as many pairs as can be co-resident (a second wave of pairs would
     // double the kernel time)
     if (ctx->tc_pairs == 0) {

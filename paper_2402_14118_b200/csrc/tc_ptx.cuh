@@ -126,6 +126,11 @@ __device__ __forceinline__ void mbar_wait_sleep_ns(uint64_t* bar, uint32_t parit
     __nanosleep(ns);
   }
 }
+// Programmatic dependent launch: a kernel launched with programmatic stream serialization
+// waits here for its predecessor grid (completion + memory flush) before touching its
+// outputs; a predecessor CTA that triggers lets the dependent grid's CTAs be scheduled early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
