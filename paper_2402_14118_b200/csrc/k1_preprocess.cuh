@@ -573,8 +573,18 @@ __global__ void k1_codes_export(const uint32_t* __restrict__ bgrp, int64_t K, in
   codes[t] = (uint8_t)code;
 }
 
+// Zero the K1 scratch (A part, B part; 16-byte words, either may be empty) — launched
+// with programmatic serialization, after the previous call's last kernel.
+__global__ void __launch_bounds__(256) k1_zero(uint4* __restrict__ za, int64_t na, uint4* __restrict__ zb, int64_t nb) {
+  tc::pdl_wait();
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = i0; i < na; i += st) za[i] = make_uint4(0u, 0u, 0u, 0u);
+  for (int64_t i = i0; i < nb; i += st) zb[i] = make_uint4(0u, 0u, 0u, 0u);
+}
+
 __global__ void __launch_bounds__(kK1Block, kK1CtasPerSm)
 k1_pass(K1Args g, K1Scratch z, int has_a, int has_b, unsigned long long* __restrict__ stats) {
+  tc::pdl_wait();  // launched with programmatic serialization after k1_zero
 #ifdef K1_PROF
   const unsigned long long t_start = k1_now();
 #endif

@@ -32,7 +32,7 @@ struct DevBuf {
     if (p) cudaFree(p);
     p = nullptr;
     cap = 0;
-    const size_t want = std::max<size_t>(bytes, 256);
+    const size_t want = std::max<size_t>((bytes + 255) & ~size_t(255), 256);  // whole 16-byte words for k1_zero
     cudaError_t e = cudaMalloc(&p, want);
     if (e == cudaSuccess) cap = want;
     return e;
@@ -84,6 +84,7 @@ struct mmmcu_ctx {
   int ops_b = 0;                                // operand sets B was staged for
   int64_t kpad = 0, m_at = 0, n_tb = 0, n_tc = 0, tc_steps = 0;
   int tc_pairs = 0;  // co-resident K2-TC CTA pairs (cudaOccupancyMaxActiveClusters), 0 = not queried
+  size_t za_zero = 0, zb_zero = 0;  // bytes of the K1 scratch to zero before the next K1 pass
   DevBuf at, tcb, tck, tcn, brows, row_off;
 
   // ---- statistics: u64 [16] = {inv, lanes, skipped, zreg, nnzA, pop, zero_codes, span, slice_nz}
@@ -239,7 +240,7 @@ mmmcu_status stage_a(mmmcu_ctx* ctx, const float* A, int64_t M, int64_t K, int64
   MMMCU_CUDA(ctx->tile_prefix.ensure(sizeof(int64_t) * (n_row_tiles(M) + 1)));
   MMMCU_CUDA(ctx->row_ptr.ensure(sizeof(int64_t) * (M + 1)));
   MMMCU_CUDA(ctx->cols.ensure((size_t)ctx->csr_idx_bytes * M * K));
-  MMMCU_CUDA(cudaMemsetAsync(ctx->za.p, 0, sizeof(uint32_t) * (M + K + n_row_tiles(M) + 2), ctx->stream));
+  ctx->za_zero = sizeof(uint32_t) * (M + K + n_row_tiles(M) + 2);  // zeroed by k1_zero (launch_k1)
   ctx->op_at = false;
   if (ops_for(ctx) & OP_AT) {
     ctx->kpad = round_up(K, 32);
@@ -275,7 +276,7 @@ mmmcu_status stage_b(mmmcu_ctx* ctx, const float* B, int64_t K, int64_t N, int64
   const int64_t n_extra = ((ops & OP_TCB) ? n_tc * kw : 0) + ((ops & OP_ROWS) ? n_cnt : 0);
   const size_t zb_bytes = kZbHead * sizeof(unsigned long long) + sizeof(uint32_t) * (2 * K + n_extra);
   MMMCU_CUDA(ctx->zb.ensure(zb_bytes));
-  MMMCU_CUDA(cudaMemsetAsync(ctx->zb.p, 0, zb_bytes, ctx->stream));
+  ctx->zb_zero = zb_bytes;  // zeroed by k1_zero (launch_k1)
   ctx->n_tb = n_tb;
   ctx->n_tc = n_tc;
   if (ops & OP_TCB) {
@@ -410,9 +411,13 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   cudaEventCreate(&ev1);
   cudaEventRecord(ev0, ctx->stream);
 #endif
-  mmmcu::k1_pass<<<k1_grid, mmmcu::kK1Block, k1_smem, ctx->stream>>>(g, z, has_a, has_b,
-                                                                       ctx->stats.as<unsigned long long>());
-  MMMCU_LAUNCHED();
+  if (ctx->za_zero || ctx->zb_zero) {  // one kernel instead of two memsets: the chain stays PDL
+    MMMCU_CUDA(launch_pdl(mmmcu::k1_zero, dim3(64), dim3(256), 0, ctx->stream, ctx->za.as<uint4>(),
+                          (int64_t)((ctx->za_zero + 15) / 16), ctx->zb.as<uint4>(), (int64_t)((ctx->zb_zero + 15) / 16)));
+    ctx->za_zero = ctx->zb_zero = 0;
+  }
+  MMMCU_CUDA(launch_pdl(mmmcu::k1_pass, dim3(k1_grid), dim3(mmmcu::kK1Block), k1_smem, ctx->stream, g, z, has_a,
+                        has_b, ctx->stats.as<unsigned long long>()));
 #ifdef K1_EVT
   cudaEventRecord(ev1, ctx->stream);
   cudaEventSynchronize(ev1);
