@@ -856,7 +856,10 @@ __device__ void k1_plan_totals(const unsigned long long* __restrict__ btot, int6
 // packs kPtSteps steps; steps straddle chunk boundaries freely (positions, not chunks,
 // define a step), so padding is at most 7 k per tile.
 constexpr int kPackThreads = 256;  // k1_pack_rows
-constexpr int kPtSteps = 4;
+#ifndef K1_PT_STEPS
+#define K1_PT_STEPS 4
+#endif
+constexpr int kPtSteps = K1_PT_STEPS;  // step images per K2-TC pack CTA
 constexpr int kPtThreads = 256;
 
 struct PackTcArgs {
