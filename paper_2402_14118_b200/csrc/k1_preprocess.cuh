@@ -194,19 +194,11 @@ __global__ void __launch_bounds__(kK1Threads) k1_row_off(const uint32_t* __restr
 // ------------------------------------------------------------------ fused K1 pass
 // One persistent launch (2 CTAs per SM): tiles [0, nA) are A tiles, [nA, nA + nB) B tiles,
 // CTA b takes tiles b, b + gridDim.x, ...  Rows reach the SM by TMA bulk copies (one per
-// row segment of <= 4 KB) into a ring of kK1Stages 8-row stages, so HBM sees the copies of
+// row segment of <= 4 KB) into a ring of 8-row stages (k1_pass<ST, CTAS>), so HBM sees the copies of
 // the next stages while the warps run the mask / shuffle / A^T work of the current one:
 // thread 0 refills a stage as soon as the 8 warps have read it into registers.  The last
 // CTA to finish (threadfence + done-counter) computes the exact counters, plan statistics
 // and the AUTO path choice.
-#ifndef K1_STAGES
-#define K1_STAGES 2
-#endif
-#ifndef K1_CTAS
-#define K1_CTAS 3
-#endif
-constexpr int kK1Stages = K1_STAGES;
-constexpr int kK1CtasPerSm = K1_CTAS;
 #ifdef K1_PROF
 __device__ unsigned long long* k1_prof = nullptr;  // debug builds: per-CTA globaltimer stamps
 __device__ __forceinline__ unsigned long long k1_now() {
@@ -216,11 +208,12 @@ __device__ __forceinline__ unsigned long long k1_now() {
 }
 #endif
 
-struct K1Ring {
-  float4 buf[kK1Stages][8][kK1Threads];  // 8 rows x 1024 columns per stage (32 KB)
-  uint64_t full[kK1Stages];
-  uint64_t empty[kK1Stages];
-  int64_t tile[kK1Stages];               // the tile this stage's group belongs to (-1: no more)
+template <int ST>
+struct K1RingT {
+  float4 buf[ST][8][kK1Threads];  // 8 rows x 1024 columns per stage (32 KB)
+  uint64_t full[ST];
+  uint64_t empty[ST];
+  int64_t tile[ST];               // the tile this stage's group belongs to (-1: no more)
 };
 
 __device__ __forceinline__ void k1_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -304,7 +297,8 @@ struct K1Cursor {
   }
   __device__ bool done() const { return t >= g->nA + g->nB; }
   // issue this group's row copies into stage slot s, then advance
-  __device__ void issue(K1Ring& r, int s) {
+  template <class R>
+  __device__ void issue(R& r, int s) {
     const K1Args& a = *g;
     const int64_t lim = t < a.nA ? a.M : rend;  // A rows past M are zeros: not read
     const int64_t rows_valid = lim - rb >= 8 ? 8 : (lim - rb > 0 ? lim - rb : 0);
@@ -316,7 +310,8 @@ struct K1Cursor {
     if (rb >= rend) next_tile();
   }
   // no more tiles: one stage tagged -1 tells the compute warps to stop
-  __device__ void finish(K1Ring& r, int s) {
+  template <class R>
+  __device__ void finish(R& r, int s) {
     r.tile[s] = -1;
     mbar_expect(&r.full[s], 0u);
   }
@@ -329,19 +324,20 @@ struct K1Cursor {
 };
 
 // Loader for the tile functions: the next 8-row group from the ring (thread 0 also refills).
-struct K1RingLoader {
-  K1Ring& r;
+template <int ST>
+struct K1RingLoaderT {
+  K1RingT<ST>& r;
   K1Cursor& cur;
   uint32_t J;  // groups consumed
   // the tile of the next group (-1: done); waits for the stage to land
   __device__ int64_t peek() {
-    const int s = J % kK1Stages;
-    k1_wait(&r.full[s], (J / kK1Stages) & 1u);
+    const int s = J % ST;
+    k1_wait(&r.full[s], (J / ST) & 1u);
     return r.tile[s];
   }
   __device__ void rows8(float4 (&v)[8], const float*, int64_t, bool col_ok, int nvalid) {
-    const int s = J % kK1Stages;
-    k1_wait(&r.full[s], (J / kK1Stages) & 1u);
+    const int s = J % ST;
+    k1_wait(&r.full[s], (J / ST) & 1u);
 #pragma unroll
     for (int u = 0; u < 8; ++u)
       v[u] = (col_ok && u < nvalid) ? r.buf[s][u][threadIdx.x] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -351,16 +347,16 @@ struct K1RingLoader {
     if ((threadIdx.x & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
                                                   (uint32_t)__cvta_generic_to_shared(&r.empty[s]))
                                               : "memory");
-    if (threadIdx.x == 0 && !cur.done()) {  // refill this slot with group J + kK1Stages
-      k1_wait(&r.empty[s], (J / kK1Stages) & 1u);
+    if (threadIdx.x == 0 && !cur.done()) {  // refill this slot with group J + ST
+      k1_wait(&r.empty[s], (J / ST) & 1u);
       cur.issue(r, s);
     }
     ++J;
   }
   // x[u][j] = row u, column colofs[j] of the next 8-row group (0 for !ok[j] or u >= nvalid)
   __device__ void rows(float (&x)[8][4], const int (&colofs)[4], const bool (&ok)[4], int nvalid) {
-    const int s = J % kK1Stages;
-    k1_wait(&r.full[s], (J / kK1Stages) & 1u);
+    const int s = J % ST;
+    k1_wait(&r.full[s], (J / ST) & 1u);
     const float* st = reinterpret_cast<const float*>(&r.buf[s][0][0]);
 #pragma unroll
     for (int u = 0; u < 8; ++u)
@@ -582,18 +578,22 @@ __global__ void __launch_bounds__(256) k1_zero(uint4* __restrict__ za, int64_t n
   for (int64_t i = i0; i < nb; i += st) zb[i] = make_uint4(0u, 0u, 0u, 0u);
 }
 
-__global__ void __launch_bounds__(kK1Block, kK1CtasPerSm)
+// ST ring stages of 32 KB per CTA, CTAS CTAs per SM: 2 x 3 for operands of a few thousand
+// tiles (the sweep), 6 x 1 for large ones (cfg4's 2.25 GiB B: K1 1.8 -> 1.3 ms), chosen at
+// launch by the tile count
+template <int ST, int CTAS>
+__global__ void __launch_bounds__(kK1Block, CTAS)
 k1_pass(K1Args g, K1Scratch z, int has_a, int has_b, unsigned long long* __restrict__ stats) {
   tc::pdl_wait();  // launched with programmatic serialization after k1_zero
 #ifdef K1_PROF
   const unsigned long long t_start = k1_now();
 #endif
   extern __shared__ __align__(128) uint8_t k1_raw[];
-  K1Ring& r = *reinterpret_cast<K1Ring*>(k1_raw + ((128 - ((uint32_t)__cvta_generic_to_shared(k1_raw) & 127)) & 127));
+  K1RingT<ST>& r = *reinterpret_cast<K1RingT<ST>*>(k1_raw + ((128 - ((uint32_t)__cvta_generic_to_shared(k1_raw) & 127)) & 127));
   const int64_t M = g.M, K = g.K, nA = g.nA, nB = g.nB, kw = g.kw, nreg = g.nreg;
   K1Cursor cur{&g, &z, (int64_t)blockIdx.x, 0, 0, 0, nullptr, 0, 0};
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kK1Stages; ++s) {
+    for (int s = 0; s < ST; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(&r.full[s])),
                    "r"(1u)
                    : "memory");
@@ -610,16 +610,16 @@ k1_pass(K1Args g, K1Scratch z, int has_a, int has_b, unsigned long long* __restr
       cur.next_tile();
       uint32_t J = 0;
       for (; !cur.done(); ++J) {
-        const int s = J % kK1Stages;
-        k1_wait(&r.empty[s], ((J / kK1Stages) & 1u) ^ 1u);
+        const int s = J % ST;
+        k1_wait(&r.empty[s], ((J / ST) & 1u) ^ 1u);
         cur.issue(r, s);
       }
-      const int s = J % kK1Stages;
-      k1_wait(&r.empty[s], ((J / kK1Stages) & 1u) ^ 1u);
+      const int s = J % ST;
+      k1_wait(&r.empty[s], ((J / ST) & 1u) ^ 1u);
       cur.finish(r, s);
     }
   } else {
-    K1RingLoader ld{r, cur, 0u};
+    K1RingLoaderT<ST> ld{r, cur, 0u};
     for (;;) {
       const int64_t t = ld.peek();
       if (t < 0) break;

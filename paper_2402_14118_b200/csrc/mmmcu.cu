@@ -153,7 +153,8 @@ void set_carveouts(int device) {
   static bool done[64] = {false};
   if (device < 0 || device >= 64 || done[device]) return;
   done[device] = true;
-  max_carveout(mmmcu::k1_pass);
+  max_carveout(mmmcu::k1_pass<2, 3>);
+  max_carveout(mmmcu::k1_pass<6, 1>);
   max_carveout(mmmcu::k1_csr<uint16_t>);
   max_carveout(mmmcu::k1_csr<uint32_t>);
   max_carveout(mmmcu::k1_pack_auto);
@@ -402,9 +403,14 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   if (ctx->num_sms == 0) MMMCU_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
   const mmmcu::K1Args g{ctx->A, ctx->M, K, ctx->lda, ctx->abits.as<uint32_t>(), a_tx, nA,
                         ctx->B, ctx->ldb, ctx->ldb / 64, ctx->bgrp.as<uint32_t>(), b_tx, nB, kw};
-  const int k1_smem = (int)sizeof(mmmcu::K1Ring) + 128;
-  MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k1_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, k1_smem));
-  const unsigned k1_grid = (unsigned)std::min<int64_t>(nA + nB, mmmcu::kK1CtasPerSm * (int64_t)ctx->num_sms);
+  // ring shape: 2 stages x 3 CTAs per SM in general (the sweep's 1024 tiles: 121 vs 134 us;
+  // cfg5's A-heavy 10k tiles: 0.86 vs 1.02 ms), 6 stages x 1 CTA for streams dominated by
+  // many B tiles, which carry no A^T work (cfg4's 18k B tiles: 1.26 vs 1.82 ms) — measured
+  const bool big = nA + nB > 4 * 3 * (int64_t)ctx->num_sms && nB > 4 * nA;
+  auto k1fn = big ? mmmcu::k1_pass<6, 1> : mmmcu::k1_pass<2, 3>;
+  const int k1_smem = (int)(big ? sizeof(mmmcu::K1RingT<6>) : sizeof(mmmcu::K1RingT<2>)) + 128;
+  MMMCU_CUDA(cudaFuncSetAttribute(k1fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k1_smem));
+  const unsigned k1_grid = (unsigned)std::min<int64_t>(nA + nB, (big ? 1 : 3) * (int64_t)ctx->num_sms);
 #ifdef K1_EVT
   cudaEvent_t ev0, ev1;
   cudaEventCreate(&ev0);
@@ -416,8 +422,8 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
                           (int64_t)((ctx->za_zero + 15) / 16), ctx->zb.as<uint4>(), (int64_t)((ctx->zb_zero + 15) / 16)));
     ctx->za_zero = ctx->zb_zero = 0;
   }
-  MMMCU_CUDA(launch_pdl(mmmcu::k1_pass, dim3(k1_grid), dim3(mmmcu::kK1Block), k1_smem, ctx->stream, g, z, has_a,
-                        has_b, ctx->stats.as<unsigned long long>()));
+  MMMCU_CUDA(launch_pdl(k1fn, dim3(k1_grid), dim3(mmmcu::kK1Block), k1_smem, ctx->stream, g, z, has_a, has_b,
+                        ctx->stats.as<unsigned long long>()));
 #ifdef K1_EVT
   cudaEventRecord(ev1, ctx->stream);
   cudaEventSynchronize(ev1);
@@ -434,8 +440,7 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
     cudaMemcpyToSymbol(mmmcu::k1_prof, &dbuf, sizeof(dbuf));
     // rerun (idempotent outputs; counters are re-zeroed by the caller's memsets only once, so
     // use the stamps, not the counters)
-    mmmcu::k1_pass<<<k1_grid, mmmcu::kK1Block, k1_smem, ctx->stream>>>(g, z, has_a, has_b,
-                                                                         ctx->stats.as<unsigned long long>());
+    k1fn<<<k1_grid, mmmcu::kK1Block, k1_smem, ctx->stream>>>(g, z, has_a, has_b, ctx->stats.as<unsigned long long>());
     cudaDeviceSynchronize();
     std::vector<unsigned long long> h(4 * k1_grid);
     cudaMemcpy(h.data(), dbuf, 8 * 4 * k1_grid, cudaMemcpyDeviceToHost);
