@@ -519,7 +519,7 @@ mmmcu_status launch_simt(mmmcu_ctx* ctx, float* C, int64_t ldc, int span_hint, i
   if (ctx->op_at && ctx->op_rows) {
     const int smem = mmmcu::kS2SmemBase + (int)(sizeof(int64_t) * (kw + 1));
     if (smem > 232448) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "K too large for the SIMT v2 kernel");
-    const int64_t row_tiles = ctx->m_at / 128;
+    const int64_t row_tiles = (M + 127) / 128;  // not m_at / 128: A^T is padded to the 256-row TC pairs
     if (row_tiles > 65535) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "M larger than 8388480 rows");
     dim3 grid((unsigned)((Np + 255) / 256), (unsigned)row_tiles);
     if (span_hint == 0) {  // one launch, span (or exit) chosen on the device
