@@ -63,7 +63,9 @@ __device__ unsigned long long* td_prof = nullptr;  // debug builds only: per-CTA
 #endif
 constexpr int kTdTN = TD_TN;
 constexpr int kTdStepFloats = kTdTN * 8 * 2;  // one K1 step image (8 k tf32 or 16 k fp16): hi | lo, 12 KB
-constexpr int kTdThreads = 480;  // warps 0-7 transform, 8-11 accumulators, 12 / 14 producers, 13 MMA
+#ifndef TD_NPROD16
+#define TD_NPROD16 2
+#endif
 constexpr int kTdTM = 128;
 #ifndef TD_SLOTS32
 #define TD_SLOTS32 2
@@ -107,6 +109,11 @@ struct TdCfg {
   // reuse) already completed, which the same-parity waiter guarantees iff both are even (odd
   // counts gave false-positive waits: corrupted A slots with 4 / 5, a hang with 2 / 3).
   static_assert(kStages % 2 == 0 && kSlots % 2 == 0, "alternating roles need even ring sizes");
+  // producer warps 12, 14, 15, ...: stage J goes to producer J % kProd
+  static constexpr int kProd = F16 ? TD_NPROD16 : 2;
+  static_assert(kStages % kProd == 0, "each producer must own whole ring slots");
+  // warps 0-7 transform, 8-11 accumulators, 12 and 14.. producers, 13 MMA
+  static constexpr int kThreads = 32 * (13 + kProd);
 };
 
 template <bool F16>
@@ -160,7 +167,7 @@ __device__ __forceinline__ bool td_dense(int32_t live, int64_t kpad) { return 4 
 // accumulator warps update C for the previous one.  F16: amax / bmax hold the bits of max|A|
 // / max|B| (K1), from which the operand scales and the epilogue's unscale follow.
 template <bool F16>
-__global__ void __launch_bounds__(kTdThreads, 1)
+__global__ void __launch_bounds__(TdCfg<F16>::kThreads, 1)
 k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb, const int32_t* __restrict__ tck,
       const int32_t* __restrict__ tcn, int64_t maxsteps, float* __restrict__ C, int64_t ldc, int64_t M, int64_t N,
       int64_t m_tiles, int64_t n_tiles, const unsigned long long* __restrict__ sel,
@@ -226,7 +233,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
   const uint32_t tbase = sh.tmem_base;
   constexpr uint32_t kPcol = kTdTN, kAcol = 2 * kTdTN;  // TMEM columns of P and of the A slots
 
-  if (warp == 12 || warp == 14) {
+  if (warp == 12 || warp >= 14) {
     // ---------------------------------------------------- producers (B and A per stage)
     // Two warps, producer p = (warp - 12) / 2 fills the stages J with J % 2 == p (one warp's
     // per-stage instruction chain, ~760 cycles, was longer than the stage's 630 MMA cycles).
@@ -240,7 +247,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
     long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const long long p0 = clock64();
 #endif
-    const uint32_t pp = (uint32_t)(warp - 12) >> 1;
+    const uint32_t pp = warp == 12 ? 0u : (uint32_t)(warp - 13);  // producer index
     const uint64_t pol = TD_HINT ? td_policy_evict_last() : 0ull;
     for (int64_t t = unit0; t < ntiles; t += nunits) {
       int64_t ru, tb;
@@ -261,15 +268,16 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
         return (lane < kStageK && pn < npos) ? __ldg(kx + pn) : -1;
       };
       // this producer's stages of the tile: j0, j0 + 2, ... (J advances by the tile's count)
-      const int j0 = (int)((pp + 2u - (J & 1u)) & 1u);
-      int kc = kload(j0), k1 = kload(j0 + 2), k2 = kload(j0 + 4), k3 = kload(j0 + 6);
-      for (int j = j0; j < nstage; j += 2) {
+      constexpr int NP = Cfg::kProd;
+      const int j0 = (int)((pp + NP - (J % NP)) % NP);
+      int kc = kload(j0), k1 = kload(j0 + NP), k2 = kload(j0 + 2 * NP), k3 = kload(j0 + 3 * NP);
+      for (int j = j0; j < nstage; j += NP) {
         const uint32_t Jj = J + (uint32_t)j;
         const int st = Jj % kStages;
         const int kn = k1;
         k1 = k2;
         k2 = k3;
-        k3 = kload(j + 8);
+        k3 = kload(j + 4 * NP);
         const int prev = __shfl_up_sync(0xffffffffu, kc, 1);
         const bool valid = kc >= 0;
         const bool cont = valid && lane > 0 && prev + 1 == kc;

@@ -574,7 +574,7 @@ mmmcu_status launch_tc_t(mmmcu_ctx* ctx, float* C, int64_t ldc, const unsigned l
   MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k2_tc<F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   if (ctx->num_sms == 0) MMMCU_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
   cudaLaunchConfig_t cfg = {};
-  cfg.blockDim = dim3(mmmcu::kTdThreads);
+  cfg.blockDim = dim3(mmmcu::TdCfg<F16>::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = ctx->stream;
   cudaLaunchAttribute attr[2];
