@@ -66,6 +66,11 @@ constexpr int kTdStepFloats = kTdTN * 8 * 2;  // one K1 step image (8 k tf32 or 
 #ifndef TD_NPROD16
 #define TD_NPROD16 2
 #endif
+#ifndef TD_ACC8
+#define TD_ACC8 1  // two accumulator groups (column halves): the segment drain that stalls the MMAs halves
+#endif
+constexpr int kTdAccGroups = TD_ACC8 ? 2 : 1;
+constexpr int kTdXbuf = TD_ACC8 ? 1 : 2;  // C-update staging buffers per accumulator warp
 constexpr int kTdTM = 128;
 #ifndef TD_SLOTS32
 #define TD_SLOTS32 2
@@ -112,8 +117,9 @@ struct TdCfg {
   // producer warps 12, 14, 15, ...: stage J goes to producer J % kProd
   static constexpr int kProd = F16 ? TD_NPROD16 : 2;
   static_assert(kStages % kProd == 0, "each producer must own whole ring slots");
-  // warps 0-7 transform, 8-11 accumulators, 12 and 14.. producers, 13 MMA
-  static constexpr int kThreads = 32 * (13 + kProd);
+  // warps 0-7 transform, 8-11 accumulators, 12 and 14.. producers, 13 MMA, then the second
+  // accumulator group (TD_ACC8)
+  static constexpr int kThreads = 32 * (13 + kProd) + 128 * (kTdAccGroups - 1);
 };
 
 template <bool F16>
@@ -121,7 +127,7 @@ struct TdShared {
   using Cfg = TdCfg<F16>;
   float b[Cfg::kStages][Cfg::kBStageFloats];   // B step images (pair: this CTA's half)
   float a[Cfg::kStages][Cfg::kStageK][kTdTM];  // the stage's live A^T rows
-  float xp[4][2][32][kTdXrow];                 // per accumulator warp: C-update staging, 2 buffers
+  float xp[4 * kTdAccGroups][kTdXbuf][32][kTdXrow];  // per accumulator warp: C-update staging
   uint64_t tma[Cfg::kStages];    // stage data landed (TMA bytes / cp.async arrivals)
   uint64_t empty[Cfg::kStages];  // stage consumed: 4 transform arrivals (one group) + 1 tcgen05.commit
   uint64_t full[Cfg::kSlots];       // A slot written (transform warps; pair: both CTAs')
@@ -176,7 +182,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
   constexpr int kStages = Cfg::kStages, kSub = Cfg::kSub, kStepK = Cfg::kStepK, kStageK = Cfg::kStageK,
                 kSeg = Cfg::kSeg, kTdSlots = Cfg::kSlots;
   constexpr bool kPair = Cfg::kPair;
-  constexpr int kNAccum = kPair ? 8 : 4;    // accumulator warps signalling the MMA issuer (seg_empty)
+  constexpr int kNAccum = (kPair ? 8 : 4) * kTdAccGroups;  // accumulator warps signalling seg_empty
   constexpr int kNXform = kPair ? 8 : 4;    // transform warps signalling the MMA issuer (full): one group
   tc::pdl_wait();  // launched with programmatic serialization after the K1 kernels / gated K2-SIMT
   // (sel is read by both CTAs of a pair: both exit, or neither)
@@ -233,7 +239,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
   const uint32_t tbase = sh.tmem_base;
   constexpr uint32_t kPcol = kTdTN, kAcol = 2 * kTdTN;  // TMEM columns of P and of the A slots
 
-  if (warp == 12 || warp >= 14) {
+  if (warp == 12 || (warp >= 14 && warp < 13 + Cfg::kProd)) {
     // ---------------------------------------------------- producers (B and A per stage)
     // Two warps, producer p = (warp - 12) / 2 fills the stages J with J % 2 == p (one warp's
     // per-stage instruction chain, ~760 cycles, was longer than the stage's 630 MMA cycles).
@@ -468,7 +474,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
     }
 #endif
   } else {
-    // ------------------------------------------------------- accumulator warps 8..11
+    // ------------------------------------------------------- accumulator warps 8..11 (+ 15..18)
     // Thread = tile row r = 32*(w%4) + lane (its TMEM lane).  Per segment: D (fp16: times
     // 2^-(sA+sB), exact) is added into the partial P in TMEM (round-to-nearest; P = D for
     // the first segment), 32 columns per tcgen05.ld, then the MMA issuer may start the next
@@ -479,6 +485,9 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
     // almost at once (a load-add-store C update held that drain, and with it the MMAs, for
     // ~25 us per tile).
     const int q4 = warp & 3;
+    const int ag = warp >= 13 + Cfg::kProd ? 1 : 0;  // accumulator group: columns [96 ag, 96 ag + 96)
+    constexpr int kCh = kTdTN / 32 / kTdAccGroups;   // 32-column chunks per group
+    const int c0 = ag * kCh;
     const uint32_t taddr = tbase + ((uint32_t)(q4 * 32) << 16);
     const float ia = F16 ? tc::exp2_int(-tc::f16_scale_exp(*amax)) : 1.0f;
     const float ib = F16 ? tc::exp2_int(-tc::f16_scale_exp((uint32_t)*bmax)) : 1.0f;
@@ -496,7 +505,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
         else tc::mbar_wait(&sh.seg_full, G & 1u);
         tc::fence_after_sync();
 #pragma unroll 1
-        for (int c = 0; c < kTdTN / 32; ++c) {
+        for (int c = c0; c < c0 + kCh; ++c) {
           uint32_t d[32], p[32];
           tc::tmem_ld32(taddr + 32 * c, d);
           if (g > 0) tc::tmem_ld32(taddr + kPcol + 32 * c, p);
@@ -520,10 +529,13 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       const int64_t row = rt * kTdTM + 32 * q4 + lane, n0 = tb * kTdTN;
       tc::fence_after_sync();
 #pragma unroll 1
-      for (int c = 0; c < kTdTN / 32; ++c, ++R) {
-        float* buf = &sh.xp[q4][R & 1][lane][0];
-        // this thread's reduce from the buffer's previous use (2 chunks ago) has read it
-        if (R >= 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      for (int c = c0; c < c0 + kCh; ++c, ++R) {
+        float* buf = &sh.xp[4 * ag + q4][R % kTdXbuf][lane][0];
+        // this thread's reduce from the buffer's previous use has read it
+        if (R >= (uint32_t)kTdXbuf) {
+          if (kTdXbuf == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
         uint32_t p[32];
         tc::tmem_ld32(taddr + kPcol + 32 * c, p);
         tc::tmem_ld_wait();
