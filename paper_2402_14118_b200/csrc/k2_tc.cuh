@@ -37,10 +37,11 @@
 //     segment).  At the end C = C0 + P, transposed through shared memory so that C is read
 //     and written in coalesced 128-byte rows.
 //
-// Warp roles (480 threads): 0-7 A transform, 8-11 accumulators, 12 and 14 producers (even /
-// odd stages), 13 MMA issuer (the pair leader's; the follower's warp 13 idles).  TMEM (512 columns): D [0,192), P [192,384),
-// 4 A slots [384,512) of 32 columns (per MMA step: hi 8 | lo 8 columns; fp16 packs 2 k per
-// column, even k in the low half).
+// Warp roles (608 threads): 0-7 A transform (two groups, alternate stages), 8-11 and 15-18
+// accumulators (two groups, column halves of D / P), 12 and 14 producers (alternate stages),
+// 13 MMA issuer (the pair leader's; the follower's warp 13 idles).  TMEM (512 columns):
+// D [0,192), P [192,384), 4 A slots [384,512) of 32 columns (per MMA step: hi 8 | lo 8
+// columns; fp16 packs 2 k per column, even k in the low half).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
