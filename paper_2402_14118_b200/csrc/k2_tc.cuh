@@ -33,9 +33,8 @@
 //     Σ|a||b| with 512 tf32 steps, 0.9e-6 with 64).  So k is cut into segments of 64 MMA
 //     steps (1024 k fp16, 512 k tf32); after each, the accumulator warps add D (unscaled by
 //     2^-(sA+sB) for fp16) into the tile's fp32 partial P in TMEM with round-to-nearest adds
-//     (`seg_full` -> `seg_empty`; the MMAs of the next segment wait for the drain, ~5% of a
-//     segment).  At the end C = C0 + P, transposed through shared memory so that C is read
-//     and written in coalesced 128-byte rows.
+//     (`seg_full` -> `seg_empty`; the MMAs of the next segment wait for the drain).  At the
+//     end C += P by bulk reduce-adds from shared memory (the L2 does the fp32 adds).
 //
 // Warp roles (608 threads): 0-7 A transform (two groups, alternate stages), 8-11 and 15-18
 // accumulators (two groups, column halves of D / P), 12 and 14 producers (alternate stages),
