@@ -20,6 +20,12 @@
 #include "k2_simt.cuh"
 #include "k2_tc.cuh"
 
+// K1 pass ring for ordinary operand mixes: stages x CTAs per SM (measured best of 2x3, 3x2, 1x6)
+#ifndef K1_SMALL_ST
+#define K1_SMALL_ST 2
+#define K1_SMALL_CTAS 3
+#endif
+
 namespace {
 
 thread_local std::string g_err;
@@ -153,7 +159,7 @@ void set_carveouts(int device) {
   static bool done[64] = {false};
   if (device < 0 || device >= 64 || done[device]) return;
   done[device] = true;
-  max_carveout(mmmcu::k1_pass<2, 3>);
+  max_carveout(mmmcu::k1_pass<K1_SMALL_ST, K1_SMALL_CTAS>);
   max_carveout(mmmcu::k1_pass<6, 1>);
   max_carveout(mmmcu::k1_csr<uint16_t>);
   max_carveout(mmmcu::k1_csr<uint32_t>);
@@ -407,10 +413,11 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   // cfg5's A-heavy 10k tiles: 0.86 vs 1.02 ms), 6 stages x 1 CTA for streams dominated by
   // many B tiles, which carry no A^T work (cfg4's 18k B tiles: 1.26 vs 1.82 ms) — measured
   const bool big = nA + nB > 4 * 3 * (int64_t)ctx->num_sms && nB > 4 * nA;
-  auto k1fn = big ? mmmcu::k1_pass<6, 1> : mmmcu::k1_pass<2, 3>;
-  const int k1_smem = (int)(big ? sizeof(mmmcu::K1RingT<6>) : sizeof(mmmcu::K1RingT<2>)) + 128;
+  auto k1fn = big ? mmmcu::k1_pass<6, 1> : mmmcu::k1_pass<K1_SMALL_ST, K1_SMALL_CTAS>;
+  const int k1_smem = (int)(big ? sizeof(mmmcu::K1RingT<6>) : sizeof(mmmcu::K1RingT<K1_SMALL_ST>)) + 128;
   MMMCU_CUDA(cudaFuncSetAttribute(k1fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k1_smem));
-  const unsigned k1_grid = (unsigned)std::min<int64_t>(nA + nB, (big ? 1 : 3) * (int64_t)ctx->num_sms);
+  const unsigned k1_grid =
+      (unsigned)std::min<int64_t>(nA + nB, (big ? 1 : K1_SMALL_CTAS) * (int64_t)ctx->num_sms);
 #ifdef K1_EVT
   cudaEvent_t ev0, ev1;
   cudaEventCreate(&ev0);
