@@ -1,5 +1,8 @@
-"""Regenerate the committed evidence under profiles/ from a tools/_capture.sh run
-(gpurun_out/r01_launches.csv, r01_cell_full.ncu-rep, r01_k2tc_sparse.ncu-rep, r01_bench.json).
+"""Regenerate the committed evidence under profiles/ from a tools/capture_evidence.sh run
+(gpurun_out/r01_launches.csv, r01_cell_full.ncu-rep, r01_k2tc_sparse.ncu-rep, r01_bench.json):
+
+    gpurun -- ./tools/capture_evidence.sh   # on the GPU box
+    python tools/make_profiles.py 450      # here
 
     python tools/make_profiles.py <launches per bench step>
 """
