@@ -678,7 +678,10 @@ k1_pass(K1Args g, K1Scratch z, int has_a, int has_b, unsigned long long* __restr
 // offset within its row is the popcount of the row's earlier words; it expands its chunk's
 // set bits through a per-warp smem buffer so the index stores are coalesced.  Index type:
 // uint16 when K <= 65536, else uint32.
-constexpr int kCsrRows = 2;
+#ifndef K1_CSR_ROWS
+#define K1_CSR_ROWS 2
+#endif
+constexpr int kCsrRows = K1_CSR_ROWS;
 
 template <typename Idx>
 __global__ void __launch_bounds__(256) k1_csr(const uint32_t* __restrict__ abits, const uint32_t* __restrict__ arow,
