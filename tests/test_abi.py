@@ -28,6 +28,16 @@ def test_library_loads_and_exports_header_symbols():
     assert lib.mmmcu_abi_version() == 1
 
 
+def test_algo_constants_match_header():
+    # the Python mirror's algorithm ids are the C ABI's mmmcu_algo enum values
+    src = open(os.path.join(ROOT, "include", "mmmcu.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    enum = {k: int(v) for k, v in re.findall(r"\bMMMCU_ALGO_([A-Z0-9_]+)\s*=\s*(\d+)", src)}
+    assert enum["TC"] == 5 and enum["TC32"] == 6
+    for name, value in enum.items():
+        assert getattr(N, "ALGO_" + name) == value, name
+
+
 def test_no_device_fails_loudly_without_fallback():
     torch = pytest.importorskip("torch")
     if torch.cuda.is_available():
