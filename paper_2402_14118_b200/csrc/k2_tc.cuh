@@ -85,7 +85,7 @@ constexpr int kTdTM = 128;
 #define TD_SEGS 32
 #endif
 #ifndef TD_ACC_SLEEP
-#define TD_ACC_SLEEP 256  // ns between the accumulator warps' seg_full polls
+#define TD_ACC_SLEEP 32  // ns between the accumulator warps' seg_full polls (256 measured 1% slower)
 #endif
 #ifndef TD_HINT
 #define TD_HINT 1  // L2 evict_last on the A^T / B-image bulk copies (dense cell 0.31 -> 0.29 ms)
