@@ -348,6 +348,34 @@ def test_stale_and_errors(ctx):
         ctx.preprocess(a.double(), b)
 
 
+def test_split_preprocess_paths(ctx):
+    # preprocess_b / preprocess_a on their own: the K1 scratch of only one
+    # operand is re-zeroed, the gated packs re-run on the device choice, and the plans follow
+    # the new operand (AUTO, K2-TC for these densities; the exact path beside it)
+    M, K, N_ = 512, 768, 640
+    A, B = gen_pair(31, M, K, N_, 0.6, 0.7, 16)
+    A2, B2 = gen_pair(32, M, K, N_, 0.7, 0.6, 8)
+    a, b, a2, b2 = dev(A), dev(B), dev(A2), dev(B2)
+    for algo in (N.ALGO_AUTO, EXACT):
+        ctx.set_algo(algo)
+        ctx.preprocess(a, b)
+        for which, aa, bb, An, Bn in (("b", a, b2, A, B2), ("a", a2, b2, A2, B2)):
+            if which == "b":
+                ctx.preprocess_b_only(bb)
+            else:
+                ctx.preprocess_a_only(aa)
+            c = torch.zeros((M, N_), dtype=torch.float32, device="cuda")
+            cnt = mmm.multiply_mmm(ctx, c, aa, bb)
+            Cr, ocnt = run_oracle(An, Bn)
+            if algo == EXACT:
+                assert bitexact(c.cpu().numpy(), Cr), which
+            else:
+                ok, worst = within_tol(c.cpu().numpy(), Cr, An, Bn)
+                assert ok and worst < 0.5 * TOL, (which, worst)
+            assert_counters(cnt, ocnt)
+    ctx.set_algo(N.ALGO_AUTO)
+
+
 def test_parallel_determinism(ctx):
     # identical bits and counters across runs and worker counts
     A, B = gen_pair(14, 512, 512, 512, 0.8, 0.8, 16)
