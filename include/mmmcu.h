@@ -156,8 +156,14 @@ mmmcu_status mmmcu_export_ablock_index(mmmcu_ctx* ctx, int64_t block_dim, uint8_
 /*
  * multiply_mmm: C (M x N, ldc) += A * B over the masks of the current
  * plan.  A and B must be the preprocessed operands (same pointers, same versions).
- * Each C element receives the ascending-k fmaf chain of its surviving terms, bit-identical
- * to the CPU oracle.  counters may be NULL; filling it synchronises the stream.
+ * Accuracy depends on the algorithm (mmmcu_set_algo):
+ *   MMMCU_ALGO_SIMT_* and MMMCU_ALGO_DENSE: each C element receives the ascending-k fmaf
+ *     chain of its surviving terms, bit-identical to the CPU oracle / reference kernel table;
+ *   MMMCU_ALGO_AUTO (default), MMMCU_ALGO_TC, MMMCU_ALGO_TC32: the north_star tolerance,
+ *     |dC| <= 1e-5 * (|c0| + sum_k |a_ik||b_kj|), not bit-exact (AUTO runs an exact SIMT
+ *     kernel whenever its guards — Inf / NaN / subnormal operands, mixed-scale rows or
+ *     groups — or its cost model say so).
+ * counters may be NULL; filling it synchronises the stream.
  */
 mmmcu_status mmmcu_multiply(mmmcu_ctx* ctx, float* C, int64_t ldc, const float* A, const float* B,
                             uint64_t a_version, uint64_t b_version, mmmcu_counters* counters);
@@ -168,7 +174,8 @@ mmmcu_status mmmcu_multiply_parallel(mmmcu_ctx* ctx, float* C, int64_t ldc, cons
                                      int worker_count, mmmcu_counters* counters);
 /* Force a kernel variant (MMMCU_ALGO_AUTO by default). */
 mmmcu_status mmmcu_set_algo(mmmcu_ctx* ctx, mmmcu_algo algo);
-/* Variant the last mmmcu_multiply ran. */
+/* Variant the last mmmcu_multiply ran (AUTO and SIMT_BCAST resolve to the kernel the
+ * device chose: TC, SIMT_SPAN8 or SIMT_SPAN16; synchronises the stream). */
 mmmcu_status mmmcu_last_algo(mmmcu_ctx* ctx, mmmcu_algo* algo);
 
 /* multiply_simple: dense i-k-j C += A*B, fmaf per term. */

@@ -56,12 +56,20 @@ struct K1Scratch {
   uint32_t* acol;
   uint32_t* tile_sum;     // [ceil(M/32)] non-zeros per 32-row tile (zeroed)
   uint32_t* nonfinite_a;  // set iff A holds an Inf / NaN / subnormal (zeroed): AUTO keeps K2-SIMT
-  uint32_t* amax;         // bits of max|A| (zeroed, atomicMax): K2-TC's fp16 operand scale
+  // fp16-split operand scales and range guard (K2-TC, AUTO): per A row and per 8-column B
+  // group, the bits of max|x| and the complement of the SMALLEST LOCAL MAXIMUM (A: of the
+  // row's 512-column half-tiles, B: of the group's 32-k tiles that hold a non-zero), both
+  // zero-initialised and updated with atomicMax (a complement turns the min into a max)
+  uint32_t* rmax;         // [M]
+  uint32_t* rminc;        // [M]
+  uint32_t* gmax;         // [ldb / 8]
+  uint32_t* gminc;        // [ldb / 8]
+  int64_t ngrp;           // ldb / 8
   int64_t* tile_prefix;   // [ceil(M/32) + 1] exclusive prefix of tile_sum (written by the last CTA)
   uint32_t* bpop;
   uint32_t* bnz;
-  unsigned long long* btot;  // B totals: {Σ non-zero (k, slice), Σ bpop, Σ bnz, Inf/NaN/subnormal seen,
-                             //            bits of max|B|} (zeroed)
+  unsigned long long* btot;  // B totals: {Σ non-zero (k, slice), Σ bpop, Σ bnz, Inf/NaN/subnormal seen}
+                             // (zeroed)
   unsigned int* done;
   unsigned int* next_tile;  // K1 tile counter (dynamic scheduling; reset by the last CTA)
   // K2-TC operands (nullptr when the TC path is not prepared)
@@ -73,6 +81,7 @@ struct K1Scratch {
   int64_t n_tb;           // 256-column tiles of B (K2-SIMT records)
   int64_t n_tc;           // kTcTileN-column tiles of B (K2-TC)
   int choose;             // AUTO: pick K2-SIMT vs K2-TC from the cost model (both operand sets built)
+  int num_sms;            // the device's SM count (cost-model parallelism)
   // K2-SIMT operand: raw non-zero B block rows per (256-column tile, chunk)
   uint32_t* row_cnt;      // [n_tb][kw] non-zero (k, 16-column slice) rows (zeroed)
   int64_t* row_off;       // [n_tb * kw + 1] exclusive prefix of (row_cnt + 3 header rows), 64-byte units
@@ -90,9 +99,10 @@ __device__ void k1_plan_totals(const unsigned long long* __restrict__ btot, int6
 //             measured on the dense 4096^3 cells)
 //   + K1 packing traffic at 0.0433 SM-cycles per byte (HBM): K2-SIMT rows 2 x 64 B per
 //     non-zero (k, slice); K2-TC step images 2 x 768 B per live (k, tile) (fp16 hi | lo);
-//   each divided by min(148 SMs, its CTA count).
+//   each divided by min(#SMs, its CTA count).
 __device__ void k1_choose_path(const K1Scratch& z, int64_t M, int64_t kw, unsigned long long* __restrict__ out) {
   __shared__ unsigned long long s_stage[32], s_live[32];
+  __shared__ uint32_t s_pick;
   unsigned long long st = 0, live = 0;
   {
     // warp per tile: lanes stream the tile's kw mask words (coalesced), warp popc sum
@@ -133,18 +143,33 @@ __device__ void k1_choose_path(const K1Scratch& z, int64_t M, int64_t kw, unsign
                         0.0433 * 128.0 * slice_nz;
     const double tc = rt * (24200.0 * (double)z.n_tc + 940.0 * (double)stages) + 0.0433 * 2.0 * 768.0 * (double)lv;
     // time ~ work / min(SMs, CTAs): short operands leave SMs idle
-    const double par_simt = fmin(148.0, rt * (double)z.n_tb), par_tc = fmin(148.0, rt * (double)z.n_tc);
+    const double sms = (double)z.num_sms;
+    const double par_simt = fmin(sms, rt * (double)z.n_tb), par_tc = fmin(sms, rt * (double)z.n_tc);
     // K2-TC multiplies A's zeros and reads tf32: an Inf / NaN operand would turn 0 * Inf
     // terms the reference never forms into NaN, subnormals would be flushed — keep the
     // exact path
     const bool nonfinite = *z.nonfinite_a != 0u || z.btot[3] != 0ull;
-    // fp16 split: operand scales within [-100, 100] (max|x| within 2^-86 .. 2^114)
-    auto range_ok = [](uint32_t m) {
-      const int e = (int)(m >> 23) - 127;
-      return m == 0u || (e >= -86 && e <= 114);
+    s_pick = (!nonfinite && tc / par_tc < simt / par_simt) ? 1u : 0u;
+  }
+  __syncthreads();
+  // fp16-split range guard, only when K2-TC would be chosen.  The split scales every A row
+  // and every 8-column B group by its own power of two, so a row / group far below the
+  // operand max loses nothing; what it cannot scale away is a MIXED-scale row or group
+  // (parts of it 2^17 or more below its max), whose small part would lose its lo bits
+  // (K2-TC accuracy).  Every row / group must have its max|x| exponent within
+  // [-86, 114] (scale |s| <= 100) and all its local maxima (A: per 512-column half-tile, B:
+  // per 32-k tile) within 2^17 of its max; otherwise AUTO keeps the exact K2-SIMT.
+  if (s_pick) {
+    uint32_t wide = 0u;
+    auto bad = [](uint32_t mx, uint32_t mnc) {
+      if (mx == 0u) return false;  // all-zero row / group: never multiplied
+      const int emax = (int)(mx >> 23) - 127, emin = (int)(~mnc >> 23) - 127;
+      return emax < -86 || emax > 114 || emax - emin > 17;
     };
-    const bool ranged = range_ok(*z.amax) && range_ok((uint32_t)z.btot[4]);
-    if (!nonfinite && ranged && tc / par_tc < simt / par_simt) out[7] = 32ull;
+    for (int64_t i = threadIdx.x; i < M; i += blockDim.x) wide |= bad(z.rmax[i], z.rminc[i]) ? 1u : 0u;
+    for (int64_t g = threadIdx.x; g < z.ngrp; g += blockDim.x) wide |= bad(z.gmax[g], z.gminc[g]) ? 1u : 0u;
+    wide = __syncthreads_or(wide);
+    if (threadIdx.x == 0 && !wide) out[7] = 32ull;
   }
   __syncthreads();
 }
@@ -384,6 +409,11 @@ __device__ __forceinline__ int k1_chunk(int w, int j) { return 2 * w + (j & 1) +
 // subnormals (tf32 operands are flushed).  The tile loops track max / min of the |x| bit
 // patterns; K1 flags them and AUTO keeps K2-SIMT.
 
+// per-row maxima of the current A tile's two 512-column halves (k1_a_tile_b; chunks 2w, 2w+1
+// of warp w lie in the first half, 2w+16, 2w+17 in the second); reset after each tile,
+// initialised by k1_pass before its first tile
+__shared__ uint32_t k1_s_hmax[kK1Rows][2];
+
 template <typename Loader>
 __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, uint32_t* __restrict__ abits, int64_t kw,
                                             const K1Scratch& z, int64_t tx, int64_t ty) {
@@ -399,8 +429,10 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
     ok[j] = col[j] < K;
   }
   uint32_t warp_total = 0;
-  // |x| bit patterns: max (fp16 operand scale; >= 0x7F800000 = Inf / NaN) and min of
-  // |x| - 1 (unsigned: zeros wrap to 0xFFFFFFFF; < 0x7FFFFF = a subnormal)
+  // |x| bit patterns: max (>= 0x7F800000 = Inf / NaN) and min of |x| - 1 (unsigned: zeros wrap
+  // to 0xFFFFFFFF; < 0x7FFFFF = a subnormal) for the operand flags; per row the max of each
+  // 512-column half of the tile, folded over the 8 warps in shared memory, then one atomic
+  // pair per row and tile (row max, smallest half max)
   uint32_t amax_b = 0u, amin_b = 0xFFFFFFFFu;
   __shared__ uint32_t s_ab[kK1Rows][32];  // the tile's bitmap words (row, chunk)
   const int64_t rend = min(r0 + kK1Rows, M);
@@ -411,27 +443,15 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
 #ifdef K1_NOCOMP_A
     continue;
 #endif
-#ifndef K1_NOAT
     if (z.at) {
-#else
-    if (false) {
-#endif
       // A^T tile row k = col holds rows rb..rb+7 at offset rb % 128: two 16-byte stores
       const int64_t rt = rb >> 7;
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         if (col[j] < z.kpad) {
           float4* d4 = reinterpret_cast<float4*>(z.at + (rt * z.kpad + col[j]) * 128 + (rb & 127));
-#ifdef K1_STCS
-          __stcs(d4, make_float4(x[0][j], x[1][j], x[2][j], x[3][j]));
-          __stcs(d4 + 1, make_float4(x[4][j], x[5][j], x[6][j], x[7][j]));
-#elif defined(K1_STWT)
-          __stwt(d4, make_float4(x[0][j], x[1][j], x[2][j], x[3][j]));
-          __stwt(d4 + 1, make_float4(x[4][j], x[5][j], x[6][j], x[7][j]));
-#else
           d4[0] = make_float4(x[0][j], x[1][j], x[2][j], x[3][j]);
           d4[1] = make_float4(x[4][j], x[5][j], x[6][j], x[7][j]);
-#endif
         }
     }
     if (rb >= rend) continue;
@@ -439,20 +459,27 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
     for (int u = 0; u < 8; ++u) {
       const int64_t i = rb + u;
       if (i >= rend) break;
-      uint32_t cnt = 0;
+      uint32_t cnt = 0, hmx[2] = {0u, 0u}, rmn = 0xFFFFFFFFu;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const bool nz = x[u][j] != 0.0f;
         const uint32_t ab = __float_as_uint(x[u][j]) & 0x7FFFFFFFu;
-        amax_b = max(amax_b, ab);
-        amin_b = min(amin_b, ab - 1u);
+        hmx[j >> 1] = max(hmx[j >> 1], ab);
+        rmn = min(rmn, ab - 1u);
         const uint32_t m = __ballot_sync(0xffffffffu, nz);
         cnt += __popc(m);
         if (lane == j) s_ab[i - r0][k1_chunk(w, j)] = m;  // staged: written row-contiguous below
       }
-#ifndef K1_NOATOM
+      if (z.rmax) {  // the warp's part of each 512-column half of the row
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t hm = __reduce_max_sync(0xffffffffu, hmx[h]);
+          if (lane == 0 && hm) atomicMax(&k1_s_hmax[i - r0][h], hm);
+        }
+      }
+      amax_b = max(amax_b, max(hmx[0], hmx[1]));
+      amin_b = min(amin_b, rmn);
       if (lane == 0 && cnt) atomicAdd(&z.arow[i], cnt);
-#endif
       warp_total += cnt;
     }
   }
@@ -460,7 +487,6 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
   {
     const uint32_t mb = __reduce_max_sync(0xffffffffu, amax_b), mn = __reduce_min_sync(0xffffffffu, amin_b);
     if (lane == 0 && (mb >= 0x7F800000u || mn < 0x007FFFFFu)) atomicOr(z.nonfinite_a, 1u);
-    if (lane == 0 && mb && z.amax) atomicMax(z.amax, mb);
   }
   // (per-column non-zero counts, for the WorkCounters only, come from the bitmap on request:
   // k1_acol)
@@ -469,6 +495,17 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
   const int64_t wd = (c0 >> 5) + lane;
   for (int rr = w; rr < kK1Rows; rr += kK1Threads / 32)
     if (r0 + rr < rend && wd < kw) abits[(r0 + rr) * kw + wd] = s_ab[rr][lane];
+  if (threadIdx.x < kK1Rows) {  // per-row range (one atomic pair per row and tile), then reset
+    const int rr = threadIdx.x;
+    const uint32_t h0 = k1_s_hmax[rr][0], h1 = k1_s_hmax[rr][1];
+    if (z.rmax && r0 + rr < rend && (h0 | h1)) {
+      atomicMax(&z.rmax[r0 + rr], max(h0, h1));
+      // smallest non-zero half max of the row
+      atomicMax(&z.rminc[r0 + rr], ~(h0 && h1 ? min(h0, h1) : (h0 | h1)));
+    }
+    k1_s_hmax[rr][0] = 0u;
+    k1_s_hmax[rr][1] = 0u;
+  }
   asm volatile("bar.sync 2, %0;" ::"r"(kK1Threads) : "memory");
 }
 
@@ -501,7 +538,9 @@ __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, 
   for (int j = 0; j < 4; ++j) sel[j] = gj == j ? 0xFFFFFFFFu : 0u;
   const uint32_t gmask = 0xFFu << (8 * gs);
   uint32_t gword = 0;
-  uint32_t amax_b = 0u, amin_b = 0xFFFFFFFFu;  // as in k1_a_tile_b
+  // per-column |x| range as in k1_a_tile_b (lane = column l of chunk j), reduced per 8-column
+  // group at the end of the tile
+  uint32_t cmx[4] = {0u, 0u, 0u, 0u}, cmn[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
   const int64_t kend = min(k0 + 32, K);
   for (int64_t kb = k0; kb < kend; kb += 8) {
     float x[8][4];
@@ -516,8 +555,8 @@ __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, 
       for (int j = 0; j < 4; ++j) {
         m[j] = __ballot_sync(0xffffffffu, x[u][j] != 0.0f);
         const uint32_t ab = __float_as_uint(x[u][j]) & 0x7FFFFFFFu;
-        amax_b = max(amax_b, ab);
-        amin_b = min(amin_b, ab - 1u);
+        cmx[j] = max(cmx[j], ab);
+        cmn[j] = min(cmn[j], ab - 1u);
       }
       const uint32_t mg = (m[0] & sel[0]) | (m[1] & sel[1]) | (m[2] & sel[2]) | (m[3] & sel[3]);  // branch-free
       gword |= (uint32_t)((mg & gmask) != 0) << (uint32_t)(kb - k0 + u);
@@ -540,9 +579,25 @@ __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, 
     nz_w += __shfl_xor_sync(0xffffffffu, nz_w, o);
   }
   {
+    uint32_t amax_b = 0u, amin_b = 0xFFFFFFFFu;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint32_t mx = cmx[j], mn = cmn[j];
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      }
+      const int64_t g = (c0 + 32 * k1_chunk(w, j) + (lane & ~7)) >> 3;  // this lane's 8-column group
+      if (z.gmax && (lane & 7) == 0 && mx && 8 * g < ldb) {  // group max, smallest tile max
+        atomicMax(&z.gmax[g], mx);
+        atomicMax(&z.gminc[g], ~mx);
+      }
+      amax_b = max(amax_b, mx);
+      amin_b = min(amin_b, mn);
+    }
     const uint32_t mb = __reduce_max_sync(0xffffffffu, amax_b), mn = __reduce_min_sync(0xffffffffu, amin_b);
     if (lane == 0 && (mb >= 0x7F800000u || mn < 0x007FFFFFu)) atomicOr(&z.btot[3], 1ull);
-    if (lane == 0 && mb) atomicMax(&z.btot[4], (unsigned long long)mb);
   }
   if (lane == 0 && pop_w) atomicAdd(&z.btot[1], (unsigned long long)pop_w);
   if (lane == 0 && nz_w) atomicAdd(&z.btot[2], (unsigned long long)nz_w);
@@ -602,6 +657,10 @@ k1_pass(K1Args g, K1Scratch z, int has_a, int has_b, unsigned long long* __restr
                    : "memory");
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < kK1Rows) {
+    k1_s_hmax[threadIdx.x][0] = 0u;
+    k1_s_hmax[threadIdx.x][1] = 0u;
   }
   __syncthreads();
   if (threadIdx.x >= kK1Threads) {
@@ -873,8 +932,8 @@ struct PackTcArgs {
   float* tcb;
   int32_t* tck;
   int32_t* tcn;
-  int f16;                            // fp16 split: 16 live k per step, B scaled by 2^sB
-  const unsigned long long* bmax;     // bits of max|B| (K1 pass), fp16 only
+  int f16;                            // fp16 split: 16 live k per step, B group g scaled by 2^sB[g]
+  const uint32_t* gmax;               // bits of max|B| per 8-column group (K1 pass), fp16 only
 };
 
 // CTA (bx = step block, tb = tile) of the K2-TC pack; dynamic smem (2 kw + 1) words.
@@ -947,12 +1006,12 @@ __device__ __forceinline__ void k1_pack_tc_cta(const PackTcArgs& g, int64_t bx, 
     // column half h (96 columns) of B: a tile's images are stored per half, [h][step], a
     // half step = hi image (3 KB) | lo image (3 KB), element (c, j) of column c = n - 96h at
     // byte (c % 8) * 16 + (c / 8) * 256 + (j / 8) * 128 + (j % 8) * 2 of its image
-    const float sb = tc::exp2_int(tc::f16_scale_exp((uint32_t)*g.bmax));
     for (int j = tid; j < kPtSteps * 2 * kTcTileN; j += kPtThreads) {
       const int sl = j / (2 * kTcTileN), q = (j / kTcTileN) & 1, n = j % kTcTileN;
       const int64_t s = s0 + sl;
       if (s >= nsteps) break;
       const bool col_ok = n0 + n < ldb;
+      const float sb = col_ok ? tc::exp2_int(tc::f16_scale_exp(__ldg(g.gmax + ((n0 + n) >> 3)))) : 1.0f;
       float v[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {

@@ -18,9 +18,9 @@
 //           (cp.async, 16 B granules).  B values reach the FMAs as warp broadcasts.
 //
 // Every C element receives fmaf(a_ik, b_kj, c) for its surviving k in ascending order,
-// exactly the oracle's chain (orc_multiply_mmm), so results are bit-identical.  Groups of
-// the 16-column slice whose own code bit is 0 while the sibling group is non-zero are
-// FMA'd with b = +0.0 (exact no-op for finite a and c != -0.0; SPAN=8 avoids even that).
+// exactly the oracle's chain (orc_multiply_mmm), so results are bit-identical.  This v1
+// kernel is only launched with SPAN=8 (each group walks its own mask); the TMA-fed v2 below
+// is the normal exact path.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -298,8 +298,10 @@ k2_dense(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, 
 //           initialised from C).  Per non-zero B row k of its slice the warp issues one
 //           conflict-free LDS.128 of the 4 A values, 4 broadcast LDS.128 of B[k][slice] and
 //           32 FFMA2 predicated on a != 0 — the ascending-k fmaf chain of the oracle.
-//   SPAN  = 16: one walk per slice over the union mask (zero groups add exact +0.0 terms);
-//           8: one walk per 8-column group over its own mask (exact group skipping).
+//   SPAN  = 16: one walk per slice over the union mask, each group's FMAs predicated on its
+//           own code bit; 8: one walk per 8-column group over its own mask.  Both touch set
+//           groups only (kernel_table.cpp:17-20), so Inf / NaN in A and -0.0 in C behave as
+//           in the reference.
 // ====================================================================================
 constexpr int kS2Warps = 16;
 constexpr int kS2Threads = kS2Warps * 32;  // no producer warp: 4 warps/SMSP keep 128 registers
@@ -411,8 +413,11 @@ __device__ __forceinline__ void k2_simt2_body(const float* __restrict__ AT, int6
     for (int s = 0; s < NS; ++s) {
       uint32_t m = NS == 1 ? um : (s == 0 ? g0 : g1);
       // two non-zero B rows per iteration: both rows' loads are issued before the FMAs
-      // (ILP across k); FMAs stay in ascending k, so the per-element fmaf chain is unchanged
-      auto fma_row = [&](const float4& av, const float4 (&bq)[SPAN / 4]) {
+      // (ILP across k); FMAs stay in ascending k, so the per-element fmaf chain is unchanged.
+      // SPAN 16 walks the slice's union mask, so each 8-column group is FMA'd only when ITS
+      // code bit is set (kernel_table.cpp:17-20 touches set groups only): no fma(a, +0, c)
+      // terms, which would turn Inf / NaN a into NaN and -0.0 c into +0.0.
+      auto fma_row = [&](const float4& av, const float4 (&bq)[SPAN / 4], bool live0, bool live1) {
         float2 b[SPAN / 2];
 #pragma unroll
         for (int q = 0; q < SPAN / 4; ++q) {
@@ -422,10 +427,12 @@ __device__ __forceinline__ void k2_simt2_body(const float* __restrict__ AT, int6
         const float a4[4] = {av.x, av.y, av.z, av.w};
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-          if (a4[r] != 0.0f) {
-            const float2 a2 = make_float2(a4[r], a4[r]);
+          const float2 a2 = make_float2(a4[r], a4[r]);
+          const bool anz = a4[r] != 0.0f;
 #pragma unroll
-            for (int q = 0; q < SPAN / 2; ++q) acc[s][r][q] = __ffma2_rn(a2, b[q], acc[s][r][q]);
+          for (int q = 0; q < SPAN / 2; ++q) {
+            const bool live = q < 4 ? live0 : live1;  // group of columns 2q, 2q+1
+            if (anz && live) acc[s][r][q] = __ffma2_rn(a2, b[q], acc[s][r][q]);
           }
         }
       };
@@ -446,8 +453,13 @@ __device__ __forceinline__ void k2_simt2_body(const float* __restrict__ AT, int6
           b1[q] = S.rows[r1][s * (SPAN / 4) + q];
           b2[q] = S.rows[r2][s * (SPAN / 4) + q];
         }
-        fma_row(av1, b1);
-        if (two) fma_row(av2, b2);
+        if (NS == 1) {
+          fma_row(av1, b1, (g0 >> k1) & 1u, (g1 >> k1) & 1u);
+          if (two) fma_row(av2, b2, (g0 >> k2) & 1u, (g1 >> k2) & 1u);
+        } else {  // SPAN 8: m is the group's own mask
+          fma_row(av1, b1, true, true);
+          if (two) fma_row(av2, b2, true, true);
+        }
       }
     }
     __syncwarp();

@@ -8,7 +8,8 @@
 // whole k steps; A's element zeros are multiplied (the tile is dense enough by the choice of
 // this path).  Two operand precisions:
 //   fp16 split (MMMCU_ALGO_TC, AUTO): x = hi + lo with hi = fp16(x * 2^s), lo = fp16(x * 2^s -
-//     hi), s a power-of-two scale per operand from K1's max|A| / max|B| (tc::f16_scale_exp);
+//     hi), s a power-of-two scale per A ROW and per 8-column B GROUP from K1's per-row /
+//     per-group max|x| (tc::f16_scale_exp), undone exactly in the segment drain;
 //     kind::f16 MMAs of K = 16, and CTA pairs (cta_group::2): a pair tile is 256 rows, each
 //     CTA holds its 128 A rows (TMEM) and D rows, and HALF of B's 192 columns in its shared
 //     memory — the leader CTA issues M=256 MMAs that read both halves, so each SM fetches
@@ -170,14 +171,15 @@ __device__ __forceinline__ bool td_dense(int32_t live, int64_t kpad) { return 4 
 // t % m_units, column tile t / m_units), so the CTAs running together share B column tiles
 // (L2 reuse).  Every role walks the same unit sequence with running stage / slot / segment
 // counters, so the producer and the transform warps run into the next tile while the
-// accumulator warps update C for the previous one.  F16: amax / bmax hold the bits of max|A|
-// / max|B| (K1), from which the operand scales and the epilogue's unscale follow.
+// accumulator warps update C for the previous one.  F16: rmax [M] / gmax [ldb/8] hold the bits
+// of max|a| per A row and max|b| per 8-column B group (K1), from which the operand scales and
+// the drain's unscale follow.
 template <bool F16>
 __global__ void __launch_bounds__(TdCfg<F16>::kThreads, 1)
 k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb, const int32_t* __restrict__ tck,
       const int32_t* __restrict__ tcn, int64_t maxsteps, float* __restrict__ C, int64_t ldc, int64_t M, int64_t N,
       int64_t m_tiles, int64_t n_tiles, const unsigned long long* __restrict__ sel,
-      const uint32_t* __restrict__ amax, const unsigned long long* __restrict__ bmax) {
+      const uint32_t* __restrict__ rmax, const uint32_t* __restrict__ gmax) {
   using Cfg = TdCfg<F16>;
   constexpr int kStages = Cfg::kStages, kSub = Cfg::kSub, kStepK = Cfg::kStepK, kStageK = Cfg::kStageK,
                 kSeg = Cfg::kSeg, kTdSlots = Cfg::kSlots;
@@ -406,7 +408,6 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
     // columns and signals the MMA issuer (`full`).
     const int grp = warp >> 2, r = 32 * (warp & 3) + lane;
     const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
-    const float sa = F16 ? tc::exp2_int(tc::f16_scale_exp(*amax)) : 1.0f;
     uint32_t J = 0;
 #ifdef TD_PROF
     long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -419,6 +420,9 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       const int nsteps = nsteps_of(total);
       const int nstage = (nsteps + kSub - 1) / kSub;
       const int j0 = (int)(((uint32_t)grp + 2u - (J & 1u)) & 1u);
+      // fp16: this row's power-of-two scale 2^sA (from its max|a|, K1)
+      const int64_t grow = row_tile(ru) * kTdTM + r;
+      const float sa = F16 ? tc::exp2_int(tc::f16_scale_exp(grow < M ? __ldg(rmax + grow) : 0u)) : 1.0f;
       for (int j = j0; j < nstage; j += 2) {
         const uint32_t Jj = J + (uint32_t)j;
         const int st = Jj % kStages, sl = Jj % kTdSlots;
@@ -489,8 +493,6 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
     constexpr int kCh = kTdTN / 32 / kTdAccGroups;   // 32-column chunks per group
     const int c0 = ag * kCh;
     const uint32_t taddr = tbase + ((uint32_t)(q4 * 32) << 16);
-    const float ia = F16 ? tc::exp2_int(-tc::f16_scale_exp(*amax)) : 1.0f;
-    const float ib = F16 ? tc::exp2_int(-tc::f16_scale_exp((uint32_t)*bmax)) : 1.0f;
     uint32_t G = 0, R = 0;  // segments drained, C chunks reduced
     for (int64_t t = unit0; t < ntiles; t += nunits) {
       int64_t ru, tb;
@@ -500,6 +502,9 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       const int nstage = (nsteps + kSub - 1) / kSub;
       const int nseg = (nstage + kSeg - 1) / kSeg;
       if (nseg == 0) continue;
+      // fp16: undo this row's scale 2^sA and each 8-column group's 2^sB (exact powers of two)
+      const int64_t grow = rt * kTdTM + 32 * q4 + lane;
+      const float ia = F16 ? tc::exp2_int(-tc::f16_scale_exp(grow < M ? __ldg(rmax + grow) : 0u)) : 1.0f;
       for (int g = 0; g < nseg; ++g, ++G) {
         if (TD_ACC_SLEEP > 0) tc::mbar_wait_sleep_ns(&sh.seg_full, G & 1u, TD_ACC_SLEEP);
         else tc::mbar_wait(&sh.seg_full, G & 1u);
@@ -509,13 +514,19 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
           uint32_t d[32], p[32];
           tc::tmem_ld32(taddr + 32 * c, d);
           if (g > 0) tc::tmem_ld32(taddr + kPcol + 32 * c, p);
+          float ib[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int64_t gc = tb * kTdTN + 32 * c + 8 * q;  // 8-column group of this chunk
+            ib[q] = F16 ? tc::exp2_int(-tc::f16_scale_exp(gc < N ? __ldg(gmax + (gc >> 3)) : 0u)) : 1.0f;
+          }
           tc::tmem_ld_wait();
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
             float x = __uint_as_float(d[e]);
             if (F16) x *= ia;  // exact (power of two)
             // p + x*ib in one rounding (x*ib exact): the same value as the add of the product
-            x = g > 0 ? fmaf(x, ib, __uint_as_float(p[e])) : x * ib;
+            x = g > 0 ? fmaf(x, ib[e >> 3], __uint_as_float(p[e])) : x * ib[e >> 3];
             d[e] = __float_as_uint(x);
           }
           tc::tmem_st32(taddr + kPcol + 32 * c, d);

@@ -208,15 +208,20 @@ uint32_t* za_acol(mmmcu_ctx* ctx) { return ctx->za.as<uint32_t>() + ctx->M; }
 uint32_t* za_tiles(mmmcu_ctx* ctx) { return ctx->za.as<uint32_t>() + ctx->M + ctx->Ka; }
 int64_t n_row_tiles(int64_t M) { return (M + mmmcu::kK1Rows - 1) / mmmcu::kK1Rows; }
 unsigned long long* zb_slice(mmmcu_ctx* ctx) { return ctx->zb.as<unsigned long long>(); }
-uint32_t* zb_bpop(mmmcu_ctx* ctx) {
-  return reinterpret_cast<uint32_t*>(ctx->zb.as<unsigned long long>() + 6);  // after kZbHead
+uint32_t* zb_bpop(mmmcu_ctx* ctx) {  // after the head and the group ranges (zb_gmax)
+  return reinterpret_cast<uint32_t*>(ctx->zb.as<unsigned long long>() + 6) + 2 * (ctx->ldb / 8);
 }
 // one word after the A scratch: set iff A holds an Inf / NaN (zeroed with za)
 uint32_t* za_nonfinite(mmmcu_ctx* ctx) { return za_tiles(ctx) + n_row_tiles(ctx->M); }
-// and one more: bits of max|A| (K2-TC's fp16 scale)
-uint32_t* za_amax(mmmcu_ctx* ctx) { return za_nonfinite(ctx) + 1; }
-// zb starts with 6 u64 B totals (k1_preprocess.cuh K1Scratch::btot; [4] = bits of max|B|)
+// then per-row max|a| bits and min-complements (fp16-split scales and range guard)
+uint32_t* za_rmax(mmmcu_ctx* ctx) { return za_nonfinite(ctx) + 1; }
+uint32_t* za_rminc(mmmcu_ctx* ctx) { return za_rmax(ctx) + ctx->M; }
+int64_t za_words(int64_t M, int64_t K) { return M + K + n_row_tiles(M) + 1 + 2 * M; }
+// zb starts with 6 u64 B totals (k1_preprocess.cuh K1Scratch::btot), then per-8-column-group
+// max|b| bits and min-complements, then bpop [K], bnz [K], ...
 constexpr int kZbHead = 6;
+uint32_t* zb_gmax(mmmcu_ctx* ctx) { return reinterpret_cast<uint32_t*>(ctx->zb.as<unsigned long long>() + kZbHead); }
+uint32_t* zb_gminc(mmmcu_ctx* ctx) { return zb_gmax(ctx) + ctx->ldb / 8; }
 uint32_t* zb_bnz(mmmcu_ctx* ctx) { return zb_bpop(ctx) + ctx->Kb; }
 // Operand sets K1 emits for K2: A^T tiles (SIMT v2, TC), raw B rows (SIMT v2), tf32 B step
 // images + live-k lists (TC).
@@ -243,11 +248,11 @@ mmmcu_status stage_a(mmmcu_ctx* ctx, const float* A, int64_t M, int64_t K, int64
   ctx->has_a = false;
   ctx->csr_idx_bytes = K <= 65536 ? 2 : 4;
   MMMCU_CUDA(ctx->abits.ensure(sizeof(uint32_t) * M * kw));
-  MMMCU_CUDA(ctx->za.ensure(sizeof(uint32_t) * (M + K + n_row_tiles(M) + 2)));
+  MMMCU_CUDA(ctx->za.ensure(sizeof(uint32_t) * za_words(M, K)));
   MMMCU_CUDA(ctx->tile_prefix.ensure(sizeof(int64_t) * (n_row_tiles(M) + 1)));
   MMMCU_CUDA(ctx->row_ptr.ensure(sizeof(int64_t) * (M + 1)));
   MMMCU_CUDA(ctx->cols.ensure((size_t)ctx->csr_idx_bytes * M * K));
-  ctx->za_zero = sizeof(uint32_t) * (M + K + n_row_tiles(M) + 2);  // zeroed by k1_zero (launch_k1)
+  ctx->za_zero = sizeof(uint32_t) * za_words(M, K);  // zeroed by k1_zero (launch_k1)
   ctx->op_at = false;
   if (ops_for(ctx) & OP_AT) {
     ctx->kpad = round_up(K, 32);
@@ -271,6 +276,8 @@ mmmcu_status stage_b(mmmcu_ctx* ctx, const float* B, int64_t K, int64_t N, int64
   const int64_t kw = (K + 31) / 32;
   const int64_t nreg = ldb / 64, ngrp = ldb / 8;
   ctx->has_b = false;
+  ctx->ldb = ldb;  // the zb_* scratch offsets depend on it
+  ctx->Kb = K;
   MMMCU_CUDA(ctx->codes.ensure((size_t)K * nreg));
   MMMCU_CUDA(ctx->bgrp.ensure(sizeof(uint32_t) * ngrp * kw));
   ctx->op_rows = ctx->op_tcb = false;
@@ -281,7 +288,7 @@ mmmcu_status stage_b(mmmcu_ctx* ctx, const float* B, int64_t K, int64_t N, int64
   const int64_t n_cnt = n_tb * kw;
   const int64_t n_tc = (ldb + mmmcu::kTcTileN - 1) / mmmcu::kTcTileN;
   const int64_t n_extra = ((ops & OP_TCB) ? n_tc * kw : 0) + ((ops & OP_ROWS) ? n_cnt : 0);
-  const size_t zb_bytes = kZbHead * sizeof(unsigned long long) + sizeof(uint32_t) * (2 * K + n_extra);
+  const size_t zb_bytes = kZbHead * sizeof(unsigned long long) + sizeof(uint32_t) * (2 * (ldb / 8) + 2 * K + n_extra);
   MMMCU_CUDA(ctx->zb.ensure(zb_bytes));
   ctx->zb_zero = zb_bytes;  // zeroed by k1_zero (launch_k1)
   ctx->n_tb = n_tb;
@@ -315,7 +322,7 @@ mmmcu::PackRowsArgs rows_args(mmmcu_ctx* ctx) {
 mmmcu::PackTcArgs tc_args(mmmcu_ctx* ctx, bool f16) {
   return mmmcu::PackTcArgs{ctx->B, ctx->ldb, zb_tlive(ctx), (ctx->Kb + 31) / 32, ctx->tc_steps,
                            ctx->tcb.as<float>(), ctx->tck.as<int32_t>(), ctx->tcn.as<int32_t>(), f16 ? 1 : 0,
-                           zb_slice(ctx) + 4};
+                           zb_gmax(ctx)};
 }
 // AUTO and MMMCU_ALGO_TC use the fp16 split, MMMCU_ALGO_TC32 the tf32 split
 bool tc_f16(const mmmcu_ctx* ctx) { return ctx->algo != MMMCU_ALGO_TC32; }
@@ -392,7 +399,11 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   z.bpop = b_valid ? zb_bpop(ctx) : nullptr;
   z.bnz = b_valid ? zb_bnz(ctx) : nullptr;
   z.btot = b_valid ? zb_slice(ctx) : ctx->stats.as<unsigned long long>() + 16;
-  z.amax = a_valid ? za_amax(ctx) : nullptr;
+  z.rmax = a_valid ? za_rmax(ctx) : nullptr;
+  z.rminc = a_valid ? za_rminc(ctx) : nullptr;
+  z.gmax = b_valid ? zb_gmax(ctx) : nullptr;
+  z.gminc = b_valid ? zb_gminc(ctx) : nullptr;
+  z.ngrp = b_valid ? ctx->ldb / 8 : 0;
   z.done = ctx->ctl.as<unsigned int>();
   z.next_tile = ctx->ctl.as<unsigned int>() + 1;
   z.at = tc_a ? ctx->at.as<float>() : nullptr;
@@ -404,6 +415,8 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   z.n_tb = ctx->n_tb;
   z.n_tc = ctx->n_tc;
   z.choose = gate ? 1 : 0;
+  if (ctx->num_sms == 0) MMMCU_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  z.num_sms = ctx->num_sms;
   const int has_a = a_valid && (same_k || !b_valid) ? 1 : 0;
   const int has_b = b_valid && (same_k || !a_valid) ? 1 : 0;
   if (ctx->num_sms == 0) MMMCU_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
@@ -557,19 +570,12 @@ mmmcu_status launch_simt(mmmcu_ctx* ctx, float* C, int64_t ldc, int span_hint, i
   const int64_t row_tiles = (M + mmmcu::kK2TM - 1) / mmmcu::kK2TM;
   if (row_tiles > 65535) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "M larger than 8388480 rows");
   dim3 grid((unsigned)((Np + mmmcu::kK2TN - 1) / mmmcu::kK2TN), (unsigned)row_tiles);
-  MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k2_simt_bcast<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mmmcu::kK2Smem));
+  // (operands prepared for K2-TC only: the v1 kernel stages its own; span 8 only, because a
+  // 16-column span would FMA zero groups of the slice)
   MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k2_simt_bcast<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mmmcu::kK2Smem));
-  const unsigned long long* sel = span_hint == 0 ? ctx->stats.as<unsigned long long>() + sel_slot : nullptr;
-  if (span_hint == 0 || span_hint == 8) {
-    mmmcu::k2_simt_bcast<8><<<grid, mmmcu::kK2Threads, mmmcu::kK2Smem, ctx->stream>>>(
-        ctx->A, ctx->lda, ctx->B, ctx->ldb, C, ldc, M, K, Np, ctx->bgrp.as<uint32_t>(), kw, sel);
-    MMMCU_LAUNCHED();
-  }
-  if (span_hint == 0 || span_hint == 16) {
-    mmmcu::k2_simt_bcast<16><<<grid, mmmcu::kK2Threads, mmmcu::kK2Smem, ctx->stream>>>(
-        ctx->A, ctx->lda, ctx->B, ctx->ldb, C, ldc, M, K, Np, ctx->bgrp.as<uint32_t>(), kw, sel);
-    MMMCU_LAUNCHED();
-  }
+  mmmcu::k2_simt_bcast<8><<<grid, mmmcu::kK2Threads, mmmcu::kK2Smem, ctx->stream>>>(
+      ctx->A, ctx->lda, ctx->B, ctx->ldb, C, ldc, M, K, Np, ctx->bgrp.as<uint32_t>(), kw, nullptr);
+  MMMCU_LAUNCHED();
   return MMMCU_OK;
 }
 
@@ -613,8 +619,8 @@ mmmcu_status launch_tc_t(mmmcu_ctx* ctx, float* C, int64_t ldc, const unsigned l
     return cudaLaunchKernelEx(&cfg, mmmcu::k2_tc<F16>, (const float*)ctx->at.as<float>(), ctx->kpad,
                               (const float*)ctx->tcb.as<float>(), (const int32_t*)ctx->tck.as<int32_t>(),
                               (const int32_t*)ctx->tcn.as<int32_t>(), (int64_t)ctx->tc_steps, C, ldc, ctx->M, ctx->N,
-                              row_tiles, ctx->n_tc, sel, (const uint32_t*)za_amax(ctx),
-                              (const unsigned long long*)(zb_slice(ctx) + 4));
+                              row_tiles, ctx->n_tc, sel, (const uint32_t*)za_rmax(ctx),
+                              (const uint32_t*)zb_gmax(ctx));
   };
   MMMCU_CUDA(launch());
 #ifdef TD_PROF
@@ -888,11 +894,16 @@ mmmcu_status mmmcu_set_algo(mmmcu_ctx* ctx, mmmcu_algo algo) {
 
 mmmcu_status mmmcu_last_algo(mmmcu_ctx* ctx, mmmcu_algo* algo) {
   if (!ctx || !algo) return fail(ctx, MMMCU_ERR_INVALID_ARG, "null argument");
-  if (ctx->auto_pending) {  // AUTO was resolved on the device: read the choice
+  if (ctx->auto_pending || ctx->last_algo == MMMCU_ALGO_SIMT_BCAST) {  // resolved on the device: read it
     MMMCU_TRY(bind(ctx));
     unsigned long long s[16];
     MMMCU_TRY(read_stats(ctx, s));
-    ctx->last_algo = s[7] == 32 ? MMMCU_ALGO_TC : s[7] == 8 ? MMMCU_ALGO_SIMT_SPAN8 : MMMCU_ALGO_SIMT_SPAN16;
+    if (ctx->auto_pending)
+      ctx->last_algo = s[7] == 32 ? MMMCU_ALGO_TC : s[7] == 8 ? MMMCU_ALGO_SIMT_SPAN8 : MMMCU_ALGO_SIMT_SPAN16;
+    else if (ctx->op_at && ctx->op_rows)  // the K2-SIMT span K1 chose (the v1 fallback runs span 8)
+      ctx->last_algo = s[8] == 8 ? MMMCU_ALGO_SIMT_SPAN8 : MMMCU_ALGO_SIMT_SPAN16;
+    else
+      ctx->last_algo = MMMCU_ALGO_SIMT_SPAN8;
     ctx->auto_pending = false;
   }
   *algo = ctx->last_algo;
@@ -1030,7 +1041,8 @@ mmmcu_status mmmcu_generate(mmmcu_ctx* ctx, float* out, int64_t rows, int64_t co
       !(p >= 0.0 && p <= 1.0))
     return fail(ctx, MMMCU_ERR_INVALID_ARG, "bad generator spec");
   const int64_t total = rows * ld;
-  const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 64);
+  if (ctx->num_sms == 0) MMMCU_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)ctx->num_sms * 64);
   mmmcu::k_generate<<<blocks, 256, 0, ctx->stream>>>(out, rows, cols, ld, row0, seed, value_kind, sigma, thresh, mask_kind, p,
                                                      block);
   MMMCU_LAUNCHED();
