@@ -10,10 +10,12 @@ workload, inputs resident in HBM.  The default workload is BASELINE.json configs
 4096^3 fp32 sparsity sweep, zA x zB in {.6,.7,.8,.9,.95}^2 x B block width {8,16,32}
 (75 cells), uniform[-1,1] values, i.i.d. Bernoulli masks (seeded synthetic data).
 
-Multi-GPU (torchrun, one rank per GPU, NCCL): A/C rows are partitioned across ranks — rank r
-owns global rows [r*M, (r+1)*M) of a (N*M) x K A, so per-GPU work is fixed ("weak") — and the
-B operands are generated on rank 0 and broadcast ONCE with NCCL before timing (reported as
-broadcast_ms).  Each rank computes its own C rows; timing is max over ranks.
+Multi-GPU (--gpus N: one process per GPU, re-launched under torchrun when WORLD_SIZE is not
+set; NCCL): the default workload becomes configs[4] with STRONG scaling — one 32768 x 8192 A
+whose rows are partitioned across the ranks by mmmcu_shard_rows (each rank generates its own
+rows), B generated on rank 0 and broadcast ONCE with NCCL before timing (broadcast_ms) — and
+each rank computes its own C rows; timing is max over ranks.  The N=1 sweep line also carries
+the 1-GPU configs[4] value (cfg5_1gpu) as the same-workload reference of the scaling run.
 
 value     = Σ 2*lane_fma_ops over all ranks / step time     (useful GFLOP/s)
 e2e       = the same metric through the host-buffer public API (mmmcu_multiply_host): H2D of
@@ -216,8 +218,22 @@ def probe_fp32_peak(device):
 
 
 # ----------------------------------------------------------------------------- setup
+def shard_cells(cells, rank, world):
+    """Strong scaling: every cell's A/C rows are partitioned across the
+    ranks with mmmcu_shard_rows; rank r gets rows [r0, r1) of the SAME job.  Returns cells
+    with per-rank M plus each cell's first global row."""
+    import paper_2402_14118_b200 as mmm
+
+    out = []
+    for (label, M, K, N, sa, sb) in cells:
+        r0, r1 = mmm.shard_rows(M, world, rank)
+        out.append((label, r1 - r0, K, N, dict(sa, row0=r0), sb))
+    return out
+
+
 def make_inputs(cells, ctx, rank, world, torch, dist, device):
-    """Generate A shards locally and B on rank 0 (broadcast once).  Returns dicts of tensors."""
+    """Generate this rank's A rows locally (row-offset generator: the rows of the full matrix)
+    and B on rank 0, broadcast once with NCCL.  Returns dicts of tensors."""
     import paper_2402_14118_b200 as mmm
 
     As, Bs = {}, {}
@@ -226,10 +242,11 @@ def make_inputs(cells, ctx, rank, world, torch, dist, device):
         ka = sa["key"]
         if ka not in As:
             lda = mmm.round_up(K, 64)
-            t = torch.empty((M, lda), dtype=torch.float32, device=device)
+            t = torch.empty((max(M, 1), lda), dtype=torch.float32, device=device)
             mmm.generate(t, seed=seed_of(ka), value_kind=sa["value_kind"], sigma=sa["sigma"], thresh=sa["thresh"],
-                         mask_kind=sa["mask_kind"], p=sa["p"], block=sa["block"], cols=K, row0=rank * M, ctx=ctx)
-            As[ka] = t[:, :K]
+                         mask_kind=sa["mask_kind"], p=sa["p"], block=sa["block"], cols=K, row0=sa.get("row0", 0),
+                         ctx=ctx)
+            As[ka] = t[:M, :K]
         kb = sb["key"]
         if kb not in Bs:
             ldb = mmm.round_up(N, 64)
@@ -305,6 +322,36 @@ def run_step(cells, As, Bs, Cs, ctx, torch, events=None):
             events[t][2].record()
 
 
+def quick_measure(workload, ctx, torch, device, steps, warmup):
+    """Device-timed value of another workload on this GPU (the N=1 reference point of the
+    multi-GPU configs[4] run): same step definition, CUDA events, inputs freed afterwards."""
+    cells = workload_cells(workload)
+    As, Bs, _ = make_inputs(cells, ctx, 0, 1, torch, None, device)
+    Cs = {}
+    for (_, M, K, N, sa, sb) in cells:
+        if (M, N) not in Cs:
+            import paper_2402_14118_b200 as mmm
+
+            Cs[(M, N)] = torch.zeros((M, mmm.round_up(N, 64)), dtype=torch.float32, device=device)[:, :N]
+    stats = cell_stats(cells, As, Bs, ctx, torch)
+    for _ in range(warmup):
+        run_step(cells, As, Bs, Cs, ctx, torch)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        run_step(cells, As, Bs, Cs, ctx, torch)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    flops = float(sum(x["flops"] for x in stats))
+    del As, Bs, Cs
+    torch.cuda.empty_cache()
+    return {"workload": workload, "value": round(flops / (ms * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
+            "ms_per_step": round(ms, 4), "steps": steps, "warmup": warmup,
+            "paths": sorted({x["path"] for x in stats})}
+
+
 def count_launches(cells):
     # per cell (AUTO): K1 = k1_zero (scratch) + k1_pass (A and B tiles, last-CTA plan totals / scans / path
     # choice) + k1_csr + k1_pack_auto (both packs in one launch, gated on the device by the
@@ -362,19 +409,40 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", default="sweep")
+    ap.add_argument("--workload", default="",
+                    help="sweep (configs[1]; the N=1 default) | cfg1 | cfg3 | cfg4 | cfg5 (the N>1 default: "
+                         "strong scaling, one 32768-row A partitioned across the ranks)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU work for cpu_baseline")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
     ap.add_argument("--per-cell", default="", help="write per-cell timings (JSON) to this path")
+    ap.add_argument("--no-cfg5-ref", action="store_true", help="N=1: skip the 1-GPU configs[4] reference line")
     args = ap.parse_args()
     warmup = max(args.warmup, 3)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch under torchrun (the driver may also launch us that way)
+        import socket
+
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        raise SystemExit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (launch one rank per GPU)")
+    if not args.workload:
+        args.workload = "sweep" if world == 1 else "cfg5"
     cells = workload_cells(args.workload)
+    strong = world > 1
+    if strong:
+        cells = shard_cells(cells, rank, world)
     metric = "useful GFLOP/s of masked fp32 matmul (60-95% zeros)"
     cfg = {"workload": {"sweep": "configs[1]: 4096^3 fp32 sparsity sweep, zA x zB in {.6,.7,.8,.9,.95}^2 x "
                                   "B block width {8,16,32} (75 cells), uniform[-1,1], i.i.d. Bernoulli masks",
@@ -383,9 +451,17 @@ def main():
                                 "B~N(0,0.02) 32-wide blocks kept p=0.1",
                         "cfg4": "configs[3]: skinny decode 64x12288x49152, A ReLU 95% zeros, B 16-wide blocks kept 0.15",
                         "cfg5": "configs[4]: 32768x8192x8192 per GPU, 0.85/0.85, bw 16"}[args.workload],
-           "cells": len(cells), "rows_per_gpu": cells[0][1], "shard": "A/C rows per rank (weak), B NCCL-broadcast once",
-           "l2": "inputs larger than L2 per cell (A+B+C >= 126 MB for the sweep; consecutive cells use distinct "
-                 "operands)", "global_batch": cells[0][1] * world, "parallelism": f"dp{world} (A/C row shards)"}
+           "cells": len(cells), "rows_per_gpu": cells[0][1],
+           "shard": ("A/C rows partitioned across the ranks (mmmcu_shard_rows, strong scaling: the same job at "
+                     "every N), B generated on rank 0 and NCCL-broadcast once before timing (broadcast_ms)")
+           if strong else "one GPU, whole job",
+           "step": "K1 (preprocess_a + preprocess_b: masks, index lists, codes, B operand pack) + K2 (C += A*B) "
+                   "for every cell",
+           "l2": "inputs larger than L2 per cell (A+B+C >= 126 MB for the sweep; A is shared by the 15 cells of "
+                 "one zA, B by the 5 cells of one (zB, bw), each cell is one preprocess + multiply)",
+           "global_batch": sum(c[1] for c in cells) // max(len(cells), 1) * world if not strong
+           else workload_cells(args.workload)[0][1],
+           "parallelism": f"dp{world} (A/C row shards)"}
 
     if args.impl == "reference":
         return run_reference_arm(args, cells, cfg, metric, world, rank, warmup)
@@ -487,15 +563,19 @@ def main():
               "hbm_peak_gbs": hbm_peak, "hbm_peak_source": hbm_src,
               "hbm_achieved_gbs": round(hbm_bytes / t_meas / 1e9, 1),
               "k1_ms_per_step": round(float(k1_ms.sum()), 4), "k2_ms_per_step": round(float(k2_ms.sum()), 4)}
-    if dominant == "k2_tc" and tensor is not None and tensor["frac"] is not None:
-        # the dominant kernel's own roofline: the tensor pipe (fp16-split MMAs it must issue)
-        roofline = {"bound": "tensor", "achieved": tensor["executed_tflops"], "peak": tensor["peak_tflops"],
-                    "unit": "TFLOP/s", "frac": tensor["frac"], "peak_source": tensor["peak_source"],
-                    "def": tensor["def"] + " (K2 device time per cell from CUDA events in the timed region)",
-                    **common}
-    else:  # K2-SIMT dominant: FP32 pipe on the FMAs it issues ~ useful FLOPs
-        roofline = {"bound": "fp32", "achieved": useful["achieved"], "peak": useful["peak"], "unit": "TFLOP/s",
-                    "frac": useful["frac"], "peak_source": fp32_src, "def": useful["def"], **common}
+    # SURVEY.md §8(d) roofline: per cell T_roof = max(useful flops / P_fp32, algorithmic bytes /
+    # BW_hbm); achieved = useful TFLOP/s over the device time of the step (K1 + K2), peak = the
+    # rate the roofline allows for the same cells (flops / Σ T_roof), so frac = Σ T_roof / Σ T.
+    # The tensor-pipe view of K2-TC (executed fp16-split MMAs vs the bf16 peak) is kept as
+    # roofline.tensor, the K2-only useful rate as roofline.useful.
+    total_flops = float(sum(x["flops"] for x in stats))
+    roofline = {"bound": "fp32+hbm", "achieved": round(total_flops / t_meas / 1e12, 3),
+                "peak": round(total_flops / t_roof / 1e12, 3), "unit": "TFLOP/s",
+                "frac": round(t_roof / t_meas, 4),
+                "def": "SURVEY.md §8(d): per cell max(2*lane_fma_ops / P_fp32, 4*(MK + K_live*N + MN) / BW_hbm); "
+                       "achieved = useful FLOPs / (K1+K2 device time, CUDA events per cell); peak = useful FLOPs / "
+                       "Σ roofline times",
+                "peak_fp32_tflops": round(fp32_peak, 2), "peak_fp32_source": fp32_src, "tensor": tensor, **common}
 
     # ---- e2e through the host-buffer public API
     e2e = None
@@ -519,6 +599,12 @@ def main():
             cpu = {"value": None, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {type(e).__name__}: {e}"}
 
+    # ---- the 1-GPU point of the multi-GPU workload (configs[4]), so the N>1 lines of the
+    # scaling run have a same-workload N=1 reference
+    cfg5_1gpu = None
+    if world == 1 and args.workload == "sweep" and not args.no_cfg5_ref:
+        cfg5_1gpu = quick_measure("cfg5", ctx, torch, device, max(3, args.steps // 4), 3)
+
     if args.per_cell and rank == 0:
         json.dump([dict(s, k1_ms=float(k1_ms[i]), k2_ms=float(k2_ms[i])) for i, s in enumerate(stats)],
                   open(args.per_cell, "w"), indent=1)
@@ -526,12 +612,14 @@ def main():
     if rank == 0:
         line = {
             "metric": metric, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True, "scaling": "weak",
+            "warmup": warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded counter-hash generator, device side)",
             "config": cfg,
             "roofline": roofline,
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": count_launches(cells) * args.steps,
             "broadcast_ms": round(bcast_ms, 3),
+            **({"cfg5_1gpu": cfg5_1gpu} if cfg5_1gpu else {}),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -618,7 +706,8 @@ def run_reference_arm(args, cells, cfg, metric, world, rank, warmup):
             vals.append(flops_total / time_total / 1e9)
     v = float(np.median(vals))
     line = {"impl": "reference", "metric": metric, "value": round(v, 3), "unit": "GFLOP/s", "n_gpus": world,
-            "steps": args.steps, "warmup": warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "steps": args.steps, "warmup": warmup, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (seeded counter-hash generator, host side)", "config": cfg,
             "cpu_baseline": {"value": round(v, 3), "unit": "GFLOP/s", "cores": orc.ref_lib().ref_max_threads(),
                              "kind": "reference",

@@ -221,6 +221,51 @@ mmmcu_status mmmcu_generate(mmmcu_ctx* ctx, float* out, int64_t rows, int64_t co
 
 /* Row partition of a sharded multiply: rank r of `world` owns [*row0, *row1). */
 mmmcu_status mmmcu_shard_rows(int64_t M, int world, int rank, int64_t* row0, int64_t* row1);
+/* Column partition (skinny A): rank r owns columns [*col0, *col1), whole 64-column regions. */
+mmmcu_status mmmcu_shard_cols(int64_t N, int world, int rank, int64_t* col0, int64_t* col1);
+
+/* ---- multi-GPU (one process, one context + stream per GPU; csrc/mmmcu_group.cu) -------
+ *
+ * multiply_parallel's row partition (the reference runs it with OpenMP,
+ * /root/reference/proj/include/mmm/matrix.hpp:170) spread over the GPUs of one box, as
+ * north_star puts it: A/C rows are sharded (mmmcu_shard_rows), B is broadcast ONCE over
+ * NVLink with NCCL (ncclCommInitAll + ncclBroadcast from devices[0]; NCCL is dlopen'ed), and
+ * each GPU runs K1 + K2 on its rows with no further exchange.  A group whose device list
+ * repeats a device replicates with device copies instead (NCCL rejects duplicate devices).
+ */
+typedef struct mmmcu_group mmmcu_group;
+
+mmmcu_status mmmcu_group_create(int ngpus, const int* devices, mmmcu_group** out);
+mmmcu_status mmmcu_group_destroy(mmmcu_group* g);
+const char* mmmcu_group_last_error(const mmmcu_group* g);
+int mmmcu_group_size(const mmmcu_group* g);
+int mmmcu_group_uses_nccl(const mmmcu_group* g);
+/* The per-rank context (device devices[rank]); owned by the group. */
+mmmcu_ctx* mmmcu_group_ctx(mmmcu_group* g, int rank);
+mmmcu_status mmmcu_group_set_algo(mmmcu_group* g, mmmcu_algo algo);
+
+/*
+ * Row-sharded multiply_parallel: C = C + A * B over g ranks.  A_shards[r] / C_shards[r] hold
+ * rows mmmcu_shard_rows(M, g, r) on devices[r] (strides lda / ldc); B (K x N, ldb a multiple
+ * of 64, Matrix layout) lives on devices[0] and is broadcast to the other ranks when its
+ * pointer or b_version changed since the last call (*broadcast_ms = its wall time, 0 when
+ * skipped).  Each rank re-preprocesses only when its operands or versions changed.  Returns
+ * after every rank finished; counters (may be NULL) are summed over the ranks.
+ */
+mmmcu_status mmmcu_multiply_sharded(mmmcu_group* g, float* const* C_shards, int64_t ldc, const float* const* A_shards,
+                                    int64_t lda, const float* B, int64_t ldb, int64_t M, int64_t K, int64_t N,
+                                    uint64_t a_version, uint64_t b_version, mmmcu_counters* counters,
+                                    double* broadcast_ms);
+/*
+ * Column-sharded variant for skinny A (M too small to row-shard, BASELINE configs[3]): rank r
+ * owns columns mmmcu_shard_cols(N, g, r); A (M x K, lda) on devices[0] is broadcast, rank r's
+ * B slab is copied peer-to-peer from B on devices[0], and C_slabs[r] (M x slab width, ldc)
+ * on devices[r] receives C[:, col0:col1] += A * B[:, col0:col1].
+ */
+mmmcu_status mmmcu_multiply_sharded_cols(mmmcu_group* g, float* const* C_slabs, int64_t ldc, const float* A, int64_t lda,
+                                         const float* B, int64_t ldb, int64_t M, int64_t K, int64_t N,
+                                         uint64_t a_version, uint64_t b_version, mmmcu_counters* counters,
+                                         double* broadcast_ms);
 
 #ifdef __cplusplus
 }

@@ -12,6 +12,7 @@ from .api import (  # noqa: F401
     LaneConfig,
     MmmContext,
     MmmError,
+    MmmGroup,
     NoDeviceError,
     PlanStats,
     StaleContextError,
@@ -27,6 +28,7 @@ from .api import (  # noqa: F401
     preprocess_a,
     preprocess_b,
     round_up,
+    shard_cols,
     shard_rows,
 )
 from . import _native  # noqa: F401

@@ -85,6 +85,20 @@ SIGNATURES = [
                                c_double,
                                c_int, c_double, c_int64]),
     ("mmmcu_shard_rows", c_int, [c_int64, c_int, c_int, POINTER(c_int64), POINTER(c_int64)]),
+    ("mmmcu_shard_cols", c_int, [c_int64, c_int, c_int, POINTER(c_int64), POINTER(c_int64)]),
+    ("mmmcu_group_create", c_int, [c_int, POINTER(c_int), POINTER(c_void_p)]),
+    ("mmmcu_group_destroy", c_int, [c_void_p]),
+    ("mmmcu_group_last_error", c_char_p, [c_void_p]),
+    ("mmmcu_group_size", c_int, [c_void_p]),
+    ("mmmcu_group_uses_nccl", c_int, [c_void_p]),
+    ("mmmcu_group_ctx", c_void_p, [c_void_p, c_int]),
+    ("mmmcu_group_set_algo", c_int, [c_void_p, c_int]),
+    ("mmmcu_multiply_sharded", c_int, [c_void_p, POINTER(c_void_p), c_int64, POINTER(c_void_p), c_int64, c_void_p,
+                                       c_int64, c_int64, c_int64, c_int64, c_uint64, c_uint64, POINTER(Counters),
+                                       POINTER(c_double)]),
+    ("mmmcu_multiply_sharded_cols", c_int, [c_void_p, POINTER(c_void_p), c_int64, c_void_p, c_int64, c_void_p,
+                                            c_int64, c_int64, c_int64, c_int64, c_uint64, c_uint64, POINTER(Counters),
+                                            POINTER(c_double)]),
     ("mmmcu_preprocess_host", c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int64, Lane,
                                       c_uint64, c_uint64]),
     ("mmmcu_multiply_planned_host", c_int, [c_void_p, c_void_p, c_int64, c_uint64, c_uint64, c_int,

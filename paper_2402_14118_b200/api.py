@@ -416,6 +416,120 @@ def shard_rows(M: int, world: int, rank: int):
     return r0.value, r1.value
 
 
+def shard_cols(Ncols: int, world: int, rank: int):
+    """Column partition for skinny A (SURVEY.md §8(e) "Other shapes"): whole 64-column regions."""
+    c0, c1 = ctypes.c_int64(), ctypes.c_int64()
+    st = _lib().mmmcu_shard_cols(Ncols, world, rank, ctypes.byref(c0), ctypes.byref(c1))
+    if st != N.OK:
+        _raise(st, _lib().mmmcu_last_error(None).decode())
+    return c0.value, c1.value
+
+
+class MmmGroup:
+    """Single-process multi-GPU group (mmmcu_group_*): one context + stream per device, B (or,
+    column-sharded, A) broadcast with NCCL from devices[0].  Row-sharded calls take per-rank A / C
+    shards on their devices (rows shard_rows(M, g, r))."""
+
+    def __init__(self, devices):
+        lib = _lib()
+        self.devices = [int(d) for d in devices]
+        arr = (ctypes.c_int * len(self.devices))(*self.devices)
+        h = ctypes.c_void_p()
+        st = lib.mmmcu_group_create(len(self.devices), arr, ctypes.byref(h))
+        if st != N.OK:
+            _raise(st, lib.mmmcu_group_last_error(None).decode())
+        self._h = h
+        self.broadcast_ms = 0.0
+
+    def _check(self, status: int):
+        if status != N.OK:
+            _raise(status, _lib().mmmcu_group_last_error(self._h).decode())
+
+    @property
+    def size(self) -> int:
+        return _lib().mmmcu_group_size(self._h)
+
+    @property
+    def uses_nccl(self) -> bool:
+        return bool(_lib().mmmcu_group_uses_nccl(self._h))
+
+    def set_algo(self, algo: int):
+        self._check(_lib().mmmcu_group_set_algo(self._h, int(algo)))
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib().mmmcu_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def multiply_sharded(self, c_shards, a_shards, b, version_a: int = 0, version_b: int = 0) -> WorkCounters:
+        """C_r += A_r * B for every rank r (A_r / C_r = rows shard_rows(M, g, r) on devices[r])."""
+        import torch
+
+        g = self.size
+        if len(c_shards) != g or len(a_shards) != g:
+            raise ValueError(f"need {g} A and C shards")
+        pb, ldb = _check_tensor(b, "b")
+        K, Nn = b.shape
+        M = sum(int(a.shape[0]) for a in a_shards)
+        lda = ldc = None
+        pa, pc = [], []
+        for r, (a, c) in enumerate(zip(a_shards, c_shards)):
+            r0, r1 = shard_rows(M, g, r)
+            if a.shape[0] != r1 - r0 or c.shape[0] != r1 - r0:
+                raise DimensionMismatchError(f"shard {r} must hold rows [{r0}, {r1})")
+            x, la = _check_tensor(a, "a")
+            y, lc = _check_tensor(c, "c")
+            if (lda is not None and la != lda) or (ldc is not None and lc != ldc):
+                raise ValueError("all shards must share one leading dimension")
+            lda, ldc = la, lc
+            pa.append(x)
+            pc.append(y)
+        for d in set(self.devices):
+            torch.cuda.synchronize(d)
+        A = (ctypes.c_void_p * g)(*pa)
+        C = (ctypes.c_void_p * g)(*pc)
+        cnt, ms = N.Counters(), ctypes.c_double()
+        self._check(_lib().mmmcu_multiply_sharded(self._h, C, ldc, A, lda, pb, ldb, M, K, Nn, int(version_a),
+                                                  int(version_b), ctypes.byref(cnt), ctypes.byref(ms)))
+        self.broadcast_ms = ms.value
+        return WorkCounters._from(cnt)
+
+    def multiply_sharded_cols(self, c_slabs, a, b, version_a: int = 0, version_b: int = 0) -> WorkCounters:
+        """C[:, slab r] += A * B[:, slab r] on devices[r] (slabs shard_cols(N, g, r)); A, B on devices[0]."""
+        import torch
+
+        g = self.size
+        pa, lda = _check_tensor(a, "a")
+        pb, ldb = _check_tensor(b, "b")
+        M, K = a.shape
+        Nn = b.shape[1]
+        ldc = None
+        pc = []
+        for r, c in enumerate(c_slabs):
+            c0, c1 = shard_cols(Nn, g, r)
+            y, lc = _check_tensor(c, "c")
+            if c.shape[0] != M or c.shape[1] != c1 - c0:
+                raise DimensionMismatchError(f"slab {r} must be {M} x {c1 - c0}")
+            if ldc is not None and lc != ldc:
+                raise ValueError("all slabs must share one leading dimension")
+            ldc = lc
+            pc.append(y)
+        for d in set(self.devices):
+            torch.cuda.synchronize(d)
+        C = (ctypes.c_void_p * g)(*pc)
+        cnt, ms = N.Counters(), ctypes.c_double()
+        self._check(_lib().mmmcu_multiply_sharded_cols(self._h, C, ldc, pa, lda, pb, ldb, M, K, Nn, int(version_a),
+                                                       int(version_b), ctypes.byref(cnt), ctypes.byref(ms)))
+        self.broadcast_ms = ms.value
+        return WorkCounters._from(cnt)
+
+
 def matrix_seed(seed: int, tag: str) -> int:
     """Per-matrix seed hash_coords(seed, tag) (SURVEY.md §7 hard part 9; rng.hpp:18)."""
     def mix64(x):

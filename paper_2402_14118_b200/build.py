@@ -26,9 +26,9 @@ def build_lib(verbose_ptxas: bool = False) -> str:
     out_dir = os.path.join(HERE, "_lib")
     os.makedirs(out_dir, exist_ok=True)
     out = os.path.join(out_dir, "libmmmcu.so")
-    src = os.path.join(HERE, "csrc", "mmmcu.cu")
+    srcs = [os.path.join(HERE, "csrc", f) for f in ("mmmcu.cu", "mmmcu_group.cu")]
     cmd = [NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-           "-I", os.path.join(ROOT, "include"), "-o", out, src]
+           "-I", os.path.join(ROOT, "include"), "-o", out, *srcs, "-ldl"]
     if verbose_ptxas:
         cmd.insert(1, "-Xptxas=-v")
     _run(cmd)
