@@ -50,26 +50,26 @@ __device__ __forceinline__ uint32_t nz4(float4 v) {
 }
 
 // Zero-initialised per-plan scratch (one cudaMemsetAsync per preprocess):
-//   za = arow[M] | acol[K] | tile_sum[M/32];  zb = btot (3 x u64) | bpop[K] | bnz[K] | ...
+//   za = arow[M] | acol[K] | flags | row ranges;  zb = btot (6 x u64) | group ranges | bpop[K] | bnz[K] | ...
 struct K1Scratch {
   uint32_t* arow;
   uint32_t* acol;
   uint32_t* tile_sum;     // [ceil(M/32)] non-zeros per 32-row tile (zeroed)
   uint32_t* nonfinite_a;  // set iff A holds an Inf / NaN / subnormal (zeroed): AUTO keeps K2-SIMT
+  int64_t* tile_prefix;   // [ceil(M/32) + 1] exclusive prefix of tile_sum (written by the last CTA)
   // fp16-split operand scales and range guard (K2-TC, AUTO): per A row and per 8-column B
   // group, the bits of max|x| and the complement of the SMALLEST LOCAL MAXIMUM (A: of the
-  // row's 512-column half-tiles, B: of the group's 32-k tiles that hold a non-zero), both
-  // zero-initialised and updated with atomicMax (a complement turns the min into a max)
-  uint32_t* rmax;         // [M]
-  uint32_t* rminc;        // [M]
-  uint32_t* gmax;         // [ldb / 8]
-  uint32_t* gminc;        // [ldb / 8]
+  // row's 128-column chunks, B: of the group's 32-k tiles that hold a non-zero), packed in one
+  // zero-initialised 64-bit word (a complement turns the min into a max)
+  unsigned long long* rrng;  // [M]: (max << 32) | ~(smallest 128-column chunk max), k1_fold_range
+  unsigned long long* grng;  // [ldb / 8]: the same per 8-column group over its 32-k tiles
   int64_t ngrp;           // ldb / 8
-  int64_t* tile_prefix;   // [ceil(M/32) + 1] exclusive prefix of tile_sum (written by the last CTA)
+  uint32_t* wide_a;       // set when some A row's range is too wide for the fp16 split (zeroed);
+                          // btot[4] is the same flag for the B groups
   uint32_t* bpop;
   uint32_t* bnz;
-  unsigned long long* btot;  // B totals: {Σ non-zero (k, slice), Σ bpop, Σ bnz, Inf/NaN/subnormal seen}
-                             // (zeroed)
+  unsigned long long* btot;  // B totals: {Σ non-zero (k, slice), Σ bpop, Σ bnz, Inf/NaN/subnormal seen,
+                             //            some group too wide for the fp16 split} (zeroed)
   unsigned int* done;
   unsigned int* next_tile;  // K1 tile counter (dynamic scheduling; reset by the last CTA)
   // K2-TC operands (nullptr when the TC path is not prepared)
@@ -157,20 +157,9 @@ __device__ void k1_choose_path(const K1Scratch& z, int64_t M, int64_t kw, unsign
   // operand max loses nothing; what it cannot scale away is a MIXED-scale row or group
   // (parts of it 2^17 or more below its max), whose small part would lose its lo bits
   // (K2-TC accuracy).  Every row / group must have its max|x| exponent within
-  // [-86, 114] (scale |s| <= 100) and all its local maxima (A: per 512-column half-tile, B:
-  // per 32-k tile) within 2^17 of its max; otherwise AUTO keeps the exact K2-SIMT.
-  if (s_pick) {
-    uint32_t wide = 0u;
-    auto bad = [](uint32_t mx, uint32_t mnc) {
-      if (mx == 0u) return false;  // all-zero row / group: never multiplied
-      const int emax = (int)(mx >> 23) - 127, emin = (int)(~mnc >> 23) - 127;
-      return emax < -86 || emax > 114 || emax - emin > 17;
-    };
-    for (int64_t i = threadIdx.x; i < M; i += blockDim.x) wide |= bad(z.rmax[i], z.rminc[i]) ? 1u : 0u;
-    for (int64_t g = threadIdx.x; g < z.ngrp; g += blockDim.x) wide |= bad(z.gmax[g], z.gminc[g]) ? 1u : 0u;
-    wide = __syncthreads_or(wide);
-    if (threadIdx.x == 0 && !wide) out[7] = 32ull;
-  }
+  // [-86, 114] (scale |s| <= 100) and all its local maxima (A: per 128-column chunk, B: per
+  // 32-k tile) within 2^17 of its max; otherwise AUTO keeps the exact K2-SIMT.
+  if (threadIdx.x == 0 && s_pick && *z.wide_a == 0u && z.btot[4] == 0ull) out[7] = 32ull;
   __syncthreads();
 }
 
@@ -409,10 +398,30 @@ __device__ __forceinline__ int k1_chunk(int w, int j) { return 2 * w + (j & 1) +
 // subnormals (tf32 operands are flushed).  The tile loops track max / min of the |x| bit
 // patterns; K1 flags them and AUTO keeps K2-SIMT.
 
-// per-row maxima of the current A tile's two 512-column halves (k1_a_tile_b; chunks 2w, 2w+1
-// of warp w lie in the first half, 2w+16, 2w+17 in the second); reset after each tile,
-// initialised by k1_pass before its first tile
-__shared__ uint32_t k1_s_hmax[kK1Rows][2];
+// Fold a tile's local maxima (bits of |x|: largest mx, smallest mn) into a row's / group's
+// range word rng = (max << 32) | ~(smallest local max), one 64-bit compare-and-swap, so every
+// update sees the whole state it produced.  Returns true when that state is too wide for the
+// fp16 split (max exponent outside [-86, 114], or local maxima more than 2^17 apart).  The
+// thread whose CAS is the row's / group's last one sees the final range, so a wide final
+// range is always reported; earlier states are narrower, so nothing is reported falsely.
+__device__ __forceinline__ bool k1_fold_range(unsigned long long* rng, uint32_t mx, uint32_t mn) {
+  unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(rng), nv;
+  for (;;) {
+    const uint32_t m = max((uint32_t)(cur >> 32), mx), c = max((uint32_t)cur, ~mn);
+    nv = ((unsigned long long)m << 32) | c;
+    if (nv == cur) break;
+    const unsigned long long seen = atomicCAS(rng, cur, nv);
+    if (seen == cur) break;
+    cur = seen;
+  }
+  const uint32_t cmax = (uint32_t)(nv >> 32), cmin = ~(uint32_t)nv;
+  const int emax = (int)(cmax >> 23) - 127, emin = (int)(cmin >> 23) - 127;
+  return emax < -86 || emax > 114 || emax - emin > 17;
+}
+
+// A tiles: warp w owns the contiguous 128 columns 128w .. 128w+127 (chunks 4w .. 4w+3), so
+// one warp-wide max per row is the max of a contiguous 128-column chunk of the row
+__device__ __forceinline__ int k1_chunk_a(int w, int j) { return 4 * w + j; }
 
 template <typename Loader>
 __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, uint32_t* __restrict__ abits, int64_t kw,
@@ -424,17 +433,17 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
   int64_t col[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    colofs[j] = 32 * k1_chunk(w, j) + lane;
+    colofs[j] = 32 * k1_chunk_a(w, j) + lane;
     col[j] = c0 + colofs[j];
     ok[j] = col[j] < K;
   }
-  uint32_t warp_total = 0;
   // |x| bit patterns: max (>= 0x7F800000 = Inf / NaN) and min of |x| - 1 (unsigned: zeros wrap
   // to 0xFFFFFFFF; < 0x7FFFFF = a subnormal) for the operand flags; per row the max of each
-  // 512-column half of the tile, folded over the 8 warps in shared memory, then one atomic
-  // pair per row and tile (row max, smallest half max)
-  uint32_t amax_b = 0u, amin_b = 0xFFFFFFFFu;
+  // warp's contiguous 128-column chunk (one warp max per row), folded over the 8 warps at the
+  // end of the tile into one atomic pair per row (row max, smallest non-zero chunk max)
+  uint32_t amax_b = 0u, amin_b = 0xFFFFFFFFu, warp_total = 0u;
   __shared__ uint32_t s_ab[kK1Rows][32];  // the tile's bitmap words (row, chunk)
+  __shared__ uint32_t s_cm[kK1Rows][8];   // per row, the max of each warp's 128-column chunk
   const int64_t rend = min(r0 + kK1Rows, M);
   const int64_t rend_at = z.at ? min(r0 + kK1Rows, z.m_at) : rend;
   for (int64_t rb = r0; rb < rend_at; rb += 8) {
@@ -459,25 +468,24 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
     for (int u = 0; u < 8; ++u) {
       const int64_t i = rb + u;
       if (i >= rend) break;
-      uint32_t cnt = 0, hmx[2] = {0u, 0u}, rmn = 0xFFFFFFFFu;
+      uint32_t cnt = 0, rmx = 0u, rmn = 0xFFFFFFFFu;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const bool nz = x[u][j] != 0.0f;
         const uint32_t ab = __float_as_uint(x[u][j]) & 0x7FFFFFFFu;
-        hmx[j >> 1] = max(hmx[j >> 1], ab);
+        rmx = max(rmx, ab);
         rmn = min(rmn, ab - 1u);
         const uint32_t m = __ballot_sync(0xffffffffu, nz);
         cnt += __popc(m);
-        if (lane == j) s_ab[i - r0][k1_chunk(w, j)] = m;  // staged: written row-contiguous below
+        if (lane == j) s_ab[i - r0][k1_chunk_a(w, j)] = m;  // staged: written row-contiguous below
       }
-      if (z.rmax) {  // the warp's part of each 512-column half of the row
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t hm = __reduce_max_sync(0xffffffffu, hmx[h]);
-          if (lane == 0 && hm) atomicMax(&k1_s_hmax[i - r0][h], hm);
-        }
+#ifndef K1_NO_RANGE
+      if (z.rrng) {  // max of the row's 128-column chunk (this warp's columns)
+        const uint32_t cm = __reduce_max_sync(0xffffffffu, rmx);
+        if (lane == 0) s_cm[i - r0][w] = cm;
       }
-      amax_b = max(amax_b, max(hmx[0], hmx[1]));
+#endif
+      amax_b = max(amax_b, rmx);
       amin_b = min(amin_b, rmn);
       if (lane == 0 && cnt) atomicAdd(&z.arow[i], cnt);
       warp_total += cnt;
@@ -493,19 +501,23 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
   // the tile's bitmap words, row by row (32 words = 128 contiguous bytes per row)
   asm volatile("bar.sync 2, %0;" ::"r"(kK1Threads) : "memory");
   const int64_t wd = (c0 >> 5) + lane;
-  for (int rr = w; rr < kK1Rows; rr += kK1Threads / 32)
+  for (int rr = w; rr < kK1Rows; rr += kK1Threads / 32) {
     if (r0 + rr < rend && wd < kw) abits[(r0 + rr) * kw + wd] = s_ab[rr][lane];
-  if (threadIdx.x < kK1Rows) {  // per-row range (one atomic pair per row and tile), then reset
-    const int rr = threadIdx.x;
-    const uint32_t h0 = k1_s_hmax[rr][0], h1 = k1_s_hmax[rr][1];
-    if (z.rmax && r0 + rr < rend && (h0 | h1)) {
-      atomicMax(&z.rmax[r0 + rr], max(h0, h1));
-      // smallest non-zero half max of the row
-      atomicMax(&z.rminc[r0 + rr], ~(h0 && h1 ? min(h0, h1) : (h0 | h1)));
-    }
-    k1_s_hmax[rr][0] = 0u;
-    k1_s_hmax[rr][1] = 0u;
   }
+#ifndef K1_NO_RANGE
+  if (z.rrng && threadIdx.x < kK1Rows && r0 + threadIdx.x < rend) {  // one CAS per row and tile
+    const int rr = threadIdx.x;
+    uint32_t mx = 0u, mn = 0xFFFFFFFFu;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      // chunks past K hold no column: their max stays 0 and is no local max
+      const uint32_t v = (c0 + 128 * q < K) ? s_cm[rr][q] : 0u;
+      mx = max(mx, v);
+      if (v) mn = min(mn, v);
+    }
+    if (mx && k1_fold_range(&z.rrng[r0 + rr], mx, mn)) atomicOr(z.wide_a, 1u);
+  }
+#endif
   asm volatile("bar.sync 2, %0;" ::"r"(kK1Threads) : "memory");
 }
 
@@ -589,10 +601,8 @@ __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, 
         mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
       }
       const int64_t g = (c0 + 32 * k1_chunk(w, j) + (lane & ~7)) >> 3;  // this lane's 8-column group
-      if (z.gmax && (lane & 7) == 0 && mx && 8 * g < ldb) {  // group max, smallest tile max
-        atomicMax(&z.gmax[g], mx);
-        atomicMax(&z.gminc[g], ~mx);
-      }
+      if (z.grng && (lane & 7) == 0 && mx && 8 * g < ldb)  // this tile's max of the group
+        if (k1_fold_range(&z.grng[g], mx, mx)) atomicOr(&z.btot[4], 1ull);
       amax_b = max(amax_b, mx);
       amin_b = min(amin_b, mn);
     }
@@ -658,10 +668,6 @@ k1_pass(K1Args g, K1Scratch z, int has_a, int has_b, unsigned long long* __restr
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (threadIdx.x < kK1Rows) {
-    k1_s_hmax[threadIdx.x][0] = 0u;
-    k1_s_hmax[threadIdx.x][1] = 0u;
-  }
   __syncthreads();
   if (threadIdx.x >= kK1Threads) {
     // TMA producer warp: refill a stage as soon as the 8 compute warps have read it
@@ -715,7 +721,7 @@ k1_pass(K1Args g, K1Scratch z, int has_a, int has_b, unsigned long long* __restr
   // the K2-SIMT record offsets only when K2-SIMT can run (its pack is gated out otherwise)
   if (z.row_cnt && nB > 0 && !(z.choose && stats[7] == 32ull))
     k1_block_exclusive_scan(z.row_cnt, z.n_tb * kw, 3, z.row_off);
-  if (nA > 0) {  // exclusive prefix of the 32-row tile sums for k1_csr's row_ptr
+  if (nA > 0) {  // exclusive prefix of the 32-row tile sums for the CSR's row_ptr (k1_csr_cta)
     const int64_t ntile = (M + kK1Rows - 1) / kK1Rows;
     const uint32_t* ts = z.tile_sum;
     k1_block_scan_fn<uint32_t>(ntile, [&](int64_t i) { return (int64_t)ts[i]; }, z.tile_prefix);
@@ -729,56 +735,59 @@ k1_pass(K1Args g, K1Scratch z, int has_a, int has_b, unsigned long long* __restr
 }
 
 // --------------------------------------------------------------- CSR index lists
-// Per-row ascending index lists (CSR) from the bitmap, no second pass over A.  A CTA owns
-// kCsrRows rows; its 8 warps take the (row, 1024-column chunk) pairs, so a row's chunks are
-// expanded in parallel (one warp walking a row's chunks in turn left the kernel latency-
-// bound: 11 us for a 4096^2 cell).  row_ptr comes from the 32-row tile prefix the K1 pass's
-// last CTA scanned, plus at most 31 row counts: no separate scan launch.  A warp's chunk
-// offset within its row is the popcount of the row's earlier words; it expands its chunk's
-// set bits through a per-warp smem buffer so the index stores are coalesced.  Index type:
-// uint16 when K <= 65536, else uint32.
-#ifndef K1_CSR_ROWS
-#define K1_CSR_ROWS 2
-#endif
-constexpr int kCsrRows = K1_CSR_ROWS;
+// Per-row ascending index lists (CSR: row_ptr int64 [M+1] + columns) from K1's bitmap, no
+// second pass over A: warp ballot words -> popc -> warp prefix sums -> positions.  A CTA owns
+// kCsrRows rows; its 8 warps take the (row, 1024-column chunk) pairs.  row_ptr comes from the
+// 32-row tile prefix the K1 pass's last CTA scanned plus at most 31 row counts; a warp's chunk
+// offset within its row is the popcount of the row's earlier words.  The set bits are
+// expanded by each lane into a per-warp shared staging buffer and copied out coalesced.  In
+// AUTO these CTAs ride in the B pack launch (k1_pack_auto), next to the memory-bound pack
+// CTAs, instead of a launch of their own.
+// Index type: uint16 when K <= 65536, else uint32.
+constexpr int kCsrRows = 2;
 
-template <typename Idx>
-__global__ void __launch_bounds__(256) k1_csr(const uint32_t* __restrict__ abits, const uint32_t* __restrict__ arow,
-                                              const int64_t* __restrict__ tile_prefix, int64_t M, int64_t kw,
-                                              int64_t* __restrict__ row_ptr, Idx* __restrict__ cols) {
+struct CsrArgs {
+  const uint32_t* abits;
+  const uint32_t* arow;
+  const int64_t* tile_prefix;
+  int64_t M, kw;
+  int64_t* row_ptr;
+  void* cols;       // uint16_t or uint32_t
+  int idx_bytes;    // 2 or 4
+};
+
+// stage: dynamic shared memory of (blockDim / 32) x 1024 indices (k1_csr_smem)
+__device__ __forceinline__ void k1_csr_cta(const CsrArgs& g, int64_t cta, void* stage) {
   __shared__ int64_t s_off[kCsrRows + 1];
-  __shared__ Idx s_buf[8][1024];
-  tc::pdl_wait();  // launched with programmatic serialization after k1_pass
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t r0 = (int64_t)blockIdx.x * kCsrRows;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = (int)(blockDim.x >> 5);
+  const int64_t r0 = cta * kCsrRows, M = g.M, kw = g.kw;
   if (warp == 0) {
     const int64_t t0 = (r0 / 32) * 32;  // first row of r0's 32-row tile
     // counts of rows [t0, r0) (lanes 0..r0-t0-1) and of this CTA's rows (lanes 0..kCsrRows-1)
     const int64_t i_pre = t0 + lane;
-    uint32_t pre = (i_pre < r0) ? arow[i_pre] : 0u;
+    uint32_t pre = (i_pre < r0) ? g.arow[i_pre] : 0u;
 #pragma unroll
     for (int o = 16; o; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
     const int64_t i_own = r0 + lane;
-    const uint32_t own = (lane < kCsrRows && i_own < M) ? arow[i_own] : 0u;
+    const uint32_t own = (lane < kCsrRows && i_own < M) ? g.arow[i_own] : 0u;
     uint32_t x = own;
 #pragma unroll
     for (int o = 1; o < kCsrRows; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
       if (lane >= o) x += y;
     }
-    const int64_t base = tile_prefix[r0 / 32] + (int64_t)pre;
+    const int64_t base = g.tile_prefix[r0 / 32] + (int64_t)pre;
     if (lane < kCsrRows) s_off[lane] = base + (int64_t)(x - own);
     if (lane == kCsrRows - 1) s_off[kCsrRows] = base + (int64_t)x;
   }
   __syncthreads();
-  if (threadIdx.x < kCsrRows && r0 + threadIdx.x < M) row_ptr[r0 + threadIdx.x] = s_off[threadIdx.x];
-  if (threadIdx.x == 0 && r0 + kCsrRows >= M) row_ptr[M] = s_off[M - r0];
+  if (threadIdx.x < kCsrRows && r0 + threadIdx.x < M) g.row_ptr[r0 + threadIdx.x] = s_off[threadIdx.x];
+  if (threadIdx.x == 0 && r0 + kCsrRows >= M) g.row_ptr[M] = s_off[M - r0];
   const int64_t nch = (kw + 31) / 32;
-  Idx* buf = s_buf[warp];
-  for (int64_t pr = warp; pr < kCsrRows * nch; pr += 8) {
+  for (int64_t pr = warp; pr < kCsrRows * nch; pr += nwarp) {
     const int64_t rr = pr / nch, ch = pr % nch, row = r0 + rr;
     if (row >= M) break;
-    const uint32_t* bits = abits + row * kw;
+    const uint32_t* bits = g.abits + row * kw;
     const int64_t w = ch * 32 + lane;
     uint32_t word = w < kw ? bits[w] : 0u;
     uint32_t before = 0;  // set bits of the row's earlier chunks
@@ -792,18 +801,37 @@ __global__ void __launch_bounds__(256) k1_csr(const uint32_t* __restrict__ abits
       const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
       if (lane >= o) x += y;
     }
-    uint32_t pos = x - n;
-    while (word) {
-      const int b = __ffs(word) - 1;
-      word &= word - 1;
-      buf[pos++] = (Idx)(w * 32 + b);
-    }
-    const uint32_t total = __shfl_sync(0xffffffffu, x, 31);
-    __syncwarp();
+    // expand the set bits into this warp's shared staging run (lane order = ascending column),
+    // then one coalesced copy of the chunk's list (scattered 2-byte global stores cost the L2
+    // ~20x their bytes in partial-sector writes: measured +25 us per 4096^2 cell)
     const int64_t out = s_off[rr] + before;
-    for (uint32_t i = lane; i < total; i += 32) cols[out + i] = buf[i];
+    const uint32_t col0 = (uint32_t)(w * 32), total = __shfl_sync(0xffffffffu, x, 31);
+    uint32_t pos = x - n;
+    if (g.idx_bytes == 2) {
+      uint16_t* buf = reinterpret_cast<uint16_t*>(stage) + warp * 1024;
+      for (; word; word &= word - 1u) buf[pos++] = (uint16_t)(col0 + (uint32_t)__ffs(word) - 1u);
+      __syncwarp();
+      uint16_t* dst = static_cast<uint16_t*>(g.cols) + out;
+      for (uint32_t i = lane; i < total; i += 32) dst[i] = buf[i];
+    } else {
+      uint32_t* buf = reinterpret_cast<uint32_t*>(stage) + warp * 1024;
+      for (; word; word &= word - 1u) buf[pos++] = col0 + (uint32_t)__ffs(word) - 1u;
+      __syncwarp();
+      uint32_t* dst = static_cast<uint32_t*>(g.cols) + out;
+      for (uint32_t i = lane; i < total; i += 32) dst[i] = buf[i];
+    }
     __syncwarp();
   }
+  __syncthreads();  // s_off is reused by this CTA's next row pair (k1_pack_auto)
+}
+
+// Standalone launch (forced K2 variants, A-only preprocessing).
+__host__ __device__ constexpr int k1_csr_smem(int idx_bytes) { return 8 * 1024 * idx_bytes; }
+
+__global__ void __launch_bounds__(256) k1_csr(CsrArgs g) {
+  extern __shared__ __align__(16) uint8_t csr_stage[];
+  tc::pdl_wait();  // launched with programmatic serialization after k1_pass
+  k1_csr_cta(g, blockIdx.x, csr_stage);
 }
 
 // ---------------------------------------------------------------- counters + stats
@@ -933,7 +961,7 @@ struct PackTcArgs {
   int32_t* tck;
   int32_t* tcn;
   int f16;                            // fp16 split: 16 live k per step, B group g scaled by 2^sB[g]
-  const uint32_t* gmax;               // bits of max|B| per 8-column group (K1 pass), fp16 only
+  const unsigned long long* grng;     // per 8-column group: max|B| bits << 32 | ... (K1 pass), fp16 only
 };
 
 // CTA (bx = step block, tb = tile) of the K2-TC pack; dynamic smem (2 kw + 1) words.
@@ -1011,7 +1039,7 @@ __device__ __forceinline__ void k1_pack_tc_cta(const PackTcArgs& g, int64_t bx, 
       const int64_t s = s0 + sl;
       if (s >= nsteps) break;
       const bool col_ok = n0 + n < ldb;
-      const float sb = col_ok ? tc::exp2_int(tc::f16_scale_exp(__ldg(g.gmax + ((n0 + n) >> 3)))) : 1.0f;
+      const float sb = col_ok ? tc::exp2_int(tc::f16_scale_exp((uint32_t)(__ldg(g.grng + ((n0 + n) >> 3)) >> 32))) : 1.0f;
       float v[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -1128,11 +1156,17 @@ __global__ void __launch_bounds__(kPackThreads) k1_pack_rows(PackRowsArgs g) {
 // gated-out half exits at entry.
 __global__ void __launch_bounds__(kPtThreads)
 k1_pack_auto(PackRowsArgs gr, int64_t rows_x, int64_t n_rows, PackTcArgs gt, int64_t tc_x,
-             const unsigned long long* __restrict__ sel) {
-  // the K2-TC CTAs first: the gated-out K2-SIMT CTAs (the larger part of the grid) exit
-  // behind the work instead of in front of it when TC is chosen
-  tc::pdl_wait();  // launched with programmatic serialization after k1_csr / k1_pass
-  const int64_t bid = blockIdx.x, n_tcb = (int64_t)gridDim.x - n_rows;
+             const unsigned long long* __restrict__ sel, CsrArgs gc, int64_t n_csr) {
+  // CTAs [0, n_csr): the CSR index lists of A (when A was preprocessed); then the K2-TC CTAs:
+  // the gated-out K2-SIMT CTAs (the larger part of the grid) exit behind the work instead of
+  // in front of it when TC is chosen
+  tc::pdl_wait();  // launched with programmatic serialization after k1_pass
+  if ((int64_t)blockIdx.x < n_csr) {
+    extern __shared__ __align__(16) uint32_t pt_smem[];  // (the TC pack's dynamic smem, here the CSR staging)
+    k1_csr_cta(gc, blockIdx.x, pt_smem);
+    return;
+  }
+  const int64_t bid = blockIdx.x - n_csr, n_tcb = (int64_t)gridDim.x - n_csr - n_rows;
   const bool tc = *sel == 32ull;
   if (bid < n_tcb) {
     if (tc) k1_pack_tc_cta(gt, bid % tc_x, bid / tc_x);

@@ -171,15 +171,15 @@ __device__ __forceinline__ bool td_dense(int32_t live, int64_t kpad) { return 4 
 // t % m_units, column tile t / m_units), so the CTAs running together share B column tiles
 // (L2 reuse).  Every role walks the same unit sequence with running stage / slot / segment
 // counters, so the producer and the transform warps run into the next tile while the
-// accumulator warps update C for the previous one.  F16: rmax [M] / gmax [ldb/8] hold the bits
-// of max|a| per A row and max|b| per 8-column B group (K1), from which the operand scales and
-// the drain's unscale follow.
+// accumulator warps update C for the previous one.  F16: the high words of rrng [M] / grng
+// [ldb/8] hold the bits of max|a| per A row and max|b| per 8-column B group (K1), from which
+// the operand scales and the drain's unscale follow.
 template <bool F16>
 __global__ void __launch_bounds__(TdCfg<F16>::kThreads, 1)
 k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb, const int32_t* __restrict__ tck,
       const int32_t* __restrict__ tcn, int64_t maxsteps, float* __restrict__ C, int64_t ldc, int64_t M, int64_t N,
       int64_t m_tiles, int64_t n_tiles, const unsigned long long* __restrict__ sel,
-      const uint32_t* __restrict__ rmax, const uint32_t* __restrict__ gmax) {
+      const unsigned long long* __restrict__ rrng, const unsigned long long* __restrict__ grng) {
   using Cfg = TdCfg<F16>;
   constexpr int kStages = Cfg::kStages, kSub = Cfg::kSub, kStepK = Cfg::kStepK, kStageK = Cfg::kStageK,
                 kSeg = Cfg::kSeg, kTdSlots = Cfg::kSlots;
@@ -422,7 +422,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       const int j0 = (int)(((uint32_t)grp + 2u - (J & 1u)) & 1u);
       // fp16: this row's power-of-two scale 2^sA (from its max|a|, K1)
       const int64_t grow = row_tile(ru) * kTdTM + r;
-      const float sa = F16 ? tc::exp2_int(tc::f16_scale_exp(grow < M ? __ldg(rmax + grow) : 0u)) : 1.0f;
+      const float sa = F16 ? tc::exp2_int(tc::f16_scale_exp(grow < M ? (uint32_t)(__ldg(rrng + grow) >> 32) : 0u)) : 1.0f;
       for (int j = j0; j < nstage; j += 2) {
         const uint32_t Jj = J + (uint32_t)j;
         const int st = Jj % kStages, sl = Jj % kTdSlots;
@@ -504,7 +504,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       if (nseg == 0) continue;
       // fp16: undo this row's scale 2^sA and each 8-column group's 2^sB (exact powers of two)
       const int64_t grow = rt * kTdTM + 32 * q4 + lane;
-      const float ia = F16 ? tc::exp2_int(-tc::f16_scale_exp(grow < M ? __ldg(rmax + grow) : 0u)) : 1.0f;
+      const float ia = F16 ? tc::exp2_int(-tc::f16_scale_exp(grow < M ? (uint32_t)(__ldg(rrng + grow) >> 32) : 0u)) : 1.0f;
       for (int g = 0; g < nseg; ++g, ++G) {
         if (TD_ACC_SLEEP > 0) tc::mbar_wait_sleep_ns(&sh.seg_full, G & 1u, TD_ACC_SLEEP);
         else tc::mbar_wait(&sh.seg_full, G & 1u);
@@ -518,7 +518,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int64_t gc = tb * kTdTN + 32 * c + 8 * q;  // 8-column group of this chunk
-            ib[q] = F16 ? tc::exp2_int(-tc::f16_scale_exp(gc < N ? __ldg(gmax + (gc >> 3)) : 0u)) : 1.0f;
+            ib[q] = F16 ? tc::exp2_int(-tc::f16_scale_exp(gc < N ? (uint32_t)(__ldg(grng + (gc >> 3)) >> 32) : 0u)) : 1.0f;
           }
           tc::tmem_ld_wait();
 #pragma unroll

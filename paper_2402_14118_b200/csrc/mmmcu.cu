@@ -73,7 +73,7 @@ struct mmmcu_ctx {
   int64_t M = 0, Ka = 0, lda = 0;
   uint64_t av = 0;
   int csr_idx_bytes = 4;
-  DevBuf abits, za, tile_prefix, row_ptr, cols;
+  DevBuf abits, za, tile_prefix, row_ptr, cols;  // row_ptr + cols: K1's per-row index lists (CSR)
 
   // ---- B plan (preprocess_b)
   bool has_b = false;
@@ -161,9 +161,8 @@ void set_carveouts(int device) {
   done[device] = true;
   max_carveout(mmmcu::k1_pass<K1_SMALL_ST, K1_SMALL_CTAS>);
   max_carveout(mmmcu::k1_pass<6, 1>);
-  max_carveout(mmmcu::k1_csr<uint16_t>);
-  max_carveout(mmmcu::k1_csr<uint32_t>);
   max_carveout(mmmcu::k1_pack_auto);
+  max_carveout(mmmcu::k1_csr);
   max_carveout(mmmcu::k1_pack_tc);
   max_carveout(mmmcu::k1_pack_rows);
   max_carveout(mmmcu::k1_row_off);
@@ -203,25 +202,24 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 
 // Zeroed scratch of the fused K1 launch: za = [arow M | acol K], zb = [slice_nz u64 |
 // bpop K | bnz K]; ctl = the last-block counter, which the last block resets itself.
-uint32_t* za_arow(mmmcu_ctx* ctx) { return ctx->za.as<uint32_t>(); }
-uint32_t* za_acol(mmmcu_ctx* ctx) { return ctx->za.as<uint32_t>() + ctx->M; }
-uint32_t* za_tiles(mmmcu_ctx* ctx) { return ctx->za.as<uint32_t>() + ctx->M + ctx->Ka; }
+// (the per-row fp16 range words first: 8-byte aligned)
+unsigned long long* za_rrng(mmmcu_ctx* ctx) { return ctx->za.as<unsigned long long>(); }
+uint32_t* za_arow(mmmcu_ctx* ctx) { return reinterpret_cast<uint32_t*>(za_rrng(ctx) + ctx->M); }
+uint32_t* za_acol(mmmcu_ctx* ctx) { return za_arow(ctx) + ctx->M; }
+uint32_t* za_tiles(mmmcu_ctx* ctx) { return za_acol(ctx) + ctx->Ka; }
 int64_t n_row_tiles(int64_t M) { return (M + mmmcu::kK1Rows - 1) / mmmcu::kK1Rows; }
 unsigned long long* zb_slice(mmmcu_ctx* ctx) { return ctx->zb.as<unsigned long long>(); }
-uint32_t* zb_bpop(mmmcu_ctx* ctx) {  // after the head and the group ranges (zb_gmax)
+uint32_t* zb_bpop(mmmcu_ctx* ctx) {  // after the head and the group range words (zb_grng)
   return reinterpret_cast<uint32_t*>(ctx->zb.as<unsigned long long>() + 6) + 2 * (ctx->ldb / 8);
 }
 // one word after the A scratch: set iff A holds an Inf / NaN (zeroed with za)
 uint32_t* za_nonfinite(mmmcu_ctx* ctx) { return za_tiles(ctx) + n_row_tiles(ctx->M); }
-// then per-row max|a| bits and min-complements (fp16-split scales and range guard)
-uint32_t* za_rmax(mmmcu_ctx* ctx) { return za_nonfinite(ctx) + 1; }
-uint32_t* za_rminc(mmmcu_ctx* ctx) { return za_rmax(ctx) + ctx->M; }
-int64_t za_words(int64_t M, int64_t K) { return M + K + n_row_tiles(M) + 1 + 2 * M; }
+uint32_t* za_wide(mmmcu_ctx* ctx) { return za_nonfinite(ctx) + 1; }  // fp16-split range flag
+int64_t za_words(int64_t M, int64_t K) { return 2 * M + M + K + n_row_tiles(M) + 1 + 1; }
 // zb starts with 6 u64 B totals (k1_preprocess.cuh K1Scratch::btot), then per-8-column-group
 // max|b| bits and min-complements, then bpop [K], bnz [K], ...
 constexpr int kZbHead = 6;
-uint32_t* zb_gmax(mmmcu_ctx* ctx) { return reinterpret_cast<uint32_t*>(ctx->zb.as<unsigned long long>() + kZbHead); }
-uint32_t* zb_gminc(mmmcu_ctx* ctx) { return zb_gmax(ctx) + ctx->ldb / 8; }
+unsigned long long* zb_grng(mmmcu_ctx* ctx) { return ctx->zb.as<unsigned long long>() + kZbHead; }
 uint32_t* zb_bnz(mmmcu_ctx* ctx) { return zb_bpop(ctx) + ctx->Kb; }
 // Operand sets K1 emits for K2: A^T tiles (SIMT v2, TC), raw B rows (SIMT v2), tf32 B step
 // images + live-k lists (TC).
@@ -322,7 +320,7 @@ mmmcu::PackRowsArgs rows_args(mmmcu_ctx* ctx) {
 mmmcu::PackTcArgs tc_args(mmmcu_ctx* ctx, bool f16) {
   return mmmcu::PackTcArgs{ctx->B, ctx->ldb, zb_tlive(ctx), (ctx->Kb + 31) / 32, ctx->tc_steps,
                            ctx->tcb.as<float>(), ctx->tck.as<int32_t>(), ctx->tcn.as<int32_t>(), f16 ? 1 : 0,
-                           zb_gmax(ctx)};
+                           zb_grng(ctx)};
 }
 // AUTO and MMMCU_ALGO_TC use the fp16 split, MMMCU_ALGO_TC32 the tf32 split
 bool tc_f16(const mmmcu_ctx* ctx) { return ctx->algo != MMMCU_ALGO_TC32; }
@@ -349,15 +347,24 @@ mmmcu_status pack_tc(mmmcu_ctx* ctx) {
   return MMMCU_OK;
 }
 
-mmmcu_status pack_auto(mmmcu_ctx* ctx, const unsigned long long* sel) {
+mmmcu::CsrArgs csr_args(mmmcu_ctx* ctx) {
+  return mmmcu::CsrArgs{ctx->abits.as<uint32_t>(), za_arow(ctx), ctx->tile_prefix.as<int64_t>(), ctx->M,
+                        (ctx->Ka + 31) / 32, ctx->row_ptr.as<int64_t>(), ctx->cols.p, ctx->csr_idx_bytes};
+}
+int64_t csr_ctas(const mmmcu_ctx* ctx) { return (ctx->M + mmmcu::kCsrRows - 1) / mmmcu::kCsrRows; }
+
+mmmcu_status pack_auto(mmmcu_ctx* ctx, const unsigned long long* sel, bool with_csr) {
   const int smem = pack_tc_smem(ctx);
   if (smem > 200 * 1024) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "K too large for the TC packer");
   const int64_t rows_x = (ctx->Kb + 31) / 32, n_rows = rows_x * ctx->n_tb;
   const int64_t tc_x = (pack_steps(ctx, true) + mmmcu::kPtSteps - 1) / mmmcu::kPtSteps, n_tc = tc_x * ctx->n_tc;
-  if (n_rows + n_tc > 0x7fffffff) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "B too large for one pack launch");
-  MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k1_pack_auto, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  MMMCU_CUDA(launch_pdl(mmmcu::k1_pack_auto, dim3((unsigned)(n_rows + n_tc)), dim3(mmmcu::kPtThreads), smem,
-                        ctx->stream, rows_args(ctx), rows_x, n_rows, tc_args(ctx, true), tc_x, sel));
+  const int64_t n_csr = with_csr ? csr_ctas(ctx) : 0;  // A's CSR CTAs ride in this launch
+  const int smem_all = with_csr ? std::max(smem, mmmcu::k1_csr_smem(ctx->csr_idx_bytes)) : smem;
+  if (n_rows + n_tc + n_csr > 0x7fffffff) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "B too large for one pack launch");
+  MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k1_pack_auto, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_all));
+  MMMCU_CUDA(launch_pdl(mmmcu::k1_pack_auto, dim3((unsigned)(n_rows + n_tc + n_csr)), dim3(mmmcu::kPtThreads), smem_all,
+                        ctx->stream, rows_args(ctx), rows_x, n_rows, tc_args(ctx, true), tc_x, sel, csr_args(ctx),
+                        n_csr));
   MMMCU_LAUNCHED();
   ctx->tcb_f16 = true;
   return MMMCU_OK;
@@ -399,11 +406,10 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   z.bpop = b_valid ? zb_bpop(ctx) : nullptr;
   z.bnz = b_valid ? zb_bnz(ctx) : nullptr;
   z.btot = b_valid ? zb_slice(ctx) : ctx->stats.as<unsigned long long>() + 16;
-  z.rmax = a_valid ? za_rmax(ctx) : nullptr;
-  z.rminc = a_valid ? za_rminc(ctx) : nullptr;
-  z.gmax = b_valid ? zb_gmax(ctx) : nullptr;
-  z.gminc = b_valid ? zb_gminc(ctx) : nullptr;
+  z.rrng = a_valid ? za_rrng(ctx) : nullptr;
+  z.grng = b_valid ? zb_grng(ctx) : nullptr;
   z.ngrp = b_valid ? ctx->ldb / 8 : 0;
+  z.wide_a = a_valid ? za_wide(ctx) : nullptr;
   z.done = ctx->ctl.as<unsigned int>();
   z.next_tile = ctx->ctl.as<unsigned int>() + 1;
   z.at = tc_a ? ctx->at.as<float>() : nullptr;
@@ -479,23 +485,19 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
     cudaMemcpyToSymbol(mmmcu::k1_prof, &zp, sizeof(zp));
   }
 #endif
-  if (do_a) {
-    const unsigned blocks = (unsigned)((ctx->M + mmmcu::kCsrRows - 1) / mmmcu::kCsrRows);
-    const int64_t akw = (ctx->Ka + 31) / 32;
-    if (ctx->csr_idx_bytes == 2)
-      MMMCU_CUDA(launch_pdl(mmmcu::k1_csr<uint16_t>, dim3(blocks), dim3(256), 0, ctx->stream,
-                            (const uint32_t*)ctx->abits.as<uint32_t>(), (const uint32_t*)za_arow(ctx),
-                            (const int64_t*)ctx->tile_prefix.as<int64_t>(), ctx->M, akw, ctx->row_ptr.as<int64_t>(),
-                            ctx->cols.as<uint16_t>()));
-    else
-      MMMCU_CUDA(launch_pdl(mmmcu::k1_csr<uint32_t>, dim3(blocks), dim3(256), 0, ctx->stream,
-                            (const uint32_t*)ctx->abits.as<uint32_t>(), (const uint32_t*)za_arow(ctx),
-                            (const int64_t*)ctx->tile_prefix.as<int64_t>(), ctx->M, akw, ctx->row_ptr.as<int64_t>(),
-                            ctx->cols.as<uint32_t>()));
+#ifdef K1_CSR_SEPARATE
+  const bool csr_alone = do_a;
+#else
+  const bool csr_alone = do_a && !gate;
+#endif
+  if (csr_alone) {  // A's CSR index lists on their own (in AUTO they ride in the pack launch)
+    const int csmem = mmmcu::k1_csr_smem(ctx->csr_idx_bytes);
+    MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k1_csr, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem));
+    MMMCU_CUDA(launch_pdl(mmmcu::k1_csr, dim3((unsigned)csr_ctas(ctx)), dim3(256), csmem, ctx->stream, csr_args(ctx)));
     MMMCU_LAUNCHED();
   }
   if (gate) {
-    MMMCU_TRY(pack_auto(ctx, sel));
+    MMMCU_TRY(pack_auto(ctx, sel, do_a && !csr_alone));
     ctx->rows_fresh = ctx->tcb_fresh = false;
   } else {
     if (rows_b) {
@@ -619,8 +621,8 @@ mmmcu_status launch_tc_t(mmmcu_ctx* ctx, float* C, int64_t ldc, const unsigned l
     return cudaLaunchKernelEx(&cfg, mmmcu::k2_tc<F16>, (const float*)ctx->at.as<float>(), ctx->kpad,
                               (const float*)ctx->tcb.as<float>(), (const int32_t*)ctx->tck.as<int32_t>(),
                               (const int32_t*)ctx->tcn.as<int32_t>(), (int64_t)ctx->tc_steps, C, ldc, ctx->M, ctx->N,
-                              row_tiles, ctx->n_tc, sel, (const uint32_t*)za_rmax(ctx),
-                              (const uint32_t*)zb_gmax(ctx));
+                              row_tiles, ctx->n_tc, sel, (const unsigned long long*)za_rrng(ctx),
+                              (const unsigned long long*)zb_grng(ctx));
   };
   MMMCU_CUDA(launch());
 #ifdef TD_PROF
