@@ -20,6 +20,7 @@
 //   bnz     uint32 [K]              # codes != 0 in row k     (kernel invocations per A nz)
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "tc_ptx.cuh"
@@ -82,6 +83,11 @@ struct K1Scratch {
   int64_t n_tc;           // kTcTileN-column tiles of B (K2-TC)
   int choose;             // AUTO: pick K2-SIMT vs K2-TC from the cost model (both operand sets built)
   int num_sms;            // the device's SM count (cost-model parallelism)
+  // the other halves of the double-buffered scratch, zeroed by this pass for the next plan
+  uint4* zero_a;
+  int64_t zero_a_n;
+  uint4* zero_b;
+  int64_t zero_b_n;
   // K2-SIMT operand: raw non-zero B block rows per (256-column tile, chunk)
   uint32_t* row_cnt;      // [n_tb][kw] non-zero (k, 16-column slice) rows (zeroed)
   int64_t* row_off;       // [n_tb * kw + 1] exclusive prefix of (row_cnt + 3 header rows), 64-byte units
@@ -368,6 +374,8 @@ struct K1RingLoaderT {
     ++J;
   }
   // x[u][j] = row u, column colofs[j] of the next 8-row group (0 for !ok[j] or u >= nvalid)
+  // FULL: all 8 rows and all columns of the group are valid (no per-element selects)
+  template <bool FULL = false>
   __device__ void rows(float (&x)[8][4], const int (&colofs)[4], const bool (&ok)[4], int nvalid) {
     const int s = J % ST;
     k1_wait(&r.full[s], (J / ST) & 1u);
@@ -375,7 +383,8 @@ struct K1RingLoaderT {
 #pragma unroll
     for (int u = 0; u < 8; ++u)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) x[u][j] = (ok[j] && u < nvalid) ? st[u * kK1Cols + colofs[j]] : 0.0f;
+      for (int j = 0; j < 4; ++j)
+        x[u][j] = (FULL || (ok[j] && u < nvalid)) ? st[u * kK1Cols + colofs[j]] : 0.0f;
 #ifndef K1_NOFENCE
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #endif
@@ -444,30 +453,30 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
   uint32_t amax_b = 0u, amin_b = 0xFFFFFFFFu, warp_total = 0u;
   __shared__ uint32_t s_ab[kK1Rows][32];  // the tile's bitmap words (row, chunk)
   __shared__ uint32_t s_cm[kK1Rows][8];   // per row, the max of each warp's 128-column chunk
+  __shared__ uint32_t s_cnt[kK1Rows][8];  // per row, the non-zeros of each warp's chunk
   const int64_t rend = min(r0 + kK1Rows, M);
   const int64_t rend_at = z.at ? min(r0 + kK1Rows, z.m_at) : rend;
-  for (int64_t rb = r0; rb < rend_at; rb += 8) {
+  // one 8-row group: the A^T stores, then per row the ballot words, counts and ranges.  FULL:
+  // all 8 rows and all 1024 columns valid (the common case; no per-element bounds tests)
+  auto group = [&](auto full_tag, int64_t rb, int nvalid) {
+    constexpr bool FULL = decltype(full_tag)::value;
     float x[8][4];
-    ld.rows(x, colofs, ok, rend - rb >= 8 ? 8 : (rend - rb > 0 ? (int)(rend - rb) : 0));
-#ifdef K1_NOCOMP_A
-    continue;
-#endif
+    ld.template rows<FULL>(x, colofs, ok, nvalid);
     if (z.at) {
       // A^T tile row k = col holds rows rb..rb+7 at offset rb % 128: two 16-byte stores
       const int64_t rt = rb >> 7;
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if (col[j] < z.kpad) {
+        if (FULL || col[j] < z.kpad) {
           float4* d4 = reinterpret_cast<float4*>(z.at + (rt * z.kpad + col[j]) * 128 + (rb & 127));
           d4[0] = make_float4(x[0][j], x[1][j], x[2][j], x[3][j]);
           d4[1] = make_float4(x[4][j], x[5][j], x[6][j], x[7][j]);
         }
     }
-    if (rb >= rend) continue;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
+      if (!FULL && u >= nvalid) break;
       const int64_t i = rb + u;
-      if (i >= rend) break;
       uint32_t cnt = 0, rmx = 0u, rmn = 0xFFFFFFFFu;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -487,9 +496,15 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
 #endif
       amax_b = max(amax_b, rmx);
       amin_b = min(amin_b, rmn);
-      if (lane == 0 && cnt) atomicAdd(&z.arow[i], cnt);
+      if (lane == 0) s_cnt[i - r0][w] = cnt;
       warp_total += cnt;
     }
+  };
+  const bool cols_full = c0 + kK1Cols <= K;
+  for (int64_t rb = r0; rb < rend_at; rb += 8) {
+    const int nvalid = rend - rb >= 8 ? 8 : (rend - rb > 0 ? (int)(rend - rb) : 0);
+    if (cols_full && nvalid == 8) group(std::true_type{}, rb, 8);
+    else group(std::false_type{}, rb, nvalid);
   }
   if (lane == 0 && warp_total) atomicAdd(&z.tile_sum[ty], warp_total);
   {
@@ -503,6 +518,12 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
   const int64_t wd = (c0 >> 5) + lane;
   for (int rr = w; rr < kK1Rows; rr += kK1Threads / 32) {
     if (r0 + rr < rend && wd < kw) abits[(r0 + rr) * kw + wd] = s_ab[rr][lane];
+  }
+  if (threadIdx.x < kK1Rows && r0 + threadIdx.x < rend) {  // one count atomic per row and tile
+    uint32_t n = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) n += s_cnt[threadIdx.x][q];
+    if (n) atomicAdd(&z.arow[r0 + threadIdx.x], n);
   }
 #ifndef K1_NO_RANGE
   if (z.rrng && threadIdx.x < kK1Rows && r0 + threadIdx.x < rend) {  // one CAS per row and tile
@@ -554,9 +575,11 @@ __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, 
   // group at the end of the tile
   uint32_t cmx[4] = {0u, 0u, 0u, 0u}, cmn[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
   const int64_t kend = min(k0 + 32, K);
+  const bool cols_full = c0 + kK1Cols <= ldb;
   for (int64_t kb = k0; kb < kend; kb += 8) {
     float x[8][4];
-    ld.rows(x, colofs, ok, kend - kb >= 8 ? 8 : (int)(kend - kb));
+    if (cols_full && kend - kb >= 8) ld.template rows<true>(x, colofs, ok, 8);
+    else ld.rows(x, colofs, ok, kend - kb >= 8 ? 8 : (int)(kend - kb));
 #ifdef K1_NOCOMP_B
     continue;
 #endif
@@ -634,22 +657,18 @@ __global__ void k1_codes_export(const uint32_t* __restrict__ bgrp, int64_t K, in
   codes[t] = (uint8_t)code;
 }
 
-// Zero the K1 scratch (A part, B part; 16-byte words, either may be empty) — launched
-// with programmatic serialization, after the previous call's last kernel.
-__global__ void __launch_bounds__(256) k1_zero(uint4* __restrict__ za, int64_t na, uint4* __restrict__ zb, int64_t nb) {
-  tc::pdl_wait();
-  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, st = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = i0; i < na; i += st) za[i] = make_uint4(0u, 0u, 0u, 0u);
-  for (int64_t i = i0; i < nb; i += st) zb[i] = make_uint4(0u, 0u, 0u, 0u);
-}
-
 // ST ring stages of 32 KB per CTA, CTAS CTAs per SM: 2 x 3 for operands of a few thousand
 // tiles (the sweep), 6 x 1 for large ones (cfg4's 2.25 GiB B: K1 1.8 -> 1.3 ms), chosen at
 // launch by the tile count
 template <int ST, int CTAS>
 __global__ void __launch_bounds__(kK1Block, CTAS)
 k1_pass(K1Args g, K1Scratch z, int has_a, int has_b, unsigned long long* __restrict__ stats) {
-  tc::pdl_wait();  // launched with programmatic serialization after k1_zero
+  tc::pdl_wait();  // launched with programmatic serialization after the previous call's last kernel
+  {  // the next plan's scratch halves (nothing reads them any more: the previous kernels are done)
+    const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, st = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = i0; i < z.zero_a_n; i += st) z.zero_a[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int64_t i = i0; i < z.zero_b_n; i += st) z.zero_b[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
 #ifdef K1_PROF
   const unsigned long long t_start = k1_now();
 #endif

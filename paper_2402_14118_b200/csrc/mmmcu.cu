@@ -90,7 +90,13 @@ struct mmmcu_ctx {
   int ops_b = 0;                                // operand sets B was staged for
   int64_t kpad = 0, m_at = 0, n_tb = 0, n_tc = 0, tc_steps = 0;
   int tc_pairs = 0;  // co-resident K2-TC CTA pairs (cudaOccupancyMaxActiveClusters), 0 = not queried
-  size_t za_zero = 0, zb_zero = 0;  // bytes of the K1 scratch to zero before the next K1 pass
+  // K1 scratch (zeroed, atomically accumulated) is double-buffered: a plan uses half p of za /
+  // zb while its K1 pass zeroes the other half for the next plan, so no zeroing launch or
+  // memset sits in the per-call chain.  clean[h]: half h is known to be zero.
+  size_t za_half = 0, zb_half = 0;  // bytes per half
+  int pa = 0, pb = 0;
+  bool za_clean[2] = {false, false}, zb_clean[2] = {false, false};
+  bool zero_a_next = false, zero_b_next = false;  // the coming K1 pass zeroes the other half
   DevBuf at, tcb, tck, tcn, brows, row_off;
 
   // ---- statistics: u64 [16] = {inv, lanes, skipped, zreg, nnzA, pop, zero_codes, span, slice_nz}
@@ -203,14 +209,16 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 // Zeroed scratch of the fused K1 launch: za = [arow M | acol K], zb = [slice_nz u64 |
 // bpop K | bnz K]; ctl = the last-block counter, which the last block resets itself.
 // (the per-row fp16 range words first: 8-byte aligned)
-unsigned long long* za_rrng(mmmcu_ctx* ctx) { return ctx->za.as<unsigned long long>(); }
+uint8_t* za_base(mmmcu_ctx* ctx) { return ctx->za.as<uint8_t>() + ctx->pa * ctx->za_half; }
+uint8_t* zb_base(mmmcu_ctx* ctx) { return ctx->zb.as<uint8_t>() + ctx->pb * ctx->zb_half; }
+unsigned long long* za_rrng(mmmcu_ctx* ctx) { return reinterpret_cast<unsigned long long*>(za_base(ctx)); }
 uint32_t* za_arow(mmmcu_ctx* ctx) { return reinterpret_cast<uint32_t*>(za_rrng(ctx) + ctx->M); }
 uint32_t* za_acol(mmmcu_ctx* ctx) { return za_arow(ctx) + ctx->M; }
 uint32_t* za_tiles(mmmcu_ctx* ctx) { return za_acol(ctx) + ctx->Ka; }
 int64_t n_row_tiles(int64_t M) { return (M + mmmcu::kK1Rows - 1) / mmmcu::kK1Rows; }
-unsigned long long* zb_slice(mmmcu_ctx* ctx) { return ctx->zb.as<unsigned long long>(); }
+unsigned long long* zb_slice(mmmcu_ctx* ctx) { return reinterpret_cast<unsigned long long*>(zb_base(ctx)); }
 uint32_t* zb_bpop(mmmcu_ctx* ctx) {  // after the head and the group range words (zb_grng)
-  return reinterpret_cast<uint32_t*>(ctx->zb.as<unsigned long long>() + 6) + 2 * (ctx->ldb / 8);
+  return reinterpret_cast<uint32_t*>(zb_slice(ctx) + 6) + 2 * (ctx->ldb / 8);
 }
 // one word after the A scratch: set iff A holds an Inf / NaN (zeroed with za)
 uint32_t* za_nonfinite(mmmcu_ctx* ctx) { return za_tiles(ctx) + n_row_tiles(ctx->M); }
@@ -219,7 +227,7 @@ int64_t za_words(int64_t M, int64_t K) { return 2 * M + M + K + n_row_tiles(M) +
 // zb starts with 6 u64 B totals (k1_preprocess.cuh K1Scratch::btot), then per-8-column-group
 // max|b| bits and min-complements, then bpop [K], bnz [K], ...
 constexpr int kZbHead = 6;
-unsigned long long* zb_grng(mmmcu_ctx* ctx) { return ctx->zb.as<unsigned long long>() + kZbHead; }
+unsigned long long* zb_grng(mmmcu_ctx* ctx) { return zb_slice(ctx) + kZbHead; }
 uint32_t* zb_bnz(mmmcu_ctx* ctx) { return zb_bpop(ctx) + ctx->Kb; }
 // Operand sets K1 emits for K2: A^T tiles (SIMT v2, TC), raw B rows (SIMT v2), tf32 B step
 // images + live-k lists (TC).
@@ -237,6 +245,25 @@ uint32_t* zb_tlive(mmmcu_ctx* ctx) { return zb_bnz(ctx) + ctx->Kb; }
 int64_t n_cnt_tc(const mmmcu_ctx* ctx) { return ctx->n_tc * ((ctx->Kb + 31) / 32); }
 uint32_t* zb_row_cnt(mmmcu_ctx* ctx) { return zb_tlive(ctx) + ((ctx->ops_b & OP_TCB) ? n_cnt_tc(ctx) : 0); }
 
+// Switch a double-buffered K1 scratch to its other half (zeroed by the previous K1 pass), or
+// (re)allocate both halves zeroed when the size changes.  A half that is not known to be
+// clean (the pass that should have zeroed it never ran) is zeroed here.
+mmmcu_status next_half(mmmcu_ctx* ctx, DevBuf& buf, size_t& half, int& p, bool (&clean)[2], size_t bytes) {
+  const size_t want = (bytes + 255) & ~size_t(255);
+  if (want > half || !buf.p) {
+    MMMCU_CUDA(buf.ensure(2 * want));
+    half = want;
+    MMMCU_CUDA(cudaMemsetAsync(buf.p, 0, 2 * want, ctx->stream));
+    clean[0] = clean[1] = true;
+    p = 0;
+  } else {
+    p ^= 1;
+    if (!clean[p]) MMMCU_CUDA(cudaMemsetAsync(static_cast<uint8_t*>(buf.p) + p * half, 0, half, ctx->stream));
+  }
+  clean[p] = false;  // the coming K1 pass accumulates into it
+  return MMMCU_OK;
+}
+
 mmmcu_status stage_a(mmmcu_ctx* ctx, const float* A, int64_t M, int64_t K, int64_t lda, uint64_t av) {
   if (M <= 0 || K <= 0) return fail(ctx, MMMCU_ERR_INVALID_ARG, "matrix dimensions must be positive");
   if (!A) return fail(ctx, MMMCU_ERR_INVALID_ARG, "A is null");
@@ -246,11 +273,11 @@ mmmcu_status stage_a(mmmcu_ctx* ctx, const float* A, int64_t M, int64_t K, int64
   ctx->has_a = false;
   ctx->csr_idx_bytes = K <= 65536 ? 2 : 4;
   MMMCU_CUDA(ctx->abits.ensure(sizeof(uint32_t) * M * kw));
-  MMMCU_CUDA(ctx->za.ensure(sizeof(uint32_t) * za_words(M, K)));
+  MMMCU_TRY(next_half(ctx, ctx->za, ctx->za_half, ctx->pa, ctx->za_clean, sizeof(uint32_t) * za_words(M, K)));
   MMMCU_CUDA(ctx->tile_prefix.ensure(sizeof(int64_t) * (n_row_tiles(M) + 1)));
   MMMCU_CUDA(ctx->row_ptr.ensure(sizeof(int64_t) * (M + 1)));
   MMMCU_CUDA(ctx->cols.ensure((size_t)ctx->csr_idx_bytes * M * K));
-  ctx->za_zero = sizeof(uint32_t) * za_words(M, K);  // zeroed by k1_zero (launch_k1)
+  ctx->zero_a_next = true;
   ctx->op_at = false;
   if (ops_for(ctx) & OP_AT) {
     ctx->kpad = round_up(K, 32);
@@ -287,8 +314,8 @@ mmmcu_status stage_b(mmmcu_ctx* ctx, const float* B, int64_t K, int64_t N, int64
   const int64_t n_tc = (ldb + mmmcu::kTcTileN - 1) / mmmcu::kTcTileN;
   const int64_t n_extra = ((ops & OP_TCB) ? n_tc * kw : 0) + ((ops & OP_ROWS) ? n_cnt : 0);
   const size_t zb_bytes = kZbHead * sizeof(unsigned long long) + sizeof(uint32_t) * (2 * (ldb / 8) + 2 * K + n_extra);
-  MMMCU_CUDA(ctx->zb.ensure(zb_bytes));
-  ctx->zb_zero = zb_bytes;  // zeroed by k1_zero (launch_k1)
+  MMMCU_TRY(next_half(ctx, ctx->zb, ctx->zb_half, ctx->pb, ctx->zb_clean, zb_bytes));
+  ctx->zero_b_next = true;
   ctx->n_tb = n_tb;
   ctx->n_tc = n_tc;
   if (ops & OP_TCB) {
@@ -443,13 +470,16 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   cudaEventCreate(&ev1);
   cudaEventRecord(ev0, ctx->stream);
 #endif
-  if (ctx->za_zero || ctx->zb_zero) {  // one kernel instead of two memsets: the chain stays PDL
-    MMMCU_CUDA(launch_pdl(mmmcu::k1_zero, dim3(64), dim3(256), 0, ctx->stream, ctx->za.as<uint4>(),
-                          (int64_t)((ctx->za_zero + 15) / 16), ctx->zb.as<uint4>(), (int64_t)((ctx->zb_zero + 15) / 16)));
-    ctx->za_zero = ctx->zb_zero = 0;
-  }
+  // the K1 pass zeroes the other halves of the scratch for the next plan (double buffering)
+  z.zero_a = ctx->zero_a_next ? reinterpret_cast<uint4*>(ctx->za.as<uint8_t>() + (ctx->pa ^ 1) * ctx->za_half) : nullptr;
+  z.zero_a_n = ctx->zero_a_next ? (int64_t)(ctx->za_half / 16) : 0;
+  z.zero_b = ctx->zero_b_next ? reinterpret_cast<uint4*>(ctx->zb.as<uint8_t>() + (ctx->pb ^ 1) * ctx->zb_half) : nullptr;
+  z.zero_b_n = ctx->zero_b_next ? (int64_t)(ctx->zb_half / 16) : 0;
   MMMCU_CUDA(launch_pdl(k1fn, dim3(k1_grid), dim3(mmmcu::kK1Block), k1_smem, ctx->stream, g, z, has_a, has_b,
                         ctx->stats.as<unsigned long long>()));
+  if (ctx->zero_a_next) ctx->za_clean[ctx->pa ^ 1] = true;
+  if (ctx->zero_b_next) ctx->zb_clean[ctx->pb ^ 1] = true;
+  ctx->zero_a_next = ctx->zero_b_next = false;
 #ifdef K1_EVT
   cudaEventRecord(ev1, ctx->stream);
   cudaEventSynchronize(ev1);
