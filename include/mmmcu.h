@@ -43,7 +43,10 @@ typedef enum {
   MMMCU_ERR_NOT_READY = 6,     /* multiply before preprocess */
   MMMCU_ERR_OVERFLOW = 7,      /* std::overflow_error (matrix.hpp:77-80) */
   MMMCU_ERR_WORKERS = 8,       /* SPEC.md:290 worker_count == 0 */
-  MMMCU_ERR_NO_DEVICE = 9      /* no CUDA device: the product never falls back to the CPU */
+  MMMCU_ERR_NO_DEVICE = 9,     /* no CUDA device: the product never falls back to the CPU */
+  MMMCU_ERR_FILE_IO = 10,      /* IoError (matrix_io.hpp:27-29): open / write failures */
+  MMMCU_ERR_FILE_FORMAT = 11,  /* BadMagicError, UnknownDtypeError, bad version (matrix_io.hpp:18-26) */
+  MMMCU_ERR_FILE_TRUNCATED = 12 /* TruncatedFileError (matrix_io.hpp:21-23) */
 } mmmcu_status;
 
 typedef struct mmmcu_ctx mmmcu_ctx;
@@ -266,6 +269,23 @@ mmmcu_status mmmcu_multiply_sharded_cols(mmmcu_group* g, float* const* C_slabs, 
                                          const float* B, int64_t ldb, int64_t M, int64_t K, int64_t N,
                                          uint64_t a_version, uint64_t b_version, mmmcu_counters* counters,
                                          double* broadcast_ms);
+
+/* ---- MMMB files <-> device memory (csrc/mmmcu_io.cu) ----------------------------------
+ *
+ * The reference's interchange format (/root/reference/proj/include/mmm/matrix_io.hpp:11-13):
+ * "MMMB" | u32 version 1 | u32 dtype (0 f32, 1 f64) | u64 rows | u64 cols | row-major payload.
+ * These replace write_matrix / read_matrix / peek_dtype (matrix_io.hpp:32-49) for device
+ * operands: the payload streams through pinned staging straight into the Matrix layout on the
+ * device (ld columns per row, padding zeroed).  f64 files are MMMCU_ERR_UNSUPPORTED.  The
+ * message of the last failure of these calls is mmmcu_io_last_error().
+ */
+const char* mmmcu_io_last_error(void);
+mmmcu_status mmmcu_mmmb_peek(const char* path, int32_t* dtype, int64_t* rows, int64_t* cols);
+/* Load into dev (max_rows x ld floats, cudaStream_t stream); *rows / *cols receive the shape.
+ * Synchronises the stream before returning. */
+mmmcu_status mmmcu_mmmb_load(const char* path, float* dev, int64_t ld, int64_t max_rows, void* stream, int64_t* rows,
+                             int64_t* cols);
+mmmcu_status mmmcu_mmmb_save(const char* path, const float* dev, int64_t rows, int64_t cols, int64_t ld, void* stream);
 
 #ifdef __cplusplus
 }

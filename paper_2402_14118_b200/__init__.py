@@ -12,6 +12,7 @@ from .api import (  # noqa: F401
     LaneConfig,
     MmmContext,
     MmmError,
+    MatrixFileError,
     MmmGroup,
     NoDeviceError,
     PlanStats,
@@ -20,6 +21,9 @@ from .api import (  # noqa: F401
     WorkCounters,
     generate,
     matrix_seed,
+    mmmb_load,
+    mmmb_peek,
+    mmmb_save,
     multiply_host,
     multiply_mmm,
     multiply_parallel,

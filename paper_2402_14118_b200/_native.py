@@ -23,6 +23,9 @@ ERR_NOT_READY = 6
 ERR_OVERFLOW = 7
 ERR_WORKERS = 8
 ERR_NO_DEVICE = 9
+ERR_FILE_IO = 10
+ERR_FILE_FORMAT = 11
+ERR_FILE_TRUNCATED = 12
 
 # mmmcu_algo
 ALGO_AUTO = 0
@@ -86,6 +89,10 @@ SIGNATURES = [
                                c_int, c_double, c_int64]),
     ("mmmcu_shard_rows", c_int, [c_int64, c_int, c_int, POINTER(c_int64), POINTER(c_int64)]),
     ("mmmcu_shard_cols", c_int, [c_int64, c_int, c_int, POINTER(c_int64), POINTER(c_int64)]),
+    ("mmmcu_io_last_error", c_char_p, []),
+    ("mmmcu_mmmb_peek", c_int, [c_char_p, POINTER(c_int32), POINTER(c_int64), POINTER(c_int64)]),
+    ("mmmcu_mmmb_load", c_int, [c_char_p, c_void_p, c_int64, c_int64, c_void_p, POINTER(c_int64), POINTER(c_int64)]),
+    ("mmmcu_mmmb_save", c_int, [c_char_p, c_void_p, c_int64, c_int64, c_int64, c_void_p]),
     ("mmmcu_group_create", c_int, [c_int, POINTER(c_int), POINTER(c_void_p)]),
     ("mmmcu_group_destroy", c_int, [c_void_p]),
     ("mmmcu_group_last_error", c_char_p, [c_void_p]),

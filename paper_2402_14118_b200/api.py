@@ -54,6 +54,22 @@ class CudaError(MmmError):
     pass
 
 
+class MatrixFileError(MmmError):
+    """MatrixFileError family of matrix_io.hpp:15-29 (MMMB files)."""
+
+
+class BadFormatError(MatrixFileError):
+    """BadMagicError / UnknownDtypeError / unsupported version."""
+
+
+class TruncatedFileError(MatrixFileError):
+    pass
+
+
+class FileIoError(MatrixFileError):
+    pass
+
+
 class NoDeviceError(MmmError):
     pass
 
@@ -73,6 +89,12 @@ def _raise(status: int, msg: str):
         raise ValueError(msg)  # SPEC.md:290 worker_count == 0 rejected
     if status == N.ERR_NO_DEVICE:
         raise NoDeviceError(msg)
+    if status == N.ERR_FILE_IO:
+        raise FileIoError(msg)
+    if status == N.ERR_FILE_FORMAT:
+        raise BadFormatError(msg)
+    if status == N.ERR_FILE_TRUNCATED:
+        raise TruncatedFileError(msg)
     if status == N.ERR_NOT_READY:
         raise MmmError(msg)
     raise CudaError(msg)
@@ -414,6 +436,44 @@ def shard_rows(M: int, world: int, rank: int):
     if st != N.OK:
         _raise(st, _lib().mmmcu_last_error(None).decode())
     return r0.value, r1.value
+
+
+# ------------------------------------------------------------------ MMMB files (f3)
+def mmmb_peek(path: str):
+    """(dtype, rows, cols) of an MMMB file (peek_dtype, matrix_io.hpp:37-38); no device needed."""
+    d, r, c = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()
+    st = _lib().mmmcu_mmmb_peek(str(path).encode(), ctypes.byref(d), ctypes.byref(r), ctypes.byref(c))
+    if st != N.OK:
+        _raise(st, _lib().mmmcu_io_last_error().decode())
+    return {0: "f32", 1: "f64"}[d.value], r.value, c.value
+
+
+def mmmb_load(path: str, device: int = 0, lane: LaneConfig = LaneConfig()):
+    """read_matrix<float> (matrix_io.hpp:42-48) into device memory: a CUDA tensor with the
+    Matrix padding (ld = round_up(cols, region width), padding zero); returns the logical view."""
+    import torch
+
+    _, rows, cols = mmmb_peek(path)
+    ld = round_up(cols, lane.region_width())
+    t = torch.empty((rows, ld), dtype=torch.float32, device=f"cuda:{device}")
+    r, c = ctypes.c_int64(), ctypes.c_int64()
+    st = _lib().mmmcu_mmmb_load(str(path).encode(), t.data_ptr(), ld, rows,
+                                ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream), ctypes.byref(r),
+                                ctypes.byref(c))
+    if st != N.OK:
+        _raise(st, _lib().mmmcu_io_last_error().decode())
+    return t[:, :cols]
+
+
+def mmmb_save(path: str, t) -> None:
+    """write_matrix (matrix_io.hpp:32-33) of a CUDA float32 matrix (logical columns only)."""
+    import torch
+
+    p, ld = _check_tensor(t, "t")
+    st = _lib().mmmcu_mmmb_save(str(path).encode(), p, t.shape[0], t.shape[1], ld,
+                                ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream))
+    if st != N.OK:
+        _raise(st, _lib().mmmcu_io_last_error().decode())
 
 
 def shard_cols(Ncols: int, world: int, rank: int):

@@ -26,12 +26,23 @@ def build_lib(verbose_ptxas: bool = False) -> str:
     out_dir = os.path.join(HERE, "_lib")
     os.makedirs(out_dir, exist_ok=True)
     out = os.path.join(out_dir, "libmmmcu.so")
-    srcs = [os.path.join(HERE, "csrc", f) for f in ("mmmcu.cu", "mmmcu_group.cu")]
+    srcs = [os.path.join(HERE, "csrc", f) for f in ("mmmcu.cu", "mmmcu_group.cu", "mmmcu_io.cu")]
     cmd = [NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
            "-I", os.path.join(ROOT, "include"), "-o", out, *srcs, "-ldl"]
     if verbose_ptxas:
         cmd.insert(1, "-Xptxas=-v")
     _run(cmd)
+    return out
+
+
+def build_cli() -> str:
+    """The SPEC bench-cli on the GPU path (cli/mmm_cuda.cpp -> _lib/mmm-cuda), linked against
+    libmmmcu.so (C ABI) and cuBLAS (the dense comparator only)."""
+    out = os.path.join(HERE, "_lib", "mmm-cuda")
+    cuda = os.path.dirname(os.path.dirname(NVCC))
+    _run(["g++", "-O2", "-std=c++17", "-I", os.path.join(ROOT, "include"), "-I", os.path.join(cuda, "include"),
+          os.path.join(HERE, "cli", "mmm_cuda.cpp"), "-L", os.path.join(HERE, "_lib"), "-L", os.path.join(cuda, "lib64"),
+          "-lmmmcu", "-lcublas", "-lcudart", "-Wl,-rpath,$ORIGIN", "-o", out])
     return out
 
 
@@ -67,6 +78,7 @@ def build_oracle() -> None:
 
 def main(argv=None):
     build_lib()
+    build_cli()
     build_probe()
     build_dropin_test()
     build_oracle()
