@@ -79,6 +79,7 @@ struct K1Scratch {
   int64_t m_at;           // M rounded up to 256 (K2-TC pair tiles)
   uint32_t* tlive;        // [n_tc][kw] live-k mask per kTcTileN-column TC tile: bit kk of word c
                           // set iff B[32c + kk, tile columns] has a non-zero (zeroed, atomicOr)
+  uint32_t* tcnt;         // [n_tc] live k per TC tile (each bit counted by the thread that set it)
   int64_t n_tb;           // 256-column tiles of B (K2-SIMT records)
   int64_t n_tc;           // kTcTileN-column tiles of B (K2-TC)
   int choose;             // AUTO: pick K2-SIMT vs K2-TC from the cost model (both operand sets built)
@@ -110,20 +111,10 @@ __device__ void k1_choose_path(const K1Scratch& z, int64_t M, int64_t kw, unsign
   __shared__ unsigned long long s_stage[32], s_live[32];
   __shared__ uint32_t s_pick;
   unsigned long long st = 0, live = 0;
-  {
-    // warp per tile: lanes stream the tile's kw mask words (coalesced), warp popc sum
-    const int lane0 = threadIdx.x & 31, nw = (int)(blockDim.x >> 5);
-    for (int64_t tb = threadIdx.x >> 5; tb < z.n_tc; tb += nw) {
-      uint32_t n = 0;
-#pragma unroll 4
-      for (int64_t c = lane0; c < kw; c += 32) n += __popc(z.tlive[tb * kw + c]);
-#pragma unroll
-      for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
-      if (lane0 == 0) {
-        live += n;
-        st += (n + 31) / 32;  // fp16-split stages of 32 live k
-      }
-    }
+  for (int64_t tb = threadIdx.x; tb < z.n_tc; tb += blockDim.x) {  // live k per tile, counted by K1
+    const uint32_t n = z.tcnt[tb];
+    live += n;
+    st += (n + 31) / 32;  // fp16-split stages of 32 live k
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -228,9 +219,18 @@ __device__ __forceinline__ unsigned long long k1_now() {
 }
 #endif
 
+// Rows per ring stage: an 8-row group (the tile functions' unit) spans 8 / kK1SR stages, so a
+// stage is released, and refilled, after half a group (finer-grained refills keep more of the
+// ring in flight while the warps compute: 4 x 16 KB measured faster than 2 x 32 KB).
+#ifndef K1_SR
+#define K1_SR 4
+#endif
+constexpr int kK1SR = K1_SR;
+static_assert(8 % kK1SR == 0, "stage rows must divide the 8-row group");
+
 template <int ST>
 struct K1RingT {
-  float4 buf[ST][8][kK1Threads];  // 8 rows x 1024 columns per stage (32 KB)
+  float4 buf[ST][kK1SR][kK1Threads];  // kK1SR rows x 1024 columns per stage
   uint64_t full[ST];
   uint64_t empty[ST];
   int64_t tile[ST];               // the tile this stage's group belongs to (-1: no more)
@@ -321,13 +321,13 @@ struct K1Cursor {
   __device__ void issue(R& r, int s) {
     const K1Args& a = *g;
     const int64_t lim = t < a.nA ? a.M : rend;  // A rows past M are zeros: not read
-    const int64_t rows_valid = lim - rb >= 8 ? 8 : (lim - rb > 0 ? lim - rb : 0);
+    const int64_t rows_valid = lim - rb >= kK1SR ? kK1SR : (lim - rb > 0 ? lim - rb : 0);
     const uint32_t bytes = (uint32_t)((cols - c0 >= kK1Cols ? kK1Cols : cols - c0) * 4);
     r.tile[s] = t;
     mbar_expect(&r.full[s], (uint32_t)rows_valid * bytes);
     for (int u = 0; u < rows_valid; ++u) k1_bulk(&r.buf[s][u][0], base + (rb + u) * ld + c0, bytes, &r.full[s]);
-    rb += 8;
-    if (rb >= rend) next_tile();
+    rb += kK1SR;
+    if (rb >= rend && (rb & 7) == 0) next_tile();  // whole 8-row groups (a group's stages share a tile)
   }
   // no more tiles: one stage tagged -1 tells the compute warps to stop
   template <class R>
@@ -355,44 +355,30 @@ struct K1RingLoaderT {
     k1_wait(&r.full[s], (J / ST) & 1u);
     return r.tile[s];
   }
-  __device__ void rows8(float4 (&v)[8], const float*, int64_t, bool col_ok, int nvalid) {
-    const int s = J % ST;
-    k1_wait(&r.full[s], (J / ST) & 1u);
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      v[u] = (col_ok && u < nvalid) ? r.buf[s][u][threadIdx.x] : make_float4(0.f, 0.f, 0.f, 0.f);
-    // the TMA refill of this slot (async proxy) must not overtake these generic-proxy reads
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
-                                                  (uint32_t)__cvta_generic_to_shared(&r.empty[s]))
-                                              : "memory");
-    if (threadIdx.x == 0 && !cur.done()) {  // refill this slot with group J + ST
-      k1_wait(&r.empty[s], (J / ST) & 1u);
-      cur.issue(r, s);
-    }
-    ++J;
-  }
   // x[u][j] = row u, column colofs[j] of the next 8-row group (0 for !ok[j] or u >= nvalid)
   // FULL: all 8 rows and all columns of the group are valid (no per-element selects)
   template <bool FULL = false>
   __device__ void rows(float (&x)[8][4], const int (&colofs)[4], const bool (&ok)[4], int nvalid) {
-    const int s = J % ST;
-    k1_wait(&r.full[s], (J / ST) & 1u);
-    const float* st = reinterpret_cast<const float*>(&r.buf[s][0][0]);
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int h = 0; h < 8 / kK1SR; ++h) {  // the group's stages, in order
+      const int s = J % ST;
+      k1_wait(&r.full[s], (J / ST) & 1u);
+      const float* st = reinterpret_cast<const float*>(&r.buf[s][0][0]);
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        x[u][j] = (FULL || (ok[j] && u < nvalid)) ? st[u * kK1Cols + colofs[j]] : 0.0f;
-#ifndef K1_NOFENCE
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-#endif
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
-                                                  (uint32_t)__cvta_generic_to_shared(&r.empty[s]))
-                                              : "memory");
-    ++J;
+      for (int v = 0; v < kK1SR; ++v) {
+        const int u = h * kK1SR + v;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          x[u][j] = (FULL || (ok[j] && u < nvalid)) ? st[v * kK1Cols + colofs[j]] : 0.0f;
+      }
+      // the TMA refill of this slot (async proxy) must not overtake these generic-proxy reads
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                                                    (uint32_t)__cvta_generic_to_shared(&r.empty[s]))
+                                                : "memory");
+      ++J;
+    }
   }
 };
 
@@ -462,7 +448,14 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
     constexpr bool FULL = decltype(full_tag)::value;
     float x[8][4];
     ld.template rows<FULL>(x, colofs, ok, nvalid);
+#ifdef K1_NOCOMP_A
+    return;
+#endif
+#ifdef K1_NOAT
+    if (false) {
+#else
     if (z.at) {
+#endif
       // A^T tile row k = col holds rows rb..rb+7 at offset rb % 128: two 16-byte stores
       const int64_t rt = rb >> 7;
 #pragma unroll
@@ -641,7 +634,12 @@ __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, 
 #pragma unroll
   for (int o = 16; o; o >>= 1) srows += __shfl_xor_sync(0xffffffffu, srows, o);
   if (lane == 0 && srows) atomicAdd(&z.btot[0], (unsigned long long)srows);
-  if (z.tlive && gword) atomicOr(&z.tlive[(gcol / kTcTileN) * kw + kwi], gword);
+  if (z.tlive && gword) {  // the bits this thread sets first are its tile's newly live k
+    const int64_t tb = gcol / kTcTileN;
+    const uint32_t old = atomicOr(&z.tlive[tb * kw + kwi], gword);
+    const uint32_t fresh = __popc(gword & ~old);
+    if (fresh) atomicAdd(&z.tcnt[tb], fresh);
+  }
 }
 
 // Region codes (kernel_table.cpp:19: bit 7-j <-> 8-column group j, MSB first) from the group

@@ -22,8 +22,11 @@
 
 // K1 pass ring for ordinary operand mixes: stages x CTAs per SM (measured best of 2x3, 3x2, 1x6)
 #ifndef K1_SMALL_ST
-#define K1_SMALL_ST 2
+#define K1_SMALL_ST (16 / K1_SR)  // 64 KB ring per CTA
 #define K1_SMALL_CTAS 3
+#endif
+#ifndef K1_BIG_ST
+#define K1_BIG_ST (48 / K1_SR)    // 192 KB ring, 1 CTA per SM
 #endif
 
 namespace {
@@ -166,7 +169,7 @@ void set_carveouts(int device) {
   if (device < 0 || device >= 64 || done[device]) return;
   done[device] = true;
   max_carveout(mmmcu::k1_pass<K1_SMALL_ST, K1_SMALL_CTAS>);
-  max_carveout(mmmcu::k1_pass<6, 1>);
+  max_carveout(mmmcu::k1_pass<K1_BIG_ST, 1>);
   max_carveout(mmmcu::k1_pack_auto);
   max_carveout(mmmcu::k1_csr);
   max_carveout(mmmcu::k1_pack_tc);
@@ -243,7 +246,11 @@ int ops_for(const mmmcu_ctx* ctx) {
 }
 uint32_t* zb_tlive(mmmcu_ctx* ctx) { return zb_bnz(ctx) + ctx->Kb; }
 int64_t n_cnt_tc(const mmmcu_ctx* ctx) { return ctx->n_tc * ((ctx->Kb + 31) / 32); }
-uint32_t* zb_row_cnt(mmmcu_ctx* ctx) { return zb_tlive(ctx) + ((ctx->ops_b & OP_TCB) ? n_cnt_tc(ctx) : 0); }
+// live k per TC tile (counted as K1 sets the tlive bits), then the K2-SIMT record counts
+uint32_t* zb_tcnt(mmmcu_ctx* ctx) { return zb_tlive(ctx) + n_cnt_tc(ctx); }
+uint32_t* zb_row_cnt(mmmcu_ctx* ctx) {
+  return zb_tlive(ctx) + ((ctx->ops_b & OP_TCB) ? n_cnt_tc(ctx) + ctx->n_tc : 0);
+}
 
 // Switch a double-buffered K1 scratch to its other half (zeroed by the previous K1 pass), or
 // (re)allocate both halves zeroed when the size changes.  A half that is not known to be
@@ -312,7 +319,7 @@ mmmcu_status stage_b(mmmcu_ctx* ctx, const float* B, int64_t K, int64_t N, int64
   const int64_t n_tb = (ldb + 255) / 256;
   const int64_t n_cnt = n_tb * kw;
   const int64_t n_tc = (ldb + mmmcu::kTcTileN - 1) / mmmcu::kTcTileN;
-  const int64_t n_extra = ((ops & OP_TCB) ? n_tc * kw : 0) + ((ops & OP_ROWS) ? n_cnt : 0);
+  const int64_t n_extra = ((ops & OP_TCB) ? n_tc * kw + n_tc : 0) + ((ops & OP_ROWS) ? n_cnt : 0);
   const size_t zb_bytes = kZbHead * sizeof(unsigned long long) + sizeof(uint32_t) * (2 * (ldb / 8) + 2 * K + n_extra);
   MMMCU_TRY(next_half(ctx, ctx->zb, ctx->zb_half, ctx->pb, ctx->zb_clean, zb_bytes));
   ctx->zero_b_next = true;
@@ -443,6 +450,7 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   z.kpad = ctx->kpad;
   z.m_at = ctx->m_at;
   z.tlive = tcb_b ? zb_tlive(ctx) : nullptr;
+  z.tcnt = tcb_b ? zb_tcnt(ctx) : nullptr;
   z.row_cnt = rows_b ? zb_row_cnt(ctx) : nullptr;
   z.row_off = rows_b ? ctx->row_off.as<int64_t>() : nullptr;
   z.n_tb = ctx->n_tb;
@@ -459,8 +467,8 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   // cfg5's A-heavy 10k tiles: 0.86 vs 1.02 ms), 6 stages x 1 CTA for streams dominated by
   // many B tiles, which carry no A^T work (cfg4's 18k B tiles: 1.26 vs 1.82 ms) — measured
   const bool big = nA + nB > 4 * 3 * (int64_t)ctx->num_sms && nB > 4 * nA;
-  auto k1fn = big ? mmmcu::k1_pass<6, 1> : mmmcu::k1_pass<K1_SMALL_ST, K1_SMALL_CTAS>;
-  const int k1_smem = (int)(big ? sizeof(mmmcu::K1RingT<6>) : sizeof(mmmcu::K1RingT<K1_SMALL_ST>)) + 128;
+  auto k1fn = big ? mmmcu::k1_pass<K1_BIG_ST, 1> : mmmcu::k1_pass<K1_SMALL_ST, K1_SMALL_CTAS>;
+  const int k1_smem = (int)(big ? sizeof(mmmcu::K1RingT<K1_BIG_ST>) : sizeof(mmmcu::K1RingT<K1_SMALL_ST>)) + 128;
   MMMCU_CUDA(cudaFuncSetAttribute(k1fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k1_smem));
   const unsigned k1_grid =
       (unsigned)std::min<int64_t>(nA + nB, (big ? 1 : K1_SMALL_CTAS) * (int64_t)ctx->num_sms);
