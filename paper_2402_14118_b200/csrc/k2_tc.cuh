@@ -43,6 +43,7 @@
 // D [0,192), P [192,384), 4 A slots [384,512) of 32 columns (per MMA step: hi 8 | lo 8
 // columns; fp16 packs 2 k per column, even k in the low half).
 #pragma once
+#include <cuda.h>  // CUtensorMap (the A^T gather descriptor)
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -90,6 +91,13 @@ constexpr int kTdTM = 128;
 #endif
 #ifndef TD_HINT
 #define TD_HINT 1  // L2 evict_last on the A^T / B-image bulk copies (dense cell 0.31 -> 0.29 ms)
+#endif
+#ifndef TD_GATHER
+#define TD_GATHER 1  // the stage's live A^T rows by TMA tile::gather4 (4 rows per instruction)
+#endif
+#ifndef TD_GATHER_RUNS
+#define TD_GATHER_RUNS 16  // stages with at most this many runs of consecutive live k use bulk copies
+                           // (measured: gathers win at ~23 runs per stage, lose at ~9)
 #endif
 constexpr int kTdGroup = TD_GROUP;            // row units per scheduling group (L2 reuse of A^T and B)
 constexpr int kTdXrow = 36;                   // C-update staging row stride (floats): 16-byte aligned rows,
@@ -164,6 +172,20 @@ __device__ __forceinline__ void td_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+// Four A^T rows (row coordinates r0..r3 of the 2-D A^T tensor, 128 floats each) into 2 KB of
+// shared memory with one TMA tile::gather4 (sm_100): the live rows of a sparse-k stage arrive in
+// 8 instructions however they are scattered (one bulk copy per run of consecutive live k left
+// the transform warps waiting 58% of their time on sparse-k cells).
+__device__ __forceinline__ void td_gather4(void* smem_dst, const CUtensorMap* tmap, int r0, int r1, int r2, int r3,
+                                           uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(tc::smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(tc::smem_u32(bar)),
+      "l"(policy)
+      : "memory");
+}
+
 // A tile is "mostly live" when >= 3/4 of its k are live (scheduling groups, below).
 __device__ __forceinline__ bool td_dense(int32_t live, int64_t kpad) { return 4 * (int64_t)live >= 3 * kpad; }
 
@@ -179,7 +201,8 @@ __global__ void __launch_bounds__(TdCfg<F16>::kThreads, 1)
 k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb, const int32_t* __restrict__ tck,
       const int32_t* __restrict__ tcn, int64_t maxsteps, float* __restrict__ C, int64_t ldc, int64_t M, int64_t N,
       int64_t m_tiles, int64_t n_tiles, const unsigned long long* __restrict__ sel,
-      const unsigned long long* __restrict__ rrng, const unsigned long long* __restrict__ grng) {
+      const unsigned long long* __restrict__ rrng, const unsigned long long* __restrict__ grng,
+      const __grid_constant__ CUtensorMap tmap_at) {
   using Cfg = TdCfg<F16>;
   constexpr int kStages = Cfg::kStages, kSub = Cfg::kSub, kStepK = Cfg::kStepK, kStageK = Cfg::kStageK,
                 kSeg = Cfg::kSeg, kTdSlots = Cfg::kSlots;
@@ -269,7 +292,9 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       constexpr int kStepCopy = kPair ? kTdStepFloats / 2 : kTdStepFloats;  // floats per step in this CTA
       const float* bsrc = tcb + (kPair ? (tb * 2 + rank) : tb) * maxsteps * kStepCopy;
       const int32_t* kx = tck + tb * maxsteps * 8;
+#if !TD_GATHER
       const float* atile = AT + rt * kpad * 128;
+#endif
       const int npos = nsteps * kStepK;
       auto kload = [&](int jj) {
         const int pn = jj * kStageK + lane;
@@ -297,6 +322,41 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
         __syncwarp();
         TD_CLK(q1);
         TD_ADD(0, q1 - q0);
+#if TD_GATHER
+        // the stage's live A^T rows: one bulk copy per run of consecutive live k when they form at
+        // most TD_GATHER_RUNS runs (dense tiles: one 16 KB copy; tiles with ~9 runs per stage
+        // measured 4% faster with copies), else lane g < ceil(nvalid / 4) gathers rows 4g .. 4g+3
+        // (positions past the tile's live count repeat a valid row: their B images are zero;
+        // very sparse-k tiles, ~23 runs per stage, measured 7-15% faster with gathers)
+        const int nv = __popc(vmask);
+        const bool runs = __popc(vmask & ~cmask) <= TD_GATHER_RUNS;
+        const int ng = runs ? 0 : (nv + 3) >> 2;
+        if (runs) {
+          const float* atile = AT + rt * kpad * 128;
+          if (lane == 0) {
+            td_expect_tx(&sh.tma[st], bytes + 512u * (uint32_t)nv);
+            if (TD_HINT) td_bulk_hint(sh.b[st], bsrc + (int64_t)kSub * j * kStepCopy, bytes, &sh.tma[st], pol);
+            else td_bulk(sh.b[st], bsrc + (int64_t)kSub * j * kStepCopy, bytes, &sh.tma[st]);
+          }
+          __syncwarp();
+          if (valid && !cont) {  // run start: rows kc .. kc + len - 1 -> slots lane .. lane + len - 1
+            const uint32_t len = lane == 31 ? 1u : (uint32_t)__ffs(~(cmask >> (lane + 1)));
+            td_bulk_hint(sh.a[st][lane], atile + (int64_t)kc * 128, 512u * len, &sh.tma[st], pol);
+          }
+        } else if (lane == 0) {
+          td_expect_tx(&sh.tma[st], bytes + 2048u * (uint32_t)ng);
+          if (TD_HINT) td_bulk_hint(sh.b[st], bsrc + (int64_t)kSub * j * kStepCopy, bytes, &sh.tma[st], pol);
+          else td_bulk(sh.b[st], bsrc + (int64_t)kSub * j * kStepCopy, bytes, &sh.tma[st]);
+        }
+        __syncwarp();
+        if (!runs) {  // (warp-uniform)
+          const int k0 = __shfl_sync(0xffffffffu, kc, 0);
+          const int rowk = (int)(rt * kpad) + (valid ? kc : k0);
+          const int q0 = __shfl_sync(0xffffffffu, rowk, (4 * lane) & 31), q1 = __shfl_sync(0xffffffffu, rowk, (4 * lane + 1) & 31);
+          const int q2 = __shfl_sync(0xffffffffu, rowk, (4 * lane + 2) & 31), q3 = __shfl_sync(0xffffffffu, rowk, (4 * lane + 3) & 31);
+          if (lane < ng) td_gather4(sh.a[st][4 * lane], &tmap_at, q0, q1, q2, q3, &sh.tma[st], pol);
+        }
+#else
         if (lane == 0) {
           td_expect_tx(&sh.tma[st], bytes + 512u * (uint32_t)__popc(vmask));
           if (TD_HINT) td_bulk_hint(sh.b[st], bsrc + (int64_t)kSub * j * kStepCopy, bytes, &sh.tma[st], pol);
@@ -308,6 +368,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
           if (TD_HINT) td_bulk_hint(sh.a[st][lane], atile + (int64_t)kc * 128, 512u * len, &sh.tma[st], pol);
           else td_bulk(sh.a[st][lane], atile + (int64_t)kc * 128, 512u * len, &sh.tma[st]);
         }
+#endif
         kc = kn;
       }
       J += (uint32_t)nstage;

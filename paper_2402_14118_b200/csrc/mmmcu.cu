@@ -101,6 +101,10 @@ struct mmmcu_ctx {
   bool za_clean[2] = {false, false}, zb_clean[2] = {false, false};
   bool zero_a_next = false, zero_b_next = false;  // the coming K1 pass zeroes the other half
   DevBuf at, tcb, tck, tcn, brows, row_off;
+  // TMA descriptor of A^T as a 2-D tensor [m_at / 128 * kpad rows][128 floats] (K2-TC gather4)
+  CUtensorMap tmap_at;
+  const void* tmap_at_ptr = nullptr;
+  int64_t tmap_at_rows = 0;
 
   // ---- statistics: u64 [16] = {inv, lanes, skipped, zreg, nnzA, pop, zero_codes, span, slice_nz}
   DevBuf stats;
@@ -619,10 +623,40 @@ mmmcu_status launch_simt(mmmcu_ctx* ctx, float* C, int64_t ldc, int span_hint, i
   return MMMCU_OK;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+mmmcu_status at_tensor_map(mmmcu_ctx* ctx) {
+  const int64_t rows = (ctx->m_at / 128) * ctx->kpad;
+  if (ctx->tmap_at_ptr == ctx->at.p && ctx->tmap_at_rows == rows) return MMMCU_OK;
+  static EncodeTiledFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    MMMCU_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess)
+      return fail(ctx, MMMCU_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<EncodeTiledFn>(fn);
+  }
+  const cuuint64_t dims[2] = {128, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {128 * sizeof(float)};
+  const cuuint32_t box[2] = {128, 1};  // gather4 moves 4 such rows
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(&ctx->tmap_at, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ctx->at.p, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ctx, MMMCU_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  ctx->tmap_at_ptr = ctx->at.p;
+  ctx->tmap_at_rows = rows;
+  return MMMCU_OK;
+}
+
 // K2-TC over the dense-tile operands (sel: device-side path choice, nullptr = forced).
 template <bool F16>
 mmmcu_status launch_tc_t(mmmcu_ctx* ctx, float* C, int64_t ldc, const unsigned long long* sel) {
   const int64_t row_tiles = ctx->m_at / mmmcu::kTdTM;
+  MMMCU_TRY(at_tensor_map(ctx));
   constexpr int smem = mmmcu::td_smem<F16>();
   MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k2_tc<F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   if (ctx->num_sms == 0) MMMCU_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
@@ -660,7 +694,7 @@ mmmcu_status launch_tc_t(mmmcu_ctx* ctx, float* C, int64_t ldc, const unsigned l
                               (const float*)ctx->tcb.as<float>(), (const int32_t*)ctx->tck.as<int32_t>(),
                               (const int32_t*)ctx->tcn.as<int32_t>(), (int64_t)ctx->tc_steps, C, ldc, ctx->M, ctx->N,
                               row_tiles, ctx->n_tc, sel, (const unsigned long long*)za_rrng(ctx),
-                              (const unsigned long long*)zb_grng(ctx));
+                              (const unsigned long long*)zb_grng(ctx), ctx->tmap_at);
   };
   MMMCU_CUDA(launch());
 #ifdef TD_PROF
