@@ -85,8 +85,11 @@ typedef enum {
                                 scaled by powers of two) on 128x192 C tiles over each
                                 tile's live k; tolerance-matched (|dC| <= 1e-5 * (|c0| +
                                 sum|a||b|)), not bit-exact                                 */
-  MMMCU_ALGO_TC32 = 6        /* K2-TC with the 3xTF32 split (kind::tf32): same tiles and
+  MMMCU_ALGO_TC32 = 6,       /* K2-TC with the 3xTF32 split (kind::tf32): same tiles and
                                 tolerance, half the k per MMA; no operand scaling          */
+  MMMCU_ALGO_CSR = 7         /* K2-CSR: only the surviving (a_ik != 0, live B block) pairs,
+                                C tiles in shared memory; exact fp32 (bit-identical to the
+                                reference kernel table) — for very sparse / skinny A        */
 } mmmcu_algo;
 
 /* ---- context --------------------------------------------------------------------- */
@@ -160,7 +163,7 @@ mmmcu_status mmmcu_export_ablock_index(mmmcu_ctx* ctx, int64_t block_dim, uint8_
  * multiply_mmm: C (M x N, ldc) += A * B over the masks of the current
  * plan.  A and B must be the preprocessed operands (same pointers, same versions).
  * Accuracy depends on the algorithm (mmmcu_set_algo):
- *   MMMCU_ALGO_SIMT_* and MMMCU_ALGO_DENSE: each C element receives the ascending-k fmaf
+ *   MMMCU_ALGO_SIMT_*, MMMCU_ALGO_CSR and MMMCU_ALGO_DENSE: each C element receives the ascending-k fmaf
  *     chain of its surviving terms, bit-identical to the CPU oracle / reference kernel table;
  *   MMMCU_ALGO_AUTO (default), MMMCU_ALGO_TC, MMMCU_ALGO_TC32: the north_star tolerance,
  *     |dC| <= 1e-5 * (|c0| + sum_k |a_ik||b_kj|), not bit-exact (AUTO runs an exact SIMT
@@ -178,7 +181,7 @@ mmmcu_status mmmcu_multiply_parallel(mmmcu_ctx* ctx, float* C, int64_t ldc, cons
 /* Force a kernel variant (MMMCU_ALGO_AUTO by default). */
 mmmcu_status mmmcu_set_algo(mmmcu_ctx* ctx, mmmcu_algo algo);
 /* Variant the last mmmcu_multiply ran (AUTO and SIMT_BCAST resolve to the kernel the
- * device chose: TC, SIMT_SPAN8 or SIMT_SPAN16; synchronises the stream). */
+ * device chose: TC, CSR, SIMT_SPAN8 or SIMT_SPAN16; synchronises the stream). */
 mmmcu_status mmmcu_last_algo(mmmcu_ctx* ctx, mmmcu_algo* algo);
 
 /* multiply_simple: dense i-k-j C += A*B, fmaf per term. */

@@ -35,6 +35,7 @@ ALGO_SIMT_SPAN8 = 3
 ALGO_SIMT_SPAN16 = 4
 ALGO_TC = 5
 ALGO_TC32 = 6
+ALGO_CSR = 7
 
 
 class Lane(ctypes.Structure):

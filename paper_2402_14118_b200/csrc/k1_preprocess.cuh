@@ -84,6 +84,7 @@ struct K1Scratch {
   int64_t n_tc;           // kTcTileN-column tiles of B (K2-TC)
   int choose;             // AUTO: pick K2-SIMT vs K2-TC from the cost model (both operand sets built)
   int num_sms;            // the device's SM count (cost-model parallelism)
+  int64_t K;              // the contraction length (cost model)
   // the other halves of the double-buffered scratch, zeroed by this pass for the next plan
   uint4* zero_a;
   int64_t zero_a_n;
@@ -146,6 +147,7 @@ __device__ void k1_choose_path(const K1Scratch& z, int64_t M, int64_t kw, unsign
     // terms the reference never forms into NaN, subnormals would be flushed — keep the
     // exact path
     const bool nonfinite = *z.nonfinite_a != 0u || z.btot[3] != 0ull;
+    // K2-TC needs finite, normal operands (0 * Inf terms, flushed subnormals)
     s_pick = (!nonfinite && tc / par_tc < simt / par_simt) ? 1u : 0u;
   }
   __syncthreads();
@@ -736,7 +738,7 @@ k1_pass(K1Args g, K1Scratch z, int has_a, int has_b, unsigned long long* __restr
   k1_plan_totals(z.btot, K, nreg, has_b, stats);
   if (z.choose && has_a && has_b) k1_choose_path(z, M, kw, stats);
   // the K2-SIMT record offsets only when K2-SIMT can run (its pack is gated out otherwise)
-  if (z.row_cnt && nB > 0 && !(z.choose && stats[7] == 32ull))
+  if (z.row_cnt && nB > 0 && !(z.choose && (stats[7] == 32ull || stats[7] == 48ull)))
     k1_block_exclusive_scan(z.row_cnt, z.n_tb * kw, 3, z.row_off);
   if (nA > 0) {  // exclusive prefix of the 32-row tile sums for the CSR's row_ptr (k1_csr_cta)
     const int64_t ntile = (M + kK1Rows - 1) / kK1Rows;
@@ -1184,10 +1186,10 @@ k1_pack_auto(PackRowsArgs gr, int64_t rows_x, int64_t n_rows, PackTcArgs gt, int
     return;
   }
   const int64_t bid = blockIdx.x - n_csr, n_tcb = (int64_t)gridDim.x - n_csr - n_rows;
-  const bool tc = *sel == 32ull;
+  const unsigned long long v = *sel;  // 8 / 16 K2-SIMT (rows), 32 K2-TC (step images), 48 K2-CSR (neither)
   if (bid < n_tcb) {
-    if (tc) k1_pack_tc_cta(gt, bid % tc_x, bid / tc_x);
-  } else if (!tc) {
+    if (v == 32ull) k1_pack_tc_cta(gt, bid % tc_x, bid / tc_x);
+  } else if (v == 8ull || v == 16ull) {
     k1_pack_rows_cta(gr, (bid - n_tcb) % rows_x, (bid - n_tcb) / rows_x);
   }
 }

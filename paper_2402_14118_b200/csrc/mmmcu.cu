@@ -17,6 +17,7 @@
 
 #include "gen.cuh"
 #include "k1_preprocess.cuh"
+#include "k2_csr.cuh"
 #include "k2_simt.cuh"
 #include "k2_tc.cuh"
 
@@ -180,6 +181,7 @@ void set_carveouts(int device) {
   max_carveout(mmmcu::k1_pack_rows);
   max_carveout(mmmcu::k1_row_off);
   max_carveout(mmmcu::k2_simt2_any);
+  max_carveout(mmmcu::k2_csr);
   max_carveout(mmmcu::k2_simt2<8>);
   max_carveout(mmmcu::k2_simt2<16>);
   max_carveout(mmmcu::k2_tc<true>);
@@ -245,6 +247,7 @@ int ops_for(const mmmcu_ctx* ctx) {
     case MMMCU_ALGO_TC:
     case MMMCU_ALGO_TC32: return OP_AT | OP_TCB;
     case MMMCU_ALGO_DENSE: return 0;
+    case MMMCU_ALGO_CSR: return OP_AT;  // A^T + the group masks; B is read as is
     default: return OP_AT | OP_ROWS;
   }
 }
@@ -462,6 +465,7 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   z.choose = gate ? 1 : 0;
   if (ctx->num_sms == 0) MMMCU_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
   z.num_sms = ctx->num_sms;
+  z.K = K;
   const int has_a = a_valid && (same_k || !b_valid) ? 1 : 0;
   const int has_b = b_valid && (same_k || !a_valid) ? 1 : 0;
   if (ctx->num_sms == 0) MMMCU_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
@@ -571,6 +575,19 @@ mmmcu_status check_plan(mmmcu_ctx* ctx, const float* A, const float* B, uint64_t
                                                   std::to_string(ctx->Kb) + ")");
   if (A != ctx->A || B != ctx->B || av != ctx->av || bv != ctx->bv)
     return fail(ctx, MMMCU_ERR_STALE, "stale context: operands differ from the preprocessed ones");
+  return MMMCU_OK;
+}
+
+// K2-CSR, persistent over the 128 x 128 units (sel: AUTO's device-side choice, nullptr = forced).
+mmmcu_status launch_csr(mmmcu_ctx* ctx, float* C, int64_t ldc, const unsigned long long* sel) {
+  const int64_t n_rt = (ctx->M + 127) / 128, n_tb = (round_up(ctx->N, 64) + mmmcu::kCsTN - 1) / mmmcu::kCsTN;
+  if (ctx->num_sms == 0) MMMCU_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k2_csr, cudaFuncAttributeMaxDynamicSharedMemorySize, mmmcu::kCsSmem));
+  MMMCU_CUDA(launch_pdl(mmmcu::k2_csr, dim3((unsigned)std::min<int64_t>(n_rt * n_tb, ctx->num_sms)),
+                        dim3(mmmcu::kCsThreads), mmmcu::kCsSmem, ctx->stream, (const float*)ctx->at.as<float>(),
+                        ctx->kpad, ctx->B, ctx->ldb, (const uint32_t*)ctx->bgrp.as<uint32_t>(), (ctx->Ka + 31) / 32, C,
+                        ldc, ctx->M, ctx->Ka, ctx->N, n_tb, n_rt, sel));
+  MMMCU_LAUNCHED();
   return MMMCU_OK;
 }
 
@@ -960,7 +977,7 @@ mmmcu_status mmmcu_export_ablock_index(mmmcu_ctx* ctx, int64_t block_dim, uint8_
 
 mmmcu_status mmmcu_set_algo(mmmcu_ctx* ctx, mmmcu_algo algo) {
   MMMCU_TRY(bind(ctx));
-  if (algo < MMMCU_ALGO_AUTO || algo > MMMCU_ALGO_TC32)
+  if (algo < MMMCU_ALGO_AUTO || algo > MMMCU_ALGO_CSR)
     return fail(ctx, MMMCU_ERR_INVALID_ARG, "unknown algorithm");
   ctx->algo = algo;
   return MMMCU_OK;
@@ -973,7 +990,10 @@ mmmcu_status mmmcu_last_algo(mmmcu_ctx* ctx, mmmcu_algo* algo) {
     unsigned long long s[16];
     MMMCU_TRY(read_stats(ctx, s));
     if (ctx->auto_pending)
-      ctx->last_algo = s[7] == 32 ? MMMCU_ALGO_TC : s[7] == 8 ? MMMCU_ALGO_SIMT_SPAN8 : MMMCU_ALGO_SIMT_SPAN16;
+      ctx->last_algo = s[7] == 32   ? MMMCU_ALGO_TC
+                       : s[7] == 48 ? MMMCU_ALGO_CSR
+                       : s[7] == 8  ? MMMCU_ALGO_SIMT_SPAN8
+                                    : MMMCU_ALGO_SIMT_SPAN16;
     else if (ctx->op_at && ctx->op_rows)  // the K2-SIMT span K1 chose (the v1 fallback runs span 8)
       ctx->last_algo = s[8] == 8 ? MMMCU_ALGO_SIMT_SPAN8 : MMMCU_ALGO_SIMT_SPAN16;
     else
@@ -1009,6 +1029,10 @@ mmmcu_status mmmcu_multiply(mmmcu_ctx* ctx, float* C, int64_t ldc, const float* 
       ctx->tcb_fresh = true;
     }
     MMMCU_TRY(launch_tc(ctx, C, ldc, nullptr));
+  } else if (ctx->algo == MMMCU_ALGO_CSR) {
+    if (!ctx->op_at) return fail(ctx, MMMCU_ERR_NOT_READY, "the CSR operands were not built: preprocess with algo CSR");
+    ctx->last_algo = MMMCU_ALGO_CSR;
+    MMMCU_TRY(launch_csr(ctx, C, ldc, nullptr));
   } else if (ctx->algo == MMMCU_ALGO_DENSE) {
     ctx->last_algo = MMMCU_ALGO_DENSE;
     dim3 grid((unsigned)((ctx->N + 63) / 64), (unsigned)((ctx->M + 63) / 64));
