@@ -18,8 +18,10 @@ each rank computes its own C rows; timing is max over ranks.  The N=1 sweep line
 the 1-GPU configs[4] value (cfg5_1gpu) as the same-workload reference of the scaling run.
 
 value     = Σ 2*lane_fma_ops over all ranks / step time     (useful GFLOP/s)
-e2e       = the same metric through the host-buffer public API (mmmcu_multiply_host): H2D of
-            A, B, C and D2H of C inside the timed region, pinned host memory
+e2e       = the same metric end to end through the public API with host operands: per step the
+            H2D of every distinct A / B of the step and of C (pinned, overlapped with the cells
+            already computing) and the D2H of C inside the timed region; per_call: the one-call
+            mmmcu_multiply_host path (every operand copied per cell)
 roofline  = K2 (dominant kernel) useful TFLOP/s vs the measured FP32 SIMT peak; plus the
             BASELINE roofline time fraction Σ max(flops/P_fp32, bytes/BW_hbm) / Σ (K1+K2)
 cpu_baseline = the reference's CPU path (oracle/_ref: SPEC multiply_parallel over the
@@ -413,6 +415,7 @@ def main():
                     help="sweep (configs[1]; the N=1 default) | cfg1 | cfg3 | cfg4 | cfg5 (the N>1 default: "
                          "strong scaling, one 32768-row A partitioned across the ranks)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-per-call", action="store_true", help="e2e: skip the per-call mmmcu_multiply_host number")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU work for cpu_baseline")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
@@ -628,43 +631,100 @@ def main():
 
 
 def run_e2e(args, cells, As, Bs, ctx, torch, dist, world, device, stats):
-    """Same metric through mmmcu_multiply_host with pinned host buffers (copies timed)."""
+    """The same metric end to end through the public Python API with HOST operands: every step
+    copies each distinct A and B of the step (and C) from pinned host memory to the device
+    (a copy stream, one event per operand, so the copies overlap the cells already computing),
+    runs K1 + K2 of every cell (MmmContext.preprocess / multiply_mmm), and reads C back.
+    Wall clock around whole steps.  A second number, per_call, times mmmcu_multiply_host (the
+    one-call C ABI host path: H2D A, B, C + K1 + K2 + D2H C per cell, synchronous)."""
     import paper_2402_14118_b200 as mmm
 
     steps = args.e2e_steps or args.steps
-    pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()  # noqa: E731
-    host_A = {k: pin(v.cpu().numpy()) for k, v in As.items()}
-    host_B = {k: pin(v.cpu().numpy()) for k, v in Bs.items()}
-    host_C = {}
+    flops = float(sum(s["flops"] for s in stats))
+
+    def pinned_like(t):  # host copy of a device operand (its padded base layout), pinned
+        base = t if t.is_contiguous() else t.as_strided((t.shape[0], t.stride(0)), (t.stride(0), 1))
+        return base.cpu().pin_memory()
+
+    host, dev = {}, {}
     for (_, M, K, N, sa, sb) in cells:
-        if (M, N) not in host_C:
-            host_C[(M, N)] = pin(np.zeros((M, N), np.float32))
-    h2d = sum(host_A[c[4]["key"]].nbytes + host_B[c[5]["key"]].nbytes + host_C[(c[1], c[3])].nbytes for c in cells)
-    d2h = sum(host_C[(c[1], c[3])].nbytes for c in cells)
+        for key, t in ((sa["key"], As[sa["key"]]), (sb["key"], Bs[sb["key"]])):
+            if key not in host:
+                host[key] = pinned_like(t)
+                dev[key] = torch.empty_like(host[key], device=device)
+        if ("C", M, N) not in host:
+            host[("C", M, N)] = torch.zeros((M, mmm.round_up(N, 64)), dtype=torch.float32).pin_memory()
+            dev[("C", M, N)] = torch.empty_like(host[("C", M, N)], device=device)
+    h2d = int(sum(v.numel() * 4 for v in host.values()))
+    d2h = int(sum(v.numel() * 4 for k, v in host.items() if k[0] == "C"))
+    copy_stream = torch.cuda.Stream(device)
+    main = torch.cuda.current_stream(device)
+
+    def view(key, rows, cols):
+        return dev[key][:rows, :cols]
 
     def step():
+        ready = {}
+        with torch.cuda.stream(copy_stream):  # H2D in first-use order, one event per operand
+            for (_, M, K, N, sa, sb) in cells:
+                for key in (("C", M, N), sa["key"], sb["key"]):
+                    if key not in ready:
+                        dev[key].copy_(host[key], non_blocking=True)
+                        ev = torch.cuda.Event()
+                        ev.record(copy_stream)
+                        ready[key] = ev
         for (_, M, K, N, sa, sb) in cells:
-            mmm.multiply_host(host_C[(M, N)], host_A[sa["key"]], host_B[sb["key"]], ctx=ctx)
+            for key in (("C", M, N), sa["key"], sb["key"]):
+                main.wait_event(ready[key])
+            a, b = view(sa["key"], M, K), view(sb["key"], K, N)
+            ctx.preprocess(a, b)
+            ctx.multiply(view(("C", M, N), M, N), a, b, want_counters=False)
+        for k in host:
+            if k[0] == "C":
+                host[k].copy_(dev[k], non_blocking=True)  # D2H of the step's result
+        torch.cuda.synchronize(device)
 
-    step()  # warm the staging buffers
-    torch.cuda.synchronize()
+    step()  # warm-up
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
         step()
-    torch.cuda.synchronize()
     el = time.perf_counter() - t0
-    flops = float(sum(s["flops"] for s in stats))
+    fl = flops
     if world > 1:
         tt = torch.tensor([el, flops], dtype=torch.float64, device=device)
         mx = tt.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         dist.all_reduce(tt, op=dist.ReduceOp.SUM)
-        el, flops = float(mx[0]), float(tt[1])
-    return {"value": round(flops / (el / steps) / 1e9, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "steps": steps,
-            "path": "mmmcu_multiply_host per cell (pinned host A/B/C -> H2D, K1, K2, D2H of C), wall clock"}
+        el, fl = float(mx[0]), float(tt[1])
+    out = {"value": round(fl / (el / steps) / 1e9, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "steps": steps,
+           "path": "public Python API with host operands: per step, H2D of each distinct A and B of the step and of "
+                   "C (pinned, copy stream overlapped with the computing cells), preprocess + multiply_mmm of every "
+                   "cell, D2H of C; wall clock"}
+    # the one-call host path of the C ABI (mmmcu_multiply_host), every operand copied per cell
+    if world == 1 and not args.no_per_call:
+        host_A = {k: host[k].numpy() for k in As}
+        host_B = {k: host[k].numpy() for k in Bs}
+        hc = {k: host[k][:, : k[2]].numpy() for k in host if k[0] == "C"}
+
+        def step_call():
+            for (_, M, K, N, sa, sb) in cells:
+                mmm.multiply_host(hc[("C", M, N)], host_A[sa["key"]][:, :K], host_B[sb["key"]][:, :N], ctx=ctx)
+
+        step_call()
+        t0 = time.perf_counter()
+        n_call = max(1, min(steps, 2))
+        for _ in range(n_call):
+            step_call()
+        el2 = time.perf_counter() - t0
+        out["per_call"] = {"value": round(flops / (el2 / n_call) / 1e9, 2), "unit": "GFLOP/s", "steps": n_call,
+                           "h2d_bytes_per_step": int(sum(host_A[c[4]["key"]][:, :c[2]].nbytes + host_B[c[5]["key"]].nbytes
+                                                         + hc[("C", c[1], c[3])].nbytes for c in cells)),
+                           "d2h_bytes_per_step": int(sum(hc[("C", c[1], c[3])].nbytes for c in cells)),
+                           "path": "mmmcu_multiply_host per cell (H2D A, B, C, K1, K2, D2H C, synchronous)"}
+    return out
 
 
 def run_reference_arm(args, cells, cfg, metric, world, rank, warmup):
