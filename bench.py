@@ -24,7 +24,8 @@ e2e       = the same metric end to end through the public API with host operands
             mmmcu_multiply_host path (every operand copied per cell)
 roofline  = K2 (dominant kernel) useful TFLOP/s vs the measured FP32 SIMT peak; plus the
             BASELINE roofline time fraction Σ max(flops/P_fp32, bytes/BW_hbm) / Σ (K1+K2)
-cpu_baseline = the reference's CPU path (oracle/_ref: SPEC multiply_parallel over the
+cpu_baseline = the reference's CPU path (oracle/_ref: SPEC preprocess_a (ABlockIndex) /
+            preprocess_b and the leaf-blocked multiply_parallel over the
             reference's compiled KernelTable) on a bounded row sample, all host cores
 """
 from __future__ import annotations
@@ -364,6 +365,13 @@ def count_launches(cells):
 
 
 # ---------------------------------------------------------------------------- CPU leg
+def ref_build():
+    from oracle import oracle as orc  # cpu_baseline leg only
+
+    v4 = orc.ref_so_path().endswith("_v4.so")
+    return "-O3 -fopenmp " + ("-march=x86-64-v4: AVX-512 host" if v4 else "-march=x86-64-v3: AVX2 host")
+
+
 def cpu_reference_sample(cells, host_A, host_B, budget_s, threads, stats):
     """The reference CPU path on a bounded row sample of every cell (oracle/_ref).
 
@@ -379,7 +387,7 @@ def cpu_reference_sample(cells, host_A, host_B, budget_s, threads, stats):
     B = host_B[sb["key"]]
     C = np.zeros((64, B.shape[1]), np.float32)
     t0 = time.perf_counter()
-    cnt = orc.ref_multiply_parallel(C, np.ascontiguousarray(A[:64]), B, workers=threads)
+    cnt = orc.ref_multiply_mmm(C, np.ascontiguousarray(A[:64]), B, workers=threads)
     rate = 2 * cnt["lane_fma_ops"] / max(cnt["multiply_ns"], 1) * 1e9  # flop/s
     per_cell_s = budget_s / len(cells)
     flops_total, time_total, rows_total = 0.0, 0.0, 0
@@ -389,7 +397,7 @@ def cpu_reference_sample(cells, host_A, host_B, budget_s, threads, stats):
         flops_per_row = stats[i]["flops"] / M
         rows = int(min(M, max(8, per_cell_s * rate / max(flops_per_row, 1.0))))
         C = np.zeros((rows, B.shape[1]), np.float32)
-        cnt = orc.ref_multiply_parallel(C, np.ascontiguousarray(A[:rows]), B, workers=threads)
+        cnt = orc.ref_multiply_mmm(C, np.ascontiguousarray(A[:rows]), B, workers=threads)
         flops_total += 2 * cnt["lane_fma_ops"]
         time_total += (cnt["multiply_ns"] + cnt["preprocess_ns"] * rows / M) * 1e-9
         rows_total += rows
@@ -596,8 +604,9 @@ def main():
             cpu = {"value": round(v, 3), "unit": "GFLOP/s", "cores": orc.ref_lib().ref_max_threads(),
                    "kind": "reference",
                    "sample": f"{rows} A rows spread over the {len(cells)} cells (each cell's leading rows), full B "
-                             f"preprocessing amortised per row; {wall:.1f} s wall; oracle/_ref = SPEC multiply_parallel "
-                             f"over the reference's compiled KernelTable (-O3 -march=x86-64-v3 -fopenmp)"}
+                             f"preprocessing amortised per row; {wall:.1f} s wall; oracle/_ref = SPEC preprocess_a/b + "
+                             f"ABlockIndex-driven leaf-blocked multiply_parallel over the reference's compiled "
+                             f"KernelTable ({ref_build()})"}
         except Exception as e:  # the baseline is reported, never required
             cpu = {"value": None, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {type(e).__name__}: {e}"}
@@ -758,7 +767,7 @@ def run_reference_arm(args, cells, cfg, metric, world, rank, warmup):
             A = orc.gen_iid(rows, K, seed_of(sa["key"]), value_kind=sa["value_kind"], sigma=sa["sigma"],
                             thresh=sa["thresh"], mask_kind=sa["mask_kind"], p=sa["p"], block=sa["block"])
             C = np.zeros((rows, host_B[sb["key"]].shape[1]), np.float32)
-            cnt = orc.ref_multiply_parallel(C, A, host_B[sb["key"]], workers=threads)
+            cnt = orc.ref_multiply_mmm(C, A, host_B[sb["key"]], workers=threads)
             flops_total += 2 * cnt["lane_fma_ops"]
             time_total += (cnt["multiply_ns"] + cnt["preprocess_ns"] * rows / M) * 1e-9
             rows_used += rows
@@ -772,8 +781,8 @@ def run_reference_arm(args, cells, cfg, metric, world, rank, warmup):
             "cpu_baseline": {"value": round(v, 3), "unit": "GFLOP/s", "cores": orc.ref_lib().ref_max_threads(),
                              "kind": "reference",
                              "sample": f"per step {rows_used} A rows over {len(cells)} cells (full B preprocessing "
-                                       f"amortised per row); SPEC multiply_parallel over the reference's compiled "
-                                       f"KernelTable; median of {args.steps} steps"},
+                                       f"amortised per row); SPEC preprocess_a/b + ABlockIndex-driven leaf-blocked multiply_parallel over the reference's compiled "
+                                       f"KernelTable ({ref_build()}); median of {args.steps} steps"},
             "e2e": {"value": round(v, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

@@ -18,6 +18,21 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORC_SO = os.path.join(HERE, "_build", "liborc.so")
 REF_SO = os.path.join(HERE, "_ref", "libmmmref.so")
+REF_SO_V4 = os.path.join(HERE, "_ref", "libmmmref_v4.so")  # -march=x86-64-v4 (AVX-512) build
+
+
+def _cpu_has_avx512() -> bool:
+    try:
+        flags = open("/proc/cpuinfo").read()
+    except OSError:
+        return False
+    return all(f in flags for f in (" avx512f", " avx512bw", " avx512dq", " avx512vl"))
+
+
+def ref_so_path() -> str:
+    """The reference build for this host: the AVX-512 one where the CPU has it (what the
+    reference's own -march=native gives there), else the AVX2 one."""
+    return REF_SO_V4 if (os.path.exists(REF_SO_V4) and _cpu_has_avx512()) else REF_SO
 
 STRUCTURES = {"random": 0, "block_random": 1, "column": 2, "block_column": 3}
 
@@ -102,7 +117,7 @@ def ref_lib():
     if _ref is None:
         if not ref_available():
             raise FileNotFoundError(f"{REF_SO} not built (needs /root/reference at build time)")
-        L = ctypes.CDLL(REF_SO)
+        L = ctypes.CDLL(ref_so_path())
         L.ref_generate_f32.restype = c_int
         L.ref_generate_f32.argtypes = [c_int64, c_int64, c_int, c_double, c_int64, c_uint64, c_int, c_int, c_int,
                                        c_void_p, POINTER(c_int64)]
@@ -115,6 +130,9 @@ def ref_lib():
         L.ref_multiply_parallel_f32.restype = c_int
         L.ref_multiply_parallel_f32.argtypes = [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64,
                                                 c_int64, c_int64, c_int64, c_int64, c_int, POINTER(RefCounters)]
+        L.ref_multiply_mmm_f32.restype = c_int
+        L.ref_multiply_mmm_f32.argtypes = [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64,
+                                           c_int64, c_int64, c_int, POINTER(RefCounters)]
         L.ref_max_threads.restype = c_int
         _ref = L
     return _ref
@@ -287,6 +305,20 @@ def ref_kernel_apply(code, c, a, b, lane=(8, 8, 1)):
     b = np.ascontiguousarray(b, dtype=np.float32)
     st = ref_lib().ref_kernel_apply_f32(*lane, code, _p(c), a, _p(b))
     return st, c
+
+
+def ref_multiply_mmm(C, A, B, row0=0, row1=None, workers=0):
+    """The reference-kind CPU baseline: SPEC preprocess_b / preprocess_a (ABlockIndex) and the
+    leaf-blocked multiply over the reference's compiled KernelTable (ref_driver.cpp)."""
+    M, lda = A.shape
+    K, ldb = B.shape
+    row1 = M if row1 is None else row1
+    cnt = RefCounters()
+    st = ref_lib().ref_multiply_mmm_f32(_p(C), C.shape[1], _p(A), lda, _p(B), ldb, K, ldb, row0, row1, workers,
+                                        ctypes.byref(cnt))
+    if st != 0:
+        raise RuntimeError(f"reference multiply failed with status {st}")
+    return {k: int(getattr(cnt, k)) for k, _ in RefCounters._fields_}
 
 
 def ref_multiply_parallel(C, A, B, row0=0, row1=None, workers=0):
