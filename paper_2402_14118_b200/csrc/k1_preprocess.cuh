@@ -62,7 +62,7 @@ struct K1Scratch {
   // group, the bits of max|x| and the complement of the SMALLEST LOCAL MAXIMUM (A: of the
   // row's 128-column chunks, B: of the group's 32-k tiles that hold a non-zero), packed in one
   // zero-initialised 64-bit word (a complement turns the min into a max)
-  unsigned long long* rrng;  // [M]: (max << 32) | ~(smallest 128-column chunk max), k1_fold_range
+  unsigned long long* rrng;  // [M]: (max << 32) | ~(smallest 128-column chunk max), k1_red_range
   unsigned long long* grng;  // [ldb / 8]: the same per 8-column group over its 32-k tiles
   int64_t ngrp;           // ldb / 8
   uint32_t* wide_a;       // set when some A row's range is too wide for the fp16 split (zeroed);
@@ -79,7 +79,6 @@ struct K1Scratch {
   int64_t m_at;           // M rounded up to 256 (K2-TC pair tiles)
   uint32_t* tlive;        // [n_tc][kw] live-k mask per kTcTileN-column TC tile: bit kk of word c
                           // set iff B[32c + kk, tile columns] has a non-zero (zeroed, atomicOr)
-  uint32_t* tcnt;         // [n_tc] live k per TC tile (each bit counted by the thread that set it)
   int64_t n_tb;           // 256-column tiles of B (K2-SIMT records)
   int64_t n_tc;           // kTcTileN-column tiles of B (K2-TC)
   int choose;             // AUTO: pick K2-SIMT vs K2-TC from the cost model (both operand sets built)
@@ -98,6 +97,21 @@ struct K1Scratch {
 __device__ void k1_plan_totals(const unsigned long long* __restrict__ btot, int64_t K, int64_t nreg, int has_b,
                                unsigned long long* __restrict__ out);
 
+__device__ __forceinline__ bool k1_range_wide(unsigned long long rng);
+
+// The fp16-split range guard once every tile is in (K1's last CTA): any A row / B group whose
+// range word is too wide (k1_range_wide) sets wide_a / btot[4].
+__device__ void k1_range_flags(const K1Scratch& z, int64_t M, int do_a, int do_b) {
+  bool wa = false, wb = false;
+  if (do_a && z.rrng)
+    for (int64_t i = threadIdx.x; i < M; i += blockDim.x) wa |= k1_range_wide(z.rrng[i]);
+  if (do_b && z.grng)
+    for (int64_t g = threadIdx.x; g < z.ngrp; g += blockDim.x) wb |= k1_range_wide(z.grng[g]);
+  if (__syncthreads_or(wa) && threadIdx.x == 0) *z.wide_a = 1u;
+  if (__syncthreads_or(wb) && threadIdx.x == 0) z.btot[4] = 1ull;
+  __syncthreads();
+}
+
 // AUTO path choice (stats[7] := 32 for K2-TC, else the K2-SIMT span stays): estimated
 // SM-cycles of each path from the plan, constants measured on B200 (K2 choice):
 //   K2-SIMT = records * 1158 + row tiles * (span 16: 26 * slice_nz | span 8: 17.5 * pop)
@@ -112,12 +126,18 @@ __device__ void k1_choose_path(const K1Scratch& z, int64_t M, int64_t kw, unsign
   __shared__ unsigned long long s_stage[32], s_live[32];
   __shared__ uint32_t s_pick;
   unsigned long long st = 0, live = 0;
-  for (int64_t tb = threadIdx.x; tb < z.n_tc; tb += blockDim.x) {  // live k per tile, counted by K1
-    const uint32_t n = z.tcnt[tb];
-    live += n;
-    st += (n + 31) / 32;  // fp16-split stages of 32 live k
-  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // live k per TC tile = popcount of its kw live-k words; a warp per tile
+  for (int64_t tb = warp; tb < z.n_tc; tb += blockDim.x >> 5) {
+    uint32_t n = 0;
+    for (int64_t w = lane; w < kw; w += 32) n += __popc(z.tlive[tb * kw + w]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+    if (lane == 0) {
+      live += n;
+      st += (n + 31) / 32;  // fp16-split stages of 32 live k
+    }
+  }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     st += __shfl_xor_sync(0xffffffffu, st, o);
@@ -396,22 +416,20 @@ __device__ __forceinline__ int k1_chunk(int w, int j) { return 2 * w + (j & 1) +
 // patterns; K1 flags them and AUTO keeps K2-SIMT.
 
 // Fold a tile's local maxima (bits of |x|: largest mx, smallest mn) into a row's / group's
-// range word rng = (max << 32) | ~(smallest local max), one 64-bit compare-and-swap, so every
-// update sees the whole state it produced.  Returns true when that state is too wide for the
-// fp16 split (max exponent outside [-86, 114], or local maxima more than 2^17 apart).  The
-// thread whose CAS is the row's / group's last one sees the final range, so a wide final
-// range is always reported; earlier states are narrower, so nothing is reported falsely.
-__device__ __forceinline__ bool k1_fold_range(unsigned long long* rng, uint32_t mx, uint32_t mn) {
-  unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(rng), nv;
-  for (;;) {
-    const uint32_t m = max((uint32_t)(cur >> 32), mx), c = max((uint32_t)cur, ~mn);
-    nv = ((unsigned long long)m << 32) | c;
-    if (nv == cur) break;
-    const unsigned long long seen = atomicCAS(rng, cur, nv);
-    if (seen == cur) break;
-    cur = seen;
-  }
-  const uint32_t cmax = (uint32_t)(nv >> 32), cmin = ~(uint32_t)nv;
+// range word rng = (max << 32) | ~(smallest local max) with two non-returning 32-bit atomic
+// maxima (RED.MAX: the complement turns the min into a max), so no tile waits on a round
+// trip; whether the final range is too wide for the fp16 split is decided once all tiles are
+// in (k1_range_flags, the last CTA).
+__device__ __forceinline__ void k1_red_range(unsigned long long* rng, uint32_t mx, uint32_t mn) {
+  uint32_t* w = reinterpret_cast<uint32_t*>(rng);  // little-endian: w[1] = high word
+  atomicMax(w + 1, mx);
+  atomicMax(w, ~mn);
+}
+// A final range word too wide for the fp16 split: max exponent outside [-86, 114], or local
+// maxima more than 2^17 apart (0: no non-zero seen)
+__device__ __forceinline__ bool k1_range_wide(unsigned long long rng) {
+  const uint32_t cmax = (uint32_t)(rng >> 32), cmin = ~(uint32_t)rng;
+  if (cmax == 0u) return false;
   const int emax = (int)(cmax >> 23) - 127, emin = (int)(cmin >> 23) - 127;
   return emax < -86 || emax > 114 || emax - emin > 17;
 }
@@ -463,9 +481,13 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         if (FULL || col[j] < z.kpad) {
-          float4* d4 = reinterpret_cast<float4*>(z.at + (rt * z.kpad + col[j]) * 128 + (rb & 127));
-          d4[0] = make_float4(x[0][j], x[1][j], x[2][j], x[3][j]);
-          d4[1] = make_float4(x[4][j], x[5][j], x[6][j], x[7][j]);
+          // one 32-byte store (STG.256: a whole sector per request; two 16-byte stores per
+          // sector made the A^T writes L2-request bound)
+          float* d = z.at + (rt * z.kpad + col[j]) * 128 + (rb & 127);
+          asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(d), "f"(x[0][j]),
+                       "f"(x[1][j]), "f"(x[2][j]), "f"(x[3][j]), "f"(x[4][j]), "f"(x[5][j]), "f"(x[6][j]),
+                       "f"(x[7][j])
+                       : "memory");
         }
     }
 #pragma unroll
@@ -521,7 +543,7 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
     if (n) atomicAdd(&z.arow[r0 + threadIdx.x], n);
   }
 #ifndef K1_NO_RANGE
-  if (z.rrng && threadIdx.x < kK1Rows && r0 + threadIdx.x < rend) {  // one CAS per row and tile
+  if (z.rrng && threadIdx.x < kK1Rows && r0 + threadIdx.x < rend) {  // one RED pair per row and tile
     const int rr = threadIdx.x;
     uint32_t mx = 0u, mn = 0xFFFFFFFFu;
 #pragma unroll
@@ -531,7 +553,7 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
       mx = max(mx, v);
       if (v) mn = min(mn, v);
     }
-    if (mx && k1_fold_range(&z.rrng[r0 + rr], mx, mn)) atomicOr(z.wide_a, 1u);
+    if (mx) k1_red_range(&z.rrng[r0 + rr], mx, mn);
   }
 #endif
   asm volatile("bar.sync 2, %0;" ::"r"(kK1Threads) : "memory");
@@ -620,7 +642,7 @@ __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, 
       }
       const int64_t g = (c0 + 32 * k1_chunk(w, j) + (lane & ~7)) >> 3;  // this lane's 8-column group
       if (z.grng && (lane & 7) == 0 && mx && 8 * g < ldb)  // this tile's max of the group
-        if (k1_fold_range(&z.grng[g], mx, mx)) atomicOr(&z.btot[4], 1ull);
+        k1_red_range(&z.grng[g], mx, mx);
       amax_b = max(amax_b, mx);
       amin_b = min(amin_b, mn);
     }
@@ -636,12 +658,9 @@ __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, 
 #pragma unroll
   for (int o = 16; o; o >>= 1) srows += __shfl_xor_sync(0xffffffffu, srows, o);
   if (lane == 0 && srows) atomicAdd(&z.btot[0], (unsigned long long)srows);
-  if (z.tlive && gword) {  // the bits this thread sets first are its tile's newly live k
-    const int64_t tb = gcol / kTcTileN;
-    const uint32_t old = atomicOr(&z.tlive[tb * kw + kwi], gword);
-    const uint32_t fresh = __popc(gword & ~old);
-    if (fresh) atomicAdd(&z.tcnt[tb], fresh);
-  }
+  // the TC tile's live-k word (non-returning RED.OR; the live counts per tile are taken from
+  // the words by the last CTA, k1_choose_path, and by the TC pack)
+  if (z.tlive && gword) atomicOr(&z.tlive[(gcol / kTcTileN) * kw + kwi], gword);
 }
 
 // Region codes (kernel_table.cpp:19: bit 7-j <-> 8-column group j, MSB first) from the group
@@ -736,6 +755,7 @@ k1_pass(K1Args g, K1Scratch z, int has_a, int has_b, unsigned long long* __restr
     *z.next_tile = 0u;
   }
   k1_plan_totals(z.btot, K, nreg, has_b, stats);
+  k1_range_flags(z, M, nA > 0, nB > 0);
   if (z.choose && has_a && has_b) k1_choose_path(z, M, kw, stats);
   // the K2-SIMT record offsets only when K2-SIMT can run (its pack is gated out otherwise)
   if (z.row_cnt && nB > 0 && !(z.choose && (stats[7] == 32ull || stats[7] == 48ull)))
@@ -756,14 +776,14 @@ k1_pass(K1Args g, K1Scratch z, int has_a, int has_b, unsigned long long* __restr
 // --------------------------------------------------------------- CSR index lists
 // Per-row ascending index lists (CSR: row_ptr int64 [M+1] + columns) from K1's bitmap, no
 // second pass over A: warp ballot words -> popc -> warp prefix sums -> positions.  A CTA owns
-// kCsrRows rows; its 8 warps take the (row, 1024-column chunk) pairs.  row_ptr comes from the
-// 32-row tile prefix the K1 pass's last CTA scanned plus at most 31 row counts; a warp's chunk
-// offset within its row is the popcount of the row's earlier words.  The set bits are
-// expanded by each lane into a per-warp shared staging buffer and copied out coalesced.  In
-// AUTO these CTAs ride in the B pack launch (k1_pack_auto), next to the memory-bound pack
-// CTAs, instead of a launch of their own.
+// kCsrRows = 8 rows, warp w row r0 + w, walked in 1024-column chunks with a running offset
+// (so no word is read twice).  row_ptr comes from the 32-row tile prefix the K1 pass's last
+// CTA scanned plus at most 31 row counts.  Each lane expands its word's set bits into the
+// warp's shared staging run (lane order = ascending column), then the chunk's list is copied
+// out coalesced.  In AUTO these items ride in the pack launch (k1_pack_auto), next to the
+// memory-bound pack items, instead of a launch of their own.
 // Index type: uint16 when K <= 65536, else uint32.
-constexpr int kCsrRows = 2;
+constexpr int kCsrRows = 8;
 
 struct CsrArgs {
   const uint32_t* abits;
@@ -775,10 +795,10 @@ struct CsrArgs {
   int idx_bytes;    // 2 or 4
 };
 
-// stage: dynamic shared memory of (blockDim / 32) x 1024 indices (k1_csr_smem)
+// stage: dynamic shared memory of (blockDim / 32) x 1024 indices (k1_csr_smem); 256 threads
 __device__ __forceinline__ void k1_csr_cta(const CsrArgs& g, int64_t cta, void* stage) {
   __shared__ int64_t s_off[kCsrRows + 1];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = (int)(blockDim.x >> 5);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t r0 = cta * kCsrRows, M = g.M, kw = g.kw;
   if (warp == 0) {
     const int64_t t0 = (r0 / 32) * 32;  // first row of r0's 32-row tile
@@ -802,46 +822,44 @@ __device__ __forceinline__ void k1_csr_cta(const CsrArgs& g, int64_t cta, void* 
   __syncthreads();
   if (threadIdx.x < kCsrRows && r0 + threadIdx.x < M) g.row_ptr[r0 + threadIdx.x] = s_off[threadIdx.x];
   if (threadIdx.x == 0 && r0 + kCsrRows >= M) g.row_ptr[M] = s_off[M - r0];
-  const int64_t nch = (kw + 31) / 32;
-  for (int64_t pr = warp; pr < kCsrRows * nch; pr += nwarp) {
-    const int64_t rr = pr / nch, ch = pr % nch, row = r0 + rr;
-    if (row >= M) break;
+  const int64_t row = r0 + warp;
+  if (warp < kCsrRows && row < M) {
     const uint32_t* bits = g.abits + row * kw;
-    const int64_t w = ch * 32 + lane;
-    uint32_t word = w < kw ? bits[w] : 0u;
-    uint32_t before = 0;  // set bits of the row's earlier chunks
-    for (int64_t e = lane; e < ch * 32; e += 32) before += __popc(bits[e]);
+    int64_t out = s_off[warp];
+    uint32_t nxt = lane < kw ? bits[lane] : 0u;  // the next chunk's word, loaded one chunk ahead
+    for (int64_t c0 = 0; c0 < kw; c0 += 32) {
+      const int64_t w = c0 + lane;
+      uint32_t word = nxt;
+      nxt = w + 32 < kw ? bits[w + 32] : 0u;
+      const uint32_t n = __popc(word);
+      uint32_t x = n;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
-    const uint32_t n = __popc(word);
-    uint32_t x = n;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      // expand the set bits into this warp's shared staging run, then one coalesced copy of
+      // the chunk's list (scattered 2-byte global stores cost the L2 ~20x their bytes)
+      const uint32_t col0 = (uint32_t)(w * 32), total = __shfl_sync(0xffffffffu, x, 31);
+      uint32_t pos = x - n;
+      if (g.idx_bytes == 2) {
+        uint16_t* buf = reinterpret_cast<uint16_t*>(stage) + warp * 1024;
+        for (; word; word &= word - 1u) buf[pos++] = (uint16_t)(col0 + (uint32_t)__ffs(word) - 1u);
+        __syncwarp();
+        uint16_t* dst = static_cast<uint16_t*>(g.cols) + out;
+        for (uint32_t i = lane; i < total; i += 32) dst[i] = buf[i];
+      } else {
+        uint32_t* buf = reinterpret_cast<uint32_t*>(stage) + warp * 1024;
+        for (; word; word &= word - 1u) buf[pos++] = col0 + (uint32_t)__ffs(word) - 1u;
+        __syncwarp();
+        uint32_t* dst = static_cast<uint32_t*>(g.cols) + out;
+        for (uint32_t i = lane; i < total; i += 32) dst[i] = buf[i];
+      }
+      out += total;
+      __syncwarp();  // the staging run is reused by the next chunk
     }
-    // expand the set bits into this warp's shared staging run (lane order = ascending column),
-    // then one coalesced copy of the chunk's list (scattered 2-byte global stores cost the L2
-    // ~20x their bytes in partial-sector writes: measured +25 us per 4096^2 cell)
-    const int64_t out = s_off[rr] + before;
-    const uint32_t col0 = (uint32_t)(w * 32), total = __shfl_sync(0xffffffffu, x, 31);
-    uint32_t pos = x - n;
-    if (g.idx_bytes == 2) {
-      uint16_t* buf = reinterpret_cast<uint16_t*>(stage) + warp * 1024;
-      for (; word; word &= word - 1u) buf[pos++] = (uint16_t)(col0 + (uint32_t)__ffs(word) - 1u);
-      __syncwarp();
-      uint16_t* dst = static_cast<uint16_t*>(g.cols) + out;
-      for (uint32_t i = lane; i < total; i += 32) dst[i] = buf[i];
-    } else {
-      uint32_t* buf = reinterpret_cast<uint32_t*>(stage) + warp * 1024;
-      for (; word; word &= word - 1u) buf[pos++] = col0 + (uint32_t)__ffs(word) - 1u;
-      __syncwarp();
-      uint32_t* dst = static_cast<uint32_t*>(g.cols) + out;
-      for (uint32_t i = lane; i < total; i += 32) dst[i] = buf[i];
-    }
-    __syncwarp();
   }
-  __syncthreads();  // s_off is reused by this CTA's next row pair (k1_pack_auto)
+  __syncthreads();  // s_off is reused by this CTA's next item (k1_pack_auto)
 }
 
 // Standalone launch (forced K2 variants, A-only preprocessing).
@@ -966,7 +984,7 @@ __device__ void k1_plan_totals(const unsigned long long* __restrict__ btot, int6
 // define a step), so padding is at most 7 k per tile.
 constexpr int kPackThreads = 256;  // k1_pack_rows
 #ifndef K1_PT_STEPS
-#define K1_PT_STEPS 4
+#define K1_PT_STEPS 8
 #endif
 constexpr int kPtSteps = K1_PT_STEPS;  // step images per K2-TC pack CTA
 constexpr int kPtThreads = 256;
@@ -1048,32 +1066,55 @@ __device__ __forceinline__ void k1_pack_tc_cta(const PackTcArgs& g, int64_t bx, 
   }
   __syncthreads();
   if (g.f16) {
-    // job = (step, k-octet q, column n): 8 B values (scaled by 2^sB) -> 8 fp16 hi + 8 fp16
-    // lo, one 16-byte store each.  K2-TC runs fp16 tiles on CTA pairs, each CTA holding one
-    // column half h (96 columns) of B: a tile's images are stored per half, [h][step], a
-    // half step = hi image (3 KB) | lo image (3 KB), element (c, j) of column c = n - 96h at
-    // byte (c % 8) * 16 + (c / 8) * 256 + (j / 8) * 128 + (j % 8) * 2 of its image
-    for (int j = tid; j < kPtSteps * 2 * kTcTileN; j += kPtThreads) {
-      const int sl = j / (2 * kTcTileN), q = (j / kTcTileN) & 1, n = j % kTcTileN;
+    // job = (step, k-octet q, 4-column group c4 of the 48 in the tile): 8 rows x 4 columns of B
+    // by 8 independent 16-byte loads (a warp reads 512 contiguous bytes per row), scaled by the
+    // columns' 8-column group's 2^sB, split into fp16 hi / lo: 4 columns x 8 k = one 16-byte
+    // hi and one 16-byte lo store per column.  K2-TC runs fp16 tiles on CTA pairs, each CTA
+    // holding one column half h (96 columns) of B: a tile's images are stored per half,
+    // [h][step], a half step = hi image (3 KB) | lo image (3 KB), element (c, j) of column
+    // c = n - 96h at byte (c % 8) * 16 + (c / 8) * 256 + (j / 8) * 128 + (j % 8) * 2 of its image
+    constexpr int kC4 = kTcTileN / 4, kHalf = kTcTileN / 2;
+    constexpr int kJobs = kPtSteps * 2 * kC4, kPer = (kJobs + kPtThreads - 1) / kPtThreads;
+    // per job 8 independent 16-byte loads in flight (4 CTAs per SM: ~128 KB per SM)
+#pragma unroll 1
+    for (int u = 0; u < kPer; ++u) {
+      const int j = tid + u * kPtThreads;
+      const int sl = j / (2 * kC4), q = (j / kC4) & 1, n = 4 * (j % kC4);
       const int64_t s = s0 + sl;
-      if (s >= nsteps) break;
-      const bool col_ok = n0 + n < ldb;
-      const float sb = col_ok ? tc::exp2_int(tc::f16_scale_exp((uint32_t)(__ldg(g.grng + ((n0 + n) >> 3)) >> 32))) : 1.0f;
-      float v[8];
+      if (j >= kJobs || s >= nsteps) break;
+      float4 v[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const int32_t k = s_k[sl * 16 + 8 * q + i];
-        v[i] = (k >= 0 && col_ok) ? __ldg(B + (int64_t)k * ldb + n0 + n) * sb : 0.0f;
+        const int32_t k = n0 + n < ldb ? s_k[sl * 16 + 8 * q + i] : -1;
+        v[i] = k >= 0 ? ldg_stream(B + (int64_t)k * ldb + n0 + n) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      uint32_t h[4], l[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) tc::split_f16x2(v[2 * i], v[2 * i + 1], h[i], l[i]);
-      constexpr int kHalf = kTcTileN / 2;
+      const bool col_ok = n0 + n < ldb;
+      const float sb = col_ok ? tc::exp2_int(tc::f16_scale_exp((uint32_t)(__ldg(g.grng + ((n0 + n) >> 3)) >> 32))) : 1.0f;
       const int hf = n / kHalf, c = n % kHalf;
       float* img = tcb + ((tb * 2 + hf) * maxsteps + s) * (kHalf * 16);
-      const int off = (c & 7) * 4 + (c >> 3) * 64 + q * 32;  // in floats
-      *reinterpret_cast<uint4*>(img + off) = make_uint4(h[0], h[1], h[2], h[3]);
-      *reinterpret_cast<uint4*>(img + kHalf * 8 + off) = make_uint4(l[0], l[1], l[2], l[3]);
+      const int off = (c & 7) * 4 + (c >> 3) * 64 + q * 32;  // in floats; columns c .. c+3 follow at +4
+      uint32_t h[4][4], l[4][4];
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        float x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          x[i] = (cc == 0 ? v[i].x : cc == 1 ? v[i].y : cc == 2 ? v[i].z : v[i].w) * sb;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) tc::split_f16x2(x[2 * i], x[2 * i + 1], h[cc][i], l[cc][i]);
+      }
+      // columns c, c+1 (and c+2, c+3) are adjacent 16-byte chunks: two 32-byte stores per image
+#pragma unroll
+      for (int pr = 0; pr < 2; ++pr) {
+        asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(img + off + 8 * pr),
+                     "r"(h[2 * pr][0]), "r"(h[2 * pr][1]), "r"(h[2 * pr][2]), "r"(h[2 * pr][3]),
+                     "r"(h[2 * pr + 1][0]), "r"(h[2 * pr + 1][1]), "r"(h[2 * pr + 1][2]), "r"(h[2 * pr + 1][3])
+                     : "memory");
+        asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(img + kHalf * 8 + off + 8 * pr),
+                     "r"(l[2 * pr][0]), "r"(l[2 * pr][1]), "r"(l[2 * pr][2]), "r"(l[2 * pr][3]),
+                     "r"(l[2 * pr + 1][0]), "r"(l[2 * pr + 1][1]), "r"(l[2 * pr + 1][2]), "r"(l[2 * pr + 1][3])
+                     : "memory");
+      }
     }
     return;
   }
@@ -1102,7 +1143,7 @@ __device__ __forceinline__ void k1_pack_tc_cta(const PackTcArgs& g, int64_t bx, 
   }
 }
 
-__global__ void __launch_bounds__(kPtThreads) k1_pack_tc(PackTcArgs g) { k1_pack_tc_cta(g, blockIdx.x, blockIdx.y); }
+__global__ void __launch_bounds__(kPtThreads, 4) k1_pack_tc(PackTcArgs g) { k1_pack_tc_cta(g, blockIdx.x, blockIdx.y); }
 
 // ----------------------------------------------------------- B rows for K2-SIMT
 // For each 256-column tile tb and 32-k chunk c, a contiguous record at row_off[tb*kw + c]
@@ -1170,27 +1211,25 @@ __global__ void __launch_bounds__(kPackThreads) k1_pack_rows(PackRowsArgs g) {
   k1_pack_rows_cta(g, blockIdx.x, blockIdx.y);
 }
 
-// AUTO: both packs in one launch (CTAs [0, n_tc) = K2-TC steps, the rest = K2-SIMT rows),
-// each CTA gated by the path K1's last CTA chose — one launch instead of two, and the
-// gated-out half exits at entry.
-__global__ void __launch_bounds__(kPtThreads)
-k1_pack_auto(PackRowsArgs gr, int64_t rows_x, int64_t n_rows, PackTcArgs gt, int64_t tc_x,
+// AUTO: the K2-TC step images, the K2-SIMT record rows (only the one K1's last CTA chose) and
+// A's CSR index lists in ONE persistent launch: each CTA walks the work items w = blockIdx.x,
+// + gridDim.x, ... of [chosen pack items | CSR items], so the gated-out pack costs nothing
+// (one CTA per item made ~5.5 k CTAs per 4096^2 cell, most of them exiting at entry).
+__global__ void __launch_bounds__(kPtThreads, 4)
+k1_pack_auto(PackRowsArgs gr, int64_t rows_x, int64_t n_rows, PackTcArgs gt, int64_t tc_x, int64_t n_tcb,
              const unsigned long long* __restrict__ sel, CsrArgs gc, int64_t n_csr) {
-  // CTAs [0, n_csr): the CSR index lists of A (when A was preprocessed); then the K2-TC CTAs:
-  // the gated-out K2-SIMT CTAs (the larger part of the grid) exit behind the work instead of
-  // in front of it when TC is chosen
   tc::pdl_wait();  // launched with programmatic serialization after k1_pass
-  if ((int64_t)blockIdx.x < n_csr) {
-    extern __shared__ __align__(16) uint32_t pt_smem[];  // (the TC pack's dynamic smem, here the CSR staging)
-    k1_csr_cta(gc, blockIdx.x, pt_smem);
-    return;
-  }
-  const int64_t bid = blockIdx.x - n_csr, n_tcb = (int64_t)gridDim.x - n_csr - n_rows;
+  extern __shared__ __align__(16) uint32_t pt_smem[];  // TC pack scan words / CSR staging
   const unsigned long long v = *sel;  // 8 / 16 K2-SIMT (rows), 32 K2-TC (step images), 48 K2-CSR (neither)
-  if (bid < n_tcb) {
-    if (v == 32ull) k1_pack_tc_cta(gt, bid % tc_x, bid / tc_x);
-  } else if (v == 8ull || v == 16ull) {
-    k1_pack_rows_cta(gr, (bid - n_tcb) % rows_x, (bid - n_tcb) / rows_x);
+  const int64_t n_pack = v == 32ull ? n_tcb : (v == 8ull || v == 16ull) ? n_rows : 0;
+  for (int64_t w = blockIdx.x; w < n_pack + n_csr; w += gridDim.x) {
+    if (w < n_pack) {
+      if (v == 32ull) k1_pack_tc_cta(gt, w % tc_x, w / tc_x);
+      else k1_pack_rows_cta(gr, w % rows_x, w / rows_x);
+    } else {
+      k1_csr_cta(gc, w - n_pack, pt_smem);
+    }
+    __syncthreads();  // shared memory is reused by the next item
   }
 }
 

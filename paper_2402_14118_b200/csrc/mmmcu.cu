@@ -253,10 +253,9 @@ int ops_for(const mmmcu_ctx* ctx) {
 }
 uint32_t* zb_tlive(mmmcu_ctx* ctx) { return zb_bnz(ctx) + ctx->Kb; }
 int64_t n_cnt_tc(const mmmcu_ctx* ctx) { return ctx->n_tc * ((ctx->Kb + 31) / 32); }
-// live k per TC tile (counted as K1 sets the tlive bits), then the K2-SIMT record counts
-uint32_t* zb_tcnt(mmmcu_ctx* ctx) { return zb_tlive(ctx) + n_cnt_tc(ctx); }
+// after the TC live-k words: the K2-SIMT record counts
 uint32_t* zb_row_cnt(mmmcu_ctx* ctx) {
-  return zb_tlive(ctx) + ((ctx->ops_b & OP_TCB) ? n_cnt_tc(ctx) + ctx->n_tc : 0);
+  return zb_tlive(ctx) + ((ctx->ops_b & OP_TCB) ? n_cnt_tc(ctx) : 0);
 }
 
 // Switch a double-buffered K1 scratch to its other half (zeroed by the previous K1 pass), or
@@ -403,9 +402,12 @@ mmmcu_status pack_auto(mmmcu_ctx* ctx, const unsigned long long* sel, bool with_
   const int smem_all = with_csr ? std::max(smem, mmmcu::k1_csr_smem(ctx->csr_idx_bytes)) : smem;
   if (n_rows + n_tc + n_csr > 0x7fffffff) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "B too large for one pack launch");
   MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k1_pack_auto, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_all));
-  MMMCU_CUDA(launch_pdl(mmmcu::k1_pack_auto, dim3((unsigned)(n_rows + n_tc + n_csr)), dim3(mmmcu::kPtThreads), smem_all,
-                        ctx->stream, rows_args(ctx), rows_x, n_rows, tc_args(ctx, true), tc_x, sel, csr_args(ctx),
-                        n_csr));
+  // persistent: 4 CTAs per SM (the register-limited residency) walk the items of the chosen
+  // pack and the CSR
+  const int64_t items = std::max(n_rows, n_tc) + n_csr;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(items, 4 * (int64_t)ctx->num_sms));
+  MMMCU_CUDA(launch_pdl(mmmcu::k1_pack_auto, dim3((unsigned)grid), dim3(mmmcu::kPtThreads), smem_all, ctx->stream,
+                        rows_args(ctx), rows_x, n_rows, tc_args(ctx, true), tc_x, n_tc, sel, csr_args(ctx), n_csr));
   MMMCU_LAUNCHED();
   ctx->tcb_f16 = true;
   return MMMCU_OK;
@@ -457,7 +459,6 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   z.kpad = ctx->kpad;
   z.m_at = ctx->m_at;
   z.tlive = tcb_b ? zb_tlive(ctx) : nullptr;
-  z.tcnt = tcb_b ? zb_tcnt(ctx) : nullptr;
   z.row_cnt = rows_b ? zb_row_cnt(ctx) : nullptr;
   z.row_off = rows_b ? ctx->row_off.as<int64_t>() : nullptr;
   z.n_tb = ctx->n_tb;
