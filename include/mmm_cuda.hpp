@@ -1,7 +1,7 @@
 // mmm_cuda.hpp — C++ drop-in for the reference's masked-multiply engine, on the B200 C ABI.
 //
 // A caller of the reference (namespace mmm) keeps its types and call sites:
-// Matrix<float> and LaneConfig come from the reference's own mmm/matrix.hpp
+// Matrix<T> (T = float or double) and LaneConfig come from the reference's own mmm/matrix.hpp
 // (/root/reference/proj/include/mmm/matrix.hpp:31-164, on the include path of the
 // integrating build), and the SPEC entry points below forward to include/mmmcu.h.
 // Header-only; link libmmmcu.so.  Exceptions mirror the reference's error behaviour:
@@ -15,7 +15,9 @@
 
 #include <cstdint>
 #include <stdexcept>
+#include <algorithm>
 #include <string>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -48,7 +50,7 @@ struct WorkCounters {
 // BPlan and ABlockIndex (layout decision :229).
 struct BPlan {
   int64_t submatrix_id = 0;
-  std::vector<uint8_t> codes;  // P = 8: one byte per region, multiply order
+  std::vector<uint16_t> codes;  // one P-bit code (P <= 16) per region, multiply order
 };
 struct ABlockIndex {
   int64_t block_dim = 256;
@@ -103,29 +105,37 @@ class Handle {
 template <typename T>
 class MmmContext;
 
-// How C is accumulated.  Auto (default): the plan picks K2-SIMT or the fp16-split tensor-core
-// K2-TC per multiply, C within the north_star tolerance |dC| <= 1e-5 (|c0| + sum|a||b|).
-// Exact: K2-SIMT only, which replays the reference kernel's ascending-k fmaf chain: C is
-// bit-identical to KernelTable::apply (kernel_table.cpp).
 enum class Accumulation { Auto, Exact };
 
-template <>
-class MmmContext<float> {
+namespace cuda_detail {
+template <typename T>
+constexpr mmmcu_dtype dtype_code() {
+  static_assert(std::is_same_v<T, float> || std::is_same_v<T, double>, "the reference compiles f32 and f64 only");
+  return std::is_same_v<T, double> ? MMMCU_F64 : MMMCU_F32;
+}
+}  // namespace cuda_detail
+
+// MmmContext<T> for the reference's two dtypes and any valid LaneConfig:
+// f32 with the default lane runs the fused K1 / K2 kernels (Accumulation::Auto picks K2-TC
+// or the exact K2-SIMT on the device; Exact forces the bit-identical chain); every other
+// (dtype, lane) runs the lane-general kernels, always bit-identical to KernelTable<T>.
+template <typename T>
+class MmmContext {
  public:
-  MmmContext(const Matrix<float>& a, const Matrix<float>& b,
-             LaneConfig lane = LaneConfig::defaults(Dtype::f32), int64_t leaf_dim = 256, int device = 0,
-             Accumulation accumulation = Accumulation::Auto)
+  MmmContext(const Matrix<T>& a, const Matrix<T>& b, LaneConfig lane = LaneConfig::defaults(dtype_of<T>()),
+             int64_t leaf_dim = 256, int device = 0, Accumulation accumulation = Accumulation::Auto)
       : h_(device), lane_(lane), leaf_dim_(leaf_dim), rows_(a.rows()), inner_(a.cols()), cols_(b.cols()) {
     if (a.cols() != b.rows())
       throw DimensionMismatch("a.cols (" + std::to_string(a.cols()) + ") != b.rows (" + std::to_string(b.rows()) +
                               ")");
-    cuda_detail::check(mmmcu_validate_lane(h_.get(), cuda_detail::lane_of(lane)), h_.get());
+    constexpr mmmcu_dtype dt = cuda_detail::dtype_code<T>();
+    cuda_detail::check(mmmcu_validate_lane_t(h_.get(), dt, cuda_detail::lane_of(lane)), h_.get());
     cuda_detail::check(
         mmmcu_set_algo(h_.get(), accumulation == Accumulation::Exact ? MMMCU_ALGO_SIMT_BCAST : MMMCU_ALGO_AUTO),
         h_.get());
-    cuda_detail::check(mmmcu_preprocess_host(h_.get(), a.data(), a.rows(), a.cols(), a.padded_cols(), b.data(),
-                                             b.cols(), b.padded_cols(), cuda_detail::lane_of(lane), a.version(),
-                                             b.version()),
+    cuda_detail::check(mmmcu_preprocess_host_t(h_.get(), dt, a.data(), a.rows(), a.cols(), a.padded_cols(), b.data(),
+                                               b.cols(), b.padded_cols(), cuda_detail::lane_of(lane), a.version(),
+                                               b.version()),
                        h_.get());
     av_ = a.version();
     bv_ = b.version();
@@ -137,15 +147,15 @@ class MmmContext<float> {
   const WorkCounters& counters() const { return counters_; }
   mmmcu_ctx* native() const { return h_.get(); }
 
-  WorkCounters multiply(Matrix<float>& c, const Matrix<float>& a, const Matrix<float>& b, int workers) {
+  WorkCounters multiply(Matrix<T>& c, const Matrix<T>& a, const Matrix<T>& b, int workers) {
     if (a.rows() != rows_ || a.cols() != inner_ || b.cols() != cols_ || c.rows() != rows_ || c.cols() != cols_)
       throw DimensionMismatch("operand shapes differ from the context's plans");
     if (a.version() != av_ || b.version() != bv_)
       throw StaleContextError("stale context: operands changed since preprocessing (Matrix::version)");
     mmmcu_counters cnt{};
     // c.data() (mutable) bumps c's version: c is written, as in the reference engine
-    cuda_detail::check(mmmcu_multiply_planned_host(h_.get(), c.data(), c.padded_cols(), a.version(), b.version(),
-                                                   workers, &cnt),
+    cuda_detail::check(mmmcu_multiply_planned_host_t(h_.get(), cuda_detail::dtype_code<T>(), c.data(),
+                                                     c.padded_cols(), a.version(), b.version(), workers, &cnt),
                        h_.get());
     counters_ = cuda_detail::counters_of(cnt);
     return counters_;
@@ -161,23 +171,24 @@ class MmmContext<float> {
 };
 
 // preprocess_b: one BPlan per leaf_dim x leaf_dim sub-block of B.
-inline std::vector<BPlan> preprocess_b(const Matrix<float>& b, const LaneConfig& lane, int64_t leaf_dim = 256,
-                                       int device = 0) {
+template <typename T>
+std::vector<BPlan> preprocess_b(const Matrix<T>& b, const LaneConfig& lane, int64_t leaf_dim = 256, int device = 0) {
   cuda_detail::Handle h(device);
-  cuda_detail::check(mmmcu_validate_lane(h.get(), cuda_detail::lane_of(lane)), h.get());
+  constexpr mmmcu_dtype dt = cuda_detail::dtype_code<T>();
+  cuda_detail::check(mmmcu_validate_lane_t(h.get(), dt, cuda_detail::lane_of(lane)), h.get());
   // device copy of B through the host-plan path (a 1 x b.rows() zero A keeps shapes valid)
-  Matrix<float> a0(1, b.rows(), lane);
-  cuda_detail::check(mmmcu_preprocess_host(h.get(), a0.data(), 1, b.rows(), a0.padded_cols(), b.data(), b.cols(),
-                                           b.padded_cols(), cuda_detail::lane_of(lane), 0, b.version()),
+  Matrix<T> a0(1, b.rows(), lane);
+  cuda_detail::check(mmmcu_preprocess_host_t(h.get(), dt, a0.data(), 1, b.rows(), a0.padded_cols(), b.data(),
+                                             b.cols(), b.padded_cols(), cuda_detail::lane_of(lane), 0, b.version()),
                      h.get());
   const int64_t nreg = b.padded_cols() / lane.region_width();
-  const int64_t rpl = leaf_dim / lane.region_width();
+  const int64_t rpl = std::max<int64_t>(leaf_dim / lane.region_width(), 1);
   const int64_t n_pl = ((b.rows() + leaf_dim - 1) / leaf_dim) * ((nreg + rpl - 1) / rpl);
-  std::vector<uint8_t> flat(static_cast<size_t>(b.rows() * nreg));
+  std::vector<uint16_t> flat(static_cast<size_t>(b.rows() * nreg));
   std::vector<int64_t> off(static_cast<size_t>(n_pl + 1));
   int64_t n = 0;
-  cuda_detail::check(mmmcu_export_bplans(h.get(), leaf_dim, flat.data(), static_cast<int64_t>(flat.size()),
-                                         off.data(), static_cast<int64_t>(off.size()), &n),
+  cuda_detail::check(mmmcu_export_bplans16(h.get(), leaf_dim, flat.data(), static_cast<int64_t>(flat.size()),
+                                           off.data(), static_cast<int64_t>(off.size()), &n),
                      h.get());
   std::vector<BPlan> plans(static_cast<size_t>(n));
   for (int64_t p = 0; p < n; ++p) {
@@ -188,12 +199,14 @@ inline std::vector<BPlan> preprocess_b(const Matrix<float>& b, const LaneConfig&
 }
 
 // preprocess_a.
-inline ABlockIndex preprocess_a(const Matrix<float>& a, int64_t block_dim = 256, int device = 0) {
+template <typename T>
+ABlockIndex preprocess_a(const Matrix<T>& a, int64_t block_dim = 256, int device = 0) {
   cuda_detail::Handle h(device);
-  const LaneConfig lane = LaneConfig::defaults(Dtype::f32);
-  Matrix<float> b0(a.cols(), 1, lane);
-  cuda_detail::check(mmmcu_preprocess_host(h.get(), a.data(), a.rows(), a.cols(), a.padded_cols(), b0.data(), 1,
-                                           b0.padded_cols(), cuda_detail::lane_of(lane), a.version(), 0),
+  const LaneConfig lane = LaneConfig::defaults(dtype_of<T>());
+  Matrix<T> b0(a.cols(), 1, lane);
+  cuda_detail::check(mmmcu_preprocess_host_t(h.get(), cuda_detail::dtype_code<T>(), a.data(), a.rows(), a.cols(),
+                                             a.padded_cols(), b0.data(), 1, b0.padded_cols(),
+                                             cuda_detail::lane_of(lane), a.version(), 0),
                      h.get());
   ABlockIndex idx;
   idx.block_dim = block_dim;
@@ -212,7 +225,7 @@ inline PlanStats plan_stats(const std::vector<BPlan>& plans) {
   PlanStats s;
   int64_t zeros = 0, pop = 0;
   for (const BPlan& p : plans)
-    for (uint8_t c : p.codes) {
+    for (uint16_t c : p.codes) {
       ++s.region_count;
       zeros += c == 0;
       pop += __builtin_popcount(c);
@@ -225,23 +238,27 @@ inline PlanStats plan_stats(const std::vector<BPlan>& plans) {
 }
 
 // multiply_mmm / multiply_parallel.
-inline WorkCounters multiply_mmm(MmmContext<float>& ctx, Matrix<float>& c, const Matrix<float>& a,
-                                 const Matrix<float>& b) {
+template <typename T>
+WorkCounters multiply_mmm(MmmContext<T>& ctx, Matrix<T>& c, const Matrix<T>& a, const Matrix<T>& b) {
   return ctx.multiply(c, a, b, 1);
 }
-inline WorkCounters multiply_parallel(MmmContext<float>& ctx, Matrix<float>& c, const Matrix<float>& a,
-                                      const Matrix<float>& b, int worker_count) {
+template <typename T>
+WorkCounters multiply_parallel(MmmContext<T>& ctx, Matrix<T>& c, const Matrix<T>& a, const Matrix<T>& b,
+                               int worker_count) {
   if (worker_count <= 0) throw std::invalid_argument("worker_count must be positive");
   return ctx.multiply(c, a, b, worker_count);
 }
 
-// multiply_simple: dense i-k-j c += a*b with fmaf, on the GPU.
-inline void multiply_simple(Matrix<float>& c, const Matrix<float>& a, const Matrix<float>& b, int device = 0) {
+// multiply_simple: dense i-k-j c += a*b with fma per term, on the GPU.
+template <typename T>
+void multiply_simple(Matrix<T>& c, const Matrix<T>& a, const Matrix<T>& b, int device = 0) {
   if (a.cols() != b.rows() || c.rows() != a.rows() || c.cols() != b.cols())
     throw DimensionMismatch("multiply_simple: shapes do not chain");
-  MmmContext<float> ctx(a, b, LaneConfig::defaults(Dtype::f32), 256, device);
-  cuda_detail::check(mmmcu_set_algo(ctx.native(), MMMCU_ALGO_DENSE), ctx.native());
-  ctx.multiply(c, a, b, 1);
+  cuda_detail::Handle h(device);
+  cuda_detail::check(mmmcu_multiply_simple_host_t(h.get(), cuda_detail::dtype_code<T>(), c.data(), c.padded_cols(),
+                                                  a.data(), a.padded_cols(), b.data(), b.padded_cols(), a.rows(),
+                                                  a.cols(), b.cols()),
+                     h.get());
 }
 
 }  // namespace mmm

@@ -18,8 +18,10 @@
  *   - Operand layout is the reference Matrix<float> layout (matrix.hpp:61-83): row-major,
  *     element (i, j) at i*ld + j, ld a multiple of the region width R = W*P*V (64 for the
  *     f32 defaults) and columns [cols, ld) exactly zero.
- *   - Only the f32 default lane config {W=8, P=8, V=1} (matrix.hpp:36-38) is implemented
- *     on the GPU; any other returns MMMCU_ERR_UNSUPPORTED.  There is no CPU fallback.
+ *   - The f32 default lane config {W=8, P=8, V=1} (matrix.hpp:36-38) runs the fused K1 / K2
+ *     kernels; every other valid lane config (G = W*V in {1, 2, ..., 64}, P in [1, 16]) and
+ *     f64 (the *_t entry points) run the lane-general kernels (kgen.cuh), bit-identical to
+ *     the reference's KernelTable<T>.  There is no CPU fallback.
  */
 #ifndef MMMCU_H_
 #define MMMCU_H_
@@ -50,6 +52,9 @@ typedef enum {
 } mmmcu_status;
 
 typedef struct mmmcu_ctx mmmcu_ctx;
+
+/* Dtype (matrix.hpp:13-26): f32 = 0, f64 = 1. */
+typedef enum { MMMCU_F32 = 0, MMMCU_F64 = 1 } mmmcu_dtype;
 
 /* LaneConfig (matrix.hpp:31-44). */
 typedef struct {
@@ -189,6 +194,34 @@ mmmcu_status mmmcu_multiply_simple(mmmcu_ctx* ctx, float* C, int64_t ldc, const 
                                    int64_t lda, const float* B, int64_t ldb, int64_t M, int64_t K,
                                    int64_t N);
 
+/* ---- every dtype and lane config of the reference ---------------
+ * Typed (void*) twins of the calls above: dtype MMMCU_F32 with the default lane forwards to
+ * them; f32 with another lane and f64 with any lane build a lane-general plan (pattern codes
+ * of P bits per region of R = W*P*V columns, MSB first; the same A bitmap / CSR) and the
+ * multiply is the reference's per-element fma chain over it (exact, bit-identical to
+ * KernelTable<T>).  Operands are Matrix<T> layouts: ldb a multiple of R, ldc >= ldb. */
+mmmcu_status mmmcu_validate_lane_t(mmmcu_ctx* ctx, mmmcu_dtype dtype, mmmcu_lane lane);
+mmmcu_status mmmcu_preprocess_a_t(mmmcu_ctx* ctx, mmmcu_dtype dtype, const void* A, int64_t M, int64_t K,
+                                  int64_t lda, uint64_t a_version);
+mmmcu_status mmmcu_preprocess_b_t(mmmcu_ctx* ctx, mmmcu_dtype dtype, const void* B, int64_t K, int64_t N,
+                                  int64_t ldb, mmmcu_lane lane, uint64_t b_version);
+mmmcu_status mmmcu_preprocess_t(mmmcu_ctx* ctx, mmmcu_dtype dtype, const void* A, int64_t M, int64_t K,
+                                int64_t lda, const void* B, int64_t N, int64_t ldb, mmmcu_lane lane,
+                                uint64_t a_version, uint64_t b_version);
+mmmcu_status mmmcu_multiply_t(mmmcu_ctx* ctx, mmmcu_dtype dtype, void* C, int64_t ldc, const void* A,
+                              const void* B, uint64_t a_version, uint64_t b_version,
+                              mmmcu_counters* counters);
+mmmcu_status mmmcu_multiply_simple_t(mmmcu_ctx* ctx, mmmcu_dtype dtype, void* C, int64_t ldc,
+                                     const void* A, int64_t lda, const void* B, int64_t ldb,
+                                     int64_t M, int64_t K, int64_t N);
+/* Pattern codes of any plan as uint16 [K][ldb/R] (P up to 16), and the BPlan order of them. */
+mmmcu_status mmmcu_export_b_codes16(mmmcu_ctx* ctx, uint16_t* codes_host, int64_t capacity);
+mmmcu_status mmmcu_export_bplans16(mmmcu_ctx* ctx, int64_t leaf_dim, uint16_t* plans_host,
+                                   int64_t plans_capacity, int64_t* plan_off_host,
+                                   int64_t off_capacity, int64_t* n_plans);
+/* dtype and {G, P, 1} of the current B plan. */
+mmmcu_status mmmcu_plan_info(mmmcu_ctx* ctx, mmmcu_dtype* dtype, mmmcu_lane* lane);
+
 /* ---- host-buffer convenience (the drop-in path for host Matrix<float> operands) ------- */
 
 /*
@@ -210,6 +243,21 @@ mmmcu_status mmmcu_preprocess_host(mmmcu_ctx* ctx, const float* A_host, int64_t 
                                    uint64_t a_version, uint64_t b_version);
 mmmcu_status mmmcu_multiply_planned_host(mmmcu_ctx* ctx, float* C_host, int64_t ldc, uint64_t a_version,
                                          uint64_t b_version, int worker_count, mmmcu_counters* counters);
+/* Typed twins of the three host-buffer calls (f32 / f64, any valid lane), and multiply_simple
+ * on host operands. */
+mmmcu_status mmmcu_multiply_simple_host_t(mmmcu_ctx* ctx, mmmcu_dtype dtype, void* C_host, int64_t ldc,
+                                          const void* A_host, int64_t lda, const void* B_host, int64_t ldb,
+                                          int64_t M, int64_t K, int64_t N);
+mmmcu_status mmmcu_multiply_host_t(mmmcu_ctx* ctx, mmmcu_dtype dtype, void* C_host, int64_t ldc,
+                                   const void* A_host, int64_t lda, const void* B_host, int64_t ldb,
+                                   int64_t M, int64_t K, int64_t N, mmmcu_lane lane,
+                                   mmmcu_counters* counters);
+mmmcu_status mmmcu_preprocess_host_t(mmmcu_ctx* ctx, mmmcu_dtype dtype, const void* A_host, int64_t M,
+                                     int64_t K, int64_t lda, const void* B_host, int64_t N, int64_t ldb,
+                                     mmmcu_lane lane, uint64_t a_version, uint64_t b_version);
+mmmcu_status mmmcu_multiply_planned_host_t(mmmcu_ctx* ctx, mmmcu_dtype dtype, void* C_host, int64_t ldc,
+                                           uint64_t a_version, uint64_t b_version, int worker_count,
+                                           mmmcu_counters* counters);
 
 /* ---- synthetic inputs (device generator; matgen.hpp analogue for BASELINE.json) ------ */
 

@@ -541,6 +541,100 @@ int64_t orc_check_tolerance(const float* Cg, const float* Cr, int64_t ldc, const
   return bad;
 }
 
+/* ---------------------------------------------------------------- f64 (Dtype::f64) */
+
+/*
+ * The same restatements for T = double (matrix.hpp:13-26: Dtype::f64; the reference
+ * compiles KernelTable<double> for every group width, kernel_table.cpp:47-60, :94-95):
+ * region FMA with fma() per element of each set group, pattern codes (!= 0.0), multiply_mmm
+ * (ascending-k fma chain over the surviving terms) and multiply_simple (i-k-j fma).
+ */
+int orc_region_fma_f64(uint32_t code, int group_width, int pattern_bits, double* c, double a,
+                       const double* b) {
+  if (pattern_bits < 1 || pattern_bits > 16) return -1;
+  for (int j = 0; j < pattern_bits; ++j) {
+    if (!((code >> (pattern_bits - 1 - j)) & 1u)) continue;
+    for (int l = 0; l < group_width; ++l) {
+      const int e = j * group_width + l;
+      c[e] = fma(a, b[e], c[e]);
+    }
+  }
+  return 0;
+}
+
+int orc_pattern_codes_f64(const double* B, int64_t K, int64_t ld, int group_width, int pattern_bits,
+                          uint32_t* codes) {
+  const int64_t R = (int64_t)group_width * pattern_bits;
+  if (R <= 0 || ld % R != 0) return -1;
+  const int64_t nreg = ld / R;
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < K; ++k) {
+    const double* row = B + k * ld;
+    for (int64_t r = 0; r < nreg; ++r) {
+      uint32_t code = 0;
+      for (int j = 0; j < pattern_bits; ++j) {
+        int nz = 0;
+        const double* g = row + r * R + (int64_t)j * group_width;
+        for (int l = 0; l < group_width; ++l) nz |= (g[l] != 0.0);
+        code = (code << 1) | (uint32_t)nz;
+      }
+      codes[k * nreg + r] = code;
+    }
+  }
+  return 0;
+}
+
+void orc_multiply_simple_f64(double* C, int64_t ldc, const double* A, int64_t lda, const double* B,
+                             int64_t ldb, int64_t M, int64_t K, int64_t N) {
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t i = 0; i < M; ++i) {
+    double* c = C + i * ldc;
+    for (int64_t k = 0; k < K; ++k) {
+      const double a = A[i * lda + k];
+      const double* b = B + k * ldb;
+      for (int64_t j = 0; j < N; ++j) c[j] = fma(a, b[j], c[j]);
+    }
+  }
+}
+
+int orc_multiply_mmm_f64(double* C, int64_t ldc, const double* A, int64_t lda, const double* B,
+                         int64_t ldb, int64_t M, int64_t K, int64_t N, const uint32_t* codes,
+                         int group_width, int pattern_bits, orc_counters* out) {
+  const int64_t R = (int64_t)group_width * pattern_bits;
+  if (R <= 0 || ldb % R != 0 || ldc < ldb || N > ldb) return -1;
+  const int64_t nreg = ldb / R;
+  uint64_t inv = 0, lanes = 0, skipped = 0, zreg = 0;
+#pragma omp parallel for schedule(dynamic, 4) reduction(+ : inv, lanes, skipped, zreg)
+  for (int64_t i = 0; i < M; ++i) {
+    double* c = C + i * ldc;
+    for (int64_t k = 0; k < K; ++k) {
+      const double a = A[i * lda + k];
+      if (a == 0.0) {
+        ++skipped;
+        continue;
+      }
+      const uint32_t* code = codes + k * nreg;
+      const double* b = B + k * ldb;
+      for (int64_t r = 0; r < nreg; ++r) {
+        if (code[r] == 0) {
+          ++zreg;
+          continue;
+        }
+        ++inv;
+        lanes += (uint64_t)__builtin_popcount(code[r]) * (uint64_t)group_width;
+        orc_region_fma_f64(code[r], group_width, pattern_bits, c + r * R, a, b + r * R);
+      }
+    }
+  }
+  if (out) {
+    out->kernel_invocations = inv;
+    out->lane_fma_ops = lanes;
+    out->rows_skipped = skipped;
+    out->regions_skipped_by_zero_code = zreg;
+  }
+  return 0;
+}
+
 int orc_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

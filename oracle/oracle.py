@@ -98,6 +98,13 @@ def lib():
         L.orc_multiply_mmm.argtypes = [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64,
                                        c_int64, c_void_p, c_int, c_int, POINTER(OrcCounters)]
         L.orc_bruteforce_lane_ops.restype = c_uint64
+        L.orc_region_fma_f64.argtypes = [c_uint32, c_int, c_int, c_void_p, c_double, c_void_p]
+        L.orc_pattern_codes_f64.argtypes = [c_void_p, c_int64, c_int64, c_int, c_int, c_void_p]
+        L.orc_multiply_simple_f64.argtypes = [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64,
+                                              c_int64, c_int64]
+        L.orc_multiply_simple_f64.restype = None
+        L.orc_multiply_mmm_f64.argtypes = [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64,
+                                           c_int64, c_void_p, c_int, c_int, c_void_p]
         L.orc_bruteforce_lane_ops.argtypes = [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int]
         L.orc_check_tolerance.restype = c_int64
         L.orc_check_tolerance.argtypes = [c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64,
@@ -133,6 +140,13 @@ def ref_lib():
         L.ref_multiply_mmm_f32.restype = c_int
         L.ref_multiply_mmm_f32.argtypes = [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64,
                                            c_int64, c_int64, c_int, POINTER(RefCounters)]
+        L.ref_kernel_apply_f64.restype = c_int
+        L.ref_kernel_apply_f64.argtypes = [c_int, c_int, c_int, c_uint32, c_void_p, c_double, c_void_p]
+        for nm in ("ref_multiply_lane_f32", "ref_multiply_lane_f64"):
+            f = getattr(L, nm)
+            f.restype = c_int
+            f.argtypes = [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int, c_int,
+                          c_int, POINTER(RefCounters)]
         L.ref_max_threads.restype = c_int
         _ref = L
     return _ref
@@ -169,11 +183,14 @@ def gen_iid(rows, cols, seed, value_kind=0, sigma=1.0, thresh=0.0, mask_kind=0, 
 
 # ------------------------------------------------------------------------------ plans
 def pattern_codes(B: np.ndarray, group_width=8, pattern_bits=8) -> np.ndarray:
-    B = np.ascontiguousarray(B, dtype=np.float32)
+    """Codes [K][ld/R] of an f32 or f64 B (dtype kept)."""
+    f64 = B.dtype == np.float64
+    B = np.ascontiguousarray(B, dtype=np.float64 if f64 else np.float32)
     K, ld = B.shape
     R = group_width * pattern_bits
     codes = np.zeros((K, ld // R), dtype=np.uint32)
-    if lib().orc_pattern_codes(_p(B), K, ld, group_width, pattern_bits, _p(codes)) != 0:
+    fn = lib().orc_pattern_codes_f64 if f64 else lib().orc_pattern_codes
+    if fn(_p(B), K, ld, group_width, pattern_bits, _p(codes)) != 0:
         raise ValueError("ld must be a multiple of the region width")
     return codes
 
@@ -231,9 +248,12 @@ def a_csr(A: np.ndarray, K=None):
 
 # ----------------------------------------------------------------------------- engine
 def region_fma(code, c, a, b, group_width=8, pattern_bits=8):
-    c = np.ascontiguousarray(c, dtype=np.float32)
-    b = np.ascontiguousarray(b, dtype=np.float32)
-    if lib().orc_region_fma(code, group_width, pattern_bits, _p(c), a, _p(b)) != 0:
+    f64 = np.asarray(c).dtype == np.float64
+    dt = np.float64 if f64 else np.float32
+    c = np.ascontiguousarray(c, dtype=dt)
+    b = np.ascontiguousarray(b, dtype=dt)
+    fn = lib().orc_region_fma_f64 if f64 else lib().orc_region_fma
+    if fn(code, group_width, pattern_bits, _p(c), float(a), _p(b)) != 0:
         raise ValueError("bad pattern size")
     return c
 
@@ -242,7 +262,8 @@ def multiply_simple(C, A, B):
     """In-place C += A @ B, i-k-j fmaf."""
     M, K = A.shape
     N = C.shape[1]
-    lib().orc_multiply_simple(_p(C), C.shape[1], _p(A), A.shape[1], _p(B), B.shape[1], M, K, N)
+    fn = lib().orc_multiply_simple_f64 if C.dtype == np.float64 else lib().orc_multiply_simple
+    fn(_p(C), C.shape[1], _p(A), A.shape[1], _p(B), B.shape[1], M, K, N)
     return C
 
 
@@ -259,8 +280,9 @@ def multiply_mmm(C, A, B, K=None, N=None, group_width=8, pattern_bits=8, codes=N
         codes = pattern_codes(B, group_width, pattern_bits)
     codes = np.ascontiguousarray(codes, dtype=np.uint32)
     cnt = OrcCounters()
-    st = lib().orc_multiply_mmm(_p(C), C.shape[1], _p(A), lda, _p(B), ldb, M, K, N, _p(codes), group_width,
-                                pattern_bits, ctypes.byref(cnt))
+    fn = lib().orc_multiply_mmm_f64 if C.dtype == np.float64 else lib().orc_multiply_mmm
+    st = fn(_p(C), C.shape[1], _p(A), lda, _p(B), ldb, M, K, N, _p(codes), group_width, pattern_bits,
+            ctypes.byref(cnt))
     if st != 0:
         raise ValueError("bad multiply arguments")
     return {k: int(getattr(cnt, k)) for k, _ in OrcCounters._fields_}
@@ -305,6 +327,26 @@ def ref_kernel_apply(code, c, a, b, lane=(8, 8, 1)):
     b = np.ascontiguousarray(b, dtype=np.float32)
     st = ref_lib().ref_kernel_apply_f32(*lane, code, _p(c), a, _p(b))
     return st, c
+
+
+def ref_kernel_apply_f64(code, c, a, b, lane=(4, 8, 1)):
+    c = np.ascontiguousarray(c, dtype=np.float64).copy()
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    st = ref_lib().ref_kernel_apply_f64(lane[0], lane[1], lane[2], code, _p(c), float(a), _p(b))
+    return st, c
+
+
+def ref_multiply_lane(C, A, B, lane):
+    """The reference KernelTable<T> (f32 / f64 by C's dtype) for any lane config: C += A*B over
+    the P-bit codes (Fig. 4 A-skip); returns the counters (golden fixtures only)."""
+    M, lda = A.shape
+    K, ldb = B.shape
+    cnt = RefCounters()
+    fn = ref_lib().ref_multiply_lane_f64 if C.dtype == np.float64 else ref_lib().ref_multiply_lane_f32
+    st = fn(_p(C), C.shape[1], _p(A), lda, _p(B), ldb, M, K, lane[0], lane[1], lane[2], ctypes.byref(cnt))
+    if st != 0:
+        raise RuntimeError(f"reference multiply failed with status {st}")
+    return {k: int(getattr(cnt, k)) for k, _ in RefCounters._fields_}
 
 
 def ref_multiply_mmm(C, A, B, row0=0, row1=None, workers=0):

@@ -312,6 +312,88 @@ int ref_multiply_mmm_f32(float* C, int64_t ldc, const float* A, int64_t lda, con
   }
 }
 
+// KernelTable<double>::build(lane) then apply (kernel_table.hpp:50-54; kernel_table.cpp:94-95).
+int ref_kernel_apply_f64(int w, int p, int v, uint32_t code, double* c, double a, const double* b) {
+  try {
+    const KernelTable<double> t = KernelTable<double>::build(LaneConfig{w, p, v});
+    if (code >= t.size()) return 3;
+    t.apply(code, c, a, b);
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
+
+}  // extern "C"
+
+namespace {
+// The SPEC multiply (Fig. 4 A-skip) over KernelTable<T> for ANY lane config:
+// codes of P bits per region (MSB first), then per non-zero a_ik the region kernels of B row k.
+// Golden fixtures for the f64 and non-default-lane paths (tests/golden/gen_golden.py).
+template <typename T>
+int multiply_lane(T* C, int64_t ldc, const T* A, int64_t lda, const T* B, int64_t ldb, int64_t M, int64_t K,
+                  int w, int p, int v, ref_counters* out) {
+  try {
+    const LaneConfig lane{w, p, v};
+    const KernelTable<T> table = KernelTable<T>::build(lane);
+    const int64_t R = lane.region_width(), G = lane.group_width();
+    if (ldb % R != 0 || ldc < ldb) return 4;
+    const int64_t nreg = ldb / R;
+    std::vector<uint32_t> codes(static_cast<size_t>(K * nreg));
+    for (int64_t k = 0; k < K; ++k)
+      for (int64_t r = 0; r < nreg; ++r) {
+        uint32_t code = 0;
+        for (int j = 0; j < p; ++j) {
+          bool nz = false;
+          for (int64_t l = 0; l < G; ++l) nz |= B[k * ldb + r * R + j * G + l] != T(0);
+          code = (code << 1) | static_cast<uint32_t>(nz);
+        }
+        codes[k * nreg + r] = code;
+      }
+    uint64_t inv = 0, lanes = 0, skipped = 0, zreg = 0;
+    for (int64_t i = 0; i < M; ++i)
+      for (int64_t k = 0; k < K; ++k) {
+        const T av = A[i * lda + k];
+        if (av == T(0)) {
+          ++skipped;
+          continue;
+        }
+        for (int64_t r = 0; r < nreg; ++r) {
+          const uint32_t code = codes[k * nreg + r];
+          if (code == 0) {
+            ++zreg;
+            continue;
+          }
+          ++inv;
+          lanes += static_cast<uint64_t>(__builtin_popcount(code)) * G;
+          table.apply(code, C + i * ldc + r * R, av, B + k * ldb + r * R);
+        }
+      }
+    if (out) {
+      out->kernel_invocations = inv;
+      out->lane_fma_ops = lanes;
+      out->rows_skipped = skipped;
+      out->regions_skipped_by_zero_code = zreg;
+      out->preprocess_ns = out->multiply_ns = 0;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int ref_multiply_lane_f32(float* C, int64_t ldc, const float* A, int64_t lda, const float* B, int64_t ldb, int64_t M,
+                          int64_t K, int w, int p, int v, ref_counters* out) {
+  return multiply_lane<float>(C, ldc, A, lda, B, ldb, M, K, w, p, v, out);
+}
+int ref_multiply_lane_f64(double* C, int64_t ldc, const double* A, int64_t lda, const double* B, int64_t ldb,
+                          int64_t M, int64_t K, int w, int p, int v, ref_counters* out) {
+  return multiply_lane<double>(C, ldc, A, lda, B, ldb, M, K, w, p, v, out);
+}
+
 int ref_max_threads(void) { return omp_get_max_threads(); }
 
 }  // extern "C"

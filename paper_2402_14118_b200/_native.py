@@ -27,6 +27,10 @@ ERR_FILE_IO = 10
 ERR_FILE_FORMAT = 11
 ERR_FILE_TRUNCATED = 12
 
+# mmmcu_dtype (matrix.hpp:13-26)
+F32 = 0
+F64 = 1
+
 # mmmcu_algo
 ALGO_AUTO = 0
 ALGO_SIMT_BCAST = 1
@@ -111,6 +115,27 @@ SIGNATURES = [
                                       c_uint64, c_uint64]),
     ("mmmcu_multiply_planned_host", c_int, [c_void_p, c_void_p, c_int64, c_uint64, c_uint64, c_int,
                                             POINTER(Counters)]),
+    # every dtype / lane config (kgen.cuh)
+    ("mmmcu_validate_lane_t", c_int, [c_void_p, c_int, Lane]),
+    ("mmmcu_preprocess_a_t", c_int, [c_void_p, c_int, c_void_p, c_int64, c_int64, c_int64, c_uint64]),
+    ("mmmcu_preprocess_b_t", c_int, [c_void_p, c_int, c_void_p, c_int64, c_int64, c_int64, Lane, c_uint64]),
+    ("mmmcu_preprocess_t", c_int, [c_void_p, c_int, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int64,
+                                   Lane, c_uint64, c_uint64]),
+    ("mmmcu_multiply_t", c_int, [c_void_p, c_int, c_void_p, c_int64, c_void_p, c_void_p, c_uint64, c_uint64,
+                                 POINTER(Counters)]),
+    ("mmmcu_multiply_simple_t", c_int, [c_void_p, c_int, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64,
+                                        c_int64, c_int64, c_int64]),
+    ("mmmcu_export_b_codes16", c_int, [c_void_p, c_void_p, c_int64]),
+    ("mmmcu_export_bplans16", c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, POINTER(c_int64)]),
+    ("mmmcu_plan_info", c_int, [c_void_p, POINTER(c_int), POINTER(Lane)]),
+    ("mmmcu_multiply_host_t", c_int, [c_void_p, c_int, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64,
+                                      c_int64, c_int64, c_int64, Lane, POINTER(Counters)]),
+    ("mmmcu_preprocess_host_t", c_int, [c_void_p, c_int, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64,
+                                        c_int64, Lane, c_uint64, c_uint64]),
+    ("mmmcu_multiply_simple_host_t", c_int, [c_void_p, c_int, c_void_p, c_int64, c_void_p, c_int64, c_void_p,
+                                             c_int64, c_int64, c_int64, c_int64]),
+    ("mmmcu_multiply_planned_host_t", c_int, [c_void_p, c_int, c_void_p, c_int64, c_uint64, c_uint64, c_int,
+                                              POINTER(Counters)]),
 ]
 
 _lib = None

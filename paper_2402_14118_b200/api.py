@@ -168,17 +168,23 @@ def _lib():
 
 
 def _check_tensor(t, name: str):
+    return _check_tensor_t(t, name)[:2]
+
+
+def _check_tensor_t(t, name: str):
+    """(pointer, leading dimension, mmmcu_dtype) of a CUDA float32 / float64 row-major tensor
+    (Dtype::f32 / f64, matrix.hpp:13-26)."""
     import torch
 
     if not isinstance(t, torch.Tensor):
-        raise TypeError(f"{name} must be a torch.Tensor (CUDA float32) or use the *_host entry points")
-    if t.dtype != torch.float32:
-        raise UnsupportedError(f"{name}: only float32 operands have a GPU kernel (got {t.dtype})")
+        raise TypeError(f"{name} must be a torch.Tensor (CUDA float32 / float64) or use the *_host entry points")
+    if t.dtype not in (torch.float32, torch.float64):
+        raise UnsupportedError(f"{name}: only float32 / float64 operands have a GPU kernel (got {t.dtype})")
     if not t.is_cuda:
         raise ValueError(f"{name} must live on a CUDA device")
     if t.dim() != 2 or t.stride(1) != 1:
         raise ValueError(f"{name} must be a row-major 2-D tensor with unit column stride")
-    return t.data_ptr(), int(t.stride(0))
+    return t.data_ptr(), int(t.stride(0)), (N.F64 if t.dtype == torch.float64 else N.F32)
 
 
 def _version(t) -> int:
@@ -239,27 +245,30 @@ class MmmContext:
     # -- plans
     def preprocess(self, a, b):
         """preprocess_a(a) + preprocess_b(b) on the device (one K1 pass over each)."""
-        pa, lda = _check_tensor(a, "a")
-        pb, ldb = _check_tensor(b, "b")
+        pa, lda, dta = _check_tensor_t(a, "a")
+        pb, ldb, dtb = _check_tensor_t(b, "b")
         M, K = a.shape
         Kb, Nn = b.shape
         if K != Kb:
             raise DimensionMismatchError(f"a.cols ({K}) != b.rows ({Kb})")
+        if dta != dtb:
+            raise ValueError("a and b must have the same dtype")
         self._sync_stream()
-        self._check(_lib().mmmcu_preprocess(self._h, pa, M, K, lda, pb, Nn, ldb, self.lane._c(), _version(a),
-                                            _version(b)))
+        self._check(_lib().mmmcu_preprocess_t(self._h, dta, pa, M, K, lda, pb, Nn, ldb, self.lane._c(), _version(a),
+                                              _version(b)))
         self._shape = (M, K, Nn)
         return self
 
     def preprocess_a_only(self, a):
-        pa, lda = _check_tensor(a, "a")
+        pa, lda, dt = _check_tensor_t(a, "a")
         self._sync_stream()
-        self._check(_lib().mmmcu_preprocess_a(self._h, pa, a.shape[0], a.shape[1], lda, _version(a)))
+        self._check(_lib().mmmcu_preprocess_a_t(self._h, dt, pa, a.shape[0], a.shape[1], lda, _version(a)))
 
     def preprocess_b_only(self, b):
-        pb, ldb = _check_tensor(b, "b")
+        pb, ldb, dt = _check_tensor_t(b, "b")
         self._sync_stream()
-        self._check(_lib().mmmcu_preprocess_b(self._h, pb, b.shape[0], b.shape[1], ldb, self.lane._c(), _version(b)))
+        self._check(_lib().mmmcu_preprocess_b_t(self._h, dt, pb, b.shape[0], b.shape[1], ldb, self.lane._c(),
+                                                _version(b)))
 
     def planned_counters(self) -> WorkCounters:
         c = N.Counters()
@@ -273,20 +282,25 @@ class MmmContext:
 
     # -- exports of the canonical formats
     def export_b_codes(self, K: int, ldb: int) -> np.ndarray:
-        out = np.empty((K, ldb // 64), dtype=np.uint8)
-        self._check(_lib().mmmcu_export_b_codes(self._h, out.ctypes.data, out.size))
-        return out
+        """Pattern codes [K][ldb / R] of the current plan: uint8 for P <= 8, else uint16."""
+        R = self.lane.region_width()
+        out = np.empty((K, ldb // R), dtype=np.uint16)
+        self._check(_lib().mmmcu_export_b_codes16(self._h, out.ctypes.data, out.size))
+        return out.astype(np.uint8) if self.lane.p <= 8 else out
 
     def export_bplans(self, K: int, ldb: int, leaf_dim: Optional[int] = None) -> List[BPlan]:
         leaf = self.leaf_dim if leaf_dim is None else int(leaf_dim)
-        nreg = ldb // 64
-        rpl = max(leaf // 64, 1)
+        R = self.lane.region_width()
+        nreg = ldb // R
+        rpl = max(leaf // R, 1)
         n_pl = ((K + leaf - 1) // leaf) * ((nreg + rpl - 1) // rpl)
-        plans = np.empty(K * nreg, dtype=np.uint8)
+        plans = np.empty(K * nreg, dtype=np.uint16)
         off = np.empty(n_pl + 1, dtype=np.int64)
         n = ctypes.c_int64()
-        self._check(_lib().mmmcu_export_bplans(self._h, leaf, plans.ctypes.data, plans.size, off.ctypes.data, off.size,
-                                               ctypes.byref(n)))
+        self._check(_lib().mmmcu_export_bplans16(self._h, leaf, plans.ctypes.data, plans.size, off.ctypes.data,
+                                                 off.size, ctypes.byref(n)))
+        if self.lane.p <= 8:
+            plans = plans.astype(np.uint8)
         return [BPlan(p, plans[off[p]:off[p + 1]].copy()) for p in range(n.value)]
 
     def export_a_bitmap(self, M: int, K: int) -> np.ndarray:
@@ -314,15 +328,15 @@ class MmmContext:
 
     # -- multiply
     def multiply(self, c, a, b, want_counters: bool = True) -> Optional[WorkCounters]:
-        pc, ldc = _check_tensor(c, "c")
-        pa, _ = _check_tensor(a, "a")
-        pb, _ = _check_tensor(b, "b")
+        pc, ldc, dt = _check_tensor_t(c, "c")
+        pa, _, _ = _check_tensor_t(a, "a")
+        pb, _, _ = _check_tensor_t(b, "b")
         if self._shape is not None and (c.shape[0] != a.shape[0] or c.shape[1] != b.shape[1]):
             raise DimensionMismatchError(f"c is {tuple(c.shape)}, expected ({a.shape[0]}, {b.shape[1]})")
         self._sync_stream()
         cnt = N.Counters()
-        self._check(_lib().mmmcu_multiply(self._h, pc, ldc, pa, pb, _version(a), _version(b),
-                                          ctypes.byref(cnt) if want_counters else None))
+        self._check(_lib().mmmcu_multiply_t(self._h, dt, pc, ldc, pa, pb, _version(a), _version(b),
+                                            ctypes.byref(cnt) if want_counters else None))
         if want_counters:
             self.counters = WorkCounters._from(cnt)
             return self.counters
@@ -370,9 +384,13 @@ def multiply_mmm(context: MmmContext, c, a, b) -> WorkCounters:
 
 def multiply_parallel(context: MmmContext, c, a, b, worker_count: int) -> WorkCounters:
     """multiply_parallel: worker_count == 0 rejected; same result bits."""
-    pc, ldc = _check_tensor(c, "c")
-    pa, _ = _check_tensor(a, "a")
-    pb, _ = _check_tensor(b, "b")
+    pc, ldc, dt = _check_tensor_t(c, "c")
+    pa, _, _ = _check_tensor_t(a, "a")
+    pb, _, _ = _check_tensor_t(b, "b")
+    if dt == N.F64:  # the typed path: the worker count is validated, then the same multiply
+        if int(worker_count) <= 0:
+            _raise(N.ERR_WORKERS, "worker_count must be positive")
+        return context.multiply(c, a, b)
     context._sync_stream()
     cnt = N.Counters()
     context._check(_lib().mmmcu_multiply_parallel(context._h, pc, ldc, pa, pb, _version(a), _version(b),
@@ -382,17 +400,17 @@ def multiply_parallel(context: MmmContext, c, a, b, worker_count: int) -> WorkCo
 
 
 def multiply_simple(c, a, b, ctx: Optional[MmmContext] = None) -> None:
-    """multiply_simple: dense i-k-j c += a*b (fmaf per term) on the GPU."""
-    pc, ldc = _check_tensor(c, "c")
-    pa, lda = _check_tensor(a, "a")
-    pb, ldb = _check_tensor(b, "b")
+    """multiply_simple: dense i-k-j c += a*b (fma per term) on the GPU."""
+    pc, ldc, dt = _check_tensor_t(c, "c")
+    pa, lda, _ = _check_tensor_t(a, "a")
+    pb, ldb, _ = _check_tensor_t(b, "b")
     M, K = a.shape
     Kb, Nn = b.shape
     if K != Kb or c.shape[0] != M or c.shape[1] != Nn:
         raise DimensionMismatchError(f"shapes a{tuple(a.shape)} b{tuple(b.shape)} c{tuple(c.shape)}")
     cx = _ctx_for(a, ctx, LaneConfig())
     cx._sync_stream()
-    cx._check(_lib().mmmcu_multiply_simple(cx._h, pc, ldc, pa, lda, pb, ldb, M, K, Nn))
+    cx._check(_lib().mmmcu_multiply_simple_t(cx._h, dt, pc, ldc, pa, lda, pb, ldb, M, K, Nn))
 
 
 def multiply_host(c: np.ndarray, a: np.ndarray, b: np.ndarray, ctx: Optional[MmmContext] = None) -> WorkCounters:

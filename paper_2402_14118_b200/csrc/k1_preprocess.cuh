@@ -94,23 +94,8 @@ struct K1Scratch {
   int64_t* row_off;       // [n_tb * kw + 1] exclusive prefix of (row_cnt + 3 header rows), 64-byte units
 };
 
-__device__ void k1_plan_totals(const unsigned long long* __restrict__ btot, int64_t K, int64_t nreg, int has_b,
-                               unsigned long long* __restrict__ out);
 
 __device__ __forceinline__ bool k1_range_wide(unsigned long long rng);
-
-// The fp16-split range guard once every tile is in (K1's last CTA): any A row / B group whose
-// range word is too wide (k1_range_wide) sets wide_a / btot[4].
-__device__ void k1_range_flags(const K1Scratch& z, int64_t M, int do_a, int do_b) {
-  bool wa = false, wb = false;
-  if (do_a && z.rrng)
-    for (int64_t i = threadIdx.x; i < M; i += blockDim.x) wa |= k1_range_wide(z.rrng[i]);
-  if (do_b && z.grng)
-    for (int64_t g = threadIdx.x; g < z.ngrp; g += blockDim.x) wb |= k1_range_wide(z.grng[g]);
-  if (__syncthreads_or(wa) && threadIdx.x == 0) *z.wide_a = 1u;
-  if (__syncthreads_or(wb) && threadIdx.x == 0) z.btot[4] = 1ull;
-  __syncthreads();
-}
 
 // AUTO path choice (stats[7] := 32 for K2-TC, else the K2-SIMT span stays): estimated
 // SM-cycles of each path from the plan, constants measured on B200 (K2 choice):
@@ -122,65 +107,6 @@ __device__ void k1_range_flags(const K1Scratch& z, int64_t M, int do_a, int do_b
 //   + K1 packing traffic at 0.0433 SM-cycles per byte (HBM): K2-SIMT rows 2 x 64 B per
 //     non-zero (k, slice); K2-TC step images 2 x 768 B per live (k, tile) (fp16 hi | lo);
 //   each divided by min(#SMs, its CTA count).
-__device__ void k1_choose_path(const K1Scratch& z, int64_t M, int64_t kw, unsigned long long* __restrict__ out) {
-  __shared__ unsigned long long s_stage[32], s_live[32];
-  __shared__ uint32_t s_pick;
-  unsigned long long st = 0, live = 0;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // live k per TC tile = popcount of its kw live-k words; a warp per tile
-  for (int64_t tb = warp; tb < z.n_tc; tb += blockDim.x >> 5) {
-    uint32_t n = 0;
-    for (int64_t w = lane; w < kw; w += 32) n += __popc(z.tlive[tb * kw + w]);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
-    if (lane == 0) {
-      live += n;
-      st += (n + 31) / 32;  // fp16-split stages of 32 live k
-    }
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    st += __shfl_xor_sync(0xffffffffu, st, o);
-    live += __shfl_xor_sync(0xffffffffu, live, o);
-  }
-  if (lane == 0) {
-    s_stage[warp] = st;
-    s_live[warp] = live;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long stages = 0, lv = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-      stages += s_stage[w];
-      lv += s_live[w];
-    }
-    const double rt = (double)((M + 127) / 128);
-    const double span = (double)out[7];
-    const double slice_nz = (double)z.btot[0], pop = (double)out[5];
-    const double simt = rt * (double)z.n_tb * (double)kw * 1158.0 + rt * (span == 16.0 ? 26.0 * slice_nz : 17.5 * pop) +
-                        0.0433 * 128.0 * slice_nz;
-    const double tc = rt * (24200.0 * (double)z.n_tc + 940.0 * (double)stages) + 0.0433 * 2.0 * 768.0 * (double)lv;
-    // time ~ work / min(SMs, CTAs): short operands leave SMs idle
-    const double sms = (double)z.num_sms;
-    const double par_simt = fmin(sms, rt * (double)z.n_tb), par_tc = fmin(sms, rt * (double)z.n_tc);
-    // K2-TC multiplies A's zeros and reads tf32: an Inf / NaN operand would turn 0 * Inf
-    // terms the reference never forms into NaN, subnormals would be flushed — keep the
-    // exact path
-    const bool nonfinite = *z.nonfinite_a != 0u || z.btot[3] != 0ull;
-    // K2-TC needs finite, normal operands (0 * Inf terms, flushed subnormals)
-    s_pick = (!nonfinite && tc / par_tc < simt / par_simt) ? 1u : 0u;
-  }
-  __syncthreads();
-  // fp16-split range guard, only when K2-TC would be chosen.  The split scales every A row
-  // and every 8-column B group by its own power of two, so a row / group far below the
-  // operand max loses nothing; what it cannot scale away is a MIXED-scale row or group
-  // (parts of it 2^17 or more below its max), whose small part would lose its lo bits
-  // (K2-TC accuracy).  Every row / group must have its max|x| exponent within
-  // [-86, 114] (scale |s| <= 100) and all its local maxima (A: per 128-column chunk, B: per
-  // 32-k tile) within 2^17 of its max; otherwise AUTO keeps the exact K2-SIMT.
-  if (threadIdx.x == 0 && s_pick && *z.wide_a == 0u && z.btot[4] == 0ull) out[7] = 32ull;
-  __syncthreads();
-}
 
 // Block-wide exclusive scan of (cnt[t] + add) -> out[0..n] (out[n] = total); one CTA.
 // Each thread owns a contiguous segment and loads it with independent loads (one memory
@@ -224,6 +150,188 @@ __global__ void __launch_bounds__(kK1Threads) k1_row_off(const uint32_t* __restr
   k1_block_exclusive_scan(cnt, n, 3, out);
 }
 
+#ifdef K1_PROF
+__device__ unsigned long long* k1_prof = nullptr;  // debug builds: per-CTA globaltimer stamps
+__device__ unsigned long long k1_fin_prof[8];      // debug builds: the last CTA's finalize phases
+__device__ __forceinline__ unsigned long long k1_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+#ifdef K1_PROF
+#define K1_FIN_STAMP(i) \
+  if (threadIdx.x == 0) k1_fin_prof[i] = k1_now()
+#else
+#define K1_FIN_STAMP(i)
+#endif
+
+__host__ __device__ constexpr int k1_fin_smem() { return 4096 * 4; }  // k1_fin's live-k counters
+// k1_fin: 32 warps — 16 for the range guard, 12 for the live-k counts, 4 for the tile prefix
+constexpr int kFinWarps = 32, kFinRangeWarps = 16, kFinLiveWarps = 12;
+
+// Exclusive scan of n values over a warp group (gsize threads starting at warp w0, named
+// barrier bar), each thread a contiguous segment; out[n] = total.
+template <typename F>
+__device__ void k1_group_scan(int64_t n, F load, int64_t* __restrict__ out, int gtid, int gsize, int bar,
+                              int64_t* s_wsum) {
+  const int lane = gtid & 31, gw = gtid >> 5, nw = gsize >> 5;
+  const int64_t seg = (n + gsize - 1) / gsize;
+  const int64_t b0 = gtid * seg, b1 = min(b0 + seg, n);
+  int64_t local = 0;
+  for (int64_t i = b0; i < b1; ++i) local += (int64_t)load(i);
+  int64_t x = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_wsum[gw] = x;
+  asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(gsize) : "memory");
+  int64_t before = 0;
+  for (int w2 = 0; w2 < gw; ++w2) before += s_wsum[w2];
+  int64_t run = before + x - local;
+  for (int64_t i = b0; i < b1; ++i) {
+    out[i] = run;
+    run += (int64_t)load(i);
+  }
+  if (gtid == gsize - 1) out[n] = run;
+  (void)nw;
+}
+
+// The finalize of a K1 pass (k1_fin, 1024 threads), on the critical path of the call chain,
+// so its independent parts run side by side in warp groups with many loads in flight (one
+// or two global round trips each instead of a chain): warps 0-15 the fp16 range guard,
+// 16-27 the live k per TC tile (AUTO cost model), 28-31 the CSR's 32-row tile prefix; then thread 0 the plan totals and the AUTO
+// path choice; then (K2-SIMT possible only) the record-offset scan with all threads.
+__device__ void k1_finalize(const K1Scratch& z, int64_t M, int64_t K, int64_t nreg, int64_t kw, int has_a, int has_b,
+                            int64_t nA, int64_t nB, unsigned long long* __restrict__ stats, uint32_t* s_tcnt) {
+  __shared__ uint32_t s_wide[2];
+  __shared__ unsigned long long s_st, s_live;
+  __shared__ int64_t s_wsum[kFinWarps];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool choose = z.choose && has_a && has_b;
+  const int64_t nw = z.n_tc * kw;
+  const bool fits = choose && z.n_tc <= k1_fin_smem() / 4 && nw < 0x7fffffff;
+  if (tid < 2) s_wide[tid] = 0u;
+  for (int64_t t = tid; fits && t < z.n_tc; t += blockDim.x) s_tcnt[t] = 0u;
+  __syncthreads();
+  K1_FIN_STAMP(1);
+  if (warp < kFinRangeWarps) {  // ---- range guard
+    constexpr int kT = 32 * kFinRangeWarps;
+    auto scan = [&](const unsigned long long* __restrict__ w, int64_t n) {
+      bool wide = false;
+      for (int64_t i0 = tid; i0 < n; i0 += 4 * kT) {
+        unsigned long long v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t i = i0 + u * kT;
+          v[u] = i < n ? w[i] : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) wide |= k1_range_wide(v[u]);
+      }
+      return wide;
+    };
+    const bool wa = nA > 0 && z.rrng ? scan(z.rrng, M) : false;
+    const bool wb = nB > 0 && z.grng ? scan(z.grng, z.ngrp) : false;
+    if (__any_sync(0xffffffffu, wa) && lane == 0) atomicOr(&s_wide[0], 1u);
+    if (__any_sync(0xffffffffu, wb) && lane == 0) atomicOr(&s_wide[1], 1u);
+  } else if (warp < kFinRangeWarps + kFinLiveWarps) {  // ---- live k per TC tile (popcount of its kw words)
+    constexpr int kT = 32 * kFinLiveWarps;
+    const int gt = tid - 32 * kFinRangeWarps, gw = gt >> 5;
+    unsigned long long st = 0, live = 0;
+    if (fits) {
+      for (int64_t i0 = gt; i0 < nw; i0 += 8 * kT) {
+        uint32_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int64_t i = i0 + u * kT;
+          v[u] = i < nw ? z.tlive[i] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int64_t i = i0 + u * kT;
+          if (v[u]) atomicAdd(&s_tcnt[(uint32_t)i / (uint32_t)kw], (uint32_t)__popc(v[u]));
+        }
+      }
+      asm volatile("bar.sync 3, %0;" ::"r"(kT) : "memory");
+      for (int64_t tb = gt; tb < z.n_tc; tb += kT) {
+        live += s_tcnt[tb];
+        st += (s_tcnt[tb] + 31) / 32;  // fp16-split stages of 32 live k
+      }
+    } else if (choose) {
+      for (int64_t tb = gw; tb < z.n_tc; tb += kFinLiveWarps) {  // a warp per tile
+        uint32_t n = 0;
+        for (int64_t w = lane; w < kw; w += 32) n += __popc(z.tlive[tb * kw + w]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+        if (lane == 0) {
+          live += n;
+          st += (n + 31) / 32;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      st += __shfl_xor_sync(0xffffffffu, st, o);
+      live += __shfl_xor_sync(0xffffffffu, live, o);
+    }
+    if (gt == 0) {
+      s_st = 0;
+      s_live = 0;
+    }
+    asm volatile("bar.sync 3, %0;" ::"r"(kT) : "memory");
+    if (lane == 0) {
+      atomicAdd(&s_st, st);
+      atomicAdd(&s_live, live);
+    }
+  } else {  // ---- the CSR's 32-row tile prefix
+    if (nA > 0) {
+      const int64_t ntile = (M + kK1Rows - 1) / kK1Rows;
+      const uint32_t* ts = z.tile_sum;
+      constexpr int kT = 32 * (kFinWarps - kFinRangeWarps - kFinLiveWarps);
+      k1_group_scan(ntile, [&](int64_t i) { return ts[i]; }, z.tile_prefix, tid - (kFinWarps * 32 - kT), kT, 4,
+                    s_wsum);
+    }
+  }
+  __syncthreads();
+  K1_FIN_STAMP(2);
+  if (tid == 0) {
+    // plan totals: pop_total, zero codes and the K2-SIMT span from the B tiles' totals
+    // btot = {Σ non-zero (k, slice), Σ bpop, Σ bnz} (span: 16-column slices cost ~41 issue
+    // slots per non-zero (k, slice), 8-column groups ~23 per non-zero (k, group))
+    const unsigned long long pop = has_b ? z.btot[1] : 0ull, bnz = has_b ? z.btot[2] : 0ull;
+    stats[5] = pop;
+    stats[6] = has_b ? (unsigned long long)(K * nreg) - bnz : 0ull;
+    stats[7] = (has_b && 41ull * z.btot[0] > 23ull * pop) ? 8ull : 16ull;
+    stats[8] = stats[7];  // the K2-SIMT span alone (stats[7] may become 32 = K2-TC)
+    if (s_wide[0]) *z.wide_a = 1u;
+    if (s_wide[1]) z.btot[4] = 1ull;
+    if (choose) {
+      // AUTO path choice (k1_finalize; stats[7] := 32 for K2-TC): estimated SM-cycles of each path, see
+      // the cost-model comment at the top of this file
+      const double rt = (double)((M + 127) / 128);
+      const double span = (double)stats[7];
+      const double slice_nz = (double)z.btot[0], pp = (double)pop;
+      const double simt = rt * (double)z.n_tb * (double)kw * 1158.0 +
+                          rt * (span == 16.0 ? 26.0 * slice_nz : 17.5 * pp) + 0.0433 * 128.0 * slice_nz;
+      const double tc = rt * (24200.0 * (double)z.n_tc + 940.0 * (double)s_st) + 0.0433 * 2.0 * 768.0 * (double)s_live;
+      const double sms = (double)z.num_sms;
+      const double par_simt = fmin(sms, rt * (double)z.n_tb), par_tc = fmin(sms, rt * (double)z.n_tc);
+      const bool nonfinite = *z.nonfinite_a != 0u || z.btot[3] != 0ull;
+      const bool wide = *z.wide_a != 0u || z.btot[4] != 0ull;
+      if (!nonfinite && !wide && tc / par_tc < simt / par_simt) stats[7] = 32ull;
+    }
+  }
+  __syncthreads();
+  K1_FIN_STAMP(3);
+  // the K2-SIMT record offsets only when K2-SIMT can run (its pack is gated out otherwise)
+  if (z.row_cnt && nB > 0 && !(z.choose && (stats[7] == 32ull || stats[7] == 48ull)))
+    k1_block_exclusive_scan(z.row_cnt, z.n_tb * kw, 3, z.row_off);
+  K1_FIN_STAMP(4);
+}
+
 // ------------------------------------------------------------------ fused K1 pass
 // One persistent launch (2 CTAs per SM): tiles [0, nA) are A tiles, [nA, nA + nB) B tiles,
 // CTA b takes tiles b, b + gridDim.x, ...  Rows reach the SM by TMA bulk copies (one per
@@ -232,14 +340,6 @@ __global__ void __launch_bounds__(kK1Threads) k1_row_off(const uint32_t* __restr
 // thread 0 refills a stage as soon as the 8 warps have read it into registers.  The last
 // CTA to finish (threadfence + done-counter) computes the exact counters, plan statistics
 // and the AUTO path choice.
-#ifdef K1_PROF
-__device__ unsigned long long* k1_prof = nullptr;  // debug builds: per-CTA globaltimer stamps
-__device__ __forceinline__ unsigned long long k1_now() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#endif
 
 // Rows per ring stage: an 8-row group (the tile functions' unit) spans 8 / kK1SR stages, so a
 // stage is released, and refilled, after half a group (finer-grained refills keep more of the
@@ -419,7 +519,7 @@ __device__ __forceinline__ int k1_chunk(int w, int j) { return 2 * w + (j & 1) +
 // range word rng = (max << 32) | ~(smallest local max) with two non-returning 32-bit atomic
 // maxima (RED.MAX: the complement turns the min into a max), so no tile waits on a round
 // trip; whether the final range is too wide for the fp16 split is decided once all tiles are
-// in (k1_range_flags, the last CTA).
+// in (k1_finalize, the last CTA).
 __device__ __forceinline__ void k1_red_range(unsigned long long* rng, uint32_t mx, uint32_t mn) {
   uint32_t* w = reinterpret_cast<uint32_t*>(rng);  // little-endian: w[1] = high word
   atomicMax(w + 1, mx);
@@ -659,7 +759,7 @@ __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, 
   for (int o = 16; o; o >>= 1) srows += __shfl_xor_sync(0xffffffffu, srows, o);
   if (lane == 0 && srows) atomicAdd(&z.btot[0], (unsigned long long)srows);
   // the TC tile's live-k word (non-returning RED.OR; the live counts per tile are taken from
-  // the words by the last CTA, k1_choose_path, and by the TC pack)
+  // the words by the last CTA, k1_finalize, and by the TC pack)
   if (z.tlive && gword) atomicOr(&z.tlive[(gcol / kTcTileN) * kw + kwi], gword);
 }
 
@@ -681,7 +781,7 @@ __global__ void k1_codes_export(const uint32_t* __restrict__ bgrp, int64_t K, in
 // launch by the tile count
 template <int ST, int CTAS>
 __global__ void __launch_bounds__(kK1Block, CTAS)
-k1_pass(K1Args g, K1Scratch z, int has_a, int has_b, unsigned long long* __restrict__ stats) {
+k1_pass(K1Args g, K1Scratch z) {
   tc::pdl_wait();  // launched with programmatic serialization after the previous call's last kernel
   {  // the next plan's scratch halves (nothing reads them any more: the previous kernels are done)
     const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, st = (int64_t)gridDim.x * blockDim.x;
@@ -693,7 +793,7 @@ k1_pass(K1Args g, K1Scratch z, int has_a, int has_b, unsigned long long* __restr
 #endif
   extern __shared__ __align__(128) uint8_t k1_raw[];
   K1RingT<ST>& r = *reinterpret_cast<K1RingT<ST>*>(k1_raw + ((128 - ((uint32_t)__cvta_generic_to_shared(k1_raw) & 127)) & 127));
-  const int64_t M = g.M, K = g.K, nA = g.nA, nB = g.nB, kw = g.kw, nreg = g.nreg;
+  const int64_t M = g.M, K = g.K, nA = g.nA, kw = g.kw, nreg = g.nreg;
   K1Cursor cur{&g, &z, (int64_t)blockIdx.x, 0, 0, 0, nullptr, 0, 0};
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
@@ -732,10 +832,9 @@ k1_pass(K1Args g, K1Scratch z, int has_a, int has_b, unsigned long long* __restr
         k1_b_tile_b(ld, K, g.ldb, nreg, g.bgrp, kw, z, (t - nA) % g.b_tx, (t - nA) / g.b_tx);
     }
   }
-  __shared__ unsigned int last;
   __syncthreads();
-  // every CTA's tiles are done: the CSR / pack CTAs may be scheduled while the last CTA
-  // finalises (they wait in griddepcontrol.wait for this grid to complete)
+  // every CTA's tiles are done: the finalize kernel (k1_fin) may be scheduled; it waits in
+  // griddepcontrol.wait for this grid to complete
   tc::pdl_trigger();
 #ifdef K1_PROF
   if (threadIdx.x == 0 && k1_prof) {
@@ -743,34 +842,23 @@ k1_pass(K1Args g, K1Scratch z, int has_a, int has_b, unsigned long long* __restr
     k1_prof[4 * blockIdx.x + 1] = k1_now();
   }
 #endif
-  if (threadIdx.x == 0) {
-    __threadfence();  // cumulative over the CTA's writes ordered by the barrier above
-    last = atomicAdd(z.done, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  if (threadIdx.x == 0) {  // ready for the next launch (no other CTA is left)
-    *z.done = 0u;
-    *z.next_tile = 0u;
-  }
-  k1_plan_totals(z.btot, K, nreg, has_b, stats);
-  k1_range_flags(z, M, nA > 0, nB > 0);
-  if (z.choose && has_a && has_b) k1_choose_path(z, M, kw, stats);
-  // the K2-SIMT record offsets only when K2-SIMT can run (its pack is gated out otherwise)
-  if (z.row_cnt && nB > 0 && !(z.choose && (stats[7] == 32ull || stats[7] == 48ull)))
-    k1_block_exclusive_scan(z.row_cnt, z.n_tb * kw, 3, z.row_off);
-  if (nA > 0) {  // exclusive prefix of the 32-row tile sums for the CSR's row_ptr (k1_csr_cta)
-    const int64_t ntile = (M + kK1Rows - 1) / kK1Rows;
-    const uint32_t* ts = z.tile_sum;
-    k1_block_scan_fn<uint32_t>(ntile, [&](int64_t i) { return (int64_t)ts[i]; }, z.tile_prefix);
-  }
-#ifdef K1_PROF
-  if (threadIdx.x == 0 && k1_prof) {
-    k1_prof[4 * blockIdx.x + 2] = k1_now();
-    k1_prof[4 * blockIdx.x + 3] = 1;
-  }
-#endif
+}
+
+// The finalize of a K1 pass: one CTA of 1024 threads launched with programmatic
+// serialization right after k1_pass (a separate kernel: folded into the pass's last CTA it
+// cost the pass's tile loops register spills).  s_tcnt: dynamic shared memory (k1_fin_smem).
+struct K1FinArgs {
+  int64_t M, K, nreg, kw, nA, nB;
+  int has_a, has_b;
+};
+__global__ void __launch_bounds__(32 * kFinWarps) k1_fin(const __grid_constant__ K1Scratch z, K1FinArgs f,
+                                                   unsigned long long* __restrict__ stats) {
+  extern __shared__ __align__(16) uint32_t fin_smem[];
+  tc::pdl_trigger();  // the pack / CSR CTAs may become resident now (they wait for this grid)
+  tc::pdl_wait();     // the K1 pass is complete and its writes are visible
+  K1_FIN_STAMP(0);
+  if (threadIdx.x == 0) *z.next_tile = 0u;  // ready for the next pass
+  k1_finalize(z, f.M, f.K, f.nreg, f.kw, f.has_a, f.has_b, f.nA, f.nB, stats, fin_smem);
 }
 
 // --------------------------------------------------------------- CSR index lists
@@ -881,7 +969,7 @@ __global__ void __launch_bounds__(256) k1_csr(CsrArgs g) {
 // pays for this pass (mmmcu_get_counters / multiply with counters): it is not needed to
 // multiply.  The plan totals out[5] = Σ bpop (pop_total), out[6] = Σ (nreg - bnz)
 // (zero codes) and the path choice out[7] / span out[8] come from K1's last CTA
-// (k1_plan_totals) out of per-warp atomics of the B tiles.
+// (k1_finalize) out of per-warp atomics of the B tiles.
 // bpop[k] (# non-zero 8-column groups of row k) and bnz[k] (# non-zero 64-column regions)
 // from the group k-masks: thread per k walks the ld/8 groups.
 // Per-column non-zero counts of A from the bitmap (WorkCounters on request; the K1 pass no
@@ -953,22 +1041,6 @@ __global__ void __launch_bounds__(1024) k1_counters(const uint32_t* __restrict__
     out[3] = v[2];
     out[4] = v[3];
   }
-}
-
-// Plan totals (K1's last CTA): pop_total, zero codes and the K2-SIMT span from the B tiles'
-// totals btot = {Σ non-zero (k, slice), Σ bpop, Σ bnz}.
-//   span: 16-column slices cost ~41 issue slots per non-zero (k, slice), 8-column groups ~23
-//   per non-zero (k, group); pick the cheaper.
-__device__ void k1_plan_totals(const unsigned long long* __restrict__ btot, int64_t K, int64_t nreg, int has_b,
-                               unsigned long long* __restrict__ out) {
-  if (threadIdx.x == 0) {
-    const unsigned long long pop = has_b ? btot[1] : 0ull, bnz = has_b ? btot[2] : 0ull;
-    out[5] = pop;
-    out[6] = has_b ? (unsigned long long)(K * nreg) - bnz : 0ull;
-    out[7] = (has_b && 41ull * btot[0] > 23ull * pop) ? 8ull : 16ull;
-    out[8] = out[7];  // the K2-SIMT span alone (out[7] may become 32 = K2-TC, k1_choose_path)
-  }
-  __syncthreads();
 }
 
 // ------------------------------------------------------ B steps for K2-TC (dense tiles)

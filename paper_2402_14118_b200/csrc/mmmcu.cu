@@ -20,6 +20,7 @@
 #include "k2_csr.cuh"
 #include "k2_simt.cuh"
 #include "k2_tc.cuh"
+#include "kgen.cuh"
 
 // K1 pass ring for ordinary operand mixes: stages x CTAs per SM (measured best of 2x3, 3x2, 1x6)
 #ifndef K1_SMALL_ST
@@ -115,6 +116,16 @@ struct mmmcu_ctx {
 
   // ---- export scratch
   DevBuf scratch0, scratch1;
+
+  // ---- lane-general / f64 plans (kgen.cuh): every (dtype, lane config) but the f32 default
+  // lane, whose fused K1 / K2 path is above.  A plan built by them shares abits / row_ptr /
+  // cols / tile_prefix / stats with the fast path; gen_a / gen_b say which path built it.
+  bool gen_a = false, gen_b = false;
+  mmmcu_dtype a_dt = MMMCU_F32, b_dt = MMMCU_F32;
+  int gen_G = 8, gen_P = 8;                     // the B plan's group width and pattern bits
+  const void* gA = nullptr;                     // typed operand pointers of the plan
+  const void* gB = nullptr;
+  DevBuf gcodes, gza, gzb;  // uint16 codes [K][ldb/R]; A scratch arow | tile_sum | acol; B scratch bpop | bnz
 };
 
 namespace {
@@ -196,22 +207,23 @@ mmmcu_status bind(mmmcu_ctx* ctx) {
   return MMMCU_OK;
 }
 
-// KernelTable<float>::build (kernel_table.cpp:64-72) + Matrix ctor lane checks
-// (matrix.hpp:73-74), then the GPU support check.
-mmmcu_status check_lane(mmmcu_ctx* ctx, mmmcu_lane lane) {
+// KernelTable<T>::build (kernel_table.cpp:64-72) + Matrix ctor lane checks (matrix.hpp:73-74),
+// with the reference's messages (dtype_name: "f32" / "f64").
+mmmcu_status validate_lane(mmmcu_ctx* ctx, mmmcu_lane lane, mmmcu_dtype dt) {
+  if (dt != MMMCU_F32 && dt != MMMCU_F64) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "unknown dtype");
   if (lane.w <= 0 || lane.p <= 0 || lane.v <= 0)
     return fail(ctx, MMMCU_ERR_INVALID_ARG, "lane config fields must be positive");
   if (lane.p < 1 || lane.p > 16)
     return fail(ctx, MMMCU_ERR_INVALID_ARG, "pattern size must lie in [1, 16], got " + std::to_string(lane.p));
   const int g = lane.w * lane.v;
   if (g != 1 && g != 2 && g != 4 && g != 8 && g != 16 && g != 32 && g != 64)
-    return fail(ctx, MMMCU_ERR_INVALID_ARG,
-                "unsupported lane configuration: group width " + std::to_string(g) + " for f32");
-  if (!(lane.w == 8 && lane.p == 8 && lane.v == 1))
-    return fail(ctx, MMMCU_ERR_UNSUPPORTED,
-                "the GPU path implements the f32 default lane config {W=8,P=8,V=1} only");
+    return fail(ctx, MMMCU_ERR_INVALID_ARG, "unsupported lane configuration: group width " + std::to_string(g) +
+                                                " for " + (dt == MMMCU_F64 ? "f64" : "f32"));
   return MMMCU_OK;
 }
+mmmcu_status check_lane(mmmcu_ctx* ctx, mmmcu_lane lane) { return validate_lane(ctx, lane, MMMCU_F32); }
+// the fused K1 / K2 kernels: f32 with the default lane config {W=8, P=8, V=1}
+bool fast_lane(mmmcu_lane lane, mmmcu_dtype dt) { return dt == MMMCU_F32 && lane.w == 8 && lane.p == 8 && lane.v == 1; }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -284,6 +296,8 @@ mmmcu_status stage_a(mmmcu_ctx* ctx, const float* A, int64_t M, int64_t K, int64
     return fail(ctx, MMMCU_ERR_INVALID_ARG, "A must be 16-byte aligned with lda >= K and lda % 4 == 0");
   const int64_t kw = (K + 31) / 32;
   ctx->has_a = false;
+  ctx->gen_a = false;
+  ctx->a_dt = MMMCU_F32;
   ctx->csr_idx_bytes = K <= 65536 ? 2 : 4;
   MMMCU_CUDA(ctx->abits.ensure(sizeof(uint32_t) * M * kw));
   MMMCU_TRY(next_half(ctx, ctx->za, ctx->za_half, ctx->pa, ctx->za_clean, sizeof(uint32_t) * za_words(M, K)));
@@ -314,6 +328,8 @@ mmmcu_status stage_b(mmmcu_ctx* ctx, const float* B, int64_t K, int64_t N, int64
   const int64_t kw = (K + 31) / 32;
   const int64_t nreg = ldb / 64, ngrp = ldb / 8;
   ctx->has_b = false;
+  ctx->gen_b = false;
+  ctx->b_dt = MMMCU_F32;
   ctx->ldb = ldb;  // the zb_* scratch offsets depend on it
   ctx->Kb = K;
   MMMCU_CUDA(ctx->codes.ensure((size_t)K * nreg));
@@ -492,7 +508,13 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   z.zero_a_n = ctx->zero_a_next ? (int64_t)(ctx->za_half / 16) : 0;
   z.zero_b = ctx->zero_b_next ? reinterpret_cast<uint4*>(ctx->zb.as<uint8_t>() + (ctx->pb ^ 1) * ctx->zb_half) : nullptr;
   z.zero_b_n = ctx->zero_b_next ? (int64_t)(ctx->zb_half / 16) : 0;
-  MMMCU_CUDA(launch_pdl(k1fn, dim3(k1_grid), dim3(mmmcu::kK1Block), k1_smem, ctx->stream, g, z, has_a, has_b,
+  MMMCU_CUDA(launch_pdl(k1fn, dim3(k1_grid), dim3(mmmcu::kK1Block), k1_smem, ctx->stream, g, z));
+  MMMCU_LAUNCHED();
+  // the finalize (plan totals, fp16 range guard, AUTO path choice, CSR tile prefix, K2-SIMT
+  // record offsets): one CTA, programmatically serialized behind the pass
+  const mmmcu::K1FinArgs fa{ctx->M, K, ctx->ldb / 64, kw, nA, nB, has_a, has_b};
+  MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k1_fin, cudaFuncAttributeMaxDynamicSharedMemorySize, mmmcu::k1_fin_smem()));
+  MMMCU_CUDA(launch_pdl(mmmcu::k1_fin, dim3(1), dim3(32 * mmmcu::kFinWarps), mmmcu::k1_fin_smem(), ctx->stream, z, fa,
                         ctx->stats.as<unsigned long long>()));
   if (ctx->zero_a_next) ctx->za_clean[ctx->pa ^ 1] = true;
   if (ctx->zero_b_next) ctx->zb_clean[ctx->pb ^ 1] = true;
@@ -513,21 +535,25 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
     cudaMemcpyToSymbol(mmmcu::k1_prof, &dbuf, sizeof(dbuf));
     // rerun (idempotent outputs; counters are re-zeroed by the caller's memsets only once, so
     // use the stamps, not the counters)
-    k1fn<<<k1_grid, mmmcu::kK1Block, k1_smem, ctx->stream>>>(g, z, has_a, has_b, ctx->stats.as<unsigned long long>());
+    k1fn<<<k1_grid, mmmcu::kK1Block, k1_smem, ctx->stream>>>(g, z);
     cudaDeviceSynchronize();
+    cudaMemset(ctx->ctl.as<unsigned int>() + 1, 0, sizeof(unsigned int));  // the rerun's tile counter
     std::vector<unsigned long long> h(4 * k1_grid);
     cudaMemcpy(h.data(), dbuf, 8 * 4 * k1_grid, cudaMemcpyDeviceToHost);
-    unsigned long long t0 = ~0ull, t1 = 0, tmax_start = 0, fin = 0, fin_start = 0;
+    unsigned long long t0 = ~0ull, t1 = 0, tmax_start = 0;
     double dsum = 0;
     for (unsigned i = 0; i < k1_grid; ++i) {
       t0 = std::min(t0, h[4 * i]);
       tmax_start = std::max(tmax_start, h[4 * i]);
       t1 = std::max(t1, h[4 * i + 1]);
       dsum += (double)(h[4 * i + 1] - h[4 * i]);
-      if (h[4 * i + 3]) { fin = h[4 * i + 2]; fin_start = h[4 * i + 1]; }
     }
-    fprintf(stderr, "K1_PROF: grid %u, CTA start spread %.1f us, tiles done by %.1f us (mean CTA %.1f us), finalize %.1f us, total %.1f us\n",
-            k1_grid, (tmax_start - t0) / 1e3, (t1 - t0) / 1e3, dsum / k1_grid / 1e3, (fin - fin_start) / 1e3, (fin - t0) / 1e3);
+    unsigned long long fp[8];
+    cudaMemcpyFromSymbol(fp, mmmcu::k1_fin_prof, sizeof(fp));
+    fprintf(stderr, "K1_PROF k1_fin phases (us): setup %.2f | parallel part %.2f | thread-0 choice %.2f | row_off %.2f\n",
+            (fp[1] - fp[0]) / 1e3, (fp[2] - fp[1]) / 1e3, (fp[3] - fp[2]) / 1e3, (fp[4] - fp[3]) / 1e3);
+    fprintf(stderr, "K1_PROF: grid %u, CTA start spread %.1f us, tiles done by %.1f us (mean CTA %.1f us)\n", k1_grid,
+            (tmax_start - t0) / 1e3, (t1 - t0) / 1e3, dsum / k1_grid / 1e3);
     void* zp = nullptr;
     cudaMemcpyToSymbol(mmmcu::k1_prof, &zp, sizeof(zp));
   }
@@ -781,6 +807,134 @@ mmmcu_status fill_counters(mmmcu_ctx* ctx, mmmcu_counters* out) {
 }
 
 
+
+// ----------------------------------------------------------- lane-general / f64 plans
+size_t dt_size(mmmcu_dtype dt) { return dt == MMMCU_F64 ? 8 : 4; }
+// the plan's operand pointers (fast path: ctx->A / ctx->B; general path: gA / gB)
+const void* plan_a(const mmmcu_ctx* ctx) { return ctx->gen_a ? ctx->gA : static_cast<const void*>(ctx->A); }
+const void* plan_b(const mmmcu_ctx* ctx) { return ctx->gen_b ? ctx->gB : static_cast<const void*>(ctx->B); }
+int64_t gen_nreg(const mmmcu_ctx* ctx) { return ctx->ldb / ((int64_t)ctx->gen_G * ctx->gen_P); }
+
+// preprocess_a of an f32 / f64 A on the general path: bitmap + row counts by
+// kg_abits, the 32-row tile prefix, then K1's CSR kernel over the same bitmap.
+template <typename T>
+mmmcu_status gen_preprocess_a(mmmcu_ctx* ctx, const T* A, int64_t M, int64_t K, int64_t lda, uint64_t av,
+                              mmmcu_dtype dt) {
+  if (M <= 0 || K <= 0) return fail(ctx, MMMCU_ERR_INVALID_ARG, "matrix dimensions must be positive");
+  if (!A) return fail(ctx, MMMCU_ERR_INVALID_ARG, "A is null");
+  if (lda < K) return fail(ctx, MMMCU_ERR_DIM_MISMATCH, "lda smaller than the row");
+  const int64_t kw = (K + 31) / 32, ntile = (M + mmmcu::kK1Rows - 1) / mmmcu::kK1Rows;
+  ctx->has_a = false;
+  ctx->csr_idx_bytes = K <= 65536 ? 2 : 4;
+  MMMCU_CUDA(ctx->abits.ensure(sizeof(uint32_t) * M * kw));
+  MMMCU_CUDA(ctx->gza.ensure(sizeof(uint32_t) * (M + ntile + K)));
+  MMMCU_CUDA(ctx->tile_prefix.ensure(sizeof(int64_t) * (ntile + 1)));
+  MMMCU_CUDA(ctx->row_ptr.ensure(sizeof(int64_t) * (M + 1)));
+  MMMCU_CUDA(ctx->cols.ensure((size_t)ctx->csr_idx_bytes * M * K));
+  uint32_t* arow = ctx->gza.as<uint32_t>();
+  uint32_t* tsum = arow + M;
+  MMMCU_CUDA(cudaMemsetAsync(arow, 0, sizeof(uint32_t) * (M + ntile), ctx->stream));
+  const int64_t oct = (kw + 7) / 8;
+  mmmcu::kg_abits<T><<<dim3((unsigned)oct, (unsigned)M), 256, 0, ctx->stream>>>(A, M, K, lda, ctx->abits.as<uint32_t>(),
+                                                                                 kw, arow, tsum);
+  MMMCU_LAUNCHED();
+  mmmcu::kg_tile_prefix<<<1, 256, 0, ctx->stream>>>(tsum, ntile, ctx->tile_prefix.as<int64_t>());
+  MMMCU_LAUNCHED();
+  const int csmem = mmmcu::k1_csr_smem(ctx->csr_idx_bytes);
+  MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k1_csr, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem));
+  const mmmcu::CsrArgs ca{ctx->abits.as<uint32_t>(), arow, ctx->tile_prefix.as<int64_t>(), M, kw,
+                          ctx->row_ptr.as<int64_t>(), ctx->cols.p, ctx->csr_idx_bytes};
+  mmmcu::k1_csr<<<(unsigned)((M + mmmcu::kCsrRows - 1) / mmmcu::kCsrRows), 256, csmem, ctx->stream>>>(ca);
+  MMMCU_LAUNCHED();
+  ctx->gA = A;
+  ctx->A = dt == MMMCU_F32 ? reinterpret_cast<const float*>(A) : nullptr;
+  ctx->M = M;
+  ctx->Ka = K;
+  ctx->lda = lda;
+  ctx->av = av;
+  ctx->a_dt = dt;
+  ctx->gen_a = true;
+  ctx->op_at = false;
+  ctx->has_a = true;
+  return MMMCU_OK;
+}
+
+// preprocess_b for any lane: P-bit codes per region, per-row factors, totals.
+template <typename T>
+mmmcu_status gen_preprocess_b(mmmcu_ctx* ctx, const T* B, int64_t K, int64_t N, int64_t ldb, mmmcu_lane lane,
+                              uint64_t bv, mmmcu_dtype dt) {
+  if (K <= 0 || N <= 0) return fail(ctx, MMMCU_ERR_INVALID_ARG, "matrix dimensions must be positive");
+  if (!B) return fail(ctx, MMMCU_ERR_INVALID_ARG, "B is null");
+  const int64_t R = (int64_t)lane.w * lane.p * lane.v;
+  if (ldb < N || ldb % R != 0)
+    return fail(ctx, MMMCU_ERR_INVALID_ARG, "B needs ldb >= N and ldb a multiple of the region width " +
+                                                std::to_string(R) + " (Matrix padding)");
+  ctx->has_b = false;
+  const int64_t nreg = ldb / R;
+  MMMCU_CUDA(ctx->gcodes.ensure(sizeof(uint16_t) * K * nreg));
+  MMMCU_CUDA(ctx->gzb.ensure(sizeof(uint32_t) * 2 * K));
+  MMMCU_CUDA(ctx->stats.ensure(sizeof(unsigned long long) * 24));
+  const int64_t n = K * nreg;
+  mmmcu::kg_codes<T><<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(B, K, ldb, nreg, lane.w * lane.v, lane.p,
+                                                                          ctx->gcodes.as<uint16_t>());
+  MMMCU_LAUNCHED();
+  uint32_t* bpop = ctx->gzb.as<uint32_t>();
+  mmmcu::kg_bcounts<<<(unsigned)((K + 255) / 256), 256, 0, ctx->stream>>>(ctx->gcodes.as<uint16_t>(), K, nreg, bpop,
+                                                                         bpop + K);
+  MMMCU_LAUNCHED();
+  mmmcu::kg_plan_totals<<<1, 1024, 0, ctx->stream>>>(bpop, bpop + K, K, nreg, ctx->stats.as<unsigned long long>());
+  MMMCU_LAUNCHED();
+  ctx->gB = B;
+  ctx->B = dt == MMMCU_F32 ? reinterpret_cast<const float*>(B) : nullptr;
+  ctx->Kb = K;
+  ctx->N = N;
+  ctx->ldb = ldb;
+  ctx->bv = bv;
+  ctx->b_dt = dt;
+  ctx->gen_G = lane.w * lane.v;
+  ctx->gen_P = lane.p;
+  ctx->gen_b = true;
+  ctx->op_rows = ctx->op_tcb = false;
+  ctx->has_b = true;
+  return MMMCU_OK;
+}
+
+// Exact WorkCounters of a general-path plan: lane_fma_ops = Σ_k acol[k]·G·bpop[k].
+mmmcu_status gen_counters(mmmcu_ctx* ctx, mmmcu_counters* out) {
+  if (!out) return MMMCU_OK;
+  if (!ctx->has_a || !ctx->has_b) return fail(ctx, MMMCU_ERR_NOT_READY, "counters need both plans");
+  const int64_t K = ctx->Kb;
+  MMMCU_CUDA(ctx->scratch0.ensure(sizeof(uint32_t) * ctx->Ka));
+  uint32_t* acol = ctx->scratch0.as<uint32_t>();
+  mmmcu::k1_acol<<<(unsigned)((ctx->Ka + 255) / 256), 256, 0, ctx->stream>>>(ctx->abits.as<uint32_t>(), ctx->M, ctx->Ka,
+                                                                             (ctx->Ka + 31) / 32, acol);
+  MMMCU_LAUNCHED();
+  const uint32_t* bpop = ctx->gzb.as<uint32_t>();
+  mmmcu::kg_counters<<<1, 1024, 0, ctx->stream>>>(acol, bpop, bpop + K, K, ctx->M, gen_nreg(ctx), ctx->gen_G,
+                                                  ctx->stats.as<unsigned long long>());
+  MMMCU_LAUNCHED();
+  unsigned long long s[16];
+  MMMCU_TRY(read_stats(ctx, s));
+  out->kernel_invocations = s[0];
+  out->lane_fma_ops = s[1];
+  out->rows_skipped = s[2];
+  out->regions_skipped_by_zero_code = s[3];
+  return MMMCU_OK;
+}
+
+// C += A*B over a general-path B plan (kg_mul: the reference's per-element fma chain).
+template <typename T>
+mmmcu_status gen_multiply(mmmcu_ctx* ctx, T* C, int64_t ldc, const T* A) {
+  const int64_t nreg = gen_nreg(ctx);
+  dim3 grid((unsigned)((ctx->ldb + mmmcu::kKgTile - 1) / mmmcu::kKgTile),
+            (unsigned)((ctx->M + mmmcu::kKgTile - 1) / mmmcu::kKgTile));
+  mmmcu::kg_mul<T, false><<<grid, 256, 0, ctx->stream>>>(A, ctx->lda, static_cast<const T*>(ctx->gB), ctx->ldb, C, ldc,
+                                                         ctx->M, ctx->Ka, ctx->ldb, ctx->gcodes.as<uint16_t>(), nreg,
+                                                         ctx->gen_G, ctx->gen_P);
+  MMMCU_LAUNCHED();
+  return MMMCU_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -813,7 +967,8 @@ mmmcu_status mmmcu_ctx_destroy(mmmcu_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : {&ctx->abits, &ctx->za, &ctx->tile_prefix, &ctx->row_ptr, &ctx->cols, &ctx->codes, &ctx->bgrp, &ctx->zb,
                     &ctx->ctl, &ctx->at, &ctx->tcb, &ctx->tck, &ctx->tcn, &ctx->brows, &ctx->row_off,
-                    &ctx->stats, &ctx->hA, &ctx->hB, &ctx->hC, &ctx->scratch0, &ctx->scratch1})
+                    &ctx->stats, &ctx->hA, &ctx->hB, &ctx->hC, &ctx->scratch0, &ctx->scratch1, &ctx->gcodes,
+                    &ctx->gza, &ctx->gzb})
     b->release();
   delete ctx;
   return MMMCU_OK;
@@ -837,6 +992,7 @@ mmmcu_status mmmcu_preprocess_b(mmmcu_ctx* ctx, const float* B, int64_t K, int64
                                 uint64_t bv) {
   MMMCU_TRY(bind(ctx));
   MMMCU_TRY(check_lane(ctx, lane));
+  if (!fast_lane(lane, MMMCU_F32)) return gen_preprocess_b(ctx, B, K, N, ldb, lane, bv, MMMCU_F32);
   MMMCU_TRY(stage_b(ctx, B, K, N, ldb, bv));
   return launch_k1(ctx, false, true);
 }
@@ -845,6 +1001,10 @@ mmmcu_status mmmcu_preprocess(mmmcu_ctx* ctx, const float* A, int64_t M, int64_t
                               int64_t N, int64_t ldb, mmmcu_lane lane, uint64_t av, uint64_t bv) {
   MMMCU_TRY(bind(ctx));
   MMMCU_TRY(check_lane(ctx, lane));
+  if (!fast_lane(lane, MMMCU_F32)) {  // the lane-general path (kgen.cuh)
+    MMMCU_TRY(gen_preprocess_a(ctx, A, M, K, lda, av, MMMCU_F32));
+    return gen_preprocess_b(ctx, B, K, N, ldb, lane, bv, MMMCU_F32);
+  }
   MMMCU_TRY(stage_a(ctx, A, M, K, lda, av));
   MMMCU_TRY(stage_b(ctx, B, K, N, ldb, bv));
   return launch_k1(ctx, true, true);
@@ -854,6 +1014,7 @@ mmmcu_status mmmcu_get_counters(mmmcu_ctx* ctx, mmmcu_counters* out) {
   MMMCU_TRY(bind(ctx));
   if (!out) return fail(ctx, MMMCU_ERR_INVALID_ARG, "out is null");
   if (!ctx->has_a && !ctx->has_b) return fail(ctx, MMMCU_ERR_NOT_READY, "no plan");
+  if (ctx->gen_a || ctx->gen_b) return gen_counters(ctx, out);
   return fill_counters(ctx, out);
 }
 
@@ -863,7 +1024,7 @@ mmmcu_status mmmcu_get_plan_stats(mmmcu_ctx* ctx, mmmcu_plan_stats* out) {
   if (!ctx->has_b) return fail(ctx, MMMCU_ERR_NOT_READY, "no B plan");
   unsigned long long s[16];
   MMMCU_TRY(read_stats(ctx, s));
-  const int64_t n = ctx->Kb * (ctx->ldb / 64);
+  const int64_t n = ctx->Kb * (ctx->gen_b ? gen_nreg(ctx) : ctx->ldb / 64);
   out->region_count = n;
   out->zero_region_fraction = n ? (double)s[6] / (double)n : 0.0;
   out->mean_popcount = n ? (double)s[5] / (double)n : 0.0;
@@ -872,6 +1033,18 @@ mmmcu_status mmmcu_get_plan_stats(mmmcu_ctx* ctx, mmmcu_plan_stats* out) {
 
 // The region codes are not materialised by K1's hot pass; rebuild them from the group masks.
 mmmcu_status build_codes(mmmcu_ctx* ctx) {
+  if (ctx->gen_b) {  // P <= 8 (callers check): the uint16 codes narrowed
+    const int64_t n = ctx->Kb * gen_nreg(ctx);
+    MMMCU_CUDA(ctx->codes.ensure((size_t)n));
+    std::vector<uint16_t> w((size_t)n);
+    std::vector<uint8_t> b((size_t)n);
+    MMMCU_CUDA(cudaMemcpyAsync(w.data(), ctx->gcodes.p, sizeof(uint16_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    MMMCU_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int64_t t = 0; t < n; ++t) b[(size_t)t] = (uint8_t)w[(size_t)t];
+    MMMCU_CUDA(cudaMemcpyAsync(ctx->codes.p, b.data(), (size_t)n, cudaMemcpyHostToDevice, ctx->stream));
+    MMMCU_CUDA(cudaStreamSynchronize(ctx->stream));
+    return MMMCU_OK;
+  }
   const int64_t n = ctx->Kb * (ctx->ldb / 64);
   mmmcu::k1_codes_export<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(
       ctx->bgrp.as<uint32_t>(), ctx->Kb, ctx->ldb / 64, (ctx->Kb + 31) / 32, ctx->codes.as<uint8_t>());
@@ -882,7 +1055,9 @@ mmmcu_status build_codes(mmmcu_ctx* ctx) {
 mmmcu_status mmmcu_export_b_codes(mmmcu_ctx* ctx, uint8_t* codes_host, int64_t capacity) {
   MMMCU_TRY(bind(ctx));
   if (!ctx->has_b) return fail(ctx, MMMCU_ERR_NOT_READY, "no B plan");
-  const int64_t n = ctx->Kb * (ctx->ldb / 64);
+  if (ctx->gen_b && ctx->gen_P > 8)
+    return fail(ctx, MMMCU_ERR_UNSUPPORTED, "codes wider than 8 bits: use mmmcu_export_b_codes16");
+  const int64_t n = ctx->Kb * (ctx->gen_b ? gen_nreg(ctx) : ctx->ldb / 64);
   if (!codes_host || capacity < n) return fail(ctx, MMMCU_ERR_INVALID_ARG, "codes buffer too small");
   MMMCU_TRY(build_codes(ctx));
   MMMCU_CUDA(cudaMemcpyAsync(codes_host, ctx->codes.p, (size_t)n, cudaMemcpyDeviceToHost, ctx->stream));
@@ -890,21 +1065,12 @@ mmmcu_status mmmcu_export_b_codes(mmmcu_ctx* ctx, uint8_t* codes_host, int64_t c
   return MMMCU_OK;
 }
 
-mmmcu_status mmmcu_export_bplans(mmmcu_ctx* ctx, int64_t leaf_dim, uint8_t* plans_host, int64_t plans_capacity,
-                                 int64_t* plan_off_host, int64_t off_capacity, int64_t* n_plans) {
-  MMMCU_TRY(bind(ctx));
-  if (!ctx->has_b) return fail(ctx, MMMCU_ERR_NOT_READY, "no B plan");
-  if (leaf_dim <= 0 || leaf_dim % 64 != 0)
-    return fail(ctx, MMMCU_ERR_INVALID_ARG, "leaf_dim must be a positive multiple of the region width 64");
-  const int64_t K = ctx->Kb, nreg = ctx->ldb / 64, rpl = leaf_dim / 64;
+extern "C++" {
+// BPlan leaf order of row-major codes [K][nreg]
+template <typename C>
+void leaf_order(const std::vector<C>& codes, int64_t K, int64_t nreg, int64_t leaf_dim, int64_t rpl, C* plans_host,
+                int64_t* plan_off_host) {
   const int64_t n_lr = (K + leaf_dim - 1) / leaf_dim, n_lc = (nreg + rpl - 1) / rpl;
-  if (n_plans) *n_plans = n_lr * n_lc;
-  if (!plans_host || plans_capacity < K * nreg || !plan_off_host || off_capacity < n_lr * n_lc + 1)
-    return fail(ctx, MMMCU_ERR_INVALID_ARG, "plan buffers too small");
-  std::vector<uint8_t> codes((size_t)(K * nreg));
-  MMMCU_TRY(build_codes(ctx));
-  MMMCU_CUDA(cudaMemcpyAsync(codes.data(), ctx->codes.p, codes.size(), cudaMemcpyDeviceToHost, ctx->stream));
-  MMMCU_CUDA(cudaStreamSynchronize(ctx->stream));
   int64_t pos = 0, p = 0;
   for (int64_t lr = 0; lr < n_lr; ++lr)
     for (int64_t lc = 0; lc < n_lc; ++lc) {
@@ -915,6 +1081,67 @@ mmmcu_status mmmcu_export_bplans(mmmcu_ctx* ctx, int64_t leaf_dim, uint8_t* plan
         for (int64_t r = r0; r < r1; ++r) plans_host[pos++] = codes[(size_t)(k * nreg + r)];
     }
   plan_off_host[p] = pos;
+}
+
+template <typename C>
+mmmcu_status export_bplans_t(mmmcu_ctx* ctx, int64_t leaf_dim, C* plans_host, int64_t plans_capacity,
+                             int64_t* plan_off_host, int64_t off_capacity, int64_t* n_plans) {
+  MMMCU_TRY(bind(ctx));
+  if (!ctx->has_b) return fail(ctx, MMMCU_ERR_NOT_READY, "no B plan");
+  if (sizeof(C) == 1 && ctx->gen_b && ctx->gen_P > 8)
+    return fail(ctx, MMMCU_ERR_UNSUPPORTED, "codes wider than 8 bits: use mmmcu_export_bplans16");
+  const int64_t R = ctx->gen_b ? (int64_t)ctx->gen_G * ctx->gen_P : 64;
+  if (leaf_dim <= 0 || leaf_dim % R != 0)
+    return fail(ctx, MMMCU_ERR_INVALID_ARG,
+                "leaf_dim must be a positive multiple of the region width " + std::to_string(R));
+  const int64_t K = ctx->Kb, nreg = ctx->ldb / R, rpl = leaf_dim / R;
+  const int64_t n_lr = (K + leaf_dim - 1) / leaf_dim, n_lc = (nreg + rpl - 1) / rpl;
+  if (n_plans) *n_plans = n_lr * n_lc;
+  if (!plans_host || plans_capacity < K * nreg || !plan_off_host || off_capacity < n_lr * n_lc + 1)
+    return fail(ctx, MMMCU_ERR_INVALID_ARG, "plan buffers too small");
+  std::vector<C> codes((size_t)(K * nreg));
+  if (ctx->gen_b) {
+    std::vector<uint16_t> w((size_t)(K * nreg));
+    MMMCU_CUDA(cudaMemcpyAsync(w.data(), ctx->gcodes.p, sizeof(uint16_t) * w.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    MMMCU_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (size_t t = 0; t < w.size(); ++t) codes[t] = (C)w[t];
+  } else {
+    std::vector<uint8_t> b((size_t)(K * nreg));
+    MMMCU_TRY(build_codes(ctx));
+    MMMCU_CUDA(cudaMemcpyAsync(b.data(), ctx->codes.p, b.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    MMMCU_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (size_t t = 0; t < b.size(); ++t) codes[t] = (C)b[t];
+  }
+  leaf_order(codes, K, nreg, leaf_dim, rpl, plans_host, plan_off_host);
+  return MMMCU_OK;
+}
+}  // extern "C++"
+
+mmmcu_status mmmcu_export_bplans(mmmcu_ctx* ctx, int64_t leaf_dim, uint8_t* plans_host, int64_t plans_capacity,
+                                 int64_t* plan_off_host, int64_t off_capacity, int64_t* n_plans) {
+  return export_bplans_t<uint8_t>(ctx, leaf_dim, plans_host, plans_capacity, plan_off_host, off_capacity, n_plans);
+}
+
+mmmcu_status mmmcu_export_bplans16(mmmcu_ctx* ctx, int64_t leaf_dim, uint16_t* plans_host, int64_t plans_capacity,
+                                   int64_t* plan_off_host, int64_t off_capacity, int64_t* n_plans) {
+  return export_bplans_t<uint16_t>(ctx, leaf_dim, plans_host, plans_capacity, plan_off_host, off_capacity, n_plans);
+}
+
+mmmcu_status mmmcu_export_b_codes16(mmmcu_ctx* ctx, uint16_t* codes_host, int64_t capacity) {
+  MMMCU_TRY(bind(ctx));
+  if (!ctx->has_b) return fail(ctx, MMMCU_ERR_NOT_READY, "no B plan");
+  const int64_t n = ctx->Kb * (ctx->gen_b ? gen_nreg(ctx) : ctx->ldb / 64);
+  if (!codes_host || capacity < n) return fail(ctx, MMMCU_ERR_INVALID_ARG, "codes buffer too small");
+  if (ctx->gen_b) {
+    MMMCU_CUDA(cudaMemcpyAsync(codes_host, ctx->gcodes.p, sizeof(uint16_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    MMMCU_CUDA(cudaStreamSynchronize(ctx->stream));
+    return MMMCU_OK;
+  }
+  std::vector<uint8_t> b((size_t)n);
+  MMMCU_TRY(build_codes(ctx));
+  MMMCU_CUDA(cudaMemcpyAsync(b.data(), ctx->codes.p, (size_t)n, cudaMemcpyDeviceToHost, ctx->stream));
+  MMMCU_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int64_t t = 0; t < n; ++t) codes_host[t] = b[(size_t)t];
   return MMMCU_OK;
 }
 
@@ -1007,6 +1234,7 @@ mmmcu_status mmmcu_last_algo(mmmcu_ctx* ctx, mmmcu_algo* algo) {
 
 mmmcu_status mmmcu_multiply(mmmcu_ctx* ctx, float* C, int64_t ldc, const float* A, const float* B, uint64_t av,
                             uint64_t bv, mmmcu_counters* counters) {
+  if (ctx && (ctx->gen_a || ctx->gen_b)) return mmmcu_multiply_t(ctx, MMMCU_F32, C, ldc, A, B, av, bv, counters);
   MMMCU_TRY(bind(ctx));
   MMMCU_TRY(check_plan(ctx, A, B, av, bv));
   if (!C) return fail(ctx, MMMCU_ERR_INVALID_ARG, "C is null");
@@ -1072,64 +1300,102 @@ mmmcu_status mmmcu_multiply_simple(mmmcu_ctx* ctx, float* C, int64_t ldc, const 
   return MMMCU_OK;
 }
 
-mmmcu_status mmmcu_multiply_host(mmmcu_ctx* ctx, float* C_host, int64_t ldc, const float* A_host, int64_t lda,
-                                 const float* B_host, int64_t ldb, int64_t M, int64_t K, int64_t N,
-                                 mmmcu_counters* counters) {
+mmmcu_status mmmcu_multiply_host_t(mmmcu_ctx* ctx, mmmcu_dtype dt, void* C_host, int64_t ldc, const void* A_host,
+                                   int64_t lda, const void* B_host, int64_t ldb, int64_t M, int64_t K, int64_t N,
+                                   mmmcu_lane lane, mmmcu_counters* counters) {
   MMMCU_TRY(bind(ctx));
   if (M <= 0 || K <= 0 || N <= 0) return fail(ctx, MMMCU_ERR_INVALID_ARG, "matrix dimensions must be positive");
   if (!A_host || !B_host || !C_host) return fail(ctx, MMMCU_ERR_INVALID_ARG, "null operand");
-  MMMCU_CUDA(ctx->hA.ensure(sizeof(float) * M * lda));
-  MMMCU_CUDA(ctx->hB.ensure(sizeof(float) * K * ldb));
-  MMMCU_CUDA(ctx->hC.ensure(sizeof(float) * M * ldc));
-  MMMCU_CUDA(cudaMemcpyAsync(ctx->hA.p, A_host, sizeof(float) * M * lda, cudaMemcpyHostToDevice, ctx->stream));
-  MMMCU_CUDA(cudaMemcpyAsync(ctx->hB.p, B_host, sizeof(float) * K * ldb, cudaMemcpyHostToDevice, ctx->stream));
-  MMMCU_CUDA(cudaMemcpyAsync(ctx->hC.p, C_host, sizeof(float) * M * ldc, cudaMemcpyHostToDevice, ctx->stream));
-  const mmmcu_lane lane{8, 8, 1};
-  const float* dA = ctx->hA.as<float>();
-  const float* dB = ctx->hB.as<float>();
+  if (dt != MMMCU_F32 && dt != MMMCU_F64) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "unknown dtype");
+  const size_t es = dt_size(dt);
+  MMMCU_CUDA(ctx->hA.ensure(es * M * lda));
+  MMMCU_CUDA(ctx->hB.ensure(es * K * ldb));
+  MMMCU_CUDA(ctx->hC.ensure(es * M * ldc));
+  MMMCU_CUDA(cudaMemcpyAsync(ctx->hA.p, A_host, es * M * lda, cudaMemcpyHostToDevice, ctx->stream));
+  MMMCU_CUDA(cudaMemcpyAsync(ctx->hB.p, B_host, es * K * ldb, cudaMemcpyHostToDevice, ctx->stream));
+  MMMCU_CUDA(cudaMemcpyAsync(ctx->hC.p, C_host, es * M * ldc, cudaMemcpyHostToDevice, ctx->stream));
   // host operands carry no version: tag the staging copies with a per-call counter
   static thread_local uint64_t tag = 0;
   ++tag;
-  MMMCU_TRY(mmmcu_preprocess(ctx, dA, M, K, lda, dB, N, ldb, lane, tag, tag));
-  MMMCU_TRY(mmmcu_multiply(ctx, ctx->hC.as<float>(), ldc, dA, dB, tag, tag, nullptr));
-  MMMCU_CUDA(cudaMemcpyAsync(C_host, ctx->hC.p, sizeof(float) * M * ldc, cudaMemcpyDeviceToHost, ctx->stream));
+  MMMCU_TRY(mmmcu_preprocess_t(ctx, dt, ctx->hA.p, M, K, lda, ctx->hB.p, N, ldb, lane, tag, tag));
+  MMMCU_TRY(mmmcu_multiply_t(ctx, dt, ctx->hC.p, ldc, ctx->hA.p, ctx->hB.p, tag, tag, nullptr));
+  MMMCU_CUDA(cudaMemcpyAsync(C_host, ctx->hC.p, es * M * ldc, cudaMemcpyDeviceToHost, ctx->stream));
   MMMCU_CUDA(cudaStreamSynchronize(ctx->stream));
-  return fill_counters(ctx, counters);
+  return counters ? mmmcu_get_counters(ctx, counters) : MMMCU_OK;
+}
+
+mmmcu_status mmmcu_multiply_host(mmmcu_ctx* ctx, float* C_host, int64_t ldc, const float* A_host, int64_t lda,
+                                 const float* B_host, int64_t ldb, int64_t M, int64_t K, int64_t N,
+                                 mmmcu_counters* counters) {
+  return mmmcu_multiply_host_t(ctx, MMMCU_F32, C_host, ldc, A_host, lda, B_host, ldb, M, K, N, mmmcu_lane{8, 8, 1},
+                               counters);
+}
+
+mmmcu_status mmmcu_preprocess_host_t(mmmcu_ctx* ctx, mmmcu_dtype dt, const void* A_host, int64_t M, int64_t K,
+                                     int64_t lda, const void* B_host, int64_t N, int64_t ldb, mmmcu_lane lane,
+                                     uint64_t av, uint64_t bv) {
+  MMMCU_TRY(bind(ctx));
+  MMMCU_TRY(validate_lane(ctx, lane, dt));
+  if (M <= 0 || K <= 0 || N <= 0) return fail(ctx, MMMCU_ERR_INVALID_ARG, "matrix dimensions must be positive");
+  if (!A_host || !B_host) return fail(ctx, MMMCU_ERR_INVALID_ARG, "null operand");
+  if (lda < K || ldb < N) return fail(ctx, MMMCU_ERR_DIM_MISMATCH, "leading dimension smaller than the row");
+  const size_t es = dt_size(dt);
+  MMMCU_CUDA(ctx->hA.ensure(es * M * lda));
+  MMMCU_CUDA(ctx->hB.ensure(es * K * ldb));
+  MMMCU_CUDA(cudaMemcpyAsync(ctx->hA.p, A_host, es * M * lda, cudaMemcpyHostToDevice, ctx->stream));
+  MMMCU_CUDA(cudaMemcpyAsync(ctx->hB.p, B_host, es * K * ldb, cudaMemcpyHostToDevice, ctx->stream));
+  MMMCU_TRY(mmmcu_preprocess_t(ctx, dt, ctx->hA.p, M, K, lda, ctx->hB.p, N, ldb, lane, av, bv));
+  MMMCU_CUDA(cudaStreamSynchronize(ctx->stream));  // the host buffers may change after return
+  return MMMCU_OK;
 }
 
 mmmcu_status mmmcu_preprocess_host(mmmcu_ctx* ctx, const float* A_host, int64_t M, int64_t K, int64_t lda,
                                    const float* B_host, int64_t N, int64_t ldb, mmmcu_lane lane, uint64_t av,
                                    uint64_t bv) {
+  return mmmcu_preprocess_host_t(ctx, MMMCU_F32, A_host, M, K, lda, B_host, N, ldb, lane, av, bv);
+}
+
+mmmcu_status mmmcu_multiply_planned_host_t(mmmcu_ctx* ctx, mmmcu_dtype dt, void* C_host, int64_t ldc, uint64_t av,
+                                           uint64_t bv, int worker_count, mmmcu_counters* counters) {
   MMMCU_TRY(bind(ctx));
-  MMMCU_TRY(check_lane(ctx, lane));
+  if (worker_count <= 0) return fail(ctx, MMMCU_ERR_WORKERS, "worker_count must be positive");
+  if (!C_host) return fail(ctx, MMMCU_ERR_INVALID_ARG, "C is null");
+  if (!ctx->has_a || !ctx->has_b || plan_a(ctx) != ctx->hA.p || plan_b(ctx) != ctx->hB.p)
+    return fail(ctx, MMMCU_ERR_NOT_READY, "no host-operand plan: call mmmcu_preprocess_host first");
+  if (av != ctx->av || bv != ctx->bv)
+    return fail(ctx, MMMCU_ERR_STALE, "stale context: operands changed since preprocessing (Matrix::version)");
+  const size_t es = dt_size(dt);
+  const int64_t M = ctx->M;
+  MMMCU_CUDA(ctx->hC.ensure(es * M * ldc));
+  MMMCU_CUDA(cudaMemcpyAsync(ctx->hC.p, C_host, es * M * ldc, cudaMemcpyHostToDevice, ctx->stream));
+  MMMCU_TRY(mmmcu_multiply_t(ctx, dt, ctx->hC.p, ldc, ctx->hA.p, ctx->hB.p, av, bv, nullptr));
+  MMMCU_CUDA(cudaMemcpyAsync(C_host, ctx->hC.p, es * M * ldc, cudaMemcpyDeviceToHost, ctx->stream));
+  MMMCU_CUDA(cudaStreamSynchronize(ctx->stream));
+  return counters ? mmmcu_get_counters(ctx, counters) : MMMCU_OK;
+}
+
+mmmcu_status mmmcu_multiply_simple_host_t(mmmcu_ctx* ctx, mmmcu_dtype dt, void* C_host, int64_t ldc, const void* A_host,
+                                          int64_t lda, const void* B_host, int64_t ldb, int64_t M, int64_t K, int64_t N) {
+  MMMCU_TRY(bind(ctx));
   if (M <= 0 || K <= 0 || N <= 0) return fail(ctx, MMMCU_ERR_INVALID_ARG, "matrix dimensions must be positive");
-  if (!A_host || !B_host) return fail(ctx, MMMCU_ERR_INVALID_ARG, "null operand");
-  if (lda < K || ldb < N) return fail(ctx, MMMCU_ERR_DIM_MISMATCH, "leading dimension smaller than the row");
-  MMMCU_CUDA(ctx->hA.ensure(sizeof(float) * M * lda));
-  MMMCU_CUDA(ctx->hB.ensure(sizeof(float) * K * ldb));
-  MMMCU_CUDA(cudaMemcpyAsync(ctx->hA.p, A_host, sizeof(float) * M * lda, cudaMemcpyHostToDevice, ctx->stream));
-  MMMCU_CUDA(cudaMemcpyAsync(ctx->hB.p, B_host, sizeof(float) * K * ldb, cudaMemcpyHostToDevice, ctx->stream));
-  MMMCU_TRY(mmmcu_preprocess(ctx, ctx->hA.as<float>(), M, K, lda, ctx->hB.as<float>(), N, ldb, lane, av, bv));
-  MMMCU_CUDA(cudaStreamSynchronize(ctx->stream));  // the host buffers may change after return
+  if (!A_host || !B_host || !C_host) return fail(ctx, MMMCU_ERR_INVALID_ARG, "null operand");
+  if (dt != MMMCU_F32 && dt != MMMCU_F64) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "unknown dtype");
+  const size_t es = dt_size(dt);
+  MMMCU_CUDA(ctx->hA.ensure(es * M * lda));
+  MMMCU_CUDA(ctx->hB.ensure(es * K * ldb));
+  MMMCU_CUDA(ctx->hC.ensure(es * M * ldc));
+  MMMCU_CUDA(cudaMemcpyAsync(ctx->hA.p, A_host, es * M * lda, cudaMemcpyHostToDevice, ctx->stream));
+  MMMCU_CUDA(cudaMemcpyAsync(ctx->hB.p, B_host, es * K * ldb, cudaMemcpyHostToDevice, ctx->stream));
+  MMMCU_CUDA(cudaMemcpyAsync(ctx->hC.p, C_host, es * M * ldc, cudaMemcpyHostToDevice, ctx->stream));
+  MMMCU_TRY(mmmcu_multiply_simple_t(ctx, dt, ctx->hC.p, ldc, ctx->hA.p, lda, ctx->hB.p, ldb, M, K, N));
+  MMMCU_CUDA(cudaMemcpyAsync(C_host, ctx->hC.p, es * M * ldc, cudaMemcpyDeviceToHost, ctx->stream));
+  MMMCU_CUDA(cudaStreamSynchronize(ctx->stream));
   return MMMCU_OK;
 }
 
 mmmcu_status mmmcu_multiply_planned_host(mmmcu_ctx* ctx, float* C_host, int64_t ldc, uint64_t av, uint64_t bv,
                                          int worker_count, mmmcu_counters* counters) {
-  MMMCU_TRY(bind(ctx));
-  if (worker_count <= 0) return fail(ctx, MMMCU_ERR_WORKERS, "worker_count must be positive");
-  if (!C_host) return fail(ctx, MMMCU_ERR_INVALID_ARG, "C is null");
-  if (!ctx->has_a || !ctx->has_b || ctx->A != ctx->hA.as<float>() || ctx->B != ctx->hB.as<float>())
-    return fail(ctx, MMMCU_ERR_NOT_READY, "no host-operand plan: call mmmcu_preprocess_host first");
-  if (av != ctx->av || bv != ctx->bv)
-    return fail(ctx, MMMCU_ERR_STALE, "stale context: operands changed since preprocessing (Matrix::version)");
-  const int64_t M = ctx->M;
-  MMMCU_CUDA(ctx->hC.ensure(sizeof(float) * M * ldc));
-  MMMCU_CUDA(cudaMemcpyAsync(ctx->hC.p, C_host, sizeof(float) * M * ldc, cudaMemcpyHostToDevice, ctx->stream));
-  MMMCU_TRY(mmmcu_multiply(ctx, ctx->hC.as<float>(), ldc, ctx->A, ctx->B, av, bv, nullptr));
-  MMMCU_CUDA(cudaMemcpyAsync(C_host, ctx->hC.p, sizeof(float) * M * ldc, cudaMemcpyDeviceToHost, ctx->stream));
-  MMMCU_CUDA(cudaStreamSynchronize(ctx->stream));
-  return fill_counters(ctx, counters);
+  return mmmcu_multiply_planned_host_t(ctx, MMMCU_F32, C_host, ldc, av, bv, worker_count, counters);
 }
 
 mmmcu_status mmmcu_generate(mmmcu_ctx* ctx, float* out, int64_t rows, int64_t cols, int64_t ld, int64_t row0, uint64_t seed,
@@ -1153,6 +1419,95 @@ mmmcu_status mmmcu_shard_rows(int64_t M, int world, int rank, int64_t* row0, int
     return fail(nullptr, MMMCU_ERR_INVALID_ARG, "bad shard arguments");
   *row0 = M * rank / world;
   *row1 = M * (rank + 1) / world;
+  return MMMCU_OK;
+}
+
+
+// ---------------------------------------------------- every (dtype, lane config) (kgen.cuh)
+mmmcu_status mmmcu_validate_lane_t(mmmcu_ctx* ctx, mmmcu_dtype dt, mmmcu_lane lane) {
+  return validate_lane(ctx, lane, dt);
+}
+
+mmmcu_status mmmcu_preprocess_a_t(mmmcu_ctx* ctx, mmmcu_dtype dt, const void* A, int64_t M, int64_t K, int64_t lda,
+                                  uint64_t av) {
+  MMMCU_TRY(bind(ctx));
+  if (dt == MMMCU_F32) return mmmcu_preprocess_a(ctx, static_cast<const float*>(A), M, K, lda, av);
+  if (dt != MMMCU_F64) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "unknown dtype");
+  return gen_preprocess_a(ctx, static_cast<const double*>(A), M, K, lda, av, dt);
+}
+
+mmmcu_status mmmcu_preprocess_b_t(mmmcu_ctx* ctx, mmmcu_dtype dt, const void* B, int64_t K, int64_t N, int64_t ldb,
+                                  mmmcu_lane lane, uint64_t bv) {
+  MMMCU_TRY(bind(ctx));
+  MMMCU_TRY(validate_lane(ctx, lane, dt));
+  if (dt == MMMCU_F32) return mmmcu_preprocess_b(ctx, static_cast<const float*>(B), K, N, ldb, lane, bv);
+  return gen_preprocess_b(ctx, static_cast<const double*>(B), K, N, ldb, lane, bv, dt);
+}
+
+mmmcu_status mmmcu_preprocess_t(mmmcu_ctx* ctx, mmmcu_dtype dt, const void* A, int64_t M, int64_t K, int64_t lda,
+                                const void* B, int64_t N, int64_t ldb, mmmcu_lane lane, uint64_t av, uint64_t bv) {
+  MMMCU_TRY(bind(ctx));
+  MMMCU_TRY(validate_lane(ctx, lane, dt));
+  if (dt == MMMCU_F32)
+    return mmmcu_preprocess(ctx, static_cast<const float*>(A), M, K, lda, static_cast<const float*>(B), N, ldb, lane,
+                            av, bv);
+  MMMCU_TRY(gen_preprocess_a(ctx, static_cast<const double*>(A), M, K, lda, av, dt));
+  return gen_preprocess_b(ctx, static_cast<const double*>(B), K, N, ldb, lane, bv, dt);
+}
+
+mmmcu_status mmmcu_multiply_t(mmmcu_ctx* ctx, mmmcu_dtype dt, void* C, int64_t ldc, const void* A, const void* B,
+                              uint64_t av, uint64_t bv, mmmcu_counters* counters) {
+  MMMCU_TRY(bind(ctx));
+  if (dt != MMMCU_F32 && dt != MMMCU_F64) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "unknown dtype");
+  if (!(ctx->gen_a || ctx->gen_b)) {
+    if (dt != MMMCU_F32) return fail(ctx, MMMCU_ERR_NOT_READY, "no f64 plan: preprocess with mmmcu_preprocess_t");
+    return mmmcu_multiply(ctx, static_cast<float*>(C), ldc, static_cast<const float*>(A),
+                          static_cast<const float*>(B), av, bv, counters);
+  }
+  if (!ctx->has_a || !ctx->has_b)
+    return fail(ctx, MMMCU_ERR_NOT_READY, "multiply called before preprocess_a/preprocess_b");
+  if (ctx->a_dt != dt || ctx->b_dt != dt)
+    return fail(ctx, MMMCU_ERR_INVALID_ARG, "operand dtype differs from the preprocessed plan's");
+  if (ctx->Ka != ctx->Kb)
+    return fail(ctx, MMMCU_ERR_DIM_MISMATCH, "a.cols != b.rows (" + std::to_string(ctx->Ka) + " vs " +
+                                                  std::to_string(ctx->Kb) + ")");
+  if (A != plan_a(ctx) || B != plan_b(ctx) || av != ctx->av || bv != ctx->bv)
+    return fail(ctx, MMMCU_ERR_STALE, "stale context: operands differ from the preprocessed ones");
+  if (!C) return fail(ctx, MMMCU_ERR_INVALID_ARG, "C is null");
+  if (ldc < ctx->ldb)
+    return fail(ctx, MMMCU_ERR_INVALID_ARG, "C needs ldc >= the padded width of B (the regions cover the padding)");
+  if (!ctx->gen_b) return fail(ctx, MMMCU_ERR_NOT_READY, "B plan missing for the general path");
+  if (dt == MMMCU_F64)
+    MMMCU_TRY(gen_multiply(ctx, static_cast<double*>(C), ldc, static_cast<const double*>(A)));
+  else
+    MMMCU_TRY(gen_multiply(ctx, static_cast<float*>(C), ldc, static_cast<const float*>(A)));
+  ctx->last_algo = MMMCU_ALGO_SIMT_BCAST;
+  return gen_counters(ctx, counters);
+}
+
+mmmcu_status mmmcu_multiply_simple_t(mmmcu_ctx* ctx, mmmcu_dtype dt, void* C, int64_t ldc, const void* A, int64_t lda,
+                                     const void* B, int64_t ldb, int64_t M, int64_t K, int64_t N) {
+  MMMCU_TRY(bind(ctx));
+  if (dt == MMMCU_F32)
+    return mmmcu_multiply_simple(ctx, static_cast<float*>(C), ldc, static_cast<const float*>(A), lda,
+                                 static_cast<const float*>(B), ldb, M, K, N);
+  if (dt != MMMCU_F64) return fail(ctx, MMMCU_ERR_UNSUPPORTED, "unknown dtype");
+  if (M <= 0 || K <= 0 || N <= 0) return fail(ctx, MMMCU_ERR_INVALID_ARG, "matrix dimensions must be positive");
+  if (!A || !B || !C) return fail(ctx, MMMCU_ERR_INVALID_ARG, "null operand");
+  if (lda < K || ldb < N || ldc < N) return fail(ctx, MMMCU_ERR_DIM_MISMATCH, "leading dimension smaller than the row");
+  dim3 grid((unsigned)((N + mmmcu::kKgTile - 1) / mmmcu::kKgTile), (unsigned)((M + mmmcu::kKgTile - 1) / mmmcu::kKgTile));
+  mmmcu::kg_mul<double, true><<<grid, 256, 0, ctx->stream>>>(static_cast<const double*>(A), lda,
+                                                             static_cast<const double*>(B), ldb, static_cast<double*>(C),
+                                                             ldc, M, K, N, nullptr, 1, 1, 1);
+  MMMCU_LAUNCHED();
+  return MMMCU_OK;
+}
+
+mmmcu_status mmmcu_plan_info(mmmcu_ctx* ctx, mmmcu_dtype* dt, mmmcu_lane* lane) {
+  if (!ctx) return fail(nullptr, MMMCU_ERR_INVALID_ARG, "null context");
+  if (!ctx->has_b) return fail(ctx, MMMCU_ERR_NOT_READY, "no B plan");
+  if (dt) *dt = ctx->b_dt;
+  if (lane) *lane = ctx->gen_b ? mmmcu_lane{ctx->gen_G, ctx->gen_P, 1} : mmmcu_lane{8, 8, 1};
   return MMMCU_OK;
 }
 

@@ -119,6 +119,66 @@ int main() {
   for (int64_t i = 0; i < M; ++i)
     for (int64_t j = 0; j < N; ++j) CHECK(c3.at(i, j) == ref.at(i, j));
 
+  // f64 (Dtype::f64, default lane {4, 8, 1}) and an f32 non-default lane ({2, 16, 2}: G = 4,
+  // P = 16, two-part KernelTable): the reference's per-group fma chain, bit-identical
+  {
+    auto masked_ref = [](const auto& A, const auto& B, auto& C, int64_t G, uint64_t& lane_ops) {
+      for (int64_t i = 0; i < A.rows(); ++i)
+        for (int64_t k = 0; k < A.cols(); ++k) {
+          const auto av = A.at(i, k);
+          if (av == 0) continue;
+          for (int64_t g = 0; g < B.padded_cols(); g += G) {
+            bool nz = false;
+            for (int64_t l = 0; l < G; ++l) nz |= B.row(k)[g + l] != 0;
+            if (!nz) continue;
+            lane_ops += G;
+            for (int64_t l = 0; l < G && g + l < B.cols(); ++l)
+              C.row(i)[g + l] = std::fma(av, B.row(k)[g + l], C.row(i)[g + l]);
+          }
+        }
+    };
+    const LaneConfig l64 = LaneConfig::defaults(Dtype::f64);
+    Matrix<double> a64 = generate<double>(130, 200, SparsitySpec{Structure::random, 0.7, 0, 21}, l64);
+    Matrix<double> b64 = generate<double>(200, 150, SparsitySpec{Structure::block_random, 0.6, 0, 22}, l64);
+    Matrix<double> r64(130, 150, l64);
+    uint64_t ops64 = 0;
+    masked_ref(a64, b64, r64, 4, ops64);
+    MmmContext<double> c64ctx(a64, b64, l64);
+    Matrix<double> c64(130, 150, l64);
+    WorkCounters w64 = multiply_mmm(c64ctx, c64, a64, b64);
+    CHECK(w64.lane_fma_ops == ops64);
+    for (int64_t i = 0; i < 130; ++i)
+      for (int64_t j = 0; j < 150; ++j) CHECK(c64.at(i, j) == r64.at(i, j));
+    CHECK(c64.padding_is_zero());
+    std::vector<BPlan> p64 = preprocess_b(b64, l64, 256);
+    CHECK(plan_stats(p64).region_count == 200 * (b64.padded_cols() / 32));
+    Matrix<double> s64(130, 150, l64), sr(130, 150, l64);
+    multiply_simple(s64, a64, b64);
+    for (int64_t i = 0; i < 130; ++i)
+      for (int64_t k = 0; k < 200; ++k)
+        for (int64_t j = 0; j < 150; ++j) sr.row(i)[j] = std::fma(a64.at(i, k), b64.at(k, j), sr.row(i)[j]);
+    for (int64_t i = 0; i < 130; ++i)
+      for (int64_t j = 0; j < 150; ++j) CHECK(s64.at(i, j) == sr.at(i, j));
+
+    const LaneConfig l16{2, 16, 2};
+    Matrix<float> a16 = generate<float>(90, 120, SparsitySpec{Structure::random, 0.6, 0, 31}, l16);
+    Matrix<float> b16 = generate<float>(120, 200, SparsitySpec{Structure::block_random, 0.5, 0, 32}, l16);
+    Matrix<float> r16(90, 200, l16);
+    uint64_t ops16 = 0;
+    masked_ref(a16, b16, r16, 4, ops16);
+    MmmContext<float> c16ctx(a16, b16, l16);
+    Matrix<float> c16(90, 200, l16);
+    WorkCounters w16 = multiply_mmm(c16ctx, c16, a16, b16);
+    CHECK(w16.lane_fma_ops == ops16);
+    for (int64_t i = 0; i < 90; ++i)
+      for (int64_t j = 0; j < 200; ++j) CHECK(c16.at(i, j) == r16.at(i, j));
+    std::vector<BPlan> p16 = preprocess_b(b16, l16, 256);
+    bool wide_code = false;
+    for (const BPlan& p : p16)
+      for (uint16_t code : p.codes) wide_code |= code > 0xFF;  // P = 16 codes exceed a byte
+    CHECK(wide_code);
+  }
+
   std::printf("DROPIN OK lane_fma_ops=%llu\n", (unsigned long long)w.lane_fma_ops);
   return 0;
 }

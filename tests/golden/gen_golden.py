@@ -84,6 +84,64 @@ def main():
     fx["mm_counters"] = np.array([cnt["kernel_invocations"], cnt["lane_fma_ops"], cnt["rows_skipped"],
                                   cnt["regions_skipped_by_zero_code"]], dtype=np.uint64)
 
+    # ---- other lanes and f64: KernelTable<float> for every compiled
+    # group width, KernelTable<double> at the f64 default lane, and the SPEC multiply over
+    # them (ref_driver.cpp multiply_lane) on small cases
+    for (w, p, v) in ((1, 8, 1), (2, 8, 1), (4, 8, 1), (4, 4, 4), (8, 2, 4), (32, 8, 2), (2, 16, 2)):
+        G, R = w * v, w * p * v
+        n_codes = 1 << p
+        codes = np.arange(n_codes) if p <= 8 else np.unique(
+            np.concatenate([[0, n_codes - 1], rng.integers(0, n_codes, 200)]))
+        c0 = rng.uniform(-2, 2, R).astype(np.float32)
+        b = rng.uniform(-2, 2, R).astype(np.float32)
+        b[rng.random(R) < 0.3] = 0.0
+        a = np.float32(rng.uniform(-2, 2))
+        outs = []
+        for code in codes:
+            st, c = o.ref_kernel_apply(int(code), c0, a, b, lane=(w, p, v))
+            assert st == 0
+            outs.append(c)
+        tag = f"ktl_{w}_{p}_{v}"
+        fx[tag + "_codes"] = codes.astype(np.uint32)
+        fx[tag + "_c0"], fx[tag + "_b"], fx[tag + "_a"] = c0, b, np.array([a], dtype=np.float32)
+        fx[tag + "_out"] = np.stack(outs)
+    for (w, p, v) in ((4, 8, 1), (2, 16, 1), (8, 8, 1)):
+        R = w * p * v
+        c0 = rng.uniform(-2, 2, R)
+        b = rng.uniform(-2, 2, R) / 3.0  # full f64 mantissas
+        a = rng.uniform(-2, 2) / 7.0
+        codes = np.unique(np.concatenate([[0, (1 << p) - 1], rng.integers(0, 1 << p, 100)]))
+        outs = []
+        for code in codes:
+            st, c = o.ref_kernel_apply_f64(int(code), c0, a, b, lane=(w, p, v))
+            assert st == 0
+            outs.append(c)
+        tag = f"kt64_{w}_{p}_{v}"
+        fx[tag + "_codes"] = codes.astype(np.uint32)
+        fx[tag + "_c0"], fx[tag + "_b"], fx[tag + "_a"] = c0, b, np.array([a])
+        fx[tag + "_out"] = np.stack(outs)
+    mm_cases = [("f32", (4, 4, 4), 70, 150, 130), ("f32", (2, 16, 2), 40, 100, 200), ("f32", (1, 8, 1), 33, 70, 50),
+                ("f64", (4, 8, 1), 64, 130, 100), ("f64", (8, 8, 1), 48, 96, 128), ("f64", (2, 4, 1), 30, 50, 41)]
+    for t, (dt, lane, M, K, N) in enumerate(mm_cases):
+        R = lane[0] * lane[1] * lane[2]
+        ldb = (N + R - 1) // R * R
+        A = o.gen_iid(M, K, seed=300 + t, mask_kind=1, p=0.7).astype(np.float64 if dt == "f64" else np.float32)
+        B = o.gen_iid(K, N, seed=400 + t, mask_kind=2, p=0.6, block=max(1, lane[0] * lane[2]), ld=ldb)
+        B = B.astype(np.float64 if dt == "f64" else np.float32)
+        if dt == "f64":
+            A = A / 3.0
+            B = B / 7.0
+        C = np.zeros((M, ldb), dtype=A.dtype)
+        C[:, :N] = o.gen_iid(M, N, seed=500 + t).astype(A.dtype)
+        C0 = C.copy()
+        cnt = o.ref_multiply_lane(C, A, B, lane)
+        tag = f"mml{t}"
+        fx[tag + "_meta"] = np.array([1 if dt == "f64" else 0, *lane, M, K, N], dtype=np.int64)
+        fx[tag + "_A"], fx[tag + "_B"], fx[tag + "_C0"], fx[tag + "_C"] = A, B, C0, C
+        fx[tag + "_counters"] = np.array([cnt["kernel_invocations"], cnt["lane_fma_ops"], cnt["rows_skipped"],
+                                          cnt["regions_skipped_by_zero_code"]], dtype=np.uint64)
+    fx["mml_n"] = np.array([len(mm_cases)])
+
     # ---- MMMB bytes written by the reference writer
     path = os.path.join("/tmp", "golden_mmmb.bin")
     M4 = np.eye(4, dtype=np.float32) * np.float32(1.5)

@@ -61,8 +61,14 @@ def test_lane_validation_matches_reference():
     assert lib.mmmcu_validate_lane(None, N.Lane(3, 8, 1)) == N.ERR_INVALID_ARG
     assert b"unsupported lane configuration: group width 3 for f32" in lib.mmmcu_last_error(None)
     assert lib.mmmcu_validate_lane(None, N.Lane(8, 8, 0)) == N.ERR_INVALID_ARG
-    assert lib.mmmcu_validate_lane(None, N.Lane(4, 8, 1)) == N.ERR_UNSUPPORTED  # valid, no GPU kernel
-    assert lib.mmmcu_validate_lane(None, N.Lane(8, 8, 1)) == N.OK
+    # every valid lane config has a GPU path (the lane-general kernels, kgen.cuh)
+    for lane in ((4, 8, 1), (1, 16, 1), (2, 8, 4), (64, 1, 1), (8, 8, 1)):
+        assert lib.mmmcu_validate_lane(None, N.Lane(*lane)) == N.OK, lane
+    # KernelTable<double>::build (kernel_table.cpp:69-72 with dtype_name f64)
+    assert lib.mmmcu_validate_lane_t(None, N.F64, N.Lane(3, 8, 1)) == N.ERR_INVALID_ARG
+    assert b"unsupported lane configuration: group width 3 for f64" in lib.mmmcu_last_error(None)
+    assert lib.mmmcu_validate_lane_t(None, N.F64, N.Lane(4, 8, 1)) == N.OK
+    assert lib.mmmcu_validate_lane_t(None, 7, N.Lane(4, 8, 1)) == N.ERR_UNSUPPORTED  # no such dtype
 
 
 @pytest.mark.parametrize("M,world", [(32768, 1), (32768, 2), (32768, 8), (1000, 3), (7, 8)])

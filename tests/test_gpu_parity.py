@@ -341,12 +341,13 @@ def test_stale_and_errors(ctx):
     cnt1 = mmm.multiply_parallel(ctx, c, a, b, 8)
     assert cnt1.lane_fma_ops == ctx.planned_counters().lane_fma_ops
     other = mmm.MmmContext(0, lane=mmm.LaneConfig(4, 8, 1))
-    with pytest.raises(mmm.UnsupportedError):
-        other.preprocess(a, b)
+    other.preprocess(a, b)  # a non-default lane runs the lane-general kernels (tests/test_gpu_lanes.py)
     with pytest.raises(mmm.DimensionMismatchError):
         ctx.preprocess(a, dev(np.zeros((64, 128), np.float32)))
-    with pytest.raises(mmm.UnsupportedError):
+    with pytest.raises(ValueError):  # mixed dtypes
         ctx.preprocess(a.double(), b)
+    with pytest.raises(mmm.UnsupportedError):  # no GPU kernel for half precision
+        ctx.preprocess(a.half(), b.half())
 
 
 def test_split_preprocess_paths(ctx):
