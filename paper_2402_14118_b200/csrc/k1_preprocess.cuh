@@ -390,6 +390,9 @@ struct K1Args {
 // Tiles are handed out dynamically (atomic counter): the producer takes the next tile when
 // it starts issuing its groups and tags every stage with the tile, so the compute warps
 // follow the same sequence; a CTA that runs fast takes more tiles (no static tail).
+#ifndef K1_STATIC_EIGHTHS
+#define K1_STATIC_EIGHTHS 7  // eighths of the tiles dealt statically (the rest by an atomic counter)
+#endif
 struct K1Cursor {
   const K1Args* g;
   const K1Scratch* z;
@@ -402,7 +405,7 @@ struct K1Cursor {
   // contended counter on every tile
   __device__ int64_t grab() {
     const int64_t total = g->nA + g->nB;
-    const int64_t per = (total * 7 / 8) / gridDim.x;  // static tiles per CTA
+    const int64_t per = (total * K1_STATIC_EIGHTHS / 8) / gridDim.x;  // static tiles per CTA
     if (n_static < per) return blockIdx.x + (n_static++) * (int64_t)gridDim.x;
     return per * (int64_t)gridDim.x + (int64_t)atomicAdd(z->next_tile, 1u);
   }
@@ -935,7 +938,18 @@ __device__ __forceinline__ void k1_csr_cta(const CsrArgs& g, int64_t cta, void* 
         for (; word; word &= word - 1u) buf[pos++] = (uint16_t)(col0 + (uint32_t)__ffs(word) - 1u);
         __syncwarp();
         uint16_t* dst = static_cast<uint16_t*>(g.cols) + out;
-        for (uint32_t i = lane; i < total; i += 32) dst[i] = buf[i];
+        // 16-byte stores of 8 indices once dst is 16-byte aligned (2-byte stores left the L2
+        // with partial-sector writes)
+        const uint32_t head = min(total, (uint32_t)((8u - (uint32_t)((out) & 7)) & 7u));
+        if (lane < head) dst[lane] = buf[lane];
+        for (uint32_t i = head + 8 * lane; i + 8 <= total; i += 256) {
+          uint32_t w[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) w[q] = (uint32_t)buf[i + 2 * q] | ((uint32_t)buf[i + 2 * q + 1] << 16);
+          *reinterpret_cast<uint4*>(dst + i) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        const uint32_t tail0 = head + ((total - head) & ~7u);
+        if (tail0 + lane < total && total > head) dst[tail0 + lane] = buf[tail0 + lane];
       } else {
         uint32_t* buf = reinterpret_cast<uint32_t*>(stage) + warp * 1024;
         for (; word; word &= word - 1u) buf[pos++] = col0 + (uint32_t)__ffs(word) - 1u;

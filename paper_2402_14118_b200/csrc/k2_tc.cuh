@@ -33,15 +33,21 @@
 //     error that grows with the MMAs accumulated into one D (measured worst 6.7e-6 *
 //     Σ|a||b| with 512 tf32 steps, 0.9e-6 with 64).  So k is cut into segments of 64 MMA
 //     steps (1024 k fp16, 512 k tf32); after each, the accumulator warps add D (unscaled by
-//     2^-(sA+sB) for fp16) into the tile's fp32 partial P in TMEM with round-to-nearest adds
-//     (`seg_full` -> `seg_empty`; the MMAs of the next segment wait for the drain).  At the
-//     end C += P by bulk reduce-adds from shared memory (the L2 does the fp32 adds).
+//     2^-(sA+sB) for fp16) into the tile's fp32 partial P with round-to-nearest adds.  D is
+//     DOUBLE-BUFFERED in TMEM (segment G accumulates into D[G % 2]) and P lives in the
+//     accumulator threads' registers (thread = tile row, 96 columns each), so the MMAs of the
+//     next segment never wait for a drain (`seg_full[b]` -> `seg_empty[b]` only guards the
+//     reuse of D[b] two segments later; with one D the drains stalled the MMA warp 17% of a
+//     dense cell, TD_PROF).  At the end of the unit C += P by bulk reduce-adds from shared
+//     memory (the L2 does the fp32 adds).
 //
-// Warp roles (608 threads): 0-7 A transform (two groups, alternate stages), 8-11 and 15-18
-// accumulators (two groups, column halves of D / P), 12 and 14 producers (alternate stages),
-// 13 MMA issuer (the pair leader's; the follower's warp 13 idles).  TMEM (512 columns):
-// D [0,192), P [192,384), 4 A slots [384,512) of 32 columns (per MMA step: hi 8 | lo 8
-// columns; fp16 packs 2 k per column, even k in the low half).
+// Warp roles (640 threads = 5 warpgroups): WG0-1 = warps 0-7 A transform (two groups,
+// alternate stages); WG2-3 = warps 8-15 accumulators (column halves of D, P in registers:
+// setmaxnreg.inc to 136); WG4 = warps 16 and 18 producers (alternate stages), 17 the MMA
+// issuer (the pair leader's; the follower's idles), 19 a third producer or idle
+// (setmaxnreg.dec to 48).  TMEM (512 columns): D[0] [0,192), D[1] [192,384), 4 A slots
+// [384,512) of 32 columns (per MMA step: hi 8 | lo 8 columns; fp16 packs 2 k per column, even
+// k in the low half).
 #pragma once
 #include <cuda.h>  // CUtensorMap (the A^T gather descriptor)
 #include <cstdint>
@@ -68,11 +74,19 @@ constexpr int kTdStepFloats = kTdTN * 8 * 2;  // one K1 step image (8 k tf32 or 
 #ifndef TD_NPROD16
 #define TD_NPROD16 2
 #endif
-#ifndef TD_ACC8
-#define TD_ACC8 1  // two accumulator groups (column halves): the segment drain that stalls the MMAs halves
+constexpr int kTdAccGroups = 2;  // accumulator warpgroups (column halves of D and P)
+constexpr int kTdXbuf = 1;       // C-update staging buffers per accumulator warp
+#ifdef TD_NO_SETMAXNREG
+#define TD_SETMAXNREG(op, n)
+#else
+#define TD_SETMAXNREG(op, n) asm volatile("setmaxnreg." op ".sync.aligned.u32 %0;" ::"n"(n))
 #endif
-constexpr int kTdAccGroups = TD_ACC8 ? 2 : 1;
-constexpr int kTdXbuf = TD_ACC8 ? 1 : 2;  // C-update staging buffers per accumulator warp
+constexpr int kTdAccRegs = 136;  // setmaxnreg of the accumulator warpgroups (P: 96 registers)
+constexpr int kTdCtlRegs = 48;   // setmaxnreg of the producer / MMA warpgroup
+constexpr int kTdXfRegs = 80;    // setmaxnreg of the transform warpgroups
+// setmaxnreg moves registers only within the CTA's launch allocation (640 x 96): an inc that
+// the decs do not cover blocks forever (measured: a hang)
+static_assert(256 * kTdXfRegs + 256 * kTdAccRegs + 128 * kTdCtlRegs <= 640 * 96, "warpgroup register budget");
 constexpr int kTdTM = 128;
 #ifndef TD_SLOTS32
 #define TD_SLOTS32 2
@@ -123,12 +137,12 @@ struct TdCfg {
   // reuse) already completed, which the same-parity waiter guarantees iff both are even (odd
   // counts gave false-positive waits: corrupted A slots with 4 / 5, a hang with 2 / 3).
   static_assert(kStages % 2 == 0 && kSlots % 2 == 0, "alternating roles need even ring sizes");
-  // producer warps 12, 14, 15, ...: stage J goes to producer J % kProd
+  // producer warps 16, 18 (, 19): stage J goes to producer J % kProd
   static constexpr int kProd = F16 ? TD_NPROD16 : 2;
   static_assert(kStages % kProd == 0, "each producer must own whole ring slots");
-  // warps 0-7 transform, 8-11 accumulators, 12 and 14.. producers, 13 MMA, then the second
-  // accumulator group (TD_ACC8)
-  static constexpr int kThreads = 32 * (13 + kProd) + 128 * (kTdAccGroups - 1);
+  static_assert(kProd == 2 || kProd == 3, "producers are warps 16, 18 and (optionally) 19");
+  // warps 0-7 transform, 8-15 accumulators, 16 / 18 / 19 producers, 17 MMA
+  static constexpr int kThreads = 640;
 };
 
 template <bool F16>
@@ -140,8 +154,8 @@ struct TdShared {
   uint64_t tma[Cfg::kStages];    // stage data landed (TMA bytes / cp.async arrivals)
   uint64_t empty[Cfg::kStages];  // stage consumed: 4 transform arrivals (one group) + 1 tcgen05.commit
   uint64_t full[Cfg::kSlots];       // A slot written (transform warps; pair: both CTAs')
-  uint64_t seg_full;             // segment's MMAs done (tcgen05.commit)
-  uint64_t seg_empty;            // D drained into P (accumulator warps; pair: both CTAs')
+  uint64_t seg_full[2];          // segment's MMAs into D[b] done (tcgen05.commit)
+  uint64_t seg_empty[2];         // D[b] drained into P (accumulator warps; pair: both CTAs')
   uint32_t tmem_base;
 };
 template <bool F16>
@@ -218,9 +232,11 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
   // pair: rank r of the cluster owns row tile 2p + r of pair tile p; the leader (r = 0) issues
   const uint32_t rank = kPair ? tc::cluster_rank() : 0u;
   const bool leader = rank == 0u;
-  const int64_t unit0 = kPair ? blockIdx.x / 2 : blockIdx.x, nunits = kPair ? gridDim.x / 2 : gridDim.x;
-  const int64_t m_units = kPair ? (m_tiles + 1) / 2 : m_tiles;  // (pair) row tiles per column tile
-  const int64_t ntiles = m_units * n_tiles;
+  // unit indices in 32 bits (< 2^31 units for any operand that fits the device; 32-bit
+  // division in unit_rc, fewer live registers across the role branches)
+  const int unit0 = kPair ? blockIdx.x / 2 : blockIdx.x, nunits = kPair ? gridDim.x / 2 : gridDim.x;
+  const int m_units = (int)(kPair ? (m_tiles + 1) / 2 : m_tiles);  // (pair) row tiles per column tile
+  const int ntiles = m_units * (int)n_tiles;
   // unit order: groups of `grp_rows` row units; within a group, column tile major, so the
   // units running together share both B column tiles and A^T row tiles in L2.  Measured
   // (4096^3): mostly-live cells run best with groups of 4 row units (A^T reuse, 0.32 ->
@@ -228,10 +244,10 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
   int64_t live_sum = 0;
   for (int64_t i = 0; i < n_tiles; ++i) live_sum += tcn[i];
   const bool mostly_live = 4 * live_sum >= 3 * kpad * n_tiles;  // td_dense on the average tile
-  const int64_t grp_rows = mostly_live ? (int64_t)kTdGroup : m_units;
-  auto unit_rc = [&](int64_t t, int64_t& ru, int64_t& tb) {
-    const int64_t gsz = grp_rows * n_tiles, g = t / gsz, w = t % gsz;
-    const int64_t rows_g = min(grp_rows, m_units - g * grp_rows);
+  const int grp_rows = mostly_live ? kTdGroup : m_units;
+  auto unit_rc = [&](int t, int64_t& ru, int64_t& tb) {
+    const int gsz = grp_rows * (int)n_tiles, g = t / gsz, w = t % gsz;
+    const int rows_g = min(grp_rows, m_units - g * grp_rows);
     tb = w / rows_g;
     ru = g * kTdGroup + w % rows_g;
   };
@@ -249,8 +265,10 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       tc::mbar_init(&sh.empty[s], 1 + 4);
     }
     for (int t = 0; t < kTdSlots; ++t) tc::mbar_init(&sh.full[t], kNXform);
-    tc::mbar_init(&sh.seg_full, 1);
-    tc::mbar_init(&sh.seg_empty, kNAccum);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&sh.seg_full[b], 1);
+      tc::mbar_init(&sh.seg_empty[b], kNAccum);
+    }
     tc::fence_mbar_init();
   }
   if (warp == 0) {
@@ -262,9 +280,13 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
   else __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = sh.tmem_base;
-  constexpr uint32_t kPcol = kTdTN, kAcol = 2 * kTdTN;  // TMEM columns of P and of the A slots
-
-  if (warp == 12 || (warp >= 14 && warp < 13 + Cfg::kProd)) {
+  constexpr uint32_t kAcol = 2 * kTdTN;  // TMEM columns: D[0] [0,192), D[1] [192,384), then the A slots
+  // register budget per warpgroup (5 x 128 threads start at 96, setmaxnreg at the top of each
+  // role's branch): the accumulators hold P, the producers / MMA issuer need few
+  if (warp >= 16) {
+  // warpgroup 4: one setmaxnreg for the whole warpgroup, then its warps' roles
+  TD_SETMAXNREG("dec", kTdCtlRegs);
+  if (warp == 16 || warp == 18 || (Cfg::kProd == 3 && warp == 19)) {
     // ---------------------------------------------------- producers (B and A per stage)
     // Two warps, producer p = (warp - 12) / 2 fills the stages J with J % 2 == p (one warp's
     // per-stage instruction chain, ~760 cycles, was longer than the stage's 630 MMA cycles).
@@ -278,9 +300,9 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
     long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const long long p0 = clock64();
 #endif
-    const uint32_t pp = warp == 12 ? 0u : (uint32_t)(warp - 13);  // producer index
+    const uint32_t pp = warp == 16 ? 0u : (uint32_t)(warp - 17);  // producer index
     const uint64_t pol = TD_HINT ? td_policy_evict_last() : 0ull;
-    for (int64_t t = unit0; t < ntiles; t += nunits) {
+    for (int t = unit0; t < ntiles; t += nunits) {
       int64_t ru, tb;
       unit_rc(t, ru, tb);
       const int64_t rt = row_tile(ru);
@@ -374,13 +396,13 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       J += (uint32_t)nstage;
     }
 #ifdef TD_PROF
-    if (lane == 0 && td_prof && warp == 12) {
+    if (lane == 0 && td_prof && warp == 16) {
       unsigned long long* q = td_prof + 16 * blockIdx.x;
       q[8] = prof[0];
       q[9] = clock64() - p0;
     }
 #endif
-  } else if (warp == 13) {
+  } else if (warp == 17) {
     if (!leader) goto td_done;  // pair follower: the leader issues the pair's MMAs
     // ------------------------------------------------------------------ MMA issuer
     // The whole warp runs the loop (warp-uniform operands stay in uniform registers); one
@@ -393,7 +415,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
     long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const long long p0 = clock64();
 #endif
-    for (int64_t t = unit0; t < ntiles; t += nunits) {
+    for (int t = unit0; t < ntiles; t += nunits) {
       int64_t ru, tb;
       unit_rc(t, ru, tb);
       const int nsteps = nsteps_of(tcn[tb]);
@@ -401,7 +423,8 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       for (int j = 0; j < nstage; ++j, ++J) {
         const int st = J % kStages, sl = J % kTdSlots;
         TD_CLK(c0);
-        if (j % kSeg == 0 && G >= 1) tc::mbar_wait(&sh.seg_empty, (G - 1) & 1u);  // D drained
+        // D[G % 2] was drained (segment G - 2) before this segment overwrites it
+        if (j % kSeg == 0 && G >= 2) tc::mbar_wait(&sh.seg_empty[G & 1u], ((G >> 1) - 1) & 1u);
         TD_CLK(c1);
         tc::mbar_wait(&sh.tma[st], (J / kStages) & 1u);
         TD_CLK(c15);
@@ -413,6 +436,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
         tc::fence_after_sync();
         const uint32_t baddr = tc::smem_u32(sh.b[st]);
         const bool seg_end = j % kSeg == kSeg - 1 || j == nstage - 1;
+        const uint32_t dcol = tbase + kTdTN * (G & 1u);  // this segment's D buffer
         if (tc::elect_one()) {
 #pragma unroll
           for (int u = 0; u < kSub; ++u) {
@@ -424,22 +448,22 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
               const uint32_t ahi = tbase + kAcol + 32 * sl + 16 * u, alo = ahi + 8;
               const uint32_t acc0 = (j % kSeg != 0 || u > 0) ? 1u : 0u;
               if (F16) {
-                tc::mma_f16_ts_pair(tbase, alo, bhi, idesc, acc0);
-                tc::mma_f16_ts_pair(tbase, ahi, blo, idesc, 1u);
-                tc::mma_f16_ts_pair(tbase, ahi, bhi, idesc, 1u);
+                tc::mma_f16_ts_pair(dcol, alo, bhi, idesc, acc0);
+                tc::mma_f16_ts_pair(dcol, ahi, blo, idesc, 1u);
+                tc::mma_f16_ts_pair(dcol, ahi, bhi, idesc, 1u);
               } else {
-                tc::mma_tf32_ts(tbase, alo, bhi, idesc, acc0);
-                tc::mma_tf32_ts(tbase, ahi, blo, idesc, 1u);
-                tc::mma_tf32_ts(tbase, ahi, bhi, idesc, 1u);
+                tc::mma_tf32_ts(dcol, alo, bhi, idesc, acc0);
+                tc::mma_tf32_ts(dcol, ahi, blo, idesc, 1u);
+                tc::mma_tf32_ts(dcol, ahi, bhi, idesc, 1u);
               }
             }
           }
           if (kPair) {
             tc::mma_commit_pair(&sh.empty[st]);
-            if (seg_end) tc::mma_commit_pair(&sh.seg_full);
+            if (seg_end) tc::mma_commit_pair(&sh.seg_full[G & 1u]);
           } else {
             tc::mma_commit(&sh.empty[st]);
-            if (seg_end) tc::mma_commit(&sh.seg_full);
+            if (seg_end) tc::mma_commit(&sh.seg_full[G & 1u]);
           }
         }
         __syncwarp();
@@ -456,7 +480,9 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       q[10] = prof[3];
     }
 #endif
+  }  // (warp 19 with two producers: idle)
   } else if (warp < 8) {
+    TD_SETMAXNREG("dec", kTdXfRegs);
     // ---------------------------------------------------------------- A transform
     // Two groups of 4 warps; group g = w/4 transforms the stages J with J % 2 == g, warp w
     // owning tile rows 32*(w%4) .. +31 (its TMEM lanes), so two stages' chains of barrier
@@ -474,7 +500,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
     long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const long long p0 = clock64();
 #endif
-    for (int64_t t = unit0; t < ntiles; t += nunits) {
+    for (int t = unit0; t < ntiles; t += nunits) {
       int64_t ru, tb;
       unit_rc(t, ru, tb);
       const int32_t total = tcn[tb];
@@ -538,24 +564,25 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       q[7] = prof[2];
     }
 #endif
-  } else {
-    // ------------------------------------------------------- accumulator warps 8..11 (+ 15..18)
-    // Thread = tile row r = 32*(w%4) + lane (its TMEM lane).  Per segment: D (fp16: times
-    // 2^-(sA+sB), exact) is added into the partial P in TMEM (round-to-nearest; P = D for
-    // the first segment), 32 columns per tcgen05.ld, then the MMA issuer may start the next
-    // segment.  After the tile's last segment: C += P by bulk reduce-adds
-    // (cp.reduce.async.bulk .add.f32, the L2 performs the fp32 adds, one writer per element):
-    // each thread stages 32 columns of its row in shared memory (double-buffered) and issues
-    // one 128-byte reduce for it, so the warps are free for the next tile's first drain
-    // almost at once (a load-add-store C update held that drain, and with it the MMAs, for
-    // ~25 us per tile).
+  } else if (warp < 16) {
+    TD_SETMAXNREG("inc", kTdAccRegs);
+    // ------------------------------------------------------- accumulator warps 8..15
+    // Thread = tile row r = 32*(w%4) + lane (its TMEM lane); warpgroup ag = columns
+    // [96 ag, 96 ag + 96) of the tile.  Per segment G: wait for D[G % 2], add it (fp16: times
+    // 2^-(sA+sB), exact) into the row's partial P in REGISTERS with round-to-nearest adds
+    // (P = D for the unit's first segment), 16 columns per tcgen05.ld, then release D[G % 2]
+    // (its MMAs two segments later may start).  After the unit's last segment: C += P by
+    // bulk reduce-adds (cp.reduce.async.bulk .add.f32, the L2 performs the fp32 adds, one
+    // writer per element): each thread stages 32 columns of its row in shared memory and
+    // issues one 128-byte reduce for it.
     const int q4 = warp & 3;
-    const int ag = warp >= 13 + Cfg::kProd ? 1 : 0;  // accumulator group: columns [96 ag, 96 ag + 96)
-    constexpr int kCh = kTdTN / 32 / kTdAccGroups;   // 32-column chunks per group
+    const int ag = (warp >> 2) & 1;                  // accumulator group: columns [96 ag, 96 ag + 96)
+    constexpr int kCh = kTdTN / 32 / kTdAccGroups;   // 32-column chunks per group (3)
     const int c0 = ag * kCh;
     const uint32_t taddr = tbase + ((uint32_t)(q4 * 32) << 16);
+    float P[kCh * 32];
     uint32_t G = 0, R = 0;  // segments drained, C chunks reduced
-    for (int64_t t = unit0; t < ntiles; t += nunits) {
+    for (int t = unit0; t < ntiles; t += nunits) {
       int64_t ru, tb;
       unit_rc(t, ru, tb);
       const int64_t rt = row_tile(ru);
@@ -566,56 +593,51 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       // fp16: undo this row's scale 2^sA and each 8-column group's 2^sB (exact powers of two)
       const int64_t grow = rt * kTdTM + 32 * q4 + lane;
       const float ia = F16 ? tc::exp2_int(-tc::f16_scale_exp(grow < M ? (uint32_t)(__ldg(rrng + grow) >> 32) : 0u)) : 1.0f;
+      // lane q < 12 holds the unscale of 8-column group q of this group's 96 columns (read by
+      // shuffles in the drain: 12 fewer live registers beside P)
+      float ibl = 1.0f;
+      if (F16 && lane < kCh * 4) {
+        const int64_t gc = tb * kTdTN + 32 * c0 + 8 * lane;
+        ibl = tc::exp2_int(-tc::f16_scale_exp(gc < N ? (uint32_t)(__ldg(grng + (gc >> 3)) >> 32) : 0u));
+      }
       for (int g = 0; g < nseg; ++g, ++G) {
-        if (TD_ACC_SLEEP > 0) tc::mbar_wait_sleep_ns(&sh.seg_full, G & 1u, TD_ACC_SLEEP);
-        else tc::mbar_wait(&sh.seg_full, G & 1u);
+        const uint32_t b = G & 1u;
+        if (TD_ACC_SLEEP > 0) tc::mbar_wait_sleep_ns(&sh.seg_full[b], (G >> 1) & 1u, TD_ACC_SLEEP);
+        else tc::mbar_wait(&sh.seg_full[b], (G >> 1) & 1u);
         tc::fence_after_sync();
-#pragma unroll 1
-        for (int c = c0; c < c0 + kCh; ++c) {
-          uint32_t d[32], p[32];
-          tc::tmem_ld32(taddr + 32 * c, d);
-          if (g > 0) tc::tmem_ld32(taddr + kPcol + 32 * c, p);
-          float ib[4];
+        const bool first = g == 0;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int64_t gc = tb * kTdTN + 32 * c + 8 * q;  // 8-column group of this chunk
-            ib[q] = F16 ? tc::exp2_int(-tc::f16_scale_exp(gc < N ? (uint32_t)(__ldg(grng + (gc >> 3)) >> 32) : 0u)) : 1.0f;
-          }
+        for (int h = 0; h < 2 * kCh; ++h) {  // 16-column pieces
+          uint32_t d[16];
+          tc::tmem_ld16(taddr + kTdTN * b + 32 * c0 + 16 * h, d);
           tc::tmem_ld_wait();
+          const float s0 = __shfl_sync(0xffffffffu, ibl, 2 * h), s1 = __shfl_sync(0xffffffffu, ibl, 2 * h + 1);
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
+          for (int e = 0; e < 16; ++e) {
             float x = __uint_as_float(d[e]);
             if (F16) x *= ia;  // exact (power of two)
+            const float s = e < 8 ? s0 : s1;
             // p + x*ib in one rounding (x*ib exact): the same value as the add of the product
-            x = g > 0 ? fmaf(x, ib[e >> 3], __uint_as_float(p[e])) : x * ib[e >> 3];
-            d[e] = __float_as_uint(x);
+            P[16 * h + e] = first ? x * s : fmaf(x, s, P[16 * h + e]);
           }
-          tc::tmem_st32(taddr + kPcol + 32 * c, d);
         }
-        tc::tmem_st_wait();
         tc::fence_before_sync();
         __syncwarp();
-        if (lane == 0) signal_issuer(&sh.seg_empty);
+        if (lane == 0) signal_issuer(&sh.seg_empty[b]);
       }
       // C += P: row m0 + lane of this warp, 32 columns per bulk reduce
       const int64_t row = rt * kTdTM + 32 * q4 + lane, n0 = tb * kTdTN;
-      tc::fence_after_sync();
-#pragma unroll 1
-      for (int c = c0; c < c0 + kCh; ++c, ++R) {
+#pragma unroll
+      for (int c = 0; c < kCh; ++c, ++R) {
         float* buf = &sh.xp[4 * ag + q4][R % kTdXbuf][lane][0];
         // this thread's reduce from the buffer's previous use has read it
-        if (R >= (uint32_t)kTdXbuf) {
-          if (kTdXbuf == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        }
-        uint32_t p[32];
-        tc::tmem_ld32(taddr + kPcol + 32 * c, p);
-        tc::tmem_ld_wait();
+        if (R >= (uint32_t)kTdXbuf) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          *reinterpret_cast<uint4*>(buf + 4 * q) = make_uint4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]);
+          *reinterpret_cast<float4*>(buf + 4 * q) =
+              make_float4(P[32 * c + 4 * q], P[32 * c + 4 * q + 1], P[32 * c + 4 * q + 2], P[32 * c + 4 * q + 3]);
         tc::fence_async_smem();  // generic-proxy stores before the bulk (async-proxy) read
-        const int64_t col = n0 + 32 * c;
+        const int64_t col = n0 + 32 * (c0 + c);
         if (row < M && col < N) {
           const int64_t ncol = N - col < 32 ? ((N - col + 3) & ~int64_t(3)) : 32;  // 16-byte multiple
           asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(
