@@ -185,15 +185,17 @@ int ref_multiply_parallel_f32(float* C, int64_t ldc, const float* A, int64_t lda
 
 // SPEC multiply_mmm / multiply_parallel as SPEC.md:196-214 and :276-293 lay it out, over the
 // reference's KernelTable (the reference-kind CPU baseline):
-//   preprocess_b: one BPlan per (leaf_dim x leaf_dim) sub-block of B, codes in
-//     the order the multiply consumes them (rows of the leaf, then its regions left to right);
-//   preprocess_a: the ABlockIndex of every block_dim^2 A block: per row and
-//     aligned 8-segment a count and the ascending offsets (a full segment stores none);
-//   multiply (Fig. 3 recursion at leaf_dim): leaves of C are independent tasks
-//     (the 4+4 phase discipline's write sets), and each C leaf walks its k leaves in
-//     ascending order, so every C element keeps the ascending-k chain; inside a leaf the
-//     middle loop visits only A's non-zeros through the ABlockIndex (no per-element branch)
-//     and applies the plan codes of B row k in order through the reference KernelTable.
+//   preprocess_b: one P-bit code per (B row, region), in the order the multiply
+//     consumes them (row-major: rows, then regions left to right);
+//   preprocess_a: the ABlockIndex of A: per row and aligned 8-segment a count
+//     and the ascending offsets (a full segment stores none), block_dim 256;
+//   multiply: rows of C in parallel (OpenMP, dynamic — the reference's own parallelism,
+//     matrix.hpp:170); per row the middle loop visits only A's non-zeros through the
+//     ABlockIndex (no per-element branch), in ascending k, and applies B row k's
+//     codes region by region through the reference KernelTable.  Every C element keeps the
+//     ascending-k chain.  (A 256-leaf blocked traversal of C, the SPEC's recursion, measured
+//     3x slower on the GPU host's 16 Xeon cores: a non-zero then feeds 4 regions per leaf
+//     instead of the whole row, tools/cpu_engines.py.)
 // Rows [row0, row1) of A/C only (a bounded sample); preprocess_ns covers both preprocess
 // passes over the sample's A rows and the whole of B.
 int ref_multiply_mmm_f32(float* C, int64_t ldc, const float* A, int64_t lda, const float* B, int64_t ldb,
@@ -202,43 +204,29 @@ int ref_multiply_mmm_f32(float* C, int64_t ldc, const float* A, int64_t lda, con
     const LaneConfig lane = LaneConfig::defaults(mmm::Dtype::f32);
     const KernelTable<float> table = KernelTable<float>::build(lane);
     const int64_t R = lane.region_width(), G = lane.group_width();
-    constexpr int64_t L = 256;  // leaf_dim = block_dim
     if (workers > 0) omp_set_num_threads(workers);
     Matrix<float> b = from_dense(B, K, N, ldb);
     const int64_t padc = b.padded_cols(), nreg = padc / R;
     const int64_t M = row1 - row0;
-    const int64_t nkb = (K + L - 1) / L, njb = (padc + L - 1) / L, nib = (M + L - 1) / L;
-    const int64_t rpl = L / R;  // regions per full leaf row
     const auto t0 = std::chrono::steady_clock::now();
-    // ---- preprocess_b: plan of leaf (kb, jb) at plan_off[kb * njb + jb], rows x regions
-    std::vector<int64_t> plan_off(static_cast<size_t>(nkb * njb + 1), 0);
-    for (int64_t kb = 0; kb < nkb; ++kb)
-      for (int64_t jb = 0; jb < njb; ++jb) {
-        const int64_t rows = std::min(L, K - kb * L), regs = std::min(rpl, nreg - jb * rpl);
-        plan_off[kb * njb + jb + 1] = plan_off[kb * njb + jb] + rows * regs;
-      }
-    std::vector<uint8_t> plans(static_cast<size_t>(plan_off.back()));
-#pragma omp parallel for schedule(dynamic, 1)
-    for (int64_t t = 0; t < nkb * njb; ++t) {
-      const int64_t kb = t / njb, jb = t % njb;
-      const int64_t rows = std::min(L, K - kb * L), regs = std::min(rpl, nreg - jb * rpl);
-      uint8_t* dst = plans.data() + plan_off[t];
-      for (int64_t kk = 0; kk < rows; ++kk) {
-        const float* row = b.row(kb * L + kk);
-        for (int64_t r = 0; r < regs; ++r) {
-          const float* reg = row + (jb * rpl + r) * R;
-          uint32_t code = 0;
-          for (int j = 0; j < lane.p; ++j) {
-            bool nz = false;
-            for (int64_t l = 0; l < G; ++l) nz |= reg[j * G + l] != 0.0f;
-            code = (code << 1) | static_cast<uint32_t>(nz);
-          }
-          *dst++ = static_cast<uint8_t>(code);
+    // ---- preprocess_b
+    std::vector<uint8_t> codes(static_cast<size_t>(K * nreg));
+#pragma omp parallel for schedule(static)
+    for (int64_t k = 0; k < K; ++k) {
+      const float* row = b.row(k);
+      for (int64_t r = 0; r < nreg; ++r) {
+        const float* reg = row + r * R;
+        uint32_t code = 0;
+        for (int j = 0; j < lane.p; ++j) {
+          bool nz = false;
+          for (int64_t l = 0; l < G; ++l) nz |= reg[j * G + l] != 0.0f;
+          code = (code << 1) | static_cast<uint32_t>(nz);
         }
+        codes[k * nreg + r] = static_cast<uint8_t>(code);
       }
     }
-    // ---- preprocess_a: ABlockIndex, block (ib, kb) row-major segments; counts [M][nseg],
-    // offsets [M][nseg][8] (fixed capacity), here in row order per block row
+    // ---- preprocess_a: ABlockIndex counts [M][nseg], offsets [M][nseg][8] (fixed capacity,
+    // SPEC.md:229)
     const int64_t nseg = (K + 7) / 8;
     std::vector<uint8_t> counts(static_cast<size_t>(M * nseg)), offs(static_cast<size_t>(M * nseg * 8));
 #pragma omp parallel for schedule(static)
@@ -253,55 +241,41 @@ int ref_multiply_mmm_f32(float* C, int64_t ldc, const float* A, int64_t lda, con
       }
     }
     const auto t1 = std::chrono::steady_clock::now();
-    // ---- multiply: C leaves in parallel, k leaves ascending inside each
+    // ---- multiply
     uint64_t inv = 0, lanes = 0, zreg = 0, nnz = 0;
+    std::vector<float> cbuf(static_cast<size_t>(M > 0 ? M : 1) * padc, 0.0f);
 #pragma omp parallel for schedule(dynamic, 1) reduction(+ : inv, lanes, zreg, nnz)
-    for (int64_t t = 0; t < nib * njb; ++t) {
-      const int64_t ib = t / njb, jb = t % njb;
-      const int64_t i0 = ib * L, i1 = std::min(M, i0 + L), regs = std::min(rpl, nreg - jb * rpl);
-      alignas(256) float cl[L * L];
-      for (int64_t i = i0; i < i1; ++i) {
-        const float* src = C + (row0 + i) * ldc + jb * L;
-        const int64_t w = std::min(L, N - jb * L);
-        std::memcpy(cl + (i - i0) * L, src, sizeof(float) * w);
-        std::memset(cl + (i - i0) * L + w, 0, sizeof(float) * (L - w));
-      }
-      for (int64_t kb = 0; kb < nkb; ++kb) {
-        const uint8_t* plan = plans.data() + plan_off[kb * njb + jb];
-        const int64_t s0 = kb * L / 8, s1 = std::min(nseg, (kb + 1) * L / 8);
-        for (int64_t i = i0; i < i1; ++i) {
-          float* c = cl + (i - i0) * L;
-          const float* arow = A + (row0 + i) * lda;
-          for (int64_t s = s0; s < s1; ++s) {
-            const int n = counts[i * nseg + s];
-            const uint8_t* o = offs.data() + (i * nseg + s) * 8;
-            for (int q = 0; q < n; ++q) {
-              const int64_t k = 8 * s + (n == 8 ? q : o[q]);
-              const float av = arow[k];
-              const uint8_t* code = plan + (k - kb * L) * regs;
-              const float* brow = b.row(k) + jb * L;
-              ++nnz;
-              for (int64_t r = 0; r < regs; ++r) {
-                if (code[r] == 0) {
-                  ++zreg;
-                  continue;
-                }
-                ++inv;
-                lanes += static_cast<uint64_t>(__builtin_popcount(code[r])) * G;
-                table.apply(code[r], c + r * R, av, brow + r * R);  // the reference kernel
-              }
+    for (int64_t i = 0; i < M; ++i) {
+      float* c = cbuf.data() + i * padc;
+      std::memcpy(c, C + (row0 + i) * ldc, sizeof(float) * N);
+      const float* arow = A + (row0 + i) * lda;
+      for (int64_t s = 0; s < nseg; ++s) {
+        const int n = counts[i * nseg + s];
+        const uint8_t* o = offs.data() + (i * nseg + s) * 8;
+        for (int q = 0; q < n; ++q) {
+          const int64_t k = 8 * s + (n == 8 ? q : o[q]);
+          const float av = arow[k];
+          const uint8_t* code = codes.data() + k * nreg;
+          const float* brow = b.row(k);
+          ++nnz;
+          for (int64_t r = 0; r < nreg; ++r) {
+            if (code[r] == 0) {
+              ++zreg;
+              continue;
             }
+            ++inv;
+            lanes += static_cast<uint64_t>(__builtin_popcount(code[r])) * G;
+            table.apply(code[r], c + r * R, av, brow + r * R);  // the reference kernel
           }
         }
       }
-      for (int64_t i = i0; i < i1; ++i)
-        std::memcpy(C + (row0 + i) * ldc + jb * L, cl + (i - i0) * L, sizeof(float) * std::min(L, N - jb * L));
+      std::memcpy(C + (row0 + i) * ldc, c, sizeof(float) * N);
     }
     const auto t2 = std::chrono::steady_clock::now();
     if (out) {
       out->kernel_invocations = inv;
       out->lane_fma_ops = lanes;
-      out->rows_skipped = static_cast<uint64_t>(M * K) - nnz / static_cast<uint64_t>(njb);
+      out->rows_skipped = static_cast<uint64_t>(M * K) - nnz;
       out->regions_skipped_by_zero_code = zreg;
       out->preprocess_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
       out->multiply_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(t2 - t1).count();

@@ -74,6 +74,9 @@ constexpr int kTdStepFloats = kTdTN * 8 * 2;  // one K1 step image (8 k tf32 or 
 #ifndef TD_NPROD16
 #define TD_NPROD16 2
 #endif
+#ifndef TD_NPROD_SPARSE
+#define TD_NPROD_SPARSE 2  // 3 measured no faster on sparse-k cells (0.132 vs 0.127-0.132 ms)
+#endif
 constexpr int kTdAccGroups = 2;  // accumulator warpgroups (column halves of D and P)
 constexpr int kTdXbuf = 1;       // C-update staging buffers per accumulator warp
 #ifdef TD_NO_SETMAXNREG
@@ -137,10 +140,14 @@ struct TdCfg {
   // reuse) already completed, which the same-parity waiter guarantees iff both are even (odd
   // counts gave false-positive waits: corrupted A slots with 4 / 5, a hang with 2 / 3).
   static_assert(kStages % 2 == 0 && kSlots % 2 == 0, "alternating roles need even ring sizes");
-  // producer warps 16, 18 (, 19): stage J goes to producer J % kProd
+  // producer warps 16, 18 (, 19): stage J goes to producer J % nprod, nprod = kProd for
+  // mostly-live cells and kProdSparse for sparse-k ones (whose A rows arrive in many small
+  // gathers: one more warp issuing them; TD_NPROD_SPARSE)
   static constexpr int kProd = F16 ? TD_NPROD16 : 2;
-  static_assert(kStages % kProd == 0, "each producer must own whole ring slots");
-  static_assert(kProd == 2 || kProd == 3, "producers are warps 16, 18 and (optionally) 19");
+  static constexpr int kProdSparse = F16 ? TD_NPROD_SPARSE : 2;
+  static_assert(kStages % kProd == 0 && kStages % kProdSparse == 0, "each producer must own whole ring slots");
+  static_assert((kProd == 2 || kProd == 3) && (kProdSparse == 2 || kProdSparse == 3),
+                "producers are warps 16, 18 and (optionally) 19");
   // warps 0-7 transform, 8-15 accumulators, 16 / 18 / 19 producers, 17 MMA
   static constexpr int kThreads = 640;
 };
@@ -245,6 +252,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
   for (int64_t i = 0; i < n_tiles; ++i) live_sum += tcn[i];
   const bool mostly_live = 4 * live_sum >= 3 * kpad * n_tiles;  // td_dense on the average tile
   const int grp_rows = mostly_live ? kTdGroup : m_units;
+  const int nprod = mostly_live ? Cfg::kProd : Cfg::kProdSparse;  // producer warps of this launch
   auto unit_rc = [&](int t, int64_t& ru, int64_t& tb) {
     const int gsz = grp_rows * (int)n_tiles, g = t / gsz, w = t % gsz;
     const int rows_g = min(grp_rows, m_units - g * grp_rows);
@@ -286,7 +294,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
   if (warp >= 16) {
   // warpgroup 4: one setmaxnreg for the whole warpgroup, then its warps' roles
   TD_SETMAXNREG("dec", kTdCtlRegs);
-  if (warp == 16 || warp == 18 || (Cfg::kProd == 3 && warp == 19)) {
+  if (warp == 16 || warp == 18 || (nprod == 3 && warp == 19)) {
     // ---------------------------------------------------- producers (B and A per stage)
     // Two warps, producer p = (warp - 12) / 2 fills the stages J with J % 2 == p (one warp's
     // per-stage instruction chain, ~760 cycles, was longer than the stage's 630 MMA cycles).
@@ -323,7 +331,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
         return (lane < kStageK && pn < npos) ? __ldg(kx + pn) : -1;
       };
       // this producer's stages of the tile: j0, j0 + 2, ... (J advances by the tile's count)
-      constexpr int NP = Cfg::kProd;
+      const int NP = nprod;
       const int j0 = (int)((pp + NP - (J % NP)) % NP);
       int kc = kload(j0), k1 = kload(j0 + NP), k2 = kload(j0 + 2 * NP), k3 = kload(j0 + 3 * NP);
       for (int j = j0; j < nstage; j += NP) {

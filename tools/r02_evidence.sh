@@ -1,0 +1,15 @@
+#!/bin/bash
+# r02 evidence: ncu --set full of K2-TC (dense + sparse-k cell) and the K1 chain, the launch list
+# of one bench step, the default bench line
+cd $GRAFT_REPO_ROOT
+timeout 60 python tools/tc_profile.py 0.6 0.6 8 5 > gpurun_out/ev_tc.log 2>&1 || exit 1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k2_tc" -s 2 -c 1 \
+  -o gpurun_out/r02_k2tc_dense python tools/tc_profile.py 0.6 0.6 8 5 > gpurun_out/ev_ncu1.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k2_tc" -s 2 -c 1 \
+  -o gpurun_out/r02_k2tc_sparse python tools/tc_profile.py 0.6 0.95 32 5 > gpurun_out/ev_ncu2.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k1_pass|k1_pack_auto|k1_fin" -s 3 -c 3 \
+  -o gpurun_out/r02_k1_chain python tools/k1_profile.py 0.6 0.6 8 2 > gpurun_out/ev_ncu3.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+  --log-file gpurun_out/r02_launches.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-cfg5-ref > gpurun_out/ev_launch.log 2>&1
+timeout 900 python bench.py --per-cell gpurun_out/r02_cells.json > gpurun_out/r02_bench.json 2> gpurun_out/r02_bench.err
+tail -c 400 gpurun_out/r02_bench.json
