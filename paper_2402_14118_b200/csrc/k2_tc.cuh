@@ -78,7 +78,6 @@ constexpr int kTdStepFloats = kTdTN * 8 * 2;  // one K1 step image (8 k tf32 or 
 #define TD_NPROD_SPARSE 2  // 3 measured no faster on sparse-k cells (0.132 vs 0.127-0.132 ms)
 #endif
 constexpr int kTdAccGroups = 2;  // accumulator warpgroups (column halves of D and P)
-constexpr int kTdXbuf = 1;       // C-update staging buffers per accumulator warp
 #ifdef TD_NO_SETMAXNREG
 #define TD_SETMAXNREG(op, n)
 #else
@@ -117,8 +116,6 @@ constexpr int kTdTM = 128;
                            // (measured: gathers win at ~23 runs per stage, lose at ~9)
 #endif
 constexpr int kTdGroup = TD_GROUP;            // row units per scheduling group (L2 reuse of A^T and B)
-constexpr int kTdXrow = 36;                   // C-update staging row stride (floats): 16-byte aligned rows,
-                                              // conflict-free 16-byte stores by row-owning threads
 
 template <bool F16>
 struct TdCfg {
@@ -155,9 +152,11 @@ struct TdCfg {
 template <bool F16>
 struct TdShared {
   using Cfg = TdCfg<F16>;
+  // per accumulator warp: its 32 rows x 32 columns of P for the C update, the 128-byte-swizzled
+  // box one TMA tensor reduce-add takes (first: the struct is 1024-byte aligned)
+  float xp[4 * kTdAccGroups][32][32];
   float b[Cfg::kStages][Cfg::kBStageFloats];   // B step images (pair: this CTA's half)
   float a[Cfg::kStages][Cfg::kStageK][kTdTM];  // the stage's live A^T rows
-  float xp[4 * kTdAccGroups][kTdXbuf][32][kTdXrow];  // per accumulator warp: C-update staging
   uint64_t tma[Cfg::kStages];    // stage data landed (TMA bytes / cp.async arrivals)
   uint64_t empty[Cfg::kStages];  // stage consumed: 4 transform arrivals (one group) + 1 tcgen05.commit
   uint64_t full[Cfg::kSlots];       // A slot written (transform warps; pair: both CTAs')
@@ -166,7 +165,7 @@ struct TdShared {
   uint32_t tmem_base;
 };
 template <bool F16>
-constexpr int td_smem() { return (int)sizeof(TdShared<F16>) + 128; }
+constexpr int td_smem() { return (int)sizeof(TdShared<F16>) + 1024; }
 
 __device__ __forceinline__ void td_bulk(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -223,7 +222,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       const int32_t* __restrict__ tcn, int64_t maxsteps, float* __restrict__ C, int64_t ldc, int64_t M, int64_t N,
       int64_t m_tiles, int64_t n_tiles, const unsigned long long* __restrict__ sel,
       const unsigned long long* __restrict__ rrng, const unsigned long long* __restrict__ grng,
-      const __grid_constant__ CUtensorMap tmap_at) {
+      const __grid_constant__ CUtensorMap tmap_at, const __grid_constant__ CUtensorMap tmap_c) {
   using Cfg = TdCfg<F16>;
   constexpr int kStages = Cfg::kStages, kSub = Cfg::kSub, kStepK = Cfg::kStepK, kStageK = Cfg::kStageK,
                 kSeg = Cfg::kSeg, kTdSlots = Cfg::kSlots;
@@ -234,7 +233,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
   // (sel is read by both CTAs of a pair: both exit, or neither)
   if (sel && *sel != 32ull) return;  // device-side path choice (k1_finalize): 32 = TC
   extern __shared__ __align__(128) uint8_t td_raw[];
-  TdShared<F16>& sh = *reinterpret_cast<TdShared<F16>*>(td_raw + ((128 - (tc::smem_u32(td_raw) & 127)) & 127));
+  TdShared<F16>& sh = *reinterpret_cast<TdShared<F16>*>(td_raw + ((1024 - (tc::smem_u32(td_raw) & 1023)) & 1023));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // pair: rank r of the cluster owns row tile 2p + r of pair tile p; the leader (r = 0) issues
   const uint32_t rank = kPair ? tc::cluster_rank() : 0u;
@@ -633,30 +632,39 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
         __syncwarp();
         if (lane == 0) signal_issuer(&sh.seg_empty[b]);
       }
-      // C += P: row m0 + lane of this warp, 32 columns per bulk reduce
-      const int64_t row = rt * kTdTM + 32 * q4 + lane, n0 = tb * kTdTN;
+      // C += P: per 32 columns one TMA tensor reduce-add of the warp's 32 x 32 box (the L2
+      // performs the fp32 adds, one writer per element; rows / columns past M / N are clipped
+      // by the tensor map).  128-byte-swizzled staging: thread = row, its 16-byte chunk q at
+      // chunk q ^ (row % 8), so the 32 rows' stores spread over the banks.  (One 128-byte bulk
+      // reduce per thread and 32 columns queued 16x more TMA operations, which delayed the
+      // operand loads of sparse-k cells.)
+      const int64_t row0 = rt * kTdTM + 32 * q4, n0 = tb * kTdTN;
+      float* box = &sh.xp[4 * ag + q4][0][0];
 #pragma unroll
       for (int c = 0; c < kCh; ++c, ++R) {
-        float* buf = &sh.xp[4 * ag + q4][R % kTdXbuf][lane][0];
-        // this thread's reduce from the buffer's previous use has read it
-        if (R >= (uint32_t)kTdXbuf) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        if (R > 0) {  // the previous reduce of this box has read it
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          __syncwarp();
+        }
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          *reinterpret_cast<float4*>(buf + 4 * q) =
+          *reinterpret_cast<float4*>(box + 32 * lane + 4 * (q ^ (lane & 7))) =
               make_float4(P[32 * c + 4 * q], P[32 * c + 4 * q + 1], P[32 * c + 4 * q + 2], P[32 * c + 4 * q + 3]);
-        tc::fence_async_smem();  // generic-proxy stores before the bulk (async-proxy) read
-        const int64_t col = n0 + 32 * (c0 + c);
-        if (row < M && col < N) {
-          const int64_t ncol = N - col < 32 ? ((N - col + 3) & ~int64_t(3)) : 32;  // 16-byte multiple
-          asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(
-                           C + row * ldc + col),
-                       "r"(tc::smem_u32(buf)), "r"((uint32_t)(ncol * 4))
-                       : "memory");
+        tc::fence_async_smem();  // generic-proxy stores before the tensor (async-proxy) read
+        __syncwarp();
+        if (lane == 0 && row0 < M) {
+          const int32_t col = (int32_t)(n0 + 32 * (c0 + c));
+          asm volatile(
+              "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                  reinterpret_cast<uint64_t>(&tmap_c)),
+              "r"(col), "r"((int32_t)row0), "r"(tc::smem_u32(box))
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     }
-    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // reduces done before the CTA exits
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // reduces done before the CTA exits
+    __syncwarp();
   }
 td_done:
   tc::fence_before_sync();

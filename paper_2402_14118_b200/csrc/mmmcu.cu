@@ -107,6 +107,10 @@ struct mmmcu_ctx {
   CUtensorMap tmap_at;
   const void* tmap_at_ptr = nullptr;
   int64_t tmap_at_rows = 0;
+  // TMA descriptor of C (K2-TC's tensor reduce-adds), cached by (C, ldc, M, N)
+  CUtensorMap tmap_c;
+  const void* tmap_c_ptr = nullptr;
+  int64_t tmap_c_key[3] = {0, 0, 0};
 
   // ---- statistics: u64 [16] = {inv, lanes, skipped, zreg, nnzA, pop, zero_codes, span, slice_nz}
   DevBuf stats;
@@ -696,11 +700,40 @@ mmmcu_status at_tensor_map(mmmcu_ctx* ctx) {
   return MMMCU_OK;
 }
 
+// C as a 2-D fp32 tensor [M rows][N columns] (stride ldc), boxes of 32 x 32 with the 128-byte
+// swizzle of K2-TC's staging: the accumulators' C += P by TMA tensor reduce-adds.
+mmmcu_status c_tensor_map(mmmcu_ctx* ctx, float* C, int64_t ldc) {
+  if (ctx->tmap_c_ptr == C && ctx->tmap_c_key[0] == ldc && ctx->tmap_c_key[1] == ctx->M && ctx->tmap_c_key[2] == ctx->N)
+    return MMMCU_OK;
+  EncodeTiledFn encode = nullptr;
+  {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    MMMCU_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) return fail(ctx, MMMCU_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<EncodeTiledFn>(fn);
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)ctx->N, (cuuint64_t)ctx->M};
+  const cuuint64_t strides[1] = {(cuuint64_t)ldc * sizeof(float)};
+  const cuuint32_t box[2] = {32, 32};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(&ctx->tmap_c, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, C, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ctx, MMMCU_ERR_CUDA, "cuTensorMapEncodeTiled (C) failed (" + std::to_string((int)r) + ")");
+  ctx->tmap_c_ptr = C;
+  ctx->tmap_c_key[0] = ldc;
+  ctx->tmap_c_key[1] = ctx->M;
+  ctx->tmap_c_key[2] = ctx->N;
+  return MMMCU_OK;
+}
+
 // K2-TC over the dense-tile operands (sel: device-side path choice, nullptr = forced).
 template <bool F16>
 mmmcu_status launch_tc_t(mmmcu_ctx* ctx, float* C, int64_t ldc, const unsigned long long* sel) {
   const int64_t row_tiles = ctx->m_at / mmmcu::kTdTM;
   MMMCU_TRY(at_tensor_map(ctx));
+  MMMCU_TRY(c_tensor_map(ctx, C, ldc));
   constexpr int smem = mmmcu::td_smem<F16>();
   MMMCU_CUDA(cudaFuncSetAttribute(mmmcu::k2_tc<F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   if (ctx->num_sms == 0) MMMCU_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
@@ -738,7 +771,7 @@ mmmcu_status launch_tc_t(mmmcu_ctx* ctx, float* C, int64_t ldc, const unsigned l
                               (const float*)ctx->tcb.as<float>(), (const int32_t*)ctx->tck.as<int32_t>(),
                               (const int32_t*)ctx->tcn.as<int32_t>(), (int64_t)ctx->tc_steps, C, ldc, ctx->M, ctx->N,
                               row_tiles, ctx->n_tc, sel, (const unsigned long long*)za_rrng(ctx),
-                              (const unsigned long long*)zb_grng(ctx), ctx->tmap_at);
+                              (const unsigned long long*)zb_grng(ctx), ctx->tmap_at, ctx->tmap_c);
   };
   MMMCU_CUDA(launch());
 #ifdef TD_PROF
