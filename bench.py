@@ -356,12 +356,11 @@ def quick_measure(workload, ctx, torch, device, steps, warmup):
 
 
 def count_launches(cells):
-    # per cell (AUTO): K1 = k1_zero (scratch) + k1_pass (A and B tiles, last-CTA plan totals / scans / path
-    # choice) + k1_csr + k1_pack_auto (both packs in one launch, gated on the device by the
-    # path choice); K2 = k2_simt2_any + k2_tc (gated the same way: one runs, the other exits
-    # at entry).  cudaMemsetAsync nodes are not counted.  (profiles/r01_launches_summary.txt:
-    # 450 kernel launches per 75-cell step.)
-    return 6 * len(cells)
+    # per cell (AUTO): K1 = k1_pass (A and B tiles) + k1_fin (plan totals, range guard, path
+    # choice, CSR tile prefix) + k1_pack_auto (the chosen B pack and A's CSR in one persistent
+    # launch); K2 = k2_simt2_any + k2_tc (gated on the device: one runs, the other exits at
+    # entry).  (profiles/r02_launches_summary.txt: 375 kernel launches per 75-cell step.)
+    return 5 * len(cells)
 
 
 # ---------------------------------------------------------------------------- CPU leg
