@@ -104,8 +104,10 @@ __device__ __forceinline__ bool k1_range_wide(unsigned long long rng);
 //   K2-TC   = row tiles * Σ_tiles (24200 + 940 * stages), stages = ceil(live k / 32) (fp16
 //             split on CTA pairs: 6 MMAs of 16 k per stage; 940 SM-cycles per 128-row stage
 //             measured on the dense 4096^3 cells)
-//   + K1 packing traffic at 0.0433 SM-cycles per byte (HBM): K2-SIMT rows 2 x 64 B per
-//     non-zero (k, slice); K2-TC step images 2 x 768 B per live (k, tile) (fp16 hi | lo);
+//   + the K1 pack of the path's B operand, measured on configs[3] (2.4 GB of B): K2-SIMT rows
+//     19 SM-cycles per non-zero (k, slice), K2-TC step images 85 per live (k, tile) (the
+//     SIMT pack cost 0.37 ms there, 3.5x the old bytes-at-HBM-rate estimate, which made AUTO
+//     pick K2-SIMT, 2.17 ms, over K2-TC, 1.98 ms);
 //   each divided by min(#SMs, its CTA count).
 
 // Block-wide exclusive scan of (cnt[t] + add) -> out[0..n] (out[n] = total); one CTA.
@@ -315,8 +317,8 @@ __device__ void k1_finalize(const K1Scratch& z, int64_t M, int64_t K, int64_t nr
       const double span = (double)stats[7];
       const double slice_nz = (double)z.btot[0], pp = (double)pop;
       const double simt = rt * (double)z.n_tb * (double)kw * 1158.0 +
-                          rt * (span == 16.0 ? 26.0 * slice_nz : 17.5 * pp) + 0.0433 * 128.0 * slice_nz;
-      const double tc = rt * (24200.0 * (double)z.n_tc + 940.0 * (double)s_st) + 0.0433 * 2.0 * 768.0 * (double)s_live;
+                          rt * (span == 16.0 ? 26.0 * slice_nz : 17.5 * pp) + 19.0 * slice_nz;
+      const double tc = rt * (24200.0 * (double)z.n_tc + 940.0 * (double)s_st) + 85.0 * (double)s_live;
       const double sms = (double)z.num_sms;
       const double par_simt = fmin(sms, rt * (double)z.n_tb), par_tc = fmin(sms, rt * (double)z.n_tc);
       const bool nonfinite = *z.nonfinite_a != 0u || z.btot[3] != 0ull;
