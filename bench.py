@@ -669,6 +669,21 @@ def run_e2e(args, cells, As, Bs, ctx, torch, dist, world, device, stats):
 
     steps = args.e2e_steps or args.steps
     flops = float(sum(s["flops"] for s in stats))
+    # Host-path cell order: the step needs each distinct A (5) and B (15) once.  Their copies are
+    # queued interleaved (A0 B0 A1 B1 ... then the remaining B's) and the cells run in the order
+    # their two operands have both arrived, so the computable cells grow as i*j with the first
+    # copies and the later copies (one 64 MiB B per 5 cells) hide behind the compute (device
+    # order: 41 ms per step, the first A's cells waiting for all 15 B's).  Same cells, same
+    # bytes per step.
+    a_keys = list(dict.fromkeys(c[4]["key"] for c in cells))
+    b_keys = list(dict.fromkeys(c[5]["key"] for c in cells))
+    pos = {}
+    for i in range(max(len(a_keys), len(b_keys))):
+        for ks in (a_keys, b_keys):
+            if i < len(ks):
+                pos[ks[i]] = len(pos)
+    order = sorted(range(len(cells)), key=lambda i: (max(pos[cells[i][4]["key"]], pos[cells[i][5]["key"]]), i))
+    cells = [cells[i] for i in order]
 
     def pinned_like(t):  # host copy of a device operand (its padded base layout), pinned
         base = t if t.is_contiguous() else t.as_strided((t.shape[0], t.stride(0)), (t.stride(0), 1))
