@@ -111,6 +111,11 @@ constexpr int kTdTM = 128;
 #ifndef TD_GATHER
 #define TD_GATHER 1  // the stage's live A^T rows by TMA tile::gather4 (4 rows per instruction)
 #endif
+constexpr int kTdMaxTail = 256;  // >= co-resident pairs / CTAs of one launch
+#ifndef TD_TAIL_SPLIT
+#define TD_TAIL_SPLIT 0  // 1: the last, partial round of units cut along k across all pairs (measured slower:
+                         // dense cell 0.288 vs 0.273 ms, sparse-k 0.149 vs 0.129 ms; C no longer single-writer)
+#endif
 #ifndef TD_GATHER_RUNS
 #define TD_GATHER_RUNS 16  // stages with at most this many runs of consecutive live k use bulk copies
                            // (measured: gathers win at ~23 runs per stage, lose at ~9)
@@ -247,8 +252,19 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
   // units running together share both B column tiles and A^T row tiles in L2.  Measured
   // (4096^3): mostly-live cells run best with groups of 4 row units (A^T reuse, 0.32 ->
   // 0.30 ms), sparse-k cells with whole columns (their A rows are gathered per column tile)
-  int64_t live_sum = 0;
-  for (int64_t i = 0; i < n_tiles; ++i) live_sum += tcn[i];
+  // the live-k total over the tiles and the tail units' stage prefix (below), computed by all
+  // threads at once (a per-thread loop of dependent loads cost ~10 us at kernel start)
+  __shared__ unsigned long long s_live_sum;
+  __shared__ int s_tail_pre[kTdMaxTail + 1];
+  if (tid == 0) s_live_sum = 0ull;
+  __syncthreads();
+  {
+    unsigned long long part = 0;
+    for (int64_t i = tid; i < n_tiles; i += blockDim.x) part += (unsigned long long)tcn[i];
+    if (part) atomicAdd(&s_live_sum, part);
+  }
+  __syncthreads();
+  const int64_t live_sum = (int64_t)s_live_sum;
   const bool mostly_live = 4 * live_sum >= 3 * kpad * n_tiles;  // td_dense on the average tile
   const int grp_rows = mostly_live ? kTdGroup : m_units;
   const int nprod = mostly_live ? Cfg::kProd : Cfg::kProdSparse;  // producer warps of this launch
@@ -260,6 +276,58 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
   };
   auto row_tile = [&](int64_t ru) { return kPair ? 2 * ru + rank : ru; };
   auto nsteps_of = [&](int32_t total) { return (total + kStepK - 1) / kStepK; };
+  auto nstage_of = [&](int t) {
+    int64_t ru, tb;
+    unit_rc(t, ru, tb);
+    return (nsteps_of(tcn[tb]) + kSub - 1) / kSub;
+  };
+  // Work items (every role walks the same sequence): the first full_rounds rounds are whole
+  // units t = unit0 + r * nunits; the units of the last, partial round are cut along k so
+  // that every pair (CTA) gets an equal share of their concatenated stages — item = (unit,
+  // stages [jb, je)), its partial C added by the same tensor reduce-adds (352 units on 74
+  // pairs left 18 pairs idle for a fifth of a dense cell).
+  const int full_rounds = ntiles / nunits, tail0 = full_rounds * nunits, ntail = ntiles - tail0;
+  // exclusive prefix of the tail units' stage counts (ntail < nunits <= kTdMaxTail)
+  if (TD_TAIL_SPLIT) {
+    if (tid < ntail) s_tail_pre[tid + 1] = nstage_of(tail0 + tid);
+    if (tid == 0) s_tail_pre[0] = 0;
+    __syncthreads();
+    if (tid == 0)
+      for (int u = 1; u <= ntail; ++u) s_tail_pre[u] += s_tail_pre[u - 1];
+    __syncthreads();
+  }
+  const int64_t tail_total = TD_TAIL_SPLIT ? s_tail_pre[ntail] : 0;
+  auto item = [&](int it, int& t, int& jb, int& je) -> bool {
+    if (!TD_TAIL_SPLIT) {
+      t = unit0 + it * nunits;
+      if (t >= ntiles) return false;
+      jb = 0;
+      je = nstage_of(t);
+      return true;
+    }
+    if (it < full_rounds) {
+      t = unit0 + it * nunits;
+      jb = 0;
+      je = nstage_of(t);
+      return true;
+    }
+    const int64_t lo = tail_total * unit0 / nunits, hi = tail_total * (unit0 + 1) / nunits;
+    int k = it - full_rounds;
+    for (int u = 0; u < ntail; ++u) {  // (shared-memory prefix: cheap)
+      const int64_t base = s_tail_pre[u], b0 = max(base, lo), b1 = min((int64_t)s_tail_pre[u + 1], hi);
+      if (b0 < b1) {
+        if (k == 0) {
+          t = tail0 + u;
+          jb = (int)(b0 - base);
+          je = (int)(b1 - base);
+          return true;
+        }
+        --k;
+      }
+      if (s_tail_pre[u + 1] >= hi) break;
+    }
+    return false;
+  };
   // a signal for the MMA issuer: local arrive, or (pair follower) remote arrive on the leader
   auto signal_issuer = [&](uint64_t* bar) {
     if (!kPair || leader) tc::mbar_arrive(bar);
@@ -309,13 +377,13 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
 #endif
     const uint32_t pp = warp == 16 ? 0u : (uint32_t)(warp - 17);  // producer index
     const uint64_t pol = TD_HINT ? td_policy_evict_last() : 0ull;
-    for (int t = unit0; t < ntiles; t += nunits) {
+    int t, jb, je;
+    for (int it = 0; item(it, t, jb, je); ++it) {
       int64_t ru, tb;
       unit_rc(t, ru, tb);
       const int64_t rt = row_tile(ru);
       const int32_t total = tcn[tb];
       const int nsteps = nsteps_of(total);
-      const int nstage = (nsteps + kSub - 1) / kSub;
       // pair: the tile's step images are stored per column half (K1 pack), this CTA's half
       // of a stage is one contiguous copy
       constexpr int kStepCopy = kPair ? kTdStepFloats / 2 : kTdStepFloats;  // floats per step in this CTA
@@ -331,10 +399,10 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       };
       // this producer's stages of the tile: j0, j0 + 2, ... (J advances by the tile's count)
       const int NP = nprod;
-      const int j0 = (int)((pp + NP - (J % NP)) % NP);
+      const int j0 = jb + (int)((pp + NP - (J % NP)) % NP);
       int kc = kload(j0), k1 = kload(j0 + NP), k2 = kload(j0 + 2 * NP), k3 = kload(j0 + 3 * NP);
-      for (int j = j0; j < nstage; j += NP) {
-        const uint32_t Jj = J + (uint32_t)j;
+      for (int j = j0; j < je; j += NP) {
+        const uint32_t Jj = J + (uint32_t)(j - jb);
         const int st = Jj % kStages;
         const int kn = k1;
         k1 = k2;
@@ -400,7 +468,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
 #endif
         kc = kn;
       }
-      J += (uint32_t)nstage;
+      J += (uint32_t)(je - jb);
     }
 #ifdef TD_PROF
     if (lane == 0 && td_prof && warp == 16) {
@@ -422,16 +490,17 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
     long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const long long p0 = clock64();
 #endif
-    for (int t = unit0; t < ntiles; t += nunits) {
+    int t, jb, je;
+    for (int it = 0; item(it, t, jb, je); ++it) {
       int64_t ru, tb;
       unit_rc(t, ru, tb);
       const int nsteps = nsteps_of(tcn[tb]);
-      const int nstage = (nsteps + kSub - 1) / kSub;
-      for (int j = 0; j < nstage; ++j, ++J) {
+      for (int j = jb; j < je; ++j, ++J) {
+        const int jl = j - jb;  // stage within the item (segments start at the item's first stage)
         const int st = J % kStages, sl = J % kTdSlots;
         TD_CLK(c0);
         // D[G % 2] was drained (segment G - 2) before this segment overwrites it
-        if (j % kSeg == 0 && G >= 2) tc::mbar_wait(&sh.seg_empty[G & 1u], ((G >> 1) - 1) & 1u);
+        if (jl % kSeg == 0 && G >= 2) tc::mbar_wait(&sh.seg_empty[G & 1u], ((G >> 1) - 1) & 1u);
         TD_CLK(c1);
         tc::mbar_wait(&sh.tma[st], (J / kStages) & 1u);
         TD_CLK(c15);
@@ -442,7 +511,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
         TD_ADD(3, c15 - c1);
         tc::fence_after_sync();
         const uint32_t baddr = tc::smem_u32(sh.b[st]);
-        const bool seg_end = j % kSeg == kSeg - 1 || j == nstage - 1;
+        const bool seg_end = jl % kSeg == kSeg - 1 || j == je - 1;
         const uint32_t dcol = tbase + kTdTN * (G & 1u);  // this segment's D buffer
         if (tc::elect_one()) {
 #pragma unroll
@@ -453,7 +522,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
               const uint32_t bu = baddr + u * 2 * kImg;
               const uint64_t bhi = tc::smem_desc(bu, 128, 256), blo = tc::smem_desc(bu + kImg, 128, 256);
               const uint32_t ahi = tbase + kAcol + 32 * sl + 16 * u, alo = ahi + 8;
-              const uint32_t acc0 = (j % kSeg != 0 || u > 0) ? 1u : 0u;
+              const uint32_t acc0 = (jl % kSeg != 0 || u > 0) ? 1u : 0u;
               if (F16) {
                 tc::mma_f16_ts_pair(dcol, alo, bhi, idesc, acc0);
                 tc::mma_f16_ts_pair(dcol, ahi, blo, idesc, 1u);
@@ -507,18 +576,17 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
     long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const long long p0 = clock64();
 #endif
-    for (int t = unit0; t < ntiles; t += nunits) {
+    int t, jb, je;
+    for (int it = 0; item(it, t, jb, je); ++it) {
       int64_t ru, tb;
       unit_rc(t, ru, tb);
       const int32_t total = tcn[tb];
-      const int nsteps = nsteps_of(total);
-      const int nstage = (nsteps + kSub - 1) / kSub;
-      const int j0 = (int)(((uint32_t)grp + 2u - (J & 1u)) & 1u);
+      const int j0 = jb + (int)(((uint32_t)grp + 2u - (J & 1u)) & 1u);
       // fp16: this row's power-of-two scale 2^sA (from its max|a|, K1)
       const int64_t grow = row_tile(ru) * kTdTM + r;
       const float sa = F16 ? tc::exp2_int(tc::f16_scale_exp(grow < M ? (uint32_t)(__ldg(rrng + grow) >> 32) : 0u)) : 1.0f;
-      for (int j = j0; j < nstage; j += 2) {
-        const uint32_t Jj = J + (uint32_t)j;
+      for (int j = j0; j < je; j += 2) {
+        const uint32_t Jj = J + (uint32_t)(j - jb);
         const int st = Jj % kStages, sl = Jj % kTdSlots;
         const int nvalid = min(kStageK, total - kStageK * j);
         TD_CLK(q0);
@@ -560,7 +628,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
         TD_ADD(0, q1 - q0);
         TD_ADD(1, q3 - q1);
       }
-      J += (uint32_t)nstage;
+      J += (uint32_t)(je - jb);
     }
 #ifdef TD_PROF
     if (tid == 0 && td_prof) {
@@ -578,10 +646,8 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
     // [96 ag, 96 ag + 96) of the tile.  Per segment G: wait for D[G % 2], add it (fp16: times
     // 2^-(sA+sB), exact) into the row's partial P in REGISTERS with round-to-nearest adds
     // (P = D for the unit's first segment), 16 columns per tcgen05.ld, then release D[G % 2]
-    // (its MMAs two segments later may start).  After the unit's last segment: C += P by
-    // bulk reduce-adds (cp.reduce.async.bulk .add.f32, the L2 performs the fp32 adds, one
-    // writer per element): each thread stages 32 columns of its row in shared memory and
-    // issues one 128-byte reduce for it.
+    // (its MMAs two segments later may start).  After the item's last segment: C += P by TMA
+    // tensor reduce-adds (below); an item that is a k-range of a unit adds its partial sum.
     const int q4 = warp & 3;
     const int ag = (warp >> 2) & 1;                  // accumulator group: columns [96 ag, 96 ag + 96)
     constexpr int kCh = kTdTN / 32 / kTdAccGroups;   // 32-column chunks per group (3)
@@ -589,13 +655,12 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
     const uint32_t taddr = tbase + ((uint32_t)(q4 * 32) << 16);
     float P[kCh * 32];
     uint32_t G = 0, R = 0;  // segments drained, C chunks reduced
-    for (int t = unit0; t < ntiles; t += nunits) {
+    int t, jb, je;
+    for (int it = 0; item(it, t, jb, je); ++it) {
       int64_t ru, tb;
       unit_rc(t, ru, tb);
       const int64_t rt = row_tile(ru);
-      const int nsteps = nsteps_of(tcn[tb]);
-      const int nstage = (nsteps + kSub - 1) / kSub;
-      const int nseg = (nstage + kSeg - 1) / kSeg;
+      const int nseg = (je - jb + kSeg - 1) / kSeg;
       if (nseg == 0) continue;
       // fp16: undo this row's scale 2^sA and each 8-column group's 2^sB (exact powers of two)
       const int64_t grow = rt * kTdTM + 32 * q4 + lane;
