@@ -507,6 +507,28 @@ struct K1RingLoaderT {
       ++J;
     }
   }
+  // v[u] = row u, columns col4 .. col4+3 of the next 8-row group (one LDS.128 per row: a warp
+  // reads 512 contiguous bytes); zeros for !ok or u >= nvalid
+  template <bool FULL = false>
+  __device__ void rows4(uint4 (&v)[8], int col4, bool ok, int nvalid) {
+#pragma unroll
+    for (int h = 0; h < 8 / kK1SR; ++h) {
+      const int s = J % ST;
+      k1_wait(&r.full[s], (J / ST) & 1u);
+      const uint4* st = reinterpret_cast<const uint4*>(&r.buf[s][0][0]);
+#pragma unroll
+      for (int q = 0; q < kK1SR; ++q) {
+        const int u = h * kK1SR + q;
+        v[u] = (FULL || (ok && u < nvalid)) ? st[q * (kK1Cols / 4) + (col4 >> 2)] : make_uint4(0u, 0u, 0u, 0u);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                                                    (uint32_t)__cvta_generic_to_shared(&r.empty[s]))
+                                                : "memory");
+      ++J;
+    }
+  }
 };
 
 // Ballot formulation over the smem ring (k1_pass): warp w owns the 32-column chunks
@@ -664,11 +686,14 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
   asm volatile("bar.sync 2, %0;" ::"r"(kK1Threads) : "memory");
 }
 
-// B tile: per row only the 8-column group bits enter the group k-masks (gword; the lane
-// owning group g keeps it).  Everything else per row — region codes, Σ popcount(code) and
-// # non-zero codes (the WorkCounters factors), (k, slice) counts — follows from the 32 k-bit
-// masks at the end of the tile: row k's groups are the set bits k of the warp's 16 masks
-// (one ballot per k), a region's code is 8 of them.  The codes themselves are not stored:
+// B tile: warp w owns the contiguous 128 columns 128w .. 128w+127 of the 1024-column tile and
+// lane l the 4 columns 4l .. 4l+3 (half of an 8-column group): per row one LDS.128, the
+// lane's half-group k-mask bit (hw, no ballot), and the range of its |x| bit patterns with
+// 3-input integer min / max (VIMNMX3 / VIADDMNMX) — ~15 instructions per row and 128 columns
+// (the one-column-per-lane ballot formulation took ~36 and left the pass issue-bound on
+// B-dominated streams).  Everything else — group k-masks (gword = the two half masks OR-ed;
+// lane g < 16 keeps group g), region / slice / plan totals, the TC tiles' live-k words —
+// follows from the 32-bit masks at the end of the tile.  The codes themselves are not stored:
 // k1_codes_export rebuilds them from bgrp when a caller asks (export path).
 template <typename Loader>
 __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, int64_t nreg,
@@ -676,49 +701,38 @@ __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, 
                                             int64_t kwi) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t c0 = tx * kK1Cols, k0 = kwi * 32;
-  int colofs[4];
-  bool ok[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    colofs[j] = 32 * k1_chunk(w, j) + lane;
-    ok[j] = c0 + colofs[j] < ldb;
-  }
-  // lane g < 16 owns 8-column group g of the warp: chunk g >> 2, sub-group g & 3; lanes
-  // 0..7 are region (chunks 0, 1), lanes 8..15 region (chunks 2, 3)
-  const int gj = (lane >> 2) & 3, gs = lane & 3;
-  const int64_t gcol = c0 + 32 * k1_chunk(w, gj) + 8 * gs;
+  const int col4 = 128 * w + 4 * lane;       // this lane's 4 columns within the tile
+  const bool ok4 = c0 + col4 < ldb;          // (ldb is a multiple of 64: all 4 or none)
+  // lane g < 16 owns 8-column group g of the warp (lanes 2g, 2g+1 hold its halves); lanes 0..7
+  // are the warp's first 64-column region, lanes 8..15 its second
+  const int64_t gcol = c0 + 128 * w + 8 * lane;
   const bool gown = lane < 16 && gcol < ldb;
-  uint32_t sel[4];  // lane's chunk as an all-ones mask (uniform chunk masks, per-lane selection)
-#pragma unroll
-  for (int j = 0; j < 4; ++j) sel[j] = gj == j ? 0xFFFFFFFFu : 0u;
-  const uint32_t gmask = 0xFFu << (8 * gs);
-  uint32_t gword = 0;
-  // per-column |x| range as in k1_a_tile_b (lane = column l of chunk j), reduced per 8-column
-  // group at the end of the tile
-  uint32_t cmx[4] = {0u, 0u, 0u, 0u}, cmn[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+  uint32_t hw = 0;                                // k-mask of this lane's half group
+  uint32_t cmx = 0u, cmn = 0xFFFFFFFFu;           // max |x| bits, min (|x| bits - 1) of the lane's columns
   const int64_t kend = min(k0 + 32, K);
   const bool cols_full = c0 + kK1Cols <= ldb;
-  for (int64_t kb = k0; kb < kend; kb += 8) {
-    float x[8][4];
-    if (cols_full && kend - kb >= 8) ld.template rows<true>(x, colofs, ok, 8);
-    else ld.rows(x, colofs, ok, kend - kb >= 8 ? 8 : (int)(kend - kb));
+#pragma unroll
+  for (int kb8 = 0; kb8 < 4; ++kb8) {
+    const int64_t kb = k0 + 8 * kb8;
+    if (kb >= kend) break;
+    uint4 v[8];
+    if (cols_full && kend - kb >= 8) ld.template rows4<true>(v, col4, ok4, 8);
+    else ld.rows4(v, col4, ok4, kend - kb >= 8 ? 8 : (int)(kend - kb));
 #ifdef K1_NOCOMP_B
     continue;
 #endif
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      uint32_t m[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        m[j] = __ballot_sync(0xffffffffu, x[u][j] != 0.0f);
-        const uint32_t ab = __float_as_uint(x[u][j]) & 0x7FFFFFFFu;
-        cmx[j] = max(cmx[j], ab);
-        cmn[j] = min(cmn[j], ab - 1u);
-      }
-      const uint32_t mg = (m[0] & sel[0]) | (m[1] & sel[1]) | (m[2] & sel[2]) | (m[3] & sel[3]);  // branch-free
-      gword |= (uint32_t)((mg & gmask) != 0) << (uint32_t)(kb - k0 + u);
+      const uint32_t a = v[u].x & 0x7FFFFFFFu, b = v[u].y & 0x7FFFFFFFu, c = v[u].z & 0x7FFFFFFFu,
+                     d = v[u].w & 0x7FFFFFFFu;
+      const uint32_t m4 = max(max(a, b), max(c, d));
+      cmx = max(cmx, m4);
+      cmn = min(min(cmn, min(a - 1u, b - 1u)), min(c - 1u, d - 1u));
+      if (m4) hw |= 1u << (8 * kb8 + u);  // exact zero test: |x| bits != 0
     }
   }
+  const uint32_t gw2 = hw | __shfl_xor_sync(0xffffffffu, hw, 1);  // the group's mask (both halves)
+  uint32_t gword = __shfl_sync(0xffffffffu, gw2, (2 * lane) & 31);
   if (!gown) gword = 0;
   if (gown) bgrp[(gcol >> 3) * kw + kwi] = gword;
   // plan totals of the warp: Σ_k # non-zero groups = Σ_g popc(gword_g); Σ_k # non-zero
@@ -736,22 +750,11 @@ __device__ __forceinline__ void k1_b_tile_b(Loader& ld, int64_t K, int64_t ldb, 
     nz_w += __shfl_xor_sync(0xffffffffu, nz_w, o);
   }
   {
-    uint32_t amax_b = 0u, amin_b = 0xFFFFFFFFu;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      uint32_t mx = cmx[j], mn = cmn[j];
-#pragma unroll
-      for (int o = 1; o < 8; o <<= 1) {
-        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      }
-      const int64_t g = (c0 + 32 * k1_chunk(w, j) + (lane & ~7)) >> 3;  // this lane's 8-column group
-      if (z.grng && (lane & 7) == 0 && mx && 8 * g < ldb)  // this tile's max of the group
-        k1_red_range(&z.grng[g], mx, mx);
-      amax_b = max(amax_b, mx);
-      amin_b = min(amin_b, mn);
-    }
-    const uint32_t mb = __reduce_max_sync(0xffffffffu, amax_b), mn = __reduce_min_sync(0xffffffffu, amin_b);
+    // this tile's max of each 8-column group (even lane: halves 2g, 2g+1 = lanes l, l+1)
+    const uint32_t mx = max(cmx, __shfl_xor_sync(0xffffffffu, cmx, 1));
+    const int64_t g = (c0 + col4) >> 3;
+    if (z.grng && (lane & 1) == 0 && mx && 8 * g < ldb) k1_red_range(&z.grng[g], mx, mx);
+    const uint32_t mb = __reduce_max_sync(0xffffffffu, cmx), mn = __reduce_min_sync(0xffffffffu, cmn);
     if (lane == 0 && (mb >= 0x7F800000u || mn < 0x007FFFFFu)) atomicOr(&z.btot[3], 1ull);
   }
   if (lane == 0 && pop_w) atomicAdd(&z.btot[1], (unsigned long long)pop_w);
