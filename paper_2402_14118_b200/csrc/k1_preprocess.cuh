@@ -79,6 +79,10 @@ struct K1Scratch {
   int64_t m_at;           // M rounded up to 256 (K2-TC pair tiles)
   uint32_t* tlive;        // [n_tc][kw] live-k mask per kTcTileN-column TC tile: bit kk of word c
                           // set iff B[32c + kk, tile columns] has a non-zero (zeroed, atomicOr)
+  int64_t* tc_pre;        // [n_tc + 1] exclusive prefix of the tiles' fp16 step counts (k1_fin, AUTO);
+                          // tc_pre[n_tc] = -1 when k1_fin did not count the tiles (k1_pack_auto then
+                          // deals fixed step blocks).  nullptr outside AUTO
+  int32_t* tcn;           // [n_tc] live k per TC tile (k1_fin writes it with tc_pre)
   int64_t n_tb;           // 256-column tiles of B (K2-SIMT records)
   int64_t n_tc;           // kTcTileN-column tiles of B (K2-TC)
   int choose;             // AUTO: pick K2-SIMT vs K2-TC from the cost model (both operand sets built)
@@ -211,6 +215,7 @@ __device__ void k1_finalize(const K1Scratch& z, int64_t M, int64_t K, int64_t nr
   __shared__ uint32_t s_wide[2];
   __shared__ unsigned long long s_st, s_live;
   __shared__ int64_t s_wsum[kFinWarps];
+  __shared__ int64_t s_wsum_tc[kFinLiveWarps];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool choose = z.choose && has_a && has_b;
   const int64_t nw = z.n_tc * kw;
@@ -287,6 +292,16 @@ __device__ void k1_finalize(const K1Scratch& z, int64_t M, int64_t K, int64_t nr
     if (lane == 0) {
       atomicAdd(&s_st, st);
       atomicAdd(&s_live, live);
+    }
+    // the tiles' live counts and the exclusive prefix of their fp16 step counts: k1_pack_auto
+    // cuts the concatenated steps of all tiles into equal shares, one per CTA
+    if (z.tc_pre && z.choose) {
+      if (fits) {
+        for (int64_t tb = gt; tb < z.n_tc; tb += kT) z.tcn[tb] = (int32_t)s_tcnt[tb];
+        k1_group_scan(z.n_tc, [&](int64_t i) { return (s_tcnt[i] + 15u) / 16u; }, z.tc_pre, gt, kT, 3, s_wsum_tc);
+      } else if (gt == 0) {
+        z.tc_pre[z.n_tc] = -1;
+      }
     }
   } else {  // ---- the CSR's 32-row tile prefix
     if (nA > 0) {
@@ -1092,8 +1107,9 @@ struct PackTcArgs {
   const unsigned long long* grng;     // per 8-column group: max|B| bits << 32 | ... (K1 pass), fp16 only
 };
 
-// CTA (bx = step block, tb = tile) of the K2-TC pack; dynamic smem (2 kw + 1) words.
-__device__ __forceinline__ void k1_pack_tc_cta(const PackTcArgs& g, int64_t bx, int64_t tb) {
+// Steps [s_lo, s_hi) of tile tb of the K2-TC pack (s_hi is clipped to the tile's step count;
+// s_hi < 0: the fixed step block s_lo .. s_lo + kPtSteps); dynamic smem (2 kw + 1) words.
+__device__ __forceinline__ void k1_pack_tc_range(const PackTcArgs& g, int64_t tb, int64_t s_lo, int64_t s_hi) {
   const float* __restrict__ B = g.B;
   const int64_t ldb = g.ldb, kw = g.kw, maxsteps = g.maxsteps;
   const uint32_t* __restrict__ tlive = g.tlive;
@@ -1134,11 +1150,12 @@ __device__ __forceinline__ void k1_pack_tc_cta(const PackTcArgs& g, int64_t bx, 
   __syncthreads();
   const int32_t total = carry;
   const int SK = g.f16 ? 16 : 8;  // live k per step
-  const int64_t nsteps = (total + SK - 1) / SK;
-  if (bx == 0 && tid == 0) tcn[tb] = total;
-  const int64_t s0 = bx * kPtSteps;
-  if (s0 >= nsteps) return;
-  if (tid < kPtSteps * SK) {
+  const int64_t nsteps_all = (total + SK - 1) / SK;
+  if (s_lo == 0 && tid == 0) tcn[tb] = total;
+  const int64_t nsteps = s_hi < 0 ? min(nsteps_all, s_lo + kPtSteps) : min(nsteps_all, s_hi);  // end of this range
+  for (int64_t s0 = s_lo; s0 < nsteps; s0 += kPtSteps) {
+  __syncthreads();  // s_k of the previous block is no longer read
+  if (tid < kPtSteps * SK && s0 * SK + tid < nsteps * SK) {
     const int64_t p = s0 * SK + tid;
     int32_t k = -1;
     if (p < total) {
@@ -1207,7 +1224,7 @@ __device__ __forceinline__ void k1_pack_tc_cta(const PackTcArgs& g, int64_t bx, 
                      : "memory");
       }
     }
-    return;
+    continue;
   }
   // job = (step, k-quad q, column n): 4 B values -> one float4 hi + one float4 lo
   for (int j = tid; j < kPtSteps * 2 * kTcTileN; j += kPtThreads) {
@@ -1232,6 +1249,12 @@ __device__ __forceinline__ void k1_pack_tc_cta(const PackTcArgs& g, int64_t bx, 
     *reinterpret_cast<uint4*>(img + off) = make_uint4(h[0], h[1], h[2], h[3]);
     *reinterpret_cast<uint4*>(img + kTcTileN * 8 + off) = make_uint4(l[0], l[1], l[2], l[3]);
   }
+  }  // step blocks of the range
+}
+
+// CTA (bx = step block, tb = tile) of the K2-TC pack
+__device__ __forceinline__ void k1_pack_tc_cta(const PackTcArgs& g, int64_t bx, int64_t tb) {
+  k1_pack_tc_range(g, tb, bx * kPtSteps, -1);
 }
 
 __global__ void __launch_bounds__(kPtThreads, 4) k1_pack_tc(PackTcArgs g) { k1_pack_tc_cta(g, blockIdx.x, blockIdx.y); }
@@ -1308,11 +1331,37 @@ __global__ void __launch_bounds__(kPackThreads) k1_pack_rows(PackRowsArgs g) {
 // (one CTA per item made ~5.5 k CTAs per 4096^2 cell, most of them exiting at entry).
 __global__ void __launch_bounds__(kPtThreads, 4)
 k1_pack_auto(PackRowsArgs gr, int64_t rows_x, int64_t n_rows, PackTcArgs gt, int64_t tc_x, int64_t n_tcb,
-             const unsigned long long* __restrict__ sel, CsrArgs gc, int64_t n_csr) {
+             const unsigned long long* __restrict__ sel, CsrArgs gc, int64_t n_csr,
+             const int64_t* __restrict__ tc_pre, int64_t n_tiles) {
   tc::pdl_wait();  // launched with programmatic serialization after k1_pass
   extern __shared__ __align__(16) uint32_t pt_smem[];  // TC pack scan words / CSR staging
   const unsigned long long v = *sel;  // 8 / 16 K2-SIMT (rows), 32 K2-TC (step images), 48 K2-CSR (neither)
-  const int64_t n_pack = v == 32ull ? n_tcb : (v == 8ull || v == 16ull) ? n_rows : 0;
+  int64_t n_pack = v == 32ull ? n_tcb : (v == 8ull || v == 16ull) ? n_rows : 0;
+  // K2-TC with the tiles' step prefix from k1_fin: the concatenated steps of all tiles are cut
+  // into gridDim.x equal shares (fixed blocks of kPtSteps steps left the CTAs holding two
+  // blocks as the critical path: 704 blocks on 592 CTAs for a dense 4096^2 B, and every block
+  // of a sparse-k tile past its live steps still paid the prefix scan)
+  const int64_t s_all = (v == 32ull && tc_pre) ? tc_pre[n_tiles] : -1;
+  if (s_all >= 0) {
+    n_pack = 0;
+    const int64_t lo = s_all * blockIdx.x / gridDim.x, hi = s_all * (blockIdx.x + 1) / gridDim.x;
+    if (lo < hi) {
+      int64_t a = 0, b = n_tiles - 1;  // last tile tb with tc_pre[tb] <= lo
+      while (a < b) {
+        const int64_t mid = (a + b + 1) >> 1;
+        if (tc_pre[mid] <= lo) a = mid;
+        else b = mid - 1;
+      }
+      for (int64_t tb = a; tb < n_tiles && tc_pre[tb] < hi; ++tb) {
+        const int64_t t0 = tc_pre[tb], t1 = tc_pre[tb + 1];
+        const int64_t b0 = (lo > t0 ? lo : t0) - t0, b1 = (hi < t1 ? hi : t1) - t0;
+        if (b0 < b1) {
+          k1_pack_tc_range(gt, tb, b0, b1);
+          __syncthreads();  // shared memory is reused by the next piece
+        }
+      }
+    }
+  }
   for (int64_t w = blockIdx.x; w < n_pack + n_csr; w += gridDim.x) {
     if (w < n_pack) {
       if (v == 32ull) k1_pack_tc_cta(gt, w % tc_x, w / tc_x);

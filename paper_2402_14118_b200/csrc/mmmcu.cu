@@ -102,7 +102,7 @@ struct mmmcu_ctx {
   int pa = 0, pb = 0;
   bool za_clean[2] = {false, false}, zb_clean[2] = {false, false};
   bool zero_a_next = false, zero_b_next = false;  // the coming K1 pass zeroes the other half
-  DevBuf at, tcb, tck, tcn, brows, row_off;
+  DevBuf at, tcb, tck, tcn, tc_pre, brows, row_off;
   // TMA descriptor of A^T as a 2-D tensor [m_at / 128 * kpad rows][128 floats] (K2-TC gather4)
   CUtensorMap tmap_at;
   const void* tmap_at_ptr = nullptr;
@@ -357,6 +357,7 @@ mmmcu_status stage_b(mmmcu_ctx* ctx, const float* B, int64_t K, int64_t N, int64
     MMMCU_CUDA(ctx->tcb.ensure((size_t)n_tc * ctx->tc_steps * mmmcu::kTdStepFloats * 4));
     MMMCU_CUDA(ctx->tck.ensure(sizeof(int32_t) * n_tc * ctx->tc_steps * 8));
     MMMCU_CUDA(ctx->tcn.ensure(sizeof(int32_t) * n_tc));
+    MMMCU_CUDA(ctx->tc_pre.ensure(sizeof(int64_t) * (n_tc + 1)));
   }
   if (ops & OP_ROWS) {
     // worst case 3 header + 16 x 32 rows of 64 B per (tile, chunk): ~B's bytes
@@ -427,7 +428,8 @@ mmmcu_status pack_auto(mmmcu_ctx* ctx, const unsigned long long* sel, bool with_
   const int64_t items = std::max(n_rows, n_tc) + n_csr;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(items, 4 * (int64_t)ctx->num_sms));
   MMMCU_CUDA(launch_pdl(mmmcu::k1_pack_auto, dim3((unsigned)grid), dim3(mmmcu::kPtThreads), smem_all, ctx->stream,
-                        rows_args(ctx), rows_x, n_rows, tc_args(ctx, true), tc_x, n_tc, sel, csr_args(ctx), n_csr));
+                        rows_args(ctx), rows_x, n_rows, tc_args(ctx, true), tc_x, n_tc, sel, csr_args(ctx), n_csr,
+                        (const int64_t*)ctx->tc_pre.as<int64_t>(), ctx->n_tc));
   MMMCU_LAUNCHED();
   ctx->tcb_f16 = true;
   return MMMCU_OK;
@@ -483,6 +485,8 @@ mmmcu_status launch_k1(mmmcu_ctx* ctx, bool do_a, bool do_b) {
   z.row_off = rows_b ? ctx->row_off.as<int64_t>() : nullptr;
   z.n_tb = ctx->n_tb;
   z.n_tc = ctx->n_tc;
+  z.tc_pre = (gate && tcb_b) ? ctx->tc_pre.as<int64_t>() : nullptr;
+  z.tcn = (gate && tcb_b) ? ctx->tcn.as<int32_t>() : nullptr;
   z.choose = gate ? 1 : 0;
   if (ctx->num_sms == 0) MMMCU_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
   z.num_sms = ctx->num_sms;
@@ -999,7 +1003,7 @@ mmmcu_status mmmcu_ctx_destroy(mmmcu_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : {&ctx->abits, &ctx->za, &ctx->tile_prefix, &ctx->row_ptr, &ctx->cols, &ctx->codes, &ctx->bgrp, &ctx->zb,
-                    &ctx->ctl, &ctx->at, &ctx->tcb, &ctx->tck, &ctx->tcn, &ctx->brows, &ctx->row_off,
+                    &ctx->ctl, &ctx->at, &ctx->tcb, &ctx->tck, &ctx->tcn, &ctx->tc_pre, &ctx->brows, &ctx->row_off,
                     &ctx->stats, &ctx->hA, &ctx->hB, &ctx->hC, &ctx->scratch0, &ctx->scratch1, &ctx->gcodes,
                     &ctx->gza, &ctx->gzb})
     b->release();
