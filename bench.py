@@ -328,8 +328,8 @@ def run_step(cells, As, Bs, Cs, ctx, torch, events=None):
 class CellLanes:
     """The step's cells dealt round-robin to S contexts, each on its own CUDA stream: cells
     are independent jobs, so the HBM-bound K1 chain of one cell runs in the tail round and
-    the single-CTA phases of another cell's tensor-bound K2 (measured on the sweep: 23.1 ->
-    21.7 ms/step with 3 lanes).  Every lane owns its plans (context) and its C."""
+    the SMs K2-TC leaves free (it takes the fewest CTA pairs that keep its number of rounds) of
+    another cell's tensor-bound K2 (measured on the sweep: 23.1 -> 21.1 ms/step with 2 lanes).  Every lane owns its plans (context) and its C."""
 
     def __init__(self, n, cells, ctx0, device, torch):
         import paper_2402_14118_b200 as mmm
@@ -488,7 +488,7 @@ def main():
     ap.add_argument("--per-cell", default="", help="write per-cell timings (JSON) to this path")
     ap.add_argument("--no-cfg5-ref", action="store_true", help="N=1: skip the 1-GPU configs[4] reference line")
     ap.add_argument("--lanes", type=int, default=0,
-                    help="contexts / CUDA streams the step's cells are dealt to (0 = 3 for multi-cell workloads, else 1)")
+                    help="contexts / CUDA streams the step's cells are dealt to (0 = 2 for multi-cell workloads, else 1)")
     args = ap.parse_args()
     warmup = max(args.warmup, 3)
 
@@ -530,7 +530,7 @@ def main():
                    "for every cell",
            "l2": "inputs larger than L2 per cell (A+B+C >= 126 MB for the sweep; A is shared by the 15 cells of "
                  "one zA, B by the 5 cells of one (zB, bw), each cell is one preprocess + multiply)",
-           "lanes": "the step's cells are dealt round-robin to 3 contexts on 3 CUDA streams (--lanes; independent "
+           "lanes": "the step's cells are dealt round-robin to 2 contexts on 2 CUDA streams (--lanes; independent "
                     "cells overlap one cell's HBM-bound K1 with another's tensor-bound K2); 1 = one stream",
            "global_batch": sum(c[1] for c in cells) // max(len(cells), 1) * world if not strong
            else workload_cells(args.workload)[0][1],
@@ -559,7 +559,7 @@ def main():
     hbm_peak, hbm_src = measured_peaks()
 
     # ---- device-timed steps: the step's cells on `lanes` contexts / streams (CellLanes)
-    nl = args.lanes if args.lanes > 0 else (3 if len(cells) >= 3 else 1)
+    nl = args.lanes if args.lanes > 0 else (2 if len(cells) >= 2 else 1)
     nl = max(1, min(nl, len(cells)))
     lanes = CellLanes(nl, cells, ctx, device, torch)
     cfg["lanes_used"] = nl

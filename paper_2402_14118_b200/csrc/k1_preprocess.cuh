@@ -408,7 +408,11 @@ struct K1Args {
 // it starts issuing its groups and tags every stage with the tile, so the compute warps
 // follow the same sequence; a CTA that runs fast takes more tiles (no static tail).
 #ifndef K1_STATIC_EIGHTHS
-#define K1_STATIC_EIGHTHS 4  // eighths of the tiles dealt statically, the rest by an atomic counter (0, 4, 7 measured 42.9, 42.4, 44.1 us)
+// eighths of the tiles dealt statically, the rest by an atomic counter.  Alone, 0 / 4 / 7 measured
+// 42.9 / 42.4 / 44.1 us; 0 (all dynamic) is the default because a pass that shares the GPU
+// with another stream's K2-TC has only some of its CTAs resident, and statically dealt tiles
+// would wait for the others (sweep step on 2 streams: 21.8 -> 21.1 ms)
+#define K1_STATIC_EIGHTHS 0
 #endif
 struct K1Cursor {
   const K1Args* g;
@@ -880,7 +884,10 @@ __global__ void __launch_bounds__(32 * kFinWarps) k1_fin(const __grid_constant__
   tc::pdl_trigger();  // the pack / CSR CTAs may become resident now (they wait for this grid)
   tc::pdl_wait();     // the K1 pass is complete and its writes are visible
   K1_FIN_STAMP(0);
-  if (threadIdx.x == 0) *z.next_tile = 0u;  // ready for the next pass
+  if (threadIdx.x == 0) {
+    *z.next_tile = 0u;    // ready for the next pass
+    z.next_tile[1] = 0u;  // the item counter of the k1_pack_auto launch behind this kernel
+  }
   k1_finalize(z, f.M, f.K, f.nreg, f.kw, f.has_a, f.has_b, f.nA, f.nB, stats, fin_smem);
 }
 
@@ -1332,7 +1339,7 @@ __global__ void __launch_bounds__(kPackThreads) k1_pack_rows(PackRowsArgs g) {
 __global__ void __launch_bounds__(kPtThreads, 4)
 k1_pack_auto(PackRowsArgs gr, int64_t rows_x, int64_t n_rows, PackTcArgs gt, int64_t tc_x, int64_t n_tcb,
              const unsigned long long* __restrict__ sel, CsrArgs gc, int64_t n_csr,
-             const int64_t* __restrict__ tc_pre, int64_t n_tiles) {
+             const int64_t* __restrict__ tc_pre, int64_t n_tiles, unsigned int* __restrict__ item_ctr) {
   tc::pdl_wait();  // launched with programmatic serialization after k1_pass
   extern __shared__ __align__(16) uint32_t pt_smem[];  // TC pack scan words / CSR staging
   const unsigned long long v = *sel;  // 8 / 16 K2-SIMT (rows), 32 K2-TC (step images), 48 K2-CSR (neither)
@@ -1342,32 +1349,49 @@ k1_pack_auto(PackRowsArgs gr, int64_t rows_x, int64_t n_rows, PackTcArgs gt, int
   // blocks as the critical path: 704 blocks on 592 CTAs for a dense 4096^2 B, and every block
   // of a sparse-k tile past its live steps still paid the prefix scan)
   const int64_t s_all = (v == 32ull && tc_pre) ? tc_pre[n_tiles] : -1;
-  if (s_all >= 0) {
-    n_pack = 0;
-    const int64_t lo = s_all * blockIdx.x / gridDim.x, hi = s_all * (blockIdx.x + 1) / gridDim.x;
-    if (lo < hi) {
-      int64_t a = 0, b = n_tiles - 1;  // last tile tb with tc_pre[tb] <= lo
-      while (a < b) {
-        const int64_t mid = (a + b + 1) >> 1;
-        if (tc_pre[mid] <= lo) a = mid;
-        else b = mid - 1;
-      }
-      for (int64_t tb = a; tb < n_tiles && tc_pre[tb] < hi; ++tb) {
-        const int64_t t0 = tc_pre[tb], t1 = tc_pre[tb + 1];
-        const int64_t b0 = (lo > t0 ? lo : t0) - t0, b1 = (hi < t1 ? hi : t1) - t0;
-        if (b0 < b1) {
-          k1_pack_tc_range(gt, tb, b0, b1);
-          __syncthreads();  // shared memory is reused by the next piece
+  const int64_t n_shares = s_all >= 0 ? (int64_t)gridDim.x : 0;
+  if (s_all >= 0) n_pack = 0;
+  // Items are taken from an atomic counter (reset by k1_fin), not dealt by CTA index: when this
+  // launch shares the GPU with another stream's K2-TC only some of its CTAs are resident, and
+  // they walk the whole list.  Items: [step shares | fixed pack blocks | CSR row groups].
+  __shared__ unsigned int s_item;
+#ifdef K1_PACK_STATIC
+  unsigned int s_round = 0;
+#endif
+  for (;;) {
+#ifdef K1_PACK_STATIC  // (timing variant: items dealt by CTA index)
+    if (threadIdx.x == 0) s_item = s_round++ * gridDim.x + blockIdx.x;
+#else
+    if (threadIdx.x == 0) s_item = atomicAdd(item_ctr, 1u);
+#endif
+    __syncthreads();
+    const int64_t w = (int64_t)s_item;
+    __syncthreads();
+    if (w >= n_shares + n_pack + n_csr) break;
+    if (w < n_shares) {
+      const int64_t lo = s_all * w / n_shares, hi = s_all * (w + 1) / n_shares;
+      if (lo < hi) {
+        int64_t a = 0, b = n_tiles - 1;  // last tile tb with tc_pre[tb] <= lo
+        while (a < b) {
+          const int64_t mid = (a + b + 1) >> 1;
+          if (tc_pre[mid] <= lo) a = mid;
+          else b = mid - 1;
+        }
+        for (int64_t tb = a; tb < n_tiles && tc_pre[tb] < hi; ++tb) {
+          const int64_t t0 = tc_pre[tb], t1 = tc_pre[tb + 1];
+          const int64_t b0 = (lo > t0 ? lo : t0) - t0, b1 = (hi < t1 ? hi : t1) - t0;
+          if (b0 < b1) {
+            k1_pack_tc_range(gt, tb, b0, b1);
+            __syncthreads();  // shared memory is reused by the next piece
+          }
         }
       }
-    }
-  }
-  for (int64_t w = blockIdx.x; w < n_pack + n_csr; w += gridDim.x) {
-    if (w < n_pack) {
-      if (v == 32ull) k1_pack_tc_cta(gt, w % tc_x, w / tc_x);
-      else k1_pack_rows_cta(gr, w % rows_x, w / rows_x);
+    } else if (w < n_shares + n_pack) {
+      const int64_t x = w - n_shares;
+      if (v == 32ull) k1_pack_tc_cta(gt, x % tc_x, x / tc_x);
+      else k1_pack_rows_cta(gr, x % rows_x, x / rows_x);
     } else {
-      k1_csr_cta(gc, w - n_pack, pt_smem);
+      k1_csr_cta(gc, w - n_shares - n_pack, pt_smem);
     }
     __syncthreads();  // shared memory is reused by the next item
   }

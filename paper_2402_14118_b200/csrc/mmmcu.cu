@@ -429,7 +429,7 @@ mmmcu_status pack_auto(mmmcu_ctx* ctx, const unsigned long long* sel, bool with_
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(items, 4 * (int64_t)ctx->num_sms));
   MMMCU_CUDA(launch_pdl(mmmcu::k1_pack_auto, dim3((unsigned)grid), dim3(mmmcu::kPtThreads), smem_all, ctx->stream,
                         rows_args(ctx), rows_x, n_rows, tc_args(ctx, true), tc_x, n_tc, sel, csr_args(ctx), n_csr,
-                        (const int64_t*)ctx->tc_pre.as<int64_t>(), ctx->n_tc));
+                        (const int64_t*)ctx->tc_pre.as<int64_t>(), ctx->n_tc, ctx->ctl.as<unsigned int>() + 2));
   MMMCU_LAUNCHED();
   ctx->tcb_f16 = true;
   return MMMCU_OK;
@@ -766,7 +766,15 @@ mmmcu_status launch_tc_t(mmmcu_ctx* ctx, float* C, int64_t ldc, const unsigned l
       if (getenv("MMMCU_VERBOSE")) fprintf(stderr, "mmmcu: K2-TC co-resident pairs %d (SMs %d)\n", nc, ctx->num_sms);
     }
     const int64_t units = ((row_tiles + 1) / 2) * ctx->n_tc;
-    cfg.gridDim = dim3(2u * (unsigned)std::min<int64_t>(units, ctx->tc_pairs));
+    // the fewest pairs that keep the number of rounds (352 units: 5 rounds on 74 or on 71 pairs):
+    // the SMs left free run the K1 chain of a cell on another stream the whole K2 long
+    int64_t pairs = std::min<int64_t>(units, ctx->tc_pairs);
+    static const int trim = getenv("MMMCU_TC_TRIM") ? atoi(getenv("MMMCU_TC_TRIM")) : 1;  // 0: all co-resident pairs
+    if (trim && pairs > 0) {
+      const int64_t rounds = (units + pairs - 1) / pairs;
+      pairs = (units + rounds - 1) / rounds;
+    }
+    cfg.gridDim = dim3(2u * (unsigned)pairs);
   } else {
     cfg.gridDim = dim3((unsigned)std::min<int64_t>(row_tiles * ctx->n_tc, ctx->num_sms));
   }
