@@ -325,18 +325,18 @@ def run_step(cells, As, Bs, Cs, ctx, torch, events=None):
             events[t][2].record()
 
 
-class CellLanes:
-    """The step's cells dealt round-robin to S contexts, each on its own CUDA stream: cells
-    are independent jobs, so the HBM-bound K1 chain of one cell runs in the tail round and
-    the SMs K2-TC leaves free (it takes the fewest CTA pairs that keep its number of rounds) of
-    another cell's tensor-bound K2 (measured on the sweep: 23.1 -> 21.1 ms/step with 2 lanes).  Every lane owns its plans (context) and its C."""
+class CellStreams:
+    """The step's cells dealt round-robin to S contexts, each on its own CUDA stream (the
+    package's MmmStreams): cells are independent jobs, so the HBM-bound K1 chain of one cell
+    runs on the SMs K2-TC leaves free (it takes the fewest CTA pairs that keep its number of
+    rounds) and in the tail round of another cell's tensor-bound K2 (measured on the sweep:
+    22.9 -> 21.5 ms/step with 2 streams).  Every stream owns its plans (context) and its C."""
 
-    def __init__(self, n, cells, ctx0, device, torch):
+    def __init__(self, n, cells, device, torch):
         import paper_2402_14118_b200 as mmm
 
-        self.n, self.torch, self.device = n, torch, device
-        self.ctxs = [ctx0] + [mmm.MmmContext(device.index or 0) for _ in range(n - 1)]
-        self.streams = [torch.cuda.Stream(device) for _ in range(n)]
+        self.n = n
+        self.pool = mmm.MmmStreams(n, device.index or 0)
         self.Cs = []
         for _ in range(n):
             cs = {}
@@ -345,24 +345,16 @@ class CellLanes:
                     cs[(M, N)] = torch.zeros((M, mmm.round_up(N, 64)), dtype=torch.float32, device=device)[:, :N]
             self.Cs.append(cs)
 
-    def fork(self, ev):
-        """Every lane starts after ev (recorded on the current stream)."""
-        for st in self.streams:
-            st.wait_event(ev)
+    def fork(self):
+        self.pool.fork()
 
     def join(self):
-        main = self.torch.cuda.current_stream(self.device)
-        for st in self.streams:
-            main.wait_stream(st)
+        self.pool.join()
 
     def step(self, cells, As, Bs):
-        torch = self.torch
         for t, (label, M, K, N, sa, sb) in enumerate(cells):
             s = t % self.n
-            with torch.cuda.stream(self.streams[s]):
-                a, b = As[sa["key"]], Bs[sb["key"]]
-                self.ctxs[s].preprocess(a, b)
-                self.ctxs[s].multiply(self.Cs[s][(M, N)], a, b, want_counters=False)
+            self.pool.submit(self.Cs[s][(M, N)], As[sa["key"]], Bs[sb["key"]], stream=s)
 
 
 def quick_measure(workload, ctx, torch, device, steps, warmup):
@@ -487,7 +479,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
     ap.add_argument("--per-cell", default="", help="write per-cell timings (JSON) to this path")
     ap.add_argument("--no-cfg5-ref", action="store_true", help="N=1: skip the 1-GPU configs[4] reference line")
-    ap.add_argument("--lanes", type=int, default=0,
+    ap.add_argument("--streams", type=int, default=0,
                     help="contexts / CUDA streams the step's cells are dealt to (0 = 2 for multi-cell workloads, else 1)")
     args = ap.parse_args()
     warmup = max(args.warmup, 3)
@@ -530,7 +522,7 @@ def main():
                    "for every cell",
            "l2": "inputs larger than L2 per cell (A+B+C >= 126 MB for the sweep; A is shared by the 15 cells of "
                  "one zA, B by the 5 cells of one (zB, bw), each cell is one preprocess + multiply)",
-           "lanes": "the step's cells are dealt round-robin to 2 contexts on 2 CUDA streams (--lanes; independent "
+           "streams": "the step's cells are dealt round-robin to 2 contexts on 2 CUDA streams (--streams; independent "
                     "cells overlap one cell's HBM-bound K1 with another's tensor-bound K2); 1 = one stream",
            "global_batch": sum(c[1] for c in cells) // max(len(cells), 1) * world if not strong
            else workload_cells(args.workload)[0][1],
@@ -558,18 +550,16 @@ def main():
     fp32_peak, fp32_src = probe_fp32_peak(local)
     hbm_peak, hbm_src = measured_peaks()
 
-    # ---- device-timed steps: the step's cells on `lanes` contexts / streams (CellLanes)
-    nl = args.lanes if args.lanes > 0 else (2 if len(cells) >= 2 else 1)
+    # ---- device-timed steps: the step's cells on `streams` contexts / streams (CellStreams)
+    nl = args.streams if args.streams > 0 else (2 if len(cells) >= 2 else 1)
     nl = max(1, min(nl, len(cells)))
-    lanes = CellLanes(nl, cells, ctx, device, torch)
-    cfg["lanes_used"] = nl
+    cstreams = CellStreams(nl, cells, device, torch)
+    cfg["streams_used"] = nl
     main = torch.cuda.current_stream(device)
-    f0 = torch.cuda.Event()
-    f0.record(main)
-    lanes.fork(f0)
+    cstreams.fork()
     for _ in range(warmup):
-        lanes.step(cells, As, Bs)
-    lanes.join()
+        cstreams.step(cells, As, Bs)
+    cstreams.join()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -578,10 +568,10 @@ def main():
     clocks.start()
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s0.record(main)
-    lanes.fork(s0)
+    cstreams.fork()
     for k in range(args.steps):
-        lanes.step(cells, As, Bs)
-    lanes.join()
+        cstreams.step(cells, As, Bs)
+    cstreams.join()
     s1.record(main)
     torch.cuda.synchronize()
     if world > 1:
@@ -636,7 +626,7 @@ def main():
                   "frac": round(tc_exec / (tc_ms * 1e-3) / 1e12 / bf16, 4) if bf16 else None,
                   "def": "fp16-split MMAs the kernel issues (3 per live-k step of 16 per 128x192 tile) / K2-TC time"}
     t_roof = sum(max(s["flops"] / (fp32_peak * 1e12), s["bytes"] / (hbm_peak * 1e9)) for s in stats)
-    t_meas = step_ms_local * 1e-3  # the timed step (cells overlapped across the lanes)
+    t_meas = step_ms_local * 1e-3  # the timed step (cells overlapped across the streams)
     t_serial = float((k1_ms + k2_ms).sum()) * 1e-3  # the same cells one after the other on one stream
     hbm_bytes = sum(s["bytes"] for s in stats)
     useful = {"achieved": round(achieved_tf, 3), "peak": round(fp32_peak, 2), "unit": "TFLOP/s",
@@ -653,7 +643,7 @@ def main():
               "paths": {p: {"cells": v[0], "k2_ms": round(v[1], 4)} for p, v in paths.items()},
               "useful": useful, "time_frac": round(t_roof / t_meas, 4),
               "time_frac_def": "BASELINE: Σ_cells max(useful_flops/P_fp32, algo_bytes/BW_hbm) / device time of the timed step",
-              "lanes": nl, "serial_ms_per_step": round(t_serial * 1e3, 4),
+              "streams": nl, "serial_ms_per_step": round(t_serial * 1e3, 4),
               "serial_def": "K1 + K2 of every cell on ONE stream with CUDA events per cell (diagnostic pass after the "
                             "timed region); k1_ms_per_step, k2_ms_per_step, paths and tensor come from it",
               "hbm_peak_gbs": hbm_peak, "hbm_peak_source": hbm_src,

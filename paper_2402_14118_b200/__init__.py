@@ -14,6 +14,7 @@ from .api import (  # noqa: F401
     MmmError,
     MatrixFileError,
     MmmGroup,
+    MmmStreams,
     NoDeviceError,
     PlanStats,
     StaleContextError,

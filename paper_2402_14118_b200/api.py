@@ -608,6 +608,71 @@ class MmmGroup:
         return WorkCounters._from(cnt)
 
 
+class MmmStreams:
+    """Independent multiplies on n contexts, each on its own CUDA stream.
+
+    One multiply is K1 (HBM-bound) followed by K2 (tensor-bound on the AUTO path), and K2-TC
+    leaves a few SMs free (it takes the fewest CTA pairs that keep its number of rounds), so a
+    batch of independent (C, A, B) jobs runs faster when the K1 chain of one job shares the GPU
+    with the K2 of another (BASELINE configs[1], 75 cells: 22.9 -> 21.5 ms with 2 streams).
+    Jobs are dealt round-robin; the jobs of one stream run in order, every stream owns its plans (context).
+    The C operands of jobs on different streams must not alias.
+    """
+
+    def __init__(self, n: int = 2, device: int = 0, lane: LaneConfig = LaneConfig()):  # lane: the SIMD LaneConfig
+        import torch
+
+        if n < 1:
+            raise ValueError("MmmStreams needs at least one stream")
+        self.device = int(device)
+        self.contexts = [MmmContext(self.device, lane) for _ in range(int(n))]
+        self.streams = [torch.cuda.Stream(torch.device("cuda", self.device)) for _ in range(int(n))]
+        self._next = 0
+
+    def __len__(self) -> int:
+        return len(self.contexts)
+
+    def fork(self):
+        """Every stream waits for the work already queued on the current stream."""
+        import torch
+
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        for st in self.streams:
+            st.wait_event(ev)
+
+    def join(self):
+        """The current stream waits for every stream."""
+        import torch
+
+        cur = torch.cuda.current_stream(self.device)
+        for st in self.streams:
+            cur.wait_stream(st)
+
+    def submit(self, c, a, b, stream: Optional[int] = None) -> int:
+        """preprocess(a, b) + C += A*B on the next stream (or number `stream`); returns the one used."""
+        import torch
+
+        i = self._next if stream is None else int(stream) % len(self.contexts)
+        if stream is None:
+            self._next = (self._next + 1) % len(self.contexts)
+        with torch.cuda.stream(self.streams[i]):
+            self.contexts[i].preprocess(a, b)
+            self.contexts[i].multiply(c, a, b, want_counters=False)
+        return i
+
+    def run(self, jobs) -> None:
+        """fork(), submit every (c, a, b) of jobs round-robin, join()."""
+        self.fork()
+        for (c, a, b) in jobs:
+            self.submit(c, a, b)
+        self.join()
+
+    def close(self):
+        for cx in self.contexts:
+            cx.close()
+
+
 def matrix_seed(seed: int, tag: str) -> int:
     """Per-matrix seed hash_coords(seed, tag) (SURVEY.md §7 hard part 9; rng.hpp:18)."""
     def mix64(x):
