@@ -1,5 +1,5 @@
 #!/bin/bash
-# session-5 check: TC / config parity tests, K1 chain launch times of three cells, bench (no e2e)
+# K1-focused check: TC / config parity tests, K1 chain launch times of three cells, bench (no e2e)
 cd $GRAFT_REPO_ROOT
 T=${1:-s5a}
 timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "${2:-tc or auto or config or guard or sweep}" > gpurun_out/${T}_gputest.log 2>&1
