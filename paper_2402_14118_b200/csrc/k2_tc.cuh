@@ -61,7 +61,15 @@ namespace mmmcu {
 __device__ unsigned long long* td_prof = nullptr;  // debug builds only: per-CTA cycle counters
 #define TD_CLK(v) const long long v = clock64()
 #define TD_ADD(i, x) (prof[i] += (x))
+// kernel-phase timestamps (ns, %globaltimer) of thread 0: td_prof + 4096 + 8 * CTA
+#define TD_STAMP(i)                                                     \
+  if (threadIdx.x == 0 && td_prof) {                                    \
+    unsigned long long t_;                                              \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));              \
+    td_prof[4096 + 8 * blockIdx.x + (i)] = t_;                          \
+  }
 #else
+#define TD_STAMP(i)
 #define TD_CLK(v)
 #define TD_ADD(i, x)
 #endif
@@ -234,7 +242,9 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
   constexpr bool kPair = Cfg::kPair;
   constexpr int kNAccum = (kPair ? 8 : 4) * kTdAccGroups;  // accumulator warps signalling seg_empty
   constexpr int kNXform = kPair ? 8 : 4;    // transform warps signalling the MMA issuer (full): one group
+  TD_STAMP(0);
   tc::pdl_wait();  // launched with programmatic serialization after the K1 kernels / gated K2-SIMT
+  TD_STAMP(1);
   // (sel is read by both CTAs of a pair: both exit, or neither)
   if (sel && *sel != 32ull) return;  // device-side path choice (k1_finalize): 32 = TC
   extern __shared__ __align__(128) uint8_t td_raw[];
@@ -255,7 +265,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
   // the live-k total over the tiles and the tail units' stage prefix (below), computed by all
   // threads at once (a per-thread loop of dependent loads cost ~10 us at kernel start)
   __shared__ unsigned long long s_live_sum;
-  __shared__ int s_tail_pre[kTdMaxTail + 1];
+  __shared__ int s_tail_pre[TD_TAIL_SPLIT ? kTdMaxTail + 1 : 1];
   if (tid == 0) s_live_sum = 0ull;
   __syncthreads();
   {
@@ -355,6 +365,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
   else __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = sh.tmem_base;
+  TD_STAMP(2);
   constexpr uint32_t kAcol = 2 * kTdTN;  // TMEM columns: D[0] [0,192), D[1] [192,384), then the A slots
   // register budget per warpgroup (5 x 128 threads start at 96, setmaxnreg at the top of each
   // role's branch): the accumulators hold P, the producers / MMA issuer need few
@@ -413,7 +424,11 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
         const bool cont = valid && lane > 0 && prev + 1 == kc;
         const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
         const uint32_t cmask = __ballot_sync(0xffffffffu, cont);
+#ifdef TD_BHALF  // timing variant (wrong results): half of the stage's B bytes, to see how TMA-bound a cell is
+        const uint32_t bytes = (uint32_t)min(kSub, nsteps - kSub * j) * kStepCopy * 2u;
+#else
         const uint32_t bytes = (uint32_t)min(kSub, nsteps - kSub * j) * kStepCopy * 4u;
+#endif
         TD_CLK(q0);
         if (lane == 0 && Jj >= (uint32_t)kStages) tc::mbar_wait(&sh.empty[st], ((Jj / kStages) & 1u) ^ 1u);
         __syncwarp();
@@ -431,17 +446,27 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
         if (runs) {
           const float* atile = AT + rt * kpad * 128;
           if (lane == 0) {
+#ifdef TD_ANONE  // timing variant (wrong results): no A^T copies at all
+            td_expect_tx(&sh.tma[st], bytes);
+#else
             td_expect_tx(&sh.tma[st], bytes + 512u * (uint32_t)nv);
+#endif
             if (TD_HINT) td_bulk_hint(sh.b[st], bsrc + (int64_t)kSub * j * kStepCopy, bytes, &sh.tma[st], pol);
             else td_bulk(sh.b[st], bsrc + (int64_t)kSub * j * kStepCopy, bytes, &sh.tma[st]);
           }
           __syncwarp();
+#ifndef TD_ANONE
           if (valid && !cont) {  // run start: rows kc .. kc + len - 1 -> slots lane .. lane + len - 1
             const uint32_t len = lane == 31 ? 1u : (uint32_t)__ffs(~(cmask >> (lane + 1)));
             td_bulk_hint(sh.a[st][lane], atile + (int64_t)kc * 128, 512u * len, &sh.tma[st], pol);
           }
+#endif
         } else if (lane == 0) {
+#ifdef TD_ANONE
+          td_expect_tx(&sh.tma[st], bytes);
+#else
           td_expect_tx(&sh.tma[st], bytes + 2048u * (uint32_t)ng);
+#endif
           if (TD_HINT) td_bulk_hint(sh.b[st], bsrc + (int64_t)kSub * j * kStepCopy, bytes, &sh.tma[st], pol);
           else td_bulk(sh.b[st], bsrc + (int64_t)kSub * j * kStepCopy, bytes, &sh.tma[st]);
         }
@@ -451,7 +476,9 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
           const int rowk = (int)(rt * kpad) + (valid ? kc : k0);
           const int q0 = __shfl_sync(0xffffffffu, rowk, (4 * lane) & 31), q1 = __shfl_sync(0xffffffffu, rowk, (4 * lane + 1) & 31);
           const int q2 = __shfl_sync(0xffffffffu, rowk, (4 * lane + 2) & 31), q3 = __shfl_sync(0xffffffffu, rowk, (4 * lane + 3) & 31);
+#ifndef TD_ANONE
           if (lane < ng) td_gather4(sh.a[st][4 * lane], &tmap_at, q0, q1, q2, q3, &sh.tma[st], pol);
+#endif
         }
 #else
         if (lane == 0) {
@@ -506,9 +533,17 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
         TD_CLK(c15);
         tc::mbar_wait(&sh.full[sl], (J / kTdSlots) & 1u);
         TD_CLK(c2);
+#ifdef TD_PROF  // pair 0: the time every stage's MMAs are issued (ns), td_prof + 8192 + J
+        if (td_prof && blockIdx.x == 0 && lane == 0 && J < 4096u) {
+          unsigned long long t_;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+          td_prof[8192 + J] = t_;
+        }
+#endif
         TD_ADD(0, c1 - c0);
         TD_ADD(1, c2 - c1);
         TD_ADD(3, c15 - c1);
+        TD_ADD(4, jl < 8 ? c2 - c1 : 0);  // the waits of a unit's first 8 stages
         tc::fence_after_sync();
         const uint32_t baddr = tc::smem_u32(sh.b[st]);
         const bool seg_end = jl % kSeg == kSeg - 1 || j == je - 1;
@@ -554,6 +589,7 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       for (int i = 0; i < 3; ++i) q[i] = prof[i];
       q[3] = clock64() - p0;
       q[10] = prof[3];
+      q[15] = prof[4];
     }
 #endif
   }  // (warp 19 with two producers: idle)
@@ -655,6 +691,10 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
     const uint32_t taddr = tbase + ((uint32_t)(q4 * 32) << 16);
     float P[kCh * 32];
     uint32_t G = 0, R = 0;  // segments drained, C chunks reduced
+#ifdef TD_PROF
+    long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const long long p0 = clock64();
+#endif
     int t, jb, je;
     for (int it = 0; item(it, t, jb, je); ++it) {
       int64_t ru, tb;
@@ -674,9 +714,12 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
       }
       for (int g = 0; g < nseg; ++g, ++G) {
         const uint32_t b = G & 1u;
+        TD_CLK(a0);
         if (TD_ACC_SLEEP > 0) tc::mbar_wait_sleep_ns(&sh.seg_full[b], (G >> 1) & 1u, TD_ACC_SLEEP);
         else tc::mbar_wait(&sh.seg_full[b], (G >> 1) & 1u);
         tc::fence_after_sync();
+        TD_CLK(a1);
+        TD_ADD(0, a1 - a0);
         const bool first = g == 0;
 #pragma unroll
         for (int h = 0; h < 2 * kCh; ++h) {  // 16-column pieces
@@ -696,7 +739,10 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
         tc::fence_before_sync();
         __syncwarp();
         if (lane == 0) signal_issuer(&sh.seg_empty[b]);
+        TD_CLK(a2);
+        TD_ADD(1, a2 - a1);
       }
+      TD_CLK(a3);
       // C += P: per 32 columns one TMA tensor reduce-add of the warp's 32 x 32 box (the L2
       // performs the fp32 adds, one writer per element; rows / columns past M / N are clipped
       // by the tensor map).  128-byte-swizzled staging: thread = row, its 16-byte chunk q at
@@ -727,14 +773,27 @@ k2_tc(const float* __restrict__ AT, int64_t kpad, const float* __restrict__ tcb,
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
       }
+      TD_CLK(a4);
+      TD_ADD(2, a4 - a3);
     }
+#ifdef TD_PROF
+    if (lane == 0 && td_prof && warp == 8) {
+      unsigned long long* q = td_prof + 16 * blockIdx.x;
+      q[11] = prof[0];
+      q[12] = prof[1];
+      q[13] = prof[2];
+      q[14] = clock64() - p0;
+    }
+#endif
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // reduces done before the CTA exits
     __syncwarp();
   }
 td_done:
+  TD_STAMP(3);  // thread 0 (a transform thread): its role loop is done
   tc::fence_before_sync();
   if (kPair) tc::cluster_sync_all();  // both CTAs done: no remote arrive or MMA is in flight
   else __syncthreads();
+  TD_STAMP(4);
   if (warp == 0) {
     tc::fence_after_sync();
     if (kPair) tc::tmem_dealloc2(tbase, 512);

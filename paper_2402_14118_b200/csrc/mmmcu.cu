@@ -790,21 +790,67 @@ mmmcu_status launch_tc_t(mmmcu_ctx* ctx, float* C, int64_t ldc, const unsigned l
   {  // debug builds: rerun with the per-CTA cycle counters on, print their means
     const unsigned grid = cfg.gridDim.x;
     static unsigned long long* dbuf = nullptr;
-    if (!dbuf) cudaMalloc(&dbuf, 16 * 8 * 1024);
+    if (!dbuf) cudaMalloc(&dbuf, 16 * 8 * 1024);  // 1024 CTAs x 16 counters; stamps from entry 4096 on
     cudaMemset(dbuf, 0, 16 * 8 * 1024);
     cudaMemcpyToSymbol(mmmcu::td_prof, &dbuf, sizeof(dbuf));
     launch();
     cudaDeviceSynchronize();
     std::vector<unsigned long long> h(16 * grid);
     cudaMemcpy(h.data(), dbuf, 8 * 16 * grid, cudaMemcpyDeviceToHost);
+    {  // kernel phases from thread 0's %globaltimer stamps (ns): entry, after pdl_wait, after setup,
+       // role loop done, after the final cluster sync
+      std::vector<unsigned long long> st(8 * grid);
+      cudaMemcpy(st.data(), dbuf + 4096, 8 * 8 * grid, cudaMemcpyDeviceToHost);
+      unsigned long long t0 = ~0ull, t4 = 0;
+      double d[4] = {0, 0, 0, 0};
+      for (unsigned i = 0; i < grid; ++i) {
+        t0 = std::min(t0, st[8 * i]);
+        t4 = std::max(t4, st[8 * i + 4]);
+        for (int j = 0; j < 4; ++j) d[j] += (double)(st[8 * i + j + 1] - st[8 * i + j]) / grid;
+      }
+      unsigned long long first_setup = ~0ull, last_setup = 0, first_done = ~0ull;
+      for (unsigned i = 0; i < grid; ++i) {
+        first_setup = std::min(first_setup, st[8 * i + 2]);
+        last_setup = std::max(last_setup, st[8 * i + 2]);
+        first_done = std::min(first_done, st[8 * i + 3]);
+      }
+      fprintf(stderr,
+              "TD_PROF kernel span %.1f us | per CTA (mean, us): pdl_wait %.1f setup %.1f role loops %.1f final sync %.1f | "
+              "setup done %.1f .. %.1f us after the first entry, first CTA done at %.1f us\n",
+              (t4 - t0) / 1e3, d[0] / 1e3, d[1] / 1e3, d[2] / 1e3, d[3] / 1e3, (first_setup - t0) / 1e3,
+              (last_setup - t0) / 1e3, (first_done - t0) / 1e3);
+    }
+    {  // pair 0: gaps between consecutive stages' MMA issue times
+      std::vector<unsigned long long> ts(4096);
+      cudaMemcpy(ts.data(), dbuf + 8192, 8 * 4096, cudaMemcpyDeviceToHost);
+      int n = 0;
+      while (n < 4096 && ts[n]) ++n;
+      if (n > 2) {
+        std::vector<double> g;
+        for (int i = 1; i < n; ++i) g.push_back((double)(ts[i] - ts[i - 1]) / 1e3);
+        std::vector<double> sorted = g;
+        std::sort(sorted.begin(), sorted.end());
+        fprintf(stderr, "TD_PROF pair 0: %d stages in %.1f us, gap median %.3f us; gaps > 3x median:", n,
+                (double)(ts[n - 1] - ts[0]) / 1e3, sorted[sorted.size() / 2]);
+        double extra = 0;
+        for (size_t i = 0; i < g.size(); ++i)
+          if (g[i] > 3 * sorted[sorted.size() / 2]) {
+            fprintf(stderr, " [%zu: %.1f]", i + 1, g[i]);
+            extra += g[i] - sorted[sorted.size() / 2];
+          }
+        fprintf(stderr, " (sum over the median %.1f us)\n", extra);
+      }
+    }
     double a[16] = {0}, b[16] = {0};
     for (unsigned i = 0; i < grid; ++i)
       for (int j = 0; j < 16; ++j) (i % 2 == 0 ? a : b)[j] += (double)h[16 * i + j] / (grid / 2);
     for (double* x : {a, b})
       fprintf(stderr,
-              "TD_PROF/CTA cycles (%s): MMA wait-seg %.0f wait-tma+full %.0f (tma %.0f) issue %.0f total %.0f | "
-              "transform wait-tma %.0f work %.0f (slot wait %.0f) total %.0f | producer wait-empty %.0f total %.0f\n",
-              x == a ? "even" : "odd", x[0], x[1], x[10], x[2], x[3], x[4], x[5], x[7], x[6], x[8], x[9]);
+              "TD_PROF/CTA cycles (%s): MMA wait-seg %.0f wait-tma+full %.0f (tma %.0f; first 8 stages of units %.0f) issue %.0f total %.0f | "
+              "transform wait-tma %.0f work %.0f (slot wait %.0f) total %.0f | producer wait-empty %.0f total %.0f | "
+              "accumulator wait-seg %.0f drain %.0f C-write %.0f total %.0f\n",
+              x == a ? "even" : "odd", x[0], x[1], x[10], x[15], x[2], x[3], x[4], x[5], x[7], x[6], x[8], x[9], x[11], x[12],
+              x[13], x[14]);
     void* z = nullptr;
     cudaMemcpyToSymbol(mmmcu::td_prof, &z, sizeof(z));
   }
