@@ -586,6 +586,17 @@ def main():
     for k in range(dsteps):
         run_step(cells, As, Bs, Cs, ctx, torch, events=ev[k])
     torch.cuda.synchronize()
+    # the same step with WorkCounters returned by every multiply (the C++ drop-in's default:
+    # k1_counters + a stream synchronisation per cell), one stream, device events
+    cw0, cw1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    cw0.record()
+    for (label, M, K, N, sa, sb) in cells:
+        a_, b_ = As[sa["key"]], Bs[sb["key"]]
+        ctx.preprocess(a_, b_)
+        ctx.multiply(Cs[(M, N)], a_, b_, want_counters=True)
+    cw1.record()
+    torch.cuda.synchronize()
+    counters_ms = cw0.elapsed_time(cw1)
     k1_ms = np.zeros(len(cells))
     k2_ms = np.zeros(len(cells))
     for k in range(dsteps):
@@ -644,6 +655,7 @@ def main():
               "useful": useful, "time_frac": round(t_roof / t_meas, 4),
               "time_frac_def": "BASELINE: Σ_cells max(useful_flops/P_fp32, algo_bytes/BW_hbm) / device time of the timed step",
               "streams": nl, "serial_ms_per_step": round(t_serial * 1e3, 4),
+              "serial_with_counters_ms_per_step": round(counters_ms, 4),
               "serial_def": "K1 + K2 of every cell on ONE stream with CUDA events per cell (diagnostic pass after the "
                             "timed region); k1_ms_per_step, k2_ms_per_step, paths and tensor come from it",
               "hbm_peak_gbs": hbm_peak, "hbm_peak_source": hbm_src,

@@ -675,7 +675,7 @@ __device__ __forceinline__ void k1_a_tile_b(Loader& ld, int64_t M, int64_t K, ui
     if (lane == 0 && (mb >= 0x7F800000u || mn < 0x007FFFFFu)) atomicOr(z.nonfinite_a, 1u);
   }
   // (per-column non-zero counts, for the WorkCounters only, come from the bitmap on request:
-  // k1_acol)
+  // k1_bitcols)
   // the tile's bitmap words, row by row (32 words = 128 contiguous bytes per row)
   asm volatile("bar.sync 2, %0;" ::"r"(kK1Threads) : "memory");
   const int64_t wd = (c0 >> 5) + lane;
@@ -1011,40 +1011,54 @@ __global__ void __launch_bounds__(256) k1_csr(CsrArgs g) {
 // multiply.  The plan totals out[5] = Σ bpop (pop_total), out[6] = Σ (nreg - bnz)
 // (zero codes) and the path choice out[7] / span out[8] come from K1's last CTA
 // (k1_finalize) out of per-warp atomics of the B tiles.
-// bpop[k] (# non-zero 8-column groups of row k) and bnz[k] (# non-zero 64-column regions)
-// from the group k-masks: thread per k walks the ld/8 groups.
-// Per-column non-zero counts of A from the bitmap (WorkCounters on request; the K1 pass no
-// longer accumulates them): thread = column k, its warp reads each row's word once.
-__global__ void k1_acol(const uint32_t* __restrict__ abits, int64_t M, int64_t K, int64_t kw,
-                        uint32_t* __restrict__ acol) {
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= K) return;
-  const int64_t w = k >> 5;
-  const uint32_t bit = k & 31;
-  uint32_t n = 0;
-  for (int64_t i = 0; i < M; ++i) n += (__ldg(abits + i * kw + w) >> bit) & 1u;
-  acol[k] = n;
-}
-
-__global__ void k1_bcounts(const uint32_t* __restrict__ bgrp, int64_t K, int64_t nreg, int64_t kw,
-                           uint32_t* __restrict__ bpop, uint32_t* __restrict__ bnz) {
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= K) return;
-  const int64_t w = k >> 5;
-  const uint32_t bit = 1u << (k & 31);
-  uint32_t pop = 0, nz = 0;
-  for (int64_t r = 0; r < nreg; ++r) {
-    uint32_t any = 0;
+// bpop[k] (# non-zero 8-column groups of row k), bnz[k] (# non-zero 64-column regions) and
+// acol[k] (# non-zeros of A's column k; the K1 pass no longer accumulates them) are column
+// counts of the group k-masks / of A's bitmap:
+// Column counts of a row-major bit matrix bits[R][W] (bit b of word w <-> column 32w + b):
+// out[c] += # rows with bit c set; with ORN = 8 the rows are OR-ed in aligned groups of 8 first
+// (out[c] += # groups with bit c set in any of their rows).  Serves acol (A's bitmap, rows = A
+// rows), bpop (B's group k-masks, rows = 8-column groups) and bnz (the same masks OR-ed per
+// 64-column region).  CTA = 32 word columns x 256 rows: lane = word column (coalesced 128-byte
+// row segments), warp w rows 32w .. 32w+31; 32 per-bit counters per thread, summed over the
+// CTA's warps in shared memory, then one global atomic per column (out is zeroed by the
+// caller).  (One thread per column walking all rows, 32 lanes on the same word, took ~0.5 ms
+// per 4096^2 operand: WorkCounters on every multiply tripled the sweep step.)
+constexpr int kBcRows = 256;
+template <int ORN>
+__global__ void __launch_bounds__(256) k1_bitcols(const uint32_t* __restrict__ bits, int64_t R, int64_t W, int64_t ncols,
+                                                  uint32_t* __restrict__ out) {
+  __shared__ uint32_t acc[32][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 32 * 33; i += 256) (&acc[0][0])[i] = 0u;
+  __syncthreads();
+  const int64_t wc = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t r0 = (int64_t)blockIdx.y * kBcRows + warp * 32;
+  uint32_t cnt[32];
 #pragma unroll
-    for (int g = 0; g < 8; ++g) {
-      const uint32_t b = (bgrp[(8 * r + g) * kw + w] & bit) ? 1u : 0u;
-      pop += b;
-      any |= b;
+  for (int b = 0; b < 32; ++b) cnt[b] = 0u;
+  if (wc < W) {
+#pragma unroll 1
+    for (int g = 0; g < 32 / ORN; ++g) {
+      uint32_t word = 0u;
+#pragma unroll
+      for (int q = 0; q < ORN; ++q) {
+        const int64_t r = r0 + g * ORN + q;
+        if (r < R) word |= __ldg(bits + r * W + wc);
+      }
+#pragma unroll
+      for (int b = 0; b < 32; ++b) cnt[b] += (word >> b) & 1u;
     }
-    nz += any;
+#pragma unroll
+    for (int b = 0; b < 32; ++b)
+      if (cnt[b]) atomicAdd(&acc[lane][b], cnt[b]);
   }
-  bpop[k] = pop;
-  bnz[k] = nz;
+  __syncthreads();
+  for (int i = threadIdx.x; i < 32 * 32; i += 256) {
+    const int l = i >> 5, b = i & 31;
+    const int64_t c = ((int64_t)blockIdx.x * 32 + l) * 32 + b;
+    const uint32_t v = acc[l][b];
+    if (v && c < ncols) atomicAdd(out + c, v);
+  }
 }
 
 __global__ void __launch_bounds__(1024) k1_counters(const uint32_t* __restrict__ acol, const uint32_t* __restrict__ bpop,

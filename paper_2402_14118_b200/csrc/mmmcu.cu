@@ -867,6 +867,16 @@ mmmcu_status read_stats(mmmcu_ctx* ctx, unsigned long long* host16) {
   return MMMCU_OK;
 }
 
+// acol[k] = # non-zeros of A's column k, from the bitmap (k1_bitcols)
+mmmcu_status launch_acol(mmmcu_ctx* ctx, uint32_t* acol) {
+  const int64_t kwa = (ctx->Ka + 31) / 32;
+  MMMCU_CUDA(cudaMemsetAsync(acol, 0, sizeof(uint32_t) * ctx->Ka, ctx->stream));
+  const dim3 grid((unsigned)((kwa + 31) / 32), (unsigned)((ctx->M + mmmcu::kBcRows - 1) / mmmcu::kBcRows));
+  mmmcu::k1_bitcols<1><<<grid, 256, 0, ctx->stream>>>(ctx->abits.as<uint32_t>(), ctx->M, kwa, ctx->Ka, acol);
+  MMMCU_LAUNCHED();
+  return MMMCU_OK;
+}
+
 mmmcu_status fill_counters(mmmcu_ctx* ctx, mmmcu_counters* out) {
   if (!out) return MMMCU_OK;
   // the A-dependent sums are computed on request only (k1_counters)
@@ -874,15 +884,16 @@ mmmcu_status fill_counters(mmmcu_ctx* ctx, mmmcu_counters* out) {
   const bool same_k = a_ok && b_ok && ctx->Ka == ctx->Kb;
   const int64_t K = b_ok ? ctx->Kb : ctx->Ka;
   if (b_ok) {
-    mmmcu::k1_bcounts<<<(unsigned)((ctx->Kb + 255) / 256), 256, 0, ctx->stream>>>(
-        ctx->bgrp.as<uint32_t>(), ctx->Kb, ctx->ldb / 64, (ctx->Kb + 31) / 32, zb_bpop(ctx), zb_bnz(ctx));
+    const int64_t ngrp = ctx->ldb / 8, kwb = (ctx->Kb + 31) / 32;
+    MMMCU_CUDA(cudaMemsetAsync(zb_bpop(ctx), 0, sizeof(uint32_t) * ctx->Kb, ctx->stream));
+    MMMCU_CUDA(cudaMemsetAsync(zb_bnz(ctx), 0, sizeof(uint32_t) * ctx->Kb, ctx->stream));
+    const dim3 grid((unsigned)((kwb + 31) / 32), (unsigned)((ngrp + mmmcu::kBcRows - 1) / mmmcu::kBcRows));
+    mmmcu::k1_bitcols<1><<<grid, 256, 0, ctx->stream>>>(ctx->bgrp.as<uint32_t>(), ngrp, kwb, ctx->Kb, zb_bpop(ctx));
+    MMMCU_LAUNCHED();
+    mmmcu::k1_bitcols<8><<<grid, 256, 0, ctx->stream>>>(ctx->bgrp.as<uint32_t>(), ngrp, kwb, ctx->Kb, zb_bnz(ctx));
     MMMCU_LAUNCHED();
   }
-  if (a_ok) {
-    mmmcu::k1_acol<<<(unsigned)((ctx->Ka + 255) / 256), 256, 0, ctx->stream>>>(
-        ctx->abits.as<uint32_t>(), ctx->M, ctx->Ka, (ctx->Ka + 31) / 32, za_acol(ctx));
-    MMMCU_LAUNCHED();
-  }
+  if (a_ok) MMMCU_TRY(launch_acol(ctx, za_acol(ctx)));
   mmmcu::k1_counters<<<1, 1024, 0, ctx->stream>>>(a_ok ? za_acol(ctx) : nullptr, b_ok ? zb_bpop(ctx) : nullptr,
                                                   b_ok ? zb_bnz(ctx) : nullptr, K, ctx->M, ctx->ldb / 64,
                                                   (a_ok && (same_k || !b_ok)) ? 1 : 0, (b_ok && (same_k || !a_ok)) ? 1 : 0,
@@ -997,9 +1008,7 @@ mmmcu_status gen_counters(mmmcu_ctx* ctx, mmmcu_counters* out) {
   const int64_t K = ctx->Kb;
   MMMCU_CUDA(ctx->scratch0.ensure(sizeof(uint32_t) * ctx->Ka));
   uint32_t* acol = ctx->scratch0.as<uint32_t>();
-  mmmcu::k1_acol<<<(unsigned)((ctx->Ka + 255) / 256), 256, 0, ctx->stream>>>(ctx->abits.as<uint32_t>(), ctx->M, ctx->Ka,
-                                                                             (ctx->Ka + 31) / 32, acol);
-  MMMCU_LAUNCHED();
+  MMMCU_TRY(launch_acol(ctx, acol));
   const uint32_t* bpop = ctx->gzb.as<uint32_t>();
   mmmcu::kg_counters<<<1, 1024, 0, ctx->stream>>>(acol, bpop, bpop + K, K, ctx->M, gen_nreg(ctx), ctx->gen_G,
                                                   ctx->stats.as<unsigned long long>());
