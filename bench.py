@@ -102,6 +102,19 @@ class ClockSampler:
         self.lines = []
         self.nvml = None
 
+    @staticmethod
+    def _power_mw(pynvml, h):
+        # instantaneous board power (nvmlDeviceGetPowerUsage is a ~1 s average, useless for a
+        # 0.1 s timed region); None when the field is not available
+        try:
+            fid = getattr(pynvml, "NVML_FI_DEV_POWER_INSTANT", 186)
+            v = pynvml.nvmlDeviceGetFieldValues(h, [fid])[0]
+            if v.nvmlReturn == 0:
+                return float(v.value.uiVal)
+        except Exception:  # noqa: BLE001
+            pass
+        return None
+
     def start(self):
         # NVML in a thread (5 ms period; the timed region of a sweep step is ~0.2 s, too short
         # for nvidia-smi's start-up); nvidia-smi -lms as the fallback
@@ -117,7 +130,8 @@ class ClockSampler:
                 while self.run:
                     try:
                         self.samples.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
-                                             pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
+                                             pynvml.nvmlDeviceGetCurrentClocksEventReasons(h),
+                                             self._power_mw(pynvml, h)))
                     except Exception:  # noqa: BLE001
                         pass
                     time.sleep(0.005)
@@ -153,11 +167,20 @@ class ClockSampler:
                 mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
             except Exception:  # noqa: BLE001
                 mx = None
-            sm = [float(c) for c, _ in self.samples]
-            reasons = {name for _, bits in self.samples for bit, name in self.REASONS.items()
+            sm = [float(c) for c, _, _ in self.samples]
+            reasons = {name for _, bits, _ in self.samples for bit, name in self.REASONS.items()
                        if bits & bit and name != "gpu_idle"}
+            # board power beside the clocks: K2-TC runs at the power limit, which is what holds the
+            # SM clock below its maximum (the reason bit is not set in every 5 ms sample)
+            pw = [float(p) / 1e3 for _, _, p in self.samples if p is not None]
+            try:
+                lim = float(pynvml.nvmlDeviceGetEnforcedPowerLimit(h)) / 1e3
+            except Exception:  # noqa: BLE001
+                lim = None
             return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                    "samples": len(sm), "source": "nvml"}
+                    "samples": len(sm), "source": "nvml", "power_w": round(float(np.median(pw)), 1) if pw else None,
+                    "power_w_max": round(max(pw), 1) if pw else None, "power_limit_w": lim,
+                    "power_source": "NVML_FI_DEV_POWER_INSTANT" if pw else None}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
         time.sleep(0.06)
